@@ -1,0 +1,417 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native A^2ATS decode-time retrieval path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl a2ats|reference] [--config C2]
+
+One "step" = one decode step of the whole hot path over the batch: a0 (encode
+the new token's key and update the code histogram) + a1..a6
+(a2ats_decode_step: WRoPE query, LUT, code scan + exact top-K, sparse
+attention, LSE combine), through the C ABI of liba2ats.so.  The context grows
+by one token per step (a real decode loop) and ends at the config's N.
+
+Metric (BASELINE.json): approx-scored tokens/s = sum over steps of B*Hkv*n_ctx
+(every cached token is scored once per KV head; the G query heads of a group
+share the pass) / device time; decode-step latency = ms_per_step; % of HBM
+peak in "roofline".  Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import platform
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "approx-scored tokens/s and decode-step latency (VQ top-K attn); % of HBM peak"
+UNIT = "tokens/s"
+SEED = 0xA2A75
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return dict(hbm=float(p["hbm_gbs"]), bf16=float(p["bf16_tflops"]), sm_max=float(p.get("sm_max_mhz", 1965)),
+                    source="measured (MEASURED_PEAKS.json)")
+    except Exception:
+        return dict(hbm=6650.0, bf16=1590.0, sm_max=1965.0, source="fallback (B200_PROFILING.md)")
+
+
+# ---------------------------------------------------------------------------- clocks sampler
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int, period_s: float = 0.005):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self.period, self._stop = period_s, threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------- byte / flop model
+def stage_model(cfg, n_ctx: int, k: int):
+    """Algorithmic bytes (and flops) per launch of each stage, SURVEY §8d."""
+    B, Hq, Hkv, d, L = cfg.B, cfg.Hq, cfg.Hkv, cfg.d, cfg.L
+    P = B * Hkv
+    n_w = min(cfg.window, n_ctx)
+    w0 = n_ctx - n_w
+    n_s = min(cfg.n_sink, w0)
+    n_cand = w0 - n_s
+    keff = min(k, n_cand)
+    M = n_s + keff + n_w
+    return {
+        "encode": dict(bytes=P * d * 2 + Hkv * L * (d * 2 + 4) + Hkv * d * d * 4 + P * 2,
+                       flops=2 * P * L * d + 2 * P * d * d, bound="hbm"),
+        "lut": dict(bytes=Hkv * L * d * 2 + B * Hq * d * 2 + P * L * 4 + B * Hq * d * 4, flops=2 * B * Hq * L * d,
+                    bound="alu"),
+        "threshold": dict(bytes=P * L * 4 * 2 + P * (L // 16) * 4, flops=0, bound="hbm"),
+        "scan": dict(bytes=P * n_cand * 2 + P * keff * 4, flops=0, bound="hbm", tokens=P * n_ctx),
+        "attention": dict(bytes=P * M * d * 2 * 2 + P * keff * 4 + B * Hq * d * (2 + 4 + 4),
+                          flops=4 * B * Hq * M * d, bound="hbm", rows=P * M),
+    }
+
+
+# ---------------------------------------------------------------------------- our arm
+def run_ours(args, rank: int, world: int):
+    import torch
+
+    import paper_2502_12665_b200 as A
+    from synth import CONFIGS, budget_k, make_inputs
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    cfg = CONFIGS[args.config]
+    if args.batch:
+        cfg = cfg.with_(B=args.batch)
+    steps_total = args.warmup + args.steps
+    n0 = cfg.N - steps_total                     # prefix encoded before the loop
+    inp = make_inputs(cfg, SEED + 17 * rank, device=dev, with_h=True, n_max=cfg.n_max(extra=256))
+    q, kc, vc = inp["q"], inp["k_cache"], inp["v_cache"]
+    params = A.Params(topk=budget_k(cfg.N))
+    dec = A.Decoder(cfg.B, cfg.Hq, cfg.Hkv, cfg.L, inp["n_max"], inp["codebook"], inp["H"], params, device=dev)
+    dec.encode(kc, 0, n0)                       # prefill codes + running histogram (untimed)
+    out = torch.empty((cfg.B, cfg.Hq, cfg.d), dtype=torch.float32, device=dev)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)   # 256 MB > 126 MB L2
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream()
+    n_stage = 6
+    stage_ev = [[torch.cuda.Event(enable_timing=True) for _ in range(n_stage)] for _ in range(args.steps)]
+    enc_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for evs in stage_ev:
+        for e in evs:
+            e.record(stream)      # materialise handles
+
+    def one_step(n, k_step):
+        tb = enc_ev[k_step][0] if k_step is not None else None
+        if tb is not None:
+            tb.record(stream)
+            A.a2ats_set_stage_events(stage_ev[k_step])
+        dec.encode(kc, n - 1, n)                 # a0: the new token's code (+ hist)
+        dec.params.topk = budget_k(n)
+        dec.step(q, kc, vc, n, out=out)          # a1..a6
+        if tb is not None:
+            enc_ev[k_step][1].record(stream)
+            A.a2ats_set_stage_events(None)
+
+    n = n0
+    for _ in range(args.warmup):
+        n += 1
+        flush.fill_(1.0)
+        one_step(n, None)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    tokens = 0
+    with ClockSampler(local) as clk:
+        for s in range(args.steps):
+            n += 1
+            if not args.no_flush:
+                flush.fill_(float(s))
+            one_step(n, s)
+            tokens += cfg.B * cfg.Hkv * n
+        torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    step_ms = [enc_ev[s][0].elapsed_time(enc_ev[s][1]) for s in range(args.steps)]
+    names = ["lut", "threshold", "scan", "attention"]
+    stage_ms = {nm: [] for nm in names}
+    stage_ms["encode"] = []
+    for s in range(args.steps):
+        ev = stage_ev[s]
+        stage_ms["encode"].append(enc_ev[s][0].elapsed_time(ev[0]))
+        for i, nm in enumerate(names):
+            stage_ms[nm].append(ev[i].elapsed_time(ev[i + 1]))
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+        tk = torch.tensor([float(tokens)], device=dev)
+        torch.distributed.all_reduce(tk)
+        tokens = tk.item()
+    value = tokens / (total_ms / 1e3)
+
+    # ---- e2e: same step through the public API with host buffers (pinned), copies inside the timed region
+    e2e = run_e2e(args, dec, cfg, kc, vc, q, n, stream, A, budget_k)
+
+    res = dict(value=value, ms_per_step=total_ms / args.steps, stage_ms={k: statistics.mean(v) for k, v in stage_ms.items()},
+               clocks=clk.summary(), e2e=e2e, n_last=n, cfg=cfg)
+    return res
+
+
+def run_e2e(args, dec, cfg, kc, vc, q, n_start, stream, A, budget_k):
+    import torch
+    steps = max(3, args.steps // 2)
+    B, Hq, Hkv, d = cfg.B, cfg.Hq, cfg.Hkv, cfg.d
+    q_host = q.detach().cpu().pin_memory()
+    knew = torch.empty((B, Hkv, d), dtype=torch.bfloat16).pin_memory()
+    vnew = torch.empty((B, Hkv, d), dtype=torch.bfloat16).pin_memory()
+    out_host = torch.empty((B, Hq, d), dtype=torch.float32).pin_memory()
+    q_dev = torch.empty_like(q)
+    out = torch.empty((B, Hq, d), dtype=torch.float32, device=q.device)
+    # the decode loop keeps appending: the new token's K/V rows come from the synthetic cache, staged in
+    # pinned host buffers and copied in inside the timed region
+    n = n_start
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    tot = 0.0
+    tokens = 0
+    for s in range(steps):
+        n += 1
+        knew.copy_(kc[:, :, n - 1].cpu())
+        vnew.copy_(vc[:, :, n - 1].cpu())
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        q_dev.copy_(q_host, non_blocking=True)
+        kc[:, :, n - 1].copy_(knew, non_blocking=True)
+        vc[:, :, n - 1].copy_(vnew, non_blocking=True)
+        dec.encode(kc, n - 1, n)
+        dec.params.topk = budget_k(n)
+        dec.step(q_dev, kc, vc, n, out=out)
+        out_host.copy_(out, non_blocking=True)
+        ev1.record(stream)
+        ev1.synchronize()
+        tot += ev0.elapsed_time(ev1)
+        tokens += B * Hkv * n
+    h2d = q_host.numel() * 2 + knew.numel() * 2 + vnew.numel() * 2
+    d2h = out_host.numel() * 4
+    return {"value": tokens / (tot / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "ms_per_step": tot / steps, "steps": steps}
+
+
+# ---------------------------------------------------------------------------- CPU oracle (baseline / reference arm)
+def oracle_sample(cfg, seconds_budget: float = 15.0, max_pairs: int = 64):
+    """Times the fp64 oracle (as it stands) on whole (b, kv-head) pairs of the
+    workload: same N, L, G, budget; per-pair work identical to the GPU arm."""
+    import numpy as np
+    import torch
+
+    from oracle import a2ats_oracle as O
+    from synth import budget_k, make_inputs
+
+    try:
+        from threadpoolctl import threadpool_limits
+        limiter = threadpool_limits(1)
+    except Exception:
+        limiter = None
+    G = cfg.Hq // cfg.Hkv
+    one = cfg.with_(B=1, Hq=G, Hkv=1)
+    inp = make_inputs(one, SEED + 99, device="cpu", with_h=False)
+    qg = inp["q"][0].double().numpy()
+    k = inp["k_cache"][0, 0].double().numpy()
+    v = inp["v_cache"][0, 0].double().numpy()
+    codes = inp["z"][0, 0].numpy().astype(np.int64)
+    C = inp["codebook"][0].double().numpy()
+    K = budget_k(cfg.N)
+    pairs, t_total = 0, 0.0
+    while pairs < max_pairs and (t_total < seconds_budget or pairs == 0):
+        t0 = time.perf_counter()
+        O.decode_step_pair(qg, k, v, codes, C, cfg.N, window=cfg.window, bridge=cfg.bridge, n_sink=cfg.n_sink, topk=K)
+        t_total += time.perf_counter() - t0
+        pairs += 1
+    if limiter is not None:
+        limiter.unregister() if hasattr(limiter, "unregister") else None
+    value = pairs * cfg.N / t_total
+    return dict(value=value, unit=UNIT, cores=1, kind="oracle",
+                sample=f"{pairs} (b, kv-head) pairs of {cfg.name} (N={cfg.N}, L={cfg.L}, G={G}, K={K}), "
+                       f"fp64 numpy oracle, 1 thread, {t_total:.1f} s; tokens/s = pairs*N/time",
+                cpu=platform.processor() or _cpu_model(), seconds=t_total)
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def run_reference(args):
+    from synth import CONFIGS
+    cfg = CONFIGS[args.config]
+    per_step = []
+    t_all = time.perf_counter()
+    for s in range(args.warmup + args.steps):
+        r = oracle_sample(cfg, seconds_budget=args.ref_seconds, max_pairs=1)
+        if s >= args.warmup:
+            per_step.append(r)
+    tot = sum(r["seconds"] for r in per_step)
+    tokens = len(per_step) * cfg.N
+    value = tokens / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(per_step),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg.name, "note": cfg.note, "B": cfg.B, "Hq": cfg.Hq, "Hkv": cfg.Hkv, "d": cfg.d,
+                   "N": cfg.N, "L": cfg.L, "K": cfg.K},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"each step = 1 (b, kv-head) pair of {cfg.name} through the fp64 numpy oracle "
+                                   f"(a1-a6 given codes), 1 thread; tokens/s = N/time"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": time.perf_counter() - t_all,
+    }
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="a2ats", choices=["a2ats", "reference", "ours"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-seconds", type=float, default=2.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        if rank == 0:
+            run_reference(args)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        dist.init_process_group("nccl")
+    r = run_ours(args, rank, world)
+    if rank != 0:
+        return
+    pk = peaks()
+    from synth import budget_k
+    cfg = r["cfg"]
+    model = stage_model(cfg, r["n_last"], budget_k(r["n_last"]))
+    kernels = {}
+    for nm, ms in r["stage_ms"].items():
+        m = model[nm]
+        gbs = m["bytes"] / (ms * 1e-3) / 1e9 if ms > 0 else None
+        kernels[nm] = {"ms": ms, "alg_bytes": m["bytes"], "GBps": gbs,
+                       "frac_hbm": (gbs / pk["hbm"]) if gbs else None, "flops": m["flops"],
+                       "TFLOPs": m["flops"] / (ms * 1e-3) / 1e12 if ms > 0 else None}
+    dom = max(("attention", "scan", "lut", "threshold", "encode"), key=lambda k: r["stage_ms"][k])
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(dom)
+        except Exception:
+            traffic = None
+    if model[dom]["bound"] == "alu":
+        # FMA-bound LUT: peak = 148 SMs x 128 FP32 lanes x 2 flop x clock
+        sm_mhz = r["clocks"]["sm_mhz"] or pk["sm_max"]
+        peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
+        ach = kernels[dom]["TFLOPs"]
+        roof = {"bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                "traffic": traffic, "kernel": dom}
+    else:
+        ach = kernels[dom]["GBps"]
+        roof = {"bound": "hbm", "achieved": ach, "peak": pk["hbm"], "unit": "GB/s", "frac": ach / pk["hbm"],
+                "traffic": traffic, "kernel": dom, "peak_source": pk["source"]}
+    cpu = None
+    if not args.no_cpu_baseline and world >= 1:
+        try:
+            cpu = oracle_sample(cfg, seconds_budget=15.0)
+        except Exception as e:  # never let the baseline kill the line
+            cpu = {"error": repr(e)}
+    launches_per_step = 6  # keyh + encode_argmin + lut + threshold + scan + attention
+    line = {
+        "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": cfg.name, "note": cfg.note, "B": cfg.B, "Hq": cfg.Hq, "Hkv": cfg.Hkv, "d": cfg.d,
+                   "N_final": r["n_last"], "L": cfg.L, "K_final": budget_k(r["n_last"]), "window": cfg.window,
+                   "bridge": cfg.bridge, "n_sink": cfg.n_sink,
+                   "parallelism": f"replicas x{world} (batch/head parallel, no collective)" if world > 1 else "1 GPU",
+                   "l2": "flushed between steps (256 MB write, outside the timed events)" if not args.no_flush else "not flushed",
+                   "step": "a0 encode new token (+hist) + a2ats_decode_step (a1..a6)",
+                   "sparsity": (budget_k(r["n_last"]) + 68) / r["n_last"], "aux_mem": 2 / (cfg.d * 2)},
+        "roofline": roof,
+        "kernels": kernels,
+        "cpu_baseline": cpu,
+        "e2e": r["e2e"],
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": r["clocks"],
+    }
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,188 @@
+/*
+ * a2ats.h -- C ABI of the B200-native A^2ATS decode-time retrieval path.
+ *
+ * A^2ATS (arXiv 2502.12665).  "P:n" = line n of the paper's LaTeX source
+ * (PAPER.md).  Readings Q1-Q24 of the paper's silent / ambiguous points are
+ * listed in DESIGN.md.
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - All tensor pointers are DEVICE pointers (cudaMalloc / PyTorch CUDA
+ *    storage) unless a comment says "host".  With kv_location ==
+ *    A2ATS_KV_HOST_MAPPED the K/V cache pointers may instead be device
+ *    aliases of mapped pinned host memory (cudaHostAlloc(..Mapped) +
+ *    cudaHostGetDevicePointer).
+ *  - Every buffer is caller-owned.  The library allocates nothing on the hot
+ *    path and retains no pointer after return.
+ *  - bf16 tensors are passed as `const void*` (IEEE bfloat16 bit patterns,
+ *    round-to-nearest-even conversions everywhere, reading Q17).
+ *  - Layouts are dense row-major (C order); the last dimension is d = 128
+ *    and is contiguous.  n_max % 8 == 0 so 16-byte vector loads of codes and
+ *    rows are aligned; every pointer must be 16-byte aligned.
+ *  - `stream` is a cudaStream_t passed as void*; NULL = the legacy default
+ *    stream.  All work is enqueued asynchronously; nothing synchronises the
+ *    host.  Asynchronous device faults surface at the caller's next sync.
+ *  - Workspaces: query the size with the *_workspace_bytes function, hand
+ *    over a device buffer of at least that many bytes that is ZERO-FILLED
+ *    before its first use.  Every successful call leaves the workspace in
+ *    that zero state again, so the same buffer can be reused call after call
+ *    on one stream.  Concurrent calls need distinct workspaces.
+ *  - Return value: A2ATS_OK (0) or a negative status (see below); no
+ *    exception crosses the ABI.  Argument validation happens before any CUDA
+ *    call, so EINVAL / EUNSUPPORTED / EWORKSPACE are returned without
+ *    touching the device.
+ *  - Results are bitwise deterministic for fixed inputs and shapes: no
+ *    order-dependent floating-point atomics are used anywhere.
+ */
+#ifndef A2ATS_H_
+#define A2ATS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define A2ATS_ABI_VERSION 1
+
+/* ---- status codes ---------------------------------------------------- */
+#define A2ATS_OK 0
+#define A2ATS_EINVAL (-1)       /* bad argument: null required pointer, d odd, Hq % Hkv != 0,
+                                   n_ctx <= 0 or > n_max, topk < 0, token range out of bounds,
+                                   misalignment (mirrors SPEC "dimension mismatch", "odd-length
+                                   row", "empty store") */
+#define A2ATS_EUNSUPPORTED (-2) /* valid but not implemented: d != 128, G = Hq/Hkv not in
+                                   {1,2,4,8}, L > 16384 */
+#define A2ATS_EWORKSPACE (-3)   /* ws == NULL or ws_bytes smaller than the queried size */
+#define A2ATS_ECUDA (-4)        /* a CUDA launch failed (cudaGetLastError after launch) */
+#define A2ATS_ENCCL (-5)        /* an NCCL call failed (sharded entry points) */
+
+/* group_reduce: how the G query heads of one KV head are folded into one
+ * ranking score per token (paper silent; reading Q10). */
+#define A2ATS_GROUP_MAX 0
+#define A2ATS_GROUP_SUM 1
+
+/* kv_location (reading: the paper's CPU-resident KV cache of P:392-394). */
+#define A2ATS_KV_DEVICE 0       /* K/V cache in HBM */
+#define A2ATS_KV_HOST_MAPPED 1  /* K/V cache in mapped pinned host memory, read over PCIe */
+
+typedef struct a2ats_shape {
+  int32_t B;      /* batch size (sequences)                                   */
+  int32_t Hq;     /* query heads                                              */
+  int32_t Hkv;    /* KV heads (one codebook per KV head); Hq % Hkv == 0 */
+  int32_t d;      /* head dimension; 128 in this version                      */
+  int32_t L;      /* codebook size (P:431 uses 4096); 1 <= L <= 16384         */
+  int32_t n_max;  /* capacity (tokens) of the K/V cache and code arrays; % 8 == 0 */
+} a2ats_shape;
+
+typedef struct a2ats_params {
+  int32_t window;        /* w of Eq. 11: i-j < w is local; 64      */
+  int32_t bridge;        /* b of Eq. 11/12: fixed relative position; 2048     */
+  int32_t n_sink;        /* statically preserved initial tokens; 4            */
+  int32_t topk;          /* K: number of retrieved candidates (absolute; reading Q9)  */
+  double rope_theta;     /* RoPE base; 1e4 by default (reading Q1)                    */
+  const double* inv_freq;/* optional HOST array [d/2] of rotation frequencies that
+                            overrides rope_theta (e.g. Llama-3.1 scaled frequencies)   */
+  int32_t group_reduce;  /* A2ATS_GROUP_MAX (default) | A2ATS_GROUP_SUM               */
+  int32_t kv_location;   /* A2ATS_KV_DEVICE (default) | A2ATS_KV_HOST_MAPPED          */
+} a2ats_params;
+
+/* Fills the paper's configuration: w = 64, b = 2048, n_sink = 4, topk = 0,
+ * theta = 1e4, GROUP_MAX, KV on device. */
+void a2ats_default_params(a2ats_params* p);
+
+const char* a2ats_status_string(int status);
+int a2ats_abi_version(void);
+
+/* ---------------------------------------------------------------------
+ * a2ats_qavq_prepare -- codebook-side term of the query-aware quantizer.
+ *
+ * f'(k; C) = argmin_j (k - c_j) H (k - c_j)^T            (Eq. 14)
+ *          = argmin_j ( n_j - 2 (k H) . c_j ),  n_j = c_j H c_j^T   (H = H^T)
+ * This writes n [Hkv, L] fp32 (the per-codeword constant of that argmin).
+ *   codebook : [Hkv, L, d] bf16, the shared codebook C
+ *   H        : [Hkv, d, d] fp32 symmetric positive definite second-moment
+ *              matrix of post-PE queries; NULL => H = I (conventional
+ *              VQ, Eq. 5)
+ *   nrm      : [Hkv, L] fp32 output
+ * Call once per codebook (offline state); no workspace.
+ * ------------------------------------------------------------------- */
+int a2ats_qavq_prepare(const a2ats_shape* shape, const void* codebook, const float* H,
+                       float* nrm, void* stream);
+
+/* ---------------------------------------------------------------------
+ * a2ats_build_codes -- inference-time quantization (Eq. 20).
+ *
+ * For every (b, h) and token t in [t_begin, t_end):
+ *   codes[b,h,t] = f'(k_t; C_h)  (lowest codeword index on exact ties, Q12)
+ * and, if hist != NULL, hist[b,h,codes[b,h,t]] += 1.
+ *   keys     : [B, Hkv, n_max, d] bf16 PRE-PE keys (under WRoPE the post-PE
+ *              key equals the pre-PE key, Eq. 12)
+ *   codebook : [Hkv, L, d] bf16;  H : [Hkv, d, d] fp32 or NULL (as above)
+ *   nrm      : [Hkv, L] fp32 from a2ats_qavq_prepare with the same C, H
+ *   codes    : [B, Hkv, n_max] uint16 out; only [t_begin, t_end) written
+ *   hist     : optional [B, Hkv, L] int32 running histogram, accumulated
+ * 0 <= t_begin <= t_end <= n_max.  Used for prefill (whole prompt) and for
+ * each decode step (the new token).
+ * ------------------------------------------------------------------- */
+size_t a2ats_build_codes_workspace_bytes(const a2ats_shape* shape);
+int a2ats_build_codes(const a2ats_shape* shape, const void* keys, int32_t t_begin, int32_t t_end,
+                      const void* codebook, const float* H, const float* nrm, uint16_t* codes,
+                      int32_t* hist, void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------
+ * a2ats_decode_step -- one decode step of the retrieval path, all pairs.
+ *
+ * Per (b, KV head h), with i = n_ctx - 1 the current token (in the cache):
+ *  a1  q~ = q R_b                                     (Eq. 12)
+ *  a2  LUT[l] = q~ . c_l                              (Eq. 21)
+ *  a3  score[t] = LUT[codes[t]];  agg[t] = max (or sum) over the G query
+ *      heads of the group                             (Eq. 21; reading Q10)
+ *  a4  Sel = Sinks u TopK u Window: Window = {t >= n_ctx - w}, Sinks = the
+ *      first n_sink tokens outside it, TopK = the first
+ *      min(topk, |Cand|) candidates by (agg desc, t asc)  (readings Q8, Q12)
+ *  a5  u_j = q~ . k_j for sinks/top-K (bridge), u_j = (q R_{i-j}) . k_j in
+ *      the window (Eq. 11); o = softmax(u / sqrt(d)) V over Sel
+ *      (Eq. 2), fp32 online softmax, split over row chunks
+ *  a6  log-sum-exp combine of the chunks in fixed order
+ * Arguments:
+ *   n_ctx    : N, cached tokens including the current one; 1 <= N <= n_max
+ *   q        : [B, Hq, d] bf16 PRE-PE queries (q of head hq uses KV head hq / G)
+ *   k_cache, v_cache : [B, Hkv, n_max, d] bf16 (pre-PE keys; rows < N read)
+ *   codes    : [B, Hkv, n_max] uint16, valid for all t < N
+ *   codebook : [Hkv, L, d] bf16
+ *   hist     : optional [B, Hkv, L] int32: counts of codes over tokens
+ *              [0, N) exactly (as maintained by a2ats_build_codes).  With it
+ *              the code stream is read once; NULL => histogram computed
+ *              in-step with an extra pass.  Results are bitwise identical.
+ *   out      : [B, Hq, d] fp32 attention output
+ *   sel_out  : optional [B, Hkv, K_eff] int32, the top-K token indices in
+ *              ascending order, K_eff = min(topk, |Cand|)
+ *   scores_out : optional [B, Hq, n_ctx] fp32 debug output of the
+ *              approximate scores u^ (Eq. 21) of every token
+ * ------------------------------------------------------------------- */
+size_t a2ats_decode_workspace_bytes(const a2ats_shape* shape, const a2ats_params* params);
+int a2ats_decode_step(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx,
+                      const void* q, const void* k_cache, const void* v_cache,
+                      const uint16_t* codes, const void* codebook, const int32_t* hist,
+                      float* out, int32_t* sel_out, float* scores_out,
+                      void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------
+ * a2ats_set_stage_events -- optional instrumentation for benchmarks.
+ *
+ * events: host array of n cudaEvent_t handles (passed as void*), or NULL to
+ * disable.  While set, every a2ats_decode_step records events[0..5] on its
+ * stream at the stage boundaries: [0] before a1/a2 (LUT), [1] after the LUT,
+ * [2] after the threshold (a4 part 1), [3] after the code scan (a3 + a4),
+ * [4] after attention + combine (a5 + a6), [5] at the end.  Requires n >= 6.
+ * The array is copied; the events stay caller-owned.  Process-global, not
+ * thread-safe: for single-threaded benchmarking only.
+ * ------------------------------------------------------------------- */
+int a2ats_set_stage_events(void* const* events, int n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* A2ATS_H_ */

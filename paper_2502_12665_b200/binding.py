@@ -1,0 +1,195 @@
+"""Thin ctypes binding of liba2ats.so (include/a2ats.h).
+
+Argument marshalling only: every step of the retrieval path runs in the CUDA
+kernels behind the C ABI.  Torch tensors are accepted for convenience (device,
+dtype and contiguity are checked, then ``data_ptr()`` is passed); there is no
+CPU fallback -- if the library cannot be loaded every entry point raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "lib", "liba2ats.so")
+
+A2ATS_OK = 0
+A2ATS_EINVAL = -1
+A2ATS_EUNSUPPORTED = -2
+A2ATS_EWORKSPACE = -3
+A2ATS_ECUDA = -4
+A2ATS_ENCCL = -5
+A2ATS_GROUP_MAX = 0
+A2ATS_GROUP_SUM = 1
+A2ATS_KV_DEVICE = 0
+A2ATS_KV_HOST_MAPPED = 1
+
+
+class A2ATSError(RuntimeError):
+    def __init__(self, fn: str, status: int):
+        self.status = status
+        super().__init__(f"{fn} -> {status}: {status_string(status)}")
+
+
+class a2ats_shape(ctypes.Structure):
+    _fields_ = [("B", ctypes.c_int32), ("Hq", ctypes.c_int32), ("Hkv", ctypes.c_int32),
+                ("d", ctypes.c_int32), ("L", ctypes.c_int32), ("n_max", ctypes.c_int32)]
+
+
+class a2ats_params(ctypes.Structure):
+    _fields_ = [("window", ctypes.c_int32), ("bridge", ctypes.c_int32), ("n_sink", ctypes.c_int32),
+                ("topk", ctypes.c_int32), ("rope_theta", ctypes.c_double),
+                ("inv_freq", ctypes.POINTER(ctypes.c_double)), ("group_reduce", ctypes.c_int32),
+                ("kv_location", ctypes.c_int32)]
+
+
+_VP = ctypes.c_void_p
+_SIGS = {
+    "a2ats_default_params": (None, [ctypes.POINTER(a2ats_params)]),
+    "a2ats_status_string": (ctypes.c_char_p, [ctypes.c_int]),
+    "a2ats_abi_version": (ctypes.c_int, []),
+    "a2ats_qavq_prepare": (ctypes.c_int, [ctypes.POINTER(a2ats_shape), _VP, _VP, _VP, _VP]),
+    "a2ats_build_codes_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(a2ats_shape)]),
+    "a2ats_build_codes": (ctypes.c_int, [ctypes.POINTER(a2ats_shape), _VP, ctypes.c_int32, ctypes.c_int32, _VP, _VP,
+                                         _VP, _VP, _VP, _VP, ctypes.c_size_t, _VP]),
+    "a2ats_decode_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(a2ats_shape), ctypes.POINTER(a2ats_params)]),
+    "a2ats_set_stage_events": (ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int]),
+    "a2ats_decode_step": (ctypes.c_int, [ctypes.POINTER(a2ats_shape), ctypes.POINTER(a2ats_params), ctypes.c_int32,
+                                         _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, ctypes.c_size_t, _VP]),
+}
+
+_lib = None
+
+
+def load(path: str = LIB_PATH, build_if_missing: bool = True) -> ctypes.CDLL:
+    """Load (building first if needed) liba2ats.so and declare its signatures."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path) and build_if_missing:
+        from .build import build
+        build()
+    if not os.path.exists(path):
+        raise OSError(f"liba2ats.so not found at {path}: run `python -m paper_2502_12665_b200.build`")
+    lib = ctypes.CDLL(path)
+    for name, (res, args) in _SIGS.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = lib
+    return lib
+
+
+def status_string(status: int) -> str:
+    return load().a2ats_status_string(status).decode()
+
+
+def _check(fn: str, rc: int):
+    if rc != A2ATS_OK:
+        raise A2ATSError(fn, rc)
+
+
+# ------------------------------------------------------------------ shapes / params
+def make_shape(B, Hq, Hkv, d, L, n_max) -> a2ats_shape:
+    return a2ats_shape(B, Hq, Hkv, d, L, n_max)
+
+
+@dataclass
+class Params:
+    window: int = 64
+    bridge: int = 2048
+    n_sink: int = 4
+    topk: int = 0
+    rope_theta: float = 1e4
+    inv_freq: tuple | None = None
+    group_reduce: int = A2ATS_GROUP_MAX
+    kv_location: int = A2ATS_KV_DEVICE
+
+    def c(self) -> a2ats_params:
+        p = a2ats_params()
+        load().a2ats_default_params(ctypes.byref(p))
+        p.window, p.bridge, p.n_sink, p.topk = self.window, self.bridge, self.n_sink, self.topk
+        p.rope_theta = self.rope_theta
+        if self.inv_freq is not None:
+            self._freq_buf = (ctypes.c_double * len(self.inv_freq))(*self.inv_freq)
+            p.inv_freq = ctypes.cast(self._freq_buf, ctypes.POINTER(ctypes.c_double))
+        p.group_reduce, p.kv_location = self.group_reduce, self.kv_location
+        return p
+
+
+def _ptr(t, name, dtype=None, optional=False, host_ok=False):
+    if t is None:
+        if optional:
+            return None
+        raise ValueError(f"{name} is required")
+    if isinstance(t, int):
+        return t
+    if dtype is not None and t.dtype != dtype:
+        raise TypeError(f"{name}: expected {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if not host_ok and not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    return t.data_ptr()
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    return getattr(stream, "cuda_stream", stream)
+
+
+# ------------------------------------------------------------------ entry points (same names as the C ABI)
+def a2ats_qavq_prepare(shape: a2ats_shape, codebook, H, nrm, stream=None):
+    import torch
+    rc = load().a2ats_qavq_prepare(ctypes.byref(shape), _ptr(codebook, "codebook", torch.bfloat16),
+                                   _ptr(H, "H", torch.float32, optional=True), _ptr(nrm, "nrm", torch.float32),
+                                   _stream(stream))
+    _check("a2ats_qavq_prepare", rc)
+
+
+def a2ats_build_codes_workspace_bytes(shape: a2ats_shape) -> int:
+    return int(load().a2ats_build_codes_workspace_bytes(ctypes.byref(shape)))
+
+
+def a2ats_build_codes(shape: a2ats_shape, keys, t_begin: int, t_end: int, codebook, H, nrm, codes, hist, ws,
+                      stream=None):
+    import torch
+    rc = load().a2ats_build_codes(ctypes.byref(shape), _ptr(keys, "keys", torch.bfloat16), int(t_begin), int(t_end),
+                                  _ptr(codebook, "codebook", torch.bfloat16), _ptr(H, "H", torch.float32, optional=True),
+                                  _ptr(nrm, "nrm", torch.float32), _ptr(codes, "codes", torch.uint16),
+                                  _ptr(hist, "hist", torch.int32, optional=True), _ptr(ws, "ws"),
+                                  ws.numel() * ws.element_size(), _stream(stream))
+    _check("a2ats_build_codes", rc)
+
+
+def a2ats_decode_workspace_bytes(shape: a2ats_shape, params) -> int:
+    p = params.c() if isinstance(params, Params) else params
+    return int(load().a2ats_decode_workspace_bytes(ctypes.byref(shape), ctypes.byref(p)))
+
+
+def a2ats_decode_step(shape: a2ats_shape, params, n_ctx: int, q, k_cache, v_cache, codes, codebook, hist, out,
+                      sel_out, scores_out, ws, stream=None, kv_host: bool = False):
+    import torch
+    p = params.c() if isinstance(params, Params) else params
+    rc = load().a2ats_decode_step(
+        ctypes.byref(shape), ctypes.byref(p), int(n_ctx), _ptr(q, "q", torch.bfloat16),
+        _ptr(k_cache, "k_cache", torch.bfloat16, host_ok=kv_host), _ptr(v_cache, "v_cache", torch.bfloat16, host_ok=kv_host),
+        _ptr(codes, "codes", torch.uint16), _ptr(codebook, "codebook", torch.bfloat16),
+        _ptr(hist, "hist", torch.int32, optional=True), _ptr(out, "out", torch.float32),
+        _ptr(sel_out, "sel_out", torch.int32, optional=True), _ptr(scores_out, "scores_out", torch.float32, optional=True),
+        _ptr(ws, "ws"), ws.numel() * ws.element_size(), _stream(stream))
+    _check("a2ats_decode_step", rc)
+
+
+def a2ats_set_stage_events(events):
+    """events: list of >= 6 torch.cuda.Event(enable_timing=True) (already recorded
+    once so the handle exists), or None to disable."""
+    lib = load()
+    if events is None:
+        _check("a2ats_set_stage_events", lib.a2ats_set_stage_events(None, 0))
+        return
+    arr = (ctypes.c_void_p * len(events))(*[e.cuda_event for e in events])
+    _check("a2ats_set_stage_events", lib.a2ats_set_stage_events(arr, len(events)))

@@ -1,0 +1,379 @@
+// C-ABI of liba2ats.so (declared and documented in include/a2ats.h).
+// Host orchestration only: validation, workspace carving, kernel launches on
+// the caller's stream.  No allocation, no host synchronisation.
+#include <cmath>
+#include <cstring>
+#include <mutex>
+
+#include "internal.cuh"
+
+namespace a2ats {
+
+int sm_count() {
+  static int cached[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  if (cached[dev] == 0) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cached[dev] = n > 0 ? n : 148;
+  }
+  return cached[dev];
+}
+
+namespace {
+
+constexpr size_t kAlign = 256;
+inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+// Rows of the Sel list handled by one attention CTA (fixed per shape so the
+// workspace size does not depend on n_ctx).
+constexpr int kAttnRows = 256;
+constexpr int kMinChunk = 4096;  // smallest scan tile (U = 2)
+
+struct Derived {
+  int G, P, n_w, w0, n_s, c0, c1, n_cand, keff, M;
+  int U, CH, first_chunk, nchunks;
+  int R, nsplit, GT, nz, W;
+};
+
+int check_shape(const a2ats_shape* s) {
+  if (!s) return A2ATS_EINVAL;
+  if (s->B <= 0 || s->Hq <= 0 || s->Hkv <= 0 || s->d <= 0 || s->L <= 0 || s->n_max <= 0) return A2ATS_EINVAL;
+  if (s->d % 2) return A2ATS_EINVAL;
+  if (s->Hq % s->Hkv) return A2ATS_EINVAL;
+  if (s->n_max % 8) return A2ATS_EINVAL;
+  if (s->d != kD) return A2ATS_EUNSUPPORTED;
+  const int G = s->Hq / s->Hkv;
+  if (G != 1 && G != 2 && G != 4 && G != 8) return A2ATS_EUNSUPPORTED;
+  if (s->L > 16384) return A2ATS_EUNSUPPORTED;
+  return A2ATS_OK;
+}
+
+int check_params(const a2ats_params* p) {
+  if (!p) return A2ATS_EINVAL;
+  if (p->window < 1 || p->bridge < 0 || p->n_sink < 0 || p->topk < 0) return A2ATS_EINVAL;
+  if (!(p->rope_theta > 0.0) && !p->inv_freq) return A2ATS_EINVAL;
+  if (p->group_reduce != A2ATS_GROUP_MAX && p->group_reduce != A2ATS_GROUP_SUM) return A2ATS_EINVAL;
+  if (p->kv_location != A2ATS_KV_DEVICE && p->kv_location != A2ATS_KV_HOST_MAPPED) return A2ATS_EINVAL;
+  return A2ATS_OK;
+}
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+void derive(const a2ats_shape* s, const a2ats_params* p, int n_ctx, Derived* d) {
+  d->G = s->Hq / s->Hkv;
+  d->P = s->B * s->Hkv;
+  d->n_w = std::min(p->window, n_ctx);              // W = {t >= N - w}     (Eq. 11 locality)
+  d->w0 = n_ctx - d->n_w;
+  d->n_s = std::min(p->n_sink, d->w0);              // sinks outside W
+  d->c0 = d->n_s;
+  d->c1 = d->w0;
+  d->n_cand = d->c1 - d->c0;
+  d->keff = std::min(p->topk, d->n_cand);
+  d->M = d->n_s + d->keff + d->n_w;
+  // scan tile: enough tiles to cover the machine a few times
+  const long long tokens = (long long)d->P * std::max(d->n_cand, 1);
+  const long long want = 4LL * sm_count();
+  d->U = (tokens / 16384 >= want) ? 8 : ((tokens / 8192 >= want) ? 4 : 2);
+  d->CH = 2048 * d->U;
+  d->first_chunk = d->c0 / d->CH;
+  d->nchunks = d->n_cand > 0 ? ((d->c1 + d->CH - 1) / d->CH - d->first_chunk) : 0;
+  d->R = kAttnRows;
+  d->nsplit = (d->M + d->R - 1) / d->R;
+  d->GT = d->G >= 4 ? 4 : d->G;
+  d->nz = d->G / d->GT;
+  d->W = (s->L + 15) / 16;
+}
+
+struct DecodeWs {
+  size_t qrot, cs, agg, lut, cls, pinfo, status, tilectr, sel, part, actr, total;
+};
+
+DecodeWs decode_layout(const a2ats_shape* s, const a2ats_params* p) {
+  const int G = s->Hq / s->Hkv, P = s->B * s->Hkv;
+  const int W = (s->L + 15) / 16;
+  const long long kmax = std::min<long long>(p->topk, s->n_max);
+  const long long mmax = kmax + p->n_sink + p->window;
+  const long long nsplit_max = (mmax + kAttnRows - 1) / kAttnRows;
+  const long long maxchunks = s->n_max / kMinChunk + 2;
+  const int GT = G >= 4 ? 4 : G;
+  DecodeWs w;
+  size_t o = 0;
+  w.qrot = o; o = align_up(o + (size_t)s->B * s->Hq * kD * 4);
+  w.cs = o; o = align_up(o + (size_t)p->window * kHalf * 8);
+  w.agg = o; o = align_up(o + (size_t)P * s->L * 4);
+  w.lut = o; o = align_up(o + (size_t)s->B * s->Hq * s->L * 4);
+  w.cls = o; o = align_up(o + (size_t)P * W * 4);
+  w.pinfo = o; o = align_up(o + (size_t)P * 16);
+  w.status = o; o = align_up(o + (size_t)P * maxchunks * 8);
+  w.tilectr = o; o = align_up(o + 16);
+  w.sel = o; o = align_up(o + (size_t)P * std::max<long long>(kmax, 1) * 4);
+  w.part = o; o = align_up(o + (size_t)P * (G / GT) * GT * nsplit_max * 130 * 4);
+  w.actr = o; o = align_up(o + (size_t)P * (G / GT) * 4);
+  w.total = o;
+  return w;
+}
+
+constexpr int kEncVcap = 16384;  // key vectors per KV head encoded per launch
+
+struct EncodeWs {
+  size_t u, slot, ctr, total;
+};
+EncodeWs encode_layout(const a2ats_shape* s) {
+  EncodeWs w;
+  size_t o = 0;
+  w.u = o; o = align_up(o + (size_t)s->Hkv * kEncVcap * kD * 4);
+  w.slot = o; o = align_up(o + (size_t)s->Hkv * kEncVcap * 8);
+  w.ctr = o; o = align_up(o + (size_t)s->Hkv * (kEncVcap / 64) * 4);
+  w.total = o;
+  return w;
+}
+
+void fill_rope(const a2ats_params* p, RopeTab* rt) {
+  for (int m = 0; m < kHalf; ++m)
+    rt->inv_freq[m] = p->inv_freq ? p->inv_freq[m] : std::pow(p->rope_theta, -2.0 * m / (double)kD);
+}
+
+inline int cuda_status(cudaError_t e) { return e == cudaSuccess ? A2ATS_OK : A2ATS_ECUDA; }
+
+// Benchmark instrumentation (a2ats_set_stage_events).
+constexpr int kStageEvents = 6;
+bool g_stage_on = false;
+cudaEvent_t g_stage[kStageEvents];
+inline void stage_mark(int i, cudaStream_t st) {
+  if (g_stage_on) cudaEventRecord(g_stage[i], st);
+}
+
+}  // namespace
+}  // namespace a2ats
+
+using namespace a2ats;
+
+extern "C" {
+
+void a2ats_default_params(a2ats_params* p) {
+  if (!p) return;
+  std::memset(p, 0, sizeof(*p));
+  p->window = 64;
+  p->bridge = 2048;
+  p->n_sink = 4;
+  p->topk = 0;
+  p->rope_theta = 1e4;
+  p->inv_freq = nullptr;
+  p->group_reduce = A2ATS_GROUP_MAX;
+  p->kv_location = A2ATS_KV_DEVICE;
+}
+
+const char* a2ats_status_string(int status) {
+  switch (status) {
+    case A2ATS_OK: return "A2ATS_OK";
+    case A2ATS_EINVAL: return "A2ATS_EINVAL: invalid argument";
+    case A2ATS_EUNSUPPORTED: return "A2ATS_EUNSUPPORTED: shape not supported by this build";
+    case A2ATS_EWORKSPACE: return "A2ATS_EWORKSPACE: workspace missing or too small";
+    case A2ATS_ECUDA: return "A2ATS_ECUDA: CUDA launch failed";
+    case A2ATS_ENCCL: return "A2ATS_ENCCL: NCCL call failed";
+    default: return "A2ATS: unknown status";
+  }
+}
+
+int a2ats_abi_version(void) { return A2ATS_ABI_VERSION; }
+
+int a2ats_set_stage_events(void* const* events, int n) {
+  if (!events) {
+    g_stage_on = false;
+    return A2ATS_OK;
+  }
+  if (n < kStageEvents) return A2ATS_EINVAL;
+  for (int i = 0; i < kStageEvents; ++i) {
+    if (!events[i]) return A2ATS_EINVAL;
+    g_stage[i] = static_cast<cudaEvent_t>(events[i]);
+  }
+  g_stage_on = true;
+  return A2ATS_OK;
+}
+
+int a2ats_qavq_prepare(const a2ats_shape* shape, const void* codebook, const float* H, float* nrm, void* stream) {
+  int rc = check_shape(shape);
+  if (rc) return rc;
+  if (!codebook || !nrm || !aligned16(codebook) || (H && !aligned16(H))) return A2ATS_EINVAL;
+  return cuda_status(launch_prepare(static_cast<const uint16_t*>(codebook), H, nrm, shape->Hkv, shape->L,
+                                    static_cast<cudaStream_t>(stream)));
+}
+
+size_t a2ats_build_codes_workspace_bytes(const a2ats_shape* shape) {
+  if (check_shape(shape)) return 0;
+  return encode_layout(shape).total;
+}
+
+int a2ats_build_codes(const a2ats_shape* shape, const void* keys, int32_t t_begin, int32_t t_end,
+                      const void* codebook, const float* H, const float* nrm, uint16_t* codes, int32_t* hist,
+                      void* ws, size_t ws_bytes, void* stream) {
+  int rc = check_shape(shape);
+  if (rc) return rc;
+  if (!keys || !codebook || !nrm || !codes) return A2ATS_EINVAL;
+  if (!aligned16(keys) || !aligned16(codebook) || (H && !aligned16(H))) return A2ATS_EINVAL;
+  if (t_begin < 0 || t_end < t_begin || t_end > shape->n_max) return A2ATS_EINVAL;
+  const EncodeWs L = encode_layout(shape);
+  if (!ws || ws_bytes < L.total) return A2ATS_EWORKSPACE;
+  if (t_end == t_begin) return A2ATS_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  EncArgs a;
+  a.keys = static_cast<const uint16_t*>(keys);
+  a.codebook = static_cast<const uint16_t*>(codebook);
+  a.H = H;
+  a.nrm = nrm;
+  a.u = reinterpret_cast<float*>(base + L.u);
+  a.slot = reinterpret_cast<unsigned long long*>(base + L.slot);
+  a.counter = reinterpret_cast<unsigned int*>(base + L.ctr);
+  a.codes = codes;
+  a.hist = hist;
+  a.B = shape->B;
+  a.Hkv = shape->Hkv;
+  a.L = shape->L;
+  a.n_max = shape->n_max;
+  const int ntiles = (shape->L + 127) / 128;
+  const int tmax = std::max(1, kEncVcap / shape->B);  // tokens per launch so that B*T <= vcap
+  for (int t0 = t_begin; t0 < t_end; t0 += tmax) {
+    a.t_begin = t0;
+    a.T = std::min(tmax, t_end - t0);
+    a.nvec = shape->B * a.T;
+    if (a.nvec > kEncVcap) return A2ATS_EUNSUPPORTED;  // B > vcap
+    const int vt = (a.nvec + 63) / 64;
+    // split the codeword range so the grid covers the machine about twice
+    int lsplit = (2 * sm_count() + vt * shape->Hkv - 1) / (vt * shape->Hkv);
+    lsplit = std::max(1, std::min(lsplit, ntiles));
+    a.tiles_per_split = (ntiles + lsplit - 1) / lsplit;
+    a.lsplit = (ntiles + a.tiles_per_split - 1) / a.tiles_per_split;
+    rc = cuda_status(launch_encode(a, st));
+    if (rc) return rc;
+  }
+  return A2ATS_OK;
+}
+
+size_t a2ats_decode_workspace_bytes(const a2ats_shape* shape, const a2ats_params* params) {
+  if (check_shape(shape) || check_params(params)) return 0;
+  return decode_layout(shape, params).total;
+}
+
+int a2ats_decode_step(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx, const void* q,
+                      const void* k_cache, const void* v_cache, const uint16_t* codes, const void* codebook,
+                      const int32_t* hist, float* out, int32_t* sel_out, float* scores_out, void* ws,
+                      size_t ws_bytes, void* stream) {
+  int rc = check_shape(shape);
+  if (rc) return rc;
+  rc = check_params(params);
+  if (rc) return rc;
+  if (!q || !k_cache || !v_cache || !codes || !codebook || !out) return A2ATS_EINVAL;
+  if (!aligned16(q) || !aligned16(k_cache) || !aligned16(v_cache) || !aligned16(codes) || !aligned16(codebook) ||
+      !aligned16(out))
+    return A2ATS_EINVAL;
+  if (n_ctx <= 0 || n_ctx > shape->n_max) return A2ATS_EINVAL;
+  const DecodeWs Lw = decode_layout(shape, params);
+  if (!ws || ws_bytes < Lw.total) return A2ATS_EWORKSPACE;
+
+  Derived d;
+  derive(shape, params, n_ctx, &d);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  float* qrot = reinterpret_cast<float*>(base + Lw.qrot);
+  float2* cs = reinterpret_cast<float2*>(base + Lw.cs);
+  float* agg = reinterpret_cast<float*>(base + Lw.agg);
+  float* lut_full = scores_out ? reinterpret_cast<float*>(base + Lw.lut) : nullptr;
+  int32_t* sel = sel_out ? sel_out : reinterpret_cast<int32_t*>(base + Lw.sel);
+
+  // a1 + a2 (+ window rotation table)
+  LutArgs la;
+  la.q = static_cast<const uint16_t*>(q);
+  la.codebook = static_cast<const uint16_t*>(codebook);
+  la.agg = agg;
+  la.lut_full = lut_full;
+  la.qrot = qrot;
+  la.cs = cs;
+  la.B = shape->B;
+  la.Hq = shape->Hq;
+  la.Hkv = shape->Hkv;
+  la.G = d.G;
+  la.L = shape->L;
+  la.window = params->window;
+  la.bridge = params->bridge;
+  la.group_reduce = params->group_reduce;
+  fill_rope(params, &la.rt);
+  stage_mark(0, st);
+  rc = cuda_status(launch_lut(la, st));
+  if (rc) return rc;
+  stage_mark(1, st);
+
+  // a3 + a4
+  if (d.keff > 0) {
+    SelArgs sa;
+    sa.agg = agg;
+    sa.hist = hist;
+    sa.codes = codes;
+    sa.cls = reinterpret_cast<uint32_t*>(base + Lw.cls);
+    sa.pinfo = reinterpret_cast<int32_t*>(base + Lw.pinfo);
+    sa.status = reinterpret_cast<unsigned long long*>(base + Lw.status);
+    sa.tile_counter = reinterpret_cast<unsigned int*>(base + Lw.tilectr);
+    sa.sel = sel;
+    sa.L = shape->L;
+    sa.W = d.W;
+    sa.n_max = shape->n_max;
+    sa.n_ctx = n_ctx;
+    sa.c0 = d.c0;
+    sa.c1 = d.c1;
+    sa.n_s = d.n_s;
+    sa.w0 = d.w0;
+    sa.keff = d.keff;
+    sa.nchunks = d.nchunks;
+    sa.first_chunk = d.first_chunk;
+    sa.chunk_tokens = d.CH;
+    rc = cuda_status(launch_threshold(sa, d.P, st));
+    if (rc) return rc;
+    stage_mark(2, st);
+    rc = cuda_status(launch_scan(sa, d.P, d.U, st));
+    if (rc) return rc;
+    stage_mark(3, st);
+  } else {
+    stage_mark(2, st);
+    stage_mark(3, st);
+  }
+
+  // a5 + a6
+  AttnArgs aa;
+  aa.q = static_cast<const uint16_t*>(q);
+  aa.qrot = qrot;
+  aa.cs = cs;
+  aa.kc = static_cast<const uint16_t*>(k_cache);
+  aa.vc = static_cast<const uint16_t*>(v_cache);
+  aa.sel = sel;
+  aa.part = reinterpret_cast<float*>(base + Lw.part);
+  aa.counter = reinterpret_cast<unsigned int*>(base + Lw.actr);
+  aa.out = out;
+  aa.Hq = shape->Hq;
+  aa.Hkv = shape->Hkv;
+  aa.G = d.G;
+  aa.n_max = shape->n_max;
+  aa.n_ctx = n_ctx;
+  aa.n_s = d.n_s;
+  aa.keff = d.keff;
+  aa.n_w = d.n_w;
+  aa.w0 = d.w0;
+  aa.M = d.M;
+  aa.R = d.R;
+  aa.nsplit = d.nsplit;
+  aa.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)kD));
+  rc = cuda_status(launch_attention(aa, d.P, d.GT, st));
+  if (rc) return rc;
+  stage_mark(4, st);
+
+  if (scores_out) {
+    rc = cuda_status(launch_scores(lut_full, codes, scores_out, shape->B, shape->Hq, shape->Hkv, d.G, shape->L,
+                                   shape->n_max, n_ctx, st));
+    if (rc) return rc;
+  }
+  stage_mark(5, st);
+  return A2ATS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,49 @@
+"""Convenience owner of the per-model state around the C ABI: the prepared
+codebook term n_j, zero-initialised workspaces, the code array and the running
+code histogram.  Every method is a single call (or a short sequence of calls)
+into liba2ats.so; no arithmetic of the method happens here."""
+from __future__ import annotations
+
+import torch
+
+from . import binding as _b
+
+
+class Decoder:
+    def __init__(self, B, Hq, Hkv, L, n_max, codebook, H=None, params: _b.Params | None = None, device="cuda",
+                 stream=None):
+        self.device = torch.device(device)
+        self.shape = _b.make_shape(B, Hq, Hkv, 128, L, n_max)
+        self.params = params or _b.Params()
+        self.stream = stream
+        self.codebook = codebook.contiguous()
+        self.H = None if H is None else H.contiguous().float()
+        self.nrm = torch.empty((Hkv, L), dtype=torch.float32, device=self.device)
+        _b.a2ats_qavq_prepare(self.shape, self.codebook, self.H, self.nrm, stream)
+        self.ws_enc = torch.zeros(_b.a2ats_build_codes_workspace_bytes(self.shape), dtype=torch.uint8,
+                                  device=self.device)
+        self.ws_dec = torch.zeros(_b.a2ats_decode_workspace_bytes(self.shape, self.params), dtype=torch.uint8,
+                                  device=self.device)
+        self.codes = torch.zeros((B, Hkv, n_max), dtype=torch.uint16, device=self.device)
+        self.hist = torch.zeros((B, Hkv, L), dtype=torch.int32, device=self.device)
+
+    def set_topk(self, k: int):
+        self.params.topk = int(k)
+        need = _b.a2ats_decode_workspace_bytes(self.shape, self.params)
+        if need > self.ws_dec.numel():
+            self.ws_dec = torch.zeros(need, dtype=torch.uint8, device=self.device)
+
+    def encode(self, keys, t_begin: int, t_end: int, update_hist: bool = True, codes=None):
+        _b.a2ats_build_codes(self.shape, keys, t_begin, t_end, self.codebook, self.H, self.nrm,
+                             self.codes if codes is None else codes, self.hist if update_hist else None,
+                             self.ws_enc, self.stream)
+
+    def step(self, q, k_cache, v_cache, n_ctx: int, out=None, sel_out=None, scores_out=None, use_hist=True,
+             codes=None, kv_host=False):
+        if out is None:
+            out = torch.empty((self.shape.B, self.shape.Hq, 128), dtype=torch.float32, device=self.device)
+        _b.a2ats_decode_step(self.shape, self.params, n_ctx, q, k_cache, v_cache,
+                             self.codes if codes is None else codes, self.codebook,
+                             self.hist if use_hist else None, out, sel_out, scores_out, self.ws_dec, self.stream,
+                             kv_host=kv_host)
+        return out

@@ -1,0 +1,281 @@
+"""GPU parity: the CUDA path through the C ABI vs the fp64 oracle, element by
+element, on the same seeded inputs (BJ tolerances: codes and top-K sets
+bit-exact, scores 1e-4 row-relative, output 2e-3 relative L2)."""
+import numpy as np
+import pytest
+import torch
+
+from helpers import OUT_RTOL, SCORE_RTOL, codes_np, cut_gap, f64, pair_oracle, redraw_for_gap, rel_l2, row_rel_max
+from oracle import a2ats_oracle as O
+from synth import CONFIGS, Config, make_inputs
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    import paper_2502_12665_b200 as A
+
+
+def hist_of(codes: torch.Tensor, L: int, n_ctx: int) -> torch.Tensor:
+    B, Hkv, _ = codes.shape
+    c = codes[:, :, :n_ctx].to(torch.int64)
+    h = torch.zeros((B, Hkv, L), dtype=torch.int32, device=codes.device)
+    h.scatter_add_(2, c, torch.ones_like(c, dtype=torch.int32))
+    return h
+
+
+def run_case(cfg: Config, seed: int, family="g2", code_dist="uniform", bridge=None, n_ctx=None, use_hist=True,
+             scores=True, gap_redraw=True, group_reduce=O.GROUP_MAX, pairs=None, device="cuda"):
+    n_ctx = cfg.N if n_ctx is None else n_ctx
+    bridge = cfg.bridge if bridge is None else bridge
+    inp = make_inputs(cfg, seed, device="cpu", family=family, code_dist=code_dist, with_h=False)
+    inp["codes"] = inp["z"].to(torch.uint16)
+    if gap_redraw and family != "g1":
+        redraw_for_gap(inp, cfg.with_(bridge=bridge), n_ctx, seed, pairs=pairs)
+    dev = {k: (v.to(device) if isinstance(v, torch.Tensor) else v) for k, v in inp.items()}
+    params = A.Params(window=cfg.window, bridge=bridge, n_sink=cfg.n_sink, topk=cfg.K, group_reduce=group_reduce)
+    shape = A.make_shape(cfg.B, cfg.Hq, cfg.Hkv, cfg.d, cfg.L, inp["n_max"])
+    ws = torch.zeros(A.a2ats_decode_workspace_bytes(shape, params), dtype=torch.uint8, device=device)
+    out = torch.full((cfg.B, cfg.Hq, cfg.d), float("nan"), device=device)
+    S, cand, W = O.token_sets(n_ctx, cfg.window, cfg.n_sink)
+    keff = min(cfg.K, cand.size)
+    sel = torch.full((cfg.B, cfg.Hkv, max(keff, 1)), -1, dtype=torch.int32, device=device)
+    sc = torch.empty((cfg.B, cfg.Hq, n_ctx), device=device) if scores else None
+    hist = hist_of(dev["codes"], cfg.L, n_ctx) if use_hist else None
+    A.a2ats_decode_step(shape, params, n_ctx, dev["q"], dev["k_cache"], dev["v_cache"], dev["codes"],
+                        dev["codebook"], hist, out, sel, sc, ws)
+    torch.cuda.synchronize()
+    return inp, dict(out=out.cpu().numpy(), sel=sel.cpu().numpy()[:, :, :keff], scores=None if sc is None else sc.cpu().numpy(),
+                     ws=ws), params
+
+
+def check_against_oracle(cfg, inp, gpu, n_ctx=None, bridge=None, pairs=None, exact_sets=True,
+                         group_reduce=O.GROUP_MAX):
+    n_ctx = cfg.N if n_ctx is None else n_ctx
+    G = cfg.Hq // cfg.Hkv
+    C = f64(inp["codebook"])
+    codes = codes_np(inp["codes"])
+    pairs = pairs or [(b, h) for b in range(cfg.B) for h in range(cfg.Hkv)]
+    worst = dict(score=0.0, out=0.0)
+    for b, h in pairs:
+        r = pair_oracle(f64(inp["q"][b, h * G:(h + 1) * G]), f64(inp["k_cache"][b, h]), f64(inp["v_cache"][b, h]),
+                        codes[b, h], C[h], n_ctx, cfg, bridge=bridge, group_reduce=group_reduce)
+        if exact_sets:
+            np.testing.assert_array_equal(gpu["sel"][b, h], r["sel"], err_msg=f"top-K set of pair {(b, h)}")
+        if gpu["scores"] is not None:
+            for g in range(G):
+                e = row_rel_max(gpu["scores"][b, h * G + g], r["scores"][g])
+                worst["score"] = max(worst["score"], e)
+                assert e <= SCORE_RTOL, f"scores row {(b, h * G + g)} rel err {e}"
+        for g in range(G):
+            e = rel_l2(gpu["out"][b, h * G + g], r["out"][g])
+            worst["out"] = max(worst["out"], e)
+            assert e <= OUT_RTOL, f"output row {(b, h * G + g)} rel L2 {e}"
+    return worst
+
+
+# ------------------------------------------------------------------ C1 and small multi-tile shapes
+def test_c1_realistic():
+    cfg = CONFIGS["C1"]
+    inp, gpu, _ = run_case(cfg, seed=11)
+    w = check_against_oracle(cfg, inp, gpu)
+    assert w["out"] < 1e-4
+
+
+def test_c1_integer_exact_ties():
+    # G1 family with b = 0: LUT values exact in fp32 -> cross-code ties exact on both sides
+    cfg = CONFIGS["C1"]
+    inp, gpu, _ = run_case(cfg, seed=12, family="g1", bridge=0)
+    check_against_oracle(cfg, inp, gpu, bridge=0)
+
+
+SMALL = Config("small", B=2, Hq=8, Hkv=2, d=128, N=20001, L=1000, K=1200)
+
+
+@pytest.mark.parametrize("use_hist", [True, False])
+def test_multi_tile_ragged(use_hist):
+    inp, gpu, _ = run_case(SMALL, seed=21, use_hist=use_hist)
+    check_against_oracle(SMALL, inp, gpu)
+
+
+def test_multi_tile_integer_ties_gqa():
+    cfg = SMALL.with_(L=300, K=5000)
+    inp, gpu, _ = run_case(cfg, seed=22, family="g1", bridge=0, code_dist="zipf")
+    check_against_oracle(cfg, inp, gpu, bridge=0)
+
+
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
+def test_gqa_group_sizes(G):
+    cfg = Config("gqa", B=2, Hq=2 * G, Hkv=2, d=128, N=3000, L=512, K=180)
+    inp, gpu, _ = run_case(cfg, seed=30 + G)
+    check_against_oracle(cfg, inp, gpu)
+
+
+def test_group_sum():
+    cfg = Config("gsum", B=2, Hq=8, Hkv=2, d=128, N=5000, L=512, K=300)
+    inp, gpu, _ = run_case(cfg, seed=41, family="g1", bridge=0, group_reduce=O.GROUP_SUM)
+    check_against_oracle(cfg, inp, gpu, bridge=0, group_reduce=O.GROUP_SUM)
+
+
+@pytest.mark.parametrize("n_ctx,k", [(1, 5), (7, 5), (64, 5), (65, 5), (66, 5), (68, 5), (69, 1), (70, 100),
+                                     (1000, 0), (1000, 932), (1000, 10_000), (4093, 1)])
+def test_degenerate_sizes(n_ctx, k):
+    cfg = Config("deg", B=1, Hq=4, Hkv=1, d=128, N=n_ctx, L=64, K=k)
+    inp, gpu, _ = run_case(cfg.with_(), seed=50 + n_ctx, n_ctx=n_ctx)
+    check_against_oracle(cfg, inp, gpu, n_ctx=n_ctx)
+
+
+def test_window_covers_context_equals_rope():
+    cfg = Config("win", B=1, Hq=4, Hkv=1, d=128, N=60, L=64, K=5)
+    inp, gpu, _ = run_case(cfg, seed=61)
+    check_against_oracle(cfg, inp, gpu)
+
+
+def test_hist_and_no_hist_bitwise_equal_and_deterministic():
+    cfg = SMALL
+    inp1, g1, _ = run_case(cfg, seed=71, use_hist=True, scores=False)
+    inp2, g2, _ = run_case(cfg, seed=71, use_hist=False, scores=False)
+    _, g3, _ = run_case(cfg, seed=71, use_hist=True, scores=False)
+    np.testing.assert_array_equal(g1["sel"], g2["sel"])
+    assert np.array_equal(g1["out"].view(np.uint32), g2["out"].view(np.uint32))
+    assert np.array_equal(g1["out"].view(np.uint32), g3["out"].view(np.uint32))
+
+
+def test_workspace_returns_to_zero_state_for_counters():
+    # calling twice with the same workspace gives identical results (counters reset by the kernels)
+    cfg = SMALL
+    inp = make_inputs(cfg, 81, device="cpu", with_h=False)
+    inp["codes"] = inp["z"].to(torch.uint16)
+    dev = {k: (v.cuda() if isinstance(v, torch.Tensor) else v) for k, v in inp.items()}
+    params = A.Params(topk=cfg.K)
+    shape = A.make_shape(cfg.B, cfg.Hq, cfg.Hkv, 128, cfg.L, inp["n_max"])
+    ws = torch.zeros(A.a2ats_decode_workspace_bytes(shape, params), dtype=torch.uint8, device="cuda")
+    outs = []
+    for _ in range(3):
+        out = torch.empty((cfg.B, cfg.Hq, 128), device="cuda")
+        A.a2ats_decode_step(shape, params, cfg.N, dev["q"], dev["k_cache"], dev["v_cache"], dev["codes"],
+                            dev["codebook"], None, out, None, None, ws)
+        outs.append(out.cpu())
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[1], outs[2])
+
+
+def test_needle_attention():
+    cfg = Config("needle", B=2, Hq=8, Hkv=2, d=128, N=8000, L=512, K=480)
+    inp, gpu, _ = run_case(cfg, seed=91, family="needle")
+    check_against_oracle(cfg, inp, gpu)
+
+
+def test_lossless_codebook_exact_scores():
+    # every key its own codeword: u^ equals the exact bridge score q~ . k_t (BJ pin), on the GPU
+    cfg = Config("lossless", B=1, Hq=1, Hkv=1, d=128, N=1024, L=1024, K=100)
+    inp = make_inputs(cfg, 101, device="cpu", with_h=False)
+    inp["codebook"] = inp["k_cache"][0, :, :cfg.L].clone()
+    inp["codes"] = torch.arange(cfg.N, dtype=torch.int32).view(1, 1, -1).to(torch.uint16)
+    inp["codes"] = torch.nn.functional.pad(inp["codes"].to(torch.int32), (0, inp["n_max"] - cfg.N)).to(torch.uint16)
+    dev = {k: (v.cuda() if isinstance(v, torch.Tensor) else v) for k, v in inp.items()}
+    params = A.Params(topk=cfg.K)
+    shape = A.make_shape(1, 1, 1, 128, cfg.L, inp["n_max"])
+    ws = torch.zeros(A.a2ats_decode_workspace_bytes(shape, params), dtype=torch.uint8, device="cuda")
+    out = torch.empty((1, 1, 128), device="cuda")
+    sc = torch.empty((1, 1, cfg.N), device="cuda")
+    A.a2ats_decode_step(shape, params, cfg.N, dev["q"], dev["k_cache"], dev["v_cache"], dev["codes"],
+                        dev["codebook"], None, out, None, sc, ws)
+    qrot = O.wrope_query(f64(inp["q"][0, 0]), 2048, O.inv_freq(128))
+    exact = f64(inp["k_cache"][0, 0, :cfg.N]) @ qrot
+    assert row_rel_max(sc.cpu().numpy()[0, 0], exact) <= SCORE_RTOL
+
+
+# ------------------------------------------------------------------ encoding (a0)
+@pytest.mark.parametrize("with_h", [True, False])
+def test_build_codes_matches_oracle(with_h):
+    cfg = Config("enc", B=3, Hq=8, Hkv=2, d=128, N=700, L=384, K=10)
+    inp = make_inputs(cfg, 111, device="cpu", with_h=True)
+    H = inp["H"] if with_h else None
+    dev = {k: (v.cuda() if isinstance(v, torch.Tensor) else v) for k, v in inp.items()}
+    dec = A.Decoder(cfg.B, cfg.Hq, cfg.Hkv, cfg.L, inp["n_max"], dev["codebook"], None if H is None else dev["H"])
+    dec.encode(dev["k_cache"], 0, 300)
+    dec.encode(dev["k_cache"], 300, cfg.N)
+    torch.cuda.synchronize()
+    got = codes_np(dec.codes)
+    C = f64(inp["codebook"])
+    for b in range(cfg.B):
+        for h in range(cfg.Hkv):
+            keys = f64(inp["k_cache"][b, h, :cfg.N])
+            ref = O.qavq_encode(keys, C[h], None if H is None else f64(H[h]))
+            np.testing.assert_array_equal(got[b, h, :cfg.N], ref)
+            np.testing.assert_array_equal(dec.hist[b, h].cpu().numpy(), np.bincount(ref, minlength=cfg.L))
+    # with keys drawn around codewords, the codes recover the generating assignment
+    if not with_h:
+        np.testing.assert_array_equal(got[:, :, :cfg.N], codes_np(inp["z"])[:, :, :cfg.N])
+
+
+def test_build_codes_keys_equal_codewords_and_ties():
+    cfg = Config("enc2", B=1, Hq=1, Hkv=1, d=128, N=256, L=128, K=10)
+    inp = make_inputs(cfg, 121, device="cpu", with_h=True, family="g1")
+    C = inp["codebook"].clone()
+    C[0, 100] = C[0, 3]              # duplicate codeword: lowest index wins
+    keys = torch.zeros((1, 1, inp["n_max"], 128), dtype=torch.bfloat16)
+    keys[0, 0, :128] = C[0]
+    dec = A.Decoder(1, 1, 1, cfg.L, inp["n_max"], C.cuda(), inp["H"].cuda())
+    dec.encode(keys.cuda(), 0, 128)
+    got = codes_np(dec.codes)[0, 0, :128]
+    want = np.arange(128)
+    want[100] = 3
+    np.testing.assert_array_equal(got, want)
+
+
+# ------------------------------------------------------------------ host-mapped K/V (offload gather, C3 mirror)
+def test_host_mapped_kv():
+    cfg = Config("host", B=2, Hq=8, Hkv=2, d=128, N=9000, L=512, K=540)
+    inp = make_inputs(cfg, 131, device="cpu", with_h=False)
+    inp["codes"] = inp["z"].to(torch.uint16)
+    redraw_for_gap(inp, cfg, cfg.N, 131)
+    kh = inp["k_cache"].pin_memory()
+    vh = inp["v_cache"].pin_memory()
+    dev = {k: (v.cuda() if isinstance(v, torch.Tensor) else v) for k, v in inp.items()}
+    params = A.Params(topk=cfg.K, kv_location=A.A2ATS_KV_HOST_MAPPED)
+    shape = A.make_shape(cfg.B, cfg.Hq, cfg.Hkv, 128, cfg.L, inp["n_max"])
+    ws = torch.zeros(A.a2ats_decode_workspace_bytes(shape, params), dtype=torch.uint8, device="cuda")
+    out = torch.empty((cfg.B, cfg.Hq, 128), device="cuda")
+    sel = torch.empty((cfg.B, cfg.Hkv, cfg.K), dtype=torch.int32, device="cuda")
+    A.a2ats_decode_step(shape, params, cfg.N, dev["q"], kh, vh, dev["codes"], dev["codebook"], None, out, sel, None,
+                        ws, kv_host=True)
+    torch.cuda.synchronize()
+    gpu = dict(out=out.cpu().numpy(), sel=sel.cpu().numpy(), scores=None)
+    check_against_oracle(cfg, inp, gpu)
+
+
+# ------------------------------------------------------------------ full size (C2), sampled
+def test_c2_full_size_sampled():
+    cfg = CONFIGS["C2"]
+    seed = 0xA2A75 + 2
+    inp = make_inputs(cfg, seed, device="cuda", with_h=False)
+    inp["codes"] = inp["z"].to(torch.uint16)
+    sample = [(0, 0), (3, 5), (7, 7), (15, 2), (9, 4), (12, 1)]
+    host = dict(q=inp["q"].cpu(), codebook=inp["codebook"].cpu(), codes=inp["codes"].cpu())
+    redraw_for_gap(host, cfg, cfg.N, seed, pairs=sample)
+    inp["q"] = host["q"].cuda()
+    dec = A.Decoder(cfg.B, cfg.Hq, cfg.Hkv, cfg.L, inp["n_max"], inp["codebook"])
+    dec.codes = inp["codes"]
+    dec.hist = hist_of(inp["codes"], cfg.L, cfg.N)
+    dec.set_topk(cfg.K)
+    sel = torch.empty((cfg.B, cfg.Hkv, cfg.K), dtype=torch.int32, device="cuda")
+    out = dec.step(inp["q"], inp["k_cache"], inp["v_cache"], cfg.N, sel_out=sel)
+    torch.cuda.synchronize()
+    s = sel.cpu().numpy()
+    # properties at every pair: ascending, unique, inside the candidate range
+    assert np.all(np.diff(s, axis=2) > 0)
+    assert s.min() >= cfg.n_sink and s.max() < cfg.N - cfg.window
+    small = dict(q=host["q"], codebook=host["codebook"], codes=host["codes"],
+                 k_cache=_PairView(inp["k_cache"]), v_cache=_PairView(inp["v_cache"]))
+    gpu = dict(out=out.cpu().numpy(), sel=s, scores=None)
+    check_against_oracle(cfg, small, gpu, pairs=sample)
+
+
+class _PairView:
+    """Indexes [b, h] of a device tensor lazily so only sampled pairs cross to the host."""
+
+    def __init__(self, t):
+        self.t = t
+
+    def __getitem__(self, idx):
+        return self.t[idx].cpu()
