@@ -114,8 +114,8 @@ def stage_model(cfg, n_ctx: int, k: int):
                        flops=2 * P * L * d + 2 * P * d * d, bound="hbm"),
         "lut": dict(bytes=Hkv * L * d * 2 + B * Hq * d * 2 + P * L * 4 + B * Hq * d * 4, flops=2 * B * Hq * L * d,
                     bound="alu"),
-        "threshold": dict(bytes=P * L * 4 * 2 + P * (L // 16) * 4, flops=0, bound="hbm"),
-        "scan": dict(bytes=P * n_cand * 2 + P * keff * 4, flops=0, bound="hbm", tokens=P * n_ctx),
+        "select": dict(bytes=P * n_cand * 2 + P * keff * 4, flops=0, bound="hbm", tokens=P * n_ctx,
+                       aux_bytes=P * L * 4 * 2),
         "attention": dict(bytes=P * M * d * 2 * 2 + P * keff * 4 + B * Hq * d * (2 + 4 + 4),
                           flops=4 * B * Hq * M * d, bound="hbm", rows=P * M),
     }
@@ -134,64 +134,86 @@ def run_ours(args, rank: int, world: int):
     cfg = CONFIGS[args.config]
     if args.batch:
         cfg = cfg.with_(B=args.batch)
-    steps_total = args.warmup + args.steps
-    n0 = cfg.N - steps_total                     # prefix encoded before the loop
-    inp = make_inputs(cfg, SEED + 17 * rank, device=dev, with_h=True, n_max=cfg.n_max(extra=256))
+    e2e_steps = max(3, args.steps // 2)
+    steps_total = 1 + args.warmup + args.steps     # 1 eager step sets kernel attributes before capture
+    n0 = cfg.N - steps_total                        # prefix encoded before the loop; last timed step has n = N
+    inp = make_inputs(cfg, SEED + 17 * rank, device=dev, with_h=True, n_max=cfg.n_max(extra=e2e_steps + 8))
     q, kc, vc = inp["q"], inp["k_cache"], inp["v_cache"]
-    params = A.Params(topk=budget_k(cfg.N))
+    params = A.Params(topk=budget_k(cfg.N + e2e_steps))
     dec = A.Decoder(cfg.B, cfg.Hq, cfg.Hkv, cfg.L, inp["n_max"], inp["codebook"], inp["H"], params, device=dev)
-    dec.encode(kc, 0, n0)                       # prefill codes + running histogram (untimed)
+    dec.encode(kc, 0, n0)                           # prefill codes + running histogram (untimed)
     out = torch.empty((cfg.B, cfg.Hq, cfg.d), dtype=torch.float32, device=dev)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)   # 256 MB > 126 MB L2
     torch.cuda.synchronize()
 
-    stream = torch.cuda.current_stream()
-    n_stage = 6
-    stage_ev = [[torch.cuda.Event(enable_timing=True) for _ in range(n_stage)] for _ in range(args.steps)]
+    def one_step(n, evs=None, enc=None):
+        st = torch.cuda.current_stream()
+        if enc is not None:
+            enc[0].record(st)
+            A.a2ats_set_stage_events(evs)
+        dec.encode(kc, n - 1, n)                    # a0: the new token's code (+ hist)
+        dec.params.topk = budget_k(n)
+        dec.step(q, kc, vc, n, out=out)             # a1..a6
+        if enc is not None:
+            enc[1].record(st)
+            A.a2ats_set_stage_events(None)
+
+    stage_ev = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(args.steps)]
     enc_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     for evs in stage_ev:
         for e in evs:
-            e.record(stream)      # materialise handles
+            e.record()                              # materialise the handles
+    n = n0 + 1
+    one_step(n)                                     # eager: one-time cudaFuncSetAttribute etc.
+    torch.cuda.synchronize()
 
-    def one_step(n, k_step):
-        tb = enc_ev[k_step][0] if k_step is not None else None
-        if tb is not None:
-            tb.record(stream)
-            A.a2ats_set_stage_events(stage_ev[k_step])
-        dec.encode(kc, n - 1, n)                 # a0: the new token's code (+ hist)
-        dec.params.topk = budget_k(n)
-        dec.step(q, kc, vc, n, out=out)          # a1..a6
-        if tb is not None:
-            enc_ev[k_step][1].record(stream)
-            A.a2ats_set_stage_events(None)
-
-    n = n0
-    for _ in range(args.warmup):
+    # One CUDA graph per step (n_ctx differs per step): replay = one launch per step, so the
+    # device timeline is not paced by host-side launch latency.
+    use_graph = not args.no_graph
+    graphs, ns = [], []
+    for s in range(args.warmup + args.steps):
         n += 1
+        ns.append(n)
+        k = s - args.warmup
+        evs = stage_ev[k] if k >= 0 else None
+        enc = enc_ev[k] if k >= 0 else None
+        if use_graph:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                one_step(n, evs, enc)
+            graphs.append(g)
+    torch.cuda.synchronize()
+
+    def run(s):
+        if use_graph:
+            graphs[s].replay()
+        else:
+            k = s - args.warmup
+            one_step(ns[s], stage_ev[k] if k >= 0 else None, enc_ev[k] if k >= 0 else None)
+
+    for s in range(args.warmup):
         flush.fill_(1.0)
-        one_step(n, None)
+        run(s)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
     tokens = 0
     with ClockSampler(local) as clk:
-        for s in range(args.steps):
-            n += 1
+        for s in range(args.warmup, args.warmup + args.steps):
             if not args.no_flush:
                 flush.fill_(float(s))
-            one_step(n, s)
-            tokens += cfg.B * cfg.Hkv * n
+            run(s)
+            tokens += cfg.B * cfg.Hkv * ns[s]
         torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
-    step_ms = [enc_ev[s][0].elapsed_time(enc_ev[s][1]) for s in range(args.steps)]
-    names = ["lut", "threshold", "scan", "attention"]
-    stage_ms = {nm: [] for nm in names}
-    stage_ms["encode"] = []
-    for s in range(args.steps):
-        ev = stage_ev[s]
-        stage_ms["encode"].append(enc_ev[s][0].elapsed_time(ev[0]))
+    step_ms = [enc_ev[k][0].elapsed_time(enc_ev[k][1]) for k in range(args.steps)]
+    names = ["lut", "select", "attention"]
+    stage_ms = {nm: [] for nm in ["encode"] + names}
+    for k in range(args.steps):
+        ev = stage_ev[k]
+        stage_ms["encode"].append(enc_ev[k][0].elapsed_time(ev[0]))
         for i, nm in enumerate(names):
             stage_ms[nm].append(ev[i].elapsed_time(ev[i + 1]))
     total_ms = sum(step_ms)
@@ -203,55 +225,72 @@ def run_ours(args, rank: int, world: int):
         torch.distributed.all_reduce(tk)
         tokens = tk.item()
     value = tokens / (total_ms / 1e3)
+    n_last = ns[-1]
+    del graphs
 
-    # ---- e2e: same step through the public API with host buffers (pinned), copies inside the timed region
-    e2e = run_e2e(args, dec, cfg, kc, vc, q, n, stream, A, budget_k)
-
-    res = dict(value=value, ms_per_step=total_ms / args.steps, stage_ms={k: statistics.mean(v) for k, v in stage_ms.items()},
-               clocks=clk.summary(), e2e=e2e, n_last=n, cfg=cfg)
-    return res
+    e2e = run_e2e(e2e_steps, dec, cfg, kc, vc, q, n_last, A, budget_k, use_graph, world, dev)
+    return dict(value=value, ms_per_step=total_ms / args.steps,
+                stage_ms={k: statistics.mean(v) for k, v in stage_ms.items()},
+                clocks=clk.summary(), e2e=e2e, n_last=n_last, cfg=cfg, graph=use_graph)
 
 
-def run_e2e(args, dec, cfg, kc, vc, q, n_start, stream, A, budget_k):
+def run_e2e(steps, dec, cfg, kc, vc, q, n_start, A, budget_k, use_graph, world, dev):
+    """Same step through the public API with HOST buffers: every step copies its
+    inputs (q, the new token's k and v rows) from pinned host memory into the
+    device, runs a0 + decode_step, and reads the output back to pinned host
+    memory, all inside the timed region (CUDA events)."""
     import torch
-    steps = max(3, args.steps // 2)
     B, Hq, Hkv, d = cfg.B, cfg.Hq, cfg.Hkv, cfg.d
     q_host = q.detach().cpu().pin_memory()
-    knew = torch.empty((B, Hkv, d), dtype=torch.bfloat16).pin_memory()
-    vnew = torch.empty((B, Hkv, d), dtype=torch.bfloat16).pin_memory()
+    k_host = [kc[:, :, n_start + s].cpu().pin_memory() for s in range(steps)]   # rows appended by this loop
+    v_host = [vc[:, :, n_start + s].cpu().pin_memory() for s in range(steps)]
     out_host = torch.empty((B, Hq, d), dtype=torch.float32).pin_memory()
     q_dev = torch.empty_like(q)
-    out = torch.empty((B, Hq, d), dtype=torch.float32, device=q.device)
-    # the decode loop keeps appending: the new token's K/V rows come from the synthetic cache, staged in
-    # pinned host buffers and copied in inside the timed region
-    n = n_start
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    tot = 0.0
-    tokens = 0
-    for s in range(steps):
-        n += 1
-        knew.copy_(kc[:, :, n - 1].cpu())
-        vnew.copy_(vc[:, :, n - 1].cpu())
-        torch.cuda.synchronize()
-        ev0.record(stream)
+    out = torch.empty((B, Hq, d), dtype=torch.float32, device=dev)
+
+    def one(s):
+        n = n_start + s + 1
         q_dev.copy_(q_host, non_blocking=True)
-        kc[:, :, n - 1].copy_(knew, non_blocking=True)
-        vc[:, :, n - 1].copy_(vnew, non_blocking=True)
+        kc[:, :, n - 1].copy_(k_host[s], non_blocking=True)
+        vc[:, :, n - 1].copy_(v_host[s], non_blocking=True)
         dec.encode(kc, n - 1, n)
         dec.params.topk = budget_k(n)
         dec.step(q_dev, kc, vc, n, out=out)
         out_host.copy_(out, non_blocking=True)
-        ev1.record(stream)
-        ev1.synchronize()
-        tot += ev0.elapsed_time(ev1)
-        tokens += B * Hkv * n
-    h2d = q_host.numel() * 2 + knew.numel() * 2 + vnew.numel() * 2
+
+    graphs = []
+    if use_graph:
+        for s in range(steps):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                one(s)
+            graphs.append(g)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    tokens = 0
+    ev0.record()
+    for s in range(steps):
+        if use_graph:
+            graphs[s].replay()
+        else:
+            one(s)
+        tokens += B * Hkv * (n_start + s + 1)
+    ev1.record()
+    ev1.synchronize()
+    tot = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([tot], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        tot = float(t.item())
+        tk = torch.tensor([float(tokens)], device=dev)
+        torch.distributed.all_reduce(tk)
+        tokens = tk.item()
+    h2d = q_host.numel() * 2 + k_host[0].numel() * 2 + v_host[0].numel() * 2
     d2h = out_host.numel() * 4
     return {"value": tokens / (tot / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "ms_per_step": tot / steps, "steps": steps}
+            "ms_per_step": tot / steps, "steps": steps, "l2": "not flushed (back-to-back steps)"}
 
 
-# ---------------------------------------------------------------------------- CPU oracle (baseline / reference arm)
 def oracle_sample(cfg, seconds_budget: float = 15.0, max_pairs: int = 64):
     """Times the fp64 oracle (as it stands) on whole (b, kv-head) pairs of the
     workload: same N, L, G, budget; per-pair work identical to the GPU arm."""
@@ -336,6 +375,7 @@ def main():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=2.0)
     args = ap.parse_args()
@@ -366,7 +406,7 @@ def main():
         kernels[nm] = {"ms": ms, "alg_bytes": m["bytes"], "GBps": gbs,
                        "frac_hbm": (gbs / pk["hbm"]) if gbs else None, "flops": m["flops"],
                        "TFLOPs": m["flops"] / (ms * 1e-3) / 1e12 if ms > 0 else None}
-    dom = max(("attention", "scan", "lut", "threshold", "encode"), key=lambda k: r["stage_ms"][k])
+    dom = max(("attention", "select", "lut", "encode"), key=lambda k: r["stage_ms"][k])
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
@@ -391,7 +431,7 @@ def main():
             cpu = oracle_sample(cfg, seconds_budget=15.0)
         except Exception as e:  # never let the baseline kill the line
             cpu = {"error": repr(e)}
-    launches_per_step = 6  # keyh + encode_argmin + lut + threshold + scan + attention
+    launches_per_step = 5  # keyh + encode_argmin + lut + select + attention
     line = {
         "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak",
@@ -402,6 +442,7 @@ def main():
                    "parallelism": f"replicas x{world} (batch/head parallel, no collective)" if world > 1 else "1 GPU",
                    "l2": "flushed between steps (256 MB write, outside the timed events)" if not args.no_flush else "not flushed",
                    "step": "a0 encode new token (+hist) + a2ats_decode_step (a1..a6)",
+                   "launch": "one CUDA graph per step (replay)" if r["graph"] else "eager launches",
                    "sparsity": (budget_k(r["n_last"]) + 68) / r["n_last"], "aux_mem": 2 / (cfg.d * 2)},
         "roofline": roof,
         "kernels": kernels,

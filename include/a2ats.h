@@ -173,10 +173,10 @@ int a2ats_decode_step(const a2ats_shape* shape, const a2ats_params* params, int3
  * a2ats_set_stage_events -- optional instrumentation for benchmarks.
  *
  * events: host array of n cudaEvent_t handles (passed as void*), or NULL to
- * disable.  While set, every a2ats_decode_step records events[0..5] on its
+ * disable.  While set, every a2ats_decode_step records events[0..4] on its
  * stream at the stage boundaries: [0] before a1/a2 (LUT), [1] after the LUT,
- * [2] after the threshold (a4 part 1), [3] after the code scan (a3 + a4),
- * [4] after attention + combine (a5 + a6), [5] at the end.  Requires n >= 6.
+ * [2] after the code scan + top-K (a3 + a4), [3] after attention + combine
+ * (a5 + a6), [4] at the end.  Requires n >= 5.
  * The array is copied; the events stay caller-owned.  Process-global, not
  * thread-safe: for single-threaded benchmarking only.
  * ------------------------------------------------------------------- */

@@ -29,11 +29,9 @@ inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 // Rows of the Sel list handled by one attention CTA (fixed per shape so the
 // workspace size does not depend on n_ctx).
 constexpr int kAttnRows = 256;
-constexpr int kMinChunk = 4096;  // smallest scan tile (U = 2)
 
 struct Derived {
   int G, P, n_w, w0, n_s, c0, c1, n_cand, keff, M;
-  int U, CH, first_chunk, nchunks;
   int R, nsplit, GT, nz, W;
 };
 
@@ -72,13 +70,6 @@ void derive(const a2ats_shape* s, const a2ats_params* p, int n_ctx, Derived* d) 
   d->n_cand = d->c1 - d->c0;
   d->keff = std::min(p->topk, d->n_cand);
   d->M = d->n_s + d->keff + d->n_w;
-  // scan tile: enough tiles to cover the machine a few times
-  const long long tokens = (long long)d->P * std::max(d->n_cand, 1);
-  const long long want = 4LL * sm_count();
-  d->U = (tokens / 16384 >= want) ? 8 : ((tokens / 8192 >= want) ? 4 : 2);
-  d->CH = 2048 * d->U;
-  d->first_chunk = d->c0 / d->CH;
-  d->nchunks = d->n_cand > 0 ? ((d->c1 + d->CH - 1) / d->CH - d->first_chunk) : 0;
   d->R = kAttnRows;
   d->nsplit = (d->M + d->R - 1) / d->R;
   d->GT = d->G >= 4 ? 4 : d->G;
@@ -87,16 +78,14 @@ void derive(const a2ats_shape* s, const a2ats_params* p, int n_ctx, Derived* d) 
 }
 
 struct DecodeWs {
-  size_t qrot, cs, agg, lut, cls, pinfo, status, tilectr, sel, part, actr, total;
+  size_t qrot, cs, agg, lut, sel, part, actr, total;
 };
 
 DecodeWs decode_layout(const a2ats_shape* s, const a2ats_params* p) {
   const int G = s->Hq / s->Hkv, P = s->B * s->Hkv;
-  const int W = (s->L + 15) / 16;
   const long long kmax = std::min<long long>(p->topk, s->n_max);
   const long long mmax = kmax + p->n_sink + p->window;
   const long long nsplit_max = (mmax + kAttnRows - 1) / kAttnRows;
-  const long long maxchunks = s->n_max / kMinChunk + 2;
   const int GT = G >= 4 ? 4 : G;
   DecodeWs w;
   size_t o = 0;
@@ -104,10 +93,6 @@ DecodeWs decode_layout(const a2ats_shape* s, const a2ats_params* p) {
   w.cs = o; o = align_up(o + (size_t)p->window * kHalf * 8);
   w.agg = o; o = align_up(o + (size_t)P * s->L * 4);
   w.lut = o; o = align_up(o + (size_t)s->B * s->Hq * s->L * 4);
-  w.cls = o; o = align_up(o + (size_t)P * W * 4);
-  w.pinfo = o; o = align_up(o + (size_t)P * 16);
-  w.status = o; o = align_up(o + (size_t)P * maxchunks * 8);
-  w.tilectr = o; o = align_up(o + 16);
   w.sel = o; o = align_up(o + (size_t)P * std::max<long long>(kmax, 1) * 4);
   w.part = o; o = align_up(o + (size_t)P * (G / GT) * GT * nsplit_max * 130 * 4);
   w.actr = o; o = align_up(o + (size_t)P * (G / GT) * 4);
@@ -138,7 +123,7 @@ void fill_rope(const a2ats_params* p, RopeTab* rt) {
 inline int cuda_status(cudaError_t e) { return e == cudaSuccess ? A2ATS_OK : A2ATS_ECUDA; }
 
 // Benchmark instrumentation (a2ats_set_stage_events).
-constexpr int kStageEvents = 6;
+constexpr int kStageEvents = 5;
 bool g_stage_on = false;
 cudaEvent_t g_stage[kStageEvents];
 inline void stage_mark(int i, cudaStream_t st) {
@@ -233,14 +218,14 @@ int a2ats_build_codes(const a2ats_shape* shape, const void* keys, int32_t t_begi
   a.Hkv = shape->Hkv;
   a.L = shape->L;
   a.n_max = shape->n_max;
-  const int ntiles = (shape->L + 127) / 128;
+  const int ntiles = (shape->L + encode_codeword_tile() - 1) / encode_codeword_tile();
   const int tmax = std::max(1, kEncVcap / shape->B);  // tokens per launch so that B*T <= vcap
   for (int t0 = t_begin; t0 < t_end; t0 += tmax) {
     a.t_begin = t0;
     a.T = std::min(tmax, t_end - t0);
     a.nvec = shape->B * a.T;
     if (a.nvec > kEncVcap) return A2ATS_EUNSUPPORTED;  // B > vcap
-    const int vt = (a.nvec + 63) / 64;
+    const int vt = (a.nvec + encode_key_tile() - 1) / encode_key_tile();
     // split the codeword range so the grid covers the machine about twice
     int lsplit = (2 * sm_count() + vt * shape->Hkv - 1) / (vt * shape->Hkv);
     lsplit = std::max(1, std::min(lsplit, ntiles));
@@ -300,6 +285,10 @@ int a2ats_decode_step(const a2ats_shape* shape, const a2ats_params* params, int3
   la.bridge = params->bridge;
   la.group_reduce = params->group_reduce;
   fill_rope(params, &la.rt);
+  for (int m = 0; m < kHalf; ++m) {  // bridge rotation R_b: fp64 angles, fp32 cos/sin (reading Q16)
+    const double ang = (double)params->bridge * la.rt.inv_freq[m];
+    la.bcs[m] = make_float2((float)std::cos(ang), (float)std::sin(ang));
+  }
   stage_mark(0, st);
   rc = cuda_status(launch_lut(la, st));
   if (rc) return rc;
@@ -311,10 +300,6 @@ int a2ats_decode_step(const a2ats_shape* shape, const a2ats_params* params, int3
     sa.agg = agg;
     sa.hist = hist;
     sa.codes = codes;
-    sa.cls = reinterpret_cast<uint32_t*>(base + Lw.cls);
-    sa.pinfo = reinterpret_cast<int32_t*>(base + Lw.pinfo);
-    sa.status = reinterpret_cast<unsigned long long*>(base + Lw.status);
-    sa.tile_counter = reinterpret_cast<unsigned int*>(base + Lw.tilectr);
     sa.sel = sel;
     sa.L = shape->L;
     sa.W = d.W;
@@ -325,19 +310,10 @@ int a2ats_decode_step(const a2ats_shape* shape, const a2ats_params* params, int3
     sa.n_s = d.n_s;
     sa.w0 = d.w0;
     sa.keff = d.keff;
-    sa.nchunks = d.nchunks;
-    sa.first_chunk = d.first_chunk;
-    sa.chunk_tokens = d.CH;
-    rc = cuda_status(launch_threshold(sa, d.P, st));
+    rc = cuda_status(launch_select(sa, d.P, st));
     if (rc) return rc;
-    stage_mark(2, st);
-    rc = cuda_status(launch_scan(sa, d.P, d.U, st));
-    if (rc) return rc;
-    stage_mark(3, st);
-  } else {
-    stage_mark(2, st);
-    stage_mark(3, st);
   }
+  stage_mark(2, st);
 
   // a5 + a6
   AttnArgs aa;
@@ -365,14 +341,14 @@ int a2ats_decode_step(const a2ats_shape* shape, const a2ats_params* params, int3
   aa.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)kD));
   rc = cuda_status(launch_attention(aa, d.P, d.GT, st));
   if (rc) return rc;
-  stage_mark(4, st);
+  stage_mark(3, st);
 
   if (scores_out) {
     rc = cuda_status(launch_scores(lut_full, codes, scores_out, shape->B, shape->Hq, shape->Hkv, d.G, shape->L,
                                    shape->n_max, n_ctx, st));
     if (rc) return rc;
   }
-  stage_mark(5, st);
+  stage_mark(4, st);
   return A2ATS_OK;
 }
 

@@ -4,55 +4,99 @@
 //   window rows        : u_j = (q R_{i-j}) . k_j = sum_m cos(r f_m) A_m + sin(r f_m) B_m,
 //                        A_m = q_m k_m + q_{m+64} k_{m+64}, B_m = q_m k_{m+64} - q_{m+64} k_m
 //                        (the relative identity of Eq. 3 applied to the query only).
-// One CTA = one (pair, row split, head subset); 4 warps; each warp takes groups
-// of 4 rows, lane = (row-in-group rsub, 16-element slice ds) so that q and the
-// output accumulator of GT heads live in registers.  K/V rows are gathered with
-// cp.async (16 B per lane-piece) into a warp-private ring of kStages stages; a
-// lane consumes exactly the pieces it copied, so the ring needs no barrier.
-// fp32 online softmax in base 2; partial (m, l, o) per split; the last CTA of a
-// (pair, head subset) combines the splits in fixed order (deterministic LSE).
+//
+// HBM-bound gather: every selected K/V row (2 x 256 B, scattered) is read once
+// and shared by the G query heads of the GQA group.  One CTA = (row split,
+// pair); 4 warps; a warp owns 16-row tiles.  Rows are gathered with cp.async
+// (16 B pieces, XOR-swizzled so ldmatrix is conflict-free) into a warp-private
+// ring of kStages tiles.  The per-tile contractions S = K_tile Q~^T (16 rows x
+// G heads x 128) and O^T += V_tile^T P (128 x G x 16) use mma.sync m16n8k16
+// (bf16 in, fp32 accumulate) only to keep the issue rate far below the memory
+// rate; q~ and P are split hi + lo into two bf16 halves so both products carry
+// fp32-level accuracy (~2^-16).  Window tiles compute their logits on FP32
+// CUDA cores (the rotation differs per row).  fp32 online softmax in base 2;
+// partial (m, l, o) per split; the last CTA of a pair combines the splits in
+// fixed order (deterministic LSE combine, a6).
 #include "internal.cuh"
+#include "umma.cuh"
 
 namespace a2ats {
 
 namespace {
-constexpr int kStages = 8;
 constexpr int kWarps = 4;
+constexpr int kStages = 3;
+constexpr int kTileBytes = 16 * 256;           // one K (or V) tile: 16 rows x 256 B
+constexpr int kStageBytes = 2 * kTileBytes;    // K + V
 
 struct SmemLayout {
-  int tok_off, ring_off, red_off, total;
+  int tok, ring, q, sS, red, total;
 };
-__host__ __device__ inline SmemLayout attn_smem(int R, int GT) {
+__host__ __device__ inline SmemLayout attn_smem(int R) {
   SmemLayout s;
-  s.tok_off = 0;
-  s.ring_off = ((R * 4) + 127) / 128 * 128;
-  s.red_off = s.ring_off + kWarps * kStages * 4 * 32 * 16;
-  s.total = s.red_off + kWarps * GT * 130 * 4;
+  s.tok = 0;
+  s.ring = ((R * 4) + 127) / 128 * 128;
+  s.q = s.ring + kWarps * kStages * kStageBytes;     // raw q (scaled) [8][128] fp32 for window tiles
+  s.sS = s.q + 8 * kD * 4;                           // window logits [4 warps][16 rows][8 heads]
+  s.red = s.ring;                                    // warp partials [4][8 heads][130], after the ring is dead
+  s.total = s.sS + kWarps * 16 * 8 * 4;
   return s;
 }
 
-template <int GT>
-__global__ __launch_bounds__(128, 2) void sparse_attention_kernel(AttnArgs a) {
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t movm_t(uint32_t x) {
+  uint32_t y;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t pack_bf16(uint16_t lo, uint16_t hi) { return lo | (uint32_t(hi) << 16); }
+__device__ __forceinline__ void split_pair(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+  uint16_t h0, l0, h1, l1;
+  umma::split_bf16(x0, h0, l0);
+  umma::split_bf16(x1, h1, l1);
+  hi = pack_bf16(h0, h1);
+  lo = pack_bf16(l0, l1);
+}
+// byte offset of (row, 16-B chunk) inside a 16 x 256 B tile, XOR swizzle on the chunk
+__device__ __forceinline__ uint32_t swz(int row, int chunk) { return row * 256 + ((chunk ^ (row & 7)) << 4); }
+
+__global__ __launch_bounds__(128, 2) void attn_mma_kernel(AttnArgs a) {
   extern __shared__ __align__(128) uint8_t smraw[];
-  const SmemLayout L = attn_smem(a.R, GT);
-  int32_t* s_tok = reinterpret_cast<int32_t*>(smraw + L.tok_off);
-  uint4* ring = reinterpret_cast<uint4*>(smraw + L.ring_off);
-  float* red = reinterpret_cast<float*>(smraw + L.red_off);
+  const SmemLayout SL = attn_smem(a.R);
+  int32_t* s_tok = reinterpret_cast<int32_t*>(smraw + SL.tok);
+  float* sQ = reinterpret_cast<float*>(smraw + SL.q);
+  float* red = reinterpret_cast<float*>(smraw + SL.red);
 
-  const int split = blockIdx.x, pair = blockIdx.y, gz = blockIdx.z;
-  const int nz = gridDim.z;
-  const int b = pair / a.Hkv, h = pair - (pair / a.Hkv) * a.Hkv;
-  const int hq0 = h * a.G + gz * GT;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, rsub = lane >> 3, ds = lane & 7;
+  const int split = blockIdx.x, pair = blockIdx.y;
+  const int b = pair / a.Hkv, h = pair - b * a.Hkv;
+  const int G = a.G;
+  const int hq0 = h * G;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g8 = lane >> 2, t4 = lane & 3;  // mma fragment coordinates
 
-  const int p0 = split * a.R;
-  const int p1 = min(p0 + a.R, a.M);
-  const int pw = a.n_s + a.keff;  // first window position in the Sel list
-  // segment A (bridge rows) and segment B (window rows) of this split
-  const int nA = max(0, min(p1, pw) - p0);
-  const int nB = (p1 - p0) - nA;
-  const int gA = (nA + 3) >> 2, gB = (nB + 3) >> 2;
-  const int ngroups = gA + gB;
+  const int p0 = split * a.R, p1 = min(p0 + a.R, a.M);
+  const int pw = a.n_s + a.keff;             // first window position in the Sel list
+  const int nA = max(0, min(p1, pw) - p0);   // bridge rows of this split
+  const int nB = (p1 - p0) - nA;             // window rows of this split
+  const int gA = (nA + 15) >> 4, gB = (nB + 15) >> 4, ngroups = gA + gB;
 
   for (int i = tid; i < p1 - p0; i += 128) {
     const int p = p0 + i;
@@ -62,210 +106,227 @@ __global__ __launch_bounds__(128, 2) void sparse_attention_kernel(AttnArgs a) {
     else t = a.w0 + (p - pw);
     s_tok[i] = t;
   }
+  if (nB > 0) {
+    for (int i = tid; i < 8 * kD; i += 128) {
+      const int g = i >> 7, e = i & (kD - 1);
+      sQ[i] = (g < G) ? bf_u16(a.q[((size_t)b * a.Hq + hq0 + g) * kD + e]) * a.scale_log2 : 0.f;
+    }
+  }
   __syncthreads();
 
-  const size_t rowbase = (size_t)pair * a.n_max;
-  const uint8_t* kbase = reinterpret_cast<const uint8_t*>(a.kc) + rowbase * 256;
-  const uint8_t* vbase = reinterpret_cast<const uint8_t*>(a.vc) + rowbase * 256;
-  uint4* wring = ring + warp * (kStages * 4 * 32);
+  const uint8_t* kbase = reinterpret_cast<const uint8_t*>(a.kc) + (size_t)pair * a.n_max * 256;
+  const uint8_t* vbase = reinterpret_cast<const uint8_t*>(a.vc) + (size_t)pair * a.n_max * 256;
+  uint8_t* wring = smraw + SL.ring + warp * (kStages * kStageBytes);
+  const uint32_t wring_s = smem_u32(wring);
 
-  auto local_row = [&](int g, int& li) -> bool {
+  // tile g of this warp's sequence -> (first local row, row count, is window)
+  auto tile_of = [&](int g, int& r0, int& nr) -> bool {
     if (g < gA) {
-      li = g * 4 + rsub;
-      return li < nA;
+      r0 = g * 16;
+      nr = min(16, nA - r0);
+      return false;
     }
-    li = nA + (g - gA) * 4 + rsub;
-    return li < nA + nB;
+    r0 = nA + (g - gA) * 16;
+    nr = min(16, nA + nB - r0);
+    return true;
   };
   auto issue = [&](int s) {
     const int g = s * kWarps + warp;
-    int li;
-    if (g < ngroups && local_row(g, li)) {
-      const size_t off = (size_t)s_tok[li] * 256 + ds * 16;
-      uint4* slot = wring + (s % kStages) * (4 * 32);
-      cp_async16(slot + 0 * 32 + lane, kbase + off);
-      cp_async16(slot + 1 * 32 + lane, kbase + off + 128);
-      cp_async16(slot + 2 * 32 + lane, vbase + off);
-      cp_async16(slot + 3 * 32 + lane, vbase + off + 128);
+    if (g < ngroups) {
+      int r0, nr;
+      tile_of(g, r0, nr);
+      uint8_t* st = wring + (s % kStages) * kStageBytes;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int idx = lane + 32 * i;  // 512 pieces: (kv, row, chunk)
+        const int kv = idx >> 8, row = (idx >> 4) & 15, chunk = idx & 15;
+        const int rr = row < nr ? row : nr - 1;  // pad rows re-read a valid row (finite data)
+        const size_t off = (size_t)s_tok[r0 + rr] * 256 + chunk * 16;
+        cp_async16(st + kv * kTileBytes + swz(row, chunk), (kv ? vbase : kbase) + off);
+      }
     }
     cp_async_commit();
   };
 
-  // q~ (bridge), pre-scaled by log2(e)/sqrt(d): lane holds elements ds*8+i and 64+ds*8+i.
-  float qr[GT][16];
+  // q~ (bridge) fragments as the mma B operand: head n = g8, d = 16kk + 2t4 + {0,1} (+8)
+  uint32_t qh[8][2], ql[8][2];
+  {
+    const bool valid = g8 < G;
+    const float* src = a.qrot + ((size_t)b * a.Hq + hq0 + (valid ? g8 : 0)) * kD;
 #pragma unroll
-  for (int g = 0; g < GT; ++g) {
-    const float* src = a.qrot + ((size_t)b * a.Hq + hq0 + g) * kD;
+    for (int kk = 0; kk < 8; ++kk)
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      qr[g][i] = src[ds * 8 + i] * a.scale_log2;
-      qr[g][8 + i] = src[kHalf + ds * 8 + i] * a.scale_log2;
-    }
+      for (int hf = 0; hf < 2; ++hf) {
+        const int d0 = kk * 16 + 2 * t4 + 8 * hf;
+        const float x0 = valid ? src[d0] * a.scale_log2 : 0.f;
+        const float x1 = valid ? src[d0 + 1] * a.scale_log2 : 0.f;
+        split_pair(x0, x1, qh[kk][hf], ql[kk][hf]);
+      }
   }
-  float o[GT][16], mrun[GT], lsum[GT];
+
+  float o[8][4];
 #pragma unroll
-  for (int g = 0; g < GT; ++g) {
-    mrun[g] = -INFINITY;
-    lsum[g] = 0.f;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) o[g][i] = 0.f;
-  }
+  for (int i = 0; i < 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float mrun0 = -INFINITY, mrun1 = -INFINITY, lrun0 = 0.f, lrun1 = 0.f;  // heads 2*t4, 2*t4+1
 
   const int nsteps = (ngroups > warp) ? (ngroups - warp + kWarps - 1) / kWarps : 0;
 #pragma unroll 1
   for (int s = 0; s < kStages - 1; ++s) issue(s);
-
-  bool in_window = false;
   const int icur = a.n_ctx - 1;
+  float* sS = reinterpret_cast<float*>(smraw + SL.sS) + warp * 128;
+
 #pragma unroll 1
   for (int s = 0; s < nsteps; ++s) {
     issue(s + kStages - 1);
     cp_async_wait<kStages - 1>();
+    __syncwarp();
     const int g = s * kWarps + warp;
-    int li;
-    const bool valid = local_row(g, li);
-    const bool win = g >= gA;
-    if (win && !in_window) {
-      // switch the query registers to the raw (pre-PE) query for the window band
-#pragma unroll
-      for (int gg = 0; gg < GT; ++gg) {
-        const uint16_t* src = a.q + ((size_t)b * a.Hq + hq0 + gg) * kD;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          qr[gg][i] = bf_u16(src[ds * 8 + i]) * a.scale_log2;
-          qr[gg][8 + i] = bf_u16(src[kHalf + ds * 8 + i]) * a.scale_log2;
-        }
-      }
-      in_window = true;
-    }
-    const uint4* slot = wring + (s % kStages) * (4 * 32);
-    const uint4 k0 = slot[0 * 32 + lane], k1 = slot[1 * 32 + lane];
-    float kf[16];
-    {
-      const uint32_t w[8] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w};
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        kf[2 * i] = bf_lo(w[i]);
-        kf[2 * i + 1] = bf_hi(w[i]);
-      }
-    }
-    float sc[GT];
+    int r0, nr;
+    const bool win = tile_of(g, r0, nr);
+    const uint32_t kst = wring_s + (s % kStages) * kStageBytes;
+    const uint32_t vst = kst + kTileBytes;
+    const int mi = lane >> 3, rr = lane & 7;
+
+    float sc[4];
     if (!win) {
+      sc[0] = sc[1] = sc[2] = sc[3] = 0.f;
 #pragma unroll
-      for (int gg = 0; gg < GT; ++gg) {
-        float x = 0.f;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) x = fmaf(qr[gg][i], kf[i], x);
-        sc[gg] = x;
+      for (int kk = 0; kk < 8; ++kk) {
+        uint32_t af[4];
+        ldsm_x4(kst + swz(rr + 8 * (mi & 1), 2 * kk + (mi >> 1)), af);
+        mma16816(sc, af, qh[kk][0], qh[kk][1]);
+        mma16816(sc, af, ql[kk][0], ql[kk][1]);
       }
     } else {
-      const int r = valid ? (icur - s_tok[li]) : 0;
-      const float4* csp = reinterpret_cast<const float4*>(a.cs + (size_t)r * kHalf + ds * 8);
-      float cv[8], sv[8];
+      // window rows: exact relative rotation per row on FP32 cores (lane = row, half of the pairs)
+      const int row = lane >> 1, hf = lane & 1;
+      const int rrow = row < nr ? row : nr - 1;
+      const int r = icur - s_tok[r0 + rrow];
+      const float4* csp = reinterpret_cast<const float4*>(a.cs + (size_t)r * kHalf + hf * 32);
+      const uint8_t* krow = wring + (s % kStages) * kStageBytes;
+      float acc[8];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float4 t = csp[i];
-        cv[2 * i] = t.x; sv[2 * i] = t.y; cv[2 * i + 1] = t.z; sv[2 * i + 1] = t.w;
-      }
+      for (int gg = 0; gg < 8; ++gg) acc[gg] = 0.f;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {  // 8 pairs per chunk: m = hf*32 + c*8 + i
+        const int ch1 = hf * 4 + c, ch2 = 8 + hf * 4 + c;
+        const uint4 k1 = *reinterpret_cast<const uint4*>(krow + swz(row, ch1));
+        const uint4 k2 = *reinterpret_cast<const uint4*>(krow + swz(row, ch2));
+        const uint32_t w1[4] = {k1.x, k1.y, k1.z, k1.w}, w2[4] = {k2.x, k2.y, k2.z, k2.w};
+        float cv[8], sv[8];
 #pragma unroll
-      for (int gg = 0; gg < GT; ++gg) {
-        float x = 0.f;
+        for (int i = 0; i < 4; ++i) {
+          const float4 t = csp[c * 4 + i];
+          cv[2 * i] = t.x; sv[2 * i] = t.y; cv[2 * i + 1] = t.z; sv[2 * i + 1] = t.w;
+        }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const float A = fmaf(qr[gg][i], kf[i], qr[gg][8 + i] * kf[8 + i]);
-          const float Bm = fmaf(qr[gg][i], kf[8 + i], -qr[gg][8 + i] * kf[i]);
-          x = fmaf(cv[i], A, fmaf(sv[i], Bm, x));
+          const float ka = (i & 1) ? bf_hi(w1[i >> 1]) : bf_lo(w1[i >> 1]);
+          const float kb = (i & 1) ? bf_hi(w2[i >> 1]) : bf_lo(w2[i >> 1]);
+          const int m = hf * 32 + c * 8 + i;
+#pragma unroll
+          for (int gg = 0; gg < 8; ++gg) {
+            if (gg < G) {
+              const float qa = sQ[gg * kD + m], qb = sQ[gg * kD + m + kHalf];
+              const float A = fmaf(qa, ka, qb * kb);
+              const float Bm = fmaf(qa, kb, -qb * ka);
+              acc[gg] = fmaf(cv[i], A, fmaf(sv[i], Bm, acc[gg]));
+            }
+          }
         }
-        sc[gg] = x;
-      }
-    }
-#pragma unroll
-    for (int gg = 0; gg < GT; ++gg) {
-      sc[gg] += __shfl_xor_sync(0xffffffffu, sc[gg], 1);
-      sc[gg] += __shfl_xor_sync(0xffffffffu, sc[gg], 2);
-      sc[gg] += __shfl_xor_sync(0xffffffffu, sc[gg], 4);
-    }
-    if (valid) {
-      const uint4 v0 = slot[2 * 32 + lane], v1 = slot[3 * 32 + lane];
-      const uint32_t w[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-      float vf[16];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        vf[2 * i] = bf_lo(w[i]);
-        vf[2 * i + 1] = bf_hi(w[i]);
       }
 #pragma unroll
-      for (int gg = 0; gg < GT; ++gg) {
-        if (sc[gg] > mrun[gg]) {
-          const float corr = exp2f(mrun[gg] - sc[gg]);
-          lsum[gg] *= corr;
+      for (int gg = 0; gg < 8; ++gg) acc[gg] += __shfl_xor_sync(0xffffffffu, acc[gg], 1);
+      if (hf == 0) {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) o[gg][i] *= corr;
-          mrun[gg] = sc[gg];
-        }
-        const float p = exp2f(sc[gg] - mrun[gg]);
-        lsum[gg] += p;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) o[gg][i] = fmaf(p, vf[i], o[gg][i]);
+        for (int gg = 0; gg < 8; ++gg) sS[row * 8 + gg] = acc[gg];
       }
+      __syncwarp();
+      sc[0] = sS[g8 * 8 + 2 * t4];
+      sc[1] = sS[g8 * 8 + 2 * t4 + 1];
+      sc[2] = sS[(g8 + 8) * 8 + 2 * t4];
+      sc[3] = sS[(g8 + 8) * 8 + 2 * t4 + 1];
     }
+    // mask pad rows of the tile
+    if (g8 >= nr) sc[0] = sc[1] = -INFINITY;
+    if (g8 + 8 >= nr) sc[2] = sc[3] = -INFINITY;
+
+    // online softmax per head (heads 2*t4, 2*t4+1); rows spread over lanes with equal t4
+    float mx0 = fmaxf(sc[0], sc[2]), mx1 = fmaxf(sc[1], sc[3]);
+#pragma unroll
+    for (int off = 4; off < 32; off <<= 1) {
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+    }
+    const float mn0 = fmaxf(mrun0, mx0), mn1 = fmaxf(mrun1, mx1);  // finite: every tile has >= 1 row
+    const float sc0 = exp2f(mrun0 - mn0), sc1 = exp2f(mrun1 - mn1);
+    mrun0 = mn0;
+    mrun1 = mn1;
+    const float p0 = exp2f(sc[0] - mn0), p1 = exp2f(sc[1] - mn1);
+    const float p2 = exp2f(sc[2] - mn0), p3 = exp2f(sc[3] - mn1);
+    lrun0 = lrun0 * sc0 + p0 + p2;
+    lrun1 = lrun1 * sc1 + p1 + p3;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      o[i][0] *= sc0;
+      o[i][1] *= sc1;
+      o[i][2] *= sc0;
+      o[i][3] *= sc1;
+    }
+    uint32_t ph0, pl0, ph1, pl1;
+    split_pair(p0, p1, ph0, pl0);  // rows g8:   heads (2t4, 2t4+1)
+    split_pair(p2, p3, ph1, pl1);  // rows g8+8
+    const uint32_t bh0 = movm_t(ph0), bh1 = movm_t(ph1), bl0 = movm_t(pl0), bl1 = movm_t(pl1);
+#pragma unroll
+    for (int ds = 0; ds < 8; ++ds) {
+      uint32_t af[4];
+      ldsm_x4_t(vst + swz(rr + 8 * (mi >> 1), 2 * ds + (mi & 1)), af);
+      mma16816(o[ds], af, bh0, bh1);
+      mma16816(o[ds], af, bl0, bl1);
+    }
+    __syncwarp();  // every lane done with this ring slot before it is refilled
   }
   cp_async_wait<0>();
+  __syncthreads();  // all warps out of the ring: it is reused for the warp partials
 
-  // combine the 4 row-slots (rsub) of the warp: lanes ds, ds+8, ds+16, ds+24
+  // per-warp partial: l summed over rows (lanes with equal t4)
 #pragma unroll
-  for (int gg = 0; gg < GT; ++gg) {
-#pragma unroll
-    for (int off = 8; off <= 16; off <<= 1) {
-      const float mo = __shfl_xor_sync(0xffffffffu, mrun[gg], off);
-      const float lo = __shfl_xor_sync(0xffffffffu, lsum[gg], off);
-      const float mn = fmaxf(mrun[gg], mo);
-      const float a1 = (mrun[gg] == -INFINITY) ? 0.f : exp2f(mrun[gg] - mn);
-      const float a2 = (mo == -INFINITY) ? 0.f : exp2f(mo - mn);
-      lsum[gg] = lsum[gg] * a1 + lo * a2;
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const float oo = __shfl_xor_sync(0xffffffffu, o[gg][i], off);
-        o[gg][i] = o[gg][i] * a1 + oo * a2;
-      }
-      mrun[gg] = mn;
-    }
+  for (int off = 4; off < 32; off <<= 1) {
+    lrun0 += __shfl_xor_sync(0xffffffffu, lrun0, off);
+    lrun1 += __shfl_xor_sync(0xffffffffu, lrun1, off);
   }
-  // element index of o[gg][i]: i < 8 -> ds*8+i, else 64 + ds*8 + (i-8)
-  if (rsub == 0) {
+  {
+    float* r0p = red + (warp * 8 + 2 * t4) * 130;
+    float* r1p = red + (warp * 8 + 2 * t4 + 1) * 130;
+    if (g8 == 0) {
+      r0p[0] = mrun0; r0p[1] = lrun0;
+      r1p[0] = mrun1; r1p[1] = lrun1;
+    }
 #pragma unroll
-    for (int gg = 0; gg < GT; ++gg) {
-      float* r = red + (warp * GT + gg) * 130;
-      if (ds == 0) {
-        r[0] = mrun[gg];
-        r[1] = lsum[gg];
-      }
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        r[2 + ds * 8 + i] = o[gg][i];
-        r[2 + kHalf + ds * 8 + i] = o[gg][8 + i];
-      }
+    for (int ds = 0; ds < 8; ++ds) {
+      r0p[2 + ds * 16 + g8] = o[ds][0];
+      r1p[2 + ds * 16 + g8] = o[ds][1];
+      r0p[2 + ds * 16 + g8 + 8] = o[ds][2];
+      r1p[2 + ds * 16 + g8 + 8] = o[ds][3];
     }
   }
   __syncthreads();
 
-  // combine the 4 warps: thread tid -> element e = tid (128 threads = d)
+  // combine the 4 warps: thread tid -> element e = tid
   const int e = tid;
-  const int pz = pair * nz + gz;
-  float* part = a.part + (size_t)pz * GT * a.nsplit * 130;
+  float* part = a.part + (size_t)pair * G * a.nsplit * 130;
   const bool single = (a.nsplit == 1);
-#pragma unroll
-  for (int gg = 0; gg < GT; ++gg) {
+  for (int gg = 0; gg < G; ++gg) {
     float M = -INFINITY;
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) M = fmaxf(M, red[(w * GT + gg) * 130]);
+    for (int w = 0; w < kWarps; ++w) M = fmaxf(M, red[(w * 8 + gg) * 130]);
     float acc = 0.f, den = 0.f;
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) {
-      const float mw = red[(w * GT + gg) * 130];
+      const float mw = red[(w * 8 + gg) * 130];
       const float sw = (mw == -INFINITY) ? 0.f : exp2f(mw - M);
-      acc = fmaf(red[(w * GT + gg) * 130 + 2 + e], sw, acc);
-      den = fmaf(red[(w * GT + gg) * 130 + 1], sw, den);
+      acc = fmaf(red[(w * 8 + gg) * 130 + 2 + e], sw, acc);
+      den = fmaf(red[(w * 8 + gg) * 130 + 1], sw, den);
     }
     if (single) {
       a.out[((size_t)b * a.Hq + hq0 + gg) * kD + e] = acc / den;
@@ -284,14 +345,13 @@ __global__ __launch_bounds__(128, 2) void sparse_attention_kernel(AttnArgs a) {
   __threadfence();
   __syncthreads();
   if (tid == 0) {
-    const unsigned prev = atomicAdd(a.counter + pz, 1u);
+    const unsigned prev = atomicAdd(a.counter + pair, 1u);
     s_last = (prev == (unsigned)(a.nsplit - 1));
   }
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-#pragma unroll 1
-  for (int gg = 0; gg < GT; ++gg) {
+  for (int gg = 0; gg < G; ++gg) {
     const float* src = part + (size_t)gg * a.nsplit * 130;
     float M = -INFINITY;
     for (int s = 0; s < a.nsplit; ++s) M = fmaxf(M, __ldcg(src + s * 130));
@@ -304,31 +364,21 @@ __global__ __launch_bounds__(128, 2) void sparse_attention_kernel(AttnArgs a) {
     }
     a.out[((size_t)b * a.Hq + hq0 + gg) * kD + e] = num / den;
   }
-  if (tid == 0) a.counter[pz] = 0u;  // leave the workspace in its zero state
-}
-
-template <int GT>
-cudaError_t launch_attn_t(const AttnArgs& a, int P, cudaStream_t st) {
-  const SmemLayout L = attn_smem(a.R, GT);
-  static int smem_set = -1;
-  if (smem_set < L.total) {
-    cudaError_t e = cudaFuncSetAttribute(sparse_attention_kernel<GT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         L.total);
-    if (e != cudaSuccess) return e;
-    smem_set = L.total;
-  }
-  dim3 grid(a.nsplit, P, a.G / GT);
-  sparse_attention_kernel<GT><<<grid, 128, L.total, st>>>(a);
-  return cudaGetLastError();
+  if (tid == 0) a.counter[pair] = 0u;  // leave the workspace in its zero state
 }
 }  // namespace
 
-cudaError_t launch_attention(const AttnArgs& a, int P, int GT, cudaStream_t st) {
-  switch (GT) {
-    case 1: return launch_attn_t<1>(a, P, st);
-    case 2: return launch_attn_t<2>(a, P, st);
-    default: return launch_attn_t<4>(a, P, st);
+cudaError_t launch_attention(const AttnArgs& a, int P, int /*GT*/, cudaStream_t st) {
+  const SmemLayout L = attn_smem(a.R);
+  static int smem_set = -1;
+  if (smem_set < L.total) {
+    cudaError_t e = cudaFuncSetAttribute(attn_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);
+    if (e != cudaSuccess) return e;
+    smem_set = L.total;
   }
+  dim3 grid(a.nsplit, P, 1);
+  attn_mma_kernel<<<grid, 128, L.total, st>>>(a);
+  return cudaGetLastError();
 }
 
 }  // namespace a2ats

@@ -73,18 +73,15 @@ struct LutArgs {
   float2* cs;                // [window, 64]   (cos, sin)(r f_m)
   int B, Hq, Hkv, G, L, window, bridge, group_reduce;
   RopeTab rt;
+  float2 bcs[kHalf];         // (cos, sin)(b f_m), from fp64 angles on the host
 };
 
 struct SelArgs {
   const float* agg;             // [P, L]
   const int32_t* hist;          // [P, L] or nullptr
   const uint16_t* codes;        // [P, n_max]
-  uint32_t* cls;                // [P, W] 2-bit class per code: 1 = above v*, 2 = at v*
-  int32_t* pinfo;               // [P, 4]: tie quota m, #above, -, -
-  unsigned long long* status;   // [P, nchunks] look-back words
-  unsigned int* tile_counter;   // 1 word
   int32_t* sel;                 // [P, keff]
-  int L, W, n_max, n_ctx, c0, c1, n_s, w0, keff, nchunks, first_chunk, chunk_tokens;
+  int L, W, n_max, n_ctx, c0, c1, n_s, w0, keff;
 };
 
 struct AttnArgs {
@@ -118,12 +115,13 @@ struct EncArgs {
 cudaError_t launch_lut(const LutArgs& a, cudaStream_t st);
 cudaError_t launch_scores(const float* lut_full, const uint16_t* codes, float* scores, int B, int Hq, int Hkv,
                           int G, int L, int n_max, int n_ctx, cudaStream_t st);
-cudaError_t launch_threshold(const SelArgs& a, int P, cudaStream_t st);
-cudaError_t launch_scan(const SelArgs& a, int P, int U, cudaStream_t st);
+cudaError_t launch_select(const SelArgs& a, int P, cudaStream_t st);
 cudaError_t launch_attention(const AttnArgs& a, int P, int GT, cudaStream_t st);
 cudaError_t launch_prepare(const uint16_t* codebook, const float* H, float* nrm, int Hkv, int L, cudaStream_t st);
 cudaError_t launch_encode(const EncArgs& a, cudaStream_t st);
 
 int sm_count();
+int encode_codeword_tile();
+int encode_key_tile();
 
 }  // namespace a2ats

@@ -1,35 +1,59 @@
 // a1 + a2: WRoPE query rotation and the score table LUT = q~ C^T, folded over
 // the GQA group into agg[b, h, l] (Eq. 12, Eq. 21).
 //
-// v1 kernel: fp32 FMA GEMM tile (128 codewords x 64 query vectors per CTA,
-// 4x8 register micro-tile per thread).  The bf16 codebook is converted exactly
-// to fp32 in shared memory; q~ is fp32 from fp64 angles, so every LUT entry is
-// an fp32-accumulated dot product (row-relative error ~1e-7 << 1e-4).
+// Per KV head this is a dense contraction (M = L codewords, N = B*G queries,
+// K = d) run on the 5th-gen tensor cores: one CTA computes a 128-codeword x
+// N-query tile with tcgen05.mma (kind::f16, fp32 accumulator in TMEM).
+// Precision: the codebook is exact in bf16; q~ (fp32, from fp64 angles) is
+// split q~ = hi + lo into two bf16 halves and both are accumulated into the
+// same TMEM accumulator (K = 2 x 128), so LUT entries carry ~2^-16 relative
+// error (row-relative error ~1e-6 << 1e-4, SURVEY §8c probe).
+// The epilogue reads the accumulator row of its codeword (tcgen05.ld), folds
+// the G query heads (max or sum, reading Q10) and writes agg coalesced.
 #include "internal.cuh"
+#include "umma.cuh"
 
 namespace a2ats {
 
 namespace {
-constexpr int kTC = 128;          // codewords per CTA
-constexpr int kTV = 64;           // query vectors per CTA
-constexpr int kCS = kTC + 4;      // C^T row stride (floats)
-constexpr int kVS = kTV + 4;      // Q^T row stride (floats)
-constexpr int kLutSmem = (kD * kCS + kD * kVS) * 4;
+constexpr int kTC = 128;  // codewords per CTA (MMA M)
 
-__global__ __launch_bounds__(256) void lut_fma_kernel(LutArgs a) {
-  extern __shared__ __align__(16) float smem[];
-  float* Ct = smem;               // [128 d][kCS]  codeword tile, transposed
-  float* Vt = smem + kD * kCS;    // [128 d][kVS]  rotated queries, transposed
-  __shared__ float2 bcs[kHalf];   // (cos, sin)(b f_m)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
 
-  const int tid = threadIdx.x;
+template <uint32_t kTmemCols, int G>
+__global__ __launch_bounds__(128, 1) void lut_umma_kernel(LutArgs a, int NV) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sA = smem;                // [16 chunks][128 codes][16 B]
+  uint8_t* sB = smem + kTC * kD * 2; // [32 chunks][NV vectors][16 B]: chunks 0..15 hi, 16..31 lo
+  __shared__ uint64_t mbar;
+  __shared__ uint32_t tslot;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int h = blockIdx.z;
   const int code0 = blockIdx.x * kTC;
-  const int vec0 = blockIdx.y * kTV;
-  const int nvec = a.B * a.G;
+  const int vec0 = blockIdx.y * NV;
+  const int nvec = a.B * G;
+  const float2* bcs = a.bcs;
 
-  // Window relative-rotation table cs[r][m] = (cos, sin)(r f_m), r < w, from fp64
-  // angles; spread over the first CTAs (row r by linear CTA r).
+  if (warp == 0) umma::tmem_alloc<kTmemCols>(&tslot);
+  if (tid == 0) {
+    umma::mbar_init(&mbar, 1);
+    umma::mbar_fence_init();
+  }
+
+  // codeword tile -> canonical K-major layout (cp.async, 16 B per piece)
+  for (int idx = tid; idx < kTC * 16; idx += 128) {
+    const int r = idx >> 4, c = idx & 15;
+    uint8_t* dst = sA + (c * kTC + r) * 16;
+    if (code0 + r < a.L) cp_async16(dst, a.codebook + ((size_t)h * a.L + code0 + r) * kD + c * 8);
+    else *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
+  }
+  cp_async_commit();
+
+  // window relative-rotation table cs[r][m] = (cos, sin)(r f_m) from fp64 angles,
+  // one row per CTA (linear CTA index r < w)
   const int lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
   const int nlin = gridDim.x * gridDim.y * gridDim.z;
   for (int r = lin; r < a.window; r += nlin) {
@@ -39,108 +63,115 @@ __global__ __launch_bounds__(256) void lut_fma_kernel(LutArgs a) {
       a.cs[r * kHalf + tid] = make_float2((float)c, (float)s);
     }
   }
-  if (tid < kHalf) {
-    double s, c;
-    sincos((double)a.bridge * a.rt.inv_freq[tid], &s, &c);
-    bcs[tid] = make_float2((float)c, (float)s);
-  }
-
-  // Codeword tile -> C^T (exact bf16 -> fp32).
-  for (int idx = tid; idx < kTC * 16; idx += 256) {
-    const int c = idx & (kTC - 1), dc = idx >> 7;
-    const int code = code0 + c;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (code < a.L) v = ld_nc_u4(a.codebook + ((size_t)h * a.L + code) * kD + dc * 8);
-    float* col = Ct + (dc * 8) * kCS + c;
-    col[0 * kCS] = bf_lo(v.x); col[1 * kCS] = bf_hi(v.x);
-    col[2 * kCS] = bf_lo(v.y); col[3 * kCS] = bf_hi(v.y);
-    col[4 * kCS] = bf_lo(v.z); col[5 * kCS] = bf_hi(v.z);
-    col[6 * kCS] = bf_lo(v.w); col[7 * kCS] = bf_hi(v.w);
-  }
-  __syncthreads();  // bcs visible
-
-  // Query tile: q~ = q R_b (Eq. 12), half-split pairs (m, m+64).
-  for (int idx = tid; idx < kTV * kHalf; idx += 256) {
-    const int m = idx & (kHalf - 1), vv = idx >> 6;
-    const int n = vec0 + vv;
-    float x1 = 0.f, x2 = 0.f;
-    size_t qoff = 0;
-    if (n < nvec) {
-      const int b = n / a.G, g = n - (n / a.G) * a.G;
-      qoff = ((size_t)b * a.Hq + h * a.G + g) * kD;
-      x1 = bf_u16(a.q[qoff + m]);
-      x2 = bf_u16(a.q[qoff + m + kHalf]);
-    }
-    const float2 cs = bcs[m];
-    const float y1 = fmaf(x1, cs.x, -x2 * cs.y);
-    const float y2 = fmaf(x2, cs.x, x1 * cs.y);
-    Vt[m * kVS + vv] = y1;
-    Vt[(m + kHalf) * kVS + vv] = y2;
-    if (blockIdx.x == 0 && n < nvec) {
-      a.qrot[qoff + m] = y1;
-      a.qrot[qoff + m + kHalf] = y2;
-    }
-  }
-  __syncthreads();
-
-  const int tx = tid & 31, ty = tid >> 5;
-  float acc[8][4];
+  // query tile: q~ = q R_b (Eq. 12), half-split pairs (m, m+64); hi/lo bf16 split
+  for (int idx = tid; idx < NV * 8; idx += 128) {
+    const int n = idx % NV, c = idx / NV;  // chunk c pairs with chunk c+8 (elements m, m+64)
+    const int vn = vec0 + n;
+    uint16_t h1[8], l1[8], h2[8], l2[8];
+    if (vn < nvec) {
+      const int b = vn / G, g = vn - b * G;
+      const size_t qoff = ((size_t)b * a.Hq + h * G + g) * kD;
+      const uint4 x1v = ld_nc_u4(a.q + qoff + c * 8);
+      const uint4 x2v = ld_nc_u4(a.q + qoff + kHalf + c * 8);
+      const uint32_t w1[4] = {x1v.x, x1v.y, x1v.z, x1v.w}, w2[4] = {x2v.x, x2v.y, x2v.z, x2v.w};
+      float y1[8], y2[8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
-
-#pragma unroll 4
-  for (int d = 0; d < kD; ++d) {
-    const float4 c4 = *reinterpret_cast<const float4*>(Ct + d * kCS + tx * 4);
-    const float4 v0 = *reinterpret_cast<const float4*>(Vt + d * kVS + ty * 8);
-    const float4 v1 = *reinterpret_cast<const float4*>(Vt + d * kVS + ty * 8 + 4);
-    const float cc[4] = {c4.x, c4.y, c4.z, c4.w};
-    const float vv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(vv[i], cc[j], acc[i][j]);
-  }
-
-  const int cbase = code0 + tx * 4;
-  if (a.lut_full) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int n = vec0 + ty * 8 + i;
-      if (n >= nvec) break;
-      const int b = n / a.G, g = n - (n / a.G) * a.G;
-      float* dst = a.lut_full + ((size_t)b * a.Hq + h * a.G + g) * a.L;
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (cbase + j < a.L) dst[cbase + j] = acc[i][j];
-    }
-  }
-  // Fold the G query heads of each batch element (G divides 8; vec0 % G == 0).
-  const int nb = 8 / a.G;
-  for (int bb = 0; bb < nb; ++bb) {
-    const int n0 = vec0 + ty * 8 + bb * a.G;
-    if (n0 >= nvec) break;
-    const int b = n0 / a.G;
-    float r[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      float x = acc[bb * a.G][j];
-      for (int g = 1; g < a.G; ++g) {
-        const float y = acc[bb * a.G + g][j];
-        x = (a.group_reduce == A2ATS_GROUP_SUM) ? x + y : fmaxf(x, y);
+      for (int i = 0; i < 8; ++i) {
+        const float x1 = (i & 1) ? bf_hi(w1[i >> 1]) : bf_lo(w1[i >> 1]);
+        const float x2 = (i & 1) ? bf_hi(w2[i >> 1]) : bf_lo(w2[i >> 1]);
+        const float2 cs = bcs[c * 8 + i];
+        y1[i] = fmaf(x1, cs.x, -x2 * cs.y);
+        y2[i] = fmaf(x2, cs.x, x1 * cs.y);
+        umma::split_bf16(y1[i], h1[i], l1[i]);
+        umma::split_bf16(y2[i], h2[i], l2[i]);
       }
-      r[j] = x;
-    }
-    float* dst = a.agg + ((size_t)b * a.Hkv + h) * a.L;
-    if (cbase + 3 < a.L && (a.L & 3) == 0) {
-      *reinterpret_cast<float4*>(dst + cbase) = make_float4(r[0], r[1], r[2], r[3]);
+      if (blockIdx.x == 0) {
+        float4* q1 = reinterpret_cast<float4*>(a.qrot + qoff + c * 8);
+        float4* q2 = reinterpret_cast<float4*>(a.qrot + qoff + kHalf + c * 8);
+        q1[0] = make_float4(y1[0], y1[1], y1[2], y1[3]);
+        q1[1] = make_float4(y1[4], y1[5], y1[6], y1[7]);
+        q2[0] = make_float4(y2[0], y2[1], y2[2], y2[3]);
+        q2[1] = make_float4(y2[4], y2[5], y2[6], y2[7]);
+      }
     } else {
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (cbase + j < a.L) dst[cbase + j] = r[j];
+      for (int i = 0; i < 8; ++i) h1[i] = l1[i] = h2[i] = l2[i] = 0;
+    }
+    auto pack = [](const uint16_t* v) {
+      return make_uint4(v[0] | (uint32_t(v[1]) << 16), v[2] | (uint32_t(v[3]) << 16), v[4] | (uint32_t(v[5]) << 16),
+                        v[6] | (uint32_t(v[7]) << 16));
+    };
+    *reinterpret_cast<uint4*>(sB + ((c)*NV + n) * 16) = pack(h1);
+    *reinterpret_cast<uint4*>(sB + ((c + 8) * NV + n) * 16) = pack(h2);
+    *reinterpret_cast<uint4*>(sB + ((16 + c) * NV + n) * 16) = pack(l1);
+    *reinterpret_cast<uint4*>(sB + ((24 + c) * NV + n) * 16) = pack(l2);
+  }
+  cp_async_wait<0>();
+  umma::fence_proxy_async();
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  const uint32_t tmem = tslot;
+
+  if (tid == 0) {
+    const uint32_t aBase = smem_u32(sA), bBase = smem_u32(sB);
+    const uint32_t idesc = umma::idesc_bf16(kTC, NV);
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {  // K = 256: 8 steps against q~_hi, 8 against q~_lo, same A
+      const uint64_t ad = umma::sdesc(aBase + (2 * (s & 7)) * (kTC * 16), kTC * 16, 128);
+      const uint64_t bd = umma::sdesc(bBase + (2 * s) * (NV * 16), NV * 16, 128);
+      umma::mma_bf16(tmem, ad, bd, idesc, s > 0 ? 1u : 0u);
+    }
+    umma::commit(&mbar);
+  }
+  __syncwarp();
+  umma::mbar_wait(&mbar, 0);
+  umma::fence_after();
+
+  // epilogue: thread <-> codeword row code0 + 32*warp + lane
+  const int code = code0 + warp * 32 + lane;
+  const int nv_here = min(NV, nvec - vec0);
+  for (int cb = 0; cb < nv_here; cb += 64) {
+    uint32_t r[4][16];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)  // up to 4 TMEM loads in flight, then one wait
+      if (cb + 16 * q < nv_here) umma::tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + cb + 16 * q, r[q]);
+    umma::tmem_wait_ld();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+    const int col0 = cb + 16 * q;
+    if (col0 >= nv_here) break;
+    float x[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) x[i] = __uint_as_float(r[q][i]);
+    if (code < a.L) {
+      if (a.lut_full) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int vn = vec0 + col0 + i;
+          if (vn < nvec) {
+            const int b = vn / G, g = vn - b * G;
+            a.lut_full[((size_t)b * a.Hq + h * G + g) * a.L + code] = x[i];
+          }
+        }
+      }
+      const bool sum = (a.group_reduce == A2ATS_GROUP_SUM);
+#pragma unroll
+      for (int bb = 0; bb < 16 / G; ++bb) {  // G divides 16, vec0 + col0 is a multiple of G
+        const int n0 = vec0 + col0 + bb * G;
+        if (n0 < nvec) {
+          float v = x[bb * G];
+#pragma unroll
+          for (int g = 1; g < G; ++g) v = sum ? v + x[bb * G + g] : fmaxf(v, x[bb * G + g]);
+          a.agg[((size_t)(n0 / G) * a.Hkv + h) * a.L + code] = v;
+        }
+      }
+    }
     }
   }
+  umma::fence_before();
+  __syncthreads();
+  if (warp == 0) umma::tmem_dealloc<kTmemCols>(tmem);
 }
 
 // Debug output: scores[b, hq, t] = LUT[b, hq, codes[b, h, t]] for t < n_ctx (Eq. 21).
@@ -153,18 +184,40 @@ __global__ void scores_kernel(const float* __restrict__ lut_full, const uint16_t
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n_ctx; t += gridDim.x * blockDim.x)
     scores[(size_t)bq * n_ctx + t] = lrow[crow[t]];
 }
+
+template <uint32_t kCols, int G>
+cudaError_t launch_lut_t(const LutArgs& a, int NV, cudaStream_t st) {
+  const int smem = kTC * kD * 2 + NV * 2 * kD * 2;
+  static int smem_set = -1;
+  if (smem_set < smem) {
+    cudaError_t e =
+        cudaFuncSetAttribute(lut_umma_kernel<kCols, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    smem_set = smem;
+  }
+  dim3 grid((a.L + kTC - 1) / kTC, (a.B * G + NV - 1) / NV, a.Hkv);
+  lut_umma_kernel<kCols, G><<<grid, 128, smem, st>>>(a, NV);
+  return cudaGetLastError();
+}
+
+template <int G>
+cudaError_t launch_lut_g(const LutArgs& a, cudaStream_t st) {
+  const int nvec = a.B * G;
+  const int NV = nvec >= 256 ? 256 : ((nvec + 15) / 16) * 16;  // MMA N: multiple of 16, <= 256
+  if (NV <= 32) return launch_lut_t<32, G>(a, NV, st);
+  if (NV <= 64) return launch_lut_t<64, G>(a, NV, st);
+  if (NV <= 128) return launch_lut_t<128, G>(a, NV, st);
+  return launch_lut_t<256, G>(a, NV, st);
+}
 }  // namespace
 
 cudaError_t launch_lut(const LutArgs& a, cudaStream_t st) {
-  static bool attr_done = false;  // per process; single-device use is the norm
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(lut_fma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kLutSmem);
-    if (e != cudaSuccess) return e;
-    attr_done = true;
+  switch (a.G) {
+    case 1: return launch_lut_g<1>(a, st);
+    case 2: return launch_lut_g<2>(a, st);
+    case 4: return launch_lut_g<4>(a, st);
+    default: return launch_lut_g<8>(a, st);
   }
-  dim3 grid((a.L + kTC - 1) / kTC, (a.B * a.G + kTV - 1) / kTV, a.Hkv);
-  lut_fma_kernel<<<grid, 256, kLutSmem, st>>>(a);
-  return cudaGetLastError();
 }
 
 cudaError_t launch_scores(const float* lut_full, const uint16_t* codes, float* scores, int B, int Hq, int Hkv,

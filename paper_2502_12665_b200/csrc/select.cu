@@ -2,20 +2,23 @@
 //
 // Scores take only L distinct values per (b, KV head) pair (u^_t = LUT[s_t],
 // Eq. 21), so the K-th largest score is found by a count-weighted
-// radix select over the L codewords, not over the N tokens:
+// radix select over the L codewords, not over the N tokens.  One CTA owns one
+// pair (fused kernel, no intermediate in HBM):
 //
-//   threshold kernel (one CTA per pair): candidate histogram over codewords
-//     (the caller-maintained hist minus the sink/window codes, or one pass over
-//     the codes), radix select of the K-th largest agg level v* weighted by
-//     counts, tie quota m = K - #{agg > v*}; emits a 2-bit class per codeword
-//     (1: agg > v*, 2: agg == v*, 0: below).
-//   scan kernel (persistent, one tile = 2048*U tokens of one pair): streams the
-//     uint16 codes once with 128-bit loads, classifies every token through a
-//     32x-replicated class table in shared memory (lane-private bank, no
-//     conflicts), and writes the selected token indices in ascending order with
-//     an ordered compaction across tiles (decoupled look-back).  A token with
-//     agg == v* is kept iff fewer than m such tokens precede it: the
-//     lowest-index tie-break of reading Q12.
+//  1. issue the 128-bit loads of the first code chunk (registers), so the DRAM
+//     latency overlaps steps 2-4;
+//  2. candidate histogram over codewords: the caller-maintained hist minus the
+//     sink/window codes (one pass over the code stream in total), or, without
+//     hist, an extra pass over the codes;
+//  3. count-weighted MSB-first radix select of the K-th largest agg level v*
+//     (warp-aggregated shared atomics: float keys share their top bits);
+//     tie quota m = K - #{agg > v*};
+//  4. 2-bit class per codeword (1: agg > v*, 2: agg == v*), replicated 32x in
+//     shared memory so lane l reads bank l (conflict-free gather by code);
+//  5. stream the codes chunk by chunk (next chunk prefetched into registers),
+//     classify each token, and write the selected indices in ascending order
+//     (block scan + running prefix).  A token with agg == v* is kept iff fewer
+//     than m such tokens precede it: the lowest-index tie-break of reading Q12.
 #include "internal.cuh"
 
 namespace a2ats {
@@ -31,61 +34,106 @@ __device__ __forceinline__ uint32_t spread16(uint32_t v) {
   return v;
 }
 
-constexpr int kThrThreads = 256;
 
-__global__ __launch_bounds__(kThrThreads) void select_threshold_kernel(SelArgs a) {
+template <int NT, int VPT>
+__global__ __launch_bounds__(NT, 1) void select_fused_kernel(SelArgs a) {
+  constexpr int NW = NT / 32;
+  constexpr int CH = NT * VPT * 8;  // tokens per chunk
   extern __shared__ __align__(16) uint32_t sm[];
-  int* cnt = reinterpret_cast<int*>(sm);  // [L] candidate count per codeword
+  int* cnt = reinterpret_cast<int*>(sm);  // [L]
   uint32_t* key = sm + a.L;               // [L] ~ordered(agg): ascending key = descending agg
+  uint32_t* tbl = sm;                     // [W*32] aliases cnt/key after step 4
+  __shared__ uint32_t cls[1024];          // compact 2-bit classes (W <= 1024)
   __shared__ int bins[256];
+  __shared__ int whist[NW * 256];         // per-warp digit histograms
+  __shared__ uint32_t wsum[VPT][NW];
   __shared__ int s_digit, s_kk;
+  __shared__ uint32_t s_run[2];
+  __shared__ uint32_t s_and, s_or;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int pair = blockIdx.x;
-  const float* aggp = a.agg + (size_t)pair * a.L;
   const uint16_t* cp = a.codes + (size_t)pair * a.n_max;
+  const int c0 = a.c0, c1 = a.c1;
+  const int first = (c0 >> 3) << 3;                   // 8-aligned start of the candidate range
+  const int nchunk = (c1 - first + CH - 1) / CH;
 
-  for (int i = tid; i < a.nchunks; i += kThrThreads) a.status[(size_t)pair * a.nchunks + i] = 0ull;
-  if (pair == 0 && tid == 0) *a.tile_counter = 0u;
+  // 1. prefetch chunk 0
+  uint4 v[VPT];
+#pragma unroll
+  for (int j = 0; j < VPT; ++j) {
+    const int t0 = first + (j * NT + tid) * 8;
+    v[j] = (t0 < c1) ? ld_stream_u4(cp + t0) : make_uint4(0, 0, 0, 0);
+  }
 
-  for (int l = tid; l < a.L; l += kThrThreads) {
+  // 2. candidate histogram
+  if (tid == 0) {
+    s_and = 0xffffffffu;
+    s_or = 0u;
+  }
+  const float* aggp = a.agg + (size_t)pair * a.L;
+  for (int l = tid; l < a.L; l += NT) {
     cnt[l] = a.hist ? a.hist[(size_t)pair * a.L + l] : 0;
     key[l] = ~ordered_key(aggp[l]);
   }
   __syncthreads();
   if (a.hist) {
-    // remove the sinks [0, n_s) and the window [w0, n_ctx): they are not candidates
     const int nrem = a.n_s + (a.n_ctx - a.w0);
-    for (int i = tid; i < nrem; i += kThrThreads) {
+    for (int i = tid; i < nrem; i += NT) {
       const int t = i < a.n_s ? i : a.w0 + (i - a.n_s);
       atomicSub(&cnt[cp[t]], 1);
     }
   } else {
-    // one pass over the candidate codes [c0, c1)
-    const int v0 = a.c0 >> 3, v1 = (a.c1 + 7) >> 3;
-    for (int vi = v0 + tid; vi < v1; vi += kThrThreads) {
-      const uint4 v = ld_stream_u4(cp + (size_t)vi * 8);
-      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    for (int vi = (first >> 3) + tid; vi < ((c1 + 7) >> 3); vi += NT) {
+      const uint4 x = ld_nc_u4(cp + (size_t)vi * 8);
+      const uint32_t w[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         const int t = vi * 8 + e;
-        if (t >= a.c0 && t < a.c1) atomicAdd(&cnt[(w[e >> 1] >> ((e & 1) * 16)) & 0xffffu], 1);
+        if (t >= c0 && t < c1) atomicAdd(&cnt[(w[e >> 1] >> ((e & 1) * 16)) & 0xffffu], 1);
       }
     }
   }
   __syncthreads();
 
-  // Count-weighted MSB-first radix select of the keff-th smallest key.
-  uint32_t prefix = 0, mask = 0;
+  // 3. radix select of the keff-th smallest key, weighted by counts.  Bits common to
+  //    every candidate key are skipped; digits are counted in per-warp histograms.
+  uint32_t kand = 0xffffffffu, kor = 0u;
+  for (int l = tid; l < a.L; l += NT) {
+    if (cnt[l] > 0) {
+      kand &= key[l];
+      kor |= key[l];
+    }
+  }
+  kand = __reduce_and_sync(0xffffffffu, kand);
+  kor = __reduce_or_sync(0xffffffffu, kor);
+  if (lane == 0) {
+    atomicAnd(&s_and, kand);
+    atomicOr(&s_or, kor);
+  }
+  __syncthreads();
+  const uint32_t diff = s_and ^ s_or;            // bits where candidate keys differ
+  const int top = diff ? 31 - __clz(diff) : 0;   // highest differing bit
+  const int npass = diff ? (top / 8) + 1 : 0;    // passes over digits [8*(npass-1), ...]
+  uint32_t prefix = diff ? (s_and & ~((top >= 31) ? 0xffffffffu : ((2u << top) - 1u))) : s_and;
+  uint32_t mask = diff ? ~((top >= 31) ? 0xffffffffu : ((2u << top) - 1u)) : 0xffffffffu;
   int kk = a.keff;
-  for (int pass = 0; pass < 4; ++pass) {
-    const int shift = 24 - 8 * pass;
-    bins[tid] = 0;
+  for (int pass = npass - 1; pass >= 0; --pass) {
+    const int shift = 8 * pass;
+    for (int i = tid; i < NW * 256; i += NT) whist[i] = 0;
     __syncthreads();
-    for (int l = tid; l < a.L; l += kThrThreads) {
+    int* wh = whist + warp * 256;
+    for (int l = tid; l < a.L; l += NT) {
       const int c = cnt[l];
       const uint32_t k = key[l];
-      if (c > 0 && (k & mask) == prefix) atomicAdd(&bins[(k >> shift) & 255u], c);
+      if (c > 0 && (k & mask) == prefix) atomicAdd(wh + ((k >> shift) & 255u), c);
+    }
+    __syncthreads();
+    for (int i = tid; i < 256; i += NT) {
+      int s = 0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) s += whist[w * 256 + i];
+      bins[i] = s;
     }
     __syncthreads();
     if (warp == 0) {
@@ -117,16 +165,16 @@ __global__ __launch_bounds__(kThrThreads) void select_threshold_kernel(SelArgs a
       }
     }
     __syncthreads();
-    prefix |= (uint32_t)s_digit << shift;
+    // digit bits above `top` are part of the common prefix already; OR-ing is idempotent
+    prefix = (prefix & ~(0xffu << shift)) | ((uint32_t)s_digit << shift);
     mask |= 0xffu << shift;
     kk = s_kk;
-    __syncthreads();
   }
-  const uint32_t kstar = prefix;  // key of v*; kk = tie quota m (1 <= m)
+  const uint32_t kstar = prefix;  // key of v*;  kk = tie quota m >= 1
+  const uint32_t m = (uint32_t)kk;
 
-  // 2-bit classes, 16 codewords per word: 1 = strictly above v*, 2 = equal.
-  const int ngroups = (a.L + 31) / 32;
-  for (int gi = warp; gi < ngroups; gi += kThrThreads / 32) {
+  // 4. classes: compact words, then 32x replication over the (dead) cnt/key arrays
+  for (int gi = warp; gi < (a.L + 31) / 32; gi += NW) {
     const int l = gi * 32 + lane;
     uint32_t c = 0;
     if (l < a.L) {
@@ -135,58 +183,28 @@ __global__ __launch_bounds__(kThrThreads) void select_threshold_kernel(SelArgs a
     }
     const uint32_t gtm = __ballot_sync(0xffffffffu, c == 1u);
     const uint32_t eqm = __ballot_sync(0xffffffffu, c == 2u);
-    if (lane < 2) {
-      const int wi = gi * 2 + lane;
-      if (wi < a.W) {
-        const uint32_t g16 = lane ? (gtm >> 16) : gtm, e16 = lane ? (eqm >> 16) : eqm;
-        a.cls[(size_t)pair * a.W + wi] = spread16(g16) | (spread16(e16) << 1);
-      }
+    if (lane < 2 && gi * 2 + lane < a.W) {
+      const uint32_t g16 = lane ? (gtm >> 16) : gtm, e16 = lane ? (eqm >> 16) : eqm;
+      cls[gi * 2 + lane] = spread16(g16) | (spread16(e16) << 1);
     }
   }
   if (tid == 0) {
-    a.pinfo[pair * 4 + 0] = kk;
-    a.pinfo[pair * 4 + 1] = a.keff - kk;
+    s_run[0] = 0;
+    s_run[1] = 0;
   }
-}
+  __syncthreads();
+  for (int i = tid; i < a.W * 32; i += NT) tbl[i] = cls[i >> 5];
+  __syncthreads();
 
-template <int U>
-__global__ __launch_bounds__(256) void select_scan_kernel(SelArgs a, int ntiles) {
-  extern __shared__ __align__(16) uint32_t tbl[];  // [W * 32]: word w replicated at w*32 + lane
-  __shared__ uint32_t wsum[U][8];
-  __shared__ uint32_t s_pgt, s_peq;
-  __shared__ int s_tile;
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int CH = 2048 * U;
-  int cur_pair = -1;
-
-  for (;;) {
-    if (tid == 0) s_tile = (int)atomicAdd(a.tile_counter, 1u);
-    __syncthreads();
-    const int tile = s_tile;
-    if (tile >= ntiles) break;
-    const int pair = tile / a.nchunks, chunk = tile - (tile / a.nchunks) * a.nchunks;
-    if (pair != cur_pair) {
-      const uint32_t* src = a.cls + (size_t)pair * a.W;
-      for (int i = tid; i < a.W * 32; i += 256) tbl[i] = src[i >> 5];
-      cur_pair = pair;
-    }
-    const int cb = (a.first_chunk + chunk) * CH;  // chunk begin (absolute token, 8-aligned)
-    const int lo = max(a.c0, cb), hi = min(a.c1, cb + CH);
-    const uint16_t* cp = a.codes + (size_t)pair * a.n_max + cb;
-
-    uint4 v[U];
+  // 5. classify + ordered compaction, chunk by chunk
+  int32_t* selp = a.sel + (size_t)pair * a.keff;
+  const uint32_t keff = (uint32_t)a.keff;
+  for (int ch = 0; ch < nchunk; ++ch) {
+    const int cb = first + ch * CH;
+    uint32_t packed[VPT], pk[VPT], incl[VPT];
 #pragma unroll
-    for (int j = 0; j < U; ++j) {
-      const int t0 = cb + (j * 256 + tid) * 8;
-      v[j] = (t0 < hi && t0 + 8 > lo) ? ld_stream_u4(cp + (j * 256 + tid) * 8) : make_uint4(0, 0, 0, 0);
-    }
-    __syncthreads();  // table for this pair visible
-
-    uint32_t packed[U], pk[U], incl[U];
-#pragma unroll
-    for (int j = 0; j < U; ++j) {
-      const int t0 = cb + (j * 256 + tid) * 8;
+    for (int j = 0; j < VPT; ++j) {
+      const int t0 = cb + (j * NT + tid) * 8;
       const uint32_t w[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
       uint32_t p = 0;
 #pragma unroll
@@ -195,15 +213,26 @@ __global__ __launch_bounds__(256) void select_scan_kernel(SelArgs a, int ntiles)
         const uint32_t word = tbl[((code >> 4) << 5) + lane];
         p |= ((word >> ((code & 15u) * 2u)) & 3u) << (2 * e);
       }
-      if (t0 < lo || t0 + 8 > hi) {
-        uint32_t m = 0;
+      if (t0 < c0 || t0 + 8 > c1) {
+        uint32_t mk = 0;
 #pragma unroll
         for (int e = 0; e < 8; ++e)
-          if (t0 + e >= lo && t0 + e < hi) m |= 3u << (2 * e);
-        p &= m;
+          if (t0 + e >= c0 && t0 + e < c1) mk |= 3u << (2 * e);
+        p &= mk;
       }
       packed[j] = p;
-      pk[j] = (uint32_t)__popc(p & 0x5555u) | ((uint32_t)__popc(p & 0xaaaau) << 16);
+    }
+    // prefetch the next chunk while this one is scanned
+    if (ch + 1 < nchunk) {
+#pragma unroll
+      for (int j = 0; j < VPT; ++j) {
+        const int t0 = cb + CH + (j * NT + tid) * 8;
+        v[j] = (t0 < c1) ? ld_stream_u4(cp + t0) : make_uint4(0, 0, 0, 0);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < VPT; ++j) {
+      pk[j] = (uint32_t)__popc(packed[j] & 0x5555u) | ((uint32_t)__popc(packed[j] & 0xaaaau) << 16);
       uint32_t x = pk[j];
 #pragma unroll
       for (int off = 1; off < 32; off <<= 1) {
@@ -214,50 +243,41 @@ __global__ __launch_bounds__(256) void select_scan_kernel(SelArgs a, int ntiles)
       if (lane == 31) wsum[j][warp] = x;
     }
     __syncthreads();
-
-    if (tid == 0) {
-      uint32_t run = 0;
+    if (warp == 0) {
+      // exclusive scan of the VPT*NW warp totals in (j, warp) order; 16-bit fields
+      // do not carry: a chunk holds <= 65535 tokens.
+      constexpr int NTOT = VPT * NW;
+      constexpr int PER = (NTOT + 31) / 32;
+      uint32_t loc[PER], s = 0;
 #pragma unroll
-      for (int j = 0; j < U; ++j)
-#pragma unroll
-        for (int w = 0; w < 8; ++w) {
-          const uint32_t s = wsum[j][w];
-          wsum[j][w] = run;
-          run += s;
-        }
-      const unsigned long long tgt = run & 0xffffu, teq = run >> 16;
-      unsigned long long* st = a.status + (size_t)pair * a.nchunks;
-      unsigned long long egt = 0, eeq = 0;
-      const unsigned long long FA = 1ull << 62, FP = 2ull << 62;
-      if (chunk == 0) {
-        st_release_u64(st, FP | tgt | (teq << 31));
-      } else {
-        st_release_u64(st + chunk, FA | tgt | (teq << 31));
-        for (int i = chunk - 1;; --i) {
-          unsigned long long s;
-          do {
-            s = ld_acquire_u64(st + i);
-          } while ((s >> 62) == 0ull);
-          egt += s & 0x7fffffffull;
-          eeq += (s >> 31) & 0x7fffffffull;
-          if ((s >> 62) == 2ull) break;
-        }
-        st_release_u64(st + chunk, FP | (egt + tgt) | ((eeq + teq) << 31));
+      for (int i = 0; i < PER; ++i) {
+        const int idx = lane * PER + i;
+        loc[i] = idx < NTOT ? wsum[idx / NW][idx % NW] : 0u;
+        s += loc[i];
       }
-      s_pgt = (uint32_t)egt;
-      s_peq = (uint32_t)eeq;
+      uint32_t inc = s;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, off);
+        if (lane >= off) inc += y;
+      }
+      uint32_t run = inc - s;
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        const int idx = lane * PER + i;
+        if (idx < NTOT) wsum[idx / NW][idx % NW] = run;
+        run += loc[i];
+      }
     }
     __syncthreads();
-
-    const uint32_t m = (uint32_t)a.pinfo[pair * 4 + 0];
-    int32_t* selp = a.sel + (size_t)pair * a.keff;
+    const uint32_t rgt = s_run[0], req = s_run[1];
 #pragma unroll
-    for (int j = 0; j < U; ++j) {
-      uint32_t p = packed[j];
+    for (int j = 0; j < VPT; ++j) {
+      const uint32_t p = packed[j];
       if (p == 0) continue;
       const uint32_t ex = wsum[j][warp] + incl[j] - pk[j];
-      uint32_t gb = s_pgt + (ex & 0xffffu), eb = s_peq + (ex >> 16);
-      const int t0 = cb + (j * 256 + tid) * 8;
+      uint32_t gb = rgt + (ex & 0xffffu), eb = req + (ex >> 16);
+      const int t0 = cb + (j * NT + tid) * 8;
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         const uint32_t c = (p >> (2 * e)) & 3u;
@@ -265,58 +285,43 @@ __global__ __launch_bounds__(256) void select_scan_kernel(SelArgs a, int ntiles)
         //  caller-supplied hist that is inconsistent with the codes)
         if (c == 1u) {
           const uint32_t pos = gb + min(eb, m);
-          if (pos < (uint32_t)a.keff) selp[pos] = t0 + e;
+          if (pos < keff) selp[pos] = t0 + e;
           ++gb;
         } else if (c == 2u) {
-          if (eb < m && gb + eb < (uint32_t)a.keff) selp[gb + eb] = t0 + e;
+          if (eb < m && gb + eb < keff) selp[gb + eb] = t0 + e;
           ++eb;
         }
       }
     }
     __syncthreads();
+    if (tid == NT - 1) {
+      // chunk totals = last (j, warp) exclusive prefix + its own count
+      const uint32_t tot = wsum[VPT - 1][NW - 1] + incl[VPT - 1];
+      s_run[0] = rgt + (tot & 0xffffu);
+      s_run[1] = req + (tot >> 16);
+    }
+    __syncthreads();
   }
 }
 
-template <int U>
-cudaError_t launch_scan_u(const SelArgs& a, int P, cudaStream_t st) {
-  const int smem = a.W * 32 * 4;
-  static int occ_cached = -1;
-  static int smem_cached = -1;
-  if (smem_cached != smem) {
-    cudaError_t e = cudaFuncSetAttribute(select_scan_kernel<U>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+template <int NT, int VPT>
+cudaError_t launch_fused(const SelArgs& a, int P, cudaStream_t st) {
+  const int smem = max(a.L * 8, a.W * 32 * 4);
+  static int smem_set = -1;
+  if (smem_set < smem) {
+    cudaError_t e =
+        cudaFuncSetAttribute(select_fused_kernel<NT, VPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    int occ = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, select_scan_kernel<U>, 256, smem);
-    if (e != cudaSuccess) return e;
-    occ_cached = occ > 0 ? occ : 1;
-    smem_cached = smem;
+    smem_set = smem;
   }
-  const int ntiles = P * a.nchunks;
-  int grid = sm_count() * occ_cached;
-  if (grid > ntiles) grid = ntiles;
-  select_scan_kernel<U><<<grid, 256, smem, st>>>(a, ntiles);
+  select_fused_kernel<NT, VPT><<<P, NT, smem, st>>>(a);
   return cudaGetLastError();
 }
 }  // namespace
 
-cudaError_t launch_threshold(const SelArgs& a, int P, cudaStream_t st) {
-  const int smem = a.L * 8;
-  static int smem_set = -1;
-  if (smem > 48 * 1024 && smem_set < smem) {
-    cudaError_t e = cudaFuncSetAttribute(select_threshold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    smem_set = smem;
-  }
-  select_threshold_kernel<<<P, kThrThreads, smem, st>>>(a);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_scan(const SelArgs& a, int P, int U, cudaStream_t st) {
-  switch (U) {
-    case 2: return launch_scan_u<2>(a, P, st);
-    case 4: return launch_scan_u<4>(a, P, st);
-    default: return launch_scan_u<8>(a, P, st);
-  }
+cudaError_t launch_select(const SelArgs& a, int P, cudaStream_t st) {
+  // one CTA per pair; 512 threads x 8 x 128-bit loads = 32768 tokens per chunk
+  return launch_fused<512, 8>(a, P, st);
 }
 
 }  // namespace a2ats

@@ -1,0 +1,58 @@
+"""Kernel micro-benchmark for ncu / quick timing: C2-shaped decode steps through the C ABI.
+
+    python tools/kbench.py [--config C2] [--iters 5] [--no-hist] [--encode]
+Not the bench contract (see bench.py); used for ncu captures and per-kernel timing.
+"""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import paper_2502_12665_b200 as A  # noqa: E402
+from synth import CONFIGS, budget_k, make_inputs  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="C2")
+ap.add_argument("--iters", type=int, default=5)
+ap.add_argument("--no-hist", action="store_true")
+ap.add_argument("--batch", type=int, default=0)
+ap.add_argument("--L", type=int, default=0)
+ap.add_argument("--N", type=int, default=0)
+args = ap.parse_args()
+cfg = CONFIGS[args.config]
+if args.batch:
+    cfg = cfg.with_(B=args.batch)
+if args.L:
+    cfg = cfg.with_(L=args.L)
+if args.N:
+    cfg = cfg.with_(N=args.N, K=budget_k(args.N))
+inp = make_inputs(cfg, 5, device="cuda", with_h=True)
+codes = inp["z"].to(torch.uint16)
+hist = torch.zeros((cfg.B, cfg.Hkv, cfg.L), dtype=torch.int32, device="cuda")
+c = codes[:, :, :cfg.N].to(torch.int64)
+hist.scatter_add_(2, c, torch.ones_like(c, dtype=torch.int32))
+dec = A.Decoder(cfg.B, cfg.Hq, cfg.Hkv, cfg.L, inp["n_max"], inp["codebook"], inp["H"], A.Params(topk=cfg.K))
+dec.codes, dec.hist = codes, hist
+out = torch.empty((cfg.B, cfg.Hq, 128), device="cuda")
+scratch_codes = torch.zeros_like(codes)
+flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+evs = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+for e in evs:
+    e.record()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+for it in range(args.iters):
+    flush.fill_(it)
+    e0.record()
+    dec.encode(inp["k_cache"], cfg.N - 1, cfg.N, update_hist=False, codes=scratch_codes)
+    e1.record()
+    A.a2ats_set_stage_events(evs)
+    dec.step(inp["q"], inp["k_cache"], inp["v_cache"], cfg.N, out=out, use_hist=not args.no_hist)
+    A.a2ats_set_stage_events(None)
+    torch.cuda.synchronize()
+    names = ["lut", "select", "attn", "tail"]
+    print("it", it, "enc %.1f" % (e0.elapsed_time(e1) * 1e3), " ".join(
+        "%s %.1f" % (n, evs[i].elapsed_time(evs[i + 1]) * 1e3) for i, n in enumerate(names)), "us")
