@@ -137,27 +137,27 @@ def run_ours(args, rank: int, world: int):
     e2e_steps = max(3, args.steps // 2)
     steps_total = 1 + args.warmup + args.steps     # 1 eager step sets kernel attributes before capture
     n0 = cfg.N - steps_total                        # prefix encoded before the loop; last timed step has n = N
-    inp = make_inputs(cfg, SEED + 17 * rank, device=dev, with_h=True, n_max=cfg.n_max(extra=e2e_steps + 8))
+    inp = make_inputs(cfg, SEED + 17 * rank, device=dev, with_h=True,
+                      n_max=cfg.n_max(extra=e2e_steps + args.steps + 8))
     q, kc, vc = inp["q"], inp["k_cache"], inp["v_cache"]
-    params = A.Params(topk=budget_k(cfg.N + e2e_steps))
+    params = A.Params(topk=budget_k(cfg.N + e2e_steps + args.steps))
     dec = A.Decoder(cfg.B, cfg.Hq, cfg.Hkv, cfg.L, inp["n_max"], inp["codebook"], inp["H"], params, device=dev)
     dec.encode(kc, 0, n0)                           # prefill codes + running histogram (untimed)
     out = torch.empty((cfg.B, cfg.Hq, cfg.d), dtype=torch.float32, device=dev)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)   # 256 MB > 126 MB L2
     torch.cuda.synchronize()
 
-    def one_step(n, evs=None, enc=None):
-        st = torch.cuda.current_stream()
-        if enc is not None:
-            enc[0].record(st)
-            A.a2ats_set_stage_events(evs)
+    def one_step(n, evs=None):
+        if evs is not None:
+            A.a2ats_set_stage_events(evs[1:])
         dec.encode(kc, n - 1, n)                    # a0: the new token's code (+ hist)
         dec.params.topk = budget_k(n)
         dec.step(q, kc, vc, n, out=out)             # a1..a6
-        if enc is not None:
-            enc[1].record(st)
+        if evs is not None:
             A.a2ats_set_stage_events(None)
 
+    # 7 events per profiled step: [start, after encode == before LUT, after LUT, after select,
+    # after attention, end]; the library records [1..5] via a2ats_set_stage_events
     stage_ev = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(args.steps)]
     enc_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     for evs in stage_ev:
@@ -168,19 +168,18 @@ def run_ours(args, rank: int, world: int):
     torch.cuda.synchronize()
 
     # One CUDA graph per step (n_ctx differs per step): replay = one launch per step, so the
-    # device timeline is not paced by host-side launch latency.
+    # device timeline is not paced by host-side launch latency, and the kernels' programmatic
+    # dependent launches overlap inside the graph.  Events are recorded outside the graphs
+    # (event nodes between PDL kernels are rejected and would serialise them anyway).
     use_graph = not args.no_graph
     graphs, ns = [], []
     for s in range(args.warmup + args.steps):
         n += 1
         ns.append(n)
-        k = s - args.warmup
-        evs = stage_ev[k] if k >= 0 else None
-        enc = enc_ev[k] if k >= 0 else None
         if use_graph:
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
-                one_step(n, evs, enc)
+                one_step(n)
             graphs.append(g)
     torch.cuda.synchronize()
 
@@ -188,8 +187,7 @@ def run_ours(args, rank: int, world: int):
         if use_graph:
             graphs[s].replay()
         else:
-            k = s - args.warmup
-            one_step(ns[s], stage_ev[k] if k >= 0 else None, enc_ev[k] if k >= 0 else None)
+            one_step(ns[s])
 
     for s in range(args.warmup):
         flush.fill_(1.0)
@@ -199,23 +197,38 @@ def run_ours(args, rank: int, world: int):
         torch.distributed.barrier()
     torch.cuda.synchronize()
     tokens = 0
+    stream = torch.cuda.current_stream()
     with ClockSampler(local) as clk:
-        for s in range(args.warmup, args.warmup + args.steps):
+        for k, s in enumerate(range(args.warmup, args.warmup + args.steps)):
             if not args.no_flush:
                 flush.fill_(float(s))
+            enc_ev[k][0].record(stream)
             run(s)
+            enc_ev[k][1].record(stream)
             tokens += cfg.B * cfg.Hkv * ns[s]
         torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
+    # profiling pass (untimed, eager launches): per-kernel device times from the library's stage events
+    prof_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for k in range(args.steps):
+        n += 1
+        if not args.no_flush:
+            flush.fill_(float(k))
+        torch.cuda.synchronize()
+        stage_ev[k][0].record(stream)
+        one_step(n, stage_ev[k])
+        torch.cuda.synchronize()
+    ns.append(n)
     step_ms = [enc_ev[k][0].elapsed_time(enc_ev[k][1]) for k in range(args.steps)]
-    names = ["lut", "select", "attention"]
-    stage_ms = {nm: [] for nm in ["encode"] + names}
+    names = ["encode", "lut", "select", "attention"]
+    stage_ms = {nm: [] for nm in names}
+    prof_step = []
     for k in range(args.steps):
         ev = stage_ev[k]
-        stage_ms["encode"].append(enc_ev[k][0].elapsed_time(ev[0]))
         for i, nm in enumerate(names):
             stage_ms[nm].append(ev[i].elapsed_time(ev[i + 1]))
+        prof_step.append(ev[0].elapsed_time(ev[5]))
     total_ms = sum(step_ms)
     if world > 1:
         t = torch.tensor([total_ms], device=dev)
@@ -231,7 +244,9 @@ def run_ours(args, rank: int, world: int):
     e2e = run_e2e(e2e_steps, dec, cfg, kc, vc, q, n_last, A, budget_k, use_graph, world, dev)
     return dict(value=value, ms_per_step=total_ms / args.steps,
                 stage_ms={k: statistics.mean(v) for k, v in stage_ms.items()},
-                clocks=clk.summary(), e2e=e2e, n_last=n_last, cfg=cfg, graph=use_graph)
+                prof_step_ms=statistics.mean(prof_step),
+                clocks=clk.summary(), e2e=e2e, n_last=ns[args.warmup + args.steps - 1], cfg=cfg, graph=use_graph)
+
 
 
 def run_e2e(steps, dec, cfg, kc, vc, q, n_start, A, budget_k, use_graph, world, dev):
@@ -431,7 +446,7 @@ def main():
             cpu = oracle_sample(cfg, seconds_budget=15.0)
         except Exception as e:  # never let the baseline kill the line
             cpu = {"error": repr(e)}
-    launches_per_step = 5  # keyh + encode_argmin + lut + select + attention
+    launches_per_step = 5  # keyh + encode + lut + select + attention
     line = {
         "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak",
@@ -446,6 +461,7 @@ def main():
                    "sparsity": (budget_k(r["n_last"]) + 68) / r["n_last"], "aux_mem": 2 / (cfg.d * 2)},
         "roofline": roof,
         "kernels": kernels,
+        "profiled_step_ms": r["prof_step_ms"],
         "cpu_baseline": cpu,
         "e2e": r["e2e"],
         "gpu_launches": launches_per_step * args.steps,

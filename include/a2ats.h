@@ -94,6 +94,8 @@ void a2ats_default_params(a2ats_params* p);
 
 const char* a2ats_status_string(int status);
 int a2ats_abi_version(void);
+/* Description of the calling thread's last A2ATS_ECUDA failure ("" if none). */
+const char* a2ats_last_cuda_error(void);
 
 /* ---------------------------------------------------------------------
  * a2ats_qavq_prepare -- codebook-side term of the query-aware quantizer.
@@ -168,6 +170,46 @@ int a2ats_decode_step(const a2ats_shape* shape, const a2ats_params* params, int3
                       const uint16_t* codes, const void* codebook, const int32_t* hist,
                       float* out, int32_t* sel_out, float* scores_out,
                       void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------
+ * Sequence-sharded decode step (the paper is single-GPU,
+ * P:732-733).  Rank r of R holds, for every (b, KV head), the contiguous
+ * global token range [shard_begin, shard_begin + shard_len) of the context in
+ * its own arrays of capacity shape->n_max (local row = global - shard_begin):
+ * codes [B,Hkv,n_max] uint16, k_cache / v_cache [B,Hkv,n_max,d] bf16 and the
+ * optional running histogram hist [B,Hkv,L] of the local tokens' codes.  q and
+ * the codebook are replicated.  n_ctx is the GLOBAL context length.  One step:
+ *
+ *   a2ats_shard_hist       LUT (a1+a2; bitwise identical on every rank) and the
+ *                          rank's candidate histogram -> cand_hist [B,Hkv,L] i32
+ *   [caller]               all-reduce(SUM) cand_hist over ranks (in place)
+ *   a2ats_shard_threshold  the K-th level v* and tie quota m of the GLOBAL
+ *                          top-K (identical on every rank) and this rank's
+ *                          (#candidates above v*, #at v*) -> counts [B,Hkv,2] i32
+ *   [caller]               all-gather counts -> counts_all [R,B,Hkv,2]
+ *   a2ats_shard_attend     local top-K emission (ties to the lowest global index,
+ *                          Q12: rank r keeps the first m - sum_{r'<r} eq_{r'}
+ *                          tied tokens it holds) and exact attention over the
+ *                          rank's rows of Sel -> partial [B,Hq,130] f32 =
+ *                          (max logit m, sum l, unnormalised o[128]) in the
+ *                          base-2 logit domain; optional sel_out [B,Hkv,K]
+ *   [caller]               all-gather partials -> [R,B,Hq,130]
+ *   a2ats_combine          log-sum-exp combine in rank order -> out [B,Hq,d]
+ * The union of the ranks' selections equals the single-GPU top-K exactly.
+ * All calls share one zero-initialised workspace (a2ats_shard_workspace_bytes).
+ * ------------------------------------------------------------------- */
+size_t a2ats_shard_workspace_bytes(const a2ats_shape* shape, const a2ats_params* params);
+int a2ats_shard_hist(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx, int32_t shard_begin,
+                     int32_t shard_len, const void* q, const uint16_t* codes, const void* codebook,
+                     const int32_t* hist, int32_t* cand_hist, void* ws, size_t ws_bytes, void* stream);
+int a2ats_shard_threshold(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx,
+                          const int32_t* cand_hist_global, int32_t* counts, void* ws, size_t ws_bytes,
+                          void* stream);
+int a2ats_shard_attend(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx, int32_t shard_begin,
+                       int32_t shard_len, int32_t rank, int32_t nranks, const int32_t* counts_all, const void* q,
+                       const void* k_cache, const void* v_cache, const uint16_t* codes, float* partial,
+                       int32_t* sel_out, void* ws, size_t ws_bytes, void* stream);
+int a2ats_combine(const a2ats_shape* shape, int32_t nparts, const float* partials, float* out, void* stream);
 
 /* ---------------------------------------------------------------------
  * a2ats_set_stage_events -- optional instrumentation for benchmarks.

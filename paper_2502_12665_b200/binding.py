@@ -12,7 +12,8 @@ import os
 from dataclasses import dataclass
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "lib", "liba2ats.so")
+# A2ATS_LIB selects a tuning variant built by build.build_variant (tools only)
+LIB_PATH = os.environ.get("A2ATS_LIB") or os.path.join(PKG, "lib", "liba2ats.so")
 
 A2ATS_OK = 0
 A2ATS_EINVAL = -1
@@ -29,7 +30,10 @@ A2ATS_KV_HOST_MAPPED = 1
 class A2ATSError(RuntimeError):
     def __init__(self, fn: str, status: int):
         self.status = status
-        super().__init__(f"{fn} -> {status}: {status_string(status)}")
+        extra = ""
+        if status == A2ATS_ECUDA:
+            extra = " [" + load().a2ats_last_cuda_error().decode() + "]"
+        super().__init__(f"{fn} -> {status}: {status_string(status)}{extra}")
 
 
 class a2ats_shape(ctypes.Structure):
@@ -49,6 +53,7 @@ _SIGS = {
     "a2ats_default_params": (None, [ctypes.POINTER(a2ats_params)]),
     "a2ats_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "a2ats_abi_version": (ctypes.c_int, []),
+    "a2ats_last_cuda_error": (ctypes.c_char_p, []),
     "a2ats_qavq_prepare": (ctypes.c_int, [ctypes.POINTER(a2ats_shape), _VP, _VP, _VP, _VP]),
     "a2ats_build_codes_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(a2ats_shape)]),
     "a2ats_build_codes": (ctypes.c_int, [ctypes.POINTER(a2ats_shape), _VP, ctypes.c_int32, ctypes.c_int32, _VP, _VP,
@@ -193,3 +198,72 @@ def a2ats_set_stage_events(events):
         return
     arr = (ctypes.c_void_p * len(events))(*[e.cuda_event for e in events])
     _check("a2ats_set_stage_events", lib.a2ats_set_stage_events(arr, len(events)))
+
+
+# ------------------------------------------------------------------ sequence-sharded step
+_SIGS.update({
+    "a2ats_shard_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(a2ats_shape), ctypes.POINTER(a2ats_params)]),
+    "a2ats_shard_hist": (ctypes.c_int, [ctypes.POINTER(a2ats_shape), ctypes.POINTER(a2ats_params), ctypes.c_int32,
+                                        ctypes.c_int32, ctypes.c_int32, _VP, _VP, _VP, _VP, _VP, _VP, ctypes.c_size_t,
+                                        _VP]),
+    "a2ats_shard_threshold": (ctypes.c_int, [ctypes.POINTER(a2ats_shape), ctypes.POINTER(a2ats_params),
+                                             ctypes.c_int32, _VP, _VP, _VP, ctypes.c_size_t, _VP]),
+    "a2ats_shard_attend": (ctypes.c_int, [ctypes.POINTER(a2ats_shape), ctypes.POINTER(a2ats_params), ctypes.c_int32,
+                                          ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _VP, _VP,
+                                          _VP, _VP, _VP, _VP, _VP, _VP, ctypes.c_size_t, _VP]),
+    "a2ats_combine": (ctypes.c_int, [ctypes.POINTER(a2ats_shape), ctypes.c_int32, _VP, _VP, _VP]),
+})
+if _lib is not None:  # declared after load(): attach the new signatures
+    for _n in ("a2ats_shard_workspace_bytes", "a2ats_shard_hist", "a2ats_shard_threshold", "a2ats_shard_attend",
+               "a2ats_combine"):
+        _f = getattr(_lib, _n)
+        _f.restype, _f.argtypes = _SIGS[_n]
+
+
+def a2ats_shard_workspace_bytes(shape: a2ats_shape, params) -> int:
+    p = params.c() if isinstance(params, Params) else params
+    return int(load().a2ats_shard_workspace_bytes(ctypes.byref(shape), ctypes.byref(p)))
+
+
+def a2ats_shard_hist(shape, params, n_ctx, shard_begin, shard_len, q, codes, codebook, hist, cand_hist, ws,
+                     stream=None):
+    import torch
+    p = params.c() if isinstance(params, Params) else params
+    rc = load().a2ats_shard_hist(ctypes.byref(shape), ctypes.byref(p), int(n_ctx), int(shard_begin), int(shard_len),
+                                 _ptr(q, "q", torch.bfloat16), _ptr(codes, "codes", torch.uint16),
+                                 _ptr(codebook, "codebook", torch.bfloat16),
+                                 _ptr(hist, "hist", torch.int32, optional=True),
+                                 _ptr(cand_hist, "cand_hist", torch.int32), _ptr(ws, "ws"),
+                                 ws.numel() * ws.element_size(), _stream(stream))
+    _check("a2ats_shard_hist", rc)
+
+
+def a2ats_shard_threshold(shape, params, n_ctx, cand_hist_global, counts, ws, stream=None):
+    import torch
+    p = params.c() if isinstance(params, Params) else params
+    rc = load().a2ats_shard_threshold(ctypes.byref(shape), ctypes.byref(p), int(n_ctx),
+                                      _ptr(cand_hist_global, "cand_hist_global", torch.int32),
+                                      _ptr(counts, "counts", torch.int32), _ptr(ws, "ws"),
+                                      ws.numel() * ws.element_size(), _stream(stream))
+    _check("a2ats_shard_threshold", rc)
+
+
+def a2ats_shard_attend(shape, params, n_ctx, shard_begin, shard_len, rank, nranks, counts_all, q, k_cache, v_cache,
+                       codes, partial, sel_out, ws, stream=None):
+    import torch
+    p = params.c() if isinstance(params, Params) else params
+    rc = load().a2ats_shard_attend(ctypes.byref(shape), ctypes.byref(p), int(n_ctx), int(shard_begin), int(shard_len),
+                                   int(rank), int(nranks), _ptr(counts_all, "counts_all", torch.int32),
+                                   _ptr(q, "q", torch.bfloat16), _ptr(k_cache, "k_cache", torch.bfloat16),
+                                   _ptr(v_cache, "v_cache", torch.bfloat16), _ptr(codes, "codes", torch.uint16),
+                                   _ptr(partial, "partial", torch.float32),
+                                   _ptr(sel_out, "sel_out", torch.int32, optional=True), _ptr(ws, "ws"),
+                                   ws.numel() * ws.element_size(), _stream(stream))
+    _check("a2ats_shard_attend", rc)
+
+
+def a2ats_combine(shape, nparts, partials, out, stream=None):
+    import torch
+    rc = load().a2ats_combine(ctypes.byref(shape), int(nparts), _ptr(partials, "partials", torch.float32),
+                              _ptr(out, "out", torch.float32), _stream(stream))
+    _check("a2ats_combine", rc)

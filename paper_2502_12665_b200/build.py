@@ -46,14 +46,29 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(f) <= t for f in _deps())
 
 
-def _compile(src: str, log: list) -> str:
-    obj = os.path.join(OBJDIR, os.path.splitext(src)[0] + ".o")
-    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-c", os.path.join(CSRC, src), "-o", obj]
+def _compile(src: str, log: list, defines=(), objdir=OBJDIR) -> str:
+    obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
+    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", INCLUDE, "-I", CSRC, "-c",
+           os.path.join(CSRC, src), "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     log.append((src, r.stdout + r.stderr))
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
     return obj
+
+
+def build_variant(name: str, defines: list[str]) -> str:
+    """Tuning builds only (tools/): same sources with extra -D defines, into lib/<name>.so."""
+    objdir = os.path.join(ROOT, "build", "obj_" + name)
+    os.makedirs(objdir, exist_ok=True)
+    log: list = []
+    with cf.ThreadPoolExecutor(max_workers=min(8, len(SOURCES))) as ex:
+        objs = list(ex.map(lambda s: _compile(s, log, defines, objdir), SOURCES))
+    out = os.path.join(LIBDIR, name + ".so")
+    r = subprocess.run([nvcc(), *ARCH, "-shared", "-o", out, *objs, "-cudart", "static"], capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"link failed:\n{r.stderr}")
+    return out
 
 
 def build(force: bool = False, verbose: bool = False) -> str:

@@ -2,6 +2,7 @@
 // Host orchestration only: validation, workspace carving, kernel launches on
 // the caller's stream.  No allocation, no host synchronisation.
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <mutex>
 
@@ -28,7 +29,10 @@ inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 // Rows of the Sel list handled by one attention CTA (fixed per shape so the
 // workspace size does not depend on n_ctx).
-constexpr int kAttnRows = 256;
+#ifndef A2ATS_ATTN_ROWS
+#define A2ATS_ATTN_ROWS 1024  // measured on B200 at C2: 256 -> 68 us, 512 -> 55 us, 1024 -> 49 us
+#endif
+constexpr int kAttnRows = A2ATS_ATTN_ROWS;
 
 struct Derived {
   int G, P, n_w, w0, n_s, c0, c1, n_cand, keff, M;
@@ -78,7 +82,7 @@ void derive(const a2ats_shape* s, const a2ats_params* p, int n_ctx, Derived* d) 
 }
 
 struct DecodeWs {
-  size_t qrot, cs, agg, lut, sel, part, actr, total;
+  size_t qrot, cs, agg, lut, qB, sel, part, actr, cand_keep, pinfo, nsel, total;
 };
 
 DecodeWs decode_layout(const a2ats_shape* s, const a2ats_params* p) {
@@ -93,9 +97,16 @@ DecodeWs decode_layout(const a2ats_shape* s, const a2ats_params* p) {
   w.cs = o; o = align_up(o + (size_t)p->window * kHalf * 8);
   w.agg = o; o = align_up(o + (size_t)P * s->L * 4);
   w.lut = o; o = align_up(o + (size_t)s->B * s->Hq * s->L * 4);
+  {
+    const int nvec = s->B * G, NV = lut_tile_nv(nvec), nvt = (nvec + NV - 1) / NV;
+    w.qB = o; o = align_up(o + (size_t)s->Hkv * nvt * 32 * NV * 16);
+  }
   w.sel = o; o = align_up(o + (size_t)P * std::max<long long>(kmax, 1) * 4);
   w.part = o; o = align_up(o + (size_t)P * (G / GT) * GT * nsplit_max * 130 * 4);
   w.actr = o; o = align_up(o + (size_t)P * (G / GT) * 4);
+  w.cand_keep = o; o = align_up(o + (size_t)P * s->L * 4);   // sharded step only
+  w.pinfo = o; o = align_up(o + (size_t)P * 16);
+  w.nsel = o; o = align_up(o + (size_t)P * 4);
   w.total = o;
   return w;
 }
@@ -120,7 +131,14 @@ void fill_rope(const a2ats_params* p, RopeTab* rt) {
     rt->inv_freq[m] = p->inv_freq ? p->inv_freq[m] : std::pow(p->rope_theta, -2.0 * m / (double)kD);
 }
 
-inline int cuda_status(cudaError_t e) { return e == cudaSuccess ? A2ATS_OK : A2ATS_ECUDA; }
+// last CUDA failure (code + api.cu line of the launch), for a2ats_last_cuda_error()
+thread_local char g_last_err[160] = "";
+inline int cuda_status(cudaError_t e, int line = __builtin_LINE()) {
+  if (e == cudaSuccess) return A2ATS_OK;
+  std::snprintf(g_last_err, sizeof(g_last_err), "%s (%s) at api.cu:%d", cudaGetErrorName(e), cudaGetErrorString(e),
+                line);
+  return A2ATS_ECUDA;
+}
 
 // Benchmark instrumentation (a2ats_set_stage_events).
 constexpr int kStageEvents = 5;
@@ -163,6 +181,8 @@ const char* a2ats_status_string(int status) {
 }
 
 int a2ats_abi_version(void) { return A2ATS_ABI_VERSION; }
+
+const char* a2ats_last_cuda_error(void) { return g_last_err; }
 
 int a2ats_set_stage_events(void* const* events, int n) {
   if (!events) {
@@ -284,6 +304,9 @@ int a2ats_decode_step(const a2ats_shape* shape, const a2ats_params* params, int3
   la.window = params->window;
   la.bridge = params->bridge;
   la.group_reduce = params->group_reduce;
+  la.qB = base + Lw.qB;
+  la.NV = lut_tile_nv(shape->B * d.G);
+  la.nvt = (shape->B * d.G + la.NV - 1) / la.NV;
   fill_rope(params, &la.rt);
   for (int m = 0; m < kHalf; ++m) {  // bridge rotation R_b: fp64 angles, fp32 cos/sin (reading Q16)
     const double ang = (double)params->bridge * la.rt.inv_freq[m];
@@ -310,6 +333,16 @@ int a2ats_decode_step(const a2ats_shape* shape, const a2ats_params* params, int3
     sa.n_s = d.n_s;
     sa.w0 = d.w0;
     sa.keff = d.keff;
+    sa.sel_stride = d.keff;
+    sa.shard_begin = 0;
+    sa.shard_len = shape->n_max;
+    sa.rank = 0;
+    sa.cand_out = sa.cand_keep = nullptr;
+    sa.cand_in = nullptr;
+    sa.pinfo = nullptr;
+    sa.counts_out = nullptr;
+    sa.counts_all = nullptr;
+    sa.nsel_out = nullptr;
     rc = cuda_status(launch_select(sa, d.P, st));
     if (rc) return rc;
   }
@@ -326,18 +359,22 @@ int a2ats_decode_step(const a2ats_shape* shape, const a2ats_params* params, int3
   aa.part = reinterpret_cast<float*>(base + Lw.part);
   aa.counter = reinterpret_cast<unsigned int*>(base + Lw.actr);
   aa.out = out;
+  aa.nsel = nullptr;
+  aa.part_out = nullptr;
   aa.Hq = shape->Hq;
   aa.Hkv = shape->Hkv;
   aa.G = d.G;
   aa.n_max = shape->n_max;
   aa.n_ctx = n_ctx;
-  aa.n_s = d.n_s;
   aa.keff = d.keff;
-  aa.n_w = d.n_w;
-  aa.w0 = d.w0;
-  aa.M = d.M;
+  aa.sel_stride = d.keff;
   aa.R = d.R;
   aa.nsplit = d.nsplit;
+  aa.n_s = d.n_s;
+  aa.sink_lo = 0;
+  aa.n_w = d.n_w;
+  aa.win_lo = d.w0;
+  aa.shard_begin = 0;
   aa.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)kD));
   rc = cuda_status(launch_attention(aa, d.P, d.GT, st));
   if (rc) return rc;
@@ -350,6 +387,187 @@ int a2ats_decode_step(const a2ats_shape* shape, const a2ats_params* params, int3
   }
   stage_mark(4, st);
   return A2ATS_OK;
+}
+
+// ------------------------------------------------------------------ sequence-sharded step
+namespace {
+int shard_common(const a2ats_shape* shape, const a2ats_params* params, int n_ctx, int shard_begin, int shard_len,
+                 void* ws, size_t ws_bytes) {
+  int rc = check_shape(shape);
+  if (rc) return rc;
+  rc = check_params(params);
+  if (rc) return rc;
+  if (n_ctx <= 0 || shard_begin < 0 || shard_len < 0 || shard_len > shape->n_max || shard_begin > n_ctx)
+    return A2ATS_EINVAL;
+  if (!ws || ws_bytes < decode_layout(shape, params).total) return A2ATS_EWORKSPACE;
+  return A2ATS_OK;
+}
+}  // namespace
+
+size_t a2ats_shard_workspace_bytes(const a2ats_shape* shape, const a2ats_params* params) {
+  return a2ats_decode_workspace_bytes(shape, params);
+}
+
+int a2ats_shard_hist(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx, int32_t shard_begin,
+                     int32_t shard_len, const void* q, const uint16_t* codes, const void* codebook,
+                     const int32_t* hist, int32_t* cand_hist, void* ws, size_t ws_bytes, void* stream) {
+  int rc = shard_common(shape, params, n_ctx, shard_begin, shard_len, ws, ws_bytes);
+  if (rc) return rc;
+  if (!q || !codes || !codebook || !cand_hist || !aligned16(q) || !aligned16(codes) || !aligned16(codebook))
+    return A2ATS_EINVAL;
+  const DecodeWs Lw = decode_layout(shape, params);
+  Derived d;
+  derive(shape, params, n_ctx, &d);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  LutArgs la;
+  la.q = static_cast<const uint16_t*>(q);
+  la.codebook = static_cast<const uint16_t*>(codebook);
+  la.agg = reinterpret_cast<float*>(base + Lw.agg);
+  la.lut_full = nullptr;
+  la.qrot = reinterpret_cast<float*>(base + Lw.qrot);
+  la.cs = reinterpret_cast<float2*>(base + Lw.cs);
+  la.B = shape->B;
+  la.Hq = shape->Hq;
+  la.Hkv = shape->Hkv;
+  la.G = d.G;
+  la.L = shape->L;
+  la.window = params->window;
+  la.bridge = params->bridge;
+  la.group_reduce = params->group_reduce;
+  la.qB = base + Lw.qB;
+  la.NV = lut_tile_nv(shape->B * d.G);
+  la.nvt = (shape->B * d.G + la.NV - 1) / la.NV;
+  fill_rope(params, &la.rt);
+  for (int m = 0; m < kHalf; ++m) {
+    const double ang = (double)params->bridge * la.rt.inv_freq[m];
+    la.bcs[m] = make_float2((float)std::cos(ang), (float)std::sin(ang));
+  }
+  rc = cuda_status(launch_lut(la, st));  // replicated on every rank, bitwise identical
+  if (rc) return rc;
+  SelArgs sa{};
+  sa.agg = la.agg;
+  sa.hist = hist;
+  sa.codes = codes;
+  sa.L = shape->L;
+  sa.W = d.W;
+  sa.n_max = shape->n_max;
+  sa.n_ctx = n_ctx;
+  sa.c0 = d.c0;
+  sa.c1 = d.c1;
+  sa.n_s = d.n_s;
+  sa.w0 = d.w0;
+  sa.keff = d.keff;
+  sa.shard_begin = shard_begin;
+  sa.shard_len = shard_len;
+  sa.cand_out = cand_hist;
+  sa.cand_keep = reinterpret_cast<int32_t*>(base + Lw.cand_keep);
+  return cuda_status(launch_shard_hist(sa, d.P, st));
+}
+
+int a2ats_shard_threshold(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx,
+                          const int32_t* cand_hist_global, int32_t* counts, void* ws, size_t ws_bytes, void* stream) {
+  int rc = shard_common(shape, params, n_ctx, 0, 0, ws, ws_bytes);
+  if (rc) return rc;
+  if (!cand_hist_global || !counts) return A2ATS_EINVAL;
+  const DecodeWs Lw = decode_layout(shape, params);
+  Derived d;
+  derive(shape, params, n_ctx, &d);
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  SelArgs sa{};
+  sa.agg = reinterpret_cast<float*>(base + Lw.agg);
+  sa.L = shape->L;
+  sa.W = d.W;
+  sa.n_max = shape->n_max;
+  sa.n_ctx = n_ctx;
+  sa.keff = d.keff;
+  sa.cand_in = cand_hist_global;
+  sa.cand_keep = reinterpret_cast<int32_t*>(base + Lw.cand_keep);
+  sa.pinfo = reinterpret_cast<uint32_t*>(base + Lw.pinfo);
+  sa.counts_out = counts;
+  return cuda_status(launch_shard_thresh(sa, d.P, static_cast<cudaStream_t>(stream)));
+}
+
+int a2ats_shard_attend(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx, int32_t shard_begin,
+                       int32_t shard_len, int32_t rank, int32_t nranks, const int32_t* counts_all, const void* q,
+                       const void* k_cache, const void* v_cache, const uint16_t* codes, float* partial,
+                       int32_t* sel_out, void* ws, size_t ws_bytes, void* stream) {
+  int rc = shard_common(shape, params, n_ctx, shard_begin, shard_len, ws, ws_bytes);
+  if (rc) return rc;
+  if (nranks < 1 || rank < 0 || rank >= nranks) return A2ATS_EINVAL;
+  if (!counts_all || !q || !k_cache || !v_cache || !codes || !partial) return A2ATS_EINVAL;
+  if (!aligned16(q) || !aligned16(k_cache) || !aligned16(v_cache) || !aligned16(codes)) return A2ATS_EINVAL;
+  const DecodeWs Lw = decode_layout(shape, params);
+  Derived d;
+  derive(shape, params, n_ctx, &d);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  const int kcap = std::max(1, (int)std::min<long long>(params->topk, shape->n_max));
+  int32_t* sel = sel_out ? sel_out : reinterpret_cast<int32_t*>(base + Lw.sel);
+  int32_t* nsel = reinterpret_cast<int32_t*>(base + Lw.nsel);
+  SelArgs sa{};
+  sa.agg = reinterpret_cast<float*>(base + Lw.agg);
+  sa.codes = codes;
+  sa.sel = sel;
+  sa.sel_stride = kcap;
+  sa.L = shape->L;
+  sa.W = d.W;
+  sa.n_max = shape->n_max;
+  sa.n_ctx = n_ctx;
+  sa.c0 = d.c0;
+  sa.c1 = d.c1;
+  sa.n_s = d.n_s;
+  sa.w0 = d.w0;
+  sa.keff = d.keff;
+  sa.shard_begin = shard_begin;
+  sa.shard_len = shard_len;
+  sa.rank = rank;
+  sa.pinfo = reinterpret_cast<uint32_t*>(base + Lw.pinfo);
+  sa.counts_all = counts_all;
+  sa.nsel_out = nsel;
+  rc = cuda_status(launch_shard_scan(sa, d.P, st));
+  if (rc) return rc;
+  // rows of Sel held by this rank
+  const int se = std::min(shard_begin + shard_len, n_ctx);
+  const int s_lo = std::max(0, shard_begin), s_hi = std::min(d.n_s, se);
+  const int w_lo = std::max(d.w0, shard_begin), w_hi = std::min(n_ctx, se);
+  AttnArgs aa;
+  aa.q = static_cast<const uint16_t*>(q);
+  aa.qrot = reinterpret_cast<float*>(base + Lw.qrot);
+  aa.cs = reinterpret_cast<float2*>(base + Lw.cs);
+  aa.kc = static_cast<const uint16_t*>(k_cache);
+  aa.vc = static_cast<const uint16_t*>(v_cache);
+  aa.sel = sel;
+  aa.nsel = nsel;
+  aa.part = reinterpret_cast<float*>(base + Lw.part);
+  aa.counter = reinterpret_cast<unsigned int*>(base + Lw.actr);
+  aa.out = nullptr;
+  aa.part_out = partial;
+  aa.Hq = shape->Hq;
+  aa.Hkv = shape->Hkv;
+  aa.G = d.G;
+  aa.n_max = shape->n_max;
+  aa.n_ctx = n_ctx;
+  aa.keff = d.keff;
+  aa.sel_stride = kcap;
+  aa.R = d.R;
+  aa.n_s = std::max(0, s_hi - s_lo);
+  aa.sink_lo = s_lo;
+  aa.n_w = std::max(0, w_hi - w_lo);
+  aa.win_lo = w_lo;
+  aa.shard_begin = shard_begin;
+  const int local_cand = std::max(0, std::min(d.c1, se) - std::max(d.c0, shard_begin));
+  const int mmax = aa.n_s + std::min(d.keff, local_cand) + aa.n_w;
+  aa.nsplit = std::max(1, (mmax + d.R - 1) / d.R);  // <= the workspace's max splits
+  aa.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)kD));
+  return cuda_status(launch_attention(aa, d.P, d.GT, st));
+}
+
+int a2ats_combine(const a2ats_shape* shape, int32_t nparts, const float* partials, float* out, void* stream) {
+  int rc = check_shape(shape);
+  if (rc) return rc;
+  if (nparts < 1 || !partials || !out) return A2ATS_EINVAL;
+  return cuda_status(launch_combine(partials, nparts, shape->B * shape->Hq, out, static_cast<cudaStream_t>(stream)));
 }
 
 }  // extern "C"

@@ -85,6 +85,8 @@ __global__ __launch_bounds__(128, 2) void attn_mma_kernel(AttnArgs a) {
   float* sQ = reinterpret_cast<float*>(smraw + SL.q);
   float* red = reinterpret_cast<float*>(smraw + SL.red);
 
+  pdl_wait();  // sel / counts / q~ come from the two previous kernels
+  pdl_trigger();
   const int split = blockIdx.x, pair = blockIdx.y;
   const int b = pair / a.Hkv, h = pair - b * a.Hkv;
   const int G = a.G;
@@ -92,19 +94,41 @@ __global__ __launch_bounds__(128, 2) void attn_mma_kernel(AttnArgs a) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g8 = lane >> 2, t4 = lane & 3;  // mma fragment coordinates
 
-  const int p0 = split * a.R, p1 = min(p0 + a.R, a.M);
-  const int pw = a.n_s + a.keff;             // first window position in the Sel list
+  // Sel list of this pair on this rank: [sinks][top-K rows][window rows], ascending
+  const int keff = a.nsel ? __ldcg(a.nsel + pair) : a.keff;
+  const int M = a.n_s + keff + a.n_w;
+  const int nsplit = (M + a.R - 1) / a.R;
+  if (M == 0) {  // no row of this pair lives on this rank: empty partial (sharded mode only)
+    if (split == 0 && a.part_out) {
+      for (int i = tid; i < G * 130; i += 128) {
+        const int gg = i / 130, f = i - gg * 130;
+        a.part_out[((size_t)b * a.Hq + hq0 + gg) * 130 + f] = (f == 0) ? -INFINITY : 0.f;
+      }
+    }
+    return;
+  }
+  if (split >= nsplit) return;
+  const int p0 = split * a.R, p1 = min(p0 + a.R, M);
+  const int pw = a.n_s + keff;               // first window position in the Sel list
   const int nA = max(0, min(p1, pw) - p0);   // bridge rows of this split
   const int nB = (p1 - p0) - nA;             // window rows of this split
   const int gA = (nA + 15) >> 4, gB = (nB + 15) >> 4, ngroups = gA + gB;
 
-  for (int i = tid; i < p1 - p0; i += 128) {
-    const int p = p0 + i;
-    int t;
-    if (p < a.n_s) t = p;
-    else if (p < pw) t = a.sel[(size_t)pair * a.keff + (p - a.n_s)];
-    else t = a.w0 + (p - pw);
-    s_tok[i] = t;
+  for (int i0 = 0; i0 < p1 - p0; i0 += 4 * 128) {  // 4 index loads in flight per thread
+    int tv[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int p = p0 + i0 + j * 128 + tid;
+      tv[j] = 0;
+      if (p < p1) {  // local row index of the K/V arrays
+        if (p < a.n_s) tv[j] = a.sink_lo + p - a.shard_begin;
+        else if (p < pw) tv[j] = __ldcg(a.sel + (size_t)pair * a.sel_stride + (p - a.n_s)) - a.shard_begin;
+        else tv[j] = a.win_lo + (p - pw) - a.shard_begin;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (p0 + i0 + j * 128 + tid < p1) s_tok[i0 + j * 128 + tid] = tv[j];
   }
   if (nB > 0) {
     for (int i = tid; i < 8 * kD; i += 128) {
@@ -172,7 +196,7 @@ __global__ __launch_bounds__(128, 2) void attn_mma_kernel(AttnArgs a) {
   const int nsteps = (ngroups > warp) ? (ngroups - warp + kWarps - 1) / kWarps : 0;
 #pragma unroll 1
   for (int s = 0; s < kStages - 1; ++s) issue(s);
-  const int icur = a.n_ctx - 1;
+  const int icur = a.n_ctx - 1 - a.shard_begin;  // current token, in local row units
   float* sS = reinterpret_cast<float*>(smraw + SL.sS) + warp * 128;
 
 #pragma unroll 1
@@ -207,7 +231,7 @@ __global__ __launch_bounds__(128, 2) void attn_mma_kernel(AttnArgs a) {
       float acc[8];
 #pragma unroll
       for (int gg = 0; gg < 8; ++gg) acc[gg] = 0.f;
-#pragma unroll 1
+#pragma unroll
       for (int c = 0; c < 4; ++c) {  // 8 pairs per chunk: m = hf*32 + c*8 + i
         const int ch1 = hf * 4 + c, ch2 = 8 + hf * 4 + c;
         const uint4 k1 = *reinterpret_cast<const uint4*>(krow + swz(row, ch1));
@@ -314,8 +338,22 @@ __global__ __launch_bounds__(128, 2) void attn_mma_kernel(AttnArgs a) {
 
   // combine the 4 warps: thread tid -> element e = tid
   const int e = tid;
-  float* part = a.part + (size_t)pair * G * a.nsplit * 130;
-  const bool single = (a.nsplit == 1);
+  // final result of a pair: normalised output, or (sharded mode) the rank's partial
+  // (m, l, o) in the base-2 logit domain for the cross-rank LSE combine
+  auto emit = [&](int gg, float M, float den, float num) {
+    if (a.part_out) {
+      float* dst = a.part_out + ((size_t)b * a.Hq + hq0 + gg) * 130;
+      dst[2 + e] = num;
+      if (e == 0) {
+        dst[0] = M;
+        dst[1] = den;
+      }
+    } else {
+      a.out[((size_t)b * a.Hq + hq0 + gg) * kD + e] = num / den;
+    }
+  };
+  float* part = a.part + (size_t)pair * G * a.nsplit * 130;  // stride: max splits
+  const bool single = (nsplit == 1);
   for (int gg = 0; gg < G; ++gg) {
     float M = -INFINITY;
 #pragma unroll
@@ -329,7 +367,7 @@ __global__ __launch_bounds__(128, 2) void attn_mma_kernel(AttnArgs a) {
       den = fmaf(red[(w * 8 + gg) * 130 + 1], sw, den);
     }
     if (single) {
-      a.out[((size_t)b * a.Hq + hq0 + gg) * kD + e] = acc / den;
+      emit(gg, M, den, acc);
     } else {
       float* dst = part + ((size_t)gg * a.nsplit + split) * 130;
       dst[2 + e] = acc;
@@ -346,7 +384,7 @@ __global__ __launch_bounds__(128, 2) void attn_mma_kernel(AttnArgs a) {
   __syncthreads();
   if (tid == 0) {
     const unsigned prev = atomicAdd(a.counter + pair, 1u);
-    s_last = (prev == (unsigned)(a.nsplit - 1));
+    s_last = (prev == (unsigned)(nsplit - 1));
   }
   __syncthreads();
   if (!s_last) return;
@@ -354,17 +392,35 @@ __global__ __launch_bounds__(128, 2) void attn_mma_kernel(AttnArgs a) {
   for (int gg = 0; gg < G; ++gg) {
     const float* src = part + (size_t)gg * a.nsplit * 130;
     float M = -INFINITY;
-    for (int s = 0; s < a.nsplit; ++s) M = fmaxf(M, __ldcg(src + s * 130));
+    for (int s = 0; s < nsplit; ++s) M = fmaxf(M, __ldcg(src + s * 130));
     float num = 0.f, den = 0.f;
-    for (int s = 0; s < a.nsplit; ++s) {
+    for (int s = 0; s < nsplit; ++s) {
       const float ms = __ldcg(src + s * 130);
       const float sw = (ms == -INFINITY) ? 0.f : exp2f(ms - M);
       num = fmaf(__ldcg(src + s * 130 + 2 + e), sw, num);
       den = fmaf(__ldcg(src + s * 130 + 1), sw, den);
     }
-    a.out[((size_t)b * a.Hq + hq0 + gg) * kD + e] = num / den;
+    emit(gg, M, den, num);
   }
   if (tid == 0) a.counter[pair] = 0u;  // leave the workspace in its zero state
+}
+
+// Cross-rank log-sum-exp combine of partials [R][B*Hq][130] (base-2 logits), fixed rank order.
+__global__ void combine_kernel(const float* __restrict__ parts, int R, int rows, float* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
+  const int row = blockIdx.x, e = threadIdx.x;
+  if (row >= rows) return;
+  float M = -INFINITY;
+  for (int r = 0; r < R; ++r) M = fmaxf(M, parts[((size_t)r * rows + row) * 130]);
+  float num = 0.f, den = 0.f;
+  for (int r = 0; r < R; ++r) {
+    const float* p = parts + ((size_t)r * rows + row) * 130;
+    const float sw = (p[0] == -INFINITY) ? 0.f : exp2f(p[0] - M);
+    num = fmaf(p[2 + e], sw, num);
+    den = fmaf(p[1], sw, den);
+  }
+  out[(size_t)row * kD + e] = num / den;
 }
 }  // namespace
 
@@ -377,8 +433,11 @@ cudaError_t launch_attention(const AttnArgs& a, int P, int /*GT*/, cudaStream_t 
     smem_set = L.total;
   }
   dim3 grid(a.nsplit, P, 1);
-  attn_mma_kernel<<<grid, 128, L.total, st>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(attn_mma_kernel, grid, dim3(128), L.total, st, a);
+}
+
+cudaError_t launch_combine(const float* parts, int R, int rows, float* out, cudaStream_t st) {
+  return launch_pdl(combine_kernel, dim3(rows), dim3(kD), 0, st, parts, R, rows, out);
 }
 
 }  // namespace a2ats

@@ -91,6 +91,8 @@ __global__ __launch_bounds__(256) void keyh_kernel(EncArgs a) {
     for (int j = 0; j < 8; ++j) ks[vv][c * 8 + j] = (j & 1) ? bf_hi(w[j >> 1]) : bf_lo(w[j >> 1]);
   }
   __syncthreads();
+  pdl_wait();  // H and the keys are step inputs; u is read by the previous step's encode
+  pdl_trigger();
   const int e = tid & (kD - 1), vh = tid >> 7;  // 2 groups of 8 keys
   float acc[8];
   if (a.H) {
@@ -154,15 +156,31 @@ __global__ __launch_bounds__(128, 1) void encode_kernel(EncArgs a) {
       if (c0 + r < a.L) cp_async16(dst, a.codebook + ((size_t)h * a.L + c0 + r) * kD + c * 8);
       else *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
     }
-    for (int i = tid; i < kNB; i += 128) sN0[buf * kNB + i] = (c0 + i < a.L) ? a.nrm[(size_t)h * a.L + c0 + i] : 0.f;
+    if (c0 + kNB <= a.L && (a.L & 3) == 0) {
+      if (tid < kNB / 4) cp_async16(sN0 + buf * kNB + 4 * tid, a.nrm + (size_t)h * a.L + c0 + 4 * tid);
+    } else {
+      for (int i = tid; i < kNB; i += 128) sN0[buf * kNB + i] = (c0 + i < a.L) ? a.nrm[(size_t)h * a.L + c0 + i] : 0.f;
+    }
     cp_async_commit();
   };
-  load_tile(tbeg, 0);
+  load_tile(tbeg, 0);  // codebook tile + n_j: inputs, overlaps keyh's tail
+  pdl_wait();          // u comes from keyh
+  pdl_trigger();
 
-  // A: this thread's key row u (fp32) -> hi/lo bf16 chunks
+  // A: key rows u (fp32) staged through the (still idle) second B buffer with cp.async,
+  // then split into hi/lo bf16 chunks; this thread converts its own row.
   {
+    uint8_t* stage = sB0 + kNB * kD * 2;  // 64 KB = 128 rows x 512 B
+    const int nrow = min(kTV, a.nvec - vec0);
+    for (int p = tid; p < nrow * 32; p += 128) {
+      const int r = p >> 5, piece = p & 31;
+      cp_async16(stage + r * 512 + piece * 16, a.u + ((size_t)h * a.nvec + vec0 + r) * kD + piece * 4);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
     const int v = vec0 + tid;
-    const float4* up = reinterpret_cast<const float4*>(a.u + ((size_t)h * a.nvec + v) * kD);
+    const float4* up = reinterpret_cast<const float4*>(stage + tid * 512);
 #pragma unroll 4
     for (int c = 0; c < 16; ++c) {
       float x[8];
@@ -183,6 +201,7 @@ __global__ __launch_bounds__(128, 1) void encode_kernel(EncArgs a) {
           make_uint4(lo[0] | (uint32_t(lo[1]) << 16), lo[2] | (uint32_t(lo[3]) << 16), lo[4] | (uint32_t(lo[5]) << 16),
                      lo[6] | (uint32_t(lo[7]) << 16));
     }
+    __syncthreads();  // the staging buffer is refilled with codeword tiles below
   }
 
   float best = INFINITY;
@@ -288,13 +307,11 @@ cudaError_t launch_encode(const EncArgs& a, cudaStream_t st) {
     attr_done = true;
   }
   dim3 g1((a.nvec + kKeyhV - 1) / kKeyhV, a.Hkv);
-  keyh_kernel<<<g1, 256, a.H ? kD * kD * 4 : 0, st>>>(a);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl(keyh_kernel, g1, dim3(256), a.H ? kD * kD * 4 : 0, st, a);
   if (e != cudaSuccess) return e;
   const int ntile = (a.L + kNB - 1) / kNB;
   dim3 g2((a.nvec + kTV - 1) / kTV, a.Hkv, (ntile + a.tiles_per_split - 1) / a.tiles_per_split);
-  encode_kernel<<<g2, 128, kEncSmem, st>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(encode_kernel, g2, dim3(128), kEncSmem, st, a);
 }
 
 int encode_codeword_tile() { return kNB; }

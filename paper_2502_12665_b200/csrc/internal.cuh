@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
+
 #include "a2ats.h"
 
 namespace a2ats {
@@ -16,6 +18,50 @@ constexpr int kHalf = 64;   // d / 2 rotation pairs (half-split pairing, DESIGN.
 struct RopeTab {
   double inv_freq[kHalf];
 };
+
+// ---------------------------------------------------------------- tuning instrumentation
+// Built only into the tools/ variant (-DA2ATS_PHASES): CTA 0 of a kernel records
+// clock64() at phase boundaries; each .cu exports a2ats_debug_<file>_phases().
+#ifdef A2ATS_PHASES
+#define A2ATS_PHASE_DECL(name) __device__ long long name[16];
+#define A2ATS_PHASE(arr, i)                                                        \
+  if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0) \
+    arr[i] = clock64();
+#define A2ATS_PHASE_EXPORT(fn, arr)                                                           \
+  extern "C" int fn(long long* out) {                                                         \
+    return cudaMemcpyFromSymbol(out, arr, 16 * sizeof(long long)) == cudaSuccess ? 0 : -4; \
+  }
+#else
+#define A2ATS_PHASE_DECL(name)
+#define A2ATS_PHASE(arr, i)
+#define A2ATS_PHASE_EXPORT(fn, arr)
+#endif
+
+// ---------------------------------------------------------------- programmatic dependent launch
+// Every kernel of the path is launched with programmatic stream serialization:
+// kernel N+1 may start while kernel N runs, does its input-independent prologue
+// (TMEM alloc, constant / input loads), then pdl_wait()s for N's completion.
+// Each kernel calls pdl_trigger() only AFTER its own pdl_wait(), so at most two
+// kernels overlap and a pre-wait prologue never races a kernel two back.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  static const bool pdl_off = std::getenv("A2ATS_NO_PDL") != nullptr;  // debugging switch
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_off ? 0 : 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
 
 // ---------------------------------------------------------------- device helpers
 __device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
@@ -71,17 +117,29 @@ struct LutArgs {
   float* lut_full;           // [B, Hq, L] or nullptr (debug scores)
   float* qrot;               // [B, Hq, 128]   q~ = q R_b
   float2* cs;                // [window, 64]   (cos, sin)(r f_m)
+  uint8_t* qB;               // [Hkv, nvt, 32 chunks, NV rows, 16 B] q~ hi/lo as the tcgen05 B operand
   int B, Hq, Hkv, G, L, window, bridge, group_reduce;
+  int NV, nvt;               // query rows per MMA tile (multiple of 16, <= 256), tiles per head
   RopeTab rt;
   float2 bcs[kHalf];         // (cos, sin)(b f_m), from fp64 angles on the host
 };
+int lut_tile_nv(int nvec);
 
 struct SelArgs {
   const float* agg;             // [P, L]
-  const int32_t* hist;          // [P, L] or nullptr
-  const uint16_t* codes;        // [P, n_max]
-  int32_t* sel;                 // [P, keff]
-  int L, W, n_max, n_ctx, c0, c1, n_s, w0, keff;
+  const int32_t* hist;          // [P, L] or nullptr (counts of the LOCAL tokens' codes)
+  const uint16_t* codes;        // [P, n_max] local code array (local index = global - shard_begin)
+  int32_t* sel;                 // [P, sel_stride] selected global token indices, ascending
+  int L, W, n_max, n_ctx, c0, c1, n_s, w0, keff, sel_stride;
+  // sequence sharding (single GPU: shard_begin = 0, shard_len = n_max)
+  int shard_begin, shard_len, rank;
+  int32_t* cand_out;            // [P, L] local candidate histogram, exchanged (all-reduce in place)
+  int32_t* cand_keep;           // [P, L] local candidate histogram, kept in the workspace
+  const int32_t* cand_in;       // [P, L] all-reduced candidate histogram
+  uint32_t* pinfo;              // [P, 4] key(v*), m, K_eff (global)
+  int32_t* counts_out;          // [P, 2] this rank's candidates above / at v*
+  const int32_t* counts_all;    // [R, P, 2] all-gathered counts
+  int32_t* nsel_out;            // [P] number of locally selected tokens
 };
 
 struct AttnArgs {
@@ -90,11 +148,17 @@ struct AttnArgs {
   const float2* cs;       // [window, 64]
   const uint16_t* kc;     // bf16 [B, Hkv, n_max, 128]
   const uint16_t* vc;
-  const int32_t* sel;     // [P, keff]
-  float* part;            // [P * nz, GT, nsplit, 130]
-  unsigned int* counter;  // [P * nz]
-  float* out;             // [B, Hq, 128]
-  int Hq, Hkv, G, n_max, n_ctx, n_s, keff, n_w, w0, M, R, nsplit;
+  const int32_t* sel;     // [P, sel_stride] selected global token indices, ascending
+  const int32_t* nsel;    // [P] selected count per pair (sharded), or nullptr => keff
+  float* part;            // [P, G, nsplit (max), 130] split partials
+  unsigned int* counter;  // [P]
+  float* out;             // [B, Hq, 128] normalised output (single GPU)
+  float* part_out;        // [B, Hq, 130] this rank's partial (m, l, o) (sharded), or nullptr
+  int Hq, Hkv, G, n_max, n_ctx, keff, sel_stride, R, nsplit;
+  // rows of the Sel list held by this rank, in global token indices
+  int n_s, sink_lo;       // sinks [sink_lo, sink_lo + n_s)
+  int n_w, win_lo;        // window [win_lo, win_lo + n_w)
+  int shard_begin;        // local row = global - shard_begin
   float scale_log2;       // log2(e) / sqrt(d)
 };
 
@@ -116,7 +180,11 @@ cudaError_t launch_lut(const LutArgs& a, cudaStream_t st);
 cudaError_t launch_scores(const float* lut_full, const uint16_t* codes, float* scores, int B, int Hq, int Hkv,
                           int G, int L, int n_max, int n_ctx, cudaStream_t st);
 cudaError_t launch_select(const SelArgs& a, int P, cudaStream_t st);
+cudaError_t launch_shard_hist(const SelArgs& a, int P, cudaStream_t st);
+cudaError_t launch_shard_thresh(const SelArgs& a, int P, cudaStream_t st);
+cudaError_t launch_shard_scan(const SelArgs& a, int P, cudaStream_t st);
 cudaError_t launch_attention(const AttnArgs& a, int P, int GT, cudaStream_t st);
+cudaError_t launch_combine(const float* parts, int R, int rows, float* out, cudaStream_t st);
 cudaError_t launch_prepare(const uint16_t* codebook, const float* H, float* nrm, int Hkv, int L, cudaStream_t st);
 cudaError_t launch_encode(const EncArgs& a, cudaStream_t st);
 

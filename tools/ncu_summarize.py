@@ -1,0 +1,111 @@
+"""Summarise ncu captures into profiles/ (tracked).
+
+    python tools/ncu_summarize.py --rep gpurun_out/prof.ncu-rep --launches gpurun_out/launches.csv --tag r1
+
+Writes profiles/ncu_<tag>_full.csv (one row per profiled kernel: duration,
+DRAM bytes, throughputs, tensor-pipe activity, registers, occupancy),
+profiles/ncu_<tag>_launches.csv (per-kernel mean device time and share of the
+step from the gpu__time_duration launch list) and profiles/ncu_traffic.json
+(DRAM bytes per launch by bench stage, read by bench.py's roofline.traffic).
+"""
+import argparse
+import csv
+import io
+import json
+import os
+import re
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+STAGE = [("attn", "attention"), ("select_kernel", "select"), ("lut_umma", "lut"), ("qprep", "lut_prep"),
+         ("encode_kernel", "encode"), ("keyh", "encode_keyh")]
+METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+           "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+           "dram__throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+           "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+           "sm__inst_executed_pipe_tensor.avg.pct_of_peak_sustained_active",
+           "launch__registers_per_thread", "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__grid_size",
+           "launch__block_size", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
+
+
+def short(name):
+    n = name.split("(")[0]
+    n = re.sub(r".*::", "", n)
+    return n
+
+
+def stage_of(name):
+    for key, st in STAGE:
+        if key in name:
+            return st
+    return None
+
+
+def full(rep, tag):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units = rows[0], rows[1]
+    idx = {m: hdr.index(m) for m in METRICS if m in hdr}
+    ki = hdr.index("Kernel Name")
+    res, traffic = [], {}
+    for r in rows[2:]:
+        d = {"kernel": short(r[ki])}
+        for m, i in idx.items():
+            v = r[i].replace(",", "")
+            try:
+                d[m] = float(v)
+            except ValueError:
+                d[m] = v
+        res.append(d)
+        st = stage_of(r[ki])
+        if st and "dram__bytes_read.sum" in d:
+            unit_r = units[idx["dram__bytes_read.sum"]]
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit_r, 1)
+            rw = (d["dram__bytes_read.sum"] + d.get("dram__bytes_write.sum", 0.0)) * scale
+            traffic.setdefault(st, []).append(rw)
+    path = os.path.join(ROOT, "profiles", f"ncu_{tag}_full.csv")
+    with open(path, "w", newline="") as f:
+        w = csv.DictWriter(f, fieldnames=["kernel"] + [m for m in METRICS if m in idx])
+        w.writeheader()
+        for d in res:
+            w.writerow(d)
+    units_line = {m: units[i] for m, i in idx.items()}
+    with open(path.replace(".csv", "_units.json"), "w") as f:
+        json.dump(units_line, f, indent=1)
+    tj = {k: sum(v) / len(v) for k, v in traffic.items()}
+    with open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w") as f:
+        json.dump(dict(tj, _source=f"ncu --set full, {os.path.basename(rep)}, bytes read+written per launch"), f,
+                  indent=1)
+    print(path)
+
+
+def launches(path_csv, tag):
+    rows = list(csv.reader(open(path_csv)))
+    hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
+    h = rows[hi]
+    ki, vi = h.index("Kernel Name"), h.index("Metric Value")
+    agg = {}
+    for r in rows[hi + 1:]:
+        n = short(r[ki])
+        agg.setdefault(n, []).append(float(r[vi].replace(",", "")))
+    tot = sum(sum(v) for k, v in agg.items() if stage_of(k))
+    out = os.path.join(ROOT, "profiles", f"ncu_{tag}_launches.csv")
+    with open(out, "w", newline="") as f:
+        w = csv.writer(f)
+        w.writerow(["kernel", "launches", "mean_ns", "share_of_path_time"])
+        for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
+            w.writerow([k, len(v), sum(v) / len(v), (sum(v) / tot) if stage_of(k) and tot else ""])
+    print(out)
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--rep")
+    ap.add_argument("--launches")
+    ap.add_argument("--tag", default="r1")
+    a = ap.parse_args()
+    if a.rep:
+        full(a.rep, a.tag)
+    if a.launches:
+        launches(a.launches, a.tag)
