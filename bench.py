@@ -110,8 +110,8 @@ def stage_model(cfg, n_ctx: int, k: int):
     keff = min(k, n_cand)
     M = n_s + keff + n_w
     return {
-        "encode": dict(bytes=P * d * 2 + Hkv * L * (d * 2 + 4) + Hkv * d * d * 4 + P * 2,
-                       flops=2 * P * L * d + 2 * P * d * d, bound="hbm"),
+        # new keys + prepared codebook c^ (hi|lo bf16) and n_j + codes / histogram updates
+        "encode": dict(bytes=P * d * 2 + Hkv * L * (4 * d + 4) + P * (2 + 4), flops=2 * P * L * 2 * d, bound="hbm"),
         "lut": dict(bytes=Hkv * L * d * 2 + B * Hq * d * 2 + P * L * 4 + B * Hq * d * 4, flops=2 * B * Hq * L * d,
                     bound="alu"),
         "select": dict(bytes=P * n_cand * 2 + P * keff * 4, flops=0, bound="hbm", tokens=P * n_ctx,
@@ -446,7 +446,7 @@ def main():
             cpu = oracle_sample(cfg, seconds_budget=15.0)
         except Exception as e:  # never let the baseline kill the line
             cpu = {"error": repr(e)}
-    launches_per_step = 5  # keyh + encode + lut + select + attention
+    launches_per_step = 4  # encode + lut + select + attention
     line = {
         "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak",

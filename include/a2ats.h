@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define A2ATS_ABI_VERSION 1
+#define A2ATS_ABI_VERSION 2
 
 /* ---- status codes ---------------------------------------------------- */
 #define A2ATS_OK 0
@@ -98,20 +98,26 @@ int a2ats_abi_version(void);
 const char* a2ats_last_cuda_error(void);
 
 /* ---------------------------------------------------------------------
- * a2ats_qavq_prepare -- codebook-side term of the query-aware quantizer.
+ * a2ats_qavq_prepare -- codebook-side terms of the query-aware quantizer.
  *
  * f'(k; C) = argmin_j (k - c_j) H (k - c_j)^T            (Eq. 14)
- *          = argmin_j ( n_j - 2 (k H) . c_j ),  n_j = c_j H c_j^T   (H = H^T)
- * This writes n [Hkv, L] fp32 (the per-codeword constant of that argmin).
+ *          = argmin_j ( n_j - 2 k . c^_j )
+ * with S = (H + H^T)/2, c^_j = c_j S and n_j = c_j H c_j^T (the term k H k^T
+ * does not depend on j).  Outputs:
+ *   nrm      : [Hkv, L] fp32, n_j
+ *   chat     : [Hkv, L, 2d] bf16 (16-B aligned), row j = hi(c^_j) | lo(c^_j)
+ *              with hi = bf16(c^_j), lo = bf16(c^_j - hi) (round to nearest),
+ *              so hi + lo carries c^_j to ~2^-16 relative
+ * Inputs:
  *   codebook : [Hkv, L, d] bf16, the shared codebook C
- *   H        : [Hkv, d, d] fp32 symmetric positive definite second-moment
- *              matrix of post-PE queries; NULL => H = I (conventional
- *              VQ, Eq. 5)
- *   nrm      : [Hkv, L] fp32 output
- * Call once per codebook (offline state); no workspace.
+ *   H        : [Hkv, d, d] fp32 positive definite second-moment matrix of
+ *              post-PE queries; NULL => H = I (conventional VQ, Eq. 5,
+ *              P:115-118; then chat = c | 0 and nrm = |c|^2)
+ * Call once per codebook (offline state, SURVEY §8 a0); no workspace.
+ * Returns A2ATS_EINVAL on NULL / misaligned pointers.
  * ------------------------------------------------------------------- */
 int a2ats_qavq_prepare(const a2ats_shape* shape, const void* codebook, const float* H,
-                       float* nrm, void* stream);
+                       float* nrm, void* chat, void* stream);
 
 /* ---------------------------------------------------------------------
  * a2ats_build_codes -- inference-time quantization (Eq. 20).
@@ -121,17 +127,18 @@ int a2ats_qavq_prepare(const a2ats_shape* shape, const void* codebook, const flo
  * and, if hist != NULL, hist[b,h,codes[b,h,t]] += 1.
  *   keys     : [B, Hkv, n_max, d] bf16 PRE-PE keys (under WRoPE the post-PE
  *              key equals the pre-PE key, Eq. 12)
- *   codebook : [Hkv, L, d] bf16;  H : [Hkv, d, d] fp32 or NULL (as above)
- *   nrm      : [Hkv, L] fp32 from a2ats_qavq_prepare with the same C, H
+ *   chat, nrm: from a2ats_qavq_prepare (same C, H)
  *   codes    : [B, Hkv, n_max] uint16 out; only [t_begin, t_end) written
  *   hist     : optional [B, Hkv, L] int32 running histogram, accumulated
+ *   ws       : zero-filled before first use, ws_bytes >= the query below;
+ *              left zeroed again on return (reusable, one stream at a time)
  * 0 <= t_begin <= t_end <= n_max.  Used for prefill (whole prompt) and for
  * each decode step (the new token).
  * ------------------------------------------------------------------- */
 size_t a2ats_build_codes_workspace_bytes(const a2ats_shape* shape);
 int a2ats_build_codes(const a2ats_shape* shape, const void* keys, int32_t t_begin, int32_t t_end,
-                      const void* codebook, const float* H, const float* nrm, uint16_t* codes,
-                      int32_t* hist, void* ws, size_t ws_bytes, void* stream);
+                      const void* chat, const float* nrm, uint16_t* codes, int32_t* hist,
+                      void* ws, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------
  * a2ats_decode_step -- one decode step of the retrieval path, all pairs.

@@ -54,10 +54,10 @@ _SIGS = {
     "a2ats_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "a2ats_abi_version": (ctypes.c_int, []),
     "a2ats_last_cuda_error": (ctypes.c_char_p, []),
-    "a2ats_qavq_prepare": (ctypes.c_int, [ctypes.POINTER(a2ats_shape), _VP, _VP, _VP, _VP]),
+    "a2ats_qavq_prepare": (ctypes.c_int, [ctypes.POINTER(a2ats_shape), _VP, _VP, _VP, _VP, _VP]),
     "a2ats_build_codes_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(a2ats_shape)]),
     "a2ats_build_codes": (ctypes.c_int, [ctypes.POINTER(a2ats_shape), _VP, ctypes.c_int32, ctypes.c_int32, _VP, _VP,
-                                         _VP, _VP, _VP, _VP, ctypes.c_size_t, _VP]),
+                                         _VP, _VP, _VP, ctypes.c_size_t, _VP]),
     "a2ats_decode_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(a2ats_shape), ctypes.POINTER(a2ats_params)]),
     "a2ats_set_stage_events": (ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int]),
     "a2ats_decode_step": (ctypes.c_int, [ctypes.POINTER(a2ats_shape), ctypes.POINTER(a2ats_params), ctypes.c_int32,
@@ -65,6 +65,9 @@ _SIGS = {
 }
 
 _lib = None
+
+
+ABI_VERSION = 2  # include/a2ats.h A2ATS_ABI_VERSION
 
 
 def load(path: str = LIB_PATH, build_if_missing: bool = True) -> ctypes.CDLL:
@@ -82,6 +85,8 @@ def load(path: str = LIB_PATH, build_if_missing: bool = True) -> ctypes.CDLL:
         f = getattr(lib, name)
         f.restype = res
         f.argtypes = args
+    if lib.a2ats_abi_version() != ABI_VERSION:
+        raise OSError(f"{path}: ABI version {lib.a2ats_abi_version()}, binding expects {ABI_VERSION}; rebuild it")
     _lib = lib
     return lib
 
@@ -147,11 +152,11 @@ def _stream(stream):
 
 
 # ------------------------------------------------------------------ entry points (same names as the C ABI)
-def a2ats_qavq_prepare(shape: a2ats_shape, codebook, H, nrm, stream=None):
+def a2ats_qavq_prepare(shape: a2ats_shape, codebook, H, nrm, chat, stream=None):
     import torch
     rc = load().a2ats_qavq_prepare(ctypes.byref(shape), _ptr(codebook, "codebook", torch.bfloat16),
                                    _ptr(H, "H", torch.float32, optional=True), _ptr(nrm, "nrm", torch.float32),
-                                   _stream(stream))
+                                   _ptr(chat, "chat", torch.bfloat16), _stream(stream))
     _check("a2ats_qavq_prepare", rc)
 
 
@@ -159,12 +164,11 @@ def a2ats_build_codes_workspace_bytes(shape: a2ats_shape) -> int:
     return int(load().a2ats_build_codes_workspace_bytes(ctypes.byref(shape)))
 
 
-def a2ats_build_codes(shape: a2ats_shape, keys, t_begin: int, t_end: int, codebook, H, nrm, codes, hist, ws,
+def a2ats_build_codes(shape: a2ats_shape, keys, t_begin: int, t_end: int, chat, nrm, codes, hist, ws,
                       stream=None):
     import torch
     rc = load().a2ats_build_codes(ctypes.byref(shape), _ptr(keys, "keys", torch.bfloat16), int(t_begin), int(t_end),
-                                  _ptr(codebook, "codebook", torch.bfloat16), _ptr(H, "H", torch.float32, optional=True),
-                                  _ptr(nrm, "nrm", torch.float32), _ptr(codes, "codes", torch.uint16),
+                                  _ptr(chat, "chat", torch.bfloat16), _ptr(nrm, "nrm", torch.float32), _ptr(codes, "codes", torch.uint16),
                                   _ptr(hist, "hist", torch.int32, optional=True), _ptr(ws, "ws"),
                                   ws.numel() * ws.element_size(), _stream(stream))
     _check("a2ats_build_codes", rc)

@@ -82,7 +82,7 @@ void derive(const a2ats_shape* s, const a2ats_params* p, int n_ctx, Derived* d) 
 }
 
 struct DecodeWs {
-  size_t qrot, cs, agg, lut, qB, sel, part, actr, cand_keep, pinfo, nsel, total;
+  size_t qrot, cs, agg, lut, sel, part, actr, cand_keep, pinfo, nsel, total;
 };
 
 DecodeWs decode_layout(const a2ats_shape* s, const a2ats_params* p) {
@@ -97,10 +97,6 @@ DecodeWs decode_layout(const a2ats_shape* s, const a2ats_params* p) {
   w.cs = o; o = align_up(o + (size_t)p->window * kHalf * 8);
   w.agg = o; o = align_up(o + (size_t)P * s->L * 4);
   w.lut = o; o = align_up(o + (size_t)s->B * s->Hq * s->L * 4);
-  {
-    const int nvec = s->B * G, NV = lut_tile_nv(nvec), nvt = (nvec + NV - 1) / NV;
-    w.qB = o; o = align_up(o + (size_t)s->Hkv * nvt * 32 * NV * 16);
-  }
   w.sel = o; o = align_up(o + (size_t)P * std::max<long long>(kmax, 1) * 4);
   w.part = o; o = align_up(o + (size_t)P * (G / GT) * GT * nsplit_max * 130 * 4);
   w.actr = o; o = align_up(o + (size_t)P * (G / GT) * 4);
@@ -114,12 +110,11 @@ DecodeWs decode_layout(const a2ats_shape* s, const a2ats_params* p) {
 constexpr int kEncVcap = 16384;  // key vectors per KV head encoded per launch
 
 struct EncodeWs {
-  size_t u, slot, ctr, total;
+  size_t slot, ctr, total;
 };
 EncodeWs encode_layout(const a2ats_shape* s) {
   EncodeWs w;
   size_t o = 0;
-  w.u = o; o = align_up(o + (size_t)s->Hkv * kEncVcap * kD * 4);
   w.slot = o; o = align_up(o + (size_t)s->Hkv * kEncVcap * 8);
   w.ctr = o; o = align_up(o + (size_t)s->Hkv * (kEncVcap / 64) * 4);
   w.total = o;
@@ -198,12 +193,14 @@ int a2ats_set_stage_events(void* const* events, int n) {
   return A2ATS_OK;
 }
 
-int a2ats_qavq_prepare(const a2ats_shape* shape, const void* codebook, const float* H, float* nrm, void* stream) {
+int a2ats_qavq_prepare(const a2ats_shape* shape, const void* codebook, const float* H, float* nrm, void* chat,
+                       void* stream) {
   int rc = check_shape(shape);
   if (rc) return rc;
-  if (!codebook || !nrm || !aligned16(codebook) || (H && !aligned16(H))) return A2ATS_EINVAL;
-  return cuda_status(launch_prepare(static_cast<const uint16_t*>(codebook), H, nrm, shape->Hkv, shape->L,
-                                    static_cast<cudaStream_t>(stream)));
+  if (!codebook || !nrm || !chat || !aligned16(codebook) || !aligned16(chat) || (H && !aligned16(H)))
+    return A2ATS_EINVAL;
+  return cuda_status(launch_prepare(static_cast<const uint16_t*>(codebook), H, nrm, static_cast<uint16_t*>(chat),
+                                    shape->Hkv, shape->L, static_cast<cudaStream_t>(stream)));
 }
 
 size_t a2ats_build_codes_workspace_bytes(const a2ats_shape* shape) {
@@ -212,12 +209,12 @@ size_t a2ats_build_codes_workspace_bytes(const a2ats_shape* shape) {
 }
 
 int a2ats_build_codes(const a2ats_shape* shape, const void* keys, int32_t t_begin, int32_t t_end,
-                      const void* codebook, const float* H, const float* nrm, uint16_t* codes, int32_t* hist,
-                      void* ws, size_t ws_bytes, void* stream) {
+                      const void* chat, const float* nrm, uint16_t* codes, int32_t* hist, void* ws,
+                      size_t ws_bytes, void* stream) {
   int rc = check_shape(shape);
   if (rc) return rc;
-  if (!keys || !codebook || !nrm || !codes) return A2ATS_EINVAL;
-  if (!aligned16(keys) || !aligned16(codebook) || (H && !aligned16(H))) return A2ATS_EINVAL;
+  if (!keys || !chat || !nrm || !codes) return A2ATS_EINVAL;
+  if (!aligned16(keys) || !aligned16(chat)) return A2ATS_EINVAL;
   if (t_begin < 0 || t_end < t_begin || t_end > shape->n_max) return A2ATS_EINVAL;
   const EncodeWs L = encode_layout(shape);
   if (!ws || ws_bytes < L.total) return A2ATS_EWORKSPACE;
@@ -226,10 +223,8 @@ int a2ats_build_codes(const a2ats_shape* shape, const void* keys, int32_t t_begi
   uint8_t* base = static_cast<uint8_t*>(ws);
   EncArgs a;
   a.keys = static_cast<const uint16_t*>(keys);
-  a.codebook = static_cast<const uint16_t*>(codebook);
-  a.H = H;
+  a.chat = static_cast<const uint16_t*>(chat);
   a.nrm = nrm;
-  a.u = reinterpret_cast<float*>(base + L.u);
   a.slot = reinterpret_cast<unsigned long long*>(base + L.slot);
   a.counter = reinterpret_cast<unsigned int*>(base + L.ctr);
   a.codes = codes;
@@ -304,7 +299,6 @@ int a2ats_decode_step(const a2ats_shape* shape, const a2ats_params* params, int3
   la.window = params->window;
   la.bridge = params->bridge;
   la.group_reduce = params->group_reduce;
-  la.qB = base + Lw.qB;
   la.NV = lut_tile_nv(shape->B * d.G);
   la.nvt = (shape->B * d.G + la.NV - 1) / la.NV;
   fill_rope(params, &la.rt);
@@ -435,7 +429,6 @@ int a2ats_shard_hist(const a2ats_shape* shape, const a2ats_params* params, int32
   la.window = params->window;
   la.bridge = params->bridge;
   la.group_reduce = params->group_reduce;
-  la.qB = base + Lw.qB;
   la.NV = lut_tile_nv(shape->B * d.G);
   la.nvt = (shape->B * d.G + la.NV - 1) / la.NV;
   fill_rope(params, &la.rt);

@@ -23,6 +23,7 @@
 namespace a2ats {
 
 namespace {
+A2ATS_TL_DECL(g_attn_tl)
 constexpr int kWarps = 4;
 constexpr int kStages = 3;
 constexpr int kTileBytes = 16 * 256;           // one K (or V) tile: 16 rows x 256 B
@@ -78,7 +79,7 @@ __device__ __forceinline__ void split_pair(float x0, float x1, uint32_t& hi, uin
 // byte offset of (row, 16-B chunk) inside a 16 x 256 B tile, XOR swizzle on the chunk
 __device__ __forceinline__ uint32_t swz(int row, int chunk) { return row * 256 + ((chunk ^ (row & 7)) << 4); }
 
-__global__ __launch_bounds__(128, 2) void attn_mma_kernel(AttnArgs a) {
+__device__ __forceinline__ void attn_body(const AttnArgs& a) {
   extern __shared__ __align__(128) uint8_t smraw[];
   const SmemLayout SL = attn_smem(a.R);
   int32_t* s_tok = reinterpret_cast<int32_t*>(smraw + SL.tok);
@@ -158,8 +159,14 @@ __global__ __launch_bounds__(128, 2) void attn_mma_kernel(AttnArgs a) {
     const int g = s * kWarps + warp;
     if (g < ngroups) {
       int r0, nr;
-      tile_of(g, r0, nr);
+      const bool win = tile_of(g, r0, nr);
       uint8_t* st = wring + (s % kStages) * kStageBytes;
+      if (win) {  // warm L1 with this lane's (cos, sin) row half (2 x 128 B) for the window logits
+        const int row = lane >> 1, rr = row < nr ? row : nr - 1;
+        const float2* p = a.cs + (size_t)(a.n_ctx - 1 - a.shard_begin - s_tok[r0 + rr]) * kHalf + (lane & 1) * 32;
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(p + 16));
+      }
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         const int idx = lane + 32 * i;  // 512 pieces: (kv, row, chunk)
@@ -228,43 +235,32 @@ __global__ __launch_bounds__(128, 2) void attn_mma_kernel(AttnArgs a) {
       const int r = icur - s_tok[r0 + rrow];
       const float4* csp = reinterpret_cast<const float4*>(a.cs + (size_t)r * kHalf + hf * 32);
       const uint8_t* krow = wring + (s % kStages) * kStageBytes;
-      float acc[8];
+      // rolled loops: window tiles are few (<= 4 per pair), so code size beats ILP here
+#pragma unroll 1
+      for (int gg = 0; gg < G; ++gg) {
+        float acc = 0.f;
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {  // 8 pairs per chunk: m = hf*32 + c*8 + i
+          const int ch1 = hf * 4 + c, ch2 = 8 + hf * 4 + c;
+          const uint4 k1 = *reinterpret_cast<const uint4*>(krow + swz(row, ch1));
+          const uint4 k2 = *reinterpret_cast<const uint4*>(krow + swz(row, ch2));
+          const uint32_t w1[4] = {k1.x, k1.y, k1.z, k1.w}, w2[4] = {k2.x, k2.y, k2.z, k2.w};
+          const float* qa = sQ + gg * kD + hf * 32 + c * 8;
 #pragma unroll
-      for (int gg = 0; gg < 8; ++gg) acc[gg] = 0.f;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {  // 8 pairs per chunk: m = hf*32 + c*8 + i
-        const int ch1 = hf * 4 + c, ch2 = 8 + hf * 4 + c;
-        const uint4 k1 = *reinterpret_cast<const uint4*>(krow + swz(row, ch1));
-        const uint4 k2 = *reinterpret_cast<const uint4*>(krow + swz(row, ch2));
-        const uint32_t w1[4] = {k1.x, k1.y, k1.z, k1.w}, w2[4] = {k2.x, k2.y, k2.z, k2.w};
-        float cv[8], sv[8];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float4 t = csp[c * 4 + i];
-          cv[2 * i] = t.x; sv[2 * i] = t.y; cv[2 * i + 1] = t.z; sv[2 * i + 1] = t.w;
-        }
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const float ka = (i & 1) ? bf_hi(w1[i >> 1]) : bf_lo(w1[i >> 1]);
-          const float kb = (i & 1) ? bf_hi(w2[i >> 1]) : bf_lo(w2[i >> 1]);
-          const int m = hf * 32 + c * 8 + i;
-#pragma unroll
-          for (int gg = 0; gg < 8; ++gg) {
-            if (gg < G) {
-              const float qa = sQ[gg * kD + m], qb = sQ[gg * kD + m + kHalf];
-              const float A = fmaf(qa, ka, qb * kb);
-              const float Bm = fmaf(qa, kb, -qb * ka);
-              acc[gg] = fmaf(cv[i], A, fmaf(sv[i], Bm, acc[gg]));
-            }
+          for (int i = 0; i < 8; ++i) {
+            const float2 t = reinterpret_cast<const float2*>(csp)[c * 8 + i];
+            const float ka = (i & 1) ? bf_hi(w1[i >> 1]) : bf_lo(w1[i >> 1]);
+            const float kb = (i & 1) ? bf_hi(w2[i >> 1]) : bf_lo(w2[i >> 1]);
+            const float A = fmaf(qa[i], ka, qa[i + kHalf] * kb);
+            const float Bm = fmaf(qa[i], kb, -qa[i + kHalf] * ka);
+            acc = fmaf(t.x, A, fmaf(t.y, Bm, acc));
           }
         }
+        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+        if (hf == 0) sS[row * 8 + gg] = acc;
       }
-#pragma unroll
-      for (int gg = 0; gg < 8; ++gg) acc[gg] += __shfl_xor_sync(0xffffffffu, acc[gg], 1);
-      if (hf == 0) {
-#pragma unroll
-        for (int gg = 0; gg < 8; ++gg) sS[row * 8 + gg] = acc[gg];
-      }
+#pragma unroll 1
+      for (int gg = G + hf; gg < 8; gg += 2) sS[row * 8 + gg] = 0.f;  // unused head columns: finite
       __syncwarp();
       sc[0] = sS[g8 * 8 + 2 * t4];
       sc[1] = sS[g8 * 8 + 2 * t4 + 1];
@@ -405,6 +401,12 @@ __global__ __launch_bounds__(128, 2) void attn_mma_kernel(AttnArgs a) {
   if (tid == 0) a.counter[pair] = 0u;  // leave the workspace in its zero state
 }
 
+__global__ __launch_bounds__(128, 2) void attn_mma_kernel(AttnArgs a) {
+  A2ATS_TL(g_attn_tl, 0);
+  attn_body(a);
+  A2ATS_TL(g_attn_tl, 1);
+}
+
 // Cross-rank log-sum-exp combine of partials [R][B*Hq][130] (base-2 logits), fixed rank order.
 __global__ void combine_kernel(const float* __restrict__ parts, int R, int rows, float* __restrict__ out) {
   pdl_wait();
@@ -441,3 +443,5 @@ cudaError_t launch_combine(const float* parts, int R, int rows, float* out, cuda
 }
 
 }  // namespace a2ats
+
+A2ATS_TL_EXPORT(a2ats_debug_attn_timeline, a2ats::g_attn_tl)

@@ -31,10 +31,28 @@ struct RopeTab {
   extern "C" int fn(long long* out) {                                                         \
     return cudaMemcpyFromSymbol(out, arr, 16 * sizeof(long long)) == cudaSuccess ? 0 : -4; \
   }
+// CTA timeline: thread 0 of every CTA records %globaltimer (ns) at its start (0)
+// and end (1); a2ats_debug_<kernel>_timeline() copies [kTlMax][2].
+constexpr int kTlMax = 8192;
+#define A2ATS_TL_DECL(name) __device__ unsigned long long name[kTlMax][2];
+#define A2ATS_TL(arr, i)                                                                       \
+  if (threadIdx.x == 0) {                                                                      \
+    const unsigned cta_ = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;     \
+    unsigned long long t_;                                                                     \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                     \
+    if (cta_ < kTlMax) arr[cta_][i] = t_;                                                      \
+  }
+#define A2ATS_TL_EXPORT(fn, arr)                                                                        \
+  extern "C" int fn(unsigned long long* out) {                                                          \
+    return cudaMemcpyFromSymbol(out, arr, sizeof(unsigned long long) * 2 * a2ats::kTlMax) == cudaSuccess ? 0 : -4; \
+  }
 #else
 #define A2ATS_PHASE_DECL(name)
 #define A2ATS_PHASE(arr, i)
 #define A2ATS_PHASE_EXPORT(fn, arr)
+#define A2ATS_TL_DECL(name)
+#define A2ATS_TL(arr, i)
+#define A2ATS_TL_EXPORT(fn, arr)
 #endif
 
 // ---------------------------------------------------------------- programmatic dependent launch
@@ -117,7 +135,6 @@ struct LutArgs {
   float* lut_full;           // [B, Hq, L] or nullptr (debug scores)
   float* qrot;               // [B, Hq, 128]   q~ = q R_b
   float2* cs;                // [window, 64]   (cos, sin)(r f_m)
-  uint8_t* qB;               // [Hkv, nvt, 32 chunks, NV rows, 16 B] q~ hi/lo as the tcgen05 B operand
   int B, Hq, Hkv, G, L, window, bridge, group_reduce;
   int NV, nvt;               // query rows per MMA tile (multiple of 16, <= 256), tiles per head
   RopeTab rt;
@@ -164,10 +181,8 @@ struct AttnArgs {
 
 struct EncArgs {
   const uint16_t* keys;      // bf16 [B, Hkv, n_max, 128]
-  const uint16_t* codebook;  // bf16 [Hkv, L, 128]
-  const float* H;            // [Hkv, 128, 128] or nullptr
+  const uint16_t* chat;      // bf16 [Hkv, L, 256]   c^_j = c_j S as hi | lo
   const float* nrm;          // [Hkv, L]
-  float* u;                  // ws [Hkv, vcap, 128]   u = k H
   unsigned long long* slot;  // ws [Hkv, vcap]         ~pack(dist, code), 0 = empty
   unsigned int* counter;     // ws [Hkv, vcap / 64]
   uint16_t* codes;           // [B, Hkv, n_max]
@@ -185,11 +200,13 @@ cudaError_t launch_shard_thresh(const SelArgs& a, int P, cudaStream_t st);
 cudaError_t launch_shard_scan(const SelArgs& a, int P, cudaStream_t st);
 cudaError_t launch_attention(const AttnArgs& a, int P, int GT, cudaStream_t st);
 cudaError_t launch_combine(const float* parts, int R, int rows, float* out, cudaStream_t st);
-cudaError_t launch_prepare(const uint16_t* codebook, const float* H, float* nrm, int Hkv, int L, cudaStream_t st);
+cudaError_t launch_prepare(const uint16_t* codebook, const float* H, float* nrm, uint16_t* chat, int Hkv, int L,
+                           cudaStream_t st);
 cudaError_t launch_encode(const EncArgs& a, cudaStream_t st);
 
 int sm_count();
 int encode_codeword_tile();
 int encode_key_tile();
+int encode_cw_max();  // keys per head up to which the codeword-major (decode) encoder runs
 
 }  // namespace a2ats

@@ -1,13 +1,12 @@
 // a1 + a2: WRoPE query rotation and the score table LUT = q~ C^T, folded over
 // the GQA group into agg[b, h, l] (Eq. 12, Eq. 21).
 //
-// qprep_kernel: q~ = q R_b once per query vector (fp32, for the attention) and
-//   its bf16 hi + lo split laid out as the tcgen05 B operand of its KV head; the
-//   window relative-rotation table cs[r][m] = (cos, sin)(r f_m) from fp64 angles.
 // lut_umma_kernel: per KV head a dense contraction (M = L codewords, N = B*G
 //   queries, K = 2 x 128 for hi and lo) on the 5th-gen tensor cores: one CTA
-//   stages a 128-codeword tile and the head's query tile with cp.async in the
-//   canonical K-major layout, one thread issues 16 tcgen05.mma (kind::f16,
+//   stages a 128-codeword tile with cp.async and computes its query tile
+//   q~ = q R_b itself (bf16 hi + lo split, canonical K-major layout); the grid
+//   also writes q~ in fp32 and the window table cs[r][m] = (cos, sin)(r f_m)
+//   (fp64 angles) for the attention.  One thread issues 16 tcgen05.mma (kind::f16,
 //   fp32 accumulator in TMEM), and the epilogue reads its codeword's row
 //   (tcgen05.ld), folds the G query heads (max or sum, reading Q10) and writes
 //   agg coalesced.  The codebook is exact in bf16 and q~ = hi + lo to ~2^-16, so
@@ -18,6 +17,7 @@
 namespace a2ats {
 
 namespace {
+A2ATS_TL_DECL(g_lut_tl)
 A2ATS_PHASE_DECL(g_lut_phase)
 constexpr int kTC = 128;  // codewords per CTA (MMA M)
 
@@ -25,41 +25,32 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-// grid.x = max(B*Hq, window); 64 threads = the 64 rotation pairs (m, m+64).
-__global__ __launch_bounds__(64) void qprep_kernel(LutArgs a) {
-  const int m = threadIdx.x;
-  const int blk = blockIdx.x;
-  if (blk < a.window) {  // window table row r = blk
-    double s, c;
-    sincos((double)blk * a.rt.inv_freq[m], &s, &c);
-    a.cs[blk * kHalf + m] = make_float2((float)c, (float)s);
+// q~ = q R_b (Eq. 12) for the half-split pairs (m, m+64), m in [m0, m0 + 8): fp32.
+__device__ __forceinline__ void rotate8(const LutArgs& a, int qrow, int m0, float y1[8], float y2[8]) {
+  const uint4 u1 = ld_nc_u4(a.q + (size_t)qrow * kD + m0);
+  const uint4 u2 = ld_nc_u4(a.q + (size_t)qrow * kD + m0 + kHalf);
+  const uint32_t w1[4] = {u1.x, u1.y, u1.z, u1.w}, w2[4] = {u2.x, u2.y, u2.z, u2.w};
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const float x1 = (e & 1) ? bf_hi(w1[e >> 1]) : bf_lo(w1[e >> 1]);
+    const float x2 = (e & 1) ? bf_hi(w2[e >> 1]) : bf_lo(w2[e >> 1]);
+    const float2 cs = a.bcs[m0 + e];
+    y1[e] = fmaf(x1, cs.x, -x2 * cs.y);
+    y2[e] = fmaf(x2, cs.x, x1 * cs.y);
   }
-  if (blk < a.B * a.Hq) {
-    const int b = blk / a.Hq, hq = blk - b * a.Hq, h = hq / a.G, g = hq - h * a.G;
-    const int n = b * a.G + g, vt = n / a.NV, nr = n - vt * a.NV;
-    const size_t qoff = (size_t)blk * kD;
-    const float x1 = bf_u16(a.q[qoff + m]), x2 = bf_u16(a.q[qoff + m + kHalf]);
-    const float2 cs = a.bcs[m];
-    const float y1 = fmaf(x1, cs.x, -x2 * cs.y);  // q~ = q R_b (Eq. 12), half-split pair (m, m+64)
-    const float y2 = fmaf(x2, cs.x, x1 * cs.y);
-    a.qrot[qoff + m] = y1;
-    a.qrot[qoff + m + kHalf] = y2;
-    uint16_t h1, l1, h2, l2;
-    umma::split_bf16(y1, h1, l1);
-    umma::split_bf16(y2, h2, l2);
-    uint16_t* tile = reinterpret_cast<uint16_t*>(a.qB + ((size_t)(h * a.nvt + vt) * 32) * a.NV * 16);
-    const int c = m >> 3, e = m & 7;
-    tile[((c)*a.NV + nr) * 8 + e] = h1;            // hi, elements 0..63
-    tile[((c + 8) * a.NV + nr) * 8 + e] = h2;      // hi, elements 64..127
-    tile[((c + 16) * a.NV + nr) * 8 + e] = l1;     // lo
-    tile[((c + 24) * a.NV + nr) * 8 + e] = l2;
-  }
-  pdl_wait();  // inputs only above; wait for transitivity of the dependency chain
-  pdl_trigger();
 }
 
+__device__ __forceinline__ uint4 pack8(const uint16_t v[8]) {
+  return make_uint4(v[0] | (uint32_t(v[1]) << 16), v[2] | (uint32_t(v[3]) << 16), v[4] | (uint32_t(v[5]) << 16),
+                    v[6] | (uint32_t(v[7]) << 16));
+}
+
+// grid (ceil(L / 128), nvt, Hkv), 128 threads.  Before the dependency wait (inputs
+// only): the codeword tile and this CTA's query tile, q~ = q R_b computed here and
+// split hi/lo straight into the canonical B layout.  After it: the per-step tables
+// the attention reads (q~ fp32, window (cos, sin)), the MMAs and the G-fold epilogue.
 template <uint32_t kTmemCols, int G>
-__global__ __launch_bounds__(128, 1) void lut_umma_kernel(LutArgs a) {
+__device__ __forceinline__ void lut_body(const LutArgs& a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int NV = a.NV;
   uint8_t* sA = smem;                 // [16 chunks][128 codes][16 B]
@@ -79,7 +70,7 @@ __global__ __launch_bounds__(128, 1) void lut_umma_kernel(LutArgs a) {
     umma::mbar_init(&mbar, 1);
     umma::mbar_fence_init();
   }
-  // codeword tile -> canonical K-major layout (cp.async, 16 B per piece); a step input
+  // codeword tile -> canonical K-major layout (cp.async, 16 B per piece)
   for (int idx = tid; idx < kTC * 16; idx += 128) {
     const int r = idx >> 4, c = idx & 15;
     uint8_t* dst = sA + (c * kTC + r) * 16;
@@ -87,13 +78,56 @@ __global__ __launch_bounds__(128, 1) void lut_umma_kernel(LutArgs a) {
     else *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
   }
   cp_async_commit();
+  // query tile: vector n = b * G + g <-> q row b * Hq + h * G + g; item = (vector, 8-pair chunk)
+#pragma unroll 1
+  for (int it = tid; it < NV * 8; it += 128) {
+    const int n = it >> 3, c = it & 7, vn = vec0 + n;
+    uint16_t h1[8], l1[8], h2[8], l2[8];
+    if (vn < nvec) {
+      float y1[8], y2[8];
+      rotate8(a, (vn / G) * a.Hq + h * G + vn % G, c * 8, y1, y2);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        umma::split_bf16(y1[e], h1[e], l1[e]);
+        umma::split_bf16(y2[e], h2[e], l2[e]);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) h1[e] = l1[e] = h2[e] = l2[e] = 0;
+    }
+    *reinterpret_cast<uint4*>(sB + ((c)*NV + n) * 16) = pack8(h1);        // hi, elements 0..63
+    *reinterpret_cast<uint4*>(sB + ((c + 8) * NV + n) * 16) = pack8(h2);  // hi, elements 64..127
+    *reinterpret_cast<uint4*>(sB + ((c + 16) * NV + n) * 16) = pack8(l1); // lo
+    *reinterpret_cast<uint4*>(sB + ((c + 24) * NV + n) * 16) = pack8(l2);
+  }
   A2ATS_PHASE(g_lut_phase, 1);
-  pdl_wait();  // the query tile comes from qprep_kernel
+  pdl_wait();  // the previous step's attention reads qrot / cs; select reads agg
   pdl_trigger();
-  {
-    const uint8_t* src = a.qB + ((size_t)(h * a.nvt + blockIdx.y) * 32) * NV * 16;
-    for (int i = tid; i < 32 * NV; i += 128) cp_async16(sB + i * 16, src + (size_t)i * 16);
-    cp_async_commit();
+  if (blockIdx.x == 0) {  // q~ fp32 for the attention (bridge rows), this CTA's vectors
+#pragma unroll 1
+    for (int it = tid; it < NV * 8; it += 128) {
+      const int n = it >> 3, c = it & 7, vn = vec0 + n;
+      if (vn >= nvec) continue;
+      const int qrow = (vn / G) * a.Hq + h * G + vn % G;
+      float y1[8], y2[8];
+      rotate8(a, qrow, c * 8, y1, y2);
+      float4* dst = reinterpret_cast<float4*>(a.qrot + (size_t)qrow * kD + c * 8);
+      dst[0] = make_float4(y1[0], y1[1], y1[2], y1[3]);
+      dst[1] = make_float4(y1[4], y1[5], y1[6], y1[7]);
+      dst += kHalf / 4;
+      dst[0] = make_float4(y2[0], y2[1], y2[2], y2[3]);
+      dst[1] = make_float4(y2[4], y2[5], y2[6], y2[7]);
+    }
+  }
+  {  // window relative-rotation table cs[r][m] = (cos, sin)(r f_m) from fp64 angles, spread over the grid
+    const int ncta = gridDim.x * gridDim.y * gridDim.z;
+    const int cta = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+#pragma unroll 1
+    for (int i = cta * 128 + tid; i < a.window * kHalf; i += ncta * 128) {
+      double sn, cn;
+      sincos((double)(i >> 6) * a.rt.inv_freq[i & (kHalf - 1)], &sn, &cn);
+      a.cs[i] = make_float2((float)cn, (float)sn);
+    }
   }
   cp_async_wait<0>();
   umma::fence_proxy_async();
@@ -123,36 +157,34 @@ __global__ __launch_bounds__(128, 1) void lut_umma_kernel(LutArgs a) {
   const int code = code0 + warp * 32 + lane;
   const int nv_here = min(NV, nvec - vec0);
   const bool sum = (a.group_reduce == A2ATS_GROUP_SUM);
-  for (int cb = 0; cb < nv_here; cb += 64) {
-    uint32_t r[4][16];
-#pragma unroll
-    for (int q = 0; q < 4; ++q)  // up to 4 TMEM loads in flight, then one wait
-      if (cb + 16 * q < nv_here) umma::tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + cb + 16 * q, r[q]);
+  // rolled over 16-column blocks: this code runs once per CTA, so its size (I-cache
+  // misses) costs more than the TMEM load latency it would hide when unrolled
+#pragma unroll 1
+  for (int col0 = 0; col0 < nv_here; col0 += 16) {
+    uint32_t r[16];
+    umma::tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + col0, r);
     umma::tmem_wait_ld();
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int col0 = cb + 16 * q;
-      if (col0 >= nv_here || code >= a.L) break;
-      float x[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) x[i] = __uint_as_float(r[q][i]);
+    if (code < a.L) {
       if (a.lut_full) {
+#pragma unroll 1
+        for (int i = 0; i < 16 && vec0 + col0 + i < nvec; ++i) {
+          const int vn = vec0 + col0 + i, b = vn / G, g = vn - b * G;
+          float xi = 0.f;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int vn = vec0 + col0 + i;
-          if (vn < nvec) {
-            const int b = vn / G, g = vn - b * G;
-            a.lut_full[((size_t)b * a.Hq + h * G + g) * a.L + code] = x[i];
-          }
+          for (int j = 0; j < 16; ++j) xi = (j == i) ? __uint_as_float(r[j]) : xi;
+          a.lut_full[((size_t)b * a.Hq + h * G + g) * a.L + code] = xi;
         }
       }
 #pragma unroll
       for (int bb = 0; bb < 16 / G; ++bb) {  // G divides 16, vec0 + col0 is a multiple of G
         const int n0 = vec0 + col0 + bb * G;
         if (n0 < nvec) {
-          float v = x[bb * G];
+          float v = __uint_as_float(r[bb * G]);
 #pragma unroll
-          for (int g = 1; g < G; ++g) v = sum ? v + x[bb * G + g] : fmaxf(v, x[bb * G + g]);
+          for (int g = 1; g < G; ++g) {
+            const float x = __uint_as_float(r[bb * G + g]);
+            v = sum ? v + x : fmaxf(v, x);
+          }
           a.agg[((size_t)(n0 / G) * a.Hkv + h) * a.L + code] = v;
         }
       }
@@ -162,6 +194,13 @@ __global__ __launch_bounds__(128, 1) void lut_umma_kernel(LutArgs a) {
   umma::fence_before();
   __syncthreads();
   if (warp == 0) umma::tmem_dealloc<kTmemCols>(tmem);
+}
+
+template <uint32_t kTmemCols, int G>
+__global__ __launch_bounds__(128, 1) void lut_umma_kernel(LutArgs a) {
+  A2ATS_TL(g_lut_tl, 0);
+  lut_body<kTmemCols, G>(a);
+  A2ATS_TL(g_lut_tl, 1);
 }
 
 // Debug output: scores[b, hq, t] = LUT[b, hq, codes[b, h, t]] for t < n_ctx (Eq. 21).
@@ -203,9 +242,6 @@ cudaError_t launch_lut_g(const LutArgs& a, cudaStream_t st) {
 int lut_tile_nv(int nvec) { return nvec >= 256 ? 256 : ((nvec + 15) / 16) * 16; }  // MMA N: multiple of 16
 
 cudaError_t launch_lut(const LutArgs& a, cudaStream_t st) {
-  const int grid = max(a.B * a.Hq, a.window);
-  cudaError_t e = launch_pdl(qprep_kernel, dim3(grid), dim3(kHalf), 0, st, a);
-  if (e != cudaSuccess) return e;
   switch (a.G) {
     case 1: return launch_lut_g<1>(a, st);
     case 2: return launch_lut_g<2>(a, st);
@@ -223,3 +259,5 @@ cudaError_t launch_scores(const float* lut_full, const uint16_t* codes, float* s
 }  // namespace a2ats
 
 A2ATS_PHASE_EXPORT(a2ats_debug_lut_phases, a2ats::g_lut_phase)
+
+A2ATS_TL_EXPORT(a2ats_debug_lut_timeline, a2ats::g_lut_tl)

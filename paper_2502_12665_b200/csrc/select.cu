@@ -28,6 +28,7 @@
 namespace a2ats {
 
 namespace {
+A2ATS_TL_DECL(g_sel_tl)
 A2ATS_PHASE_DECL(g_sel_phase)
 
 constexpr int kNT = 512;             // threads per CTA
@@ -445,7 +446,7 @@ __device__ uint32_t scan_emit(const SelArgs& a, SelShared& S, const uint32_t* tb
 }
 
 template <int MODE>
-__global__ __launch_bounds__(kNT, 1) void select_kernel(SelArgs a) {
+__device__ __forceinline__ void select_body(const SelArgs& a) {
   extern __shared__ __align__(16) uint32_t sm[];
   __shared__ SelShared S;
   int* cnt = reinterpret_cast<int*>(sm);  // [L]
@@ -576,6 +577,13 @@ __global__ __launch_bounds__(kNT, 1) void select_kernel(SelArgs a) {
 }
 
 template <int MODE>
+__global__ __launch_bounds__(kNT, 1) void select_kernel(SelArgs a) {
+  A2ATS_TL(g_sel_tl, 0);
+  select_body<MODE>(a);
+  A2ATS_TL(g_sel_tl, 1);
+}
+
+template <int MODE>
 cudaError_t launch_mode(const SelArgs& a, int P, cudaStream_t st) {
   const int tbl_words = max(2 * a.L, a.W * 32);
   const int smem = ((tbl_words + 3) / 4 * 4 + 2 * kVPT * kNT) * 4 + kVPT * kNT * 16;
@@ -599,3 +607,5 @@ cudaError_t launch_shard_scan(const SelArgs& a, int P, cudaStream_t st) { return
 }  // namespace a2ats
 
 A2ATS_PHASE_EXPORT(a2ats_debug_select_phases, a2ats::g_sel_phase)
+
+A2ATS_TL_EXPORT(a2ats_debug_select_timeline, a2ats::g_sel_tl)

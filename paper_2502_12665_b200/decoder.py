@@ -1,5 +1,5 @@
 """Convenience owner of the per-model state around the C ABI: the prepared
-codebook term n_j, zero-initialised workspaces, the code array and the running
+codebook terms (n_j, c^_j), zero-initialised workspaces, the code array and the running
 code histogram.  Every method is a single call (or a short sequence of calls)
 into liba2ats.so; no arithmetic of the method happens here."""
 from __future__ import annotations
@@ -19,7 +19,8 @@ class Decoder:
         self.codebook = codebook.contiguous()
         self.H = None if H is None else H.contiguous().float()
         self.nrm = torch.empty((Hkv, L), dtype=torch.float32, device=self.device)
-        _b.a2ats_qavq_prepare(self.shape, self.codebook, self.H, self.nrm, stream)
+        self.chat = torch.empty((Hkv, L, 256), dtype=torch.bfloat16, device=self.device)
+        _b.a2ats_qavq_prepare(self.shape, self.codebook, self.H, self.nrm, self.chat, stream)
         self.ws_enc = torch.zeros(_b.a2ats_build_codes_workspace_bytes(self.shape), dtype=torch.uint8,
                                   device=self.device)
         self.ws_dec = torch.zeros(_b.a2ats_decode_workspace_bytes(self.shape, self.params), dtype=torch.uint8,
@@ -34,7 +35,7 @@ class Decoder:
             self.ws_dec = torch.zeros(need, dtype=torch.uint8, device=self.device)
 
     def encode(self, keys, t_begin: int, t_end: int, update_hist: bool = True, codes=None):
-        _b.a2ats_build_codes(self.shape, keys, t_begin, t_end, self.codebook, self.H, self.nrm,
+        _b.a2ats_build_codes(self.shape, keys, t_begin, t_end, self.chat, self.nrm,
                              self.codes if codes is None else codes, self.hist if update_hist else None,
                              self.ws_enc, self.stream)
 

@@ -46,7 +46,7 @@ def test_sm100a_code_present(lib):
 
 def test_status_strings_and_version(lib):
     from paper_2502_12665_b200 import binding as b
-    assert lib.a2ats_abi_version() == 1
+    assert lib.a2ats_abi_version() == b.ABI_VERSION == 2
     for s in (b.A2ATS_OK, b.A2ATS_EINVAL, b.A2ATS_EUNSUPPORTED, b.A2ATS_EWORKSPACE, b.A2ATS_ECUDA, b.A2ATS_ENCCL):
         assert b.status_string(s).startswith("A2ATS")
 
@@ -85,13 +85,14 @@ def test_validation_without_gpu(lib):
     bad = b.Params(topk=-1).c()
     assert _call_decode(lib, good, bad, 100) == b.A2ATS_EINVAL
     fake = 1 << 20
-    assert lib.a2ats_build_codes(ctypes.byref(good), fake, 10, 5, fake, None, fake, fake, None, fake, 1 << 40,
+    assert lib.a2ats_qavq_prepare(ctypes.byref(good), fake, None, fake, None, None) == b.A2ATS_EINVAL  # no chat
+    assert lib.a2ats_build_codes(ctypes.byref(good), fake, 10, 5, fake, fake, fake, None, fake, 1 << 40,
                                  None) == b.A2ATS_EINVAL
-    assert lib.a2ats_build_codes(ctypes.byref(good), fake, 0, 32769, fake, None, fake, fake, None, fake, 1 << 40,
+    assert lib.a2ats_build_codes(ctypes.byref(good), fake, 0, 32769, fake, fake, fake, None, fake, 1 << 40,
                                  None) == b.A2ATS_EINVAL
-    assert lib.a2ats_build_codes(ctypes.byref(good), fake, 0, 10, fake, None, fake, fake, None, fake, 8,
+    assert lib.a2ats_build_codes(ctypes.byref(good), fake, 0, 10, fake, fake, fake, None, fake, 8,
                                  None) == b.A2ATS_EWORKSPACE
-    assert lib.a2ats_build_codes(ctypes.byref(good), fake, 5, 5, fake, None, fake, fake, None, fake, 1 << 40,
+    assert lib.a2ats_build_codes(ctypes.byref(good), fake, 5, 5, fake, fake, fake, None, fake, 1 << 40,
                                  None) == b.A2ATS_OK     # empty range: nothing to do
 
 

@@ -208,6 +208,40 @@ def test_build_codes_matches_oracle(with_h):
         np.testing.assert_array_equal(got[:, :, :cfg.N], codes_np(inp["z"])[:, :, :cfg.N])
 
 
+@pytest.mark.parametrize("B,T,steps", [(3, 1, 4), (100, 2, 2), (130, 1, 2), (16, 17, 1)])
+def test_build_codes_decode_regime(B, T, steps):
+    """Few keys per head (the decode step; B*T <= 256 runs the codeword-major
+    encoder, 16*17 = 272 the bulk one): codes and running histogram vs the oracle,
+    L = 400 (ragged last codeword tile).  H gets a large antisymmetric part, which
+    leaves (k-c)H(k-c)^T unchanged (x A x^T = 0), so the codes must not move."""
+    cfg = Config("encd", B=B, Hq=2, Hkv=2, d=128, N=64, L=400, K=10)
+    inp = make_inputs(cfg, 141 + B, device="cpu", with_h=True)
+    H = inp["H"]
+    g = torch.Generator().manual_seed(5)
+    R = torch.randn(H.shape, generator=g, dtype=torch.float32) * H.abs().max()
+    H_asym = H + (R - R.transpose(1, 2))
+    dev = {k: (v.cuda() if isinstance(v, torch.Tensor) else v) for k, v in inp.items()}
+    dec = A.Decoder(cfg.B, cfg.Hq, cfg.Hkv, cfg.L, inp["n_max"], dev["codebook"], H_asym.cuda())
+    t0 = 5
+    for s in range(steps):
+        dec.encode(dev["k_cache"], t0 + s * T, t0 + (s + 1) * T)
+    torch.cuda.synchronize()
+    t1 = t0 + steps * T
+    got = codes_np(dec.codes)
+    C = f64(inp["codebook"])
+    for b in range(cfg.B):
+        for h in range(cfg.Hkv):
+            ref = O.qavq_encode(f64(inp["k_cache"][b, h, t0:t1]), C[h], f64(H[h]))
+            np.testing.assert_array_equal(got[b, h, t0:t1], ref)
+            np.testing.assert_array_equal(dec.hist[b, h].cpu().numpy(), np.bincount(ref, minlength=cfg.L))
+    assert (got[:, :, :t0] == 0).all() and (got[:, :, t1:] == 0).all()  # only [t_begin, t_end) written
+    # the workspace is left zeroed (reusable): encode again into a fresh array, same result
+    again = torch.zeros_like(dec.codes)
+    dec.encode(dev["k_cache"], t0, t1, update_hist=False, codes=again)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(codes_np(again)[:, :, t0:t1], got[:, :, t0:t1])
+
+
 def test_build_codes_keys_equal_codewords_and_ties():
     cfg = Config("enc2", B=1, Hq=1, Hkv=1, d=128, N=256, L=128, K=10)
     inp = make_inputs(cfg, 121, device="cpu", with_h=True, family="g1")

@@ -1,0 +1,86 @@
+"""Per-CTA start/end timeline of each kernel of one encode + decode step
+(tuning build liba2ats_phases.so: thread 0 of every CTA records %globaltimer).
+
+    python tools/timeline_probe.py [--config C2] [--iters 3]
+Prints, per kernel, relative to the first CTA start of the step: first/last CTA
+start, first/last CTA end, and the CTA duration quantiles; for the attention, the
+slowest CTAs as (split, pair).
+"""
+import argparse
+import ctypes
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+os.environ.setdefault("A2ATS_LIB", os.path.join(ROOT, "paper_2502_12665_b200", "lib", "liba2ats_phases.so"))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2502_12665_b200 as A  # noqa: E402
+from synth import CONFIGS, make_inputs  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="C2")
+ap.add_argument("--iters", type=int, default=3)
+args = ap.parse_args()
+cfg = CONFIGS[args.config]
+inp = make_inputs(cfg, 5, device="cuda", with_h=True)
+codes = inp["z"].to(torch.uint16)
+hist = torch.zeros((cfg.B, cfg.Hkv, cfg.L), dtype=torch.int32, device="cuda")
+c = codes[:, :, :cfg.N].to(torch.int64)
+hist.scatter_add_(2, c, torch.ones_like(c, dtype=torch.int32))
+dec = A.Decoder(cfg.B, cfg.Hq, cfg.Hkv, cfg.L, inp["n_max"], inp["codebook"], inp["H"], A.Params(topk=cfg.K))
+dec.codes, dec.hist = codes, hist
+scratch = torch.zeros_like(codes)
+out = torch.empty((cfg.B, cfg.Hq, 128), device="cuda")
+lib = A.load()
+KMAX = 8192
+kernels = ["encode", "lut", "select", "attn"]
+fns = {}
+for k in kernels:
+    f = getattr(lib, f"a2ats_debug_{k}_timeline")
+    f.argtypes = [ctypes.POINTER(ctypes.c_ulonglong)]
+    fns[k] = f
+flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+ncta = {}
+for it in range(args.iters):
+    flush.fill_(it)
+    zero = (ctypes.c_ulonglong * (2 * KMAX))()
+    dec.encode(inp["k_cache"], cfg.N - 1, cfg.N, update_hist=False, codes=scratch)
+    dec.step(inp["q"], inp["k_cache"], inp["v_cache"], cfg.N, out=out)
+    torch.cuda.synchronize()
+    tl = {}
+    for k in kernels:
+        buf = (ctypes.c_ulonglong * (2 * KMAX))()
+        fns[k](buf)
+        arr = np.frombuffer(buf, dtype=np.uint64).reshape(KMAX, 2).astype(np.int64)
+        tl[k] = arr
+    if it == 0:
+        continue
+    # CTAs written in this step: end >= start and start after the previous marks
+    t0 = min(int(tl[k][tl[k][:, 0] > 0][:, 0].max()) for k in kernels)  # placeholder, refined below
+    valid = {}
+    for k in kernels:
+        a = tl[k]
+        last = a[:, 0].max()
+        m = (a[:, 0] > last - 2_000_000) & (a[:, 1] >= a[:, 0])  # this step's CTAs (within 2 ms)
+        valid[k] = np.nonzero(m)[0]
+    t0 = min(tl[k][valid[k], 0].min() for k in kernels)
+    print(f"--- iter {it} (us from first CTA start)")
+    for k in kernels:
+        a = tl[k][valid[k]]
+        st, en = (a[:, 0] - t0) / 1e3, (a[:, 1] - t0) / 1e3
+        du = en - st
+        q = np.percentile(du, [0, 50, 90, 100])
+        print(f"{k:7s} ctas {len(a):5d} start {st.min():7.2f}..{st.max():7.2f} end {en.min():7.2f}..{en.max():7.2f}"
+              f"  dur min/med/p90/max {q[0]:6.2f} {q[1]:6.2f} {q[2]:6.2f} {q[3]:6.2f}")
+    a = tl["attn"]
+    idx = valid["attn"]
+    du = (a[idx, 1] - a[idx, 0]) / 1e3
+    order = np.argsort(-du)[:8]
+    # attention grid is (nsplit_max, P): linear id = pair * gridDim.x + split
+    nsx = int(idx.max() + 1) // (cfg.B * cfg.Hkv)
+    print("  slowest attn CTAs (split, pair, us):",
+          [(int(idx[o] % nsx), int(idx[o] // nsx), round(float(du[o]), 2)) for o in order])
+    print("  attn CTA duration by split:", {s: round(float(np.median(du[(idx % nsx) == s])), 2) for s in range(nsx)})
