@@ -112,7 +112,7 @@ def stage_model(cfg, n_ctx: int, k: int):
     return {
         # new keys + prepared codebook c^ (hi|lo bf16) and n_j + codes / histogram updates
         "encode": dict(bytes=P * d * 2 + Hkv * L * (4 * d + 4) + P * (2 + 4), flops=2 * P * L * 2 * d, bound="hbm"),
-        "lut": dict(bytes=Hkv * L * d * 2 + B * Hq * d * 2 + P * L * 4 + B * Hq * d * 4, flops=2 * B * Hq * L * d,
+        "lut": dict(bytes=Hkv * L * d * 2 + B * Hq * d * 2 + P * L * 4 + cfg.window * 64 * 8, flops=2 * B * Hq * L * d,
                     bound="alu"),
         "select": dict(bytes=P * n_cand * 2 + P * keff * 4, flops=0, bound="hbm", tokens=P * n_ctx,
                        aux_bytes=P * L * 4 * 2),

@@ -82,7 +82,7 @@ void derive(const a2ats_shape* s, const a2ats_params* p, int n_ctx, Derived* d) 
 }
 
 struct DecodeWs {
-  size_t qrot, cs, agg, lut, sel, part, actr, cand_keep, pinfo, nsel, total;
+  size_t cs, agg, lut, sel, part, actr, cand_keep, pinfo, nsel, total;
 };
 
 DecodeWs decode_layout(const a2ats_shape* s, const a2ats_params* p) {
@@ -93,7 +93,6 @@ DecodeWs decode_layout(const a2ats_shape* s, const a2ats_params* p) {
   const int GT = G >= 4 ? 4 : G;
   DecodeWs w;
   size_t o = 0;
-  w.qrot = o; o = align_up(o + (size_t)s->B * s->Hq * kD * 4);
   w.cs = o; o = align_up(o + (size_t)p->window * kHalf * 8);
   w.agg = o; o = align_up(o + (size_t)P * s->L * 4);
   w.lut = o; o = align_up(o + (size_t)s->B * s->Hq * s->L * 4);
@@ -126,6 +125,41 @@ void fill_rope(const a2ats_params* p, RopeTab* rt) {
     rt->inv_freq[m] = p->inv_freq ? p->inv_freq[m] : std::pow(p->rope_theta, -2.0 * m / (double)kD);
 }
 
+// bridge rotation R_b: fp64 angles b f_m, fp32 (cos, sin) (reading Q16)
+void fill_bcs(const a2ats_params* p, const RopeTab& rt, float2* bcs) {
+  for (int m = 0; m < kHalf; ++m) {
+    const double ang = (double)p->bridge * rt.inv_freq[m];
+    bcs[m] = make_float2((float)std::cos(ang), (float)std::sin(ang));
+  }
+}
+
+}  // namespace
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+cudaError_t make_tmap_sw128(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  static EncodeTiledFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<EncodeTiledFn>(nullptr);
+    return reinterpret_cast<EncodeTiledFn>(f);
+  }();
+  if (!fn) return cudaErrorNotSupported;
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {cols * 2};
+  const cuuint32_t box[2] = {64, box_rows};
+  const cuuint32_t es[2] = {1, 1};
+  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+namespace {
 // last CUDA failure (code + api.cu line of the launch), for a2ats_last_cuda_error()
 thread_local char g_last_err[160] = "";
 inline int cuda_status(cudaError_t e, int line = __builtin_LINE()) {
@@ -233,6 +267,9 @@ int a2ats_build_codes(const a2ats_shape* shape, const void* keys, int32_t t_begi
   a.Hkv = shape->Hkv;
   a.L = shape->L;
   a.n_max = shape->n_max;
+  CUtensorMap tm;
+  rc = cuda_status(make_tmap_sw128(&tm, chat, (uint64_t)shape->Hkv * shape->L, 2 * kD, encode_codeword_tile()));
+  if (rc) return rc;
   const int ntiles = (shape->L + encode_codeword_tile() - 1) / encode_codeword_tile();
   const int tmax = std::max(1, kEncVcap / shape->B);  // tokens per launch so that B*T <= vcap
   for (int t0 = t_begin; t0 < t_end; t0 += tmax) {
@@ -246,7 +283,7 @@ int a2ats_build_codes(const a2ats_shape* shape, const void* keys, int32_t t_begi
     lsplit = std::max(1, std::min(lsplit, ntiles));
     a.tiles_per_split = (ntiles + lsplit - 1) / lsplit;
     a.lsplit = (ntiles + a.tiles_per_split - 1) / a.tiles_per_split;
-    rc = cuda_status(launch_encode(a, st));
+    rc = cuda_status(launch_encode(a, tm, st));
     if (rc) return rc;
   }
   return A2ATS_OK;
@@ -277,7 +314,6 @@ int a2ats_decode_step(const a2ats_shape* shape, const a2ats_params* params, int3
   derive(shape, params, n_ctx, &d);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   uint8_t* base = static_cast<uint8_t*>(ws);
-  float* qrot = reinterpret_cast<float*>(base + Lw.qrot);
   float2* cs = reinterpret_cast<float2*>(base + Lw.cs);
   float* agg = reinterpret_cast<float*>(base + Lw.agg);
   float* lut_full = scores_out ? reinterpret_cast<float*>(base + Lw.lut) : nullptr;
@@ -289,7 +325,6 @@ int a2ats_decode_step(const a2ats_shape* shape, const a2ats_params* params, int3
   la.codebook = static_cast<const uint16_t*>(codebook);
   la.agg = agg;
   la.lut_full = lut_full;
-  la.qrot = qrot;
   la.cs = cs;
   la.B = shape->B;
   la.Hq = shape->Hq;
@@ -302,12 +337,12 @@ int a2ats_decode_step(const a2ats_shape* shape, const a2ats_params* params, int3
   la.NV = lut_tile_nv(shape->B * d.G);
   la.nvt = (shape->B * d.G + la.NV - 1) / la.NV;
   fill_rope(params, &la.rt);
-  for (int m = 0; m < kHalf; ++m) {  // bridge rotation R_b: fp64 angles, fp32 cos/sin (reading Q16)
-    const double ang = (double)params->bridge * la.rt.inv_freq[m];
-    la.bcs[m] = make_float2((float)std::cos(ang), (float)std::sin(ang));
-  }
+  fill_bcs(params, la.rt, la.bcs);
+  CUtensorMap tm;
+  rc = cuda_status(make_tmap_sw128(&tm, codebook, (uint64_t)shape->Hkv * shape->L, kD, 128));
+  if (rc) return rc;
   stage_mark(0, st);
-  rc = cuda_status(launch_lut(la, st));
+  rc = cuda_status(launch_lut(la, tm, st));
   if (rc) return rc;
   stage_mark(1, st);
 
@@ -345,7 +380,8 @@ int a2ats_decode_step(const a2ats_shape* shape, const a2ats_params* params, int3
   // a5 + a6
   AttnArgs aa;
   aa.q = static_cast<const uint16_t*>(q);
-  aa.qrot = qrot;
+  std::memcpy(aa.bcs, la.bcs, sizeof(aa.bcs));
+  aa.rt = la.rt;
   aa.cs = cs;
   aa.kc = static_cast<const uint16_t*>(k_cache);
   aa.vc = static_cast<const uint16_t*>(v_cache);
@@ -419,7 +455,6 @@ int a2ats_shard_hist(const a2ats_shape* shape, const a2ats_params* params, int32
   la.codebook = static_cast<const uint16_t*>(codebook);
   la.agg = reinterpret_cast<float*>(base + Lw.agg);
   la.lut_full = nullptr;
-  la.qrot = reinterpret_cast<float*>(base + Lw.qrot);
   la.cs = reinterpret_cast<float2*>(base + Lw.cs);
   la.B = shape->B;
   la.Hq = shape->Hq;
@@ -432,11 +467,11 @@ int a2ats_shard_hist(const a2ats_shape* shape, const a2ats_params* params, int32
   la.NV = lut_tile_nv(shape->B * d.G);
   la.nvt = (shape->B * d.G + la.NV - 1) / la.NV;
   fill_rope(params, &la.rt);
-  for (int m = 0; m < kHalf; ++m) {
-    const double ang = (double)params->bridge * la.rt.inv_freq[m];
-    la.bcs[m] = make_float2((float)std::cos(ang), (float)std::sin(ang));
-  }
-  rc = cuda_status(launch_lut(la, st));  // replicated on every rank, bitwise identical
+  fill_bcs(params, la.rt, la.bcs);
+  CUtensorMap tm;
+  rc = cuda_status(make_tmap_sw128(&tm, codebook, (uint64_t)shape->Hkv * shape->L, kD, 128));
+  if (rc) return rc;
+  rc = cuda_status(launch_lut(la, tm, st));  // replicated on every rank, bitwise identical
   if (rc) return rc;
   SelArgs sa{};
   sa.agg = la.agg;
@@ -526,7 +561,8 @@ int a2ats_shard_attend(const a2ats_shape* shape, const a2ats_params* params, int
   const int w_lo = std::max(d.w0, shard_begin), w_hi = std::min(n_ctx, se);
   AttnArgs aa;
   aa.q = static_cast<const uint16_t*>(q);
-  aa.qrot = reinterpret_cast<float*>(base + Lw.qrot);
+  fill_rope(params, &aa.rt);
+  fill_bcs(params, aa.rt, aa.bcs);
   aa.cs = reinterpret_cast<float2*>(base + Lw.cs);
   aa.kc = static_cast<const uint16_t*>(k_cache);
   aa.vc = static_cast<const uint16_t*>(v_cache);

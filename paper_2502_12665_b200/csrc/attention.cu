@@ -28,9 +28,10 @@ constexpr int kWarps = 4;
 constexpr int kStages = 3;
 constexpr int kTileBytes = 16 * 256;           // one K (or V) tile: 16 rows x 256 B
 constexpr int kStageBytes = 2 * kTileBytes;    // K + V
+constexpr int kWinPre = 64;                    // window rows per split whose logits are precomputed
 
 struct SmemLayout {
-  int tok, ring, q, sS, red, total;
+  int tok, ring, q, sS, bcs, sW, red, total;
 };
 __host__ __device__ inline SmemLayout attn_smem(int R) {
   SmemLayout s;
@@ -38,8 +39,10 @@ __host__ __device__ inline SmemLayout attn_smem(int R) {
   s.ring = ((R * 4) + 127) / 128 * 128;
   s.q = s.ring + kWarps * kStages * kStageBytes;     // raw q (scaled) [8][128] fp32 for window tiles
   s.sS = s.q + 8 * kD * 4;                           // window logits [4 warps][16 rows][8 heads]
+  s.bcs = s.sS + kWarps * 16 * 8 * 4;                // bridge (cos, sin) [64] float2
+  s.sW = s.bcs + kHalf * 8;                          // precomputed window logits [64 rows][8 heads]
   s.red = s.ring;                                    // warp partials [4][8 heads][130], after the ring is dead
-  s.total = s.sS + kWarps * 16 * 8 * 4;
+  s.total = s.sW + kWinPre * 8 * 4;
   return s;
 }
 
@@ -79,6 +82,72 @@ __device__ __forceinline__ void split_pair(float x0, float x1, uint32_t& hi, uin
 // byte offset of (row, 16-B chunk) inside a 16 x 256 B tile, XOR swizzle on the chunk
 __device__ __forceinline__ uint32_t swz(int row, int chunk) { return row * 256 + ((chunk ^ (row & 7)) << 4); }
 
+// Logits of the split's first nw (<= 64) window rows, u_j = (q R_{i-j}) . k_j (Eq. 11),
+// in the base-2 scaled domain, into sW[row][8 heads]: an exact per-row rotation on FP32
+// cores, computed from step inputs only (so before the dependency wait when the split's
+// rows are known).  Uses the (still idle) ring as scratch: (cos, sin)(r f_m) [64][64]
+// (fp64 angle at the first row, then fp64 rotation by -f_m per row) and the K rows,
+// both with 16-B chunks XOR-swizzled by row.
+__device__ __forceinline__ void window_logits(const AttnArgs& a, uint8_t* ring, const float* sQ, float* sW,
+                                           const uint8_t* kbase, int nw, int tok0) {
+  const int tid = threadIdx.x, G = a.G;
+  float4* csS = reinterpret_cast<float4*>(ring);          // [64 rows][32 chunks of 2 (cos, sin)]
+  uint4* kS = reinterpret_cast<uint4*>(ring + 32768);     // [64 rows][16 chunks of 8 bf16]
+  for (int i = tid; i < nw * 16; i += 128) {
+    const int row = i >> 4, c = i & 15;
+    kS[row * 16 + (c ^ (row & 7))] = ld_nc_u4(kbase + (size_t)(tok0 + row - a.shard_begin) * 256 + c * 16);
+  }
+  {
+    const int m = tid & 63, j0 = (tid >> 6) * 32;  // rows [j0, j0 + 32) of pair m
+    if (j0 < nw) {
+      const double f = a.rt.inv_freq[m];
+      double sn, cn, sf, cf;
+      sincos((double)(a.n_ctx - 1 - (tok0 + j0)) * f, &sn, &cn);  // r = i - t, t = tok0 + row
+      sincos(f, &sf, &cf);
+      float2* cs2 = reinterpret_cast<float2*>(csS);
+#pragma unroll 1
+      for (int row = j0; row < min(j0 + 32, nw); ++row) {
+        cs2[row * 64 + (((m >> 1) ^ (row & 7)) << 1) + (m & 1)] = make_float2((float)cn, (float)sn);
+        const double c2 = cn * cf + sn * sf, s2 = sn * cf - cn * sf;  // r -> r - 1
+        cn = c2;
+        sn = s2;
+      }
+    }
+  }
+  __syncthreads();
+  const int row = tid & 63, hsel = tid >> 6;  // heads hsel, hsel + 2, ...
+  if (row < nw) {
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 1
+    for (int mb = 0; mb < 8; ++mb) {  // m = 8 mb + i; pairs (m, m + 64)
+      const uint4 k1 = kS[row * 16 + (mb ^ (row & 7))];
+      const uint4 k2 = kS[row * 16 + ((mb + 8) ^ (row & 7))];
+      const uint32_t w1[4] = {k1.x, k1.y, k1.z, k1.w}, w2[4] = {k2.x, k2.y, k2.z, k2.w};
+      float4 t[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) t[j] = csS[row * 32 + ((mb * 4 + j) ^ (row & 7))];
+#pragma unroll
+      for (int hh = 0; hh < 4; ++hh) {
+        const int g = hsel + 2 * hh;
+        if (g < G) {
+          const float* qa = sQ + g * kD + mb * 8;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float ka = (i & 1) ? bf_hi(w1[i >> 1]) : bf_lo(w1[i >> 1]);
+            const float kb = (i & 1) ? bf_hi(w2[i >> 1]) : bf_lo(w2[i >> 1]);
+            const float cv = (i & 1) ? t[i >> 1].z : t[i >> 1].x, sv = (i & 1) ? t[i >> 1].w : t[i >> 1].y;
+            const float q1 = qa[i], q2 = qa[i + kHalf];
+            acc[hh] = fmaf(cv, fmaf(q1, ka, q2 * kb), fmaf(sv, fmaf(q1, kb, -q2 * ka), acc[hh]));
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int hh = 0; hh < 4; ++hh) sW[row * 8 + hsel + 2 * hh] = acc[hh];  // heads >= G: 0
+  }
+  __syncthreads();
+}
+
 __device__ __forceinline__ void attn_body(const AttnArgs& a) {
   extern __shared__ __align__(128) uint8_t smraw[];
   const SmemLayout SL = attn_smem(a.R);
@@ -86,8 +155,6 @@ __device__ __forceinline__ void attn_body(const AttnArgs& a) {
   float* sQ = reinterpret_cast<float*>(smraw + SL.q);
   float* red = reinterpret_cast<float*>(smraw + SL.red);
 
-  pdl_wait();  // sel / counts / q~ come from the two previous kernels
-  pdl_trigger();
   const int split = blockIdx.x, pair = blockIdx.y;
   const int b = pair / a.Hkv, h = pair - b * a.Hkv;
   const int G = a.G;
@@ -95,8 +162,77 @@ __device__ __forceinline__ void attn_body(const AttnArgs& a) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g8 = lane >> 2, t4 = lane & 3;  // mma fragment coordinates
 
+  // step inputs only, before the dependency wait: the query in both forms
+  // q~ (bridge) fragments as the mma B operand: head n = g8, d = 16kk + 2t4 + {0,1} (+8)
+  // q~ = q R_b (Eq. 12) computed here from the bf16 q: the lane's d and d + 64 sit in
+  // fragments kk and kk + 4, so each lane rotates its own pairs (same fp32 formula as the LUT)
+  uint32_t qh[8][2], ql[8][2];
+  {
+    float2* sbcs = reinterpret_cast<float2*>(smraw + SL.bcs);
+    if (tid < kHalf) sbcs[tid] = a.bcs[tid];
+    __syncthreads();
+    const bool valid = g8 < G;
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(a.q + ((size_t)b * a.Hq + hq0 + (valid ? g8 : 0)) * kD);
+    uint32_t qw[8][2];
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk)
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) qw[kk][hf] = valid ? __ldg(src + (kk * 16 + 2 * t4 + 8 * hf) / 2) : 0u;
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        float y1[2], y2[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const float x1 = e ? bf_hi(qw[kk][hf]) : bf_lo(qw[kk][hf]);
+          const float x2 = e ? bf_hi(qw[kk + 4][hf]) : bf_lo(qw[kk + 4][hf]);
+          const float2 cs = sbcs[kk * 16 + 2 * t4 + 8 * hf + e];
+          y1[e] = fmaf(x1, cs.x, -x2 * cs.y) * a.scale_log2;
+          y2[e] = fmaf(x2, cs.x, x1 * cs.y) * a.scale_log2;
+        }
+        split_pair(y1[0], y1[1], qh[kk][hf], ql[kk][hf]);
+        split_pair(y2[0], y2[1], qh[kk + 4][hf], ql[kk + 4][hf]);
+      }
+  }
+
+  {  // raw q (scaled) of the group's heads for the window logits: one 16-B load per thread
+    const int g = tid >> 4, e0 = (tid & 15) * 8;
+    uint4 x = make_uint4(0, 0, 0, 0);
+    if (g < G) x = ld_nc_u4(a.q + ((size_t)b * a.Hq + hq0 + g) * kD + e0);
+    const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+    float4* d = reinterpret_cast<float4*>(sQ + g * kD + e0);
+    d[0] = make_float4(bf_lo(w[0]) * a.scale_log2, bf_hi(w[0]) * a.scale_log2, bf_lo(w[1]) * a.scale_log2,
+                       bf_hi(w[1]) * a.scale_log2);
+    d[1] = make_float4(bf_lo(w[2]) * a.scale_log2, bf_hi(w[2]) * a.scale_log2, bf_lo(w[3]) * a.scale_log2,
+                       bf_hi(w[3]) * a.scale_log2);
+  }
+  const uint8_t* kbase = reinterpret_cast<const uint8_t*>(a.kc) + (size_t)pair * a.n_max * 256;
+  const uint8_t* vbase = reinterpret_cast<const uint8_t*>(a.vc) + (size_t)pair * a.n_max * 256;
+  float* sW = reinterpret_cast<float*>(smraw + SL.sW);
+  // Sel list geometry; known before the wait unless the per-pair count comes from select
+  auto wpre_rows = [&](int keff_) {  // (window rows of this split with precomputed logits, first token)
+    const int M_ = a.n_s + keff_ + a.n_w, p0_ = split * a.R, p1_ = min(p0_ + a.R, M_), pw_ = a.n_s + keff_;
+    const int first = max(p0_, pw_);
+    return make_int2(split * a.R < M_ ? max(0, min(p1_ - first, kWinPre)) : 0, a.win_lo + (first - pw_));
+  };
+  int2 wpre = make_int2(0, 0);
+  if (!a.nsel) {
+    __syncthreads();  // sQ
+    wpre = wpre_rows(a.keff);
+    if (wpre.x > 0) window_logits(a, smraw + SL.ring, sQ, sW, kbase, wpre.x, wpre.y);
+  }
+  pdl_wait();  // sel / counts come from select
+  pdl_trigger();
+
   // Sel list of this pair on this rank: [sinks][top-K rows][window rows], ascending
   const int keff = a.nsel ? __ldcg(a.nsel + pair) : a.keff;
+  if (a.nsel) {
+    __syncthreads();  // sQ
+    wpre = wpre_rows(keff);
+    if (wpre.x > 0) window_logits(a, smraw + SL.ring, sQ, sW, kbase, wpre.x, wpre.y);
+  }
+  const int nwpre = wpre.x;
   const int M = a.n_s + keff + a.n_w;
   const int nsplit = (M + a.R - 1) / a.R;
   if (M == 0) {  // no row of this pair lives on this rank: empty partial (sharded mode only)
@@ -115,10 +251,10 @@ __device__ __forceinline__ void attn_body(const AttnArgs& a) {
   const int nB = (p1 - p0) - nA;             // window rows of this split
   const int gA = (nA + 15) >> 4, gB = (nB + 15) >> 4, ngroups = gA + gB;
 
-  for (int i0 = 0; i0 < p1 - p0; i0 += 4 * 128) {  // 4 index loads in flight per thread
-    int tv[4];
+  for (int i0 = 0; i0 < p1 - p0; i0 += 8 * 128) {  // 8 index loads in flight per thread
+    int tv[8];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < 8; ++j) {
       const int p = p0 + i0 + j * 128 + tid;
       tv[j] = 0;
       if (p < p1) {  // local row index of the K/V arrays
@@ -128,32 +264,26 @@ __device__ __forceinline__ void attn_body(const AttnArgs& a) {
       }
     }
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < 8; ++j)
       if (p0 + i0 + j * 128 + tid < p1) s_tok[i0 + j * 128 + tid] = tv[j];
   }
-  if (nB > 0) {
-    for (int i = tid; i < 8 * kD; i += 128) {
-      const int g = i >> 7, e = i & (kD - 1);
-      sQ[i] = (g < G) ? bf_u16(a.q[((size_t)b * a.Hq + hq0 + g) * kD + e]) * a.scale_log2 : 0.f;
-    }
-  }
+  A2ATS_TL(g_attn_tl, 2);
   __syncthreads();
 
-  const uint8_t* kbase = reinterpret_cast<const uint8_t*>(a.kc) + (size_t)pair * a.n_max * 256;
-  const uint8_t* vbase = reinterpret_cast<const uint8_t*>(a.vc) + (size_t)pair * a.n_max * 256;
   uint8_t* wring = smraw + SL.ring + warp * (kStages * kStageBytes);
   const uint32_t wring_s = smem_u32(wring);
 
-  // tile g of this warp's sequence -> (first local row, row count, is window)
+  // tile g of this warp's sequence -> (first local row, row count, is window).  Window
+  // tiles come first: their FP32 logits then overlap the ring's loads of later tiles.
   auto tile_of = [&](int g, int& r0, int& nr) -> bool {
-    if (g < gA) {
-      r0 = g * 16;
-      nr = min(16, nA - r0);
-      return false;
+    if (g < gB) {
+      r0 = nA + g * 16;
+      nr = min(16, nA + nB - r0);
+      return true;
     }
-    r0 = nA + (g - gA) * 16;
-    nr = min(16, nA + nB - r0);
-    return true;
+    r0 = (g - gB) * 16;
+    nr = min(16, nA - r0);
+    return false;
   };
   auto issue = [&](int s) {
     const int g = s * kWarps + warp;
@@ -161,39 +291,30 @@ __device__ __forceinline__ void attn_body(const AttnArgs& a) {
       int r0, nr;
       const bool win = tile_of(g, r0, nr);
       uint8_t* st = wring + (s % kStages) * kStageBytes;
-      if (win) {  // warm L1 with this lane's (cos, sin) row half (2 x 128 B) for the window logits
+      if (win && r0 - nA >= nwpre) {  // warm L1 with this lane's (cos, sin) row half for the window logits
         const int row = lane >> 1, rr = row < nr ? row : nr - 1;
         const float2* p = a.cs + (size_t)(a.n_ctx - 1 - a.shard_begin - s_tok[r0 + rr]) * kHalf + (lane & 1) * 32;
         asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
         asm volatile("prefetch.global.L1 [%0];" ::"l"(p + 16));
       }
+      // piece idx = lane + 32 i: (kv = i >> 3, row = (lane >> 4) + 2 (i & 7), chunk = lane & 15);
+      // the lane's 8 rows are read from s_tok once, all loads before the first use
+      const int chunk = lane & 15;
+      uint32_t roff[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int row = (lane >> 4) + 2 * j;
+        roff[j] = (uint32_t)s_tok[r0 + (row < nr ? row : nr - 1)];  // pad rows re-read a valid row
+      }
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
-        const int idx = lane + 32 * i;  // 512 pieces: (kv, row, chunk)
-        const int kv = idx >> 8, row = (idx >> 4) & 15, chunk = idx & 15;
-        const int rr = row < nr ? row : nr - 1;  // pad rows re-read a valid row (finite data)
-        const size_t off = (size_t)s_tok[r0 + rr] * 256 + chunk * 16;
+        const int kv = i >> 3, row = (lane >> 4) + 2 * (i & 7);
+        const size_t off = (size_t)roff[i & 7] * 256 + chunk * 16;
         cp_async16(st + kv * kTileBytes + swz(row, chunk), (kv ? vbase : kbase) + off);
       }
     }
     cp_async_commit();
   };
-
-  // q~ (bridge) fragments as the mma B operand: head n = g8, d = 16kk + 2t4 + {0,1} (+8)
-  uint32_t qh[8][2], ql[8][2];
-  {
-    const bool valid = g8 < G;
-    const float* src = a.qrot + ((size_t)b * a.Hq + hq0 + (valid ? g8 : 0)) * kD;
-#pragma unroll
-    for (int kk = 0; kk < 8; ++kk)
-#pragma unroll
-      for (int hf = 0; hf < 2; ++hf) {
-        const int d0 = kk * 16 + 2 * t4 + 8 * hf;
-        const float x0 = valid ? src[d0] * a.scale_log2 : 0.f;
-        const float x1 = valid ? src[d0 + 1] * a.scale_log2 : 0.f;
-        split_pair(x0, x1, qh[kk][hf], ql[kk][hf]);
-      }
-  }
 
   float o[8][4];
 #pragma unroll
@@ -220,47 +341,67 @@ __device__ __forceinline__ void attn_body(const AttnArgs& a) {
 
     float sc[4];
     if (!win) {
-      sc[0] = sc[1] = sc[2] = sc[3] = 0.f;
+      // four independent accumulation chains (hi / lo x even / odd kk), summed at the end
+      float ca[4] = {0.f, 0.f, 0.f, 0.f}, cb[4] = {0.f, 0.f, 0.f, 0.f};
+      float cc[4] = {0.f, 0.f, 0.f, 0.f}, cd[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {
-        uint32_t af[4];
-        ldsm_x4(kst + swz(rr + 8 * (mi & 1), 2 * kk + (mi >> 1)), af);
-        mma16816(sc, af, qh[kk][0], qh[kk][1]);
-        mma16816(sc, af, ql[kk][0], ql[kk][1]);
+      for (int kk = 0; kk < 8; kk += 2) {
+        uint32_t af0[4], af1[4];
+        ldsm_x4(kst + swz(rr + 8 * (mi & 1), 2 * kk + (mi >> 1)), af0);
+        ldsm_x4(kst + swz(rr + 8 * (mi & 1), 2 * (kk + 1) + (mi >> 1)), af1);
+        mma16816(ca, af0, qh[kk][0], qh[kk][1]);
+        mma16816(cb, af1, qh[kk + 1][0], qh[kk + 1][1]);
+        mma16816(cc, af0, ql[kk][0], ql[kk][1]);
+        mma16816(cd, af1, ql[kk + 1][0], ql[kk + 1][1]);
       }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) sc[i] = (ca[i] + cb[i]) + (cc[i] + cd[i]);
+    } else if (r0 - nA < nwpre) {  // window rows with precomputed logits
+      const float* w = sW + (r0 - nA) * 8 + 2 * t4;
+      sc[0] = w[g8 * 8];
+      sc[1] = w[g8 * 8 + 1];
+      sc[2] = w[(g8 + 8) * 8];
+      sc[3] = w[(g8 + 8) * 8 + 1];
     } else {
-      // window rows: exact relative rotation per row on FP32 cores (lane = row, half of the pairs)
+      // further window rows: exact relative rotation per row on FP32 cores (lane = row, half of the pairs)
       const int row = lane >> 1, hf = lane & 1;
       const int rrow = row < nr ? row : nr - 1;
       const int r = icur - s_tok[r0 + rrow];
       const float4* csp = reinterpret_cast<const float4*>(a.cs + (size_t)r * kHalf + hf * 32);
       const uint8_t* krow = wring + (s % kStages) * kStageBytes;
-      // rolled loops: window tiles are few (<= 4 per pair), so code size beats ILP here
-#pragma unroll 1
-      for (int gg = 0; gg < G; ++gg) {
-        float acc = 0.f;
-#pragma unroll 1
-        for (int c = 0; c < 4; ++c) {  // 8 pairs per chunk: m = hf*32 + c*8 + i
-          const int ch1 = hf * 4 + c, ch2 = 8 + hf * 4 + c;
-          const uint4 k1 = *reinterpret_cast<const uint4*>(krow + swz(row, ch1));
-          const uint4 k2 = *reinterpret_cast<const uint4*>(krow + swz(row, ch2));
-          const uint32_t w1[4] = {k1.x, k1.y, k1.z, k1.w}, w2[4] = {k2.x, k2.y, k2.z, k2.w};
-          const float* qa = sQ + gg * kD + hf * 32 + c * 8;
+      // c (8-pair chunk) outer and rolled; per chunk the k and (cos, sin) loads are issued
+      // together, then every head of the group accumulates (heads unrolled up to 8)
+      float acc[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float2 t = reinterpret_cast<const float2*>(csp)[c * 8 + i];
-            const float ka = (i & 1) ? bf_hi(w1[i >> 1]) : bf_lo(w1[i >> 1]);
-            const float kb = (i & 1) ? bf_hi(w2[i >> 1]) : bf_lo(w2[i >> 1]);
-            const float A = fmaf(qa[i], ka, qa[i + kHalf] * kb);
-            const float Bm = fmaf(qa[i], kb, -qa[i + kHalf] * ka);
-            acc = fmaf(t.x, A, fmaf(t.y, Bm, acc));
+      for (int gg = 0; gg < 8; ++gg) acc[gg] = 0.f;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {  // m = hf*32 + c*8 + i
+        const uint4 k1 = *reinterpret_cast<const uint4*>(krow + swz(row, hf * 4 + c));
+        const uint4 k2 = *reinterpret_cast<const uint4*>(krow + swz(row, 8 + hf * 4 + c));
+        float4 t[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) t[j] = __ldg(csp + c * 4 + j);
+        const uint32_t w1[4] = {k1.x, k1.y, k1.z, k1.w}, w2[4] = {k2.x, k2.y, k2.z, k2.w};
+        const float* qa = sQ + hf * 32 + c * 8;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float ka = (i & 1) ? bf_hi(w1[i >> 1]) : bf_lo(w1[i >> 1]);
+          const float kb = (i & 1) ? bf_hi(w2[i >> 1]) : bf_lo(w2[i >> 1]);
+          const float cv = (i & 1) ? t[i >> 1].z : t[i >> 1].x, sv = (i & 1) ? t[i >> 1].w : t[i >> 1].y;
+#pragma unroll
+          for (int gg = 0; gg < 8; ++gg) {
+            if (gg < G) {
+              const float q1 = qa[gg * kD + i], q2 = qa[gg * kD + i + kHalf];
+              acc[gg] = fmaf(cv, fmaf(q1, ka, q2 * kb), fmaf(sv, fmaf(q1, kb, -q2 * ka), acc[gg]));
+            }
           }
         }
-        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-        if (hf == 0) sS[row * 8 + gg] = acc;
       }
-#pragma unroll 1
-      for (int gg = G + hf; gg < 8; gg += 2) sS[row * 8 + gg] = 0.f;  // unused head columns: finite
+#pragma unroll
+      for (int gg = 0; gg < 8; ++gg) {
+        const float v = acc[gg] + __shfl_xor_sync(0xffffffffu, acc[gg], 1);
+        if (hf == 0) sS[row * 8 + gg] = v;  // heads >= G: 0
+      }
       __syncwarp();
       sc[0] = sS[g8 * 8 + 2 * t4];
       sc[1] = sS[g8 * 8 + 2 * t4 + 1];
@@ -306,6 +447,7 @@ __device__ __forceinline__ void attn_body(const AttnArgs& a) {
     }
     __syncwarp();  // every lane done with this ring slot before it is refilled
   }
+  A2ATS_TL(g_attn_tl, 3);
   cp_async_wait<0>();
   __syncthreads();  // all warps out of the ring: it is reused for the warp partials
 
@@ -384,17 +526,38 @@ __device__ __forceinline__ void attn_body(const AttnArgs& a) {
   }
   __syncthreads();
   if (!s_last) return;
+  A2ATS_TL(g_attn_tl, 4);
   __threadfence();
+  // (m, l) of every (head, split) into smem, one load per thread; then, per head, the
+  // o values of all splits with their loads in flight together (fixed split order)
+  float* sML = red;  // the warp partials are consumed
+  for (int i = tid; i < G * nsplit; i += 128) {  // i = gg * nsplit + s; part stride is the max split count
+    const float* src = part + ((size_t)(i / nsplit) * a.nsplit + i % nsplit) * 130;
+    sML[2 * i] = __ldcg(src);
+    sML[2 * i + 1] = __ldcg(src + 1);
+  }
+  __syncthreads();
+#pragma unroll 1
   for (int gg = 0; gg < G; ++gg) {
-    const float* src = part + (size_t)gg * a.nsplit * 130;
+    const float* src = part + (size_t)gg * a.nsplit * 130 + 2 + e;
+    const float* ml = sML + 2 * gg * nsplit;
     float M = -INFINITY;
-    for (int s = 0; s < nsplit; ++s) M = fmaxf(M, __ldcg(src + s * 130));
+    for (int s = 0; s < nsplit; ++s) M = fmaxf(M, ml[2 * s]);
     float num = 0.f, den = 0.f;
-    for (int s = 0; s < nsplit; ++s) {
-      const float ms = __ldcg(src + s * 130);
-      const float sw = (ms == -INFINITY) ? 0.f : exp2f(ms - M);
-      num = fmaf(__ldcg(src + s * 130 + 2 + e), sw, num);
-      den = fmaf(__ldcg(src + s * 130 + 1), sw, den);
+#pragma unroll 1
+    for (int s0 = 0; s0 < nsplit; s0 += 8) {
+      float v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = (s0 + j < nsplit) ? __ldcg(src + (s0 + j) * 130) : 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (s0 + j < nsplit) {
+          const float ms = ml[2 * (s0 + j)];
+          const float sw = (ms == -INFINITY) ? 0.f : exp2f(ms - M);
+          num = fmaf(v[j], sw, num);
+          den = fmaf(ml[2 * (s0 + j) + 1], sw, den);
+        }
+      }
     }
     emit(gg, M, den, num);
   }

@@ -29,7 +29,7 @@ A2ATS_TL_DECL(g_enc_tl)
 constexpr int kCW = 128;   // codewords per tile (MMA M in the cw kernel, MMA N in the bulk kernel)
 constexpr int kTV = 128;   // keys per CTA in the bulk kernel (MMA M)
 constexpr int kRowB = 2 * kD * 2;  // bytes of one prepared codeword row (hi | lo bf16)
-constexpr int kBulkSmem = kTV * kD * 2 + 2 * kCW * kRowB + 2 * kCW * 4;  // A + 2 x B + 2 x n_j
+constexpr int kBulkSmem = 1024 + kTV * kD * 2 + 2 * kCW * kRowB + 2 * kCW * 4;  // align + A + 2 x B + 2 x n_j
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -95,16 +95,22 @@ __device__ __forceinline__ const uint16_t* key_row(const EncArgs& a, int h, int 
   return a.keys + (((size_t)b * a.Hkv + h) * a.n_max + t) * kD;
 }
 
-// Prepared codeword tile [kCW rows][32 chunks: hi 0..15, lo 16..31] -> canonical
-// K-major layout, chunk c of row r at (c * kCW + r) * 16.
-__device__ __forceinline__ void load_chat_tile(const EncArgs& a, int h, int c0, uint8_t* dst, float* sN) {
-  for (int idx = threadIdx.x; idx < kCW * 32; idx += blockDim.x) {
-    const int r = idx >> 5, c = idx & 31;
-    uint8_t* d = dst + (c * kCW + r) * 16;
-    if (c0 + r < a.L) cp_async16(d, a.chat + ((size_t)h * a.L + c0 + r) * (2 * kD) + c * 8);
-    else *reinterpret_cast<uint4*>(d) = make_uint4(0, 0, 0, 0);
-  }
+// Prepared codeword tile: rows h*L + c0 .. (+128) of chat, 4 TMA boxes of 64 columns
+// (c^_hi 0..63, c^_hi 64..127, c^_lo 0..63, c^_lo 64..127) into four SW128 K slabs of
+// 16 KB; one thread issues, completion on tbar.  Rows past the head belong to the
+// next head (or are zero-filled) and are never selected (code < L checks).
+__device__ __forceinline__ void issue_chat_tile(const CUtensorMap& tm, const EncArgs& a, int h, int c0, uint8_t* dst,
+                                                uint64_t* tbar) {
+  umma::mbar_expect_tx(tbar, kCW * kRowB);
+#pragma unroll
+  for (int k4 = 0; k4 < 4; ++k4) umma::tma_load_2d(dst + k4 * (kCW * 128), &tm, 64 * k4, h * a.L + c0, tbar);
+}
+__device__ __forceinline__ void load_nrm(const EncArgs& a, int h, int c0, float* sN) {
   for (int i = threadIdx.x; i < kCW; i += blockDim.x) sN[i] = (c0 + i < a.L) ? __ldg(a.nrm + (size_t)h * a.L + c0 + i) : 0.f;
+}
+// MMA k-step s (16 elements) of a chat tile: slab s / 4, 32 B per step inside the slab
+__device__ __forceinline__ uint64_t chat_desc(uint32_t base, int s) {
+  return umma::sdesc_sw128(base + (s >> 2) * (kCW * 128) + (s & 3) * 32);
 }
 
 // Cross-CTA combine of (ordered dist, code) per key, then the last CTA of the
@@ -134,13 +140,14 @@ __device__ void combine_and_finalize(const EncArgs& a, int h, int v0, int nv, un
 
 // grid (ceil(L / 128), Hkv); nvec <= 256 keys per head, NV = their MMA N (multiple of 16).
 template <uint32_t kCols>
-__device__ __forceinline__ void encode_cw_body(const EncArgs& a, int NV) {
-  extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* sA = smem;                           // [32 chunks][128 codewords][16 B]
+__device__ __forceinline__ void encode_cw_body(const CUtensorMap& tmC, const EncArgs& a, int NV) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;                           // 4 SW128 K slabs [128 codewords][128 B]
   uint8_t* sB = smem + kCW * kRowB;             // [16 chunks][NV keys][16 B]
   float* sN = reinterpret_cast<float*>(sB + NV * kD * 2);                    // [128] n_j
   unsigned long long* red = reinterpret_cast<unsigned long long*>(sN + kCW);  // [4][NV]
-  __shared__ uint64_t mbar;
+  __shared__ uint64_t mbar, tbar;
   __shared__ uint32_t tslot;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int h = blockIdx.y, code0 = blockIdx.x * kCW;
@@ -148,10 +155,12 @@ __device__ __forceinline__ void encode_cw_body(const EncArgs& a, int NV) {
   if (warp == 0) umma::tmem_alloc<kCols>(&tslot);
   if (tid == 0) {
     umma::mbar_init(&mbar, 1);
+    umma::mbar_init(&tbar, 1);
     umma::mbar_fence_init();
+    issue_chat_tile(tmC, a, h, code0, sA, &tbar);  // prepared codewords (offline state)
   }
-  // prepared codewords (offline state) and this step's keys (written before the call)
-  load_chat_tile(a, h, code0, sA, sN);
+  // this step's keys (written before the call) and n_j
+  load_nrm(a, h, code0, sN);
   for (int idx = tid; idx < NV * 16; idx += 128) {
     const int n = idx >> 4, c = idx & 15;
     uint8_t* d = sB + (c * NV + n) * 16;
@@ -168,11 +177,12 @@ __device__ __forceinline__ void encode_cw_body(const EncArgs& a, int NV) {
   pdl_trigger();
   const uint32_t tmem = tslot;
   if (tid == 0) {
+    umma::mbar_wait(&tbar, 0);
     const uint32_t aBase = smem_u32(sA), bBase = smem_u32(sB);
     const uint32_t idesc = umma::idesc_bf16(kCW, NV);
 #pragma unroll
-    for (int s = 0; s < 16; ++s) {  // K = 256: c^_hi chunks 0..15 then c^_lo chunks 16..31, same keys
-      const uint64_t ad = umma::sdesc(aBase + (2 * s) * (kCW * 16), kCW * 16, 128);
+    for (int s = 0; s < 16; ++s) {  // K = 256: c^_hi (slabs 0, 1) then c^_lo (slabs 2, 3), same keys
+      const uint64_t ad = chat_desc(aBase, s);
       const uint64_t bd = umma::sdesc(bBase + (2 * (s & 7)) * (NV * 16), NV * 16, 128);
       umma::mma_bf16(tmem, ad, bd, idesc, s > 0 ? 1u : 0u);
     }
@@ -216,19 +226,20 @@ __device__ __forceinline__ void encode_cw_body(const EncArgs& a, int NV) {
 }
 
 template <uint32_t kCols>
-__global__ __launch_bounds__(128, 1) void encode_cw_kernel(EncArgs a, int NV) {
+__global__ __launch_bounds__(128, 1) void encode_cw_kernel(const __grid_constant__ CUtensorMap tmC, EncArgs a, int NV) {
   A2ATS_TL(g_enc_tl, 0);
-  encode_cw_body<kCols>(a, NV);
+  encode_cw_body<kCols>(tmC, a, NV);
   A2ATS_TL(g_enc_tl, 1);
 }
 
 // grid (ceil(nvec / 128), Hkv, splits); CTA = 128 keys x codeword tiles [tbeg, tend) of 128.
-__global__ __launch_bounds__(128, 1) void encode_bulk_kernel(EncArgs a) {
-  extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* sA = smem;                          // [16 chunks][128 keys][16 B]
-  uint8_t* sB0 = smem + kTV * kD * 2;          // 2 x [32 chunks][128 codewords][16 B]
-  float* sN0 = reinterpret_cast<float*>(sB0 + 2 * kCW * kRowB);  // 2 x [128] n_j
-  __shared__ uint64_t mbar;
+__global__ __launch_bounds__(128, 1) void encode_bulk_kernel(const __grid_constant__ CUtensorMap tmC, EncArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sB0 = smem;                         // 2 x 4 SW128 K slabs [128 codewords][128 B]
+  uint8_t* sA = smem + 2 * kCW * kRowB;        // [16 chunks][128 keys][16 B]
+  float* sN0 = reinterpret_cast<float*>(sA + kTV * kD * 2);  // 2 x [128] n_j
+  __shared__ uint64_t mbar, tbar[2];
   __shared__ uint32_t tslot;
   const int tid = threadIdx.x, warp = tid >> 5;
   const int h = blockIdx.y, split = blockIdx.z;
@@ -239,7 +250,10 @@ __global__ __launch_bounds__(128, 1) void encode_bulk_kernel(EncArgs a) {
   if (warp == 0) umma::tmem_alloc<kCW>(&tslot);
   if (tid == 0) {
     umma::mbar_init(&mbar, 1);
+    umma::mbar_init(&tbar[0], 1);
+    umma::mbar_init(&tbar[1], 1);
     umma::mbar_fence_init();
+    issue_chat_tile(tmC, a, h, tbeg * kCW, sB0, &tbar[0]);
   }
   for (int idx = tid; idx < kTV * 16; idx += 128) {  // keys: exact bf16, canonical K-major
     const int r = idx >> 4, c = idx & 15;
@@ -247,7 +261,7 @@ __global__ __launch_bounds__(128, 1) void encode_bulk_kernel(EncArgs a) {
     if (vec0 + r < a.nvec) cp_async16(d, key_row(a, h, vec0 + r) + c * 8);
     else *reinterpret_cast<uint4*>(d) = make_uint4(0, 0, 0, 0);
   }
-  load_chat_tile(a, h, tbeg * kCW, sB0, sN0);
+  load_nrm(a, h, tbeg * kCW, sN0);
   cp_async_commit();
   pdl_wait();
   pdl_trigger();
@@ -258,24 +272,23 @@ __global__ __launch_bounds__(128, 1) void encode_bulk_kernel(EncArgs a) {
 #pragma unroll 1
   for (int tile = tbeg; tile < tend; ++tile) {
     const int buf = (tile - tbeg) & 1;
-    if (tile + 1 < tend) {
-      load_chat_tile(a, h, (tile + 1) * kCW, sB0 + (buf ^ 1) * (kCW * kRowB), sN0 + (buf ^ 1) * kCW);
-      cp_async_commit();
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
+    if (tile + 1 < tend) {  // the other buffer was released by the previous iteration's barrier
+      if (tid == 0) issue_chat_tile(tmC, a, h, (tile + 1) * kCW, sB0 + (buf ^ 1) * (kCW * kRowB), &tbar[buf ^ 1]);
+      load_nrm(a, h, (tile + 1) * kCW, sN0 + (buf ^ 1) * kCW);
     }
+    cp_async_wait<0>();  // keys (first iteration)
     umma::fence_proxy_async();
     umma::fence_before();
     __syncthreads();
     umma::fence_after();
     const uint32_t tmem = tslot;
     if (tid == 0) {
+      umma::mbar_wait(&tbar[buf], ((tile - tbeg) >> 1) & 1);
       const uint32_t aBase = smem_u32(sA), bBase = smem_u32(sB0 + buf * (kCW * kRowB));
 #pragma unroll
-      for (int s = 0; s < 16; ++s) {  // keys against c^_hi (chunks 0..15), then against c^_lo
+      for (int s = 0; s < 16; ++s) {  // keys against c^_hi (slabs 0, 1), then against c^_lo (2, 3)
         const uint64_t ad = umma::sdesc(aBase + (2 * (s & 7)) * (kTV * 16), kTV * 16, 128);
-        const uint64_t bd = umma::sdesc(bBase + (2 * s) * (kCW * 16), kCW * 16, 128);
+        const uint64_t bd = chat_desc(bBase, s);
         umma::mma_bf16(tmem, ad, bd, idesc, s > 0 ? 1u : 0u);
       }
       umma::commit(&mbar);
@@ -312,8 +325,8 @@ __global__ __launch_bounds__(128, 1) void encode_bulk_kernel(EncArgs a) {
 }
 
 template <uint32_t kCols>
-cudaError_t launch_cw_t(const EncArgs& a, int NV, cudaStream_t st) {
-  const int smem = kCW * kRowB + NV * kD * 2 + kCW * 4 + 4 * NV * 8;
+cudaError_t launch_cw_t(const EncArgs& a, const CUtensorMap& tm, int NV, cudaStream_t st) {
+  const int smem = 1024 + kCW * kRowB + NV * kD * 2 + kCW * 4 + 4 * NV * 8;
   static int smem_set = -1;
   if (smem_set < smem) {
     cudaError_t e = cudaFuncSetAttribute(encode_cw_kernel<kCols>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -321,7 +334,7 @@ cudaError_t launch_cw_t(const EncArgs& a, int NV, cudaStream_t st) {
     smem_set = smem;
   }
   dim3 grid((a.L + kCW - 1) / kCW, a.Hkv);
-  return launch_pdl(encode_cw_kernel<kCols>, grid, dim3(128), smem, st, a, NV);
+  return launch_pdl(encode_cw_kernel<kCols>, grid, dim3(128), smem, st, tm, a, NV);
 }
 }  // namespace
 
@@ -335,13 +348,13 @@ cudaError_t launch_prepare(const uint16_t* codebook, const float* H, float* nrm,
   return cudaGetLastError();
 }
 
-cudaError_t launch_encode(const EncArgs& a, cudaStream_t st) {
+cudaError_t launch_encode(const EncArgs& a, const CUtensorMap& tm, cudaStream_t st) {
   if (a.nvec <= encode_cw_max()) {
     const int NV = (a.nvec + 15) / 16 * 16;
-    if (NV <= 32) return launch_cw_t<32>(a, NV, st);
-    if (NV <= 64) return launch_cw_t<64>(a, NV, st);
-    if (NV <= 128) return launch_cw_t<128>(a, NV, st);
-    return launch_cw_t<256>(a, NV, st);
+    if (NV <= 32) return launch_cw_t<32>(a, tm, NV, st);
+    if (NV <= 64) return launch_cw_t<64>(a, tm, NV, st);
+    if (NV <= 128) return launch_cw_t<128>(a, tm, NV, st);
+    return launch_cw_t<256>(a, tm, NV, st);
   }
   static bool attr_done = false;
   if (!attr_done) {
@@ -351,7 +364,7 @@ cudaError_t launch_encode(const EncArgs& a, cudaStream_t st) {
   }
   const int ntile = (a.L + kCW - 1) / kCW;
   dim3 grid((a.nvec + kTV - 1) / kTV, a.Hkv, (ntile + a.tiles_per_split - 1) / a.tiles_per_split);
-  return launch_pdl(encode_bulk_kernel, grid, dim3(128), kBulkSmem, st, a);
+  return launch_pdl(encode_bulk_kernel, grid, dim3(128), kBulkSmem, st, tm, a);
 }
 
 int encode_codeword_tile() { return kCW; }

@@ -1,6 +1,7 @@
 // Internal declarations shared by the kernels and the C-ABI layer.
 // Product code: never includes anything from oracle/.
 #pragma once
+#include <cuda.h>  // CUtensorMap (type only; the encoder is fetched through the runtime)
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -32,9 +33,9 @@ struct RopeTab {
     return cudaMemcpyFromSymbol(out, arr, 16 * sizeof(long long)) == cudaSuccess ? 0 : -4; \
   }
 // CTA timeline: thread 0 of every CTA records %globaltimer (ns) at its start (0)
-// and end (1); a2ats_debug_<kernel>_timeline() copies [kTlMax][2].
+// and end (1), optional phase marks 2..7; a2ats_debug_<kernel>_timeline() copies [kTlMax][8].
 constexpr int kTlMax = 8192;
-#define A2ATS_TL_DECL(name) __device__ unsigned long long name[kTlMax][2];
+#define A2ATS_TL_DECL(name) __device__ unsigned long long name[kTlMax][8];
 #define A2ATS_TL(arr, i)                                                                       \
   if (threadIdx.x == 0) {                                                                      \
     const unsigned cta_ = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;     \
@@ -44,7 +45,7 @@ constexpr int kTlMax = 8192;
   }
 #define A2ATS_TL_EXPORT(fn, arr)                                                                        \
   extern "C" int fn(unsigned long long* out) {                                                          \
-    return cudaMemcpyFromSymbol(out, arr, sizeof(unsigned long long) * 2 * a2ats::kTlMax) == cudaSuccess ? 0 : -4; \
+    return cudaMemcpyFromSymbol(out, arr, sizeof(unsigned long long) * 8 * a2ats::kTlMax) == cudaSuccess ? 0 : -4; \
   }
 #else
 #define A2ATS_PHASE_DECL(name)
@@ -133,7 +134,6 @@ struct LutArgs {
   const uint16_t* codebook;  // bf16 [Hkv, L, 128]
   float* agg;                // [B, Hkv, L]
   float* lut_full;           // [B, Hq, L] or nullptr (debug scores)
-  float* qrot;               // [B, Hq, 128]   q~ = q R_b
   float2* cs;                // [window, 64]   (cos, sin)(r f_m)
   int B, Hq, Hkv, G, L, window, bridge, group_reduce;
   int NV, nvt;               // query rows per MMA tile (multiple of 16, <= 256), tiles per head
@@ -161,7 +161,6 @@ struct SelArgs {
 
 struct AttnArgs {
   const uint16_t* q;      // bf16 [B, Hq, 128] pre-PE
-  const float* qrot;      // [B, Hq, 128]
   const float2* cs;       // [window, 64]
   const uint16_t* kc;     // bf16 [B, Hkv, n_max, 128]
   const uint16_t* vc;
@@ -177,6 +176,8 @@ struct AttnArgs {
   int n_w, win_lo;        // window [win_lo, win_lo + n_w)
   int shard_begin;        // local row = global - shard_begin
   float scale_log2;       // log2(e) / sqrt(d)
+  float2 bcs[kHalf];      // (cos, sin)(b f_m), from fp64 angles on the host
+  RopeTab rt;             // f_m (fp64) for the window rotations
 };
 
 struct EncArgs {
@@ -191,7 +192,11 @@ struct EncArgs {
 };
 
 // ---------------------------------------------------------------- launchers (return cudaError_t)
-cudaError_t launch_lut(const LutArgs& a, cudaStream_t st);
+// 2D bf16 tensor map [rows, cols] (row pitch cols * 2 B), box (64 elements, box_rows),
+// SWIZZLE_128B: a box lands as the K-major SW128 layout of umma::sdesc_sw128.
+cudaError_t make_tmap_sw128(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
+
+cudaError_t launch_lut(const LutArgs& a, const CUtensorMap& tm_codebook, cudaStream_t st);
 cudaError_t launch_scores(const float* lut_full, const uint16_t* codes, float* scores, int B, int Hq, int Hkv,
                           int G, int L, int n_max, int n_ctx, cudaStream_t st);
 cudaError_t launch_select(const SelArgs& a, int P, cudaStream_t st);
@@ -202,7 +207,7 @@ cudaError_t launch_attention(const AttnArgs& a, int P, int GT, cudaStream_t st);
 cudaError_t launch_combine(const float* parts, int R, int rows, float* out, cudaStream_t st);
 cudaError_t launch_prepare(const uint16_t* codebook, const float* H, float* nrm, uint16_t* chat, int Hkv, int L,
                            cudaStream_t st);
-cudaError_t launch_encode(const EncArgs& a, cudaStream_t st);
+cudaError_t launch_encode(const EncArgs& a, const CUtensorMap& tm_chat, cudaStream_t st);
 
 int sm_count();
 int encode_codeword_tile();

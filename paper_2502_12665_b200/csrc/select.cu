@@ -2,22 +2,23 @@
 //
 // Scores take only L distinct values per (b, KV head) pair (u^_t = LUT[s_t],
 // Eq. 21), so the K-th largest score is found by a count-weighted
-// radix select over the L codewords, not over the N tokens.  One CTA owns one
-// pair:
+// selection over the L codewords, not over the N tokens.  One CTA owns one pair:
 //
-//  1. candidate histogram over codewords: the caller-maintained hist minus the
-//     sink/window codes (the code stream is then read exactly once), or,
-//     without hist, an extra pass over the codes;
-//  2. count-weighted selection of the K-th largest agg level v*: a weighted
-//     histogram over 256 equal-width key bins finds the bin holding the K-th
-//     token, its (few) codewords are compacted and the exact key is resolved by
-//     single-warp radix passes; tie quota m = K - #{agg > v*};
+//  1. candidate counts per codeword: the caller-maintained hist minus the
+//     sink/window codes, or (without hist) a pass over the candidate codes.  Both
+//     read only step inputs, so they run before the dependency wait (overlapping
+//     the LUT kernel), as does the prefetch of the first chunk of codes;
+//  2. keys = ~ordered(agg) and their range; a weighted histogram over 256
+//     equal-width value bins finds the bin holding the K-th token; its (few)
+//     codewords are compacted and the exact K-th key v* is resolved by ranking
+//     them (one thread per survivor; radix passes if there are very many); tie
+//     quota m = K - #{agg > v*};
 //  3. 2-bit class per codeword (1: agg > v*, 2: agg == v*), replicated 32x in
 //     shared memory so lane l reads bank l (conflict-free gather by code);
-//  4. stream the codes chunk by chunk (prefetched into registers), classify each
-//     token, and write the selected indices in ascending order (block scan +
-//     running prefix).  A token with agg == v* is kept iff fewer than m such
-//     tokens precede it: the lowest-index tie-break of reading Q12.
+//  4. stream the codes: each thread classifies 64 consecutive tokens, one block
+//     scan gives every thread its output offset, and the selected indices are
+//     written in ascending order.  A token with agg == v* is kept iff fewer than
+//     m such tokens precede it: the lowest-index tie-break of reading Q12.
 //
 // The same phases serve the sequence-sharded step: shard_hist
 // (local candidate histogram), shard_thresh (v*, m from the all-reduced
@@ -33,62 +34,45 @@ A2ATS_PHASE_DECL(g_sel_phase)
 
 constexpr int kNT = 512;             // threads per CTA
 constexpr int kNW = kNT / 32;
-constexpr int kVPT = 8;              // 128-bit code loads per thread per chunk
-constexpr int kCH = kNT * kVPT * 8;  // tokens per chunk (32768)
-constexpr int kSurvCap = 2048;       // survivor list capacity of the single-warp radix passes
+constexpr int kTPT = 64;             // consecutive tokens per thread per chunk
+constexpr int kCH = kNT * kTPT;      // tokens per chunk (32768: 16-bit scan fields cannot carry)
+constexpr int kSurvCap = 2048;       // survivor list capacity
+constexpr int kRankMax = kNT;        // survivors ranked directly (one thread each)
 
 enum SelMode { kFused = 0, kShardHist = 1, kShardThresh = 2, kShardScan = 3 };
 
-__device__ __forceinline__ uint32_t spread16(uint32_t v) {
-  v &= 0xffffu;
-  v = (v | (v << 8)) & 0x00ff00ffu;
-  v = (v | (v << 4)) & 0x0f0f0f0fu;
-  v = (v | (v << 2)) & 0x33333333u;
-  v = (v | (v << 1)) & 0x55555555u;
-  return v;
-}
-
 struct SelShared {
   int bins[256];
-  uint32_t cls[1024];    // compact 2-bit classes (W <= 1024)
-  uint32_t wsum[kVPT][kNW];
-  uint32_t wsum_total;
+  uint32_t wsum[kNW];
   uint32_t skey[kSurvCap];
   int scnt[kSurvCap];
-  int s_digit, s_kk, s_nsurv;
-  uint32_t s_and, s_or, s_kstar, s_m;
-  uint32_t s_run[2];
+  int s_digit, s_kk, s_nsurv, s_total;
+  uint32_t s_kmin, s_kmax, s_kstar, s_m;
+  int s_gt, s_eq;
 };
 
-// Load the per-codeword candidate counts and ordered keys of one pair into smem.
-//   cnt[l] = hist[l] - #(local sink/window tokens with code l)   (hist given)
-//          = #(local candidate tokens with code l)                (otherwise)
-// key[l] = ~ordered(agg[l]) (ascending key = descending agg).
-__device__ void load_counts(const SelArgs& a, int pair, int* cnt, uint32_t* key, const uint16_t* cp_local) {
+// cnt[l] = hist[l] - #(local sink/window tokens with code l)   (hist given)
+//        = #(local candidate tokens with code l)                (otherwise)
+// Step inputs only (hist, codes).
+__device__ void load_cnt(const SelArgs& a, int pair, int* cnt, const uint16_t* cp_local) {
   const int tid = threadIdx.x;
-  const float* aggp = a.agg + (size_t)pair * a.L;
   const int32_t* histp = a.hist ? a.hist + (size_t)pair * a.L : nullptr;
-  for (int base = 0; base < a.L; base += 8 * kNT) {  // all loads of a batch in flight before use
-    float av[8];
-    int hv[8];
+  const int lo = a.shard_begin, hi = a.shard_begin + a.shard_len;  // local global-index range
+  if (histp) {
+    for (int base = 0; base < a.L; base += 8 * kNT) {  // all loads of a batch in flight before use
+      int hv[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int l = base + i * kNT + tid;
-      av[i] = l < a.L ? __ldg(aggp + l) : 0.f;
-      hv[i] = (histp && l < a.L) ? __ldg(histp + l) : 0;
-    }
+      for (int i = 0; i < 8; ++i) {
+        const int l = base + i * kNT + tid;
+        hv[i] = l < a.L ? __ldg(histp + l) : 0;
+      }
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int l = base + i * kNT + tid;
-      if (l < a.L) {
-        cnt[l] = hv[i];
-        key[l] = ~ordered_key(av[i]);
+      for (int i = 0; i < 8; ++i) {
+        const int l = base + i * kNT + tid;
+        if (l < a.L) cnt[l] = hv[i];
       }
     }
-  }
-  __syncthreads();
-  const int lo = a.shard_begin, hi = a.shard_begin + a.shard_len;  // local global-index range
-  if (a.hist) {
+    __syncthreads();
     // remove the local sinks [0, n_s) and window [w0, n_ctx): they are not candidates
     const int nrem = a.n_s + (a.n_ctx - a.w0);
     for (int i = tid; i < nrem; i += kNT) {
@@ -96,6 +80,8 @@ __device__ void load_counts(const SelArgs& a, int pair, int* cnt, uint32_t* key,
       if (t >= lo && t < hi) atomicSub(&cnt[cp_local[t - lo]], 1);
     }
   } else {
+    for (int l = tid; l < a.L; l += kNT) cnt[l] = 0;
+    __syncthreads();
     const int c0 = max(a.c0, lo), c1 = min(a.c1, hi);
     if (c0 < c1) {
       const int v0 = (c0 - lo) >> 3, v1 = (c1 - lo + 7) >> 3;
@@ -109,6 +95,46 @@ __device__ void load_counts(const SelArgs& a, int pair, int* cnt, uint32_t* key,
         }
       }
     }
+  }
+  __syncthreads();
+}
+
+// key[l] = ~ordered(agg[l]) (ascending key = descending agg) and the key range of the
+// codewords with cnt > 0 -> S.s_kmin / S.s_kmax.  Needs cnt (synced); ends synced.
+__device__ void load_keys(const SelArgs& a, SelShared& S, int pair, const int* cnt, uint32_t* key) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  const float* aggp = a.agg + (size_t)pair * a.L;
+  if (tid == 0) {
+    S.s_kmin = 0xffffffffu;
+    S.s_kmax = 0u;
+  }
+  uint32_t kmn = 0xffffffffu, kmx = 0u;
+  for (int base = 0; base < a.L; base += 8 * kNT) {
+    float av[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int l = base + i * kNT + tid;
+      av[i] = l < a.L ? __ldcg(aggp + l) : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int l = base + i * kNT + tid;
+      if (l < a.L) {
+        const uint32_t k = ~ordered_key(av[i]);
+        key[l] = k;
+        if (cnt[l] > 0) {
+          kmn = min(kmn, k);
+          kmx = max(kmx, k);
+        }
+      }
+    }
+  }
+  kmn = __reduce_min_sync(0xffffffffu, kmn);
+  kmx = __reduce_max_sync(0xffffffffu, kmx);
+  __syncthreads();  // s_kmin / s_kmax initialised
+  if (lane == 0) {
+    atomicMin(&S.s_kmin, kmn);
+    atomicMax(&S.s_kmax, kmx);
   }
   __syncthreads();
 }
@@ -145,39 +171,12 @@ __device__ __forceinline__ void pick_digit(SelShared& S, int kk) {
   __syncwarp();
 }
 
-// Count-weighted selection of the keff-th smallest key over cnt/key (all threads).
-// Result in S.s_kstar (key of v*) and S.s_m (tie quota, >= 1).
-__device__ void radix_kth(const SelArgs& a, SelShared& S, const int* cnt, const uint32_t* key, int keff) {
-  // 1. key range of the candidates; 2. weighted histogram over 256 equal-width key
-  //    bins (monotone in the key, so in agg) to find the bin holding the K-th
-  //    token; 3. compact that bin's codewords (typically tens) and resolve the
-  //    exact K-th key with single-warp radix passes over them.  Few block barriers:
-  //    this runs once per CTA on the critical path.
+// Count-weighted selection of the keff-th smallest key over cnt / key (all threads),
+// given the key range S.s_kmin..S.s_kmax.  Result in S.s_kstar (key of v*) and
+// S.s_m (tie quota, >= 1).
+__device__ void find_level(const SelArgs& a, SelShared& S, const int* cnt, const uint32_t* key, int keff) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) {
-    S.s_and = 0xffffffffu;  // min key
-    S.s_or = 0u;            // max key
-    S.s_nsurv = 0;
-  }
-  for (int i = tid; i < 256; i += kNT) S.bins[i] = 0;
-  __syncthreads();
-  uint32_t kmn = 0xffffffffu, kmx = 0u;
-  for (int l = tid; l < a.L; l += kNT) {
-    if (cnt[l] > 0) {
-      kmn = min(kmn, key[l]);
-      kmx = max(kmx, key[l]);
-    }
-  }
-  kmn = __reduce_min_sync(0xffffffffu, kmn);
-  kmx = __reduce_max_sync(0xffffffffu, kmx);
-  if (lane == 0) {
-    atomicMin(&S.s_and, kmn);
-    atomicMax(&S.s_or, kmx);
-  }
-  __syncthreads();
-  A2ATS_PHASE(g_sel_phase, 2);
-  kmn = S.s_and;
-  kmx = S.s_or;
+  const uint32_t kmn = S.s_kmin, kmx = S.s_kmax;
   if (kmn == kmx) {  // a single level holds every candidate
     if (tid == 0) {
       S.s_kstar = kmn;
@@ -186,9 +185,11 @@ __device__ void radix_kth(const SelArgs& a, SelShared& S, const int* cnt, const 
     __syncthreads();
     return;
   }
+  for (int i = tid; i < 256; i += kNT) S.bins[i] = 0;
+  if (tid == 0) S.s_nsurv = 0;
+  __syncthreads();
   // 256 bins of equal width in agg VALUE over [amin, amax], ascending bin = descending
   // agg (monotone and deterministic: one subtract, one multiply, one truncation).
-  // Equal-width bins in key space would be one binade wide and hold hundreds of codes.
   auto key_val = [](uint32_t k) {
     const uint32_t o = ~k;  // ordered key
     return __uint_as_float((o & 0x80000000u) ? (o & 0x7fffffffu) : ~o);
@@ -209,33 +210,46 @@ __device__ void radix_kth(const SelArgs& a, SelShared& S, const int* cnt, const 
   A2ATS_PHASE(g_sel_phase, 3);
   const int bstar = S.s_digit;
   int kk = S.s_kk;
-  {
-    // survivors = candidate codewords of bin b*; one shared atomic per warp
-    int nkeep = 0;
-    for (int l0 = 0; l0 < a.L; l0 += kNT) {
-      const int l = l0 + tid;
-      nkeep += __popc(__ballot_sync(0xffffffffu, l < a.L && cnt[l] > 0 && bin_of(key[l]) == bstar));
-    }
-    int base = 0;
-    if (lane == 0 && nkeep) base = atomicAdd(&S.s_nsurv, nkeep);
-    base = __shfl_sync(0xffffffffu, base, 0);
-    for (int l0 = 0; l0 < a.L; l0 += kNT) {
-      const int l = l0 + tid;
-      const bool keep = l < a.L && cnt[l] > 0 && bin_of(key[l]) == bstar;
-      const unsigned bal = __ballot_sync(0xffffffffu, keep);
-      if (keep) {
-        const int slot = base + __popc(bal & ((1u << lane) - 1u));
-        if (slot < kSurvCap) {
-          S.skey[slot] = key[l];
-          S.scnt[slot] = cnt[l];
-        }
+  // survivors = candidate codewords of bin b*, one pass (order is irrelevant below)
+  for (int l0 = 0; l0 < a.L; l0 += kNT) {
+    const int l = l0 + tid;
+    const bool keep = l < a.L && cnt[l] > 0 && bin_of(key[l]) == bstar;
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (bal) {
+      int base = 0;
+      if (lane == 0) base = atomicAdd(&S.s_nsurv, __popc(bal));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      const int slot = base + __popc(bal & ((1u << lane) - 1u));
+      if (keep && slot < kSurvCap) {
+        S.skey[slot] = key[l];
+        S.scnt[slot] = cnt[l];
       }
-      base += __popc(bal);
     }
   }
   __syncthreads();
   A2ATS_PHASE(g_sel_phase, 4);
   const int nsurv = S.s_nsurv;
+  if (nsurv <= kRankMax) {
+    // rank each survivor directly: v* is the key with #(< v*) < kk <= #(<= v*);
+    // equal keys write equal values
+    if (tid < nsurv) {
+      const uint32_t ki = S.skey[tid];
+      int less = 0, leq = 0;
+#pragma unroll 4
+      for (int j = 0; j < nsurv; ++j) {
+        const uint32_t kj = S.skey[j];
+        const int cj = S.scnt[j];
+        less += (kj < ki) ? cj : 0;
+        leq += (kj <= ki) ? cj : 0;
+      }
+      if (less < kk && kk <= leq) {
+        S.s_kstar = ki;
+        S.s_m = (uint32_t)(kk - less);
+      }
+    }
+    __syncthreads();
+    return;
+  }
   if (nsurv <= kSurvCap) {
     if (warp == 0) {
       // exact K-th key among the survivors: radix passes from their first differing bit
@@ -301,148 +315,169 @@ __device__ void radix_kth(const SelArgs& a, SelShared& S, const int* cnt, const 
   __syncthreads();
 }
 
-// 2-bit classes vs kstar, compact then replicated 32x into tbl (may alias key/cnt).
-__device__ void build_table(const SelArgs& a, SelShared& S, const uint32_t* key, uint32_t kstar, uint32_t* tbl) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int gi = warp; gi < (a.L + 31) / 32; gi += kNW) {
-    const int l = gi * 32 + lane;
-    uint32_t c = 0;
-    if (l < a.L) {
-      const uint32_t k = key[l];
-      c = (k < kstar) ? 1u : ((k == kstar) ? 2u : 0u);
+// 2-bit classes vs kstar, replicated 32x into tbl[word * 32 + replica] (tbl may alias
+// key / cnt: every word is computed into registers before the first write).  One
+// thread per word (W <= 1024); the 16-B chunks are visited in a per-thread rotated
+// order so a quarter-warp touches distinct banks.
+__device__ void build_table(const SelArgs& a, const uint32_t* key, uint32_t kstar, uint32_t* tbl) {
+  const int tid = threadIdx.x;
+  constexpr int kMaxItems = 2;  // words tid and tid + 512
+  uint32_t word[kMaxItems];
+#pragma unroll
+  for (int j = 0; j < kMaxItems; ++j) {
+    const int w = j * kNT + tid;
+    uint32_t x = 0;
+    if (w < a.W) {
+      if (w * 16 + 16 <= a.L) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int qq = (q + w) & 3;
+          const uint4 k4 = *reinterpret_cast<const uint4*>(key + w * 16 + 4 * qq);
+          const uint32_t kv[4] = {k4.x, k4.y, k4.z, k4.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const uint32_t c = (kv[e] < kstar) ? 1u : ((kv[e] == kstar) ? 2u : 0u);
+            x |= c << (2 * (4 * qq + e));
+          }
+        }
+      } else {
+#pragma unroll 1
+        for (int e = 0; e < 16 && w * 16 + e < a.L; ++e) {
+          const uint32_t k = key[w * 16 + e];
+          x |= ((k < kstar) ? 1u : ((k == kstar) ? 2u : 0u)) << (2 * e);
+        }
+      }
     }
-    const uint32_t gtm = __ballot_sync(0xffffffffu, c == 1u);
-    const uint32_t eqm = __ballot_sync(0xffffffffu, c == 2u);
-    if (lane < 2 && gi * 2 + lane < a.W) {
-      const uint32_t g16 = lane ? (gtm >> 16) : gtm, e16 = lane ? (eqm >> 16) : eqm;
-      S.cls[gi * 2 + lane] = spread16(g16) | (spread16(e16) << 1);
+    word[j] = x;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kMaxItems; ++j) {
+    const int w = j * kNT + tid;
+    if (w < a.W) {
+      uint4* dst = reinterpret_cast<uint4*>(tbl + w * 32);
+      const uint4 v = make_uint4(word[j], word[j], word[j], word[j]);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) dst[(q + w) & 7] = v;
     }
   }
   __syncthreads();
-  for (int i = tid; i < a.W * 32; i += kNT) tbl[i] = S.cls[i >> 5];
-  __syncthreads();
 }
 
-// Stream the local candidate codes, emit the selected token indices (global) in
-// ascending order: every token above v*, plus the first m tied tokens.
-// v[] holds the prefetched first chunk.  Returns the number emitted.
+// cp.async one chunk of local codes into sC: coalesced 16-B global pieces; thread t's
+// 8 pieces (its 64 consecutive tokens) land at t*8 + (i ^ (t & 7)) (conflict-free reads).
+__device__ __forceinline__ void prefetch_chunk(const SelArgs& a, const uint16_t* cp_local, int cb, int c1, uint4* sC) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lo = a.shard_begin;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int u = j * 32 + lane;                   // piece within the warp's 256
+    const int owner = warp * 32 + (u >> 3), i = u & 7;
+    const int t0 = cb + (warp * 256 + u) * 8;      // first token of the piece (global index)
+    uint4* dst = sC + owner * 8 + (i ^ (owner & 7));
+    if (t0 < c1) cp_async16(dst, cp_local + (t0 - lo));
+    else *dst = make_uint4(0, 0, 0, 0);  // codes past the range must be valid (< L)
+  }
+  cp_async_commit();
+}
+
+__device__ __forceinline__ uint32_t span_mask(int lo, int hi) {  // 2-bit fields [lo, hi) of 16
+  lo = max(lo, 0);
+  hi = min(hi, 16);
+  if (hi <= lo) return 0u;
+  const uint32_t mh = hi >= 16 ? 0xffffffffu : ((1u << (2 * hi)) - 1u);
+  const uint32_t ml = (1u << (2 * lo)) - 1u;
+  return mh & ~ml;
+}
+
+// Stream the local candidate codes (first chunk already prefetched into sC) and emit
+// the selected global token indices in ascending order: every token above v*, plus
+// the first m tied tokens.  Returns the number emitted.
 __device__ uint32_t scan_emit(const SelArgs& a, SelShared& S, const uint32_t* tbl, const uint16_t* cp_local, int c0,
-                              int c1, uint32_t m, uint32_t cap, int32_t* selp, const uint4* sC, uint32_t* sPk,
-                              uint32_t* sIn) {
-  // Compact loops throughout (no full unrolling): this code runs once per CTA, and
-  // straight-line SASS of that size stalls on instruction fetch.
+                              int c1, uint32_t m, uint32_t cap, int32_t* selp, uint4* sC) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int lo = a.shard_begin;
   const int first = lo + (((c0 - lo) >> 3) << 3);  // 8-aligned (local index) start
   const int nchunk = c1 > c0 ? (c1 - first + kCH - 1) / kCH : 0;
-  if (tid == 0) {
-    S.s_run[0] = 0;
-    S.s_run[1] = 0;
-  }
+  uint32_t run_gt = 0, run_eq = 0;
+#pragma unroll 1
   for (int ch = 0; ch < nchunk; ++ch) {
     const int cb = first + ch * kCH;
-    cp_async_wait<0>();  // this chunk's codes (prefetched with cp.async) are in sC
-    __syncthreads();
+    cp_async_wait<0>();
+    __syncthreads();  // this chunk is in sC; the previous chunk is fully consumed
+    const int t0 = cb + tid * kTPT;
+    // classify the thread's 64 tokens, 16 per pass (rolled: straight-line code of this
+    // size stalls on instruction fetch); p0..p3 = passes 0..3 after the register shift
+    uint32_t p0 = 0u, p1 = 0u, p2 = 0u, p3 = 0u;
 #pragma unroll 1
-    for (int j = 0; j < kVPT; ++j) {
-      const int t0 = cb + (j * kNT + tid) * 8;
-      const uint4 x = sC[j * kNT + tid];
-      const uint32_t w[4] = {x.x, x.y, x.z, x.w};
-      uint32_t p = 0;
+    for (int k = 0; k < 4; ++k) {
+      const uint4 xa = sC[tid * 8 + ((2 * k) ^ (tid & 7))];
+      const uint4 xb = sC[tid * 8 + ((2 * k + 1) ^ (tid & 7))];
+      const uint32_t w[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+      uint32_t cur = 0u;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
+      for (int e = 0; e < 16; ++e) {
         const uint32_t code = (w[e >> 1] >> ((e & 1) * 16)) & 0xffffu;
         const uint32_t word = tbl[((code >> 4) << 5) + lane];
-        p |= ((word >> ((code & 15u) * 2u)) & 3u) << (2 * e);
+        cur |= ((word >> ((code & 15u) * 2u)) & 3u) << (2 * e);
       }
-      if (t0 < c0 || t0 + 8 > c1) {
-        uint32_t mk = 0;
-#pragma unroll
-        for (int e = 0; e < 8; ++e)
-          if (t0 + e >= c0 && t0 + e < c1) mk |= 3u << (2 * e);
-        p &= mk;
-      }
-      const uint32_t pk = (uint32_t)__popc(p & 0x5555u) | ((uint32_t)__popc(p & 0xaaaau) << 16);
-      uint32_t x2 = pk;
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, x2, off);
-        if (lane >= off) x2 += y;
-      }
-      if (lane == 31) S.wsum[j][warp] = x2;
-      sPk[j * kNT + tid] = p;
-      sIn[j * kNT + tid] = x2 - pk;  // exclusive within the warp
+      const int tb = t0 + 16 * k;
+      if (tb < c0 || tb + 16 > c1) cur &= span_mask(c0 - tb, c1 - tb);
+      p0 = p1;
+      p1 = p2;
+      p2 = p3;
+      p3 = cur;
     }
+    const uint32_t p[4] = {p0, p1, p2, p3};
+    uint32_t pk = 0;
+#pragma unroll
+    for (int w = 0; w < 4; ++w)
+      pk += (uint32_t)__popc(p[w] & 0x55555555u) | ((uint32_t)__popc(p[w] & 0xaaaaaaaau) << 16);
+    uint32_t incl = pk;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += y;
+    }
+    if (lane == 31) S.wsum[warp] = incl;
     __syncthreads();
-    if (ch + 1 < nchunk) {  // sC is free: prefetch the next chunk during scan + emission
-      for (int j = 0; j < kVPT; ++j) {
-        const int t0 = cb + kCH + (j * kNT + tid) * 8;
-        if (t0 < c1) cp_async16(const_cast<uint4*>(sC) + j * kNT + tid, cp_local + (t0 - lo));
-        else const_cast<uint4*>(sC)[j * kNT + tid] = make_uint4(0, 0, 0, 0);
-      }
-      cp_async_commit();
+    if (ch + 1 < nchunk) prefetch_chunk(a, cp_local, cb + kCH, c1, sC);  // sC is free
+    uint32_t pre = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < kNW; ++w) {
+      const uint32_t v = S.wsum[w];
+      pre += (w < warp) ? v : 0u;
+      tot += v;
     }
-    if (warp == 0) {
-      // exclusive scan of the kVPT*kNW warp totals in (j, warp) order; the 16-bit
-      // fields do not carry: a chunk holds 32768 tokens
-      constexpr int NTOT = kVPT * kNW;
-      constexpr int PER = (NTOT + 31) / 32;
-      uint32_t loc[PER], s = 0;
-#pragma unroll
-      for (int i = 0; i < PER; ++i) {
-        const int idx = lane * PER + i;
-        loc[i] = idx < NTOT ? S.wsum[idx / kNW][idx % kNW] : 0u;
-        s += loc[i];
-      }
-      uint32_t inc = s;
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, off);
-        if (lane >= off) inc += y;
-      }
-      uint32_t run = inc - s;
-#pragma unroll
-      for (int i = 0; i < PER; ++i) {
-        const int idx = lane * PER + i;
-        if (idx < NTOT) S.wsum[idx / kNW][idx % kNW] = run;
-        run += loc[i];
-      }
-      if (lane == 31) S.wsum_total = run;  // chunk totals
-    }
-    __syncthreads();
-    const uint32_t rgt = S.s_run[0], req = S.s_run[1];
+    const uint32_t ex = pre + incl - pk;  // 16-bit fields: a chunk holds <= 32768 tokens
+    uint32_t gb = run_gt + (ex & 0xffffu), eb = run_eq + (ex >> 16);
+    uint32_t e0 = p[0], e1 = p[1], e2 = p[2], e3 = p[3];
 #pragma unroll 1
-    for (int j = 0; j < kVPT; ++j) {
-      uint32_t p = sPk[j * kNT + tid];
-      if (p == 0) continue;
-      const uint32_t ex = S.wsum[j][warp] + sIn[j * kNT + tid];
-      uint32_t gb = rgt + (ex & 0xffffu), eb = req + (ex >> 16);
-      const int t0 = cb + (j * kNT + tid) * 8;
-      while (p) {  // selected / tied tokens in increasing token order
-        const int e = (__ffs(p) - 1) >> 1;
-        const uint32_t c = (p >> (2 * e)) & 3u;
-        p &= ~(3u << (2 * e));
+    for (int w = 0; w < 4; ++w) {
+      uint32_t q = e0;
+      e0 = e1;
+      e1 = e2;
+      e2 = e3;
+      while (q) {  // selected / tied tokens in increasing token order
+        const int bit = __ffs(q) - 1, j = bit >> 1;
+        q &= ~(3u << (2 * j));
+        const int t = t0 + 16 * w + j;
         // (positions are < cap by construction; the bound only guards against a
         //  caller-supplied hist that is inconsistent with the codes)
-        if (c == 1u) {
+        if ((bit & 1) == 0) {  // class 1: above v*
           const uint32_t pos = gb + min(eb, m);
-          if (pos < cap) selp[pos] = t0 + e;
+          if (pos < cap) selp[pos] = t;
           ++gb;
-        } else {
-          if (eb < m && gb + eb < cap) selp[gb + eb] = t0 + e;
+        } else {  // class 2: tied at v*
+          if (eb < m && gb + eb < cap) selp[gb + eb] = t;
           ++eb;
         }
       }
     }
-    __syncthreads();
-    if (tid == 0) {
-      const uint32_t tot = S.wsum_total;
-      S.s_run[0] = rgt + (tot & 0xffffu);
-      S.s_run[1] = req + (tot >> 16);
-    }
+    run_gt += tot & 0xffffu;
+    run_eq += tot >> 16;
   }
-  __syncthreads();
-  return S.s_run[0] + min(S.s_run[1], m);
+  return run_gt + min(run_eq, m);
 }
 
 template <int MODE>
@@ -450,12 +485,10 @@ __device__ __forceinline__ void select_body(const SelArgs& a) {
   extern __shared__ __align__(16) uint32_t sm[];
   __shared__ SelShared S;
   int* cnt = reinterpret_cast<int*>(sm);  // [L]
-  uint32_t* key = sm + a.L;               // [L]
+  uint32_t* key = sm + ((a.L + 3) & ~3);  // [L], 16-B aligned
   uint32_t* tbl = sm;                     // [W*32], aliases cnt/key once they are dead
-  const int tbl_words = max(2 * a.L, a.W * 32);
-  uint32_t* sPk = sm + (tbl_words + 3) / 4 * 4;    // [kVPT][kNT] token classes
-  uint32_t* sIn = sPk + kVPT * kNT;                // [kVPT][kNT] warp-exclusive counts
-  uint4* sC = reinterpret_cast<uint4*>(sIn + kVPT * kNT);  // [kVPT * kNT] one chunk of codes
+  const int tbl_words = max(((a.L + 3) & ~3) + a.L, a.W * 32);
+  uint4* sC = reinterpret_cast<uint4*>(sm + (tbl_words + 3) / 4 * 4);  // [kCH / 8] one chunk of codes
 
   const int tid = threadIdx.x;
   const int pair = blockIdx.x;
@@ -464,12 +497,10 @@ __device__ __forceinline__ void select_body(const SelArgs& a) {
   const int c0 = max(a.c0, lo), c1 = min(a.c1, hi);             // local part of the candidate range
   A2ATS_PHASE(g_sel_phase, 0);
 
-  if (MODE == kShardHist || MODE == kShardThresh) {
+  if (MODE == kShardHist) {
+    load_cnt(a, pair, cnt, cp_local);
     pdl_wait();
     pdl_trigger();
-  }
-  if (MODE == kShardHist) {
-    load_counts(a, pair, cnt, key, cp_local);
     for (int l = tid; l < a.L; l += kNT) {
       a.cand_out[(size_t)pair * a.L + l] = cnt[l];
       a.cand_keep[(size_t)pair * a.L + l] = cnt[l];
@@ -477,25 +508,22 @@ __device__ __forceinline__ void select_body(const SelArgs& a) {
     return;
   }
   if (MODE == kShardThresh) {
+    pdl_wait();
+    pdl_trigger();
     // cnt <- all-reduced histogram; key from agg
-    const float* aggp = a.agg + (size_t)pair * a.L;
-    for (int l = tid; l < a.L; l += kNT) {
-      cnt[l] = a.cand_in[(size_t)pair * a.L + l];
-      key[l] = ~ordered_key(__ldg(aggp + l));
-    }
+    for (int l = tid; l < a.L; l += kNT) cnt[l] = a.cand_in[(size_t)pair * a.L + l];
+    if (tid == 0) S.s_total = 0;
     __syncthreads();
+    load_keys(a, S, pair, cnt, key);
     int total = 0;
     for (int l = tid; l < a.L; l += kNT) total += max(cnt[l], 0);
     total = __reduce_add_sync(0xffffffffu, total);
-    __shared__ int s_total;
-    if (tid == 0) s_total = 0;
+    if ((tid & 31) == 0) atomicAdd(&S.s_total, total);
     __syncthreads();
-    if ((tid & 31) == 0) atomicAdd(&s_total, total);
-    __syncthreads();
-    const int keff = min(a.keff, s_total);
+    const int keff = min(a.keff, S.s_total);
     uint32_t kstar = 0, m = 0;
     if (keff > 0) {
-      radix_kth(a, S, cnt, key, keff);
+      find_level(a, S, cnt, key, keff);
       kstar = S.s_kstar;
       m = S.s_m;
     }
@@ -510,51 +538,45 @@ __device__ __forceinline__ void select_body(const SelArgs& a) {
     }
     gt = __reduce_add_sync(0xffffffffu, gt);
     eq = __reduce_add_sync(0xffffffffu, eq);
-    __shared__ int s_gt, s_eq;
-    if (tid == 0) s_gt = s_eq = 0;
+    if (tid == 0) S.s_gt = S.s_eq = 0;
     __syncthreads();
     if ((tid & 31) == 0) {
-      atomicAdd(&s_gt, gt);
-      atomicAdd(&s_eq, eq);
+      atomicAdd(&S.s_gt, gt);
+      atomicAdd(&S.s_eq, eq);
     }
     __syncthreads();
     if (tid == 0) {
       a.pinfo[pair * 4 + 0] = kstar;
       a.pinfo[pair * 4 + 1] = m;
       a.pinfo[pair * 4 + 2] = (uint32_t)keff;
-      a.counts_out[pair * 2 + 0] = s_gt;
-      a.counts_out[pair * 2 + 1] = s_eq;
+      a.counts_out[pair * 2 + 0] = S.s_gt;
+      a.counts_out[pair * 2 + 1] = S.s_eq;
     }
     return;
   }
 
-  // kFused / kShardScan: prefetch the first chunk of local candidate codes (cp.async -> sC)
+  // kFused / kShardScan: step inputs first (overlapping the previous kernel's tail):
+  // the first chunk of local candidate codes, and (fused) the candidate counts
   const int first = lo + (((c0 - lo) >> 3) << 3);
-  for (int j = 0; j < kVPT; ++j) {
-    const int t0 = first + (j * kNT + tid) * 8;
-    if (c0 < c1 && t0 < c1) cp_async16(sC + j * kNT + tid, cp_local + (t0 - lo));
-    else sC[j * kNT + tid] = make_uint4(0, 0, 0, 0);  // codes past the range must be valid (< L)
-  }
-  cp_async_commit();
+  if (c0 < c1) prefetch_chunk(a, cp_local, first, c1, sC);
+  if (MODE == kFused) load_cnt(a, pair, cnt, cp_local);
   A2ATS_PHASE(g_sel_phase, 1);
-  // the code prefetch above overlaps the predecessor's tail (codes are step inputs)
-  pdl_wait();
+  pdl_wait();  // agg comes from the LUT kernel
   pdl_trigger();
   uint32_t kstar, m, cap;
-  int32_t* selp;
+  int32_t* selp = a.sel + (size_t)pair * a.sel_stride;
   if (MODE == kFused) {
-    load_counts(a, pair, cnt, key, cp_local);
-    A2ATS_PHASE(g_sel_phase, 6);
-    radix_kth(a, S, cnt, key, a.keff);
-    A2ATS_PHASE(g_sel_phase, 7);
+    load_keys(a, S, pair, cnt, key);
+    A2ATS_PHASE(g_sel_phase, 2);
+    find_level(a, S, cnt, key, a.keff);
+    A2ATS_PHASE(g_sel_phase, 5);
     kstar = S.s_kstar;
     m = S.s_m;
     cap = (uint32_t)a.keff;
-    selp = a.sel + (size_t)pair * a.sel_stride;
   } else {
     // shard scan: key from agg, v*/m from shard_thresh, this rank's tie quota from the gather
     const float* aggp = a.agg + (size_t)pair * a.L;
-    for (int l = tid; l < a.L; l += kNT) key[l] = ~ordered_key(__ldg(aggp + l));
+    for (int l = tid; l < a.L; l += kNT) key[l] = ~ordered_key(__ldcg(aggp + l));
     kstar = a.pinfo[pair * 4 + 0];
     const int mg = (int)a.pinfo[pair * 4 + 1];
     const int keffg = (int)a.pinfo[pair * 4 + 2];
@@ -565,15 +587,17 @@ __device__ __forceinline__ void select_body(const SelArgs& a) {
     m = keffg > 0 ? (uint32_t)min(max(mg - eq_before, 0), eq_r) : 0u;
     cap = keffg > 0 ? (uint32_t)(gt_r + (int)m) : 0u;
     if (keffg == 0) kstar = 0u;  // nothing above key 0 except impossible keys: emit nothing
-    selp = a.sel + (size_t)pair * a.sel_stride;
     if (tid == 0) a.nsel_out[pair] = (int)cap;
     __syncthreads();
   }
-  build_table(a, S, key, kstar, tbl);
-  A2ATS_PHASE(g_sel_phase, 8);
-  if (MODE == kShardScan && cap == 0) return;
-  scan_emit(a, S, tbl, cp_local, c0, c1, m, cap, selp, sC, sPk, sIn);
-  A2ATS_PHASE(g_sel_phase, 9);
+  build_table(a, key, kstar, tbl);
+  A2ATS_PHASE(g_sel_phase, 6);
+  if (MODE == kShardScan && cap == 0) {
+    cp_async_wait<0>();
+    return;
+  }
+  scan_emit(a, S, tbl, cp_local, c0, c1, m, cap, selp, sC);
+  A2ATS_PHASE(g_sel_phase, 7);
 }
 
 template <int MODE>
@@ -585,8 +609,8 @@ __global__ __launch_bounds__(kNT, 1) void select_kernel(SelArgs a) {
 
 template <int MODE>
 cudaError_t launch_mode(const SelArgs& a, int P, cudaStream_t st) {
-  const int tbl_words = max(2 * a.L, a.W * 32);
-  const int smem = ((tbl_words + 3) / 4 * 4 + 2 * kVPT * kNT) * 4 + kVPT * kNT * 16;
+  const int tbl_words = max(((a.L + 3) & ~3) + a.L, a.W * 32);
+  const int smem = (tbl_words + 3) / 4 * 4 * 4 + kCH * 2;
   static int smem_set = -1;
   if (smem_set < smem) {
     cudaError_t e = cudaFuncSetAttribute(select_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -607,5 +631,4 @@ cudaError_t launch_shard_scan(const SelArgs& a, int P, cudaStream_t st) { return
 }  // namespace a2ats
 
 A2ATS_PHASE_EXPORT(a2ats_debug_select_phases, a2ats::g_sel_phase)
-
 A2ATS_TL_EXPORT(a2ats_debug_select_timeline, a2ats::g_sel_tl)

@@ -25,6 +25,21 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo_bytes, ui
   return d;
 }
 
+// K-major SWIZZLE_128B descriptor (the layout a TMA load with CU_TENSOR_MAP_SWIZZLE_128B
+// and a 64-element (128 B) inner box writes): row r of a 64-wide K slab at r * 128 B,
+// its 16-B chunks XOR-permuted by (r & 7); 8-row groups 1024 B apart (SBO), LBO
+// unused (1), layout type 2 at [61,64).  The slab base must be 1024-B aligned; the
+// k-th 16-element MMA step inside a slab starts at base + 32 k bytes.
+__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3fffu);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
 // Instruction descriptor, kind::f16: D fp32, A/B bf16, both K-major, M x N.
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
@@ -63,6 +78,25 @@ __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t phase) {
       "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(a),
       "r"(phase)
       : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* mbar, uint32_t bytes) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(mbar));
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+
+// ---- TMA: 2D tiled load of box (x = inner element, y = row) into smem, completion on mbar
+__device__ __forceinline__ void tma_load_2d(void* smem_dst, const void* tmap, int x, int y, uint64_t* mbar) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
+  const uint32_t m = static_cast<uint32_t>(__cvta_generic_to_shared(mbar));
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+          "r"(d),
+      "l"(tmap), "r"(x), "r"(y), "r"(m)
+      : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_desc(const void* tmap) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
 }
 
 // ---- TMEM

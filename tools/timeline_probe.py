@@ -46,15 +46,14 @@ flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
 ncta = {}
 for it in range(args.iters):
     flush.fill_(it)
-    zero = (ctypes.c_ulonglong * (2 * KMAX))()
     dec.encode(inp["k_cache"], cfg.N - 1, cfg.N, update_hist=False, codes=scratch)
     dec.step(inp["q"], inp["k_cache"], inp["v_cache"], cfg.N, out=out)
     torch.cuda.synchronize()
     tl = {}
     for k in kernels:
-        buf = (ctypes.c_ulonglong * (2 * KMAX))()
+        buf = (ctypes.c_ulonglong * (8 * KMAX))()
         fns[k](buf)
-        arr = np.frombuffer(buf, dtype=np.uint64).reshape(KMAX, 2).astype(np.int64)
+        arr = np.frombuffer(buf, dtype=np.uint64).reshape(KMAX, 8).astype(np.int64)
         tl[k] = arr
     if it == 0:
         continue
@@ -84,3 +83,14 @@ for it in range(args.iters):
     print("  slowest attn CTAs (split, pair, us):",
           [(int(idx[o] % nsx), int(idx[o] // nsx), round(float(du[o]), 2)) for o in order])
     print("  attn CTA duration by split:", {s: round(float(np.median(du[(idx % nsx) == s])), 2) for s in range(nsx)})
+    # phase marks: 2 = index prologue done (after the dependency wait), 3 = main loop done,
+    # 4 = last-arriver combine start (only the last CTA of a pair)
+    for sp in range(nsx):
+        rows = a[idx[(idx % nsx) == sp]]
+        pro = np.median((rows[:, 2] - rows[:, 0]) / 1e3)
+        loop = np.median((rows[:, 3] - rows[:, 2]) / 1e3)
+        tail = np.median((rows[:, 1] - rows[:, 3]) / 1e3)
+        last = rows[rows[:, 4] > rows[:, 0]]
+        comb = np.median((last[:, 1] - last[:, 4]) / 1e3) if len(last) else float("nan")
+        print(f"  split {sp}: start->prologue {pro:.2f}  loop {loop:.2f}  loop->end {tail:.2f}  "
+              f"last-arrivers {len(last)} combine {comb:.2f} us")
