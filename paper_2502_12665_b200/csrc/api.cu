@@ -27,12 +27,21 @@ namespace {
 constexpr size_t kAlign = 256;
 inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
-// Rows of the Sel list handled by one attention CTA (fixed per shape so the
-// workspace size does not depend on n_ctx).
-#ifndef A2ATS_ATTN_ROWS
-#define A2ATS_ATTN_ROWS 1024  // measured on B200 at C2: 256 -> 68 us, 512 -> 55 us, 1024 -> 49 us
-#endif
-constexpr int kAttnRows = A2ATS_ATTN_ROWS;
+// Rows of the Sel list handled by one attention CTA (one 8-warp CTA per SM).  Fixed
+// per (shape, params) -- not per n_ctx -- so the workspace size is too: with enough
+// (b, KV head) pairs to fill the GPU a pair is one CTA (no cross-CTA combine) up to
+// kAttnRowsMax rows; with few pairs the rows are split so the grid covers the SMs.
+constexpr int kAttnRowsMax = 2048;  // s_tok capacity of the attention smem layout
+int attn_rows(int P, long long mmax) {
+  const int sms = sm_count();
+  const long long want = (4LL * P >= 3LL * sms) ? 1 : (sms + P - 1) / P;  // splits per pair
+  long long R = (mmax + want - 1) / want;
+  R = (R + 15) / 16 * 16;
+  return (int)std::max<long long>(256, std::min<long long>(kAttnRowsMax, R));
+}
+long long attn_mmax(const a2ats_shape* s, const a2ats_params* p) {
+  return std::min<long long>(p->topk, s->n_max) + p->n_sink + p->window;
+}
 
 struct Derived {
   int G, P, n_w, w0, n_s, c0, c1, n_cand, keff, M;
@@ -74,7 +83,7 @@ void derive(const a2ats_shape* s, const a2ats_params* p, int n_ctx, Derived* d) 
   d->n_cand = d->c1 - d->c0;
   d->keff = std::min(p->topk, d->n_cand);
   d->M = d->n_s + d->keff + d->n_w;
-  d->R = kAttnRows;
+  d->R = attn_rows(d->P, attn_mmax(s, p));
   d->nsplit = (d->M + d->R - 1) / d->R;
   d->GT = d->G >= 4 ? 4 : d->G;
   d->nz = d->G / d->GT;
@@ -88,8 +97,9 @@ struct DecodeWs {
 DecodeWs decode_layout(const a2ats_shape* s, const a2ats_params* p) {
   const int G = s->Hq / s->Hkv, P = s->B * s->Hkv;
   const long long kmax = std::min<long long>(p->topk, s->n_max);
-  const long long mmax = kmax + p->n_sink + p->window;
-  const long long nsplit_max = (mmax + kAttnRows - 1) / kAttnRows;
+  const long long mmax = attn_mmax(s, p);
+  const int R = attn_rows(P, mmax);
+  const long long nsplit_max = (mmax + R - 1) / R;
   const int GT = G >= 4 ? 4 : G;
   DecodeWs w;
   size_t o = 0;

@@ -7,7 +7,7 @@
 //
 // HBM-bound gather: every selected K/V row (2 x 256 B, scattered) is read once
 // and shared by the G query heads of the GQA group.  One CTA = (row split,
-// pair); 4 warps; a warp owns 16-row tiles.  Rows are gathered with cp.async
+// pair); 8 warps (one CTA per SM); a warp owns 16-row tiles.  Rows are gathered with cp.async
 // (16 B pieces, XOR-swizzled so ldmatrix is conflict-free) into a warp-private
 // ring of kStages tiles.  The per-tile contractions S = K_tile Q~^T (16 rows x
 // G heads x 128) and O^T += V_tile^T P (128 x G x 16) use mma.sync m16n8k16
@@ -24,7 +24,8 @@ namespace a2ats {
 
 namespace {
 A2ATS_TL_DECL(g_attn_tl)
-constexpr int kWarps = 4;
+constexpr int kWarps = 8;
+constexpr int kThreads = kWarps * 32;
 constexpr int kStages = 3;
 constexpr int kTileBytes = 16 * 256;           // one K (or V) tile: 16 rows x 256 B
 constexpr int kStageBytes = 2 * kTileBytes;    // K + V
@@ -93,12 +94,12 @@ __device__ __forceinline__ void window_logits(const AttnArgs& a, uint8_t* ring, 
   const int tid = threadIdx.x, G = a.G;
   float4* csS = reinterpret_cast<float4*>(ring);          // [64 rows][32 chunks of 2 (cos, sin)]
   uint4* kS = reinterpret_cast<uint4*>(ring + 32768);     // [64 rows][16 chunks of 8 bf16]
-  for (int i = tid; i < nw * 16; i += 128) {
+  for (int i = tid; i < nw * 16; i += kThreads) {
     const int row = i >> 4, c = i & 15;
     kS[row * 16 + (c ^ (row & 7))] = ld_nc_u4(kbase + (size_t)(tok0 + row - a.shard_begin) * 256 + c * 16);
   }
   {
-    const int m = tid & 63, j0 = (tid >> 6) * 32;  // rows [j0, j0 + 32) of pair m
+    const int m = tid & 63, j0 = (tid >> 6) * 16;  // rows [j0, j0 + 16) of pair m
     if (j0 < nw) {
       const double f = a.rt.inv_freq[m];
       double sn, cn, sf, cf;
@@ -106,7 +107,7 @@ __device__ __forceinline__ void window_logits(const AttnArgs& a, uint8_t* ring, 
       sincos(f, &sf, &cf);
       float2* cs2 = reinterpret_cast<float2*>(csS);
 #pragma unroll 1
-      for (int row = j0; row < min(j0 + 32, nw); ++row) {
+      for (int row = j0; row < min(j0 + 16, nw); ++row) {
         cs2[row * 64 + (((m >> 1) ^ (row & 7)) << 1) + (m & 1)] = make_float2((float)cn, (float)sn);
         const double c2 = cn * cf + sn * sf, s2 = sn * cf - cn * sf;  // r -> r - 1
         cn = c2;
@@ -115,9 +116,9 @@ __device__ __forceinline__ void window_logits(const AttnArgs& a, uint8_t* ring, 
     }
   }
   __syncthreads();
-  const int row = tid & 63, hsel = tid >> 6;  // heads hsel, hsel + 2, ...
+  const int row = tid & 63, hsel = tid >> 6;  // heads hsel, hsel + 4
   if (row < nw) {
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    float acc[2] = {0.f, 0.f};
 #pragma unroll 1
     for (int mb = 0; mb < 8; ++mb) {  // m = 8 mb + i; pairs (m, m + 64)
       const uint4 k1 = kS[row * 16 + (mb ^ (row & 7))];
@@ -127,8 +128,8 @@ __device__ __forceinline__ void window_logits(const AttnArgs& a, uint8_t* ring, 
 #pragma unroll
       for (int j = 0; j < 4; ++j) t[j] = csS[row * 32 + ((mb * 4 + j) ^ (row & 7))];
 #pragma unroll
-      for (int hh = 0; hh < 4; ++hh) {
-        const int g = hsel + 2 * hh;
+      for (int hh = 0; hh < 2; ++hh) {
+        const int g = hsel + 4 * hh;
         if (g < G) {
           const float* qa = sQ + g * kD + mb * 8;
 #pragma unroll
@@ -143,7 +144,7 @@ __device__ __forceinline__ void window_logits(const AttnArgs& a, uint8_t* ring, 
       }
     }
 #pragma unroll
-    for (int hh = 0; hh < 4; ++hh) sW[row * 8 + hsel + 2 * hh] = acc[hh];  // heads >= G: 0
+    for (int hh = 0; hh < 2; ++hh) sW[row * 8 + hsel + 4 * hh] = acc[hh];  // heads >= G: 0
   }
   __syncthreads();
 }
@@ -196,7 +197,7 @@ __device__ __forceinline__ void attn_body(const AttnArgs& a) {
       }
   }
 
-  {  // raw q (scaled) of the group's heads for the window logits: one 16-B load per thread
+  if (tid < 128) {  // raw q (scaled) of the group's heads for the window logits: one 16-B load per thread
     const int g = tid >> 4, e0 = (tid & 15) * 8;
     uint4 x = make_uint4(0, 0, 0, 0);
     if (g < G) x = ld_nc_u4(a.q + ((size_t)b * a.Hq + hq0 + g) * kD + e0);
@@ -237,7 +238,7 @@ __device__ __forceinline__ void attn_body(const AttnArgs& a) {
   const int nsplit = (M + a.R - 1) / a.R;
   if (M == 0) {  // no row of this pair lives on this rank: empty partial (sharded mode only)
     if (split == 0 && a.part_out) {
-      for (int i = tid; i < G * 130; i += 128) {
+      for (int i = tid; i < G * 130; i += kThreads) {
         const int gg = i / 130, f = i - gg * 130;
         a.part_out[((size_t)b * a.Hq + hq0 + gg) * 130 + f] = (f == 0) ? -INFINITY : 0.f;
       }
@@ -251,11 +252,11 @@ __device__ __forceinline__ void attn_body(const AttnArgs& a) {
   const int nB = (p1 - p0) - nA;             // window rows of this split
   const int gA = (nA + 15) >> 4, gB = (nB + 15) >> 4, ngroups = gA + gB;
 
-  for (int i0 = 0; i0 < p1 - p0; i0 += 8 * 128) {  // 8 index loads in flight per thread
+  for (int i0 = 0; i0 < p1 - p0; i0 += 8 * kThreads) {  // 8 index loads in flight per thread
     int tv[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const int p = p0 + i0 + j * 128 + tid;
+      const int p = p0 + i0 + j * kThreads + tid;
       tv[j] = 0;
       if (p < p1) {  // local row index of the K/V arrays
         if (p < a.n_s) tv[j] = a.sink_lo + p - a.shard_begin;
@@ -265,7 +266,7 @@ __device__ __forceinline__ void attn_body(const AttnArgs& a) {
     }
 #pragma unroll
     for (int j = 0; j < 8; ++j)
-      if (p0 + i0 + j * 128 + tid < p1) s_tok[i0 + j * 128 + tid] = tv[j];
+      if (p0 + i0 + j * kThreads + tid < p1) s_tok[i0 + j * kThreads + tid] = tv[j];
   }
   A2ATS_TL(g_attn_tl, 2);
   __syncthreads();
@@ -474,8 +475,8 @@ __device__ __forceinline__ void attn_body(const AttnArgs& a) {
   }
   __syncthreads();
 
-  // combine the 4 warps: thread tid -> element e = tid
-  const int e = tid;
+  // combine the warps: thread tid -> element e = tid % 128 of heads tid / 128, + 2, ...
+  const int e = tid & (kD - 1), gsel = tid >> 7;
   // final result of a pair: normalised output, or (sharded mode) the rank's partial
   // (m, l, o) in the base-2 logit domain for the cross-rank LSE combine
   auto emit = [&](int gg, float M, float den, float num) {
@@ -492,7 +493,7 @@ __device__ __forceinline__ void attn_body(const AttnArgs& a) {
   };
   float* part = a.part + (size_t)pair * G * a.nsplit * 130;  // stride: max splits
   const bool single = (nsplit == 1);
-  for (int gg = 0; gg < G; ++gg) {
+  for (int gg = gsel; gg < G; gg += kThreads / kD) {
     float M = -INFINITY;
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) M = fmaxf(M, red[(w * 8 + gg) * 130]);
@@ -531,14 +532,14 @@ __device__ __forceinline__ void attn_body(const AttnArgs& a) {
   // (m, l) of every (head, split) into smem, one load per thread; then, per head, the
   // o values of all splits with their loads in flight together (fixed split order)
   float* sML = red;  // the warp partials are consumed
-  for (int i = tid; i < G * nsplit; i += 128) {  // i = gg * nsplit + s; part stride is the max split count
+  for (int i = tid; i < G * nsplit; i += kThreads) {  // i = gg * nsplit + s; part stride is the max split count
     const float* src = part + ((size_t)(i / nsplit) * a.nsplit + i % nsplit) * 130;
     sML[2 * i] = __ldcg(src);
     sML[2 * i + 1] = __ldcg(src + 1);
   }
   __syncthreads();
 #pragma unroll 1
-  for (int gg = 0; gg < G; ++gg) {
+  for (int gg = gsel; gg < G; gg += kThreads / kD) {
     const float* src = part + (size_t)gg * a.nsplit * 130 + 2 + e;
     const float* ml = sML + 2 * gg * nsplit;
     float M = -INFINITY;
@@ -564,7 +565,7 @@ __device__ __forceinline__ void attn_body(const AttnArgs& a) {
   if (tid == 0) a.counter[pair] = 0u;  // leave the workspace in its zero state
 }
 
-__global__ __launch_bounds__(128, 2) void attn_mma_kernel(AttnArgs a) {
+__global__ __launch_bounds__(kThreads, 1) void attn_mma_kernel(AttnArgs a) {
   A2ATS_TL(g_attn_tl, 0);
   attn_body(a);
   A2ATS_TL(g_attn_tl, 1);
@@ -598,7 +599,7 @@ cudaError_t launch_attention(const AttnArgs& a, int P, int /*GT*/, cudaStream_t 
     smem_set = L.total;
   }
   dim3 grid(a.nsplit, P, 1);
-  return launch_pdl(attn_mma_kernel, grid, dim3(128), L.total, st, a);
+  return launch_pdl(attn_mma_kernel, grid, dim3(kThreads), L.total, st, a);
 }
 
 cudaError_t launch_combine(const float* parts, int R, int rows, float* out, cudaStream_t st) {

@@ -405,6 +405,7 @@ __device__ uint32_t scan_emit(const SelArgs& a, SelShared& S, const uint32_t* tb
     const int cb = first + ch * kCH;
     cp_async_wait<0>();
     __syncthreads();  // this chunk is in sC; the previous chunk is fully consumed
+    A2ATS_PHASE(g_sel_phase, 8);
     const int t0 = cb + tid * kTPT;
     // classify the thread's 64 tokens, 16 per pass (rolled: straight-line code of this
     // size stalls on instruction fetch); p0..p3 = passes 0..3 after the register shift
@@ -429,6 +430,7 @@ __device__ uint32_t scan_emit(const SelArgs& a, SelShared& S, const uint32_t* tb
       p3 = cur;
     }
     const uint32_t p[4] = {p0, p1, p2, p3};
+    A2ATS_PHASE(g_sel_phase, 9);
     uint32_t pk = 0;
 #pragma unroll
     for (int w = 0; w < 4; ++w)
@@ -441,6 +443,7 @@ __device__ uint32_t scan_emit(const SelArgs& a, SelShared& S, const uint32_t* tb
     }
     if (lane == 31) S.wsum[warp] = incl;
     __syncthreads();
+    A2ATS_PHASE(g_sel_phase, 10);
     if (ch + 1 < nchunk) prefetch_chunk(a, cp_local, cb + kCH, c1, sC);  // sC is free
     uint32_t pre = 0, tot = 0;
 #pragma unroll
