@@ -110,10 +110,12 @@ def stage_model(cfg, n_ctx: int, k: int):
     keff = min(k, n_cand)
     M = n_s + keff + n_w
     return {
-        # new keys + prepared codebook c^ (hi|lo bf16) and n_j + codes / histogram updates
-        "encode": dict(bytes=P * d * 2 + Hkv * L * (4 * d + 4) + P * (2 + 4), flops=2 * P * L * 2 * d, bound="hbm"),
-        "lut": dict(bytes=Hkv * L * d * 2 + B * Hq * d * 2 + P * L * 4 + cfg.window * 64 * 8, flops=2 * B * Hq * L * d,
-                    bound="alu"),
+        # step kernel 1 (prep): a0 for the new keys (new keys + prepared codebook c^ hi|lo bf16 + n_j, codes),
+        # a1+a2 (codebook, q, agg written, window table) and the window rows' logits (K rows, q)
+        "prep": dict(bytes=(P * d * 2 + Hkv * L * (4 * d + 4) + P * 2)
+                     + (Hkv * L * d * 2 + B * Hq * d * 2 + P * L * 4 + cfg.window * 64 * 8)
+                     + (P * min(n_w, 64) * d * 2 + P * min(n_w, 64) * 8 * 4),
+                     flops=2 * P * L * 2 * d + 2 * B * Hq * L * d, bound="hbm"),
         "select": dict(bytes=P * n_cand * 2 + P * keff * 4, flops=0, bound="hbm", tokens=P * n_ctx,
                        aux_bytes=P * L * 4 * 2),
         "attention": dict(bytes=P * M * d * 2 * 2 + P * keff * 4 + B * Hq * d * (2 + 4 + 4),
@@ -150,9 +152,8 @@ def run_ours(args, rank: int, world: int):
     def one_step(n, evs=None):
         if evs is not None:
             A.a2ats_set_stage_events(evs[1:])
-        dec.encode(kc, n - 1, n)                    # a0: the new token's code (+ hist)
         dec.params.topk = budget_k(n)
-        dec.step(q, kc, vc, n, out=out)             # a1..a6
+        dec.step_append(q, kc, vc, n, out=out)      # a0 for token n-1 (+ hist) fused with a1..a6
         if evs is not None:
             A.a2ats_set_stage_events(None)
 
@@ -221,7 +222,7 @@ def run_ours(args, rank: int, world: int):
         torch.cuda.synchronize()
     ns.append(n)
     step_ms = [enc_ev[k][0].elapsed_time(enc_ev[k][1]) for k in range(args.steps)]
-    names = ["encode", "lut", "select", "attention"]
+    names = ["launch", "prep", "select", "attention"]
     stage_ms = {nm: [] for nm in names}
     prof_step = []
     for k in range(args.steps):
@@ -268,9 +269,8 @@ def run_e2e(steps, dec, cfg, kc, vc, q, n_start, A, budget_k, use_graph, world, 
         q_dev.copy_(q_host, non_blocking=True)
         kc[:, :, n - 1].copy_(k_host[s], non_blocking=True)
         vc[:, :, n - 1].copy_(v_host[s], non_blocking=True)
-        dec.encode(kc, n - 1, n)
         dec.params.topk = budget_k(n)
-        dec.step(q_dev, kc, vc, n, out=out)
+        dec.step_append(q_dev, kc, vc, n, out=out)
         out_host.copy_(out, non_blocking=True)
 
     graphs = []
@@ -416,12 +416,14 @@ def main():
     model = stage_model(cfg, r["n_last"], budget_k(r["n_last"]))
     kernels = {}
     for nm, ms in r["stage_ms"].items():
+        if nm not in model:
+            continue
         m = model[nm]
         gbs = m["bytes"] / (ms * 1e-3) / 1e9 if ms > 0 else None
         kernels[nm] = {"ms": ms, "alg_bytes": m["bytes"], "GBps": gbs,
                        "frac_hbm": (gbs / pk["hbm"]) if gbs else None, "flops": m["flops"],
                        "TFLOPs": m["flops"] / (ms * 1e-3) / 1e12 if ms > 0 else None}
-    dom = max(("attention", "select", "lut", "encode"), key=lambda k: r["stage_ms"][k])
+    dom = max(("attention", "select", "prep"), key=lambda k: r["stage_ms"][k])
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
@@ -446,7 +448,7 @@ def main():
             cpu = oracle_sample(cfg, seconds_budget=15.0)
         except Exception as e:  # never let the baseline kill the line
             cpu = {"error": repr(e)}
-    launches_per_step = 4  # encode + lut + select + attention
+    launches_per_step = 3  # prep (encode + LUT + window logits) + select + attention
     line = {
         "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak",
@@ -456,7 +458,7 @@ def main():
                    "bridge": cfg.bridge, "n_sink": cfg.n_sink,
                    "parallelism": f"replicas x{world} (batch/head parallel, no collective)" if world > 1 else "1 GPU",
                    "l2": "flushed between steps (256 MB write, outside the timed events)" if not args.no_flush else "not flushed",
-                   "step": "a0 encode new token (+hist) + a2ats_decode_step (a1..a6)",
+                   "step": "a2ats_decode_step_append: a0 for the new token (+hist) fused with a1..a6",
                    "launch": "one CUDA graph per step (replay)" if r["graph"] else "eager launches",
                    "sparsity": (budget_k(r["n_last"]) + 68) / r["n_last"], "aux_mem": 2 / (cfg.d * 2)},
         "roofline": roof,

@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define A2ATS_ABI_VERSION 2
+#define A2ATS_ABI_VERSION 3
 
 /* ---- status codes ---------------------------------------------------- */
 #define A2ATS_OK 0
@@ -177,6 +177,29 @@ int a2ats_decode_step(const a2ats_shape* shape, const a2ats_params* params, int3
                       const uint16_t* codes, const void* codebook, const int32_t* hist,
                       float* out, int32_t* sel_out, float* scores_out,
                       void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------
+ * a2ats_decode_step_append -- a0 for the new token, then a1..a6 (one
+ * decode step of the paper: the new key is quantized with Eq. 20,
+ * P:369-373, and the query retrieves with Eqs. 21 / 11 / 2).
+ *
+ * Same as a2ats_build_codes(t_begin = n_ctx - 1, t_end = n_ctx) followed by
+ * a2ats_decode_step(n_ctx), with identical results, but the encoding runs
+ * concurrently with the score table (one kernel): the new token is inside
+ * the window (w >= 1), so the selection never needs its code.
+ *   codes, hist : on entry valid for tokens [0, n_ctx - 1); on return for
+ *                 [0, n_ctx) (codes[.., n_ctx - 1] written, hist updated
+ *                 if given)
+ *   chat, nrm   : from a2ats_qavq_prepare
+ * Requires B <= 256, kv_location = A2ATS_KV_DEVICE; other arguments and the
+ * workspace as a2ats_decode_step.  EINVAL otherwise.
+ * ------------------------------------------------------------------- */
+int a2ats_decode_step_append(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx,
+                             const void* q, const void* k_cache, const void* v_cache,
+                             uint16_t* codes, const void* codebook, int32_t* hist,
+                             const void* chat, const float* nrm,
+                             float* out, int32_t* sel_out, float* scores_out,
+                             void* ws, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------
  * Sequence-sharded decode step (the paper is single-GPU,

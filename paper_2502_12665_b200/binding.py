@@ -62,12 +62,15 @@ _SIGS = {
     "a2ats_set_stage_events": (ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int]),
     "a2ats_decode_step": (ctypes.c_int, [ctypes.POINTER(a2ats_shape), ctypes.POINTER(a2ats_params), ctypes.c_int32,
                                          _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, ctypes.c_size_t, _VP]),
+    "a2ats_decode_step_append": (ctypes.c_int, [ctypes.POINTER(a2ats_shape), ctypes.POINTER(a2ats_params),
+                                                ctypes.c_int32, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
+                                                _VP, _VP, ctypes.c_size_t, _VP]),
 }
 
 _lib = None
 
 
-ABI_VERSION = 2  # include/a2ats.h A2ATS_ABI_VERSION
+ABI_VERSION = 3  # include/a2ats.h A2ATS_ABI_VERSION
 
 
 def load(path: str = LIB_PATH, build_if_missing: bool = True) -> ctypes.CDLL:
@@ -191,6 +194,21 @@ def a2ats_decode_step(shape: a2ats_shape, params, n_ctx: int, q, k_cache, v_cach
         _ptr(sel_out, "sel_out", torch.int32, optional=True), _ptr(scores_out, "scores_out", torch.float32, optional=True),
         _ptr(ws, "ws"), ws.numel() * ws.element_size(), _stream(stream))
     _check("a2ats_decode_step", rc)
+
+
+def a2ats_decode_step_append(shape: a2ats_shape, params, n_ctx: int, q, k_cache, v_cache, codes, codebook, hist,
+                             chat, nrm, out, sel_out, scores_out, ws, stream=None):
+    import torch
+    p = params.c() if isinstance(params, Params) else params
+    rc = load().a2ats_decode_step_append(
+        ctypes.byref(shape), ctypes.byref(p), int(n_ctx), _ptr(q, "q", torch.bfloat16),
+        _ptr(k_cache, "k_cache", torch.bfloat16), _ptr(v_cache, "v_cache", torch.bfloat16),
+        _ptr(codes, "codes", torch.uint16), _ptr(codebook, "codebook", torch.bfloat16),
+        _ptr(hist, "hist", torch.int32, optional=True), _ptr(chat, "chat", torch.bfloat16),
+        _ptr(nrm, "nrm", torch.float32), _ptr(out, "out", torch.float32),
+        _ptr(sel_out, "sel_out", torch.int32, optional=True), _ptr(scores_out, "scores_out", torch.float32, optional=True),
+        _ptr(ws, "ws"), ws.numel() * ws.element_size(), _stream(stream))
+    _check("a2ats_decode_step_append", rc)
 
 
 def a2ats_set_stage_events(events):

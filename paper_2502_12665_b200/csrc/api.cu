@@ -91,7 +91,7 @@ void derive(const a2ats_shape* s, const a2ats_params* p, int n_ctx, Derived* d) 
 }
 
 struct DecodeWs {
-  size_t cs, agg, lut, sel, part, actr, cand_keep, pinfo, nsel, total;
+  size_t cs, agg, lut, sel, part, actr, cand_keep, pinfo, nsel, wlog, eslot, ectr, total;
 };
 
 DecodeWs decode_layout(const a2ats_shape* s, const a2ats_params* p) {
@@ -112,6 +112,9 @@ DecodeWs decode_layout(const a2ats_shape* s, const a2ats_params* p) {
   w.cand_keep = o; o = align_up(o + (size_t)P * s->L * 4);   // sharded step only
   w.pinfo = o; o = align_up(o + (size_t)P * 16);
   w.nsel = o; o = align_up(o + (size_t)P * 4);
+  w.wlog = o; o = align_up(o + (size_t)P * kWinPre * 8 * 4);
+  w.eslot = o; o = align_up(o + (size_t)s->Hkv * std::max(s->B, 1) * 8);   // decode_step_append's encode
+  w.ectr = o; o = align_up(o + (size_t)s->Hkv * 2 * 4);
   w.total = o;
   return w;
 }
@@ -185,6 +188,65 @@ bool g_stage_on = false;
 cudaEvent_t g_stage[kStageEvents];
 inline void stage_mark(int i, cudaStream_t st) {
   if (g_stage_on) cudaEventRecord(g_stage[i], st);
+}
+
+LutArgs make_lut_args(const a2ats_shape* shape, const a2ats_params* params, const Derived& d, const void* q,
+                      const void* codebook, float* agg, float* lut_full, float2* cs) {
+  LutArgs la;
+  la.q = static_cast<const uint16_t*>(q);
+  la.codebook = static_cast<const uint16_t*>(codebook);
+  la.agg = agg;
+  la.lut_full = lut_full;
+  la.cs = cs;
+  la.B = shape->B;
+  la.Hq = shape->Hq;
+  la.Hkv = shape->Hkv;
+  la.G = d.G;
+  la.L = shape->L;
+  la.window = params->window;
+  la.bridge = params->bridge;
+  la.group_reduce = params->group_reduce;
+  la.NV = lut_tile_nv(shape->B * d.G);
+  la.nvt = (shape->B * d.G + la.NV - 1) / la.NV;
+  fill_rope(params, &la.rt);
+  fill_bcs(params, la.rt, la.bcs);
+  return la;
+}
+
+constexpr float kScaleLog2 = (float)(1.4426950408889634 / 11.313708498984761);  // log2(e) / sqrt(128)
+
+// prep kernel roles: LUT over every (code tile, vector tile, head)
+void prep_set_lut(PrepArgs& p, const LutArgs& la) {
+  p.lut = la;
+  p.lut_tx = (la.L + 127) / 128;
+  p.n_lut = p.lut_tx * la.nvt * la.Hkv;
+  p.lut_cols = prep_lut_cols(la.NV);
+}
+// window logits of tokens [win_lo, win_lo + min(n_w, 64)) of every pair
+void prep_set_window(PrepArgs& p, const a2ats_shape* s, const void* k_cache, float* wlog, int n_ctx, int win_lo,
+                     int n_w, int shard_begin) {
+  p.kc = static_cast<const uint16_t*>(k_cache);
+  p.wlog = wlog;
+  p.n_max = s->n_max;
+  p.n_ctx = n_ctx;
+  p.win_lo = win_lo;
+  p.n_wl = std::max(0, std::min(n_w, kWinPre));
+  p.shard_begin = shard_begin;
+  p.scale_log2 = kScaleLog2;
+  p.n_win = p.n_wl > 0 ? s->B * s->Hkv : 0;
+}
+// decode-time encode of tokens [t_begin, t_begin + T) (B * T <= encode_cw_max() keys per head)
+void prep_set_encode(PrepArgs& p, const EncArgs& e) {
+  p.enc = e;
+  p.enc_tx = (e.L + 127) / 128;
+  p.n_enc = p.enc_tx * e.Hkv;
+  p.enc_nv = (e.nvec + 15) / 16 * 16;
+  p.enc_cols = prep_lut_cols(p.enc_nv);
+}
+PrepArgs prep_empty() {
+  PrepArgs p;
+  std::memset(&p, 0, sizeof(p));
+  return p;
 }
 
 }  // namespace
@@ -293,7 +355,13 @@ int a2ats_build_codes(const a2ats_shape* shape, const void* keys, int32_t t_begi
     lsplit = std::max(1, std::min(lsplit, ntiles));
     a.tiles_per_split = (ntiles + lsplit - 1) / lsplit;
     a.lsplit = (ntiles + a.tiles_per_split - 1) / a.tiles_per_split;
-    rc = cuda_status(launch_encode(a, tm, st));
+    if (a.nvec <= encode_cw_max()) {
+      PrepArgs p = prep_empty();
+      prep_set_encode(p, a);
+      rc = cuda_status(launch_prep(p, tm, tm, st));
+    } else {
+      rc = cuda_status(launch_encode_bulk(a, tm, st));
+    }
     if (rc) return rc;
   }
   return A2ATS_OK;
@@ -304,10 +372,14 @@ size_t a2ats_decode_workspace_bytes(const a2ats_shape* shape, const a2ats_params
   return decode_layout(shape, params).total;
 }
 
-int a2ats_decode_step(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx, const void* q,
-                      const void* k_cache, const void* v_cache, const uint16_t* codes, const void* codebook,
-                      const int32_t* hist, float* out, int32_t* sel_out, float* scores_out, void* ws,
-                      size_t ws_bytes, void* stream) {
+}  // extern "C"
+
+namespace {
+// One decode step (a1..a6); with chat != nullptr also a0 for token n_ctx - 1 (append).
+int decode_impl(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx, const void* q,
+                const void* k_cache, const void* v_cache, uint16_t* codes, const void* codebook, int32_t* hist,
+                const void* chat, const float* nrm, float* out, int32_t* sel_out, float* scores_out, void* ws,
+                size_t ws_bytes, void* stream) {
   int rc = check_shape(shape);
   if (rc) return rc;
   rc = check_params(params);
@@ -317,6 +389,10 @@ int a2ats_decode_step(const a2ats_shape* shape, const a2ats_params* params, int3
       !aligned16(out))
     return A2ATS_EINVAL;
   if (n_ctx <= 0 || n_ctx > shape->n_max) return A2ATS_EINVAL;
+  const bool append = chat != nullptr;
+  if (append && (!nrm || !aligned16(chat) || shape->B > encode_cw_max() ||
+                 params->kv_location != A2ATS_KV_DEVICE))
+    return A2ATS_EINVAL;
   const DecodeWs Lw = decode_layout(shape, params);
   if (!ws || ws_bytes < Lw.total) return A2ATS_EWORKSPACE;
 
@@ -327,40 +403,52 @@ int a2ats_decode_step(const a2ats_shape* shape, const a2ats_params* params, int3
   float2* cs = reinterpret_cast<float2*>(base + Lw.cs);
   float* agg = reinterpret_cast<float*>(base + Lw.agg);
   float* lut_full = scores_out ? reinterpret_cast<float*>(base + Lw.lut) : nullptr;
+  float* wlog = reinterpret_cast<float*>(base + Lw.wlog);
   int32_t* sel = sel_out ? sel_out : reinterpret_cast<int32_t*>(base + Lw.sel);
 
-  // a1 + a2 (+ window rotation table)
-  LutArgs la;
-  la.q = static_cast<const uint16_t*>(q);
-  la.codebook = static_cast<const uint16_t*>(codebook);
-  la.agg = agg;
-  la.lut_full = lut_full;
-  la.cs = cs;
-  la.B = shape->B;
-  la.Hq = shape->Hq;
-  la.Hkv = shape->Hkv;
-  la.G = d.G;
-  la.L = shape->L;
-  la.window = params->window;
-  la.bridge = params->bridge;
-  la.group_reduce = params->group_reduce;
-  la.NV = lut_tile_nv(shape->B * d.G);
-  la.nvt = (shape->B * d.G + la.NV - 1) / la.NV;
-  fill_rope(params, &la.rt);
-  fill_bcs(params, la.rt, la.bcs);
-  CUtensorMap tm;
-  rc = cuda_status(make_tmap_sw128(&tm, codebook, (uint64_t)shape->Hkv * shape->L, kD, 128));
+  // prep: a1 + a2 (LUT), the window rows' logits and (append) a0 for token n_ctx - 1, as
+  // concurrent roles of one kernel; the new token is inside the window, so the selection never
+  // reads its code, and its histogram entry is added by the select kernel after its counts
+  const LutArgs la = make_lut_args(shape, params, d, q, codebook, agg, lut_full, cs);
+  PrepArgs p = prep_empty();
+  prep_set_lut(p, la);
+  prep_set_window(p, shape, k_cache, wlog, n_ctx, d.w0, d.n_w, 0);
+  CUtensorMap tmA, tmC;
+  rc = cuda_status(make_tmap_sw128(&tmA, codebook, (uint64_t)shape->Hkv * shape->L, kD, 128));
   if (rc) return rc;
+  tmC = tmA;
+  if (append) {
+    EncArgs e;
+    e.keys = static_cast<const uint16_t*>(k_cache);
+    e.chat = static_cast<const uint16_t*>(chat);
+    e.nrm = nrm;
+    e.slot = reinterpret_cast<unsigned long long*>(base + Lw.eslot);
+    e.counter = reinterpret_cast<unsigned int*>(base + Lw.ectr);
+    e.codes = codes;
+    e.hist = nullptr;  // the select kernel adds it
+    e.B = shape->B;
+    e.Hkv = shape->Hkv;
+    e.L = shape->L;
+    e.n_max = shape->n_max;
+    e.t_begin = n_ctx - 1;
+    e.T = 1;
+    e.nvec = shape->B;
+    e.lsplit = e.tiles_per_split = 0;
+    prep_set_encode(p, e);
+    rc = cuda_status(make_tmap_sw128(&tmC, chat, (uint64_t)shape->Hkv * shape->L, 2 * kD, encode_codeword_tile()));
+    if (rc) return rc;
+  }
   stage_mark(0, st);
-  rc = cuda_status(launch_lut(la, tm, st));
+  rc = cuda_status(launch_prep(p, tmA, tmC, st));
   if (rc) return rc;
   stage_mark(1, st);
 
   // a3 + a4
-  if (d.keff > 0) {
-    SelArgs sa;
+  if (d.keff > 0 || (append && hist)) {
+    SelArgs sa{};
     sa.agg = agg;
     sa.hist = hist;
+    sa.append = append ? 1 : 0;
     sa.codes = codes;
     sa.sel = sel;
     sa.L = shape->L;
@@ -372,16 +460,10 @@ int a2ats_decode_step(const a2ats_shape* shape, const a2ats_params* params, int3
     sa.n_s = d.n_s;
     sa.w0 = d.w0;
     sa.keff = d.keff;
-    sa.sel_stride = d.keff;
+    sa.sel_stride = std::max(d.keff, 1);
     sa.shard_begin = 0;
     sa.shard_len = shape->n_max;
     sa.rank = 0;
-    sa.cand_out = sa.cand_keep = nullptr;
-    sa.cand_in = nullptr;
-    sa.pinfo = nullptr;
-    sa.counts_out = nullptr;
-    sa.counts_all = nullptr;
-    sa.nsel_out = nullptr;
     rc = cuda_status(launch_select(sa, d.P, st));
     if (rc) return rc;
   }
@@ -391,7 +473,8 @@ int a2ats_decode_step(const a2ats_shape* shape, const a2ats_params* params, int3
   AttnArgs aa;
   aa.q = static_cast<const uint16_t*>(q);
   std::memcpy(aa.bcs, la.bcs, sizeof(aa.bcs));
-  aa.rt = la.rt;
+  aa.wlog = wlog;
+  aa.n_wl = p.n_wl;
   aa.cs = cs;
   aa.kc = static_cast<const uint16_t*>(k_cache);
   aa.vc = static_cast<const uint16_t*>(v_cache);
@@ -415,7 +498,7 @@ int a2ats_decode_step(const a2ats_shape* shape, const a2ats_params* params, int3
   aa.n_w = d.n_w;
   aa.win_lo = d.w0;
   aa.shard_begin = 0;
-  aa.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)kD));
+  aa.scale_log2 = kScaleLog2;
   rc = cuda_status(launch_attention(aa, d.P, d.GT, st));
   if (rc) return rc;
   stage_mark(3, st);
@@ -427,6 +510,26 @@ int a2ats_decode_step(const a2ats_shape* shape, const a2ats_params* params, int3
   }
   stage_mark(4, st);
   return A2ATS_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int a2ats_decode_step(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx, const void* q,
+                      const void* k_cache, const void* v_cache, const uint16_t* codes, const void* codebook,
+                      const int32_t* hist, float* out, int32_t* sel_out, float* scores_out, void* ws,
+                      size_t ws_bytes, void* stream) {
+  return decode_impl(shape, params, n_ctx, q, k_cache, v_cache, const_cast<uint16_t*>(codes), codebook,
+                     const_cast<int32_t*>(hist), nullptr, nullptr, out, sel_out, scores_out, ws, ws_bytes, stream);
+}
+
+int a2ats_decode_step_append(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx, const void* q,
+                             const void* k_cache, const void* v_cache, uint16_t* codes, const void* codebook,
+                             int32_t* hist, const void* chat, const float* nrm, float* out, int32_t* sel_out,
+                             float* scores_out, void* ws, size_t ws_bytes, void* stream) {
+  if (!chat) return A2ATS_EINVAL;
+  return decode_impl(shape, params, n_ctx, q, k_cache, v_cache, codes, codebook, hist, chat, nrm, out, sel_out,
+                     scores_out, ws, ws_bytes, stream);
 }
 
 // ------------------------------------------------------------------ sequence-sharded step
@@ -460,32 +563,18 @@ int a2ats_shard_hist(const a2ats_shape* shape, const a2ats_params* params, int32
   derive(shape, params, n_ctx, &d);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   uint8_t* base = static_cast<uint8_t*>(ws);
-  LutArgs la;
-  la.q = static_cast<const uint16_t*>(q);
-  la.codebook = static_cast<const uint16_t*>(codebook);
-  la.agg = reinterpret_cast<float*>(base + Lw.agg);
-  la.lut_full = nullptr;
-  la.cs = reinterpret_cast<float2*>(base + Lw.cs);
-  la.B = shape->B;
-  la.Hq = shape->Hq;
-  la.Hkv = shape->Hkv;
-  la.G = d.G;
-  la.L = shape->L;
-  la.window = params->window;
-  la.bridge = params->bridge;
-  la.group_reduce = params->group_reduce;
-  la.NV = lut_tile_nv(shape->B * d.G);
-  la.nvt = (shape->B * d.G + la.NV - 1) / la.NV;
-  fill_rope(params, &la.rt);
-  fill_bcs(params, la.rt, la.bcs);
+  const LutArgs la = make_lut_args(shape, params, d, q, codebook, reinterpret_cast<float*>(base + Lw.agg), nullptr,
+                                   reinterpret_cast<float2*>(base + Lw.cs));
+  PrepArgs p = prep_empty();
+  prep_set_lut(p, la);
   CUtensorMap tm;
   rc = cuda_status(make_tmap_sw128(&tm, codebook, (uint64_t)shape->Hkv * shape->L, kD, 128));
   if (rc) return rc;
-  rc = cuda_status(launch_lut(la, tm, st));  // replicated on every rank, bitwise identical
+  rc = cuda_status(launch_prep(p, tm, tm, st));  // the LUT, replicated on every rank, bitwise identical
   if (rc) return rc;
   SelArgs sa{};
   sa.agg = la.agg;
-  sa.hist = hist;
+  sa.hist = const_cast<int32_t*>(hist);  // read only (no append in the sharded step)
   sa.codes = codes;
   sa.L = shape->L;
   sa.W = d.W;
@@ -543,6 +632,21 @@ int a2ats_shard_attend(const a2ats_shape* shape, const a2ats_params* params, int
   const int kcap = std::max(1, (int)std::min<long long>(params->topk, shape->n_max));
   int32_t* sel = sel_out ? sel_out : reinterpret_cast<int32_t*>(base + Lw.sel);
   int32_t* nsel = reinterpret_cast<int32_t*>(base + Lw.nsel);
+  // rows of Sel held by this rank
+  const int se = std::min(shard_begin + shard_len, n_ctx);
+  const int s_lo = std::max(0, shard_begin), s_hi = std::min(d.n_s, se);
+  const int w_lo = std::max(d.w0, shard_begin), w_hi = std::min(n_ctx, se);
+  // logits of the rank's window rows (prep kernel, window role only)
+  float* wlog = reinterpret_cast<float*>(base + Lw.wlog);
+  PrepArgs p = prep_empty();
+  p.lut = make_lut_args(shape, params, d, q, nullptr, nullptr, nullptr, nullptr);  // q, shapes, rotations
+  prep_set_window(p, shape, k_cache, wlog, n_ctx, w_lo, std::max(0, w_hi - w_lo), shard_begin);
+  if (p.n_win) {
+    CUtensorMap tm;  // unused by the window role
+    std::memset(&tm, 0, sizeof(tm));
+    rc = cuda_status(launch_prep(p, tm, tm, st));
+    if (rc) return rc;
+  }
   SelArgs sa{};
   sa.agg = reinterpret_cast<float*>(base + Lw.agg);
   sa.codes = codes;
@@ -565,14 +669,11 @@ int a2ats_shard_attend(const a2ats_shape* shape, const a2ats_params* params, int
   sa.nsel_out = nsel;
   rc = cuda_status(launch_shard_scan(sa, d.P, st));
   if (rc) return rc;
-  // rows of Sel held by this rank
-  const int se = std::min(shard_begin + shard_len, n_ctx);
-  const int s_lo = std::max(0, shard_begin), s_hi = std::min(d.n_s, se);
-  const int w_lo = std::max(d.w0, shard_begin), w_hi = std::min(n_ctx, se);
   AttnArgs aa;
   aa.q = static_cast<const uint16_t*>(q);
-  fill_rope(params, &aa.rt);
-  fill_bcs(params, aa.rt, aa.bcs);
+  std::memcpy(aa.bcs, p.lut.bcs, sizeof(aa.bcs));
+  aa.wlog = wlog;
+  aa.n_wl = p.n_wl;
   aa.cs = reinterpret_cast<float2*>(base + Lw.cs);
   aa.kc = static_cast<const uint16_t*>(k_cache);
   aa.vc = static_cast<const uint16_t*>(v_cache);
@@ -598,7 +699,7 @@ int a2ats_shard_attend(const a2ats_shape* shape, const a2ats_params* params, int
   const int local_cand = std::max(0, std::min(d.c1, se) - std::max(d.c0, shard_begin));
   const int mmax = aa.n_s + std::min(d.keff, local_cand) + aa.n_w;
   aa.nsplit = std::max(1, (mmax + d.R - 1) / d.R);  // <= the workspace's max splits
-  aa.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)kD));
+  aa.scale_log2 = kScaleLog2;
   return cuda_status(launch_attention(aa, d.P, d.GT, st));
 }
 

@@ -29,7 +29,6 @@ constexpr int kThreads = kWarps * 32;
 constexpr int kStages = 3;
 constexpr int kTileBytes = 16 * 256;           // one K (or V) tile: 16 rows x 256 B
 constexpr int kStageBytes = 2 * kTileBytes;    // K + V
-constexpr int kWinPre = 64;                    // window rows per split whose logits are precomputed
 
 struct SmemLayout {
   int tok, ring, q, sS, bcs, sW, red, total;
@@ -83,72 +82,6 @@ __device__ __forceinline__ void split_pair(float x0, float x1, uint32_t& hi, uin
 // byte offset of (row, 16-B chunk) inside a 16 x 256 B tile, XOR swizzle on the chunk
 __device__ __forceinline__ uint32_t swz(int row, int chunk) { return row * 256 + ((chunk ^ (row & 7)) << 4); }
 
-// Logits of the split's first nw (<= 64) window rows, u_j = (q R_{i-j}) . k_j (Eq. 11),
-// in the base-2 scaled domain, into sW[row][8 heads]: an exact per-row rotation on FP32
-// cores, computed from step inputs only (so before the dependency wait when the split's
-// rows are known).  Uses the (still idle) ring as scratch: (cos, sin)(r f_m) [64][64]
-// (fp64 angle at the first row, then fp64 rotation by -f_m per row) and the K rows,
-// both with 16-B chunks XOR-swizzled by row.
-__device__ __forceinline__ void window_logits(const AttnArgs& a, uint8_t* ring, const float* sQ, float* sW,
-                                           const uint8_t* kbase, int nw, int tok0) {
-  const int tid = threadIdx.x, G = a.G;
-  float4* csS = reinterpret_cast<float4*>(ring);          // [64 rows][32 chunks of 2 (cos, sin)]
-  uint4* kS = reinterpret_cast<uint4*>(ring + 32768);     // [64 rows][16 chunks of 8 bf16]
-  for (int i = tid; i < nw * 16; i += kThreads) {
-    const int row = i >> 4, c = i & 15;
-    kS[row * 16 + (c ^ (row & 7))] = ld_nc_u4(kbase + (size_t)(tok0 + row - a.shard_begin) * 256 + c * 16);
-  }
-  {
-    const int m = tid & 63, j0 = (tid >> 6) * 16;  // rows [j0, j0 + 16) of pair m
-    if (j0 < nw) {
-      const double f = a.rt.inv_freq[m];
-      double sn, cn, sf, cf;
-      sincos((double)(a.n_ctx - 1 - (tok0 + j0)) * f, &sn, &cn);  // r = i - t, t = tok0 + row
-      sincos(f, &sf, &cf);
-      float2* cs2 = reinterpret_cast<float2*>(csS);
-#pragma unroll 1
-      for (int row = j0; row < min(j0 + 16, nw); ++row) {
-        cs2[row * 64 + (((m >> 1) ^ (row & 7)) << 1) + (m & 1)] = make_float2((float)cn, (float)sn);
-        const double c2 = cn * cf + sn * sf, s2 = sn * cf - cn * sf;  // r -> r - 1
-        cn = c2;
-        sn = s2;
-      }
-    }
-  }
-  __syncthreads();
-  const int row = tid & 63, hsel = tid >> 6;  // heads hsel, hsel + 4
-  if (row < nw) {
-    float acc[2] = {0.f, 0.f};
-#pragma unroll 1
-    for (int mb = 0; mb < 8; ++mb) {  // m = 8 mb + i; pairs (m, m + 64)
-      const uint4 k1 = kS[row * 16 + (mb ^ (row & 7))];
-      const uint4 k2 = kS[row * 16 + ((mb + 8) ^ (row & 7))];
-      const uint32_t w1[4] = {k1.x, k1.y, k1.z, k1.w}, w2[4] = {k2.x, k2.y, k2.z, k2.w};
-      float4 t[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) t[j] = csS[row * 32 + ((mb * 4 + j) ^ (row & 7))];
-#pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        const int g = hsel + 4 * hh;
-        if (g < G) {
-          const float* qa = sQ + g * kD + mb * 8;
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float ka = (i & 1) ? bf_hi(w1[i >> 1]) : bf_lo(w1[i >> 1]);
-            const float kb = (i & 1) ? bf_hi(w2[i >> 1]) : bf_lo(w2[i >> 1]);
-            const float cv = (i & 1) ? t[i >> 1].z : t[i >> 1].x, sv = (i & 1) ? t[i >> 1].w : t[i >> 1].y;
-            const float q1 = qa[i], q2 = qa[i + kHalf];
-            acc[hh] = fmaf(cv, fmaf(q1, ka, q2 * kb), fmaf(sv, fmaf(q1, kb, -q2 * ka), acc[hh]));
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int hh = 0; hh < 2; ++hh) sW[row * 8 + hsel + 4 * hh] = acc[hh];  // heads >= G: 0
-  }
-  __syncthreads();
-}
-
 __device__ __forceinline__ void attn_body(const AttnArgs& a) {
   extern __shared__ __align__(128) uint8_t smraw[];
   const SmemLayout SL = attn_smem(a.R);
@@ -163,77 +96,64 @@ __device__ __forceinline__ void attn_body(const AttnArgs& a) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g8 = lane >> 2, t4 = lane & 3;  // mma fragment coordinates
 
-  // step inputs only, before the dependency wait: the query in both forms
-  // q~ (bridge) fragments as the mma B operand: head n = g8, d = 16kk + 2t4 + {0,1} (+8)
-  // q~ = q R_b (Eq. 12) computed here from the bf16 q: the lane's d and d + 64 sit in
-  // fragments kk and kk + 4, so each lane rotates its own pairs (same fp32 formula as the LUT)
+  // step inputs only, before the dependency wait: the query, fp32 and scaled to the base-2
+  // logit domain, in smem (one 16-B load per thread) -- read by the window path -- and
+  // q~ = q R_b (Eq. 12) as the mma B operand: head n = g8, d = 16kk + 2t4 + {0,1} (+8);
+  // the lane's d and d + 64 sit in fragments kk and kk + 4, so it rotates its own pairs
   uint32_t qh[8][2], ql[8][2];
   {
     float2* sbcs = reinterpret_cast<float2*>(smraw + SL.bcs);
     if (tid < kHalf) sbcs[tid] = a.bcs[tid];
+    if (tid < 128) {
+      const int g = tid >> 4, e0 = (tid & 15) * 8;
+      uint4 x = make_uint4(0, 0, 0, 0);
+      if (g < G) x = ld_nc_u4(a.q + ((size_t)b * a.Hq + hq0 + g) * kD + e0);
+      const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+      float4* d = reinterpret_cast<float4*>(sQ + g * kD + e0);
+      d[0] = make_float4(bf_lo(w[0]) * a.scale_log2, bf_hi(w[0]) * a.scale_log2, bf_lo(w[1]) * a.scale_log2,
+                         bf_hi(w[1]) * a.scale_log2);
+      d[1] = make_float4(bf_lo(w[2]) * a.scale_log2, bf_hi(w[2]) * a.scale_log2, bf_lo(w[3]) * a.scale_log2,
+                         bf_hi(w[3]) * a.scale_log2);
+    }
     __syncthreads();
-    const bool valid = g8 < G;
-    const uint32_t* src = reinterpret_cast<const uint32_t*>(a.q + ((size_t)b * a.Hq + hq0 + (valid ? g8 : 0)) * kD);
-    uint32_t qw[8][2];
-#pragma unroll
-    for (int kk = 0; kk < 8; ++kk)
-#pragma unroll
-      for (int hf = 0; hf < 2; ++hf) qw[kk][hf] = valid ? __ldg(src + (kk * 16 + 2 * t4 + 8 * hf) / 2) : 0u;
+    const float* qs = sQ + g8 * kD;  // heads >= G hold zeros
 #pragma unroll
     for (int kk = 0; kk < 4; ++kk)
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {
-        float y1[2], y2[2];
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const float x1 = e ? bf_hi(qw[kk][hf]) : bf_lo(qw[kk][hf]);
-          const float x2 = e ? bf_hi(qw[kk + 4][hf]) : bf_lo(qw[kk + 4][hf]);
-          const float2 cs = sbcs[kk * 16 + 2 * t4 + 8 * hf + e];
-          y1[e] = fmaf(x1, cs.x, -x2 * cs.y) * a.scale_log2;
-          y2[e] = fmaf(x2, cs.x, x1 * cs.y) * a.scale_log2;
-        }
-        split_pair(y1[0], y1[1], qh[kk][hf], ql[kk][hf]);
-        split_pair(y2[0], y2[1], qh[kk + 4][hf], ql[kk + 4][hf]);
+        const int d0 = kk * 16 + 2 * t4 + 8 * hf;
+        const float2 x1 = *reinterpret_cast<const float2*>(qs + d0);
+        const float2 x2 = *reinterpret_cast<const float2*>(qs + d0 + kHalf);
+        const float2 c0 = sbcs[d0], c1 = sbcs[d0 + 1];
+        split_pair(fmaf(x1.x, c0.x, -x2.x * c0.y), fmaf(x1.y, c1.x, -x2.y * c1.y), qh[kk][hf], ql[kk][hf]);
+        split_pair(fmaf(x2.x, c0.x, x1.x * c0.y), fmaf(x2.y, c1.x, x1.y * c1.y), qh[kk + 4][hf], ql[kk + 4][hf]);
       }
-  }
-
-  if (tid < 128) {  // raw q (scaled) of the group's heads for the window logits: one 16-B load per thread
-    const int g = tid >> 4, e0 = (tid & 15) * 8;
-    uint4 x = make_uint4(0, 0, 0, 0);
-    if (g < G) x = ld_nc_u4(a.q + ((size_t)b * a.Hq + hq0 + g) * kD + e0);
-    const uint32_t w[4] = {x.x, x.y, x.z, x.w};
-    float4* d = reinterpret_cast<float4*>(sQ + g * kD + e0);
-    d[0] = make_float4(bf_lo(w[0]) * a.scale_log2, bf_hi(w[0]) * a.scale_log2, bf_lo(w[1]) * a.scale_log2,
-                       bf_hi(w[1]) * a.scale_log2);
-    d[1] = make_float4(bf_lo(w[2]) * a.scale_log2, bf_hi(w[2]) * a.scale_log2, bf_lo(w[3]) * a.scale_log2,
-                       bf_hi(w[3]) * a.scale_log2);
   }
   const uint8_t* kbase = reinterpret_cast<const uint8_t*>(a.kc) + (size_t)pair * a.n_max * 256;
   const uint8_t* vbase = reinterpret_cast<const uint8_t*>(a.vc) + (size_t)pair * a.n_max * 256;
   float* sW = reinterpret_cast<float*>(smraw + SL.sW);
-  // Sel list geometry; known before the wait unless the per-pair count comes from select
-  auto wpre_rows = [&](int keff_) {  // (window rows of this split with precomputed logits, first token)
+  // Window rows whose logits the prep kernel computed (wlog, rows j < n_wl of the window):
+  // the split's leading window rows, whole tiles only unless the split ends first.
+  auto load_wlog = [&](int keff_) {
     const int M_ = a.n_s + keff_ + a.n_w, p0_ = split * a.R, p1_ = min(p0_ + a.R, M_), pw_ = a.n_s + keff_;
-    const int first = max(p0_, pw_);
-    return make_int2(split * a.R < M_ ? max(0, min(p1_ - first, kWinPre)) : 0, a.win_lo + (first - pw_));
+    if (p0_ >= M_) return 0;
+    const int jA = max(p0_, pw_) - pw_, nB_ = max(0, p1_ - max(p0_, pw_));
+    const int c = max(0, min(nB_, a.n_wl - jA));
+    const int npre = (c == nB_) ? nB_ : (c / 16) * 16;
+    for (int k = tid; k < npre * 8; k += kThreads) sW[k] = __ldcg(a.wlog + ((size_t)pair * kWinPre + jA) * 8 + k);
+    return npre;
   };
-  int2 wpre = make_int2(0, 0);
-  if (!a.nsel) {
-    __syncthreads();  // sQ
-    wpre = wpre_rows(a.keff);
-    if (wpre.x > 0) window_logits(a, smraw + SL.ring, sQ, sW, kbase, wpre.x, wpre.y);
-  }
+  // wlog comes from the prep kernel, two launches back when a select kernel runs in between
+  // (complete when this grid starts); with keff == 0 no select is launched: read after the wait
+  const bool wlog_early = !a.nsel && a.keff > 0;
+  int nwpre = 0;
+  if (wlog_early) nwpre = load_wlog(a.keff);
   pdl_wait();  // sel / counts come from select
   pdl_trigger();
 
   // Sel list of this pair on this rank: [sinks][top-K rows][window rows], ascending
   const int keff = a.nsel ? __ldcg(a.nsel + pair) : a.keff;
-  if (a.nsel) {
-    __syncthreads();  // sQ
-    wpre = wpre_rows(keff);
-    if (wpre.x > 0) window_logits(a, smraw + SL.ring, sQ, sW, kbase, wpre.x, wpre.y);
-  }
-  const int nwpre = wpre.x;
+  if (!wlog_early) nwpre = load_wlog(keff);
   const int M = a.n_s + keff + a.n_w;
   const int nsplit = (M + a.R - 1) / a.R;
   if (M == 0) {  // no row of this pair lives on this rank: empty partial (sharded mode only)

@@ -7,11 +7,12 @@
 // tensor-core pass over K = 2 x 128 reproduces k . c^_j to ~2^-16 relative (keys
 // are exact in bf16).  No per-step key transform is needed.
 //
-//   encode_cw_kernel   (few keys per head, the decode step): codewords on the MMA
-//     M side, 128 per CTA, all keys of the head on N; argmin epilogue reduces the
-//     rows (codewords) of each key column across lanes and warps, CTAs of a head
-//     combine by 64-bit atomicMax on the complemented (ordered dist, index) word;
-//     the last CTA of the head writes codes and histogram.
+//   decode-time encode tile (encode_common.cuh, run as a role of prep_kernel; few
+//     keys per head): codewords on the MMA M side, 128 per CTA, all keys of the
+//     head on N; argmin epilogue reduces the rows (codewords) of each key column
+//     across lanes and warps, CTAs of a head combine by 64-bit atomicMax on the
+//     complemented (ordered dist, index) word; the last CTA of the head writes
+//     codes and histogram.
 //   encode_bulk_kernel (prefill): 128 keys on M, 128-codeword tiles on N streamed
 //     through a double buffer, per-key running argmin in registers; CTAs that split
 //     the codebook combine the same way.
@@ -19,21 +20,14 @@
 // codewords in increasing order with a strict '<', lane / warp reductions pick the
 // lowest index among equal distances, and the 64-bit combine orders by (dist, index),
 // so the result is deterministic.
-#include "internal.cuh"
-#include "umma.cuh"
+#include "encode_common.cuh"
 
 namespace a2ats {
 
 namespace {
-A2ATS_TL_DECL(g_enc_tl)
-constexpr int kCW = 128;   // codewords per tile (MMA M in the cw kernel, MMA N in the bulk kernel)
 constexpr int kTV = 128;   // keys per CTA in the bulk kernel (MMA M)
-constexpr int kRowB = 2 * kD * 2;  // bytes of one prepared codeword row (hi | lo bf16)
 constexpr int kBulkSmem = 1024 + kTV * kD * 2 + 2 * kCW * kRowB + 2 * kCW * 4;  // align + A + 2 x B + 2 x n_j
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
 
 // c^_j = c_j S, n_j = c^_j . c_j (= c_j H c_j^T); one warp per codeword, S in smem.
 __global__ __launch_bounds__(256) void prepare_kernel(const uint16_t* __restrict__ codebook, const float* __restrict__ H,
@@ -77,160 +71,6 @@ __global__ __launch_bounds__(256) void prepare_kernel(const uint16_t* __restrict
   }
 }
 
-__device__ __forceinline__ unsigned long long pack_dist(uint32_t okey, int code) {
-  return ((unsigned long long)okey << 32) | (unsigned)code;
-}
-
-__device__ __forceinline__ void finalize_code(const EncArgs& a, int h, int v, unsigned long long packed) {
-  const int code = (int)(packed & 0xffffffffull);
-  const int b = v / a.T, t = a.t_begin + (v - b * a.T);
-  const size_t pair = (size_t)b * a.Hkv + h;
-  a.codes[pair * a.n_max + t] = (uint16_t)code;
-  if (a.hist) atomicAdd(a.hist + pair * a.L + code, 1);
-}
-
-// Global row of key vector v of head h: v = b * T + (t - t_begin).
-__device__ __forceinline__ const uint16_t* key_row(const EncArgs& a, int h, int v) {
-  const int b = v / a.T, t = a.t_begin + (v - b * a.T);
-  return a.keys + (((size_t)b * a.Hkv + h) * a.n_max + t) * kD;
-}
-
-// Prepared codeword tile: rows h*L + c0 .. (+128) of chat, 4 TMA boxes of 64 columns
-// (c^_hi 0..63, c^_hi 64..127, c^_lo 0..63, c^_lo 64..127) into four SW128 K slabs of
-// 16 KB; one thread issues, completion on tbar.  Rows past the head belong to the
-// next head (or are zero-filled) and are never selected (code < L checks).
-__device__ __forceinline__ void issue_chat_tile(const CUtensorMap& tm, const EncArgs& a, int h, int c0, uint8_t* dst,
-                                                uint64_t* tbar) {
-  umma::mbar_expect_tx(tbar, kCW * kRowB);
-#pragma unroll
-  for (int k4 = 0; k4 < 4; ++k4) umma::tma_load_2d(dst + k4 * (kCW * 128), &tm, 64 * k4, h * a.L + c0, tbar);
-}
-__device__ __forceinline__ void load_nrm(const EncArgs& a, int h, int c0, float* sN) {
-  for (int i = threadIdx.x; i < kCW; i += blockDim.x) sN[i] = (c0 + i < a.L) ? __ldg(a.nrm + (size_t)h * a.L + c0 + i) : 0.f;
-}
-// MMA k-step s (16 elements) of a chat tile: slab s / 4, 32 B per step inside the slab
-__device__ __forceinline__ uint64_t chat_desc(uint32_t base, int s) {
-  return umma::sdesc_sw128(base + (s >> 2) * (kCW * 128) + (s & 3) * 32);
-}
-
-// Cross-CTA combine of (ordered dist, code) per key, then the last CTA of the
-// group [counter] finalises codes / histogram and resets its slots.
-__device__ void combine_and_finalize(const EncArgs& a, int h, int v0, int nv, unsigned int* counter, int nparts,
-                                     bool have, unsigned long long mine) {
-  const int tid = threadIdx.x;
-  if (nparts == 1) {
-    if (have) finalize_code(a, h, v0 + tid, mine);
-    return;
-  }
-  if (have) atomicMax(a.slot + (size_t)h * a.nvec + v0 + tid, ~mine);
-  __shared__ bool s_last;
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) s_last = (atomicAdd(counter, 1u) == (unsigned)nparts - 1);
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  for (int i = tid; i < nv; i += blockDim.x) {
-    unsigned long long* sp = a.slot + (size_t)h * a.nvec + v0 + i;
-    finalize_code(a, h, v0 + i, ~__ldcg(sp));
-    *sp = 0ull;
-  }
-  if (tid == 0) *counter = 0u;
-}
-
-// grid (ceil(L / 128), Hkv); nvec <= 256 keys per head, NV = their MMA N (multiple of 16).
-template <uint32_t kCols>
-__device__ __forceinline__ void encode_cw_body(const CUtensorMap& tmC, const EncArgs& a, int NV) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;                           // 4 SW128 K slabs [128 codewords][128 B]
-  uint8_t* sB = smem + kCW * kRowB;             // [16 chunks][NV keys][16 B]
-  float* sN = reinterpret_cast<float*>(sB + NV * kD * 2);                    // [128] n_j
-  unsigned long long* red = reinterpret_cast<unsigned long long*>(sN + kCW);  // [4][NV]
-  __shared__ uint64_t mbar, tbar;
-  __shared__ uint32_t tslot;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int h = blockIdx.y, code0 = blockIdx.x * kCW;
-
-  if (warp == 0) umma::tmem_alloc<kCols>(&tslot);
-  if (tid == 0) {
-    umma::mbar_init(&mbar, 1);
-    umma::mbar_init(&tbar, 1);
-    umma::mbar_fence_init();
-    issue_chat_tile(tmC, a, h, code0, sA, &tbar);  // prepared codewords (offline state)
-  }
-  // this step's keys (written before the call) and n_j
-  load_nrm(a, h, code0, sN);
-  for (int idx = tid; idx < NV * 16; idx += 128) {
-    const int n = idx >> 4, c = idx & 15;
-    uint8_t* d = sB + (c * NV + n) * 16;
-    if (n < a.nvec) cp_async16(d, key_row(a, h, n) + c * 8);
-    else *reinterpret_cast<uint4*>(d) = make_uint4(0, 0, 0, 0);
-  }
-  cp_async_commit();
-  cp_async_wait<0>();
-  umma::fence_proxy_async();
-  umma::fence_before();
-  __syncthreads();
-  umma::fence_after();
-  pdl_wait();  // slots / codes / hist are written below
-  pdl_trigger();
-  const uint32_t tmem = tslot;
-  if (tid == 0) {
-    umma::mbar_wait(&tbar, 0);
-    const uint32_t aBase = smem_u32(sA), bBase = smem_u32(sB);
-    const uint32_t idesc = umma::idesc_bf16(kCW, NV);
-#pragma unroll
-    for (int s = 0; s < 16; ++s) {  // K = 256: c^_hi (slabs 0, 1) then c^_lo (slabs 2, 3), same keys
-      const uint64_t ad = chat_desc(aBase, s);
-      const uint64_t bd = umma::sdesc(bBase + (2 * (s & 7)) * (NV * 16), NV * 16, 128);
-      umma::mma_bf16(tmem, ad, bd, idesc, s > 0 ? 1u : 0u);
-    }
-    umma::commit(&mbar);
-  }
-  __syncwarp();
-  umma::mbar_wait(&mbar, 0);
-  umma::fence_after();
-
-  // epilogue: thread <-> codeword row; per key column, argmin over the rows
-  const int row = warp * 32 + lane;
-  const bool valid = code0 + row < a.L;
-  const float nj = sN[row];
-#pragma unroll 1
-  for (int col0 = 0; col0 < NV; col0 += 16) {
-    uint32_t r[16];
-    umma::tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + col0, r);
-    umma::tmem_wait_ld();
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const uint32_t key = valid ? ordered_key(fmaf(-2.f, __uint_as_float(r[i]), nj)) : 0xffffffffu;
-      const uint32_t wmin = __reduce_min_sync(0xffffffffu, key);
-      const uint32_t hit = __ballot_sync(0xffffffffu, key == wmin);  // lowest lane = lowest codeword
-      if (lane == 0) red[warp * NV + col0 + i] = pack_dist(wmin, code0 + warp * 32 + __ffs(hit) - 1);
-    }
-  }
-  umma::fence_before();
-  __syncthreads();
-  if (warp == 0) umma::tmem_dealloc<kCols>(tmem);
-  // tid <-> key column (nvec <= 256: two passes at most)
-  for (int base = 0; base < a.nvec; base += 128) {
-    const int v = base + tid;
-    unsigned long long best = ~0ull;
-    if (v < a.nvec) {
-#pragma unroll
-      for (int w = 0; w < 4; ++w) best = min(best, red[w * NV + v]);
-    }
-    combine_and_finalize(a, h, base, min(128, a.nvec - base), a.counter + h * 2 + (base >> 7), gridDim.x,
-                         v < a.nvec, best);
-  }
-}
-
-template <uint32_t kCols>
-__global__ __launch_bounds__(128, 1) void encode_cw_kernel(const __grid_constant__ CUtensorMap tmC, EncArgs a, int NV) {
-  A2ATS_TL(g_enc_tl, 0);
-  encode_cw_body<kCols>(tmC, a, NV);
-  A2ATS_TL(g_enc_tl, 1);
-}
 
 // grid (ceil(nvec / 128), Hkv, splits); CTA = 128 keys x codeword tiles [tbeg, tend) of 128.
 __global__ __launch_bounds__(128, 1) void encode_bulk_kernel(const __grid_constant__ CUtensorMap tmC, EncArgs a) {
@@ -324,18 +164,6 @@ __global__ __launch_bounds__(128, 1) void encode_bulk_kernel(const __grid_consta
                        pack_dist(ordered_key(best), bidx));
 }
 
-template <uint32_t kCols>
-cudaError_t launch_cw_t(const EncArgs& a, const CUtensorMap& tm, int NV, cudaStream_t st) {
-  const int smem = 1024 + kCW * kRowB + NV * kD * 2 + kCW * 4 + 4 * NV * 8;
-  static int smem_set = -1;
-  if (smem_set < smem) {
-    cudaError_t e = cudaFuncSetAttribute(encode_cw_kernel<kCols>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    smem_set = smem;
-  }
-  dim3 grid((a.L + kCW - 1) / kCW, a.Hkv);
-  return launch_pdl(encode_cw_kernel<kCols>, grid, dim3(128), smem, st, tm, a, NV);
-}
 }  // namespace
 
 cudaError_t launch_prepare(const uint16_t* codebook, const float* H, float* nrm, uint16_t* chat, int Hkv, int L,
@@ -348,14 +176,9 @@ cudaError_t launch_prepare(const uint16_t* codebook, const float* H, float* nrm,
   return cudaGetLastError();
 }
 
-cudaError_t launch_encode(const EncArgs& a, const CUtensorMap& tm, cudaStream_t st) {
-  if (a.nvec <= encode_cw_max()) {
-    const int NV = (a.nvec + 15) / 16 * 16;
-    if (NV <= 32) return launch_cw_t<32>(a, tm, NV, st);
-    if (NV <= 64) return launch_cw_t<64>(a, tm, NV, st);
-    if (NV <= 128) return launch_cw_t<128>(a, tm, NV, st);
-    return launch_cw_t<256>(a, tm, NV, st);
-  }
+// Prefill encoder (more than encode_cw_max() keys per head); fewer keys go through the
+// decode-time encode role of the step kernel (prep.cu).
+cudaError_t launch_encode_bulk(const EncArgs& a, const CUtensorMap& tm, cudaStream_t st) {
   static bool attr_done = false;
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(encode_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkSmem);
@@ -373,4 +196,3 @@ int encode_cw_max() { return 256; }
 
 }  // namespace a2ats
 
-A2ATS_TL_EXPORT(a2ats_debug_encode_timeline, a2ats::g_enc_tl)

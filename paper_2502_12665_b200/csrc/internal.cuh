@@ -144,7 +144,9 @@ int lut_tile_nv(int nvec);
 
 struct SelArgs {
   const float* agg;             // [P, L]
-  const int32_t* hist;          // [P, L] or nullptr (counts of the LOCAL tokens' codes)
+  int32_t* hist;                // [P, L] or nullptr (counts of the LOCAL tokens' codes)
+  int append;                   // 1: token n_ctx-1 is encoded by this step's prep kernel: not in hist
+                                //    yet; select adds it after taking the counts
   const uint16_t* codes;        // [P, n_max] local code array (local index = global - shard_begin)
   int32_t* sel;                 // [P, sel_stride] selected global token indices, ascending
   int L, W, n_max, n_ctx, c0, c1, n_s, w0, keff, sel_stride;
@@ -177,7 +179,8 @@ struct AttnArgs {
   int shard_begin;        // local row = global - shard_begin
   float scale_log2;       // log2(e) / sqrt(d)
   float2 bcs[kHalf];      // (cos, sin)(b f_m), from fp64 angles on the host
-  RopeTab rt;             // f_m (fp64) for the window rotations
+  const float* wlog;      // [P, 64, 8] logits of the first n_wl window rows (prep kernel)
+  int n_wl;
 };
 
 struct EncArgs {
@@ -196,7 +199,25 @@ struct EncArgs {
 // SWIZZLE_128B: a box lands as the K-major SW128 layout of umma::sdesc_sw128.
 cudaError_t make_tmap_sw128(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
 
-cudaError_t launch_lut(const LutArgs& a, const CUtensorMap& tm_codebook, cudaStream_t st);
+// The step's first kernel (prep.cu): independent per-CTA roles in one launch --
+//   LUT tiles (a1 + a2), decode-time encode tiles of the new keys (a0), and the
+//   window rows' logits (a5's local part, Eq. 11) -- so they run concurrently.
+struct PrepArgs {
+  LutArgs lut;                 // LUT role (also q, rotation tables and shapes for the window role)
+  EncArgs enc;                 // encode role; enc.hist == nullptr leaves the histogram to the caller
+  int n_lut, n_enc, n_win;     // CTAs per role, in this order along blockIdx.x
+  int lut_tx, lut_cols;        // LUT: code tiles per (head, vector tile); TMEM columns
+  int enc_tx, enc_nv, enc_cols;  // encode: code tiles per head, keys as MMA N, TMEM columns
+  // window role, one CTA per pair: logits of window tokens [win_lo, win_lo + n_wl)
+  const uint16_t* kc;          // [B, Hkv, n_max, 128] (local rows: global - shard_begin)
+  float* wlog;                 // [P, 64, 8] base-2 scaled logits (heads >= G: 0)
+  int n_max, n_ctx, win_lo, n_wl, shard_begin;
+  float scale_log2;
+};
+constexpr int kWinPre = 64;    // window rows per pair whose logits the prep kernel computes
+int prep_lut_cols(int NV);
+cudaError_t launch_prep(const PrepArgs& p, const CUtensorMap& tm_codebook, const CUtensorMap& tm_chat,
+                        cudaStream_t st);
 cudaError_t launch_scores(const float* lut_full, const uint16_t* codes, float* scores, int B, int Hq, int Hkv,
                           int G, int L, int n_max, int n_ctx, cudaStream_t st);
 cudaError_t launch_select(const SelArgs& a, int P, cudaStream_t st);
@@ -207,7 +228,7 @@ cudaError_t launch_attention(const AttnArgs& a, int P, int GT, cudaStream_t st);
 cudaError_t launch_combine(const float* parts, int R, int rows, float* out, cudaStream_t st);
 cudaError_t launch_prepare(const uint16_t* codebook, const float* H, float* nrm, uint16_t* chat, int Hkv, int L,
                            cudaStream_t st);
-cudaError_t launch_encode(const EncArgs& a, const CUtensorMap& tm_chat, cudaStream_t st);
+cudaError_t launch_encode_bulk(const EncArgs& a, const CUtensorMap& tm_chat, cudaStream_t st);
 
 int sm_count();
 int encode_codeword_tile();

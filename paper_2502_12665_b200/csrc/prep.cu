@@ -1,0 +1,334 @@
+// The step's first kernel: three independent roles in one launch, so that the
+// score table, the new key's code and the window logits are computed concurrently
+// (one CTA per tile of one role; every role reads only step inputs before the
+// dependency wait).
+//
+// LUT role (a1 + a2; Eq. 12, Eq. 21): per KV head a dense
+//   contraction M = L codewords, N = B*G queries, K = 2 x 128 (q~ hi and lo) on the
+//   5th-gen tensor cores.  A CTA loads a 128-codeword tile by TMA (SWIZZLE_128B),
+//   computes its query tile q~ = q R_b itself (fp32 from fp64 angles, split into bf16
+//   hi + lo in the canonical K-major layout), issues 16 tcgen05.mma into TMEM, and the
+//   epilogue folds the G query heads (max or sum, reading Q10) into agg.  The codebook
+//   is exact in bf16 and q~ = hi + lo to ~2^-16, so LUT entries carry fp32-level error.
+//   The LUT CTAs also write the window table cs[r][m] = (cos, sin)(r f_m) (fp64
+//   angles) used by the attention for window rows beyond the precomputed ones.
+// Encode role (a0 for the decode step's new keys; Eq. 14, Eq. 20):
+//   encode_tile of encode_common.cuh.
+// Window role (a5's local rows; Eq. 11): for one (b, KV head) pair, the
+//   logits u_j = (q R_{i-j}) . k_j of the first min(w, 64) window tokens, an exact
+//   per-row rotation on FP32 cores ((cos, sin)(r f_m) from an fp64 angle at the first
+//   row, then fp64 rotations by -f_m per row), base-2 scaled, into wlog.
+#include "encode_common.cuh"
+
+namespace a2ats {
+
+namespace {
+A2ATS_TL_DECL(g_prep_tl)
+A2ATS_PHASE_DECL(g_lut_phase)
+constexpr int kTC = 128;  // codewords per LUT CTA (MMA M)
+
+__device__ __forceinline__ uint4 pack8(const uint16_t v[8]) {
+  return make_uint4(v[0] | (uint32_t(v[1]) << 16), v[2] | (uint32_t(v[3]) << 16), v[4] | (uint32_t(v[5]) << 16),
+                    v[6] | (uint32_t(v[7]) << 16));
+}
+
+__host__ __device__ constexpr int lut_tile_smem(int NV) { return kTC * kD * 2 + NV * 2 * kD * 2; }
+constexpr int kWinSmem = 32768 + 16384 + 8 * kD * 4;  // cs [64][64] float2, K [64][128] bf16, q [8][128] fp32
+
+// LUT tile i of p.n_lut: (code tile x, vector tile y, head h).  Before the dependency
+// wait: codeword tile (TMA) and q~ tile; after: the cs table share, MMAs, G-fold epilogue.
+template <int G>
+__device__ __forceinline__ void lut_tile(const CUtensorMap& tmA, const PrepArgs& p, int i, uint8_t* smem) {
+  const LutArgs& a = p.lut;
+  const int NV = a.NV;
+  uint8_t* sA = smem;                 // 2 x [128 codes][128 B] SW128 K slabs (TMA)
+  uint8_t* sB = smem + kTC * kD * 2;  // [32 chunks][NV vectors][16 B]: chunks 0..15 hi, 16..31 lo
+  __shared__ uint64_t mbar, tbar;
+  __shared__ uint32_t tslot;
+  __shared__ float2 sbcs[kHalf];  // bridge (cos, sin): smem, not divergent parameter loads
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int x = i % p.lut_tx, y = (i / p.lut_tx) % a.nvt, h = i / (p.lut_tx * a.nvt);
+  const int code0 = x * kTC;
+  const int vec0 = y * NV;
+  const int nvec = a.B * G;
+
+  A2ATS_PHASE(g_lut_phase, 0);
+  if (warp == 0) umma::tmem_alloc_n(&tslot, p.lut_cols);
+  if (tid == 0) {
+    umma::mbar_init(&mbar, 1);
+    umma::mbar_init(&tbar, 1);
+    umma::mbar_fence_init();
+    // codeword tile (rows h*L + code0 .., 128 x 128 bf16) by TMA into two SW128 K slabs;
+    // rows past the head belong to the next head (or are zero-filled): never used
+    umma::mbar_expect_tx(&tbar, kTC * kD * 2);
+    umma::tma_load_2d(sA, &tmA, 0, h * a.L + code0, &tbar);
+    umma::tma_load_2d(sA + kTC * 128, &tmA, 64, h * a.L + code0, &tbar);
+  }
+  if (tid < kHalf) sbcs[tid] = a.bcs[tid];
+  __syncthreads();
+  // query tile: vector n = b * G + g <-> q row b * Hq + h * G + g; item = (vector, 8-pair chunk).
+  // All q loads of a pass are issued before any is used (the loop is latency-bound).
+  constexpr int kIt = 4;
+#pragma unroll 1
+  for (int base = 0; base < NV * 8; base += 128 * kIt) {
+    uint4 u1[kIt], u2[kIt];
+#pragma unroll
+    for (int j = 0; j < kIt; ++j) {
+      const int it = base + j * 128 + tid, vn = vec0 + (it >> 3);
+      u1[j] = u2[j] = make_uint4(0, 0, 0, 0);
+      if (it < NV * 8 && vn < nvec) {
+        const uint16_t* qp = a.q + (size_t)((vn / G) * a.Hq + h * G + vn % G) * kD + (it & 7) * 8;
+        u1[j] = ld_nc_u4(qp);
+        u2[j] = ld_nc_u4(qp + kHalf);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kIt; ++j) {
+      const int it = base + j * 128 + tid;
+      if (it >= NV * 8) break;
+      const int n = it >> 3, c = it & 7;
+      const uint32_t w1[4] = {u1[j].x, u1[j].y, u1[j].z, u1[j].w}, w2[4] = {u2[j].x, u2[j].y, u2[j].z, u2[j].w};
+      uint16_t h1[8], l1[8], h2[8], l2[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {  // q~ = q R_b (Eq. 12), half-split pair (m, m+64); zero rows stay zero
+        const float x1 = (e & 1) ? bf_hi(w1[e >> 1]) : bf_lo(w1[e >> 1]);
+        const float x2 = (e & 1) ? bf_hi(w2[e >> 1]) : bf_lo(w2[e >> 1]);
+        const float2 cs = sbcs[c * 8 + e];
+        umma::split_bf16(fmaf(x1, cs.x, -x2 * cs.y), h1[e], l1[e]);
+        umma::split_bf16(fmaf(x2, cs.x, x1 * cs.y), h2[e], l2[e]);
+      }
+      *reinterpret_cast<uint4*>(sB + ((c)*NV + n) * 16) = pack8(h1);        // hi, elements 0..63
+      *reinterpret_cast<uint4*>(sB + ((c + 8) * NV + n) * 16) = pack8(h2);  // hi, elements 64..127
+      *reinterpret_cast<uint4*>(sB + ((c + 16) * NV + n) * 16) = pack8(l1); // lo
+      *reinterpret_cast<uint4*>(sB + ((c + 24) * NV + n) * 16) = pack8(l2);
+    }
+  }
+  A2ATS_PHASE(g_lut_phase, 1);
+  pdl_wait();  // the previous step's attention reads cs; its select reads agg
+  pdl_trigger();
+  if (tid >= 32) {  // window table cs[r][m] = (cos, sin)(r f_m) from fp64 angles, spread over the LUT CTAs
+#pragma unroll 1
+    for (int k = i * 96 + tid - 32; k < a.window * kHalf; k += p.n_lut * 96) {
+      double sn, cn;
+      sincos((double)(k >> 6) * a.rt.inv_freq[k & (kHalf - 1)], &sn, &cn);
+      a.cs[k] = make_float2((float)cn, (float)sn);
+    }
+  }
+  umma::fence_proxy_async();  // sB (generic-proxy writes) -> tensor core
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  A2ATS_PHASE(g_lut_phase, 2);
+  const uint32_t tmem = tslot;
+
+  if (tid == 0) {
+    umma::mbar_wait(&tbar, 0);  // codeword tile landed
+    const uint32_t aBase = smem_u32(sA), bBase = smem_u32(sB);
+    const uint32_t idesc = umma::idesc_bf16(kTC, NV);
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {  // K = 256: 8 steps against q~_hi, 8 against q~_lo, same A
+      const int kk = s & 7;
+      const uint64_t ad = umma::sdesc_sw128(aBase + (kk >> 2) * (kTC * 128) + (kk & 3) * 32);
+      const uint64_t bd = umma::sdesc(bBase + (2 * s) * (NV * 16), NV * 16, 128);
+      umma::mma_bf16(tmem, ad, bd, idesc, s > 0 ? 1u : 0u);
+    }
+    umma::commit(&mbar);
+  }
+  __syncwarp();
+  umma::mbar_wait(&mbar, 0);
+  umma::fence_after();
+  A2ATS_PHASE(g_lut_phase, 3);
+
+  // epilogue: thread <-> codeword row code0 + 32*warp + lane
+  const int code = code0 + warp * 32 + lane;
+  const int nv_here = min(NV, nvec - vec0);
+  const bool sum = (a.group_reduce == A2ATS_GROUP_SUM);
+  // rolled over 16-column blocks (code size over TMEM latency: this runs once per CTA)
+#pragma unroll 1
+  for (int col0 = 0; col0 < nv_here; col0 += 16) {
+    uint32_t r[16];
+    umma::tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + col0, r);
+    umma::tmem_wait_ld();
+    if (code < a.L) {
+      if (a.lut_full) {
+#pragma unroll 1
+        for (int ii = 0; ii < 16 && vec0 + col0 + ii < nvec; ++ii) {
+          const int vn = vec0 + col0 + ii, b = vn / G, g = vn - b * G;
+          float xi = 0.f;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) xi = (j == ii) ? __uint_as_float(r[j]) : xi;
+          a.lut_full[((size_t)b * a.Hq + h * G + g) * a.L + code] = xi;
+        }
+      }
+#pragma unroll
+      for (int bb = 0; bb < 16 / G; ++bb) {  // G divides 16, vec0 + col0 is a multiple of G
+        const int n0 = vec0 + col0 + bb * G;
+        if (n0 < nvec) {
+          float v = __uint_as_float(r[bb * G]);
+#pragma unroll
+          for (int g = 1; g < G; ++g) {
+            const float xg = __uint_as_float(r[bb * G + g]);
+            v = sum ? v + xg : fmaxf(v, xg);
+          }
+          a.agg[((size_t)(n0 / G) * a.Hkv + h) * a.L + code] = v;
+        }
+      }
+    }
+  }
+  A2ATS_PHASE(g_lut_phase, 4);
+  umma::fence_before();
+  __syncthreads();
+  if (warp == 0) umma::tmem_dealloc_n(tmem, p.lut_cols);
+}
+
+// Window role: pair = (b, h).  Scratch (16-B chunks XOR-swizzled by row): cs [64][64]
+// float2, K rows [64][128] bf16, q (base-2 scaled) [8][128] fp32.
+__device__ __forceinline__ void window_tile(const PrepArgs& p, int pair, uint8_t* smem) {
+  const LutArgs& a = p.lut;
+  const int tid = threadIdx.x, G = a.G, nw = p.n_wl;
+  const int b = pair / a.Hkv, h = pair - b * a.Hkv;
+  float4* csS = reinterpret_cast<float4*>(smem);                // [64 rows][32 chunks of 2 (cos, sin)]
+  uint4* kS = reinterpret_cast<uint4*>(smem + 32768);           // [64 rows][16 chunks of 8 bf16]
+  float* sQ = reinterpret_cast<float*>(smem + 32768 + 16384);   // [8][128]
+  const uint8_t* kbase = reinterpret_cast<const uint8_t*>(p.kc) + (size_t)pair * p.n_max * 256;
+  {  // q of the group's heads, scaled to the base-2 logit domain (one 16-B load per thread)
+    const int g = tid >> 4, e0 = (tid & 15) * 8;
+    uint4 xq = make_uint4(0, 0, 0, 0);
+    if (g < G) xq = ld_nc_u4(a.q + ((size_t)b * a.Hq + h * G + g) * kD + e0);
+    const uint32_t w[4] = {xq.x, xq.y, xq.z, xq.w};
+    float4* d = reinterpret_cast<float4*>(sQ + g * kD + e0);
+    d[0] = make_float4(bf_lo(w[0]) * p.scale_log2, bf_hi(w[0]) * p.scale_log2, bf_lo(w[1]) * p.scale_log2,
+                       bf_hi(w[1]) * p.scale_log2);
+    d[1] = make_float4(bf_lo(w[2]) * p.scale_log2, bf_hi(w[2]) * p.scale_log2, bf_lo(w[3]) * p.scale_log2,
+                       bf_hi(w[3]) * p.scale_log2);
+  }
+  for (int k = tid; k < nw * 16; k += 128) {
+    const int row = k >> 4, c = k & 15;
+    kS[row * 16 + (c ^ (row & 7))] = ld_nc_u4(kbase + (size_t)(p.win_lo + row - p.shard_begin) * 256 + c * 16);
+  }
+  {
+    const int m = tid & 63, j0 = (tid >> 6) * 32;  // rows [j0, j0 + 32) of pair m
+    if (j0 < nw) {
+      const double f = a.rt.inv_freq[m];
+      double sn, cn, sf, cf;
+      sincos((double)(p.n_ctx - 1 - (p.win_lo + j0)) * f, &sn, &cn);  // r = i - t, t = win_lo + row
+      sincos(f, &sf, &cf);
+      float2* cs2 = reinterpret_cast<float2*>(csS);
+#pragma unroll 1
+      for (int row = j0; row < min(j0 + 32, nw); ++row) {
+        cs2[row * 64 + (((m >> 1) ^ (row & 7)) << 1) + (m & 1)] = make_float2((float)cn, (float)sn);
+        const double c2 = cn * cf + sn * sf, s2 = sn * cf - cn * sf;  // r -> r - 1
+        cn = c2;
+        sn = s2;
+      }
+    }
+  }
+  __syncthreads();
+  const int row = tid & 63, hsel = tid >> 6;  // heads hsel, hsel + 2, ...
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  if (row < nw) {
+#pragma unroll 1
+    for (int mb = 0; mb < 8; ++mb) {  // m = 8 mb + i; pairs (m, m + 64)
+      const uint4 k1 = kS[row * 16 + (mb ^ (row & 7))];
+      const uint4 k2 = kS[row * 16 + ((mb + 8) ^ (row & 7))];
+      const uint32_t w1[4] = {k1.x, k1.y, k1.z, k1.w}, w2[4] = {k2.x, k2.y, k2.z, k2.w};
+      float4 t[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) t[j] = csS[row * 32 + ((mb * 4 + j) ^ (row & 7))];
+#pragma unroll
+      for (int hh = 0; hh < 4; ++hh) {
+        const int g = hsel + 2 * hh;
+        if (g < G) {
+          const float* qa = sQ + g * kD + mb * 8;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float ka = (e & 1) ? bf_hi(w1[e >> 1]) : bf_lo(w1[e >> 1]);
+            const float kb = (e & 1) ? bf_hi(w2[e >> 1]) : bf_lo(w2[e >> 1]);
+            const float cv = (e & 1) ? t[e >> 1].z : t[e >> 1].x, sv = (e & 1) ? t[e >> 1].w : t[e >> 1].y;
+            const float q1 = qa[e], q2 = qa[e + kHalf];
+            acc[hh] = fmaf(cv, fmaf(q1, ka, q2 * kb), fmaf(sv, fmaf(q1, kb, -q2 * ka), acc[hh]));
+          }
+        }
+      }
+    }
+  }
+  pdl_wait();  // the previous step's attention reads wlog
+  pdl_trigger();
+  if (row < nw) {
+#pragma unroll
+    for (int hh = 0; hh < 4; ++hh) p.wlog[((size_t)pair * kWinPre + row) * 8 + hsel + 2 * hh] = acc[hh];  // heads >= G: 0
+  }
+}
+
+template <int G>
+__global__ __launch_bounds__(128, 1) void prep_kernel(const __grid_constant__ CUtensorMap tmA,
+                                                      const __grid_constant__ CUtensorMap tmC, PrepArgs p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  A2ATS_TL(g_prep_tl, 0);
+  int i = blockIdx.x;
+  if (i < p.n_lut) {
+    lut_tile<G>(tmA, p, i, smem);
+  } else if ((i -= p.n_lut) < p.n_enc) {
+    encode_tile(tmC, p.enc, i % p.enc_tx, i / p.enc_tx, p.enc_tx, p.enc_nv, p.enc_cols, smem);
+  } else {
+    window_tile(p, i - p.n_enc, smem);
+  }
+  A2ATS_TL(g_prep_tl, 1);
+}
+
+// Debug output: scores[b, hq, t] = LUT[b, hq, codes[b, h, t]] for t < n_ctx (Eq. 21).
+__global__ void scores_kernel(const float* __restrict__ lut_full, const uint16_t* __restrict__ codes,
+                              float* __restrict__ scores, int Hq, int Hkv, int G, int L, int n_max, int n_ctx) {
+  pdl_wait();
+  pdl_trigger();
+  const int bq = blockIdx.y;
+  const int b = bq / Hq, hq = bq - (bq / Hq) * Hq, h = hq / G;
+  const float* lrow = lut_full + (size_t)bq * L;
+  const uint16_t* crow = codes + ((size_t)b * Hkv + h) * n_max;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n_ctx; t += gridDim.x * blockDim.x)
+    scores[(size_t)bq * n_ctx + t] = lrow[crow[t]];
+}
+
+template <int G>
+cudaError_t launch_prep_g(const PrepArgs& p, const CUtensorMap& tmA, const CUtensorMap& tmC, cudaStream_t st) {
+  int smem = 0;
+  if (p.n_lut) smem = max(smem, lut_tile_smem(p.lut.NV));
+  if (p.n_enc) smem = max(smem, encode_tile_smem(p.enc_nv));
+  if (p.n_win) smem = max(smem, kWinSmem);
+  smem += 1024;  // alignment slack for the SW128 slabs
+  static int smem_set = -1;
+  if (smem_set < smem) {
+    cudaError_t e = cudaFuncSetAttribute(prep_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    smem_set = smem;
+  }
+  const int n = p.n_lut + p.n_enc + p.n_win;
+  if (n == 0) return cudaSuccess;
+  return launch_pdl(prep_kernel<G>, dim3(n), dim3(128), smem, st, tmA, tmC, p);
+}
+}  // namespace
+
+int lut_tile_nv(int nvec) { return nvec >= 256 ? 256 : ((nvec + 15) / 16) * 16; }  // MMA N: multiple of 16
+int prep_lut_cols(int NV) { return (int)umma::tmem_cols_for(NV); }
+
+cudaError_t launch_prep(const PrepArgs& p, const CUtensorMap& tmA, const CUtensorMap& tmC, cudaStream_t st) {
+  switch (p.n_lut ? p.lut.G : 1) {
+    case 1: return launch_prep_g<1>(p, tmA, tmC, st);
+    case 2: return launch_prep_g<2>(p, tmA, tmC, st);
+    case 4: return launch_prep_g<4>(p, tmA, tmC, st);
+    default: return launch_prep_g<8>(p, tmA, tmC, st);
+  }
+}
+
+cudaError_t launch_scores(const float* lut_full, const uint16_t* codes, float* scores, int B, int Hq, int Hkv,
+                          int G, int L, int n_max, int n_ctx, cudaStream_t st) {
+  dim3 grid((n_ctx + 1023) / 1024, B * Hq);
+  return launch_pdl(scores_kernel, grid, dim3(256), 0, st, lut_full, codes, scores, Hq, Hkv, G, L, n_max, n_ctx);
+}
+
+}  // namespace a2ats
+
+A2ATS_PHASE_EXPORT(a2ats_debug_lut_phases, a2ats::g_lut_phase)
+A2ATS_TL_EXPORT(a2ats_debug_prep_timeline, a2ats::g_prep_tl)

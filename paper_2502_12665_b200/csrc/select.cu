@@ -74,7 +74,8 @@ __device__ void load_cnt(const SelArgs& a, int pair, int* cnt, const uint16_t* c
     }
     __syncthreads();
     // remove the local sinks [0, n_s) and window [w0, n_ctx): they are not candidates
-    const int nrem = a.n_s + (a.n_ctx - a.w0);
+    // (append: hist does not hold token n_ctx - 1 yet, whose code the prep kernel computes)
+    const int nrem = a.n_s + (a.n_ctx - a.append - a.w0);
     for (int i = tid; i < nrem; i += kNT) {
       const int t = i < a.n_s ? i : a.w0 + (i - a.n_s);
       if (t >= lo && t < hi) atomicSub(&cnt[cp_local[t - lo]], 1);
@@ -483,6 +484,14 @@ __device__ uint32_t scan_emit(const SelArgs& a, SelShared& S, const uint32_t* tb
   return run_gt + min(run_eq, m);
 }
 
+// append: the step's new token n_ctx - 1 (encoded by the prep kernel) joins the histogram,
+// after this pair's counts were taken (end of the kernel, off the critical path)
+__device__ __forceinline__ void append_hist(const SelArgs& a, int pair, const uint16_t* cp_local) {
+  const int lo = a.shard_begin, t = a.n_ctx - 1;
+  if (a.append && a.hist && threadIdx.x == 0 && t >= lo && t < lo + a.shard_len)
+    a.hist[(size_t)pair * a.L + cp_local[t - lo]] += 1;
+}
+
 template <int MODE>
 __device__ __forceinline__ void select_body(const SelArgs& a) {
   extern __shared__ __align__(16) uint32_t sm[];
@@ -569,6 +578,11 @@ __device__ __forceinline__ void select_body(const SelArgs& a) {
   uint32_t kstar, m, cap;
   int32_t* selp = a.sel + (size_t)pair * a.sel_stride;
   if (MODE == kFused) {
+    if (a.keff == 0) {  // nothing to select (launched for the histogram update only)
+      cp_async_wait<0>();
+      append_hist(a, pair, cp_local);
+      return;
+    }
     load_keys(a, S, pair, cnt, key);
     A2ATS_PHASE(g_sel_phase, 2);
     find_level(a, S, cnt, key, a.keff);
@@ -601,6 +615,7 @@ __device__ __forceinline__ void select_body(const SelArgs& a) {
   }
   scan_emit(a, S, tbl, cp_local, c0, c1, m, cap, selp, sC);
   A2ATS_PHASE(g_sel_phase, 7);
+  if (MODE == kFused) append_hist(a, pair, cp_local);
 }
 
 template <int MODE>
@@ -625,6 +640,7 @@ cudaError_t launch_mode(const SelArgs& a, int P, cudaStream_t st) {
 }  // namespace
 
 cudaError_t launch_select(const SelArgs& a, int P, cudaStream_t st) { return launch_mode<kFused>(a, P, st); }
+
 cudaError_t launch_shard_hist(const SelArgs& a, int P, cudaStream_t st) { return launch_mode<kShardHist>(a, P, st); }
 cudaError_t launch_shard_thresh(const SelArgs& a, int P, cudaStream_t st) {
   return launch_mode<kShardThresh>(a, P, st);

@@ -48,3 +48,13 @@ class Decoder:
                              self.hist if use_hist else None, out, sel_out, scores_out, self.ws_dec, self.stream,
                              kv_host=kv_host)
         return out
+
+    def step_append(self, q, k_cache, v_cache, n_ctx: int, out=None, sel_out=None, scores_out=None,
+                    use_hist=True):
+        """a0 for token n_ctx - 1 (its key already in k_cache) fused with the step."""
+        if out is None:
+            out = torch.empty((self.shape.B, self.shape.Hq, 128), dtype=torch.float32, device=self.device)
+        _b.a2ats_decode_step_append(self.shape, self.params, n_ctx, q, k_cache, v_cache, self.codes, self.codebook,
+                                    self.hist if use_hist else None, self.chat, self.nrm, out, sel_out, scores_out,
+                                    self.ws_dec, self.stream)
+        return out

@@ -313,3 +313,38 @@ class _PairView:
 
     def __getitem__(self, idx):
         return self.t[idx].cpu()
+
+
+# ------------------------------------------------------------------ fused append step (a0 + a1..a6)
+@pytest.mark.parametrize("use_hist,K", [(True, 60), (False, 60), (True, 0)])
+def test_decode_step_append_equals_two_calls(use_hist, K):
+    """a2ats_decode_step_append(n) == a2ats_build_codes(n-1, n) + a2ats_decode_step(n):
+    identical codes, histogram, selection and output (same arithmetic, fused launch)."""
+    cfg = Config("app", B=3, Hq=8, Hkv=2, d=128, N=900, L=384, K=K)
+    inp = make_inputs(cfg, 151, device="cpu", with_h=True)
+    dev = {k: (v.cuda() if isinstance(v, torch.Tensor) else v) for k, v in inp.items()}
+    params = A.Params(topk=cfg.K)
+    mk = lambda: A.Decoder(cfg.B, cfg.Hq, cfg.Hkv, cfg.L, inp["n_max"], dev["codebook"], dev["H"], params)
+    d1, d2 = mk(), mk()
+    for d in (d1, d2):
+        d.encode(dev["k_cache"], 0, cfg.N - 1)
+    ka = max(cfg.K, 1)
+    sel1 = torch.full((cfg.B, cfg.Hkv, ka), -1, dtype=torch.int32, device="cuda")
+    sel2 = sel1.clone()
+    d1.encode(dev["k_cache"], cfg.N - 1, cfg.N, update_hist=use_hist)
+    o1 = d1.step(dev["q"], dev["k_cache"], dev["v_cache"], cfg.N, sel_out=sel1, use_hist=use_hist)
+    o2 = d2.step_append(dev["q"], dev["k_cache"], dev["v_cache"], cfg.N, sel_out=sel2, use_hist=use_hist)
+    torch.cuda.synchronize()
+    assert torch.equal(d1.codes, d2.codes)
+    if use_hist:
+        assert torch.equal(d1.hist, d2.hist)
+        np.testing.assert_array_equal(d2.hist.cpu().numpy(), hist_of(d2.codes, cfg.L, cfg.N).cpu().numpy())
+    if K:
+        assert torch.equal(sel1, sel2)
+    assert torch.equal(o1, o2)
+    # and against the oracle's code for the new token
+    C = f64(inp["codebook"])
+    for b in range(cfg.B):
+        for h in range(cfg.Hkv):
+            ref = O.qavq_encode(f64(inp["k_cache"][b, h, cfg.N - 1:cfg.N]), C[h], f64(inp["H"][h]))
+            assert codes_np(d2.codes)[b, h, cfg.N - 1] == ref[0]

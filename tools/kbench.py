@@ -44,15 +44,18 @@ evs = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
 for e in evs:
     e.record()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+hist0 = hist.clone()
+c0 = codes[:, :, :cfg.N - 1].to(torch.int64)
+hist0.zero_().scatter_add_(2, c0, torch.ones_like(c0, dtype=torch.int32))
 for it in range(args.iters):
     flush.fill_(it)
+    dec.hist.copy_(hist0)  # covers [0, N-1): the step appends token N-1
     e0.record()
-    dec.encode(inp["k_cache"], cfg.N - 1, cfg.N, update_hist=False, codes=scratch_codes)
-    e1.record()
     A.a2ats_set_stage_events(evs)
-    dec.step(inp["q"], inp["k_cache"], inp["v_cache"], cfg.N, out=out, use_hist=not args.no_hist)
+    dec.step_append(inp["q"], inp["k_cache"], inp["v_cache"], cfg.N, out=out, use_hist=not args.no_hist)
     A.a2ats_set_stage_events(None)
+    e1.record()
     torch.cuda.synchronize()
-    names = ["lut", "select", "attn", "tail"]
-    print("it", it, "enc %.1f" % (e0.elapsed_time(e1) * 1e3), " ".join(
+    names = ["prep", "select", "attn", "tail"]
+    print("it", it, "step %.1f" % (e0.elapsed_time(e1) * 1e3), " ".join(
         "%s %.1f" % (n, evs[i].elapsed_time(evs[i + 1]) * 1e3) for i, n in enumerate(names)), "us")

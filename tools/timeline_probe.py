@@ -32,11 +32,14 @@ c = codes[:, :, :cfg.N].to(torch.int64)
 hist.scatter_add_(2, c, torch.ones_like(c, dtype=torch.int32))
 dec = A.Decoder(cfg.B, cfg.Hq, cfg.Hkv, cfg.L, inp["n_max"], inp["codebook"], inp["H"], A.Params(topk=cfg.K))
 dec.codes, dec.hist = codes, hist
+hist0 = torch.zeros_like(hist)
+c0 = codes[:, :, :cfg.N - 1].to(torch.int64)
+hist0.scatter_add_(2, c0, torch.ones_like(c0, dtype=torch.int32))
 scratch = torch.zeros_like(codes)
 out = torch.empty((cfg.B, cfg.Hq, 128), device="cuda")
 lib = A.load()
 KMAX = 8192
-kernels = ["encode", "lut", "select", "attn"]
+kernels = ["prep", "select", "attn"]
 fns = {}
 for k in kernels:
     f = getattr(lib, f"a2ats_debug_{k}_timeline")
@@ -46,8 +49,8 @@ flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
 ncta = {}
 for it in range(args.iters):
     flush.fill_(it)
-    dec.encode(inp["k_cache"], cfg.N - 1, cfg.N, update_hist=False, codes=scratch)
-    dec.step(inp["q"], inp["k_cache"], inp["v_cache"], cfg.N, out=out)
+    dec.hist.copy_(hist0)                           # covers [0, N-1); the step appends token N-1
+    dec.step_append(inp["q"], inp["k_cache"], inp["v_cache"], cfg.N, out=out)
     torch.cuda.synchronize()
     tl = {}
     for k in kernels:
@@ -74,6 +77,18 @@ for it in range(args.iters):
         q = np.percentile(du, [0, 50, 90, 100])
         print(f"{k:7s} ctas {len(a):5d} start {st.min():7.2f}..{st.max():7.2f} end {en.min():7.2f}..{en.max():7.2f}"
               f"  dur min/med/p90/max {q[0]:6.2f} {q[1]:6.2f} {q[2]:6.2f} {q[3]:6.2f}")
+    # prep roles along blockIdx.x: LUT tiles, encode tiles, window pairs
+    G = cfg.Hq // cfg.Hkv
+    nv = 256 if cfg.B * G >= 256 else (cfg.B * G + 15) // 16 * 16
+    n_lut = (cfg.L + 127) // 128 * ((cfg.B * G + nv - 1) // nv) * cfg.Hkv
+    n_enc = (cfg.L + 127) // 128 * cfg.Hkv
+    pa, pidx = tl["prep"], valid["prep"]
+    for name, lo, hi in (("lut", 0, n_lut), ("encode", n_lut, n_lut + n_enc), ("window", n_lut + n_enc, 1 << 30)):
+        sel = pidx[(pidx >= lo) & (pidx < hi)]
+        if len(sel):
+            st, en = (pa[sel, 0] - t0) / 1e3, (pa[sel, 1] - t0) / 1e3
+            print(f"  prep/{name:6s} ctas {len(sel):4d} start {st.min():7.2f}..{st.max():7.2f} end {en.min():7.2f}..{en.max():7.2f}"
+                  f"  dur med {np.median(en - st):6.2f}")
     a = tl["attn"]
     idx = valid["attn"]
     du = (a[idx, 1] - a[idx, 0]) / 1e3
