@@ -216,10 +216,11 @@ LutArgs make_lut_args(const a2ats_shape* shape, const a2ats_params* params, cons
 constexpr float kScaleLog2 = (float)(1.4426950408889634 / 11.313708498984761);  // log2(e) / sqrt(128)
 
 // prep kernel roles: LUT over every (code tile, vector tile, head)
-void prep_set_lut(PrepArgs& p, const LutArgs& la) {
+void prep_set_lut(PrepArgs& p, const LutArgs& la, int tpc = 1) {
   p.lut = la;
   p.lut_tx = (la.L + 127) / 128;
-  p.n_lut = p.lut_tx * la.nvt * la.Hkv;
+  p.lut_tpc = tpc;
+  p.n_lut = (p.lut_tx + tpc - 1) / tpc * la.nvt * la.Hkv;
   p.lut_cols = prep_lut_cols(la.NV);
 }
 // window logits of tokens [win_lo, win_lo + min(n_w, 64)) of every pair
@@ -236,13 +237,29 @@ void prep_set_window(PrepArgs& p, const a2ats_shape* s, const void* k_cache, flo
   p.n_win = p.n_wl > 0 ? s->B * s->Hkv : 0;
 }
 // decode-time encode of tokens [t_begin, t_begin + T) (B * T <= encode_cw_max() keys per head)
-void prep_set_encode(PrepArgs& p, const EncArgs& e) {
+void prep_set_encode(PrepArgs& p, const EncArgs& e, int tpc = 1) {
   p.enc = e;
   p.enc_tx = (e.L + 127) / 128;
-  p.n_enc = p.enc_tx * e.Hkv;
+  p.enc_tpc = tpc;
+  p.n_enc = (p.enc_tx + tpc - 1) / tpc * e.Hkv;
   p.enc_nv = (e.nvec + 15) / 16 * 16;
   p.enc_cols = prep_lut_cols(p.enc_nv);
 }
+// Code tiles per CTA for the LUT / encode roles so that all prep CTAs are resident at once
+// (one wave: the roles then run concurrently), doubling the encode's first.
+void prep_balance(PrepArgs& p) {
+  const int per_sm = std::max(1, (227 * 1024) / (prep_smem_bytes(p) + 1024));
+  const int cap = per_sm * sm_count();
+  for (int guard = 0; guard < 8 && p.n_lut + p.n_enc + p.n_win > cap; ++guard) {
+    if (p.n_enc && (p.enc_tpc <= p.lut_tpc || !p.n_lut) && p.enc_tpc < p.enc_tx)
+      prep_set_encode(p, p.enc, p.enc_tpc * 2);
+    else if (p.n_lut && p.lut_tpc < p.lut_tx)
+      prep_set_lut(p, p.lut, p.lut_tpc * 2);
+    else
+      break;
+  }
+}
+
 PrepArgs prep_empty() {
   PrepArgs p;
   std::memset(&p, 0, sizeof(p));
@@ -438,6 +455,7 @@ int decode_impl(const a2ats_shape* shape, const a2ats_params* params, int32_t n_
     rc = cuda_status(make_tmap_sw128(&tmC, chat, (uint64_t)shape->Hkv * shape->L, 2 * kD, encode_codeword_tile()));
     if (rc) return rc;
   }
+  prep_balance(p);
   stage_mark(0, st);
   rc = cuda_status(launch_prep(p, tmA, tmC, st));
   if (rc) return rc;

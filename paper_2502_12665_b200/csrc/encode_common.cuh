@@ -75,31 +75,30 @@ __device__ void combine_and_finalize(const EncArgs& a, int h, int v0, int nv, un
   if (tid == 0) *counter = 0u;
 }
 
-// Decode-time encode tile (few keys per head): codewords [128 x, 128 x + 128) of KV head h
-// on the MMA M side, the head's nvec (<= 256) keys on N (NV = nvec rounded up to 16,
-// ncols = TMEM columns, a power of two >= max(32, NV)).  ntile = code tiles of the head
-// (the CTAs that combine).  smem: 1024-aligned, encode_tile_smem(NV) bytes.
+// Decode-time encode (few keys per head): code tiles [xt0, xt1) (128 codewords each) of KV
+// head h, one after the other through one TMA buffer, on the MMA M side; the head's nvec
+// (<= 256) keys on N (NV = nvec rounded up to 16, ncols = TMEM columns, a power of two
+// >= max(32, NV)).  nparts = CTAs of the head (they combine through the slots).  smem:
+// 1024-aligned, encode_tile_smem(NV) bytes.
 __host__ __device__ constexpr int encode_tile_smem(int NV) { return kCW * kRowB + NV * kD * 2 + kCW * 4 + 4 * NV * 8; }
-__device__ __forceinline__ void encode_tile(const CUtensorMap& tmC, const EncArgs& a, int x, int h, int ntile, int NV,
-                                            uint32_t ncols, uint8_t* smem) {
+__device__ __forceinline__ void encode_tiles(const CUtensorMap& tmC, const EncArgs& a, int xt0, int xt1, int h,
+                                             int nparts, int NV, uint32_t ncols, uint8_t* smem) {
   uint8_t* sA = smem;                           // 4 SW128 K slabs [128 codewords][128 B]
   uint8_t* sB = smem + kCW * kRowB;             // [16 chunks][NV keys][16 B]
   float* sN = reinterpret_cast<float*>(sB + NV * kD * 2);                    // [128] n_j
-  unsigned long long* red = reinterpret_cast<unsigned long long*>(sN + kCW);  // [4][NV]
+  unsigned long long* red = reinterpret_cast<unsigned long long*>(sN + kCW);  // [4][NV] per-warp best
   __shared__ uint64_t mbar, tbar;
   __shared__ uint32_t tslot;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int code0 = x * kCW;
 
   if (warp == 0) umma::tmem_alloc_n(&tslot, ncols);
   if (tid == 0) {
     umma::mbar_init(&mbar, 1);
     umma::mbar_init(&tbar, 1);
     umma::mbar_fence_init();
-    issue_chat_tile(tmC, a, h, code0, sA, &tbar);  // prepared codewords (offline state)
+    issue_chat_tile(tmC, a, h, xt0 * kCW, sA, &tbar);  // prepared codewords (offline state)
   }
-  // this step's keys (written before the call) and n_j
-  load_nrm(a, h, code0, sN);
+  // this step's keys (written before the call)
   for (int idx = tid; idx < NV * 16; idx += 128) {
     const int n = idx >> 4, c = idx & 15;
     uint8_t* d = sB + (c * NV + n) * 16;
@@ -107,6 +106,7 @@ __device__ __forceinline__ void encode_tile(const CUtensorMap& tmC, const EncArg
     else *reinterpret_cast<uint4*>(d) = make_uint4(0, 0, 0, 0);
   }
   cp_async_commit();
+  for (int i = tid; i < 4 * NV; i += 128) red[i] = ~0ull;
   cp_async_wait<0>();
   umma::fence_proxy_async();
   umma::fence_before();
@@ -115,41 +115,51 @@ __device__ __forceinline__ void encode_tile(const CUtensorMap& tmC, const EncArg
   pdl_wait();  // slots / codes / hist are written below
   pdl_trigger();
   const uint32_t tmem = tslot;
-  if (tid == 0) {
-    umma::mbar_wait(&tbar, 0);
-    const uint32_t aBase = smem_u32(sA), bBase = smem_u32(sB);
-    const uint32_t idesc = umma::idesc_bf16(kCW, NV);
-#pragma unroll
-    for (int s = 0; s < 16; ++s) {  // K = 256: c^_hi (slabs 0, 1) then c^_lo (slabs 2, 3), same keys
-      const uint64_t ad = chat_desc(aBase, s);
-      const uint64_t bd = umma::sdesc(bBase + (2 * (s & 7)) * (NV * 16), NV * 16, 128);
-      umma::mma_bf16(tmem, ad, bd, idesc, s > 0 ? 1u : 0u);
-    }
-    umma::commit(&mbar);
-  }
-  __syncwarp();
-  umma::mbar_wait(&mbar, 0);
-  umma::fence_after();
-
-  // epilogue: thread <-> codeword row; per key column, argmin over the rows
-  const int row = warp * 32 + lane;
-  const bool valid = code0 + row < a.L;
-  const float nj = sN[row];
+  const uint32_t idesc = umma::idesc_bf16(kCW, NV);
 #pragma unroll 1
-  for (int col0 = 0; col0 < NV; col0 += 16) {
-    uint32_t r[16];
-    umma::tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + col0, r);
-    umma::tmem_wait_ld();
+  for (int xt = xt0; xt < xt1; ++xt) {
+    const int it = xt - xt0, code0 = xt * kCW;
+    load_nrm(a, h, code0, sN);
+    if (tid == 0) {
+      umma::mbar_wait(&tbar, it & 1);
+      const uint32_t aBase = smem_u32(sA), bBase = smem_u32(sB);
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const uint32_t key = valid ? ordered_key(fmaf(-2.f, __uint_as_float(r[i]), nj)) : 0xffffffffu;
-      const uint32_t wmin = __reduce_min_sync(0xffffffffu, key);
-      const uint32_t hit = __ballot_sync(0xffffffffu, key == wmin);  // lowest lane = lowest codeword
-      if (lane == 0) red[warp * NV + col0 + i] = pack_dist(wmin, code0 + warp * 32 + __ffs(hit) - 1);
+      for (int s = 0; s < 16; ++s) {  // K = 256: c^_hi (slabs 0, 1) then c^_lo (slabs 2, 3), same keys
+        const uint64_t ad = chat_desc(aBase, s);
+        const uint64_t bd = umma::sdesc(bBase + (2 * (s & 7)) * (NV * 16), NV * 16, 128);
+        umma::mma_bf16(tmem, ad, bd, idesc, s > 0 ? 1u : 0u);
+      }
+      umma::commit(&mbar);
     }
+    __syncwarp();
+    umma::mbar_wait(&mbar, it & 1);
+    umma::fence_after();
+    if (tid == 0 && xt + 1 < xt1) issue_chat_tile(tmC, a, h, code0 + kCW, sA, &tbar);  // sA is free again
+    __syncthreads();  // n_j of this tile
+    // epilogue: thread <-> codeword row; per key column, argmin over the rows (running best per warp)
+    const int row = warp * 32 + lane;
+    const bool valid = code0 + row < a.L;
+    const float nj = sN[row];
+#pragma unroll 1
+    for (int col0 = 0; col0 < NV; col0 += 16) {
+      uint32_t r[16];
+      umma::tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + col0, r);
+      umma::tmem_wait_ld();
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const uint32_t key = valid ? ordered_key(fmaf(-2.f, __uint_as_float(r[i]), nj)) : 0xffffffffu;
+        const uint32_t wmin = __reduce_min_sync(0xffffffffu, key);
+        const uint32_t hit = __ballot_sync(0xffffffffu, key == wmin);  // lowest lane = lowest codeword
+        if (lane == 0) {
+          unsigned long long* rp = red + warp * NV + col0 + i;
+          *rp = min(*rp, pack_dist(wmin, code0 + warp * 32 + __ffs(hit) - 1));
+        }
+      }
+    }
+    umma::fence_before();
+    __syncthreads();  // TMEM read out and sN consumed before the next tile
+    umma::fence_after();
   }
-  umma::fence_before();
-  __syncthreads();
   if (warp == 0) umma::tmem_dealloc_n(tmem, ncols);
   // tid <-> key column (nvec <= 256: two passes at most)
   for (int base = 0; base < a.nvec; base += 128) {
@@ -159,9 +169,10 @@ __device__ __forceinline__ void encode_tile(const CUtensorMap& tmC, const EncArg
 #pragma unroll
       for (int w = 0; w < 4; ++w) best = min(best, red[w * NV + v]);
     }
-    combine_and_finalize(a, h, base, min(128, a.nvec - base), a.counter + h * 2 + (base >> 7), ntile,
+    combine_and_finalize(a, h, base, min(128, a.nvec - base), a.counter + h * 2 + (base >> 7), nparts,
                          v < a.nvec, best);
   }
 }
+
 }  // namespace
 }  // namespace a2ats

@@ -206,8 +206,8 @@ struct PrepArgs {
   LutArgs lut;                 // LUT role (also q, rotation tables and shapes for the window role)
   EncArgs enc;                 // encode role; enc.hist == nullptr leaves the histogram to the caller
   int n_lut, n_enc, n_win;     // CTAs per role, in this order along blockIdx.x
-  int lut_tx, lut_cols;        // LUT: code tiles per (head, vector tile); TMEM columns
-  int enc_tx, enc_nv, enc_cols;  // encode: code tiles per head, keys as MMA N, TMEM columns
+  int lut_tx, lut_tpc, lut_cols;          // LUT: code tiles per (head, vector tile), tiles per CTA, TMEM cols
+  int enc_tx, enc_tpc, enc_nv, enc_cols;  // encode: code tiles per head, tiles per CTA, keys as MMA N, TMEM cols
   // window role, one CTA per pair: logits of window tokens [win_lo, win_lo + n_wl)
   const uint16_t* kc;          // [B, Hkv, n_max, 128] (local rows: global - shard_begin)
   float* wlog;                 // [P, 64, 8] base-2 scaled logits (heads >= G: 0)
@@ -216,6 +216,7 @@ struct PrepArgs {
 };
 constexpr int kWinPre = 64;    // window rows per pair whose logits the prep kernel computes
 int prep_lut_cols(int NV);
+int prep_smem_bytes(const PrepArgs& p);  // dynamic smem of a prep launch (max over its roles)
 cudaError_t launch_prep(const PrepArgs& p, const CUtensorMap& tm_codebook, const CUtensorMap& tm_chat,
                         cudaStream_t st);
 cudaError_t launch_scores(const float* lut_full, const uint16_t* codes, float* scores, int B, int Hq, int Hkv,

@@ -48,8 +48,9 @@ __device__ __forceinline__ void lut_tile(const CUtensorMap& tmA, const PrepArgs&
   __shared__ float2 sbcs[kHalf];  // bridge (cos, sin): smem, not divergent parameter loads
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int x = i % p.lut_tx, y = (i / p.lut_tx) % a.nvt, h = i / (p.lut_tx * a.nvt);
-  const int code0 = x * kTC;
+  const int cx_n = (p.lut_tx + p.lut_tpc - 1) / p.lut_tpc;  // CTAs per (vector tile, head)
+  const int cx = i % cx_n, y = (i / cx_n) % a.nvt, h = i / (cx_n * a.nvt);
+  const int xt0 = cx * p.lut_tpc, xt1 = min(p.lut_tx, xt0 + p.lut_tpc);  // code tiles of this CTA
   const int vec0 = y * NV;
   const int nvec = a.B * G;
 
@@ -62,8 +63,8 @@ __device__ __forceinline__ void lut_tile(const CUtensorMap& tmA, const PrepArgs&
     // codeword tile (rows h*L + code0 .., 128 x 128 bf16) by TMA into two SW128 K slabs;
     // rows past the head belong to the next head (or are zero-filled): never used
     umma::mbar_expect_tx(&tbar, kTC * kD * 2);
-    umma::tma_load_2d(sA, &tmA, 0, h * a.L + code0, &tbar);
-    umma::tma_load_2d(sA + kTC * 128, &tmA, 64, h * a.L + code0, &tbar);
+    umma::tma_load_2d(sA, &tmA, 0, h * a.L + xt0 * kTC, &tbar);
+    umma::tma_load_2d(sA + kTC * 128, &tmA, 64, h * a.L + xt0 * kTC, &tbar);
   }
   if (tid < kHalf) sbcs[tid] = a.bcs[tid];
   __syncthreads();
@@ -121,64 +122,73 @@ __device__ __forceinline__ void lut_tile(const CUtensorMap& tmA, const PrepArgs&
   umma::fence_after();
   A2ATS_PHASE(g_lut_phase, 2);
   const uint32_t tmem = tslot;
-
-  if (tid == 0) {
-    umma::mbar_wait(&tbar, 0);  // codeword tile landed
-    const uint32_t aBase = smem_u32(sA), bBase = smem_u32(sB);
-    const uint32_t idesc = umma::idesc_bf16(kTC, NV);
-#pragma unroll
-    for (int s = 0; s < 16; ++s) {  // K = 256: 8 steps against q~_hi, 8 against q~_lo, same A
-      const int kk = s & 7;
-      const uint64_t ad = umma::sdesc_sw128(aBase + (kk >> 2) * (kTC * 128) + (kk & 3) * 32);
-      const uint64_t bd = umma::sdesc(bBase + (2 * s) * (NV * 16), NV * 16, 128);
-      umma::mma_bf16(tmem, ad, bd, idesc, s > 0 ? 1u : 0u);
-    }
-    umma::commit(&mbar);
-  }
-  __syncwarp();
-  umma::mbar_wait(&mbar, 0);
-  umma::fence_after();
-  A2ATS_PHASE(g_lut_phase, 3);
-
-  // epilogue: thread <-> codeword row code0 + 32*warp + lane
-  const int code = code0 + warp * 32 + lane;
+  const uint32_t idesc = umma::idesc_bf16(kTC, NV);
   const int nv_here = min(NV, nvec - vec0);
   const bool sum = (a.group_reduce == A2ATS_GROUP_SUM);
-  // rolled over 16-column blocks (code size over TMEM latency: this runs once per CTA)
 #pragma unroll 1
-  for (int col0 = 0; col0 < nv_here; col0 += 16) {
-    uint32_t r[16];
-    umma::tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + col0, r);
-    umma::tmem_wait_ld();
-    if (code < a.L) {
-      if (a.lut_full) {
-#pragma unroll 1
-        for (int ii = 0; ii < 16 && vec0 + col0 + ii < nvec; ++ii) {
-          const int vn = vec0 + col0 + ii, b = vn / G, g = vn - b * G;
-          float xi = 0.f;
+  for (int xt = xt0; xt < xt1; ++xt) {  // code tiles one after the other, same q~ tile
+    const int it = xt - xt0, code0 = xt * kTC;
+    if (tid == 0) {
+      umma::mbar_wait(&tbar, it & 1);  // codeword tile landed
+      const uint32_t aBase = smem_u32(sA), bBase = smem_u32(sB);
 #pragma unroll
-          for (int j = 0; j < 16; ++j) xi = (j == ii) ? __uint_as_float(r[j]) : xi;
-          a.lut_full[((size_t)b * a.Hq + h * G + g) * a.L + code] = xi;
-        }
+      for (int s = 0; s < 16; ++s) {  // K = 256: 8 steps against q~_hi, 8 against q~_lo, same A
+        const int kk = s & 7;
+        const uint64_t ad = umma::sdesc_sw128(aBase + (kk >> 2) * (kTC * 128) + (kk & 3) * 32);
+        const uint64_t bd = umma::sdesc(bBase + (2 * s) * (NV * 16), NV * 16, 128);
+        umma::mma_bf16(tmem, ad, bd, idesc, s > 0 ? 1u : 0u);
       }
+      umma::commit(&mbar);
+    }
+    __syncwarp();
+    umma::mbar_wait(&mbar, it & 1);
+    umma::fence_after();
+    if (tid == 0 && xt + 1 < xt1) {  // next codeword tile into the (now free) A buffer
+      umma::mbar_expect_tx(&tbar, kTC * kD * 2);
+      umma::tma_load_2d(sA, &tmA, 0, h * a.L + code0 + kTC, &tbar);
+      umma::tma_load_2d(sA + kTC * 128, &tmA, 64, h * a.L + code0 + kTC, &tbar);
+    }
+    A2ATS_PHASE(g_lut_phase, 3);
+
+    // epilogue: thread <-> codeword row code0 + 32*warp + lane
+    const int code = code0 + warp * 32 + lane;
+    // rolled over 16-column blocks (code size over TMEM latency: this runs once per tile)
+#pragma unroll 1
+    for (int col0 = 0; col0 < nv_here; col0 += 16) {
+      uint32_t r[16];
+      umma::tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + col0, r);
+      umma::tmem_wait_ld();
+      if (code < a.L) {
+        if (a.lut_full) {
+#pragma unroll 1
+          for (int ii = 0; ii < 16 && vec0 + col0 + ii < nvec; ++ii) {
+            const int vn = vec0 + col0 + ii, b = vn / G, g = vn - b * G;
+            float xi = 0.f;
 #pragma unroll
-      for (int bb = 0; bb < 16 / G; ++bb) {  // G divides 16, vec0 + col0 is a multiple of G
-        const int n0 = vec0 + col0 + bb * G;
-        if (n0 < nvec) {
-          float v = __uint_as_float(r[bb * G]);
-#pragma unroll
-          for (int g = 1; g < G; ++g) {
-            const float xg = __uint_as_float(r[bb * G + g]);
-            v = sum ? v + xg : fmaxf(v, xg);
+            for (int j = 0; j < 16; ++j) xi = (j == ii) ? __uint_as_float(r[j]) : xi;
+            a.lut_full[((size_t)b * a.Hq + h * G + g) * a.L + code] = xi;
           }
-          a.agg[((size_t)(n0 / G) * a.Hkv + h) * a.L + code] = v;
+        }
+#pragma unroll
+        for (int bb = 0; bb < 16 / G; ++bb) {  // G divides 16, vec0 + col0 is a multiple of G
+          const int n0 = vec0 + col0 + bb * G;
+          if (n0 < nvec) {
+            float v = __uint_as_float(r[bb * G]);
+#pragma unroll
+            for (int g = 1; g < G; ++g) {
+              const float xg = __uint_as_float(r[bb * G + g]);
+              v = sum ? v + xg : fmaxf(v, xg);
+            }
+            a.agg[((size_t)(n0 / G) * a.Hkv + h) * a.L + code] = v;
+          }
         }
       }
     }
+    umma::fence_before();
+    __syncthreads();  // TMEM read out before the next tile's MMAs
+    umma::fence_after();
   }
   A2ATS_PHASE(g_lut_phase, 4);
-  umma::fence_before();
-  __syncthreads();
   if (warp == 0) umma::tmem_dealloc_n(tmem, p.lut_cols);
 }
 
@@ -271,7 +281,9 @@ __global__ __launch_bounds__(128, 1) void prep_kernel(const __grid_constant__ CU
   if (i < p.n_lut) {
     lut_tile<G>(tmA, p, i, smem);
   } else if ((i -= p.n_lut) < p.n_enc) {
-    encode_tile(tmC, p.enc, i % p.enc_tx, i / p.enc_tx, p.enc_tx, p.enc_nv, p.enc_cols, smem);
+    const int cx_n = (p.enc_tx + p.enc_tpc - 1) / p.enc_tpc, cx = i % cx_n;
+    encode_tiles(tmC, p.enc, cx * p.enc_tpc, min(p.enc_tx, (cx + 1) * p.enc_tpc), i / cx_n, cx_n, p.enc_nv,
+                 p.enc_cols, smem);
   } else {
     window_tile(p, i - p.n_enc, smem);
   }
@@ -293,11 +305,7 @@ __global__ void scores_kernel(const float* __restrict__ lut_full, const uint16_t
 
 template <int G>
 cudaError_t launch_prep_g(const PrepArgs& p, const CUtensorMap& tmA, const CUtensorMap& tmC, cudaStream_t st) {
-  int smem = 0;
-  if (p.n_lut) smem = max(smem, lut_tile_smem(p.lut.NV));
-  if (p.n_enc) smem = max(smem, encode_tile_smem(p.enc_nv));
-  if (p.n_win) smem = max(smem, kWinSmem);
-  smem += 1024;  // alignment slack for the SW128 slabs
+  const int smem = prep_smem_bytes(p);
   static int smem_set = -1;
   if (smem_set < smem) {
     cudaError_t e = cudaFuncSetAttribute(prep_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -309,6 +317,14 @@ cudaError_t launch_prep_g(const PrepArgs& p, const CUtensorMap& tmA, const CUten
   return launch_pdl(prep_kernel<G>, dim3(n), dim3(128), smem, st, tmA, tmC, p);
 }
 }  // namespace
+
+int prep_smem_bytes(const PrepArgs& p) {
+  int smem = 0;
+  if (p.n_lut) smem = max(smem, lut_tile_smem(p.lut.NV));
+  if (p.n_enc) smem = max(smem, encode_tile_smem(p.enc_nv));
+  if (p.n_win) smem = max(smem, kWinSmem);
+  return smem + 1024;  // alignment slack for the SW128 slabs
+}
 
 int lut_tile_nv(int nvec) { return nvec >= 256 ? 256 : ((nvec + 15) / 16) * 16; }  // MMA N: multiple of 16
 int prep_lut_cols(int NV) { return (int)umma::tmem_cols_for(NV); }

@@ -316,11 +316,16 @@ class _PairView:
 
 
 # ------------------------------------------------------------------ fused append step (a0 + a1..a6)
-@pytest.mark.parametrize("use_hist,K", [(True, 60), (False, 60), (True, 0)])
-def test_decode_step_append_equals_two_calls(use_hist, K):
+@pytest.mark.parametrize("use_hist,K,big", [(True, 60, False), (False, 60, False), (True, 0, False),
+                                             (True, 123, True)])
+def test_decode_step_append_equals_two_calls(use_hist, K, big):
     """a2ats_decode_step_append(n) == a2ats_build_codes(n-1, n) + a2ats_decode_step(n):
-    identical codes, histogram, selection and output (same arithmetic, fused launch)."""
+    identical codes, histogram, selection and output (same arithmetic, fused launch).
+    big: C2's shapes (B = 16, 32 q / 8 KV heads, L = 4096), where the prep kernel groups
+    two code tiles per CTA to keep its roles resident in one wave."""
     cfg = Config("app", B=3, Hq=8, Hkv=2, d=128, N=900, L=384, K=K)
+    if big:
+        cfg = Config("appbig", B=16, Hq=32, Hkv=8, d=128, N=1500, L=4096, K=K)
     inp = make_inputs(cfg, 151, device="cpu", with_h=True)
     dev = {k: (v.cuda() if isinstance(v, torch.Tensor) else v) for k, v in inp.items()}
     params = A.Params(topk=cfg.K)

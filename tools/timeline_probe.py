@@ -80,8 +80,18 @@ for it in range(args.iters):
     # prep roles along blockIdx.x: LUT tiles, encode tiles, window pairs
     G = cfg.Hq // cfg.Hkv
     nv = 256 if cfg.B * G >= 256 else (cfg.B * G + 15) // 16 * 16
-    n_lut = (cfg.L + 127) // 128 * ((cfg.B * G + nv - 1) // nv) * cfg.Hkv
-    n_enc = (cfg.L + 127) // 128 * cfg.Hkv
+    # mirror of api.cu prep_balance (one wave at 3 CTAs / SM): encode first, then LUT
+    tx, nvt, n_win = (cfg.L + 127) // 128, (cfg.B * G + nv - 1) // nv, cfg.B * cfg.Hkv
+    lt, et = 1, 1
+    while (-(-tx // lt)) * nvt * cfg.Hkv + (-(-tx // et)) * cfg.Hkv + n_win > 3 * 148:
+        if et <= lt and et < tx:
+            et *= 2
+        elif lt < tx:
+            lt *= 2
+        else:
+            break
+    n_lut = (-(-tx // lt)) * nvt * cfg.Hkv
+    n_enc = (-(-tx // et)) * cfg.Hkv
     pa, pidx = tl["prep"], valid["prep"]
     for name, lo, hi in (("lut", 0, n_lut), ("encode", n_lut, n_lut + n_enc), ("window", n_lut + n_enc, 1 << 30)):
         sel = pidx[(pidx >= lo) & (pidx < hi)]
