@@ -467,6 +467,7 @@ int decode_impl(const a2ats_shape* shape, const a2ats_params* params, int32_t n_
     sa.agg = agg;
     sa.hist = hist;
     sa.append = append ? 1 : 0;
+    sa.append_hist = append ? 1 : 0;
     sa.codes = codes;
     sa.sel = sel;
     sa.L = shape->L;

@@ -519,11 +519,6 @@ cudaError_t launch_attention(const AttnArgs& a, int P, int /*GT*/, cudaStream_t 
     smem_set = L.total;
   }
   dim3 grid(a.nsplit, P, 1);
-  static const bool no_pdl = std::getenv("A2ATS_ATTN_NO_PDL") != nullptr;  // tuning switch
-  if (no_pdl) {
-    attn_mma_kernel<<<grid, kThreads, L.total, st>>>(a);
-    return cudaGetLastError();
-  }
   return launch_pdl(attn_mma_kernel, grid, dim3(kThreads), L.total, st, a);
 }
 

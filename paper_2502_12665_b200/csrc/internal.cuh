@@ -145,8 +145,8 @@ int lut_tile_nv(int nvec);
 struct SelArgs {
   const float* agg;             // [P, L]
   int32_t* hist;                // [P, L] or nullptr (counts of the LOCAL tokens' codes)
-  int append;                   // 1: token n_ctx-1 is encoded by this step's prep kernel: not in hist
-                                //    yet; select adds it after taking the counts
+  int append;                   // 1: token n_ctx-1 is encoded in this step: not in hist yet, code unread
+  int append_hist;              // 1: select adds it to hist after taking the counts
   const uint16_t* codes;        // [P, n_max] local code array (local index = global - shard_begin)
   int32_t* sel;                 // [P, sel_stride] selected global token indices, ascending
   int L, W, n_max, n_ctx, c0, c1, n_s, w0, keff, sel_stride;

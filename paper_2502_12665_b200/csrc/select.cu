@@ -488,7 +488,7 @@ __device__ uint32_t scan_emit(const SelArgs& a, SelShared& S, const uint32_t* tb
 // after this pair's counts were taken (end of the kernel, off the critical path)
 __device__ __forceinline__ void append_hist(const SelArgs& a, int pair, const uint16_t* cp_local) {
   const int lo = a.shard_begin, t = a.n_ctx - 1;
-  if (a.append && a.hist && threadIdx.x == 0 && t >= lo && t < lo + a.shard_len)
+  if (a.append_hist && a.hist && threadIdx.x == 0 && t >= lo && t < lo + a.shard_len)
     a.hist[(size_t)pair * a.L + cp_local[t - lo]] += 1;
 }
 
