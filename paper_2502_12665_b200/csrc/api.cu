@@ -91,7 +91,7 @@ void derive(const a2ats_shape* s, const a2ats_params* p, int n_ctx, Derived* d) 
 }
 
 struct DecodeWs {
-  size_t cs, agg, lut, sel, part, actr, cand_keep, pinfo, nsel, wlog, eslot, ectr, total;
+  size_t cs, agg, lut, sel, part, actr, cand_keep, pinfo, nsel, wlog, eslot, ectr, tblg, desc, done, total;
 };
 
 DecodeWs decode_layout(const a2ats_shape* s, const a2ats_params* p) {
@@ -115,6 +115,9 @@ DecodeWs decode_layout(const a2ats_shape* s, const a2ats_params* p) {
   w.wlog = o; o = align_up(o + (size_t)P * kWinPre * 8 * 4);
   w.eslot = o; o = align_up(o + (size_t)s->Hkv * std::max(s->B, 1) * 8);   // decode_step_append's encode
   w.ectr = o; o = align_up(o + (size_t)s->Hkv * 2 * 4);
+  w.tblg = o; o = align_up(o + (size_t)P * ((s->L + 15) / 16) * 4);                       // long-context select
+  w.desc = o; o = align_up(o + (size_t)P * (s->n_max / select_chunk_tokens() + 2) * 8);
+  w.done = o; o = align_up(o + (size_t)P * 4);
   w.total = o;
   return w;
 }
@@ -234,7 +237,8 @@ void prep_set_window(PrepArgs& p, const a2ats_shape* s, const void* k_cache, flo
   p.n_wl = std::max(0, std::min(n_w, kWinPre));
   p.shard_begin = shard_begin;
   p.scale_log2 = kScaleLog2;
-  p.n_win = p.n_wl > 0 ? s->B * s->Hkv : 0;
+  p.win_ppc = std::max(p.win_ppc, 1);
+  p.n_win = p.n_wl > 0 ? (s->B * s->Hkv + p.win_ppc - 1) / p.win_ppc : 0;
 }
 // decode-time encode of tokens [t_begin, t_begin + T) (B * T <= encode_cw_max() keys per head)
 void prep_set_encode(PrepArgs& p, const EncArgs& e, int tpc = 1) {
@@ -250,19 +254,31 @@ void prep_set_encode(PrepArgs& p, const EncArgs& e, int tpc = 1) {
 void prep_balance(PrepArgs& p) {
   const int per_sm = std::max(1, (227 * 1024) / (prep_smem_bytes(p) + 1024));
   const int cap = per_sm * sm_count();
-  for (int guard = 0; guard < 8 && p.n_lut + p.n_enc + p.n_win > cap; ++guard) {
-    if (p.n_enc && (p.enc_tpc <= p.lut_tpc || !p.n_lut) && p.enc_tpc < p.enc_tx)
+  const int npairs = p.lut.B * p.lut.Hkv;
+  for (int guard = 0; guard < 24 && p.n_lut + p.n_enc + p.n_win > cap; ++guard) {
+    // shrink the role with the most CTAs per unit of work first
+    if (p.n_win && p.n_win >= p.n_lut && p.n_win >= p.n_enc && p.win_ppc < npairs) {
+      p.win_ppc *= 2;
+      p.n_win = (npairs + p.win_ppc - 1) / p.win_ppc;
+    } else if (p.n_enc && p.n_enc >= p.n_lut && p.enc_tpc < p.enc_tx) {
       prep_set_encode(p, p.enc, p.enc_tpc * 2);
-    else if (p.n_lut && p.lut_tpc < p.lut_tx)
+    } else if (p.n_lut && p.lut_tpc < p.lut_tx) {
       prep_set_lut(p, p.lut, p.lut_tpc * 2);
-    else
+    } else if (p.n_enc && p.enc_tpc < p.enc_tx) {
+      prep_set_encode(p, p.enc, p.enc_tpc * 2);
+    } else if (p.n_win && p.win_ppc < npairs) {
+      p.win_ppc *= 2;
+      p.n_win = (npairs + p.win_ppc - 1) / p.win_ppc;
+    } else {
       break;
+    }
   }
 }
 
 PrepArgs prep_empty() {
   PrepArgs p;
   std::memset(&p, 0, sizeof(p));
+  p.lut_tpc = p.enc_tpc = p.win_ppc = 1;
   return p;
 }
 
@@ -429,7 +445,13 @@ int decode_impl(const a2ats_shape* shape, const a2ats_params* params, int32_t n_
   const LutArgs la = make_lut_args(shape, params, d, q, codebook, agg, lut_full, cs);
   PrepArgs p = prep_empty();
   prep_set_lut(p, la);
+  // long contexts: the window logits are computed by the select threshold kernel, before its
+  // dependency wait (it waits for this kernel anyway); otherwise by the prep kernel's window role
+  const int nchunk = d.c1 > d.c0 ? (d.c1 - ((d.c0 >> 3) << 3) + select_chunk_tokens() - 1) / select_chunk_tokens() : 0;
+  const bool split_select = d.keff > 0 && nchunk >= 2;
   prep_set_window(p, shape, k_cache, wlog, n_ctx, d.w0, d.n_w, 0);
+  const int n_wl = p.n_wl;
+  if (split_select) p.n_win = 0;
   CUtensorMap tmA, tmC;
   rc = cuda_status(make_tmap_sw128(&tmA, codebook, (uint64_t)shape->Hkv * shape->L, kD, 128));
   if (rc) return rc;
@@ -470,6 +492,24 @@ int decode_impl(const a2ats_shape* shape, const a2ats_params* params, int32_t n_
     sa.append_hist = append ? 1 : 0;
     sa.codes = codes;
     sa.sel = sel;
+    sa.pinfo = reinterpret_cast<uint32_t*>(base + Lw.pinfo);
+    sa.tblg = reinterpret_cast<uint32_t*>(base + Lw.tblg);
+    sa.desc = reinterpret_cast<unsigned long long*>(base + Lw.desc);
+    sa.done = reinterpret_cast<unsigned*>(base + Lw.done);
+    sa.nchunk = nchunk;
+    sa.B = shape->B;
+    sa.wlog = nullptr;
+    if (split_select) {
+      sa.wlog = wlog;
+      sa.q = static_cast<const uint16_t*>(q);
+      sa.kc = static_cast<const uint16_t*>(k_cache);
+      sa.Hq = shape->Hq;
+      sa.G = d.G;
+      sa.n_wl = n_wl;
+      sa.win_lo = d.w0;
+      sa.scale_log2 = kScaleLog2;
+      sa.rt = la.rt;
+    }
     sa.L = shape->L;
     sa.W = d.W;
     sa.n_max = shape->n_max;
@@ -483,7 +523,8 @@ int decode_impl(const a2ats_shape* shape, const a2ats_params* params, int32_t n_
     sa.shard_begin = 0;
     sa.shard_len = shape->n_max;
     sa.rank = 0;
-    rc = cuda_status(launch_select(sa, d.P, st));
+    // one CTA per pair while the candidates fit one code chunk; beyond, threshold + chunked scan
+    rc = cuda_status(split_select ? launch_select_split(sa, d.P, st) : launch_select(sa, d.P, st));
     if (rc) return rc;
   }
   stage_mark(2, st);
@@ -493,7 +534,7 @@ int decode_impl(const a2ats_shape* shape, const a2ats_params* params, int32_t n_
   aa.q = static_cast<const uint16_t*>(q);
   std::memcpy(aa.bcs, la.bcs, sizeof(aa.bcs));
   aa.wlog = wlog;
-  aa.n_wl = p.n_wl;
+  aa.n_wl = n_wl;
   aa.cs = cs;
   aa.kc = static_cast<const uint16_t*>(k_cache);
   aa.vc = static_cast<const uint16_t*>(v_cache);

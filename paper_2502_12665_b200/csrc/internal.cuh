@@ -149,7 +149,7 @@ struct SelArgs {
   int append_hist;              // 1: select adds it to hist after taking the counts
   const uint16_t* codes;        // [P, n_max] local code array (local index = global - shard_begin)
   int32_t* sel;                 // [P, sel_stride] selected global token indices, ascending
-  int L, W, n_max, n_ctx, c0, c1, n_s, w0, keff, sel_stride;
+  int L, W, n_max, n_ctx, c0, c1, n_s, w0, keff, sel_stride, B;
   // sequence sharding (single GPU: shard_begin = 0, shard_len = n_max)
   int shard_begin, shard_len, rank;
   int32_t* cand_out;            // [P, L] local candidate histogram, exchanged (all-reduce in place)
@@ -159,6 +159,19 @@ struct SelArgs {
   int32_t* counts_out;          // [P, 2] this rank's candidates above / at v*
   const int32_t* counts_all;    // [R, P, 2] all-gathered counts
   int32_t* nsel_out;            // [P] number of locally selected tokens
+  // long contexts (launch_select_split): per-pair class table, chunk descriptors, completion
+  uint32_t* tblg;               // [P, W] compact 2-bit classes
+  unsigned long long* desc;     // [P, nchunk] published (#above, #tied) per chunk, 0 = not yet
+  unsigned* done;               // [P]
+  int nchunk;
+  // window logits computed by the threshold kernel before its dependency wait (long contexts;
+  // otherwise the prep kernel's window role): wlog == nullptr disables
+  float* wlog;                  // [P, 64, 8]
+  const uint16_t* q;            // [B, Hq, 128]
+  const uint16_t* kc;           // [B, Hkv, n_max, 128]
+  int Hq, G, n_wl, win_lo;
+  float scale_log2;
+  RopeTab rt;
 };
 
 struct AttnArgs {
@@ -212,6 +225,7 @@ struct PrepArgs {
   const uint16_t* kc;          // [B, Hkv, n_max, 128] (local rows: global - shard_begin)
   float* wlog;                 // [P, 64, 8] base-2 scaled logits (heads >= G: 0)
   int n_max, n_ctx, win_lo, n_wl, shard_begin;
+  int win_ppc;                 // pairs per window CTA
   float scale_log2;
 };
 constexpr int kWinPre = 64;    // window rows per pair whose logits the prep kernel computes
@@ -225,6 +239,8 @@ cudaError_t launch_select(const SelArgs& a, int P, cudaStream_t st);
 cudaError_t launch_shard_hist(const SelArgs& a, int P, cudaStream_t st);
 cudaError_t launch_shard_thresh(const SelArgs& a, int P, cudaStream_t st);
 cudaError_t launch_shard_scan(const SelArgs& a, int P, cudaStream_t st);
+cudaError_t launch_select_split(const SelArgs& a, int P, cudaStream_t st);
+int select_chunk_tokens();
 cudaError_t launch_attention(const AttnArgs& a, int P, int GT, cudaStream_t st);
 cudaError_t launch_combine(const float* parts, int R, int rows, float* out, cudaStream_t st);
 cudaError_t launch_prepare(const uint16_t* codebook, const float* H, float* nrm, uint16_t* chat, int Hkv, int L,

@@ -192,31 +192,15 @@ __device__ __forceinline__ void lut_tile(const CUtensorMap& tmA, const PrepArgs&
   if (warp == 0) umma::tmem_dealloc_n(tmem, p.lut_cols);
 }
 
-// Window role: pair = (b, h).  Scratch (16-B chunks XOR-swizzled by row): cs [64][64]
-// float2, K rows [64][128] bf16, q (base-2 scaled) [8][128] fp32.
-__device__ __forceinline__ void window_tile(const PrepArgs& p, int pair, uint8_t* smem) {
+// Window role: pairs [pair0, pair0 + np) (the window rows, hence the rotation table, are
+// the same for every pair).  Scratch (16-B chunks XOR-swizzled by row): cs [64][64] float2,
+// K rows [64][128] bf16, q (base-2 scaled) [8][128] fp32.
+__device__ __forceinline__ void window_tile(const PrepArgs& p, int pair0, int np, uint8_t* smem) {
   const LutArgs& a = p.lut;
   const int tid = threadIdx.x, G = a.G, nw = p.n_wl;
-  const int b = pair / a.Hkv, h = pair - b * a.Hkv;
   float4* csS = reinterpret_cast<float4*>(smem);                // [64 rows][32 chunks of 2 (cos, sin)]
   uint4* kS = reinterpret_cast<uint4*>(smem + 32768);           // [64 rows][16 chunks of 8 bf16]
   float* sQ = reinterpret_cast<float*>(smem + 32768 + 16384);   // [8][128]
-  const uint8_t* kbase = reinterpret_cast<const uint8_t*>(p.kc) + (size_t)pair * p.n_max * 256;
-  {  // q of the group's heads, scaled to the base-2 logit domain (one 16-B load per thread)
-    const int g = tid >> 4, e0 = (tid & 15) * 8;
-    uint4 xq = make_uint4(0, 0, 0, 0);
-    if (g < G) xq = ld_nc_u4(a.q + ((size_t)b * a.Hq + h * G + g) * kD + e0);
-    const uint32_t w[4] = {xq.x, xq.y, xq.z, xq.w};
-    float4* d = reinterpret_cast<float4*>(sQ + g * kD + e0);
-    d[0] = make_float4(bf_lo(w[0]) * p.scale_log2, bf_hi(w[0]) * p.scale_log2, bf_lo(w[1]) * p.scale_log2,
-                       bf_hi(w[1]) * p.scale_log2);
-    d[1] = make_float4(bf_lo(w[2]) * p.scale_log2, bf_hi(w[2]) * p.scale_log2, bf_lo(w[3]) * p.scale_log2,
-                       bf_hi(w[3]) * p.scale_log2);
-  }
-  for (int k = tid; k < nw * 16; k += 128) {
-    const int row = k >> 4, c = k & 15;
-    kS[row * 16 + (c ^ (row & 7))] = ld_nc_u4(kbase + (size_t)(p.win_lo + row - p.shard_begin) * 256 + c * 16);
-  }
   {
     const int m = tid & 63, j0 = (tid >> 6) * 32;  // rows [j0, j0 + 32) of pair m
     if (j0 < nw) {
@@ -234,40 +218,68 @@ __device__ __forceinline__ void window_tile(const PrepArgs& p, int pair, uint8_t
       }
     }
   }
-  __syncthreads();
   const int row = tid & 63, hsel = tid >> 6;  // heads hsel, hsel + 2, ...
-  float acc[4] = {0.f, 0.f, 0.f, 0.f};
-  if (row < nw) {
 #pragma unroll 1
-    for (int mb = 0; mb < 8; ++mb) {  // m = 8 mb + i; pairs (m, m + 64)
-      const uint4 k1 = kS[row * 16 + (mb ^ (row & 7))];
-      const uint4 k2 = kS[row * 16 + ((mb + 8) ^ (row & 7))];
-      const uint32_t w1[4] = {k1.x, k1.y, k1.z, k1.w}, w2[4] = {k2.x, k2.y, k2.z, k2.w};
-      float4 t[4];
+  for (int pair = pair0; pair < pair0 + np; ++pair) {
+    const int b = pair / a.Hkv, h = pair - b * a.Hkv;
+    const uint8_t* kbase = reinterpret_cast<const uint8_t*>(p.kc) + (size_t)pair * p.n_max * 256;
+    {  // q of the group's heads, scaled to the base-2 logit domain (one 16-B load per thread)
+      const int g = tid >> 4, e0 = (tid & 15) * 8;
+      uint4 xq = make_uint4(0, 0, 0, 0);
+      if (g < G) xq = ld_nc_u4(a.q + ((size_t)b * a.Hq + h * G + g) * kD + e0);
+      const uint32_t w[4] = {xq.x, xq.y, xq.z, xq.w};
+      float4* d = reinterpret_cast<float4*>(sQ + g * kD + e0);
+      d[0] = make_float4(bf_lo(w[0]) * p.scale_log2, bf_hi(w[0]) * p.scale_log2, bf_lo(w[1]) * p.scale_log2,
+                         bf_hi(w[1]) * p.scale_log2);
+      d[1] = make_float4(bf_lo(w[2]) * p.scale_log2, bf_hi(w[2]) * p.scale_log2, bf_lo(w[3]) * p.scale_log2,
+                         bf_hi(w[3]) * p.scale_log2);
+    }
+    for (int k = tid; k < nw * 16; k += 128) {
+      const int r = k >> 4, c = k & 15;
+      kS[r * 16 + (c ^ (r & 7))] = ld_nc_u4(kbase + (size_t)(p.win_lo + r - p.shard_begin) * 256 + c * 16);
+    }
+    __syncthreads();
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    if (row < nw) {
+#pragma unroll 1
+      for (int mb = 0; mb < 8; ++mb) {  // m = 8 mb + i; pairs (m, m + 64)
+        const uint4 k1 = kS[row * 16 + (mb ^ (row & 7))];
+        const uint4 k2 = kS[row * 16 + ((mb + 8) ^ (row & 7))];
+        const uint32_t w1[4] = {k1.x, k1.y, k1.z, k1.w}, w2[4] = {k2.x, k2.y, k2.z, k2.w};
+        float4 t[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) t[j] = csS[row * 32 + ((mb * 4 + j) ^ (row & 7))];
+        for (int j = 0; j < 4; ++j) t[j] = csS[row * 32 + ((mb * 4 + j) ^ (row & 7))];
 #pragma unroll
-      for (int hh = 0; hh < 4; ++hh) {
-        const int g = hsel + 2 * hh;
-        if (g < G) {
-          const float* qa = sQ + g * kD + mb * 8;
+        for (int hh = 0; hh < 4; ++hh) {
+          const int g = hsel + 2 * hh;
+          if (g < G) {
+            const float* qa = sQ + g * kD + mb * 8;
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const float ka = (e & 1) ? bf_hi(w1[e >> 1]) : bf_lo(w1[e >> 1]);
-            const float kb = (e & 1) ? bf_hi(w2[e >> 1]) : bf_lo(w2[e >> 1]);
-            const float cv = (e & 1) ? t[e >> 1].z : t[e >> 1].x, sv = (e & 1) ? t[e >> 1].w : t[e >> 1].y;
-            const float q1 = qa[e], q2 = qa[e + kHalf];
-            acc[hh] = fmaf(cv, fmaf(q1, ka, q2 * kb), fmaf(sv, fmaf(q1, kb, -q2 * ka), acc[hh]));
+            for (int e = 0; e < 8; ++e) {
+              const float ka = (e & 1) ? bf_hi(w1[e >> 1]) : bf_lo(w1[e >> 1]);
+              const float kb = (e & 1) ? bf_hi(w2[e >> 1]) : bf_lo(w2[e >> 1]);
+              const float cv = (e & 1) ? t[e >> 1].z : t[e >> 1].x, sv = (e & 1) ? t[e >> 1].w : t[e >> 1].y;
+              const float q1 = qa[e], q2 = qa[e + kHalf];
+              acc[hh] = fmaf(cv, fmaf(q1, ka, q2 * kb), fmaf(sv, fmaf(q1, kb, -q2 * ka), acc[hh]));
+            }
           }
         }
       }
     }
-  }
-  pdl_wait();  // the previous step's attention reads wlog
-  pdl_trigger();
-  if (row < nw) {
+    if (pair == pair0) {
+      pdl_wait();  // the previous step's attention reads wlog
+      pdl_trigger();
+    }
+    if (row < nw) {
 #pragma unroll
-    for (int hh = 0; hh < 4; ++hh) p.wlog[((size_t)pair * kWinPre + row) * 8 + hsel + 2 * hh] = acc[hh];  // heads >= G: 0
+      for (int hh = 0; hh < 4; ++hh)
+        p.wlog[((size_t)pair * kWinPre + row) * 8 + hsel + 2 * hh] = acc[hh];  // heads >= G: 0
+    }
+    __syncthreads();  // q / K scratch reused by the next pair
+  }
+  if (np == 0) {
+    pdl_wait();
+    pdl_trigger();
   }
 }
 
@@ -285,7 +297,10 @@ __global__ __launch_bounds__(128, 1) void prep_kernel(const __grid_constant__ CU
     encode_tiles(tmC, p.enc, cx * p.enc_tpc, min(p.enc_tx, (cx + 1) * p.enc_tpc), i / cx_n, cx_n, p.enc_nv,
                  p.enc_cols, smem);
   } else {
-    window_tile(p, i - p.n_enc, smem);
+    i -= p.n_enc;
+    const int npairs = p.lut.B * p.lut.Hkv;
+    const int pair0 = i * p.win_ppc;
+    window_tile(p, pair0, max(0, min(p.win_ppc, npairs - pair0)), smem);
   }
   A2ATS_TL(g_prep_tl, 1);
 }
@@ -326,7 +341,7 @@ int prep_smem_bytes(const PrepArgs& p) {
   return smem + 1024;  // alignment slack for the SW128 slabs
 }
 
-int lut_tile_nv(int nvec) { return nvec >= 256 ? 256 : ((nvec + 15) / 16) * 16; }  // MMA N: multiple of 16
+int lut_tile_nv(int nvec) { return nvec >= 128 ? 128 : ((nvec + 15) / 16) * 16; }  // MMA N: multiple of 16, <= 128 (B tile <= 64 KB)
 int prep_lut_cols(int NV) { return (int)umma::tmem_cols_for(NV); }
 
 cudaError_t launch_prep(const PrepArgs& p, const CUtensorMap& tmA, const CUtensorMap& tmC, cudaStream_t st) {

@@ -30,6 +30,7 @@ namespace a2ats {
 
 namespace {
 A2ATS_TL_DECL(g_sel_tl)
+A2ATS_TL_DECL(g_selc_tl)
 A2ATS_PHASE_DECL(g_sel_phase)
 
 constexpr int kNT = 512;             // threads per CTA
@@ -39,16 +40,29 @@ constexpr int kCH = kNT * kTPT;      // tokens per chunk (32768: 16-bit scan fie
 constexpr int kSurvCap = 2048;       // survivor list capacity
 constexpr int kRankMax = kNT;        // survivors ranked directly (one thread each)
 
-enum SelMode { kFused = 0, kShardHist = 1, kShardThresh = 2, kShardScan = 3 };
+// kFused: one CTA per pair does everything (contexts of one code chunk).  Long contexts
+// split it: kThresh (per pair: counts, v*, m, compact class table to global) then kScanC
+// (per (pair, chunk of 32768 tokens): classify, publish the chunk's counts, look back at
+// the pair's earlier chunks for the output offsets, emit).
+enum SelMode { kFused = 0, kShardHist = 1, kShardThresh = 2, kShardScan = 3, kThresh = 4, kScanC = 5 };
+
+constexpr int kWinScratch = 32768 + 16384 + 8 * kD * 4;  // window logits scratch (threshold kernel)
+
+template <int MODE>
+struct ModeTraits {
+  static constexpr bool surv = (MODE == kFused || MODE == kShardThresh || MODE == kThresh);  // find_level
+  static constexpr bool codes = (MODE == kFused || MODE == kShardScan || MODE == kScanC);    // code chunk
+  static constexpr int extra = (MODE == kThresh) ? kWinScratch : 0;  // bytes after the survivors
+  static constexpr int min_blocks = (MODE == kThresh || MODE == kScanC) ? 2 : 1;
+};
 
 struct SelShared {
   int bins[256];
   uint32_t wsum[kNW];
-  uint32_t skey[kSurvCap];
-  int scnt[kSurvCap];
   int s_digit, s_kk, s_nsurv, s_total;
   uint32_t s_kmin, s_kmax, s_kstar, s_m;
   int s_gt, s_eq;
+  uint32_t s_before[2];
 };
 
 // cnt[l] = hist[l] - #(local sink/window tokens with code l)   (hist given)
@@ -175,7 +189,8 @@ __device__ __forceinline__ void pick_digit(SelShared& S, int kk) {
 // Count-weighted selection of the keff-th smallest key over cnt / key (all threads),
 // given the key range S.s_kmin..S.s_kmax.  Result in S.s_kstar (key of v*) and
 // S.s_m (tie quota, >= 1).
-__device__ void find_level(const SelArgs& a, SelShared& S, const int* cnt, const uint32_t* key, int keff) {
+__device__ void find_level(const SelArgs& a, SelShared& S, const int* cnt, const uint32_t* key, int keff,
+                           uint32_t* skey, int* scnt) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t kmn = S.s_kmin, kmx = S.s_kmax;
   if (kmn == kmx) {  // a single level holds every candidate
@@ -222,8 +237,8 @@ __device__ void find_level(const SelArgs& a, SelShared& S, const int* cnt, const
       base = __shfl_sync(0xffffffffu, base, 0);
       const int slot = base + __popc(bal & ((1u << lane) - 1u));
       if (keep && slot < kSurvCap) {
-        S.skey[slot] = key[l];
-        S.scnt[slot] = cnt[l];
+        skey[slot] = key[l];
+        scnt[slot] = cnt[l];
       }
     }
   }
@@ -234,12 +249,12 @@ __device__ void find_level(const SelArgs& a, SelShared& S, const int* cnt, const
     // rank each survivor directly: v* is the key with #(< v*) < kk <= #(<= v*);
     // equal keys write equal values
     if (tid < nsurv) {
-      const uint32_t ki = S.skey[tid];
+      const uint32_t ki = skey[tid];
       int less = 0, leq = 0;
 #pragma unroll 4
       for (int j = 0; j < nsurv; ++j) {
-        const uint32_t kj = S.skey[j];
-        const int cj = S.scnt[j];
+        const uint32_t kj = skey[j];
+        const int cj = scnt[j];
         less += (kj < ki) ? cj : 0;
         leq += (kj <= ki) ? cj : 0;
       }
@@ -256,8 +271,8 @@ __device__ void find_level(const SelArgs& a, SelShared& S, const int* cnt, const
       // exact K-th key among the survivors: radix passes from their first differing bit
       uint32_t sa = 0xffffffffu, so = 0u;
       for (int i = lane; i < nsurv; i += 32) {
-        sa &= S.skey[i];
-        so |= S.skey[i];
+        sa &= skey[i];
+        so |= skey[i];
       }
       sa = __reduce_and_sync(0xffffffffu, sa);
       so = __reduce_or_sync(0xffffffffu, so);
@@ -272,8 +287,8 @@ __device__ void find_level(const SelArgs& a, SelShared& S, const int* cnt, const
           for (int i = lane; i < 256; i += 32) S.bins[i] = 0;
           __syncwarp();
           for (int i = lane; i < nsurv; i += 32) {
-            const uint32_t k = S.skey[i];
-            if ((k & mask) == prefix) atomicAdd(&S.bins[(k >> shift) & 255u], S.scnt[i]);
+            const uint32_t k = skey[i];
+            if ((k & mask) == prefix) atomicAdd(&S.bins[(k >> shift) & 255u], scnt[i]);
           }
           __syncwarp();
           pick_digit(S, kk);
@@ -492,6 +507,230 @@ __device__ __forceinline__ void append_hist(const SelArgs& a, int pair, const ui
     a.hist[(size_t)pair * a.L + cp_local[t - lo]] += 1;
 }
 
+// Window logits of the pair (Eq. 11 local rows: u_j = (q R_{i-j}) . k_j, exact per-row
+// rotation on FP32 cores, base-2 scaled) for its first n_wl window tokens, from step inputs
+// only; written to wlog for the attention.  512 threads; scratch: cs [64][64] float2 (fp64
+// angle per 8 rows, then fp64 rotations by -f_m), K rows [64][16 chunks] and q [8][128]
+// fp32, 16-B chunks XOR-swizzled by row.  Same arithmetic as the prep kernel's window role.
+__device__ void window_logits(const SelArgs& a, int pair, uint8_t* scratch, float* out_acc) {
+  const int tid = threadIdx.x, nw = a.n_wl, G = a.G;
+  const int Hkv = gridDim.x / a.B;  // (threshold kernel: one CTA per pair)
+  const int b = pair / Hkv, h = pair - b * Hkv;
+  float4* csS = reinterpret_cast<float4*>(scratch);
+  uint4* kS = reinterpret_cast<uint4*>(scratch + 32768);
+  float* sQ = reinterpret_cast<float*>(scratch + 32768 + 16384);
+  const uint8_t* kbase = reinterpret_cast<const uint8_t*>(a.kc) + (size_t)pair * a.n_max * 256;
+  if (tid < 128) {
+    const int g = tid >> 4, e0 = (tid & 15) * 8;
+    uint4 xq = make_uint4(0, 0, 0, 0);
+    if (g < G) xq = ld_nc_u4(a.q + ((size_t)b * a.Hq + h * G + g) * kD + e0);
+    const uint32_t w[4] = {xq.x, xq.y, xq.z, xq.w};
+    float4* d = reinterpret_cast<float4*>(sQ + g * kD + e0);
+    d[0] = make_float4(bf_lo(w[0]) * a.scale_log2, bf_hi(w[0]) * a.scale_log2, bf_lo(w[1]) * a.scale_log2,
+                       bf_hi(w[1]) * a.scale_log2);
+    d[1] = make_float4(bf_lo(w[2]) * a.scale_log2, bf_hi(w[2]) * a.scale_log2, bf_lo(w[3]) * a.scale_log2,
+                       bf_hi(w[3]) * a.scale_log2);
+  }
+  for (int k = tid; k < nw * 16; k += kNT) {
+    const int r = k >> 4, c = k & 15;
+    kS[r * 16 + (c ^ (r & 7))] = ld_nc_u4(kbase + (size_t)(a.win_lo + r - a.shard_begin) * 256 + c * 16);
+  }
+  {
+    const int m = tid & 63, j0 = (tid >> 6) * 8;  // rows [j0, j0 + 8) of pair m
+    if (j0 < nw) {
+      const double f = a.rt.inv_freq[m];
+      double sn, cn, sf, cf;
+      sincos((double)(a.n_ctx - 1 - (a.win_lo + j0)) * f, &sn, &cn);  // r = i - t, t = win_lo + row
+      sincos(f, &sf, &cf);
+      float2* cs2 = reinterpret_cast<float2*>(csS);
+#pragma unroll 1
+      for (int row = j0; row < min(j0 + 8, nw); ++row) {
+        cs2[row * 64 + (((m >> 1) ^ (row & 7)) << 1) + (m & 1)] = make_float2((float)cn, (float)sn);
+        const double c2 = cn * cf + sn * sf, s2 = sn * cf - cn * sf;  // r -> r - 1
+        cn = c2;
+        sn = s2;
+      }
+    }
+  }
+  __syncthreads();
+  const int row = tid & 63, g = tid >> 6;  // one (row, head) per thread
+  float acc = 0.f;
+  if (row < nw && g < G) {
+#pragma unroll 1
+    for (int mb = 0; mb < 8; ++mb) {  // m = 8 mb + i; pairs (m, m + 64)
+      const uint4 k1 = kS[row * 16 + (mb ^ (row & 7))];
+      const uint4 k2 = kS[row * 16 + ((mb + 8) ^ (row & 7))];
+      const uint32_t w1[4] = {k1.x, k1.y, k1.z, k1.w}, w2[4] = {k2.x, k2.y, k2.z, k2.w};
+      float4 t[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) t[j] = csS[row * 32 + ((mb * 4 + j) ^ (row & 7))];
+      const float* qa = sQ + g * kD + mb * 8;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float ka = (e & 1) ? bf_hi(w1[e >> 1]) : bf_lo(w1[e >> 1]);
+        const float kb = (e & 1) ? bf_hi(w2[e >> 1]) : bf_lo(w2[e >> 1]);
+        const float cv = (e & 1) ? t[e >> 1].z : t[e >> 1].x, sv = (e & 1) ? t[e >> 1].w : t[e >> 1].y;
+        const float q1 = qa[e], q2 = qa[e + kHalf];
+        acc = fmaf(cv, fmaf(q1, ka, q2 * kb), fmaf(sv, fmaf(q1, kb, -q2 * ka), acc));
+      }
+    }
+  }
+  *out_acc = acc;
+}
+
+// Long contexts (several code chunks per pair), single GPU.
+//   kThresh (grid P): counts, v*, m -> pinfo; compact 2-bit class table -> tblg.
+//   kScanC (grid P x nchunk): one 32768-token chunk; classify, publish the chunk's
+//   (#above, #tied) with a release store, sum the pair's earlier chunks' counts (they have
+//   lower block indices, so they are resident or done: the wait terminates), emit; the
+//   pair's last chunk re-arms the descriptors.
+template <int MODE>
+__device__ __forceinline__ void split_body(const SelArgs& a, SelShared& S, int* cnt, uint32_t* key, uint32_t* tbl,
+                                           uint32_t* skey, int* scnt, uint4* sC) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (MODE == kThresh) {
+    const int pair = blockIdx.x;
+    const uint16_t* cp_local = a.codes + (size_t)pair * a.n_max;
+    float wacc = 0.f;
+    if (a.wlog) window_logits(a, pair, reinterpret_cast<uint8_t*>(scnt + kSurvCap), &wacc);
+    load_cnt(a, pair, cnt, cp_local);
+    pdl_wait();  // agg comes from the LUT kernel
+    pdl_trigger();
+    if (a.wlog && (tid & 63) < a.n_wl)
+      a.wlog[((size_t)pair * 64 + (tid & 63)) * 8 + (tid >> 6)] = wacc;  // heads >= G: 0
+    uint32_t kstar = 0, m = 0;
+    if (a.keff > 0) {
+      load_keys(a, S, pair, cnt, key);
+      find_level(a, S, cnt, key, a.keff, skey, scnt);
+      kstar = S.s_kstar;
+      m = S.s_m;
+      for (int w = tid; w < a.W; w += kNT) {  // compact class table: 16 codewords x 2 bits per word
+        uint32_t x = 0;
+#pragma unroll 1
+        for (int e = 0; e < 16 && w * 16 + e < a.L; ++e) {
+          const uint32_t k = key[w * 16 + e];
+          x |= ((k < kstar) ? 1u : ((k == kstar) ? 2u : 0u)) << (2 * e);
+        }
+        a.tblg[(size_t)pair * a.W + w] = x;
+      }
+    }
+    if (tid == 0) {
+      a.pinfo[pair * 4 + 0] = kstar;
+      a.pinfo[pair * 4 + 1] = m;
+      a.pinfo[pair * 4 + 2] = (uint32_t)a.keff;
+    }
+    append_hist(a, pair, cp_local);
+    return;
+  }
+  // kScanC
+  const int pair = blockIdx.x / a.nchunk, ch = blockIdx.x - pair * a.nchunk;
+  const uint16_t* cp_local = a.codes + (size_t)pair * a.n_max;
+  const int c0 = a.c0, c1 = a.c1;
+  const int cb = ((c0 >> 3) << 3) + ch * kCH;
+  if (cb < c1) prefetch_chunk(a, cp_local, cb, c1, sC);
+  pdl_wait();  // pinfo / tblg come from kThresh
+  pdl_trigger();
+  const uint32_t kstar = __ldcg(a.pinfo + pair * 4 + 0), m = __ldcg(a.pinfo + pair * 4 + 1);
+  const uint32_t cap = __ldcg(a.pinfo + pair * 4 + 2);
+  if (cap == 0 || cb >= c1) {
+    cp_async_wait<0>();
+    return;
+  }
+  for (int it = tid; it < a.W * 2; it += kNT) {  // class table, replicated 32x (2 threads per word)
+    const int w = it >> 1;
+    const uint32_t x = __ldcg(a.tblg + (size_t)pair * a.W + w);
+    uint4* dst = reinterpret_cast<uint4*>(tbl + w * 32 + (it & 1) * 16);
+    const uint4 v = make_uint4(x, x, x, x);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) dst[(q + w) & 3] = v;
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+  const int t0 = cb + tid * kTPT;
+  uint32_t p0 = 0u, p1 = 0u, p2 = 0u, p3 = 0u;
+#pragma unroll 1
+  for (int k = 0; k < 4; ++k) {
+    const uint4 xa = sC[tid * 8 + ((2 * k) ^ (tid & 7))];
+    const uint4 xb = sC[tid * 8 + ((2 * k + 1) ^ (tid & 7))];
+    const uint32_t w8[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+    uint32_t cur = 0u;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const uint32_t code = (w8[e >> 1] >> ((e & 1) * 16)) & 0xffffu;
+      const uint32_t word = tbl[((code >> 4) << 5) + lane];
+      cur |= ((word >> ((code & 15u) * 2u)) & 3u) << (2 * e);
+    }
+    const int tb = t0 + 16 * k;
+    if (tb < c0 || tb + 16 > c1) cur &= span_mask(c0 - tb, c1 - tb);
+    p0 = p1;
+    p1 = p2;
+    p2 = p3;
+    p3 = cur;
+  }
+  uint32_t pk = (uint32_t)__popc(p0 & 0x55555555u) + (uint32_t)__popc(p1 & 0x55555555u) +
+                (uint32_t)__popc(p2 & 0x55555555u) + (uint32_t)__popc(p3 & 0x55555555u);
+  pk |= ((uint32_t)__popc(p0 & 0xaaaaaaaau) + (uint32_t)__popc(p1 & 0xaaaaaaaau) +
+         (uint32_t)__popc(p2 & 0xaaaaaaaau) + (uint32_t)__popc(p3 & 0xaaaaaaaau)) << 16;
+  uint32_t incl = pk;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += y;
+  }
+  if (lane == 31) S.wsum[warp] = incl;
+  __syncthreads();
+  uint32_t pre = 0, tot = 0;
+#pragma unroll
+  for (int w = 0; w < kNW; ++w) {
+    const uint32_t v = S.wsum[w];
+    pre += (w < warp) ? v : 0u;
+    tot += v;
+  }
+  unsigned long long* desc = a.desc + (size_t)pair * a.nchunk;
+  if (tid == 0) {  // publish this chunk's counts, then sum the earlier chunks'
+    st_release_u64(desc + ch, (1ull << 63) | ((unsigned long long)(tot >> 16) << 31) | (tot & 0xffffu));
+    uint32_t gb = 0, eb = 0;
+#pragma unroll 1
+    for (int c = 0; c < ch; ++c) {
+      unsigned long long v;
+      while (!((v = ld_acquire_u64(desc + c)) >> 63)) __nanosleep(32);
+      gb += (uint32_t)(v & 0x7fffffffull);
+      eb += (uint32_t)((v >> 31) & 0x7fffffffull);
+    }
+    S.s_before[0] = gb;
+    S.s_before[1] = eb;
+  }
+  __syncthreads();
+  const uint32_t ex = pre + incl - pk;
+  uint32_t gb = S.s_before[0] + (ex & 0xffffu), eb = S.s_before[1] + (ex >> 16);
+  int32_t* selp = a.sel + (size_t)pair * a.sel_stride;
+  uint32_t e0 = p0, e1 = p1, e2 = p2, e3 = p3;
+#pragma unroll 1
+  for (int w = 0; w < 4; ++w) {
+    uint32_t q = e0;
+    e0 = e1;
+    e1 = e2;
+    e2 = e3;
+    while (q) {  // selected / tied tokens in increasing token order
+      const int bit = __ffs(q) - 1, j = bit >> 1;
+      q &= ~(3u << (2 * j));
+      const int t = t0 + 16 * w + j;
+      if ((bit & 1) == 0) {
+        const uint32_t pos = gb + min(eb, m);
+        if (pos < cap) selp[pos] = t;
+        ++gb;
+      } else {
+        if (eb < m && gb + eb < cap) selp[gb + eb] = t;
+        ++eb;
+      }
+    }
+  }
+  if (tid == 0 && atomicAdd(a.done + pair, 1u) == (unsigned)a.nchunk - 1) {  // every chunk has looked back
+    for (int c = 0; c < a.nchunk; ++c) desc[c] = 0ull;
+    a.done[pair] = 0u;
+  }
+}
+
 template <int MODE>
 __device__ __forceinline__ void select_body(const SelArgs& a) {
   extern __shared__ __align__(16) uint32_t sm[];
@@ -499,8 +738,14 @@ __device__ __forceinline__ void select_body(const SelArgs& a) {
   int* cnt = reinterpret_cast<int*>(sm);  // [L]
   uint32_t* key = sm + ((a.L + 3) & ~3);  // [L], 16-B aligned
   uint32_t* tbl = sm;                     // [W*32], aliases cnt/key once they are dead
-  const int tbl_words = max(((a.L + 3) & ~3) + a.L, a.W * 32);
-  uint4* sC = reinterpret_cast<uint4*>(sm + (tbl_words + 3) / 4 * 4);  // [kCH / 8] one chunk of codes
+  const int tbl_words = (max(((a.L + 3) & ~3) + a.L, a.W * 32) + 3) / 4 * 4;
+  uint32_t* skey = sm + tbl_words;                                   // [kSurvCap] (find_level modes)
+  int* scnt = reinterpret_cast<int*>(skey + kSurvCap);              // [kSurvCap]
+  uint4* sC = reinterpret_cast<uint4*>(sm + tbl_words + (ModeTraits<MODE>::surv ? 2 * kSurvCap : 0));  // [kCH / 8]
+  if (MODE == kThresh || MODE == kScanC) {
+    split_body<MODE>(a, S, cnt, key, tbl, skey, scnt, sC);
+    return;
+  }
 
   const int tid = threadIdx.x;
   const int pair = blockIdx.x;
@@ -535,7 +780,7 @@ __device__ __forceinline__ void select_body(const SelArgs& a) {
     const int keff = min(a.keff, S.s_total);
     uint32_t kstar = 0, m = 0;
     if (keff > 0) {
-      find_level(a, S, cnt, key, keff);
+      find_level(a, S, cnt, key, keff, skey, scnt);
       kstar = S.s_kstar;
       m = S.s_m;
     }
@@ -585,7 +830,7 @@ __device__ __forceinline__ void select_body(const SelArgs& a) {
     }
     load_keys(a, S, pair, cnt, key);
     A2ATS_PHASE(g_sel_phase, 2);
-    find_level(a, S, cnt, key, a.keff);
+    find_level(a, S, cnt, key, a.keff, skey, scnt);
     A2ATS_PHASE(g_sel_phase, 5);
     kstar = S.s_kstar;
     m = S.s_m;
@@ -619,16 +864,25 @@ __device__ __forceinline__ void select_body(const SelArgs& a) {
 }
 
 template <int MODE>
-__global__ __launch_bounds__(kNT, 1) void select_kernel(SelArgs a) {
-  A2ATS_TL(g_sel_tl, 0);
+__global__ __launch_bounds__(kNT, ModeTraits<MODE>::min_blocks) void select_kernel(SelArgs a) {
+  if (MODE == kScanC) {
+    A2ATS_TL(g_selc_tl, 0);
+  } else {
+    A2ATS_TL(g_sel_tl, 0);
+  }
   select_body<MODE>(a);
-  A2ATS_TL(g_sel_tl, 1);
+  if (MODE == kScanC) {
+    A2ATS_TL(g_selc_tl, 1);
+  } else {
+    A2ATS_TL(g_sel_tl, 1);
+  }
 }
 
 template <int MODE>
-cudaError_t launch_mode(const SelArgs& a, int P, cudaStream_t st) {
-  const int tbl_words = max(((a.L + 3) & ~3) + a.L, a.W * 32);
-  const int smem = (tbl_words + 3) / 4 * 4 * 4 + kCH * 2;
+cudaError_t launch_mode(const SelArgs& a, int P, cudaStream_t st) {  // P: CTAs
+  const int tbl_words = (max(((a.L + 3) & ~3) + a.L, a.W * 32) + 3) / 4 * 4;
+  const int smem = tbl_words * 4 + (ModeTraits<MODE>::surv ? 2 * kSurvCap * 4 : 0) +
+                   (ModeTraits<MODE>::codes ? kCH * 2 : 0) + ModeTraits<MODE>::extra;
   static int smem_set = -1;
   if (smem_set < smem) {
     cudaError_t e = cudaFuncSetAttribute(select_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -646,8 +900,15 @@ cudaError_t launch_shard_thresh(const SelArgs& a, int P, cudaStream_t st) {
   return launch_mode<kShardThresh>(a, P, st);
 }
 cudaError_t launch_shard_scan(const SelArgs& a, int P, cudaStream_t st) { return launch_mode<kShardScan>(a, P, st); }
+cudaError_t launch_select_split(const SelArgs& a, int P, cudaStream_t st) {
+  cudaError_t e = launch_mode<kThresh>(a, P, st);
+  if (e != cudaSuccess) return e;
+  return launch_mode<kScanC>(a, P * a.nchunk, st);
+}
+int select_chunk_tokens() { return kCH; }
 
 }  // namespace a2ats
 
 A2ATS_PHASE_EXPORT(a2ats_debug_select_phases, a2ats::g_sel_phase)
 A2ATS_TL_EXPORT(a2ats_debug_select_timeline, a2ats::g_sel_tl)
+A2ATS_TL_EXPORT(a2ats_debug_selc_timeline, a2ats::g_selc_tl)

@@ -103,6 +103,22 @@ def test_multi_tile_integer_ties_gqa():
     check_against_oracle(cfg, inp, gpu, bridge=0)
 
 
+LONG = Config("long", B=2, Hq=8, Hkv=2, d=128, N=70001, L=1000, K=4200)
+
+
+@pytest.mark.parametrize("use_hist", [True, False])
+def test_long_context_chunked_select(use_hist):
+    # 3 code chunks per pair: threshold kernel + chunked scan with the cross-chunk look-back
+    inp, gpu, _ = run_case(LONG, seed=23, use_hist=use_hist, scores=False)
+    check_against_oracle(LONG, inp, gpu)
+
+
+def test_long_context_integer_ties_across_chunks():
+    cfg = LONG.with_(L=300, K=9000)
+    inp, gpu, _ = run_case(cfg, seed=24, family="g1", bridge=0, code_dist="zipf", scores=False)
+    check_against_oracle(cfg, inp, gpu, bridge=0)
+
+
 @pytest.mark.parametrize("G", [1, 2, 4, 8])
 def test_gqa_group_sizes(G):
     cfg = Config("gqa", B=2, Hq=2 * G, Hkv=2, d=128, N=3000, L=512, K=180)

@@ -39,7 +39,7 @@ scratch = torch.zeros_like(codes)
 out = torch.empty((cfg.B, cfg.Hq, 128), device="cuda")
 lib = A.load()
 KMAX = 8192
-kernels = ["prep", "select", "attn"]
+kernels = ["prep", "select", "selc", "attn"]
 fns = {}
 for k in kernels:
     f = getattr(lib, f"a2ats_debug_{k}_timeline")
@@ -61,16 +61,17 @@ for it in range(args.iters):
     if it == 0:
         continue
     # CTAs written in this step: end >= start and start after the previous marks
-    t0 = min(int(tl[k][tl[k][:, 0] > 0][:, 0].max()) for k in kernels)  # placeholder, refined below
     valid = {}
     for k in kernels:
         a = tl[k]
         last = a[:, 0].max()
-        m = (a[:, 0] > last - 2_000_000) & (a[:, 1] >= a[:, 0])  # this step's CTAs (within 2 ms)
+        m = (a[:, 0] > last - 2_000_000) & (a[:, 1] >= a[:, 0]) & (a[:, 0] > 0)  # this step's CTAs
         valid[k] = np.nonzero(m)[0]
-    t0 = min(tl[k][valid[k], 0].min() for k in kernels)
+    t0 = min(tl[k][valid[k], 0].min() for k in kernels if len(valid[k]))
     print(f"--- iter {it} (us from first CTA start)")
     for k in kernels:
+        if not len(valid[k]):
+            continue
         a = tl[k][valid[k]]
         st, en = (a[:, 0] - t0) / 1e3, (a[:, 1] - t0) / 1e3
         du = en - st
