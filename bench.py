@@ -123,6 +123,18 @@ def stage_model(cfg, n_ctx: int, k: int):
     }
 
 
+def scoring_line(cfg, r, pk):
+    from synth import budget_k
+    n = r["n_last"]
+    P = cfg.B * cfg.Hkv
+    k = budget_k(n)
+    ms = r["stage_ms"].get("prep", 0.0) + r["stage_ms"].get("select", 0.0)
+    score_bytes = P * n * 2 + cfg.Hkv * cfg.L * cfg.d * 2 + P * k * 4
+    return {"tokens_per_s": P * n / (ms * 1e-3) if ms > 0 else None, "ms": ms, "score_topk_bytes": score_bytes,
+            "hbm_frac": (score_bytes / (ms * 1e-3) / 1e9 / pk["hbm"]) if ms > 0 else None,
+            "note": "t = prep (a0 + a1 + a2 + window logits) + select (a3 + a4), eager profiling pass"}
+
+
 # ---------------------------------------------------------------------------- our arm
 def run_ours(args, rank: int, world: int):
     import torch
@@ -463,6 +475,10 @@ def main():
                    "sparsity": (budget_k(r["n_last"]) + 68) / r["n_last"], "aux_mem": 2 / (cfg.d * 2)},
         "roofline": roof,
         "kernels": kernels,
+        # SURVEY 8d's headline split: approx-scored tokens/s over t(a2 + a3 + a4) = prep + select
+        # stages of the profiling pass, and the score + top-K algorithmic bytes (codes once,
+        # codebook once, selection out) against the HBM peak
+        "scoring": scoring_line(cfg, r, pk),
         "profiled_step_ms": r["prof_step_ms"],
         "cpu_baseline": cpu,
         "e2e": r["e2e"],

@@ -91,7 +91,7 @@ void derive(const a2ats_shape* s, const a2ats_params* p, int n_ctx, Derived* d) 
 }
 
 struct DecodeWs {
-  size_t cs, agg, lut, sel, part, actr, cand_keep, pinfo, nsel, wlog, eslot, ectr, tblg, desc, done, total;
+  size_t cs, agg, lut, sel, part, actr, cand_keep, pinfo, nsel, wlog, eslot, ectr, tblg, desc, total;
 };
 
 DecodeWs decode_layout(const a2ats_shape* s, const a2ats_params* p) {
@@ -117,7 +117,6 @@ DecodeWs decode_layout(const a2ats_shape* s, const a2ats_params* p) {
   w.ectr = o; o = align_up(o + (size_t)s->Hkv * 2 * 4);
   w.tblg = o; o = align_up(o + (size_t)P * ((s->L + 15) / 16) * 4);                       // long-context select
   w.desc = o; o = align_up(o + (size_t)P * (s->n_max / select_chunk_tokens() + 2) * 8);
-  w.done = o; o = align_up(o + (size_t)P * 4);
   w.total = o;
   return w;
 }
@@ -495,7 +494,7 @@ int decode_impl(const a2ats_shape* shape, const a2ats_params* params, int32_t n_
     sa.pinfo = reinterpret_cast<uint32_t*>(base + Lw.pinfo);
     sa.tblg = reinterpret_cast<uint32_t*>(base + Lw.tblg);
     sa.desc = reinterpret_cast<unsigned long long*>(base + Lw.desc);
-    sa.done = reinterpret_cast<unsigned*>(base + Lw.done);
+    sa.desc_stride = shape->n_max / select_chunk_tokens() + 2;
     sa.nchunk = nchunk;
     sa.B = shape->B;
     sa.wlog = nullptr;

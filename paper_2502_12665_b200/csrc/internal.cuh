@@ -161,9 +161,8 @@ struct SelArgs {
   int32_t* nsel_out;            // [P] number of locally selected tokens
   // long contexts (launch_select_split): per-pair class table, chunk descriptors, completion
   uint32_t* tblg;               // [P, W] compact 2-bit classes
-  unsigned long long* desc;     // [P, nchunk] published (#above, #tied) per chunk, 0 = not yet
-  unsigned* done;               // [P]
-  int nchunk;
+  unsigned long long* desc;     // [P, desc_stride] published (#above, #tied) per chunk, 0 = not yet
+  int nchunk, desc_stride;
   // window logits computed by the threshold kernel before its dependency wait (long contexts;
   // otherwise the prep kernel's window role): wlog == nullptr disables
   float* wlog;                  // [P, 64, 8]

@@ -582,8 +582,8 @@ __device__ void window_logits(const SelArgs& a, int pair, uint8_t* scratch, floa
 //   kThresh (grid P): counts, v*, m -> pinfo; compact 2-bit class table -> tblg.
 //   kScanC (grid P x nchunk): one 32768-token chunk; classify, publish the chunk's
 //   (#above, #tied) with a release store, sum the pair's earlier chunks' counts (they have
-//   lower block indices, so they are resident or done: the wait terminates), emit; the
-//   pair's last chunk re-arms the descriptors.
+//   lower block indices, so they are resident or done: the wait terminates), emit.  The
+//   threshold kernel re-arms the descriptors of the next call.
 template <int MODE>
 __device__ __forceinline__ void split_body(const SelArgs& a, SelShared& S, int* cnt, uint32_t* key, uint32_t* tbl,
                                            uint32_t* skey, int* scnt, uint4* sC) {
@@ -619,6 +619,9 @@ __device__ __forceinline__ void split_body(const SelArgs& a, SelShared& S, int* 
       a.pinfo[pair * 4 + 1] = m;
       a.pinfo[pair * 4 + 2] = (uint32_t)a.keff;
     }
+    // re-arm the pair's chunk descriptors (the previous call's scan is complete: this runs
+    // after the dependency wait, and the scan kernel of this call waits for this one)
+    for (int c = tid; c < a.desc_stride; c += kNT) a.desc[(size_t)pair * a.desc_stride + c] = 0ull;
     append_hist(a, pair, cp_local);
     return;
   }
@@ -646,6 +649,7 @@ __device__ __forceinline__ void split_body(const SelArgs& a, SelShared& S, int* 
   }
   cp_async_wait<0>();
   __syncthreads();
+  A2ATS_TL(g_selc_tl, 2);
   const int t0 = cb + tid * kTPT;
   uint32_t p0 = 0u, p1 = 0u, p2 = 0u, p3 = 0u;
 #pragma unroll 1
@@ -679,6 +683,7 @@ __device__ __forceinline__ void split_body(const SelArgs& a, SelShared& S, int* 
   }
   if (lane == 31) S.wsum[warp] = incl;
   __syncthreads();
+  A2ATS_TL(g_selc_tl, 3);
   uint32_t pre = 0, tot = 0;
 #pragma unroll
   for (int w = 0; w < kNW; ++w) {
@@ -686,21 +691,27 @@ __device__ __forceinline__ void split_body(const SelArgs& a, SelShared& S, int* 
     pre += (w < warp) ? v : 0u;
     tot += v;
   }
-  unsigned long long* desc = a.desc + (size_t)pair * a.nchunk;
-  if (tid == 0) {  // publish this chunk's counts, then sum the earlier chunks'
-    st_release_u64(desc + ch, (1ull << 63) | ((unsigned long long)(tot >> 16) << 31) | (tot & 0xffffu));
+  unsigned long long* desc = a.desc + (size_t)pair * a.desc_stride;
+  if (warp == 0) {  // publish this chunk's counts, then sum the earlier chunks' (one lane each)
+    if (lane == 0)
+      st_release_u64(desc + ch, (1ull << 63) | ((unsigned long long)(tot >> 16) << 31) | (tot & 0xffffu));
     uint32_t gb = 0, eb = 0;
 #pragma unroll 1
-    for (int c = 0; c < ch; ++c) {
+    for (int c = lane; c < ch; c += 32) {
       unsigned long long v;
       while (!((v = ld_acquire_u64(desc + c)) >> 63)) __nanosleep(32);
       gb += (uint32_t)(v & 0x7fffffffull);
       eb += (uint32_t)((v >> 31) & 0x7fffffffull);
     }
-    S.s_before[0] = gb;
-    S.s_before[1] = eb;
+    gb = __reduce_add_sync(0xffffffffu, gb);
+    eb = __reduce_add_sync(0xffffffffu, eb);
+    if (lane == 0) {
+      S.s_before[0] = gb;
+      S.s_before[1] = eb;
+    }
   }
   __syncthreads();
+  A2ATS_TL(g_selc_tl, 4);
   const uint32_t ex = pre + incl - pk;
   uint32_t gb = S.s_before[0] + (ex & 0xffffu), eb = S.s_before[1] + (ex >> 16);
   int32_t* selp = a.sel + (size_t)pair * a.sel_stride;
@@ -724,10 +735,6 @@ __device__ __forceinline__ void split_body(const SelArgs& a, SelShared& S, int* 
         ++eb;
       }
     }
-  }
-  if (tid == 0 && atomicAdd(a.done + pair, 1u) == (unsigned)a.nchunk - 1) {  // every chunk has looked back
-    for (int c = 0; c < a.nchunk; ++c) desc[c] = 0ull;
-    a.done[pair] = 0u;
   }
 }
 

@@ -100,6 +100,13 @@ for it in range(args.iters):
             st, en = (pa[sel, 0] - t0) / 1e3, (pa[sel, 1] - t0) / 1e3
             print(f"  prep/{name:6s} ctas {len(sel):4d} start {st.min():7.2f}..{st.max():7.2f} end {en.min():7.2f}..{en.max():7.2f}"
                   f"  dur med {np.median(en - st):6.2f}")
+    if len(valid["selc"]):
+        m = tl["selc"][valid["selc"]]
+        m = m[(m[:, 4] > m[:, 0])]
+        if len(m):
+            d = lambda x, y: np.median((m[:, x] - m[:, y]) / 1e3)
+            print(f"  selc phases (median us): wait+table {d(2, 0):.2f}  classify {d(3, 2):.2f}  lookback {d(4, 3):.2f}"
+                  f"  emit+exit {d(1, 4):.2f}")
     a = tl["attn"]
     idx = valid["attn"]
     du = (a[idx, 1] - a[idx, 0]) / 1e3
