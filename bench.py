@@ -393,6 +393,78 @@ def run_reference(args):
     print(json.dumps(line))
 
 
+def run_sharded(args, rank: int, world: int):
+    """Sequence-sharded step: every rank holds a contiguous token range of every
+    (b, KV head) sequence; q and the codebook are replicated.  One step = the new token's
+    code on its owner rank + ShardStep (LUT + local candidate histogram, all-reduce, threshold,
+    all-gather of tie counts, local selection + attention, all-gather of partials, LSE
+    combine).  Total work is fixed as N grows: strong scaling."""
+    import torch
+
+    import paper_2502_12665_b200 as A
+    from paper_2502_12665_b200.sharded import GpuShardKernels, ShardStep, shard_ranges
+    from synth import CONFIGS, budget_k, make_inputs
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    cfg = CONFIGS[args.config]
+    if args.batch:
+        cfg = cfg.with_(B=args.batch)
+    steps_total = args.warmup + args.steps
+    N0 = cfg.N - steps_total                       # context before the first step; the last has N
+    lo, hi = shard_ranges(N0, world)[rank]
+    own_new = rank == world - 1                    # new tokens join the last rank's shard
+    cap = (hi - lo) + (steps_total + 8 if own_new else 0)
+    cap = (cap + 7) // 8 * 8
+    rep = make_inputs(cfg.with_(N=8), SEED, device=dev, with_h=True)          # replicated q, C, H
+    loc = make_inputs(cfg.with_(N=cap), SEED + 1 + rank, device=dev, with_h=False, n_max=cap)  # local K/V
+    params = A.Params(topk=budget_k(cfg.N))
+    kern = GpuShardKernels(cfg.B, cfg.Hq, cfg.Hkv, cfg.L, cap, rep["codebook"], params, device=dev)
+    dec = A.Decoder(cfg.B, cfg.Hq, cfg.Hkv, cfg.L, cap, rep["codebook"], rep["H"], params, device=dev)
+    kc, vc = loc["k_cache"], loc["v_cache"]
+    dec.encode(kc, 0, hi - lo)                     # local codes + local histogram (untimed)
+    step = ShardStep(kern, rank, world)
+    out = torch.empty((cfg.B, cfg.Hq, cfg.d), dtype=torch.float32, device=dev)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    torch.cuda.synchronize()
+
+    def one(s):
+        n = N0 + s + 1
+        sl = (hi - lo) + (s + 1 if own_new else 0)
+        if own_new:                                # a0 for the new token, on its owner
+            dec.encode(kc, sl - 1, sl)
+        params.topk = budget_k(n)
+        step(n, lo, sl, rep["q"], kc, vc, dec.codes, dec.hist, out)
+
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for s in range(args.warmup):
+        flush.fill_(1.0)
+        one(s)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    tokens = 0
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            s = args.warmup + k
+            flush.fill_(float(k))
+            evs[k][0].record()
+            one(s)
+            evs[k][1].record()
+            tokens += cfg.B * cfg.Hkv * (N0 + s + 1)   # whole-job tokens scored per step (all ranks)
+        torch.cuda.synchronize()
+    total_ms = sum(a.elapsed_time(b) for a, b in evs)
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+        torch.distributed.barrier()
+    return dict(value=tokens / (total_ms / 1e3), ms_per_step=total_ms / args.steps, clocks=clk.summary(), cfg=cfg,
+                lo=lo, hi=hi)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -405,7 +477,11 @@ def main():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=2.0)
+    ap.add_argument("--sharded", action="store_true",
+                    help="sequence-sharded step over the ranks (SURVEY 8e; default config C4, strong scaling)")
     args = ap.parse_args()
+    if args.sharded and args.config == "C2":
+        args.config = "C4"
     args.warmup = max(args.warmup, 3)
 
     rank = int(os.environ.get("RANK", "0"))
@@ -419,6 +495,20 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
         dist.init_process_group("nccl")
+    if args.sharded:
+        r = run_sharded(args, rank, world)
+        if rank == 0:
+            print(json.dumps({
+                "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+                "config": {"workload": r["cfg"].name + "-sharded", "B": r["cfg"].B, "Hq": r["cfg"].Hq,
+                           "Hkv": r["cfg"].Hkv, "N_final": r["cfg"].N, "L": r["cfg"].L,
+                           "parallelism": f"sequence-sharded x{world} (NCCL all-reduce of code histograms, "
+                                          f"all-gather of tie counts and partials)",
+                           "l2": "flushed between steps (256 MB write, outside the timed events)"},
+                "clocks": r["clocks"]}))
+        return
     r = run_ours(args, rank, world)
     if rank != 0:
         return
