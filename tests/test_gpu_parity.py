@@ -369,3 +369,35 @@ def test_decode_step_append_equals_two_calls(use_hist, K, big):
         for h in range(cfg.Hkv):
             ref = O.qavq_encode(f64(inp["k_cache"][b, h, cfg.N - 1:cfg.N]), C[h], f64(inp["H"][h]))
             assert codes_np(d2.codes)[b, h, cfg.N - 1] == ref[0]
+
+
+def test_wide_batch_append_sampled():
+    """512 (b, KV head) pairs (C4's B = 64) at a short context through a2ats_decode_step_append:
+    the prep kernel's balancing (two LUT vector tiles, grouped code tiles, several window pairs
+    per CTA) on sampled pairs vs the oracle, and the appended token's code."""
+    cfg = Config("wide", B=64, Hq=32, Hkv=8, d=128, N=3000, L=4096, K=180)
+    seed = 0xA2A75 + 9
+    inp = make_inputs(cfg, seed, device="cuda", with_h=True)
+    inp["codes"] = inp["z"].to(torch.uint16)
+    sample = [(0, 0), (17, 3), (31, 7), (40, 1), (63, 6), (63, 0)]
+    host = dict(q=inp["q"].cpu(), codebook=inp["codebook"].cpu(), codes=inp["codes"].cpu())
+    redraw_for_gap(host, cfg, cfg.N, seed, pairs=sample)
+    inp["q"] = host["q"].cuda()
+    dec = A.Decoder(cfg.B, cfg.Hq, cfg.Hkv, cfg.L, inp["n_max"], inp["codebook"], inp["H"])
+    dec.codes = inp["codes"].clone()
+    dec.hist = hist_of(inp["codes"], cfg.L, cfg.N - 1)
+    dec.set_topk(cfg.K)
+    sel = torch.empty((cfg.B, cfg.Hkv, cfg.K), dtype=torch.int32, device="cuda")
+    out = dec.step_append(inp["q"], inp["k_cache"], inp["v_cache"], cfg.N, sel_out=sel)
+    torch.cuda.synchronize()
+    got_codes = codes_np(dec.codes)
+    C = f64(host["codebook"])
+    H = f64(inp["H"].cpu())
+    for b, h in sample:
+        ref = O.qavq_encode(f64(inp["k_cache"][b, h, cfg.N - 1:cfg.N].cpu()), C[h], H[h])
+        assert got_codes[b, h, cfg.N - 1] == ref[0]
+    np.testing.assert_array_equal(dec.hist.cpu().numpy(), hist_of(dec.codes, cfg.L, cfg.N).cpu().numpy())
+    small = dict(q=host["q"], codebook=host["codebook"], codes=host["codes"],
+                 k_cache=_PairView(inp["k_cache"]), v_cache=_PairView(inp["v_cache"]))
+    gpu = dict(out=out.cpu().numpy(), sel=sel.cpu().numpy(), scores=None)
+    check_against_oracle(cfg, small, gpu, pairs=sample)
