@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define A2ATS_ABI_VERSION 3
+#define A2ATS_ABI_VERSION 4
 
 /* ---- status codes ---------------------------------------------------- */
 #define A2ATS_OK 0
@@ -177,6 +177,19 @@ int a2ats_decode_step(const a2ats_shape* shape, const a2ats_params* params, int3
                       const uint16_t* codes, const void* codebook, const int32_t* hist,
                       float* out, int32_t* sel_out, float* scores_out,
                       void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------
+ * a2ats_select_topk -- a1..a4 only: the score table LUT = q~ C^T and the
+ * top-K selection over the code stream, Sel written to sel_out; no K/V is
+ * read and no attention runs.  This is the part the paper runs on the GPU
+ * before handing Sel to its CPU attention.  Arguments as
+ * a2ats_decode_step (same workspace); sel_out is required.  Results are
+ * bitwise identical to the sel_out of a2ats_decode_step.
+ * ------------------------------------------------------------------- */
+int a2ats_select_topk(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx,
+                      const void* q, const uint16_t* codes, const void* codebook,
+                      const int32_t* hist, int32_t* sel_out, void* ws, size_t ws_bytes,
+                      void* stream);
 
 /* ---------------------------------------------------------------------
  * a2ats_decode_step_append -- a0 for the new token, then a1..a6 (one

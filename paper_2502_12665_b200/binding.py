@@ -65,12 +65,14 @@ _SIGS = {
     "a2ats_decode_step_append": (ctypes.c_int, [ctypes.POINTER(a2ats_shape), ctypes.POINTER(a2ats_params),
                                                 ctypes.c_int32, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
                                                 _VP, _VP, ctypes.c_size_t, _VP]),
+    "a2ats_select_topk": (ctypes.c_int, [ctypes.POINTER(a2ats_shape), ctypes.POINTER(a2ats_params), ctypes.c_int32,
+                                         _VP, _VP, _VP, _VP, _VP, _VP, ctypes.c_size_t, _VP]),
 }
 
 _lib = None
 
 
-ABI_VERSION = 3  # include/a2ats.h A2ATS_ABI_VERSION
+ABI_VERSION = 4  # include/a2ats.h A2ATS_ABI_VERSION
 
 
 def load(path: str = LIB_PATH, build_if_missing: bool = True) -> ctypes.CDLL:
@@ -209,6 +211,18 @@ def a2ats_decode_step_append(shape: a2ats_shape, params, n_ctx: int, q, k_cache,
         _ptr(sel_out, "sel_out", torch.int32, optional=True), _ptr(scores_out, "scores_out", torch.float32, optional=True),
         _ptr(ws, "ws"), ws.numel() * ws.element_size(), _stream(stream))
     _check("a2ats_decode_step_append", rc)
+
+
+def a2ats_select_topk(shape: a2ats_shape, params, n_ctx: int, q, codes, codebook, hist, sel_out, ws, stream=None):
+    """a1..a4 only (score table + top-K): Sel into sel_out [B, Hkv, K_eff] int32."""
+    import torch
+    p = params.c() if isinstance(params, Params) else params
+    rc = load().a2ats_select_topk(
+        ctypes.byref(shape), ctypes.byref(p), int(n_ctx), _ptr(q, "q", torch.bfloat16),
+        _ptr(codes, "codes", torch.uint16), _ptr(codebook, "codebook", torch.bfloat16),
+        _ptr(hist, "hist", torch.int32, optional=True), _ptr(sel_out, "sel_out", torch.int32),
+        _ptr(ws, "ws"), ws.numel() * ws.element_size(), _stream(stream))
+    _check("a2ats_select_topk", rc)
 
 
 def a2ats_set_stage_events(events):

@@ -411,15 +411,18 @@ namespace {
 int decode_impl(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx, const void* q,
                 const void* k_cache, const void* v_cache, uint16_t* codes, const void* codebook, int32_t* hist,
                 const void* chat, const float* nrm, float* out, int32_t* sel_out, float* scores_out, void* ws,
-                size_t ws_bytes, void* stream) {
+                size_t ws_bytes, void* stream, bool attend = true) {
   int rc = check_shape(shape);
   if (rc) return rc;
   rc = check_params(params);
   if (rc) return rc;
-  if (!q || !k_cache || !v_cache || !codes || !codebook || !out) return A2ATS_EINVAL;
-  if (!aligned16(q) || !aligned16(k_cache) || !aligned16(v_cache) || !aligned16(codes) || !aligned16(codebook) ||
-      !aligned16(out))
+  if (attend) {
+    if (!k_cache || !v_cache || !out || !aligned16(k_cache) || !aligned16(v_cache) || !aligned16(out))
+      return A2ATS_EINVAL;
+  } else if (!sel_out || chat) {
     return A2ATS_EINVAL;
+  }
+  if (!q || !codes || !codebook || !aligned16(q) || !aligned16(codes) || !aligned16(codebook)) return A2ATS_EINVAL;
   if (n_ctx <= 0 || n_ctx > shape->n_max) return A2ATS_EINVAL;
   const bool append = chat != nullptr;
   if (append && (!nrm || !aligned16(chat) || shape->B > encode_cw_max() ||
@@ -447,10 +450,13 @@ int decode_impl(const a2ats_shape* shape, const a2ats_params* params, int32_t n_
   // long contexts: the window logits are computed by the select threshold kernel, before its
   // dependency wait (it waits for this kernel anyway); otherwise by the prep kernel's window role
   const int nchunk = d.c1 > d.c0 ? (d.c1 - ((d.c0 >> 3) << 3) + select_chunk_tokens() - 1) / select_chunk_tokens() : 0;
-  const bool split_select = d.keff > 0 && nchunk >= 2;
+  const bool long_select = d.keff > 0 && nchunk >= 2;
+  // one streaming CTA per pair (hist given; its 32-B code loads need a 32-B aligned base)
+  const bool stream_select = long_select && hist != nullptr && (reinterpret_cast<uintptr_t>(codes) & 31u) == 0;
+  const bool split_select = long_select && !stream_select;    // threshold + chunked scan
   prep_set_window(p, shape, k_cache, wlog, n_ctx, d.w0, d.n_w, 0);
   const int n_wl = p.n_wl;
-  if (split_select) p.n_win = 0;
+  if (long_select || !attend) p.n_win = 0;  // long: the select kernel computes them before its wait
   CUtensorMap tmA, tmC;
   rc = cuda_status(make_tmap_sw128(&tmA, codebook, (uint64_t)shape->Hkv * shape->L, kD, 128));
   if (rc) return rc;
@@ -498,7 +504,7 @@ int decode_impl(const a2ats_shape* shape, const a2ats_params* params, int32_t n_
     sa.nchunk = nchunk;
     sa.B = shape->B;
     sa.wlog = nullptr;
-    if (split_select) {
+    if (long_select && attend) {
       sa.wlog = wlog;
       sa.q = static_cast<const uint16_t*>(q);
       sa.kc = static_cast<const uint16_t*>(k_cache);
@@ -522,11 +528,15 @@ int decode_impl(const a2ats_shape* shape, const a2ats_params* params, int32_t n_
     sa.shard_begin = 0;
     sa.shard_len = shape->n_max;
     sa.rank = 0;
-    // one CTA per pair while the candidates fit one code chunk; beyond, threshold + chunked scan
-    rc = cuda_status(split_select ? launch_select_split(sa, d.P, st) : launch_select(sa, d.P, st));
+    // one CTA per pair while the candidates fit one code chunk; beyond, one streaming CTA per
+    // pair (hist given) or threshold + chunked scan (counts need a pass over the codes)
+    rc = cuda_status(stream_select  ? launch_select_stream(sa, d.P, st)
+                     : split_select ? launch_select_split(sa, d.P, st)
+                                    : launch_select(sa, d.P, st));
     if (rc) return rc;
   }
   stage_mark(2, st);
+  if (!attend) return A2ATS_OK;
 
   // a5 + a6
   AttnArgs aa;
@@ -589,6 +599,14 @@ int a2ats_decode_step_append(const a2ats_shape* shape, const a2ats_params* param
   if (!chat) return A2ATS_EINVAL;
   return decode_impl(shape, params, n_ctx, q, k_cache, v_cache, codes, codebook, hist, chat, nrm, out, sel_out,
                      scores_out, ws, ws_bytes, stream);
+}
+
+int a2ats_select_topk(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx, const void* q,
+                      const uint16_t* codes, const void* codebook, const int32_t* hist, int32_t* sel_out, void* ws,
+                      size_t ws_bytes, void* stream) {
+  return decode_impl(shape, params, n_ctx, q, nullptr, nullptr, const_cast<uint16_t*>(codes), codebook,
+                     const_cast<int32_t*>(hist), nullptr, nullptr, nullptr, sel_out, nullptr, ws, ws_bytes, stream,
+                     false);
 }
 
 // ------------------------------------------------------------------ sequence-sharded step

@@ -43,6 +43,12 @@ constexpr int kTlMax = 8192;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                     \
     if (cta_ < kTlMax) arr[cta_][i] = t_;                                                      \
   }
+// slot 7: a value (e.g. the CTA's role) instead of a time
+#define A2ATS_TL_VAL(arr, v)                                                               \
+  if (threadIdx.x == 0) {                                                                  \
+    const unsigned cta_ = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x; \
+    if (cta_ < kTlMax) arr[cta_][7] = (unsigned long long)(v);                             \
+  }
 #define A2ATS_TL_EXPORT(fn, arr)                                                                        \
   extern "C" int fn(unsigned long long* out) {                                                          \
     return cudaMemcpyFromSymbol(out, arr, sizeof(unsigned long long) * 8 * a2ats::kTlMax) == cudaSuccess ? 0 : -4; \
@@ -53,6 +59,7 @@ constexpr int kTlMax = 8192;
 #define A2ATS_PHASE_EXPORT(fn, arr)
 #define A2ATS_TL_DECL(name)
 #define A2ATS_TL(arr, i)
+#define A2ATS_TL_VAL(arr, v)
 #define A2ATS_TL_EXPORT(fn, arr)
 #endif
 
@@ -239,6 +246,8 @@ cudaError_t launch_shard_hist(const SelArgs& a, int P, cudaStream_t st);
 cudaError_t launch_shard_thresh(const SelArgs& a, int P, cudaStream_t st);
 cudaError_t launch_shard_scan(const SelArgs& a, int P, cudaStream_t st);
 cudaError_t launch_select_split(const SelArgs& a, int P, cudaStream_t st);
+// long contexts with a caller-maintained hist: one streaming CTA per pair (no look-back)
+cudaError_t launch_select_stream(const SelArgs& a, int P, cudaStream_t st);
 int select_chunk_tokens();
 cudaError_t launch_attention(const AttnArgs& a, int P, int GT, cudaStream_t st);
 cudaError_t launch_combine(const float* parts, int R, int rows, float* out, cudaStream_t st);

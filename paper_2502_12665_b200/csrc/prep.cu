@@ -218,6 +218,7 @@ __device__ __forceinline__ void window_tile(const PrepArgs& p, int pair0, int np
       }
     }
   }
+  A2ATS_TL(g_prep_tl, 2);
   const int row = tid & 63, hsel = tid >> 6;  // heads hsel, hsel + 2, ...
 #pragma unroll 1
   for (int pair = pair0; pair < pair0 + np; ++pair) {
@@ -239,6 +240,7 @@ __device__ __forceinline__ void window_tile(const PrepArgs& p, int pair0, int np
       kS[r * 16 + (c ^ (r & 7))] = ld_nc_u4(kbase + (size_t)(p.win_lo + r - p.shard_begin) * 256 + c * 16);
     }
     __syncthreads();
+    if (pair == pair0) A2ATS_TL(g_prep_tl, 3);
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
     if (row < nw) {
 #pragma unroll 1
@@ -267,8 +269,10 @@ __device__ __forceinline__ void window_tile(const PrepArgs& p, int pair0, int np
       }
     }
     if (pair == pair0) {
+      A2ATS_TL(g_prep_tl, 4);
       pdl_wait();  // the previous step's attention reads wlog
       pdl_trigger();
+      A2ATS_TL(g_prep_tl, 5);
     }
     if (row < nw) {
 #pragma unroll
@@ -291,13 +295,16 @@ __global__ __launch_bounds__(128, 1) void prep_kernel(const __grid_constant__ CU
   A2ATS_TL(g_prep_tl, 0);
   int i = blockIdx.x;
   if (i < p.n_lut) {
+    A2ATS_TL_VAL(g_prep_tl, 1);
     lut_tile<G>(tmA, p, i, smem);
   } else if ((i -= p.n_lut) < p.n_enc) {
+    A2ATS_TL_VAL(g_prep_tl, 2);
     const int cx_n = (p.enc_tx + p.enc_tpc - 1) / p.enc_tpc, cx = i % cx_n;
     encode_tiles(tmC, p.enc, cx * p.enc_tpc, min(p.enc_tx, (cx + 1) * p.enc_tpc), i / cx_n, cx_n, p.enc_nv,
                  p.enc_cols, smem);
   } else {
     i -= p.n_enc;
+    A2ATS_TL_VAL(g_prep_tl, 3);
     const int npairs = p.lut.B * p.lut.Hkv;
     const int pair0 = i * p.win_ppc;
     window_tile(p, pair0, max(0, min(p.win_ppc, npairs - pair0)), smem);

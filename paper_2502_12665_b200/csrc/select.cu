@@ -68,21 +68,22 @@ struct SelShared {
 // cnt[l] = hist[l] - #(local sink/window tokens with code l)   (hist given)
 //        = #(local candidate tokens with code l)                (otherwise)
 // Step inputs only (hist, codes).
+template <int NT = kNT>
 __device__ void load_cnt(const SelArgs& a, int pair, int* cnt, const uint16_t* cp_local) {
   const int tid = threadIdx.x;
   const int32_t* histp = a.hist ? a.hist + (size_t)pair * a.L : nullptr;
   const int lo = a.shard_begin, hi = a.shard_begin + a.shard_len;  // local global-index range
   if (histp) {
-    for (int base = 0; base < a.L; base += 8 * kNT) {  // all loads of a batch in flight before use
+    for (int base = 0; base < a.L; base += 8 * NT) {  // all loads of a batch in flight before use
       int hv[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const int l = base + i * kNT + tid;
+        const int l = base + i * NT + tid;
         hv[i] = l < a.L ? __ldg(histp + l) : 0;
       }
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const int l = base + i * kNT + tid;
+        const int l = base + i * NT + tid;
         if (l < a.L) cnt[l] = hv[i];
       }
     }
@@ -90,17 +91,17 @@ __device__ void load_cnt(const SelArgs& a, int pair, int* cnt, const uint16_t* c
     // remove the local sinks [0, n_s) and window [w0, n_ctx): they are not candidates
     // (append: hist does not hold token n_ctx - 1 yet, whose code the prep kernel computes)
     const int nrem = a.n_s + (a.n_ctx - a.append - a.w0);
-    for (int i = tid; i < nrem; i += kNT) {
+    for (int i = tid; i < nrem; i += NT) {
       const int t = i < a.n_s ? i : a.w0 + (i - a.n_s);
       if (t >= lo && t < hi) atomicSub(&cnt[cp_local[t - lo]], 1);
     }
   } else {
-    for (int l = tid; l < a.L; l += kNT) cnt[l] = 0;
+    for (int l = tid; l < a.L; l += NT) cnt[l] = 0;
     __syncthreads();
     const int c0 = max(a.c0, lo), c1 = min(a.c1, hi);
     if (c0 < c1) {
       const int v0 = (c0 - lo) >> 3, v1 = (c1 - lo + 7) >> 3;
-      for (int vi = v0 + tid; vi < v1; vi += kNT) {
+      for (int vi = v0 + tid; vi < v1; vi += NT) {
         const uint4 x = ld_nc_u4(cp_local + (size_t)vi * 8);
         const uint32_t w[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
@@ -116,6 +117,7 @@ __device__ void load_cnt(const SelArgs& a, int pair, int* cnt, const uint16_t* c
 
 // key[l] = ~ordered(agg[l]) (ascending key = descending agg) and the key range of the
 // codewords with cnt > 0 -> S.s_kmin / S.s_kmax.  Needs cnt (synced); ends synced.
+template <int NT = kNT>
 __device__ void load_keys(const SelArgs& a, SelShared& S, int pair, const int* cnt, uint32_t* key) {
   const int tid = threadIdx.x, lane = tid & 31;
   const float* aggp = a.agg + (size_t)pair * a.L;
@@ -124,16 +126,16 @@ __device__ void load_keys(const SelArgs& a, SelShared& S, int pair, const int* c
     S.s_kmax = 0u;
   }
   uint32_t kmn = 0xffffffffu, kmx = 0u;
-  for (int base = 0; base < a.L; base += 8 * kNT) {
+  for (int base = 0; base < a.L; base += 8 * NT) {
     float av[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const int l = base + i * kNT + tid;
+      const int l = base + i * NT + tid;
       av[i] = l < a.L ? __ldcg(aggp + l) : 0.f;
     }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const int l = base + i * kNT + tid;
+      const int l = base + i * NT + tid;
       if (l < a.L) {
         const uint32_t k = ~ordered_key(av[i]);
         key[l] = k;
@@ -189,6 +191,7 @@ __device__ __forceinline__ void pick_digit(SelShared& S, int kk) {
 // Count-weighted selection of the keff-th smallest key over cnt / key (all threads),
 // given the key range S.s_kmin..S.s_kmax.  Result in S.s_kstar (key of v*) and
 // S.s_m (tie quota, >= 1).
+template <int NT = kNT, int SC = kSurvCap>
 __device__ void find_level(const SelArgs& a, SelShared& S, const int* cnt, const uint32_t* key, int keff,
                            uint32_t* skey, int* scnt) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -201,7 +204,7 @@ __device__ void find_level(const SelArgs& a, SelShared& S, const int* cnt, const
     __syncthreads();
     return;
   }
-  for (int i = tid; i < 256; i += kNT) S.bins[i] = 0;
+  for (int i = tid; i < 256; i += NT) S.bins[i] = 0;
   if (tid == 0) S.s_nsurv = 0;
   __syncthreads();
   // 256 bins of equal width in agg VALUE over [amin, amax], ascending bin = descending
@@ -216,7 +219,7 @@ __device__ void find_level(const SelArgs& a, SelShared& S, const int* cnt, const
     const float d = amax - key_val(k);
     return d > 0.f ? min(255, (int)(d * scale)) : 0;
   };
-  for (int l = tid; l < a.L; l += kNT) {
+  for (int l = tid; l < a.L; l += NT) {
     const int c = cnt[l];
     if (c > 0) atomicAdd(&S.bins[bin_of(key[l])], c);
   }
@@ -227,7 +230,7 @@ __device__ void find_level(const SelArgs& a, SelShared& S, const int* cnt, const
   const int bstar = S.s_digit;
   int kk = S.s_kk;
   // survivors = candidate codewords of bin b*, one pass (order is irrelevant below)
-  for (int l0 = 0; l0 < a.L; l0 += kNT) {
+  for (int l0 = 0; l0 < a.L; l0 += NT) {
     const int l = l0 + tid;
     const bool keep = l < a.L && cnt[l] > 0 && bin_of(key[l]) == bstar;
     const unsigned bal = __ballot_sync(0xffffffffu, keep);
@@ -236,7 +239,7 @@ __device__ void find_level(const SelArgs& a, SelShared& S, const int* cnt, const
       if (lane == 0) base = atomicAdd(&S.s_nsurv, __popc(bal));
       base = __shfl_sync(0xffffffffu, base, 0);
       const int slot = base + __popc(bal & ((1u << lane) - 1u));
-      if (keep && slot < kSurvCap) {
+      if (keep && slot < SC) {
         skey[slot] = key[l];
         scnt[slot] = cnt[l];
       }
@@ -245,7 +248,7 @@ __device__ void find_level(const SelArgs& a, SelShared& S, const int* cnt, const
   __syncthreads();
   A2ATS_PHASE(g_sel_phase, 4);
   const int nsurv = S.s_nsurv;
-  if (nsurv <= kRankMax) {
+  if (nsurv <= NT) {
     // rank each survivor directly: v* is the key with #(< v*) < kk <= #(<= v*);
     // equal keys write equal values
     if (tid < nsurv) {
@@ -266,7 +269,7 @@ __device__ void find_level(const SelArgs& a, SelShared& S, const int* cnt, const
     __syncthreads();
     return;
   }
-  if (nsurv <= kSurvCap) {
+  if (nsurv <= SC) {
     if (warp == 0) {
       // exact K-th key among the survivors: radix passes from their first differing bit
       uint32_t sa = 0xffffffffu, so = 0u;
@@ -310,9 +313,9 @@ __device__ void find_level(const SelArgs& a, SelShared& S, const int* cnt, const
   uint32_t prefix = 0, mask = 0;
   for (int pass = 3; pass >= 0; --pass) {
     const int shift = 8 * pass;
-    for (int i = tid; i < 256; i += kNT) S.bins[i] = 0;
+    for (int i = tid; i < 256; i += NT) S.bins[i] = 0;
     __syncthreads();
-    for (int l = tid; l < a.L; l += kNT) {
+    for (int l = tid; l < a.L; l += NT) {
       const int c = cnt[l];
       const uint32_t k = key[l];
       if (c > 0 && bin_of(k) == bstar && (k & mask) == prefix) atomicAdd(&S.bins[(k >> shift) & 255u], c);
@@ -335,13 +338,14 @@ __device__ void find_level(const SelArgs& a, SelShared& S, const int* cnt, const
 // key / cnt: every word is computed into registers before the first write).  One
 // thread per word (W <= 1024); the 16-B chunks are visited in a per-thread rotated
 // order so a quarter-warp touches distinct banks.
+template <int NT = kNT>
 __device__ void build_table(const SelArgs& a, const uint32_t* key, uint32_t kstar, uint32_t* tbl) {
   const int tid = threadIdx.x;
-  constexpr int kMaxItems = 2;  // words tid and tid + 512
+  constexpr int kMaxItems = 1024 / NT;  // words tid, tid + NT, ... (W <= 1024)
   uint32_t word[kMaxItems];
 #pragma unroll
   for (int j = 0; j < kMaxItems; ++j) {
-    const int w = j * kNT + tid;
+    const int w = j * NT + tid;
     uint32_t x = 0;
     if (w < a.W) {
       if (w * 16 + 16 <= a.L) {
@@ -369,7 +373,7 @@ __device__ void build_table(const SelArgs& a, const uint32_t* key, uint32_t ksta
   __syncthreads();
 #pragma unroll
   for (int j = 0; j < kMaxItems; ++j) {
-    const int w = j * kNT + tid;
+    const int w = j * NT + tid;
     if (w < a.W) {
       uint4* dst = reinterpret_cast<uint4*>(tbl + w * 32);
       const uint4 v = make_uint4(word[j], word[j], word[j], word[j]);
@@ -509,12 +513,15 @@ __device__ __forceinline__ void append_hist(const SelArgs& a, int pair, const ui
 
 // Window logits of the pair (Eq. 11 local rows: u_j = (q R_{i-j}) . k_j, exact per-row
 // rotation on FP32 cores, base-2 scaled) for its first n_wl window tokens, from step inputs
-// only; written to wlog for the attention.  512 threads; scratch: cs [64][64] float2 (fp64
-// angle per 8 rows, then fp64 rotations by -f_m), K rows [64][16 chunks] and q [8][128]
-// fp32, 16-B chunks XOR-swizzled by row.  Same arithmetic as the prep kernel's window role.
-__device__ void window_logits(const SelArgs& a, int pair, uint8_t* scratch, float* out_acc) {
+// only; the caller writes them to wlog for the attention.  NT threads (512 or 256): thread
+// <-> (row, heads g0, g0 + NT/64, ...); scratch: cs [64][64] float2 (fp64 angle per row
+// group, then fp64 rotations by -f_m), K rows [64][16 chunks] and q [8][128] fp32, 16-B
+// chunks XOR-swizzled by row.  Same arithmetic as the prep kernel's window role.
+template <int NT>
+__device__ void window_logits(const SelArgs& a, int pair, uint8_t* scratch, float (&out_acc)[512 / NT]) {
+  constexpr int kHS = 512 / NT;  // head slots per thread
   const int tid = threadIdx.x, nw = a.n_wl, G = a.G;
-  const int Hkv = gridDim.x / a.B;  // (threshold kernel: one CTA per pair)
+  const int Hkv = gridDim.x / a.B;  // (one CTA per pair)
   const int b = pair / Hkv, h = pair - b * Hkv;
   float4* csS = reinterpret_cast<float4*>(scratch);
   uint4* kS = reinterpret_cast<uint4*>(scratch + 32768);
@@ -531,12 +538,13 @@ __device__ void window_logits(const SelArgs& a, int pair, uint8_t* scratch, floa
     d[1] = make_float4(bf_lo(w[2]) * a.scale_log2, bf_hi(w[2]) * a.scale_log2, bf_lo(w[3]) * a.scale_log2,
                        bf_hi(w[3]) * a.scale_log2);
   }
-  for (int k = tid; k < nw * 16; k += kNT) {
+  for (int k = tid; k < nw * 16; k += NT) {
     const int r = k >> 4, c = k & 15;
     kS[r * 16 + (c ^ (r & 7))] = ld_nc_u4(kbase + (size_t)(a.win_lo + r - a.shard_begin) * 256 + c * 16);
   }
   {
-    const int m = tid & 63, j0 = (tid >> 6) * 8;  // rows [j0, j0 + 8) of pair m
+    constexpr int kRows = 64 * 64 / NT;          // rows per thread of the cs table
+    const int m = tid & 63, j0 = (tid >> 6) * kRows;  // rows [j0, j0 + kRows) of pair m
     if (j0 < nw) {
       const double f = a.rt.inv_freq[m];
       double sn, cn, sf, cf;
@@ -544,7 +552,7 @@ __device__ void window_logits(const SelArgs& a, int pair, uint8_t* scratch, floa
       sincos(f, &sf, &cf);
       float2* cs2 = reinterpret_cast<float2*>(csS);
 #pragma unroll 1
-      for (int row = j0; row < min(j0 + 8, nw); ++row) {
+      for (int row = j0; row < min(j0 + kRows, nw); ++row) {
         cs2[row * 64 + (((m >> 1) ^ (row & 7)) << 1) + (m & 1)] = make_float2((float)cn, (float)sn);
         const double c2 = cn * cf + sn * sf, s2 = sn * cf - cn * sf;  // r -> r - 1
         cn = c2;
@@ -553,9 +561,11 @@ __device__ void window_logits(const SelArgs& a, int pair, uint8_t* scratch, floa
     }
   }
   __syncthreads();
-  const int row = tid & 63, g = tid >> 6;  // one (row, head) per thread
-  float acc = 0.f;
-  if (row < nw && g < G) {
+  const int row = tid & 63, g0 = tid >> 6;  // heads g0 + s * (NT / 64)
+  float acc[kHS];
+#pragma unroll
+  for (int s2 = 0; s2 < kHS; ++s2) acc[s2] = 0.f;
+  if (row < nw && g0 < G) {
 #pragma unroll 1
     for (int mb = 0; mb < 8; ++mb) {  // m = 8 mb + i; pairs (m, m + 64)
       const uint4 k1 = kS[row * 16 + (mb ^ (row & 7))];
@@ -564,18 +574,36 @@ __device__ void window_logits(const SelArgs& a, int pair, uint8_t* scratch, floa
       float4 t[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) t[j] = csS[row * 32 + ((mb * 4 + j) ^ (row & 7))];
-      const float* qa = sQ + g * kD + mb * 8;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const float ka = (e & 1) ? bf_hi(w1[e >> 1]) : bf_lo(w1[e >> 1]);
-        const float kb = (e & 1) ? bf_hi(w2[e >> 1]) : bf_lo(w2[e >> 1]);
-        const float cv = (e & 1) ? t[e >> 1].z : t[e >> 1].x, sv = (e & 1) ? t[e >> 1].w : t[e >> 1].y;
-        const float q1 = qa[e], q2 = qa[e + kHalf];
-        acc = fmaf(cv, fmaf(q1, ka, q2 * kb), fmaf(sv, fmaf(q1, kb, -q2 * ka), acc));
+      for (int s2 = 0; s2 < kHS; ++s2) {
+        const int g = g0 + s2 * (NT / 64);
+        if (g < G) {
+          const float* qa = sQ + g * kD + mb * 8;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float ka = (e & 1) ? bf_hi(w1[e >> 1]) : bf_lo(w1[e >> 1]);
+            const float kb = (e & 1) ? bf_hi(w2[e >> 1]) : bf_lo(w2[e >> 1]);
+            const float cv = (e & 1) ? t[e >> 1].z : t[e >> 1].x, sv = (e & 1) ? t[e >> 1].w : t[e >> 1].y;
+            const float q1 = qa[e], q2 = qa[e + kHalf];
+            acc[s2] = fmaf(cv, fmaf(q1, ka, q2 * kb), fmaf(sv, fmaf(q1, kb, -q2 * ka), acc[s2]));
+          }
+        }
       }
     }
   }
-  *out_acc = acc;
+#pragma unroll
+  for (int s2 = 0; s2 < kHS; ++s2) out_acc[s2] = acc[s2];
+}
+
+// wlog rows of the pair (after the dependency wait: the previous step's attention reads them)
+template <int NT>
+__device__ __forceinline__ void store_window_logits(const SelArgs& a, int pair, const float (&acc)[512 / NT]) {
+  const int tid = threadIdx.x, row = tid & 63;
+  if (row < a.n_wl) {
+#pragma unroll
+    for (int s2 = 0; s2 < 512 / NT; ++s2)
+      a.wlog[((size_t)pair * 64 + row) * 8 + (tid >> 6) + s2 * (NT / 64)] = acc[s2];  // heads >= G: 0
+  }
 }
 
 // Long contexts (several code chunks per pair), single GPU.
@@ -591,13 +619,12 @@ __device__ __forceinline__ void split_body(const SelArgs& a, SelShared& S, int* 
   if (MODE == kThresh) {
     const int pair = blockIdx.x;
     const uint16_t* cp_local = a.codes + (size_t)pair * a.n_max;
-    float wacc = 0.f;
-    if (a.wlog) window_logits(a, pair, reinterpret_cast<uint8_t*>(scnt + kSurvCap), &wacc);
+    float wacc[1] = {0.f};
+    if (a.wlog) window_logits<kNT>(a, pair, reinterpret_cast<uint8_t*>(scnt + kSurvCap), wacc);
     load_cnt(a, pair, cnt, cp_local);
     pdl_wait();  // agg comes from the LUT kernel
     pdl_trigger();
-    if (a.wlog && (tid & 63) < a.n_wl)
-      a.wlog[((size_t)pair * 64 + (tid & 63)) * 8 + (tid >> 6)] = wacc;  // heads >= G: 0
+    if (a.wlog) store_window_logits<kNT>(a, pair, wacc);
     uint32_t kstar = 0, m = 0;
     if (a.keff > 0) {
       load_keys(a, S, pair, cnt, key);
@@ -736,6 +763,179 @@ __device__ __forceinline__ void split_body(const SelArgs& a, SelShared& S, int* 
       }
     }
   }
+}
+
+// ---------------------------------------------------------------- long contexts with hist
+// select_stream_kernel: one 256-thread CTA per pair, four resident per SM, streaming the
+// pair's whole candidate range (no cross-CTA look-back).  Before the dependency wait:
+// counts from hist, the first round of codes into registers; after: v*, m, the 2-bit class
+// table (replicated 32x), then rounds of 8192 tokens, each thread 32 consecutive tokens
+// (two 32-B loads; the next round's are issued before the current one is classified).
+// Output offsets: one warp scan, the warp totals through shared memory (one barrier per
+// round), a running count per CTA.  The codes base must be 32-B aligned.
+constexpr int kST = 256;             // threads per CTA (stream kernel)
+constexpr int kSSurv = 1024;         // survivor list capacity (stream kernel)
+constexpr int kRound = kST * 32;     // tokens per round
+
+__device__ __forceinline__ void ld_nc_v8(const uint16_t* p, uint32_t* r) {
+  asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "l"(p));
+}
+
+// tokens [t, t + 32) of the row (32-B aligned address): codes at or past c1 read as 0 (masked)
+__device__ __forceinline__ void stream_load(const uint16_t* cp, int t, int c1, uint32_t (&v)[16]) {
+  if (t < c1) {
+    ld_nc_v8(cp + t, v);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = 0u;
+  }
+  if (t + 16 < c1) {
+    ld_nc_v8(cp + t + 16, v + 8);
+  } else {
+#pragma unroll
+    for (int i = 8; i < 16; ++i) v[i] = 0u;
+  }
+}
+
+// 2-bit classes of 16 tokens (token e at bits 2e, 2e + 1): word (code >> 4) of the table,
+// replica lane, rotated right by 2 (code & 15); its low field shifted in from the top.
+__device__ __forceinline__ uint32_t classify16(const uint8_t* tb, uint32_t lane4, const uint32_t* w) {
+  uint32_t cls = 0u;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t x = w[j];
+    const uint32_t wl = *reinterpret_cast<const uint32_t*>(tb + (((x << 3) & 0x7ff80u) | lane4));
+    cls = __funnelshift_r(cls, __funnelshift_r(wl, wl, x << 1), 2);
+    const uint32_t wh = *reinterpret_cast<const uint32_t*>(tb + (((x >> 13) & 0x7ff80u) | lane4));
+    cls = __funnelshift_r(cls, __funnelshift_r(wh, wh, x >> 15), 2);  // bit 15 of x is 0 (L <= 16384)
+  }
+  return cls;
+}
+
+// emit the tokens of a 16-token class word: above-v* fields at base++, tied fields (rare)
+// through the quota; returns nothing, advances gb / eb
+__device__ __forceinline__ void emit16(uint32_t q, int t0, uint32_t& gb, uint32_t& eb, uint32_t m, uint32_t cap,
+                                       int32_t* selp) {
+  if ((q & 0xaaaaaaaau) == 0u) {  // no tied token: positions gb + min(eb, m) .. + n - 1
+    const uint32_t n = __popc(q), pos = gb + min(eb, m);
+    gb += n;
+    if (pos + n <= cap) {  // (always, unless hist is inconsistent with the codes)
+      int32_t* dst = selp + pos + n;
+      do {  // highest token first
+        const int bit = 31 - __clz(q);
+        q ^= 1u << bit;
+        *--dst = t0 + (bit >> 1);
+      } while (q);
+    }
+    return;
+  }
+  while (q) {  // in increasing token order
+    const int bit = __ffs(q) - 1;
+    q &= q - 1u;
+    const int t = t0 + (bit >> 1);
+    if ((bit & 1) == 0) {  // above v*
+      const uint32_t pos = gb + min(eb, m);
+      if (pos < cap) selp[pos] = t;
+      ++gb;
+    } else {  // tied at v*: the first m in token order
+      if (eb < m && gb + eb < cap) selp[gb + eb] = t;
+      ++eb;
+    }
+  }
+}
+
+__global__ __launch_bounds__(kST, 4) void select_stream_kernel(SelArgs a) {
+  A2ATS_TL(g_sel_tl, 0);
+  extern __shared__ __align__(16) uint32_t sm[];
+  __shared__ SelShared S;
+  __shared__ __align__(16) uint32_t sTot[2][8];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int pair = blockIdx.x;
+  int* cnt = reinterpret_cast<int*>(sm);
+  uint32_t* key = sm + ((a.L + 3) & ~3);
+  uint32_t* tbl = sm;
+  const int tbl_words = (max(((a.L + 3) & ~3) + a.L, a.W * 32) + 3) / 4 * 4;
+  uint32_t* skey = sm + tbl_words;
+  int* scnt = reinterpret_cast<int*>(skey + kSSurv);
+  const uint16_t* cp = a.codes + (size_t)pair * a.n_max;
+  const int c0 = a.c0, c1 = a.c1;
+  // rounds start 32-B aligned in memory: rows are 16-B aligned, so a row may start 8 tokens
+  // past a 32-B boundary (then first may be -8: the previous row's last codes, masked; pair 0
+  // starts at the 32-B aligned base)
+  const int mis = (int)((reinterpret_cast<uintptr_t>(cp) >> 1) & 15u);
+  const int first = ((c0 + mis) & ~15) - mis;
+  const int nround = c1 > c0 ? (c1 - first + kRound - 1) / kRound : 0;
+  float wacc[512 / kST];
+  if (a.wlog) {  // the window rows' logits (scratch aliases cnt / key, dead until load_cnt)
+    window_logits<kST>(a, pair, reinterpret_cast<uint8_t*>(sm), wacc);
+    __syncthreads();
+  }
+  uint32_t cur[16];
+  stream_load(cp, first + tid * 32, c1, cur);
+  load_cnt<kST>(a, pair, cnt, cp);
+  pdl_wait();  // agg comes from the prep kernel
+  pdl_trigger();
+  A2ATS_TL(g_sel_tl, 3);
+  if (a.wlog) store_window_logits<kST>(a, pair, wacc);
+  load_keys<kST>(a, S, pair, cnt, key);
+  A2ATS_TL(g_sel_tl, 4);
+  find_level<kST, kSSurv>(a, S, cnt, key, a.keff, skey, scnt);
+  A2ATS_TL(g_sel_tl, 5);
+  const uint32_t kstar = S.s_kstar, m = S.s_m, cap = (uint32_t)a.keff;
+  build_table<kST>(a, key, kstar, tbl);
+  A2ATS_TL(g_sel_tl, 2);
+  int32_t* selp = a.sel + (size_t)pair * a.sel_stride;
+  const uint8_t* tb = reinterpret_cast<const uint8_t*>(tbl);
+  const uint32_t lane4 = (uint32_t)lane * 4u;
+  uint32_t run_gt = 0, run_eq = 0;
+#pragma unroll 1
+  for (int r = 0; r < nround; ++r) {
+    const int t0 = first + r * kRound + tid * 32;
+    uint32_t nxt[16];
+    stream_load(cp, t0 + kRound, r + 1 < nround ? c1 : 0, nxt);
+    uint32_t ca = classify16(tb, lane4, cur), cb = classify16(tb, lane4, cur + 8);
+    if (r == 0 || r + 1 == nround) {  // tokens outside [c0, c1)
+      ca &= span_mask(c0 - t0, c1 - t0);
+      cb &= span_mask(c0 - t0 - 16, c1 - t0 - 16);
+    }
+    const uint32_t pk = (uint32_t)(__popc(ca & 0x55555555u) + __popc(cb & 0x55555555u)) |
+                        ((uint32_t)(__popc(ca & 0xaaaaaaaau) + __popc(cb & 0xaaaaaaaau)) << 16);
+    uint32_t incl = pk;  // 16-bit fields: a warp holds 1024 tokens per round
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += y;
+    }
+    const int par = r & 1;
+    if (lane == 31) sTot[par][warp] = incl;
+    __syncthreads();
+    const uint4 s0 = *reinterpret_cast<const uint4*>(&sTot[par][0]);
+    const uint4 s1 = *reinterpret_cast<const uint4*>(&sTot[par][4]);
+    const uint32_t sv[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+    uint32_t pre = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      pre += (w < warp) ? sv[w] : 0u;
+      tot += sv[w];
+    }
+    const uint32_t ex = pre + incl - pk;
+    uint32_t gb = run_gt + (ex & 0xffffu), eb = run_eq + (ex >> 16);
+    if (ca) emit16(ca, t0, gb, eb, m, cap, selp);
+    if (cb) emit16(cb, t0 + 16, gb, eb, m, cap, selp);
+    run_gt += tot & 0xffffu;
+    run_eq += tot >> 16;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) cur[i] = nxt[i];
+  }
+  append_hist(a, pair, cp);
+  A2ATS_TL(g_sel_tl, 1);
+}
+
+size_t stream_smem_bytes(int L, int W) {
+  const int tbl_words = (std::max(((L + 3) & ~3) + L, W * 32) + 3) / 4 * 4;
+  return std::max((size_t)tbl_words * 4 + 2 * kSSurv * 4, (size_t)kWinScratch);
 }
 
 template <int MODE>
@@ -913,6 +1113,17 @@ cudaError_t launch_select_split(const SelArgs& a, int P, cudaStream_t st) {
   return launch_mode<kScanC>(a, P * a.nchunk, st);
 }
 int select_chunk_tokens() { return kCH; }
+
+cudaError_t launch_select_stream(const SelArgs& a, int P, cudaStream_t st) {
+  const int smem = (int)stream_smem_bytes(a.L, a.W);
+  static int smem_set = -1;
+  if (smem_set < smem) {
+    cudaError_t e = cudaFuncSetAttribute(select_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    smem_set = smem;
+  }
+  return launch_pdl(select_stream_kernel, dim3(P), dim3(kST), smem, st, a);
+}
 
 }  // namespace a2ats
 

@@ -49,6 +49,12 @@ class Decoder:
                              kv_host=kv_host)
         return out
 
+    def select(self, q, n_ctx: int, sel_out, use_hist=True):
+        """a1..a4 only: the top-K token indices (no K/V read, no attention)."""
+        _b.a2ats_select_topk(self.shape, self.params, n_ctx, q, self.codes, self.codebook,
+                             self.hist if use_hist else None, sel_out, self.ws_dec, self.stream)
+        return sel_out
+
     def step_append(self, q, k_cache, v_cache, n_ctx: int, out=None, sel_out=None, scores_out=None,
                     use_hist=True):
         """a0 for token n_ctx - 1 (its key already in k_cache) fused with the step."""

@@ -24,10 +24,10 @@ def hist_of(codes: torch.Tensor, L: int, n_ctx: int) -> torch.Tensor:
 
 
 def run_case(cfg: Config, seed: int, family="g2", code_dist="uniform", bridge=None, n_ctx=None, use_hist=True,
-             scores=True, gap_redraw=True, group_reduce=O.GROUP_MAX, pairs=None, device="cuda"):
+             scores=True, gap_redraw=True, group_reduce=O.GROUP_MAX, pairs=None, device="cuda", n_max=None):
     n_ctx = cfg.N if n_ctx is None else n_ctx
     bridge = cfg.bridge if bridge is None else bridge
-    inp = make_inputs(cfg, seed, device="cpu", family=family, code_dist=code_dist, with_h=False)
+    inp = make_inputs(cfg, seed, device="cpu", family=family, code_dist=code_dist, with_h=False, n_max=n_max)
     inp["codes"] = inp["z"].to(torch.uint16)
     if gap_redraw and family != "g1":
         redraw_for_gap(inp, cfg.with_(bridge=bridge), n_ctx, seed, pairs=pairs)
@@ -108,14 +108,32 @@ LONG = Config("long", B=2, Hq=8, Hkv=2, d=128, N=70001, L=1000, K=4200)
 
 @pytest.mark.parametrize("use_hist", [True, False])
 def test_long_context_chunked_select(use_hist):
-    # 3 code chunks per pair: threshold kernel + chunked scan with the cross-chunk look-back
+    # 3 code chunks per pair (n_max % 16 == 8: odd rows start 16 B past a 32-B boundary):
+    # streaming select with hist, threshold kernel + chunked scan with the cross-chunk
+    # look-back without
     inp, gpu, _ = run_case(LONG, seed=23, use_hist=use_hist, scores=False)
     check_against_oracle(LONG, inp, gpu)
 
 
-def test_long_context_integer_ties_across_chunks():
+@pytest.mark.parametrize("use_hist", [True, False])
+def test_long_context_integer_ties_across_chunks(use_hist):
     cfg = LONG.with_(L=300, K=9000)
-    inp, gpu, _ = run_case(cfg, seed=24, family="g1", bridge=0, code_dist="zipf", scores=False)
+    inp, gpu, _ = run_case(cfg, seed=24, family="g1", bridge=0, code_dist="zipf", scores=False, use_hist=use_hist)
+    check_against_oracle(cfg, inp, gpu, bridge=0)
+
+
+@pytest.mark.parametrize("n_ctx", [70001, 65541, 33000])
+def test_long_context_stream_select(n_ctx):
+    # hist given and n_max % 16 == 0: one streaming CTA per pair (8192-token rounds, ragged
+    # first / last round, window end inside a round)
+    inp, gpu, _ = run_case(LONG, seed=25 + n_ctx % 7, scores=False, n_max=70016, n_ctx=n_ctx)
+    check_against_oracle(LONG, inp, gpu, n_ctx=n_ctx)
+
+
+def test_long_context_stream_integer_ties():
+    # ties spread over many rounds: the quota m is carried across rounds in token order
+    cfg = LONG.with_(L=300, K=9000)
+    inp, gpu, _ = run_case(cfg, seed=26, family="g1", bridge=0, code_dist="zipf", scores=False, n_max=70016)
     check_against_oracle(cfg, inp, gpu, bridge=0)
 
 
@@ -401,3 +419,26 @@ def test_wide_batch_append_sampled():
                  k_cache=_PairView(inp["k_cache"]), v_cache=_PairView(inp["v_cache"]))
     gpu = dict(out=out.cpu().numpy(), sel=sel.cpu().numpy(), scores=None)
     check_against_oracle(cfg, small, gpu, pairs=sample)
+
+
+@pytest.mark.parametrize("N,n_max,use_hist", [(3000, 3008, True), (3000, 3008, False), (70001, 70016, True),
+                                             (70001, 70008, True)])
+def test_select_topk_equals_decode_step(N, n_max, use_hist):
+    """a2ats_select_topk (a1..a4 only) == the sel_out of a2ats_decode_step, bit for bit, on the
+    fused, streaming and threshold + chunked-scan selection paths."""
+    cfg = Config("seltk", B=2, Hq=8, Hkv=2, d=128, N=N, L=512, K=max(60, N // 16))
+    inp = make_inputs(cfg, 161, device="cuda", with_h=False, n_max=n_max)
+    codes = inp["z"].to(torch.uint16)
+    params = A.Params(topk=cfg.K)
+    dec = A.Decoder(cfg.B, cfg.Hq, cfg.Hkv, cfg.L, inp["n_max"], inp["codebook"], None, params)
+    dec.codes = codes
+    dec.hist = hist_of(codes, cfg.L, N)
+    S, cand, W = O.token_sets(N, cfg.window, cfg.n_sink)
+    keff = min(cfg.K, cand.size)
+    s1 = torch.full((cfg.B, cfg.Hkv, keff), -1, dtype=torch.int32, device="cuda")
+    s2 = s1.clone()
+    dec.step(inp["q"], inp["k_cache"], inp["v_cache"], N, sel_out=s1, use_hist=use_hist)
+    dec.select(inp["q"], N, s2, use_hist=use_hist)
+    torch.cuda.synchronize()
+    assert torch.equal(s1, s2)
+    assert int(s2.min()) >= 0

@@ -21,6 +21,7 @@ rows = list(csv.reader(io.StringIO(out)))
 hi = [i for i, r in enumerate(rows) if "Address" in r][0]
 h = rows[hi]
 ai, si, ns = h.index("Address"), h.index("Source"), h.index("Warp Stall Sampling (All Samples)")
+ie = h.index("Instructions Executed") if "Instructions Executed" in h else None
 stall_cols = [(i, c) for i, c in enumerate(h) if c.startswith("stall_") and "Not Issued" not in c]
 wf_i = h.index("L1 Wavefronts Shared") if "L1 Wavefronts Shared" in h else None
 wfi_i = h.index("L1 Wavefronts Shared Ideal") if "L1 Wavefronts Shared Ideal" in h else None
@@ -33,6 +34,7 @@ for r in rows[hi + 1:]:
         continue
     st = {c: int(float(r[i] or 0)) for i, c in stall_cols}
     wf = (float(r[wf_i] or 0), float(r[wfi_i] or 0)) if wf_i is not None else (0.0, 0.0)
+    st["_inst"] = int(float(r[ie] or 0)) if ie is not None else 0
     samples.append((int(r[ai], 16), r[si], int(float(r[ns] or 0)), st, wf))
 base = samples[0][0]
 # offset -> line from nvdisasm of the matching function
@@ -42,6 +44,7 @@ cub = glob.glob(os.path.join(tmp, "*.cubin"))[0]
 dis = subprocess.run(["nvdisasm", "-g", "-c", cub], capture_output=True, text=True).stdout
 fn_pat = re.compile(r"\.text\.(\S+):")
 cur, line, lmap = None, None, {}
+fname = None
 want = None
 for l in dis.splitlines():
     m = fn_pat.search(l)
@@ -50,7 +53,8 @@ for l in dis.splitlines():
         continue
     m = re.search(r"line (\d+)", l)
     if "//##" in l and m:
-        line = int(m.group(1))
+        fm = re.search(r'File "([^"]+)"', l)
+        line = (os.path.basename(fm.group(1)) if fm else "?", int(m.group(1)))
         continue
     m = re.match(r"\s+/\*([0-9a-f]{4,})\*/", l)
     if m and cur and re.search(mre, cur):
@@ -69,7 +73,8 @@ for addr, src, n, st, wf in samples:
     e[3][0] += wf[0]
     e[3][1] += wf[1]
     tot += n
-print(f"kernel {kname}  function {want}  total samples {tot}")
+tot_inst = sum(st["_inst"] for _, _, _, st, _ in samples)
+print(f"kernel {kname}  function {want}  total samples {tot}  warp instructions {tot_inst}")
 src_lines = None
 srcfile = None
 srcpath = None
@@ -80,8 +85,10 @@ for l in dis.splitlines():
         break
 lines = open(srcpath).read().splitlines() if srcpath else []
 for ln, (n, s, st, wf) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
-    txt = lines[ln - 1].strip()[:80] if ln and ln <= len(lines) else s[:60]
+    f, n_ = ln if ln else ("?", 0)
+    txt = lines[n_ - 1].strip()[:80] if srcpath and f == os.path.basename(srcpath) and 0 < n_ <= len(lines) else f
+    inst = st.pop("_inst", 0)
     top2 = sorted(st.items(), key=lambda kv: -kv[1])[:2]
     why = " ".join(f"{c[6:]}:{v}" for c, v in top2 if v)
     smem = f" smem-wf {wf[0]:.0f}/{wf[1]:.0f}" if wf[0] else ""
-    print(f"{n:6d} {100.0 * n / max(tot, 1):5.1f}%  {ln}: {txt}  [{why}]{smem}")
+    print(f"{n:6d} {100.0 * n / max(tot, 1):5.1f}% inst {100.0 * inst / max(tot_inst, 1):5.1f}%  {n_}: {txt}  [{why}]{smem}")

@@ -78,28 +78,27 @@ for it in range(args.iters):
         q = np.percentile(du, [0, 50, 90, 100])
         print(f"{k:7s} ctas {len(a):5d} start {st.min():7.2f}..{st.max():7.2f} end {en.min():7.2f}..{en.max():7.2f}"
               f"  dur min/med/p90/max {q[0]:6.2f} {q[1]:6.2f} {q[2]:6.2f} {q[3]:6.2f}")
-    # prep roles along blockIdx.x: LUT tiles, encode tiles, window pairs
-    G = cfg.Hq // cfg.Hkv
-    nv = 256 if cfg.B * G >= 256 else (cfg.B * G + 15) // 16 * 16
-    # mirror of api.cu prep_balance (one wave at 3 CTAs / SM): encode first, then LUT
-    tx, nvt, n_win = (cfg.L + 127) // 128, (cfg.B * G + nv - 1) // nv, cfg.B * cfg.Hkv
-    lt, et = 1, 1
-    while (-(-tx // lt)) * nvt * cfg.Hkv + (-(-tx // et)) * cfg.Hkv + n_win > 3 * 148:
-        if et <= lt and et < tx:
-            et *= 2
-        elif lt < tx:
-            lt *= 2
-        else:
-            break
-    n_lut = (-(-tx // lt)) * nvt * cfg.Hkv
-    n_enc = (-(-tx // et)) * cfg.Hkv
+    # prep roles (slot 7: 1 LUT, 2 encode, 3 window)
     pa, pidx = tl["prep"], valid["prep"]
-    for name, lo, hi in (("lut", 0, n_lut), ("encode", n_lut, n_lut + n_enc), ("window", n_lut + n_enc, 1 << 30)):
-        sel = pidx[(pidx >= lo) & (pidx < hi)]
+    for name, role in (("lut", 1), ("encode", 2), ("window", 3)):
+        sel = pidx[pa[pidx, 7] == role]
         if len(sel):
             st, en = (pa[sel, 0] - t0) / 1e3, (pa[sel, 1] - t0) / 1e3
+            extra = ""
+            if role == 3:
+                r = pa[sel]
+                d = lambda x, y: np.median((r[:, x] - r[:, y]) / 1e3)
+                extra = (f"  [cs {d(2, 0):.2f}  1st pair loads {d(3, 2):.2f}  compute {d(4, 3):.2f}"
+                         f"  wait {d(5, 4):.2f}  rest {d(1, 5):.2f}]")
             print(f"  prep/{name:6s} ctas {len(sel):4d} start {st.min():7.2f}..{st.max():7.2f} end {en.min():7.2f}..{en.max():7.2f}"
-                  f"  dur med {np.median(en - st):6.2f}")
+                  f"  dur med {np.median(en - st):6.2f}{extra}")
+    m = tl["select"][valid["select"]]
+    m = m[(m[:, 3] > m[:, 0]) & (m[:, 2] > m[:, 3])]
+    if len(m):  # stream kernel marks: 3 = dependency wait returned, 2 = class table built
+        d = lambda x, y: np.median((m[:, x] - m[:, y]) / 1e3)
+        print(f"  select phases (median us): start->wait {d(3, 0):.2f}  threshold+table {d(2, 3):.2f}"
+              f" [keys {d(4, 3):.2f} level {d(5, 4):.2f} table {d(2, 5):.2f}]"
+              f"  stream {d(1, 2):.2f}  (wait returns {(m[:, 3].min() - t0) / 1e3:.2f}..{(m[:, 3].max() - t0) / 1e3:.2f})")
     if len(valid["selc"]):
         m = tl["selc"][valid["selc"]]
         m = m[(m[:, 4] > m[:, 0])]
