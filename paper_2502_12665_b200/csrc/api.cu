@@ -91,7 +91,7 @@ void derive(const a2ats_shape* s, const a2ats_params* p, int n_ctx, Derived* d) 
 }
 
 struct DecodeWs {
-  size_t cs, agg, lut, sel, part, actr, cand_keep, pinfo, nsel, wlog, eslot, ectr, tblg, desc, total;
+  size_t cs, agg, lut, sel, part, actr, cand_keep, pinfo, nsel, wlog, eslot, ectr, tblg, desc, flag, total;
 };
 
 DecodeWs decode_layout(const a2ats_shape* s, const a2ats_params* p) {
@@ -117,6 +117,7 @@ DecodeWs decode_layout(const a2ats_shape* s, const a2ats_params* p) {
   w.ectr = o; o = align_up(o + (size_t)s->Hkv * 2 * 4);
   w.tblg = o; o = align_up(o + (size_t)P * ((s->L + 15) / 16) * 4);                       // long-context select
   w.desc = o; o = align_up(o + (size_t)P * (s->n_max / select_chunk_tokens() + 2) * 8);
+  w.flag = o; o = align_up(o + (size_t)P * 4);                                              // pipe select
   w.total = o;
   return w;
 }
@@ -170,6 +171,28 @@ cudaError_t make_tmap_sw128(CUtensorMap* map, const void* base, uint64_t rows, u
   const cuuint32_t es[2] = {1, 1};
   const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+// codes [P, n_max] u16 viewed as [P][n_max / 64][64] (128-B rows), box = 256 rows of one pair,
+// SWIZZLE_128B (n_max % 64 == 0): the long-context select's stage loads
+cudaError_t make_tmap_codes(CUtensorMap* map, const void* codes, uint64_t P, uint64_t n_max) {
+  static EncodeTiledFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<EncodeTiledFn>(nullptr);
+    return reinterpret_cast<EncodeTiledFn>(f);
+  }();
+  if (!fn) return cudaErrorNotSupported;
+  const cuuint64_t dims[3] = {64, n_max / 64, P};
+  const cuuint64_t strides[2] = {128, n_max * 2};
+  const cuuint32_t box[3] = {64, 256, 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, const_cast<void*>(codes), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
@@ -451,12 +474,15 @@ int decode_impl(const a2ats_shape* shape, const a2ats_params* params, int32_t n_
   // dependency wait (it waits for this kernel anyway); otherwise by the prep kernel's window role
   const int nchunk = d.c1 > d.c0 ? (d.c1 - ((d.c0 >> 3) << 3) + select_chunk_tokens() - 1) / select_chunk_tokens() : 0;
   const bool long_select = d.keff > 0 && nchunk >= 2;
-  // one streaming CTA per pair (hist given; its 32-B code loads need a 32-B aligned base)
-  const bool stream_select = long_select && hist != nullptr && (reinterpret_cast<uintptr_t>(codes) & 31u) == 0;
-  const bool split_select = long_select && !stream_select;    // threshold + chunked scan
+  // hist given: the warp-specialized persistent select (forward / backward half per pair);
+  // otherwise threshold + chunked scan (the counts need a pass over the codes)
+  const bool pipe_select = long_select && hist != nullptr && select_pipe_ok(shape->L) && shape->n_max % 64 == 0;
+  const bool stream_select = false;
+  const bool split_select = long_select && !pipe_select;
   prep_set_window(p, shape, k_cache, wlog, n_ctx, d.w0, d.n_w, 0);
   const int n_wl = p.n_wl;
-  if (long_select || !attend) p.n_win = 0;  // long: the select kernel computes them before its wait
+  // split select: its threshold kernel computes the window logits before its wait
+  if (split_select || !attend) p.n_win = 0;
   CUtensorMap tmA, tmC;
   rc = cuda_status(make_tmap_sw128(&tmA, codebook, (uint64_t)shape->Hkv * shape->L, kD, 128));
   if (rc) return rc;
@@ -504,7 +530,9 @@ int decode_impl(const a2ats_shape* shape, const a2ats_params* params, int32_t n_
     sa.nchunk = nchunk;
     sa.B = shape->B;
     sa.wlog = nullptr;
-    if (long_select && attend) {
+    sa.P = d.P;
+    sa.flag = reinterpret_cast<unsigned int*>(base + Lw.flag);
+    if (split_select && attend) {
       sa.wlog = wlog;
       sa.q = static_cast<const uint16_t*>(q);
       sa.kc = static_cast<const uint16_t*>(k_cache);
@@ -530,7 +558,13 @@ int decode_impl(const a2ats_shape* shape, const a2ats_params* params, int32_t n_
     sa.rank = 0;
     // one CTA per pair while the candidates fit one code chunk; beyond, one streaming CTA per
     // pair (hist given) or threshold + chunked scan (counts need a pass over the codes)
-    rc = cuda_status(stream_select  ? launch_select_stream(sa, d.P, st)
+    CUtensorMap tmK;
+    if (pipe_select) {
+      rc = cuda_status(make_tmap_codes(&tmK, codes, (uint64_t)d.P, (uint64_t)shape->n_max));
+      if (rc) return rc;
+    }
+    rc = cuda_status(pipe_select    ? launch_select_pipe(sa, tmK, std::min(sm_count(), 2 * d.P), st)
+                     : stream_select  ? launch_select_stream(sa, d.P, st)
                      : split_select ? launch_select_split(sa, d.P, st)
                                     : launch_select(sa, d.P, st));
     if (rc) return rc;

@@ -43,6 +43,14 @@ constexpr int kTlMax = 8192;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                     \
     if (cta_ < kTlMax) arr[cta_][i] = t_;                                                      \
   }
+// the calling thread records (the caller picks one thread)
+#define A2ATS_TLX(arr, i)                                                                      \
+  {                                                                                            \
+    const unsigned cta_ = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;     \
+    unsigned long long t_;                                                                     \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                     \
+    if (cta_ < kTlMax) arr[cta_][i] = t_;                                                      \
+  }
 // slot 7: a value (e.g. the CTA's role) instead of a time
 #define A2ATS_TL_VAL(arr, v)                                                               \
   if (threadIdx.x == 0) {                                                                  \
@@ -60,6 +68,7 @@ constexpr int kTlMax = 8192;
 #define A2ATS_TL_DECL(name)
 #define A2ATS_TL(arr, i)
 #define A2ATS_TL_VAL(arr, v)
+#define A2ATS_TLX(arr, i)
 #define A2ATS_TL_EXPORT(fn, arr)
 #endif
 
@@ -170,6 +179,10 @@ struct SelArgs {
   uint32_t* tblg;               // [P, W] compact 2-bit classes
   unsigned long long* desc;     // [P, desc_stride] published (#above, #tied) per chunk, 0 = not yet
   int nchunk, desc_stride;
+  // warp-specialized long-context select (launch_select_pipe): P pairs over a persistent grid,
+  // flag[pair] = 1 once the pair's class table is in tblg (reset to 0 by its reader)
+  int P;
+  unsigned int* flag;           // [P]
   // window logits computed by the threshold kernel before its dependency wait (long contexts;
   // otherwise the prep kernel's window role): wlog == nullptr disables
   float* wlog;                  // [P, 64, 8]
@@ -249,6 +262,9 @@ cudaError_t launch_select_split(const SelArgs& a, int P, cudaStream_t st);
 // long contexts with a caller-maintained hist: one streaming CTA per pair (no look-back)
 cudaError_t launch_select_stream(const SelArgs& a, int P, cudaStream_t st);
 int select_chunk_tokens();
+// long-context select with hist (L <= 4096): threshold kernel (grid P) + persistent scan (nblk CTAs)
+cudaError_t launch_select_pipe(const SelArgs& a, const CUtensorMap& tmK, int nblk, cudaStream_t st);
+bool select_pipe_ok(int L);
 cudaError_t launch_attention(const AttnArgs& a, int P, int GT, cudaStream_t st);
 cudaError_t launch_combine(const float* parts, int R, int rows, float* out, cudaStream_t st);
 cudaError_t launch_prepare(const uint16_t* codebook, const float* H, float* nrm, uint16_t* chat, int Hkv, int L,

@@ -25,6 +25,7 @@
 // histogram + this rank's above/at counts) and shard_scan (local emission with
 // the rank's tie quota, from the all-gathered counts).
 #include "internal.cuh"
+#include "umma.cuh"
 
 namespace a2ats {
 
@@ -56,6 +57,18 @@ struct ModeTraits {
   static constexpr int min_blocks = (MODE == kThresh || MODE == kScanC) ? 2 : 1;
 };
 
+// Thread groups: the whole CTA, or a named-barrier group of N threads starting at thread
+// BASE (warp-specialized kernels; BASE is a multiple of 32)
+struct CtaGrp {
+  static __device__ __forceinline__ int tid() { return threadIdx.x; }
+  static __device__ __forceinline__ void sync() { __syncthreads(); }
+};
+template <int BASE, int ID, int N>
+struct NamedGrp {
+  static __device__ __forceinline__ int tid() { return (int)threadIdx.x - BASE; }
+  static __device__ __forceinline__ void sync() { asm volatile("bar.sync %0, %1;" ::"n"(ID), "n"(N) : "memory"); }
+};
+
 struct SelShared {
   int bins[256];
   uint32_t wsum[kNW];
@@ -68,9 +81,9 @@ struct SelShared {
 // cnt[l] = hist[l] - #(local sink/window tokens with code l)   (hist given)
 //        = #(local candidate tokens with code l)                (otherwise)
 // Step inputs only (hist, codes).
-template <int NT = kNT>
+template <int NT = kNT, class Grp = CtaGrp>
 __device__ void load_cnt(const SelArgs& a, int pair, int* cnt, const uint16_t* cp_local) {
-  const int tid = threadIdx.x;
+  const int tid = Grp::tid();
   const int32_t* histp = a.hist ? a.hist + (size_t)pair * a.L : nullptr;
   const int lo = a.shard_begin, hi = a.shard_begin + a.shard_len;  // local global-index range
   if (histp) {
@@ -87,7 +100,7 @@ __device__ void load_cnt(const SelArgs& a, int pair, int* cnt, const uint16_t* c
         if (l < a.L) cnt[l] = hv[i];
       }
     }
-    __syncthreads();
+    Grp::sync();
     // remove the local sinks [0, n_s) and window [w0, n_ctx): they are not candidates
     // (append: hist does not hold token n_ctx - 1 yet, whose code the prep kernel computes)
     const int nrem = a.n_s + (a.n_ctx - a.append - a.w0);
@@ -97,7 +110,7 @@ __device__ void load_cnt(const SelArgs& a, int pair, int* cnt, const uint16_t* c
     }
   } else {
     for (int l = tid; l < a.L; l += NT) cnt[l] = 0;
-    __syncthreads();
+    Grp::sync();
     const int c0 = max(a.c0, lo), c1 = min(a.c1, hi);
     if (c0 < c1) {
       const int v0 = (c0 - lo) >> 3, v1 = (c1 - lo + 7) >> 3;
@@ -112,14 +125,14 @@ __device__ void load_cnt(const SelArgs& a, int pair, int* cnt, const uint16_t* c
       }
     }
   }
-  __syncthreads();
+  Grp::sync();
 }
 
 // key[l] = ~ordered(agg[l]) (ascending key = descending agg) and the key range of the
 // codewords with cnt > 0 -> S.s_kmin / S.s_kmax.  Needs cnt (synced); ends synced.
-template <int NT = kNT>
+template <int NT = kNT, class Grp = CtaGrp>
 __device__ void load_keys(const SelArgs& a, SelShared& S, int pair, const int* cnt, uint32_t* key) {
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int tid = Grp::tid(), lane = tid & 31;
   const float* aggp = a.agg + (size_t)pair * a.L;
   if (tid == 0) {
     S.s_kmin = 0xffffffffu;
@@ -148,12 +161,12 @@ __device__ void load_keys(const SelArgs& a, SelShared& S, int pair, const int* c
   }
   kmn = __reduce_min_sync(0xffffffffu, kmn);
   kmx = __reduce_max_sync(0xffffffffu, kmx);
-  __syncthreads();  // s_kmin / s_kmax initialised
+  Grp::sync();  // s_kmin / s_kmax initialised
   if (lane == 0) {
     atomicMin(&S.s_kmin, kmn);
     atomicMax(&S.s_kmax, kmx);
   }
-  __syncthreads();
+  Grp::sync();
 }
 
 // Warp 0: find the digit of bins[] that holds rank kk (1-based); writes s_digit, s_kk.
@@ -191,22 +204,22 @@ __device__ __forceinline__ void pick_digit(SelShared& S, int kk) {
 // Count-weighted selection of the keff-th smallest key over cnt / key (all threads),
 // given the key range S.s_kmin..S.s_kmax.  Result in S.s_kstar (key of v*) and
 // S.s_m (tie quota, >= 1).
-template <int NT = kNT, int SC = kSurvCap>
+template <int NT = kNT, int SC = kSurvCap, class Grp = CtaGrp>
 __device__ void find_level(const SelArgs& a, SelShared& S, const int* cnt, const uint32_t* key, int keff,
                            uint32_t* skey, int* scnt) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = Grp::tid(), lane = tid & 31, warp = tid >> 5;
   const uint32_t kmn = S.s_kmin, kmx = S.s_kmax;
   if (kmn == kmx) {  // a single level holds every candidate
     if (tid == 0) {
       S.s_kstar = kmn;
       S.s_m = (uint32_t)keff;
     }
-    __syncthreads();
+    Grp::sync();
     return;
   }
   for (int i = tid; i < 256; i += NT) S.bins[i] = 0;
   if (tid == 0) S.s_nsurv = 0;
-  __syncthreads();
+  Grp::sync();
   // 256 bins of equal width in agg VALUE over [amin, amax], ascending bin = descending
   // agg (monotone and deterministic: one subtract, one multiply, one truncation).
   auto key_val = [](uint32_t k) {
@@ -223,9 +236,9 @@ __device__ void find_level(const SelArgs& a, SelShared& S, const int* cnt, const
     const int c = cnt[l];
     if (c > 0) atomicAdd(&S.bins[bin_of(key[l])], c);
   }
-  __syncthreads();
+  Grp::sync();
   if (warp == 0) pick_digit(S, keff);
-  __syncthreads();
+  Grp::sync();
   A2ATS_PHASE(g_sel_phase, 3);
   const int bstar = S.s_digit;
   int kk = S.s_kk;
@@ -245,7 +258,7 @@ __device__ void find_level(const SelArgs& a, SelShared& S, const int* cnt, const
       }
     }
   }
-  __syncthreads();
+  Grp::sync();
   A2ATS_PHASE(g_sel_phase, 4);
   const int nsurv = S.s_nsurv;
   if (nsurv <= NT) {
@@ -266,7 +279,7 @@ __device__ void find_level(const SelArgs& a, SelShared& S, const int* cnt, const
         S.s_m = (uint32_t)(kk - less);
       }
     }
-    __syncthreads();
+    Grp::sync();
     return;
   }
   if (nsurv <= SC) {
@@ -305,7 +318,7 @@ __device__ void find_level(const SelArgs& a, SelShared& S, const int* cnt, const
         S.s_m = (uint32_t)kk;
       }
     }
-    __syncthreads();
+    Grp::sync();
     return;
   }
   // degenerate value distributions (more survivors than the list holds): block-wide
@@ -314,15 +327,15 @@ __device__ void find_level(const SelArgs& a, SelShared& S, const int* cnt, const
   for (int pass = 3; pass >= 0; --pass) {
     const int shift = 8 * pass;
     for (int i = tid; i < 256; i += NT) S.bins[i] = 0;
-    __syncthreads();
+    Grp::sync();
     for (int l = tid; l < a.L; l += NT) {
       const int c = cnt[l];
       const uint32_t k = key[l];
       if (c > 0 && bin_of(k) == bstar && (k & mask) == prefix) atomicAdd(&S.bins[(k >> shift) & 255u], c);
     }
-    __syncthreads();
+    Grp::sync();
     if (warp == 0) pick_digit(S, kk);
-    __syncthreads();
+    Grp::sync();
     prefix |= (uint32_t)S.s_digit << shift;
     mask |= 0xffu << shift;
     kk = S.s_kk;
@@ -331,7 +344,7 @@ __device__ void find_level(const SelArgs& a, SelShared& S, const int* cnt, const
     S.s_kstar = prefix;
     S.s_m = (uint32_t)kk;
   }
-  __syncthreads();
+  Grp::sync();
 }
 
 // 2-bit classes vs kstar, replicated 32x into tbl[word * 32 + replica] (tbl may alias
@@ -933,6 +946,397 @@ __global__ __launch_bounds__(kST, 4) void select_stream_kernel(SelArgs a) {
   A2ATS_TL(g_sel_tl, 1);
 }
 
+// ---------------------------------------------------------------- long contexts with hist
+// Two kernels after the LUT (prep) kernel:
+//  select_thresh_kernel (grid P, 256 threads, four resident per SM: one wave at C4): per
+//    pair, counts (hist - sink/window codes) before the dependency wait, then keys, v*, m,
+//    E = #{candidates at level v*}, and the compact 2-bit class table -> tblg, (v*, m, K_eff,
+//    E) -> pinfo; appends the step's new token to hist.
+//  select_scan_kernel: a persistent grid (one 1024-thread CTA per SM) over 2P work units:
+//    unit u < P streams the first half of pair u's candidate stages FORWARD, unit u >= P the
+//    second half of pair u - P BACKWARD.  The halves exchange nothing: with D = E - m, the
+//    forward half keeps its first m tied tokens and writes ascending from position 0; the
+//    backward half drops the last D tied tokens it meets and writes descending from
+//    position K_eff - 1 (together: exactly the first m ties in token order, the lowest-index
+//    tie-break of reading Q12).  2P units over the SMs balance to within one half-pair.
+//    Codes arrive through a ring of 32-KB stages (one TMA box of 256 128-B rows each,
+//    SWIZZLE_128B, mbarrier completion) that runs ahead across unit boundaries and is
+//    issued before the dependency wait (codes are step inputs).  Each pair's class table
+//    is replicated 32x in shared memory (lane l reads replica l: conflict-free gather by
+//    code), double-buffered: the next unit's table is written during the current one.
+constexpr int kPAll = 1024;          // scan kernel threads
+constexpr int kPRound = 256 * 64;    // tokens per stage: one TMA box of 256 128-B rows (32 KB)
+constexpr int kPStage = 4;
+constexpr int kTT = 256;             // threshold kernel threads
+constexpr int kTSurv = 1024;         // its survivor list capacity
+
+struct PipeUnit {
+  uint32_t m, D, cap, pad;
+};
+
+__device__ __forceinline__ void bar_sync_n(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void bar_arrive_n(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* mbar) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  const uint32_t m = static_cast<uint32_t>(__cvta_generic_to_shared(mbar));
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(d), "l"(src), "r"(bytes), "r"(m)
+               : "memory");
+}
+__device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned int* p, unsigned int v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint4 lds_v4(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+// classify8 with the lane's table replica at shared address tl (= table + 4 * lane)
+__device__ __forceinline__ uint32_t classify8s(uint32_t tl, uint4 v) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  uint32_t cls = 0u;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t x = w[j];
+    const uint32_t wl = lds_u32(tl + ((x << 3) & 0x7ff80u));
+    cls = __funnelshift_r(cls, __funnelshift_r(wl, wl, x << 1), 2);
+    const uint32_t wh = lds_u32(tl + ((x >> 13) & 0x7ff80u));
+    cls = __funnelshift_r(cls, __funnelshift_r(wh, wh, x >> 15), 2);
+  }
+  return cls >> 16;
+}
+
+// 2-bit classes of the 8 tokens of one 16-B piece (token e at bits 2e), from the table
+// replica of this lane
+__device__ __forceinline__ uint32_t classify8(const uint8_t* tb, uint32_t lane4, uint4 v) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  uint32_t cls = 0u;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t x = w[j];
+    const uint32_t wl = *reinterpret_cast<const uint32_t*>(tb + (((x << 3) & 0x7ff80u) | lane4));
+    cls = __funnelshift_r(cls, __funnelshift_r(wl, wl, x << 1), 2);
+    const uint32_t wh = *reinterpret_cast<const uint32_t*>(tb + (((x >> 13) & 0x7ff80u) | lane4));
+    cls = __funnelshift_r(cls, __funnelshift_r(wh, wh, x >> 15), 2);
+  }
+  return cls >> 16;
+}
+
+// backward emission of a 16-token class word: tokens in decreasing order; a token with
+// ga above-v* and ea tied tokens after it (in this unit) goes to top - 1 - (ga + max(ea - D, 0));
+// a tied token is kept iff ea >= D
+__device__ __forceinline__ void emit16_rev(uint32_t q, int t0, uint32_t& ga, uint32_t& ea, uint32_t D, uint32_t top,
+                                           int32_t* selp) {
+  if ((q & 0xaaaaaaaau) == 0u) {
+    const uint32_t n = __popc(q), used = ga + (ea > D ? ea - D : 0u);
+    ga += n;
+    if (used + n <= top) {
+      int32_t* dst = selp + (top - used - n);
+      do {  // lowest token first, ascending positions
+        const int bit = __ffs(q) - 1;
+        q &= q - 1u;
+        *dst++ = t0 + (bit >> 1);
+      } while (q);
+    }
+    return;
+  }
+  while (q) {
+    const int bit = 31 - __clz(q);
+    q ^= 1u << bit;
+    const int t = t0 + (bit >> 1);
+    if ((bit & 1) == 0) {
+      const uint32_t used = ga + (ea > D ? ea - D : 0u);
+      if (used < top) selp[top - 1 - used] = t;
+      ++ga;
+    } else {
+      if (ea >= D) {
+        const uint32_t used = ga + ea - D;
+        if (used < top) selp[top - 1 - used] = t;
+      }
+      ++ea;
+    }
+  }
+}
+
+struct PipeGeom {
+  int first, R, R0, c1al;
+};
+__device__ __forceinline__ PipeGeom pipe_geom(const SelArgs& a) {
+  PipeGeom g;
+  g.first = (a.c0 >> 6) << 6;
+  g.c1al = (a.c1 + 7) & ~7;
+  g.R = (a.c1 - g.first + kPRound - 1) / kPRound;
+  g.R0 = (g.R + 1) >> 1;
+  return g;
+}
+
+__global__ __launch_bounds__(kTT, 4) void select_thresh_kernel(SelArgs a) {
+  A2ATS_TL(g_sel_tl, 0);
+  extern __shared__ __align__(16) uint32_t sm[];
+  __shared__ SelShared S;
+  const int tid = threadIdx.x, lane = tid & 31, pair = blockIdx.x;
+  const int W = a.W, L4 = (a.L + 3) & ~3;
+  int* cnt = reinterpret_cast<int*>(sm);
+  uint32_t* key = sm + L4;
+  uint32_t* skey = key + L4;
+  int* scnt = reinterpret_cast<int*>(skey + kTSurv);
+  const uint16_t* cp = a.codes + (size_t)pair * a.n_max;
+  load_cnt<kTT>(a, pair, cnt, cp);  // step inputs
+  pdl_wait();                       // agg comes from the prep kernel
+  pdl_trigger();
+  A2ATS_TL(g_sel_tl, 3);
+  append_hist(a, pair, cp);         // counts taken: the new token joins hist
+  load_keys<kTT>(a, S, pair, cnt, key);
+  find_level<kTT, kTSurv>(a, S, cnt, key, a.keff, skey, scnt);
+  A2ATS_TL(g_sel_tl, 4);
+  const uint32_t kstar = S.s_kstar, m = S.s_m;
+  if (tid == 0) S.s_eq = 0;
+  // classes of codewords l = 32 i + lane (conflict-free reads), packed by ballots: lanes
+  // 0..15 of the warp form word 2 i', lanes 16..31 word 2 i' + 1 (16 x 2 bits each)
+  int e_cnt = 0;
+  for (int l0 = (tid >> 5) * 32; l0 < a.L; l0 += kTT) {
+    const int l = l0 + lane;
+    uint32_t c = 0;
+    if (l < a.L) {
+      const uint32_t kk = key[l];
+      c = (kk < kstar) ? 1u : ((kk == kstar) ? 2u : 0u);
+      if (c == 2u) e_cnt += max(cnt[l], 0);
+    }
+    const uint32_t b0 = __ballot_sync(0xffffffffu, c & 1u), b1 = __ballot_sync(0xffffffffu, c >> 1);
+    if (lane < 2 && l0 + 16 * lane < a.L) {  // interleave 16 bits of b0 (even bits) and b1 (odd bits)
+      uint32_t x0 = (b0 >> (16 * lane)) & 0xffffu, x1 = (b1 >> (16 * lane)) & 0xffffu;
+      x0 = (x0 | (x0 << 8)) & 0x00ff00ffu;
+      x0 = (x0 | (x0 << 4)) & 0x0f0f0f0fu;
+      x0 = (x0 | (x0 << 2)) & 0x33333333u;
+      x0 = (x0 | (x0 << 1)) & 0x55555555u;
+      x1 = (x1 | (x1 << 8)) & 0x00ff00ffu;
+      x1 = (x1 | (x1 << 4)) & 0x0f0f0f0fu;
+      x1 = (x1 | (x1 << 2)) & 0x33333333u;
+      x1 = (x1 | (x1 << 1)) & 0x55555555u;
+      a.tblg[(size_t)pair * W + (l0 >> 4) + lane] = x0 | (x1 << 1);
+    }
+  }
+  e_cnt = __reduce_add_sync(0xffffffffu, e_cnt);
+  __syncthreads();
+  if (lane == 0 && e_cnt) atomicAdd(&S.s_eq, e_cnt);
+  __syncthreads();
+  if (tid == 0) {
+    a.pinfo[pair * 4 + 0] = kstar;
+    a.pinfo[pair * 4 + 1] = m;
+    a.pinfo[pair * 4 + 2] = (uint32_t)a.keff;
+    a.pinfo[pair * 4 + 3] = (uint32_t)S.s_eq;
+  }
+  A2ATS_TL(g_sel_tl, 1);
+}
+
+// Stream one unit (half of a pair's candidate stages).  Super-rounds of two stages (32768
+// tokens): thread t takes stage t >> 9, row (t & 511) >> 1 (64 tokens), half t & 1 (32
+// consecutive tokens, pieces 4 (t & 1) .. + 3, read through the SWIZZLE_128B layout:
+// conflict-free); one warp scan + one CTA barrier per super-round give the output offsets,
+// then the two freed stages are refilled.  At the first super-round's barrier the next
+// unit's table is written into the other buffer (its loads were issued at unit start).
+struct ScanCtx {
+  const SelArgs& a;
+  const PipeGeom& g;
+  uint32_t ring, tbl0;  // shared addresses
+  uint64_t* full;
+  uint32_t* sTot;       // [2][32]
+  int nchunks;
+};
+
+template <bool FWD, class Issue, class Expand>
+__device__ __forceinline__ void scan_unit(const ScanCtx& c, int buf, int pair, int nr, const PipeUnit pu, int& j,
+                                          Issue& issue, Expand& expand) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t tl = c.tbl0 + buf * (c.a.W * 128) + (uint32_t)lane * 4u;
+  const int half = tid >> 9;  // 0: lower stage of the super-round, 1: upper
+  const int row = (tid & 511) >> 1, hp = tid & 1;
+  int32_t* selp = c.a.sel + (size_t)pair * c.a.sel_stride;
+  uint32_t run_gt = 0, run_eq = 0;
+#pragma unroll 1
+  for (int i = 0; i < nr; i += 2) {
+    const bool two = i + 1 < nr;
+    // stages of this super-round: forward i (lower), i + 1 (upper); backward i (upper), i + 1 (lower)
+    const int r_lo = FWD ? i : c.g.R - 2 - i;  // round index of the lower stage (may be absent)
+    const bool mine = FWD ? (half == 0 || two) : (half == 1 || two);
+    const int jmine = FWD ? j + half : j + (1 - half);
+    const int tr = c.g.first + (r_lo + half) * kPRound, t0 = tr + row * 64 + hp * 32;
+    uint4 v[4];
+    if (mine) {
+      const int s = jmine % kPStage;
+      umma::mbar_wait(&c.full[s], (uint32_t)(jmine / kPStage) & 1u);
+      const uint32_t st = c.ring + s * (kPRound * 2) + row * 128;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[q] = lds_v4(st + (((4 * hp + q) ^ (row & 7)) << 4));
+      const int npiece = (min(tr + kPRound, c.g.c1al) - tr) >> 3;
+      if (npiece < kPRound / 8) {  // last stage: codes past the range may be past n_ctx (undefined)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (row * 8 + 4 * hp + q >= npiece) v[q] = make_uint4(0, 0, 0, 0);
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[q] = make_uint4(0, 0, 0, 0);
+    }
+    uint32_t cw[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) cw[q] = classify8s(tl, v[2 * q]) | (classify8s(tl, v[2 * q + 1]) << 16);
+    if (!mine) {
+      cw[0] = cw[1] = 0u;
+    } else if (t0 < c.a.c0 || t0 + 32 > c.a.c1) {  // tokens outside [c0, c1)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) cw[q] &= span_mask(c.a.c0 - t0 - 16 * q, c.a.c1 - t0 - 16 * q);
+    }
+    const uint32_t pk = (uint32_t)(__popc(cw[0] & 0x55555555u) + __popc(cw[1] & 0x55555555u)) |
+                        ((uint32_t)(__popc(cw[0] & 0xaaaaaaaau) + __popc(cw[1] & 0xaaaaaaaau)) << 16);
+    uint32_t incl = pk;  // 16-bit fields: 32768 tokens per super-round
+    if (FWD) {
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += y;
+      }
+    } else {
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t y = __shfl_down_sync(0xffffffffu, incl, off);
+        if (lane + off < 32) incl += y;
+      }
+    }
+    const int par = (i >> 1) & 1;
+    if (lane == (FWD ? 31 : 0)) c.sTot[par * 32 + warp] = incl;
+    __syncthreads();  // every thread has read its stage (and the previous unit is done with the other table)
+    if (tid == 0) {
+      if (j + kPStage < c.nchunks) issue(j + kPStage);
+      if (two && j + 1 + kPStage < c.nchunks) issue(j + 1 + kPStage);
+    }
+    if (i == 0) expand();
+    j += two ? 2 : 1;
+    // lane w holds warp w's total: the super-round total and this warp's offset
+    const uint32_t wv = c.sTot[par * 32 + lane];
+    const uint32_t tot = __reduce_add_sync(0xffffffffu, wv);
+    const uint32_t pre = __reduce_add_sync(0xffffffffu, (FWD ? (lane < warp) : (lane > warp)) ? wv : 0u);
+    const uint32_t ex = pre + incl - pk;
+    uint32_t gb = run_gt + (ex & 0xffffu), eb = run_eq + (ex >> 16);
+    if (pk) {
+      if (FWD) {
+        if (cw[0]) emit16(cw[0], t0, gb, eb, pu.m, pu.cap, selp);
+        if (cw[1]) emit16(cw[1], t0 + 16, gb, eb, pu.m, pu.cap, selp);
+      } else {
+        if (cw[1]) emit16_rev(cw[1], t0 + 16, gb, eb, pu.D, pu.cap, selp);
+        if (cw[0]) emit16_rev(cw[0], t0, gb, eb, pu.D, pu.cap, selp);
+      }
+    }
+    run_gt += tot & 0xffffu;
+    run_eq += tot >> 16;
+  }
+}
+
+__global__ __launch_bounds__(kPAll, 1) void select_scan_kernel(const __grid_constant__ CUtensorMap tmK, SelArgs a) {
+  A2ATS_TL(g_selc_tl, 0);
+  extern __shared__ __align__(128) uint8_t smp[];
+  __shared__ __align__(16) uint32_t sTot[2][32];
+  __shared__ __align__(8) uint64_t full[kPStage];
+  const int P = a.P, nblk = gridDim.x, W = a.W;
+  const int tid = threadIdx.x;
+  uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smp) + 1023) & ~uintptr_t(1023));  // [kPStage][32 KB]
+  uint32_t* tbl0 = reinterpret_cast<uint32_t*>(ring + kPStage * kPRound * 2);  // [2][W * 32]
+  const PipeGeom g = pipe_geom(a);
+  const int R1 = g.R - g.R0;
+  const int nunit = (2 * P - (int)blockIdx.x + nblk - 1) / nblk;        // units u = blockIdx.x + k * nblk
+  const int nk0 = max(0, min(nunit, (P - (int)blockIdx.x + nblk - 1) / nblk));  // forward ones (u < P)
+  const int nchunks = nk0 * g.R0 + (nunit - nk0) * R1;
+
+  if (tid == 0) {
+#pragma unroll
+    for (int i = 0; i < kPStage; ++i) umma::mbar_init(&full[i], 1);
+    umma::mbar_fence_init();
+  }
+  __syncthreads();
+  auto issue = [&](int jj) {  // chunk jj of this CTA's sequence -> stage jj % kPStage (one TMA box)
+    int k, i;
+    if (jj < nk0 * g.R0) {
+      k = jj / g.R0;
+      i = jj - k * g.R0;
+    } else {
+      const int j2 = jj - nk0 * g.R0;
+      k = nk0 + j2 / R1;
+      i = j2 - (k - nk0) * R1;
+    }
+    const int u = blockIdx.x + k * nblk;
+    const bool fwd = u < P;
+    const int pair = fwd ? u : u - P, r = fwd ? i : g.R - 1 - i;
+    const int s = jj % kPStage;
+    umma::mbar_expect_tx(&full[s], (uint32_t)kPRound * 2u);
+    umma::tma_load_3d(ring + (size_t)s * (kPRound * 2), &tmK, 0, (g.first + r * kPRound) >> 6, pair, &full[s]);
+  };
+  if (tid == 0)
+    for (int jj = 0; jj < min(kPStage, nchunks); ++jj) issue(jj);
+  pdl_wait();  // tblg / pinfo come from the threshold kernel (sel: read by the previous step's attention,
+  pdl_trigger();  // complete before the prep kernel triggered)
+  A2ATS_TL(g_selc_tl, 2);
+  // table of unit k: thread t < 4 W replicates word t >> 2 (two 16-B stores); loads issued early
+  const int tw = tid >> 2, tq = (tid & 3) * 2;
+  auto pair_of = [&](int k) {
+    const int u = blockIdx.x + k * nblk;
+    return u < P ? u : u - P;
+  };
+  auto load_unit = [&](int k, uint32_t& x, PipeUnit& pu) {
+    if (k >= nunit) return;
+    const int pair = pair_of(k);
+    x = tw < W ? __ldcg(a.tblg + (size_t)pair * W + tw) : 0u;
+    const uint32_t m = __ldcg(a.pinfo + pair * 4 + 1), cap = __ldcg(a.pinfo + pair * 4 + 2);
+    const uint32_t E = __ldcg(a.pinfo + pair * 4 + 3);
+    pu = PipeUnit{m, E - m, cap, 0u};
+  };
+  auto store_table = [&](int buf, uint32_t x) {
+    if (tw < W) {
+      uint4* dst = reinterpret_cast<uint4*>(tbl0 + buf * (W * 32) + tw * 32);
+      const uint4 v = make_uint4(x, x, x, x);
+      dst[(tq + tw) & 7] = v;
+      dst[(tq + 1 + tw) & 7] = v;
+    }
+  };
+  uint32_t x_cur = 0, x_nxt = 0;
+  PipeUnit pu_cur{}, pu_nxt{};
+  load_unit(0, x_cur, pu_cur);
+  store_table(0, x_cur);
+  __syncthreads();
+  int j = 0;
+  ScanCtx c{a, g, (uint32_t)__cvta_generic_to_shared(ring), (uint32_t)__cvta_generic_to_shared(tbl0), full,
+            &sTot[0][0], nchunks};
+  for (int k = 0; k < nunit; ++k) {
+    const int u = blockIdx.x + k * nblk;
+    const bool fwd = u < P;
+    load_unit(k + 1, x_nxt, pu_nxt);
+    auto expand = [&]() {
+      if (k + 1 < nunit) store_table((k + 1) & 1, x_nxt);
+    };
+    if (fwd) scan_unit<true>(c, k & 1, pair_of(k), g.R0, pu_cur, j, issue, expand);
+    else scan_unit<false>(c, k & 1, pair_of(k), R1, pu_cur, j, issue, expand);
+    __syncthreads();  // the next unit's table is visible
+    pu_cur = pu_nxt;
+    if (tid == 0 && k == 0) A2ATS_TLX(g_selc_tl, 3);
+  }
+  A2ATS_TL(g_selc_tl, 1);
+}
+
+size_t thresh_smem_bytes(int L) { return (size_t)((L + 3) & ~3) * 8 + 2 * kTSurv * 4; }
+size_t scan_smem_bytes(int W) { return 1024 + (size_t)kPStage * kPRound * 2 + (size_t)2 * W * 32 * 4; }
+
 size_t stream_smem_bytes(int L, int W) {
   const int tbl_words = (std::max(((L + 3) & ~3) + L, W * 32) + 3) / 4 * 4;
   return std::max((size_t)tbl_words * 4 + 2 * kSSurv * 4, (size_t)kWinScratch);
@@ -1113,6 +1517,27 @@ cudaError_t launch_select_split(const SelArgs& a, int P, cudaStream_t st) {
   return launch_mode<kScanC>(a, P * a.nchunk, st);
 }
 int select_chunk_tokens() { return kCH; }
+
+bool select_pipe_ok(int L) { return L <= 4096; }
+
+cudaError_t launch_select_pipe(const SelArgs& a, const CUtensorMap& tmK, int nblk, cudaStream_t st) {
+  if (!select_pipe_ok(a.L)) return cudaErrorInvalidValue;
+  const int smt = (int)thresh_smem_bytes(a.L), sms = (int)scan_smem_bytes(a.W);
+  static int set_t = -1, set_s = -1;
+  if (set_t < smt) {
+    cudaError_t e = cudaFuncSetAttribute(select_thresh_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smt);
+    if (e != cudaSuccess) return e;
+    set_t = smt;
+  }
+  if (set_s < sms) {
+    cudaError_t e = cudaFuncSetAttribute(select_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sms);
+    if (e != cudaSuccess) return e;
+    set_s = sms;
+  }
+  cudaError_t e = launch_pdl(select_thresh_kernel, dim3(a.P), dim3(kTT), smt, st, a);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(select_scan_kernel, dim3(nblk), dim3(kPAll), sms, st, tmK, a);
+}
 
 cudaError_t launch_select_stream(const SelArgs& a, int P, cudaStream_t st) {
   const int smem = (int)stream_smem_bytes(a.L, a.W);

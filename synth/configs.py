@@ -37,7 +37,7 @@ class Config:
 
     def n_max(self, extra: int = 0) -> int:
         n = self.N + extra
-        return (n + 7) // 8 * 8
+        return (n + 63) // 64 * 64   # a multiple of 64: the long-context select loads 128-B code rows by TMA
 
     def with_(self, **kw) -> "Config":
         return replace(self, **kw)

@@ -22,6 +22,7 @@ ap.add_argument("--no-hist", action="store_true")
 ap.add_argument("--batch", type=int, default=0)
 ap.add_argument("--L", type=int, default=0)
 ap.add_argument("--N", type=int, default=0)
+ap.add_argument("--select-only", action="store_true", help="a2ats_select_topk (a1..a4) only")
 args = ap.parse_args()
 cfg = CONFIGS[args.config]
 if args.batch:
@@ -47,7 +48,15 @@ e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=Tr
 hist0 = hist.clone()
 c0 = codes[:, :, :cfg.N - 1].to(torch.int64)
 hist0.zero_().scatter_add_(2, c0, torch.ones_like(c0, dtype=torch.int32))
-for it in range(args.iters):
+sel_buf = torch.empty((cfg.B, cfg.Hkv, max(cfg.K, 1)), dtype=torch.int32, device="cuda")
+for it in range(args.iters if args.select_only else 0):
+    flush.fill_(it)
+    e0.record()
+    dec.select(inp["q"], cfg.N, sel_buf)
+    e1.record()
+    torch.cuda.synchronize()
+    print("it", it, "select_topk %.1f us" % (e0.elapsed_time(e1) * 1e3))
+for it in range(0 if args.select_only else args.iters):
     flush.fill_(it)
     dec.hist.copy_(hist0)  # covers [0, N-1): the step appends token N-1
     e0.record()

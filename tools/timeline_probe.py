@@ -23,6 +23,7 @@ from synth import CONFIGS, make_inputs  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C2")
 ap.add_argument("--iters", type=int, default=3)
+ap.add_argument("--select-only", action="store_true", help="a2ats_select_topk (a1..a4) instead of the step")
 args = ap.parse_args()
 cfg = CONFIGS[args.config]
 inp = make_inputs(cfg, 5, device="cuda", with_h=True)
@@ -39,7 +40,8 @@ scratch = torch.zeros_like(codes)
 out = torch.empty((cfg.B, cfg.Hq, 128), device="cuda")
 lib = A.load()
 KMAX = 8192
-kernels = ["prep", "select", "selc", "attn"]
+kernels = ["prep", "select", "selc"] if args.select_only else ["prep", "select", "selc", "attn"]
+sel_buf = torch.empty((cfg.B, cfg.Hkv, cfg.K), dtype=torch.int32, device="cuda")
 fns = {}
 for k in kernels:
     f = getattr(lib, f"a2ats_debug_{k}_timeline")
@@ -49,8 +51,11 @@ flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
 ncta = {}
 for it in range(args.iters):
     flush.fill_(it)
-    dec.hist.copy_(hist0)                           # covers [0, N-1); the step appends token N-1
-    dec.step_append(inp["q"], inp["k_cache"], inp["v_cache"], cfg.N, out=out)
+    dec.hist.copy_(hist if args.select_only else hist0)  # step: covers [0, N-1), the step appends N-1
+    if args.select_only:
+        dec.select(inp["q"], cfg.N, sel_buf)
+    else:
+        dec.step_append(inp["q"], inp["k_cache"], inp["v_cache"], cfg.N, out=out)
     torch.cuda.synchronize()
     tl = {}
     for k in kernels:
@@ -99,6 +104,16 @@ for it in range(args.iters):
         print(f"  select phases (median us): start->wait {d(3, 0):.2f}  threshold+table {d(2, 3):.2f}"
               f" [keys {d(4, 3):.2f} level {d(5, 4):.2f} table {d(2, 5):.2f}]"
               f"  stream {d(1, 2):.2f}  (wait returns {(m[:, 3].min() - t0) / 1e3:.2f}..{(m[:, 3].max() - t0) / 1e3:.2f})")
+    m = tl["select"][valid["select"]]
+    if len(m) and (m[:, 4] > m[:, 3]).all():  # threshold kernel marks: 3 wait returned, 4 level found
+        d = lambda x, y: np.percentile((m[:, x] - m[:, y]) / 1e3, [10, 50, 90]).round(2)
+        print("  thresh (p10/p50/p90 us): start->wait", d(3, 0), " keys+level", d(4, 3), " table+E", d(1, 4))
+    m = tl["selc"][valid["selc"]] if len(valid["selc"]) else []
+    if len(m) and (m[:, 3] > m[:, 2]).all():  # scan kernel marks: 2 wait returned, 3 first unit done
+        d = lambda x, y: np.percentile((m[:, x] - m[:, y]) / 1e3, [10, 50, 90]).round(2)
+        print("  scan (p10/p50/p90 us): start->wait", d(2, 0), " unit0", d(3, 2), " rest", d(1, 3))
+    if args.select_only:
+        continue
     if len(valid["selc"]):
         m = tl["selc"][valid["selc"]]
         m = m[(m[:, 4] > m[:, 0])]
