@@ -91,7 +91,7 @@ void derive(const a2ats_shape* s, const a2ats_params* p, int n_ctx, Derived* d) 
 }
 
 struct DecodeWs {
-  size_t cs, agg, lut, sel, part, actr, cand_keep, pinfo, nsel, wlog, eslot, ectr, tblg, desc, flag, total;
+  size_t cs, agg, lut, sel, part, actr, cand_keep, pinfo, nsel, wlog, eslot, ectr, tblg, desc, flag, qt, total;
 };
 
 DecodeWs decode_layout(const a2ats_shape* s, const a2ats_params* p) {
@@ -118,6 +118,10 @@ DecodeWs decode_layout(const a2ats_shape* s, const a2ats_params* p) {
   w.tblg = o; o = align_up(o + (size_t)P * ((s->L + 15) / 16) * 4);                       // long-context select
   w.desc = o; o = align_up(o + (size_t)P * (s->n_max / select_chunk_tokens() + 2) * 8);
   w.flag = o; o = align_up(o + (size_t)P * 4);                                              // pipe select
+  {
+    const int NV = lut_tile_nv(s->B * G), nvt = (s->B * G + NV - 1) / NV;
+    w.qt = o; o = align_up(o + qprep_bytes(s->Hkv, nvt, NV));                                // q~ B tiles
+  }
   w.total = o;
   return w;
 }
@@ -219,6 +223,7 @@ LutArgs make_lut_args(const a2ats_shape* shape, const a2ats_params* params, cons
                       const void* codebook, float* agg, float* lut_full, float2* cs) {
   LutArgs la;
   la.q = static_cast<const uint16_t*>(q);
+  la.qt = nullptr;
   la.codebook = static_cast<const uint16_t*>(codebook);
   la.agg = agg;
   la.lut_full = lut_full;
@@ -467,7 +472,9 @@ int decode_impl(const a2ats_shape* shape, const a2ats_params* params, int32_t n_
   // prep: a1 + a2 (LUT), the window rows' logits and (append) a0 for token n_ctx - 1, as
   // concurrent roles of one kernel; the new token is inside the window, so the selection never
   // reads its code, and its histogram entry is added by the select kernel after its counts
-  const LutArgs la = make_lut_args(shape, params, d, q, codebook, agg, lut_full, cs);
+  LutArgs la = make_lut_args(shape, params, d, q, codebook, agg, lut_full, cs);
+  // wide query tiles: q~ hi|lo computed once by qprep_kernel instead of in every LUT CTA
+  if (la.NV > 64) la.qt = reinterpret_cast<uint16_t*>(base + Lw.qt);
   PrepArgs p = prep_empty();
   prep_set_lut(p, la);
   // long contexts: the window logits are computed by the select threshold kernel, before its
@@ -510,6 +517,10 @@ int decode_impl(const a2ats_shape* shape, const a2ats_params* params, int32_t n_
   }
   prep_balance(p);
   stage_mark(0, st);
+  if (la.qt) {
+    rc = cuda_status(launch_qprep(la, st));
+    if (rc) return rc;
+  }
   rc = cuda_status(launch_prep(p, tmA, tmC, st));
   if (rc) return rc;
   stage_mark(1, st);

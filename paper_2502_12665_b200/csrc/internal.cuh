@@ -147,6 +147,7 @@ __device__ __forceinline__ void cp_async_wait() {
 // ---------------------------------------------------------------- kernel argument blocks
 struct LutArgs {
   const uint16_t* q;         // bf16 [B, Hq, 128]
+  uint16_t* qt;              // [Hkv, nvt, 32 chunks, NV, 8] q~ hi|lo B tiles from qprep_kernel, or nullptr
   const uint16_t* codebook;  // bf16 [Hkv, L, 128]
   float* agg;                // [B, Hkv, L]
   float* lut_full;           // [B, Hq, L] or nullptr (debug scores)
@@ -250,6 +251,9 @@ struct PrepArgs {
 constexpr int kWinPre = 64;    // window rows per pair whose logits the prep kernel computes
 int prep_lut_cols(int NV);
 int prep_smem_bytes(const PrepArgs& p);  // dynamic smem of a prep launch (max over its roles)
+// q~ = q R_b split hi|lo into the LUT's canonical B-tile layout (la.qt), once per step
+cudaError_t launch_qprep(const LutArgs& la, cudaStream_t st);
+size_t qprep_bytes(int Hkv, int nvt, int NV);
 cudaError_t launch_prep(const PrepArgs& p, const CUtensorMap& tm_codebook, const CUtensorMap& tm_chat,
                         cudaStream_t st);
 cudaError_t launch_scores(const float* lut_full, const uint16_t* codes, float* scores, int B, int Hq, int Hkv,

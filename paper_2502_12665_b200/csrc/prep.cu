@@ -68,47 +68,62 @@ __device__ __forceinline__ void lut_tile(const CUtensorMap& tmA, const PrepArgs&
   }
   if (tid < kHalf) sbcs[tid] = a.bcs[tid];
   __syncthreads();
-  // query tile: vector n = b * G + g <-> q row b * Hq + h * G + g; item = (vector, 8-pair chunk).
-  // All q loads of a pass are issued before any is used (the loop is latency-bound).
-  constexpr int kIt = 4;
+  if (!a.qt) {
+    // query tile: vector n = b * G + g <-> q row b * Hq + h * G + g; item = (vector, 8-pair chunk).
+    // All q loads of a pass are issued before any is used (the loop is latency-bound).
+    constexpr int kIt = 4;
 #pragma unroll 1
-  for (int base = 0; base < NV * 8; base += 128 * kIt) {
-    uint4 u1[kIt], u2[kIt];
+    for (int base = 0; base < NV * 8; base += 128 * kIt) {
+      uint4 u1[kIt], u2[kIt];
 #pragma unroll
-    for (int j = 0; j < kIt; ++j) {
-      const int it = base + j * 128 + tid, vn = vec0 + (it >> 3);
-      u1[j] = u2[j] = make_uint4(0, 0, 0, 0);
-      if (it < NV * 8 && vn < nvec) {
-        const uint16_t* qp = a.q + (size_t)((vn / G) * a.Hq + h * G + vn % G) * kD + (it & 7) * 8;
-        u1[j] = ld_nc_u4(qp);
-        u2[j] = ld_nc_u4(qp + kHalf);
+      for (int j = 0; j < kIt; ++j) {
+        const int it = base + j * 128 + tid, vn = vec0 + (it >> 3);
+        u1[j] = u2[j] = make_uint4(0, 0, 0, 0);
+        if (it < NV * 8 && vn < nvec) {
+          const uint16_t* qp = a.q + (size_t)((vn / G) * a.Hq + h * G + vn % G) * kD + (it & 7) * 8;
+          u1[j] = ld_nc_u4(qp);
+          u2[j] = ld_nc_u4(qp + kHalf);
+        }
       }
-    }
 #pragma unroll
-    for (int j = 0; j < kIt; ++j) {
-      const int it = base + j * 128 + tid;
-      if (it >= NV * 8) break;
-      const int n = it >> 3, c = it & 7;
-      const uint32_t w1[4] = {u1[j].x, u1[j].y, u1[j].z, u1[j].w}, w2[4] = {u2[j].x, u2[j].y, u2[j].z, u2[j].w};
-      uint16_t h1[8], l1[8], h2[8], l2[8];
+      for (int j = 0; j < kIt; ++j) {
+        const int it = base + j * 128 + tid;
+        if (it >= NV * 8) break;
+        const int n = it >> 3, c = it & 7;
+        const uint32_t w1[4] = {u1[j].x, u1[j].y, u1[j].z, u1[j].w}, w2[4] = {u2[j].x, u2[j].y, u2[j].z, u2[j].w};
+        uint16_t h1[8], l1[8], h2[8], l2[8];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {  // q~ = q R_b (Eq. 12), half-split pair (m, m+64); zero rows stay zero
-        const float x1 = (e & 1) ? bf_hi(w1[e >> 1]) : bf_lo(w1[e >> 1]);
-        const float x2 = (e & 1) ? bf_hi(w2[e >> 1]) : bf_lo(w2[e >> 1]);
-        const float2 cs = sbcs[c * 8 + e];
-        umma::split_bf16(fmaf(x1, cs.x, -x2 * cs.y), h1[e], l1[e]);
-        umma::split_bf16(fmaf(x2, cs.x, x1 * cs.y), h2[e], l2[e]);
+        for (int e = 0; e < 8; ++e) {  // q~ = q R_b (Eq. 12), half-split pair (m, m+64); zero rows stay zero
+          const float x1 = (e & 1) ? bf_hi(w1[e >> 1]) : bf_lo(w1[e >> 1]);
+          const float x2 = (e & 1) ? bf_hi(w2[e >> 1]) : bf_lo(w2[e >> 1]);
+          const float2 cs = sbcs[c * 8 + e];
+          umma::split_bf16(fmaf(x1, cs.x, -x2 * cs.y), h1[e], l1[e]);
+          umma::split_bf16(fmaf(x2, cs.x, x1 * cs.y), h2[e], l2[e]);
+        }
+        *reinterpret_cast<uint4*>(sB + ((c)*NV + n) * 16) = pack8(h1);        // hi, elements 0..63
+        *reinterpret_cast<uint4*>(sB + ((c + 8) * NV + n) * 16) = pack8(h2);  // hi, elements 64..127
+        *reinterpret_cast<uint4*>(sB + ((c + 16) * NV + n) * 16) = pack8(l1); // lo
+        *reinterpret_cast<uint4*>(sB + ((c + 24) * NV + n) * 16) = pack8(l2);
       }
-      *reinterpret_cast<uint4*>(sB + ((c)*NV + n) * 16) = pack8(h1);        // hi, elements 0..63
-      *reinterpret_cast<uint4*>(sB + ((c + 8) * NV + n) * 16) = pack8(h2);  // hi, elements 64..127
-      *reinterpret_cast<uint4*>(sB + ((c + 16) * NV + n) * 16) = pack8(l1); // lo
-      *reinterpret_cast<uint4*>(sB + ((c + 24) * NV + n) * 16) = pack8(l2);
     }
   }
   A2ATS_PHASE(g_lut_phase, 1);
+  A2ATS_TL(g_prep_tl, 2);
   pdl_wait();  // the previous step's attention reads cs; its select reads agg
   pdl_trigger();
-  if (tid >= 32) {  // window table cs[r][m] = (cos, sin)(r f_m) from fp64 angles, spread over the LUT CTAs
+  A2ATS_TL(g_prep_tl, 3);
+  if (a.qt) {  // precomputed q~ tile (qprep_kernel, complete: this CTA passed its dependency wait)
+    __shared__ uint64_t qbar;
+    if (tid == 0) {
+      umma::mbar_init(&qbar, 1);
+      umma::mbar_fence_init();
+      umma::mbar_expect_tx(&qbar, (uint32_t)NV * 32 * 16);
+      umma::bulk_load(sB, a.qt + ((size_t)h * a.nvt + y) * 32 * NV * 8, (uint32_t)NV * 32 * 16, &qbar);
+    }
+    __syncthreads();
+    umma::mbar_wait(&qbar, 0);
+  }
+  if (!a.qt && tid >= 32) {  // window table cs[r][m] = (cos, sin)(r f_m) from fp64 angles, spread over the LUT CTAs
 #pragma unroll 1
     for (int k = i * 96 + tid - 32; k < a.window * kHalf; k += p.n_lut * 96) {
       double sn, cn;
@@ -121,6 +136,7 @@ __device__ __forceinline__ void lut_tile(const CUtensorMap& tmA, const PrepArgs&
   __syncthreads();
   umma::fence_after();
   A2ATS_PHASE(g_lut_phase, 2);
+  A2ATS_TL(g_prep_tl, 4);
   const uint32_t tmem = tslot;
   const uint32_t idesc = umma::idesc_bf16(kTC, NV);
   const int nv_here = min(NV, nvec - vec0);
@@ -143,6 +159,7 @@ __device__ __forceinline__ void lut_tile(const CUtensorMap& tmA, const PrepArgs&
     __syncwarp();
     umma::mbar_wait(&mbar, it & 1);
     umma::fence_after();
+    if (it == 0) A2ATS_TL(g_prep_tl, 5);
     if (tid == 0 && xt + 1 < xt1) {  // next codeword tile into the (now free) A buffer
       umma::mbar_expect_tx(&tbar, kTC * kD * 2);
       umma::tma_load_2d(sA, &tmA, 0, h * a.L + code0 + kTC, &tbar);
@@ -152,12 +169,8 @@ __device__ __forceinline__ void lut_tile(const CUtensorMap& tmA, const PrepArgs&
 
     // epilogue: thread <-> codeword row code0 + 32*warp + lane
     const int code = code0 + warp * 32 + lane;
-    // rolled over 16-column blocks (code size over TMEM latency: this runs once per tile)
-#pragma unroll 1
-    for (int col0 = 0; col0 < nv_here; col0 += 16) {
-      uint32_t r[16];
-      umma::tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + col0, r);
-      umma::tmem_wait_ld();
+    // 32-column blocks: two TMEM loads in flight per wait
+    auto fold = [&](const uint32_t (&r)[16], int col0) {
       if (code < a.L) {
         if (a.lut_full) {
 #pragma unroll 1
@@ -183,10 +196,21 @@ __device__ __forceinline__ void lut_tile(const CUtensorMap& tmA, const PrepArgs&
           }
         }
       }
+    };
+#pragma unroll 1
+    for (int col0 = 0; col0 < nv_here; col0 += 32) {
+      uint32_t r0[16], r1[16];
+      const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16) + col0;
+      umma::tmem_ld16(ta, r0);
+      if (col0 + 16 < nv_here) umma::tmem_ld16(ta + 16, r1);
+      umma::tmem_wait_ld();
+      fold(r0, col0);
+      if (col0 + 16 < nv_here) fold(r1, col0 + 16);
     }
     umma::fence_before();
     __syncthreads();  // TMEM read out before the next tile's MMAs
     umma::fence_after();
+    if (it == 0) A2ATS_TL(g_prep_tl, 6);
   }
   A2ATS_PHASE(g_lut_phase, 4);
   if (warp == 0) umma::tmem_dealloc_n(tmem, p.lut_cols);
@@ -287,6 +311,46 @@ __device__ __forceinline__ void window_tile(const PrepArgs& p, int pair0, int np
   }
 }
 
+// q~ = q R_b (Eq. 12) split into bf16 hi + lo, in the LUT's canonical K-major B layout:
+// tile (h, y) = [32 chunks (0..15 hi, 16..31 lo)][NV vectors][8 bf16]; vectors past B*G are 0.
+// Thread <-> (tile, 8-pair chunk c, vector n), n fastest (coalesced 16-B stores).  Also writes
+// the window table cs (fp64 angles) that the LUT CTAs write when there is no qprep.
+__global__ __launch_bounds__(256) void qprep_kernel(LutArgs a) {
+  pdl_wait();  // the previous step's LUT reads qt
+  pdl_trigger();
+  const int NV = a.NV, nvec = a.B * a.G;
+  const int it = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int k = it; k < a.window * kHalf; k += gridDim.x * blockDim.x) {  // window table cs[r][m]
+    double sn, cn;
+    sincos((double)(k >> 6) * a.rt.inv_freq[k & (kHalf - 1)], &sn, &cn);
+    a.cs[k] = make_float2((float)cn, (float)sn);
+  }
+  if (it >= a.Hkv * a.nvt * 8 * NV) return;
+  const int n = it % NV, c = (it / NV) & 7, ty = it / (NV * 8), y = ty % a.nvt, h = ty / a.nvt;
+  const int vn = y * NV + n;
+  uint4 u1 = make_uint4(0, 0, 0, 0), u2 = u1;
+  if (vn < nvec) {
+    const uint16_t* qp = a.q + (size_t)((vn / a.G) * a.Hq + h * a.G + vn % a.G) * kD + c * 8;
+    u1 = ld_nc_u4(qp);
+    u2 = ld_nc_u4(qp + kHalf);
+  }
+  const uint32_t w1[4] = {u1.x, u1.y, u1.z, u1.w}, w2[4] = {u2.x, u2.y, u2.z, u2.w};
+  uint16_t h1[8], l1[8], h2[8], l2[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {  // half-split pair (m, m+64); zero rows stay zero
+    const float x1 = (e & 1) ? bf_hi(w1[e >> 1]) : bf_lo(w1[e >> 1]);
+    const float x2 = (e & 1) ? bf_hi(w2[e >> 1]) : bf_lo(w2[e >> 1]);
+    const float2 cs = a.bcs[c * 8 + e];
+    umma::split_bf16(fmaf(x1, cs.x, -x2 * cs.y), h1[e], l1[e]);
+    umma::split_bf16(fmaf(x2, cs.x, x1 * cs.y), h2[e], l2[e]);
+  }
+  uint4* dst = reinterpret_cast<uint4*>(a.qt + (size_t)ty * 32 * NV * 8);
+  dst[c * NV + n] = pack8(h1);
+  dst[(c + 8) * NV + n] = pack8(h2);
+  dst[(c + 16) * NV + n] = pack8(l1);
+  dst[(c + 24) * NV + n] = pack8(l2);
+}
+
 template <int G>
 __global__ __launch_bounds__(128, 1) void prep_kernel(const __grid_constant__ CUtensorMap tmA,
                                                       const __grid_constant__ CUtensorMap tmC, PrepArgs p) {
@@ -346,6 +410,12 @@ int prep_smem_bytes(const PrepArgs& p) {
   if (p.n_enc) smem = max(smem, encode_tile_smem(p.enc_nv));
   if (p.n_win) smem = max(smem, kWinSmem);
   return smem + 1024;  // alignment slack for the SW128 slabs
+}
+
+size_t qprep_bytes(int Hkv, int nvt, int NV) { return (size_t)Hkv * nvt * 32 * NV * 16; }
+cudaError_t launch_qprep(const LutArgs& la, cudaStream_t st) {
+  const int n = la.Hkv * la.nvt * 8 * la.NV;
+  return launch_pdl(qprep_kernel, dim3((n + 255) / 256), dim3(256), 0, st, la);
 }
 
 int lut_tile_nv(int nvec) { return nvec >= 128 ? 128 : ((nvec + 15) / 16) * 16; }  // MMA N: multiple of 16, <= 128 (B tile <= 64 KB)

@@ -240,9 +240,45 @@ __device__ void find_level(const SelArgs& a, SelShared& S, const int* cnt, const
   if (warp == 0) pick_digit(S, keff);
   Grp::sync();
   A2ATS_PHASE(g_sel_phase, 3);
+  if (NT == 256 && tid == 0) A2ATS_TLX(g_sel_tl, 6);
   const int bstar = S.s_digit;
   int kk = S.s_kk;
   // survivors = candidate codewords of bin b*, one pass (order is irrelevant below)
+  if (a.L <= 32 * NT) {  // keep flags per thread in a mask, one block scan for the slots
+    uint32_t kmask = 0u;
+#pragma unroll 4
+    for (int i = 0; i < 32; ++i) {
+      const int l = i * NT + tid;
+      if (l < a.L && cnt[l] > 0 && bin_of(key[l]) == bstar) kmask |= 1u << i;
+    }
+    const int nk = __popc(kmask);
+    int incl = nk;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += y;
+    }
+    if (lane == 31) S.wsum[warp] = (uint32_t)incl;
+    Grp::sync();
+    int base = incl - nk, tot = 0;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) {
+      const int v = (int)S.wsum[w];
+      base += (w < warp) ? v : 0;
+      tot += v;
+    }
+    while (kmask) {
+      const int i = __ffs(kmask) - 1;
+      kmask &= kmask - 1u;
+      const int l = i * NT + tid;
+      if (base < SC) {
+        skey[base] = key[l];
+        scnt[base] = cnt[l];
+      }
+      ++base;
+    }
+    if (tid == 0) S.s_nsurv = tot;
+  } else
   for (int l0 = 0; l0 < a.L; l0 += NT) {
     const int l = l0 + tid;
     const bool keep = l < a.L && cnt[l] > 0 && bin_of(key[l]) == bstar;
@@ -260,6 +296,7 @@ __device__ void find_level(const SelArgs& a, SelShared& S, const int* cnt, const
   }
   Grp::sync();
   A2ATS_PHASE(g_sel_phase, 4);
+  if (NT == 256 && tid == 0) A2ATS_TLX(g_sel_tl, 7);
   const int nsurv = S.s_nsurv;
   if (nsurv <= NT) {
     // rank each survivor directly: v* is the key with #(< v*) < kk <= #(<= v*);
@@ -1100,6 +1137,7 @@ __global__ __launch_bounds__(kTT, 4) void select_thresh_kernel(SelArgs a) {
   A2ATS_TL(g_sel_tl, 3);
   append_hist(a, pair, cp);         // counts taken: the new token joins hist
   load_keys<kTT>(a, S, pair, cnt, key);
+  if (tid == 0) A2ATS_TLX(g_sel_tl, 5);
   find_level<kTT, kTSurv>(a, S, cnt, key, a.keff, skey, scnt);
   A2ATS_TL(g_sel_tl, 4);
   const uint32_t kstar = S.s_kstar, m = S.s_m;

@@ -95,6 +95,11 @@ for it in range(args.iters):
                 d = lambda x, y: np.median((r[:, x] - r[:, y]) / 1e3)
                 extra = (f"  [cs {d(2, 0):.2f}  1st pair loads {d(3, 2):.2f}  compute {d(4, 3):.2f}"
                          f"  wait {d(5, 4):.2f}  rest {d(1, 5):.2f}]")
+            if role == 1:
+                r = pa[sel]
+                d = lambda x, y: np.median((r[:, x] - r[:, y]) / 1e3)
+                extra = (f"  [q~ {d(2, 0):.2f}  wait {d(3, 2):.2f}  cs {d(4, 3):.2f}  mma1 {d(5, 4):.2f}"
+                         f"  epi1 {d(6, 5):.2f}  rest {d(1, 6):.2f}]")
             print(f"  prep/{name:6s} ctas {len(sel):4d} start {st.min():7.2f}..{st.max():7.2f} end {en.min():7.2f}..{en.max():7.2f}"
                   f"  dur med {np.median(en - st):6.2f}{extra}")
     m = tl["select"][valid["select"]]
@@ -108,6 +113,7 @@ for it in range(args.iters):
     if len(m) and (m[:, 4] > m[:, 3]).all():  # threshold kernel marks: 3 wait returned, 4 level found
         d = lambda x, y: np.percentile((m[:, x] - m[:, y]) / 1e3, [10, 50, 90]).round(2)
         print("  thresh (p10/p50/p90 us): start->wait", d(3, 0), " keys+level", d(4, 3), " table+E", d(1, 4))
+        print("    keys", d(5, 3), " bins+pick", d(6, 5), " survivors", d(7, 6), " rank", d(4, 7))
     m = tl["selc"][valid["selc"]] if len(valid["selc"]) else []
     if len(m) and (m[:, 3] > m[:, 2]).all():  # scan kernel marks: 2 wait returned, 3 first unit done
         d = lambda x, y: np.percentile((m[:, x] - m[:, y]) / 1e3, [10, 50, 90]).round(2)
