@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define A2ATS_ABI_VERSION 4
+#define A2ATS_ABI_VERSION 5
 
 /* ---- status codes ---------------------------------------------------- */
 #define A2ATS_OK 0
@@ -67,6 +67,14 @@ extern "C" {
 #define A2ATS_KV_DEVICE 0       /* K/V cache in HBM */
 #define A2ATS_KV_HOST_MAPPED 1  /* K/V cache in mapped pinned host memory, read over PCIe */
 
+/* lut_engine: which pipes compute the score table LUT = q~ C^T (a2, Eq. 21).  The
+ * contraction is M = L, N = B*G, K = d per KV head: a dense GEMM for large B*G*L (tensor
+ * cores, bf16 hi+lo split of q~), a few thousand FMAs per CTA otherwise. */
+#define A2ATS_LUT_AUTO 0    /* FMA when B*G*L <= A2ATS_LUT_FMA_MAX (0: never), tensor cores above */
+#define A2ATS_LUT_TENSOR 1  /* tcgen05 (TMEM accumulators)                             */
+#define A2ATS_LUT_FMA 2     /* FP32 FMA, one thread per codeword                        */
+#define A2ATS_LUT_FMA_MAX 0  /* measured: no crossover (reading Q26) */
+
 typedef struct a2ats_shape {
   int32_t B;      /* batch size (sequences)                                   */
   int32_t Hq;     /* query heads                                              */
@@ -86,10 +94,12 @@ typedef struct a2ats_params {
                             overrides rope_theta (e.g. Llama-3.1 scaled frequencies)   */
   int32_t group_reduce;  /* A2ATS_GROUP_MAX (default) | A2ATS_GROUP_SUM               */
   int32_t kv_location;   /* A2ATS_KV_DEVICE (default) | A2ATS_KV_HOST_MAPPED          */
+  int32_t lut_engine;    /* A2ATS_LUT_AUTO (default) | A2ATS_LUT_TENSOR | A2ATS_LUT_FMA */
+  int32_t reserved;      /* 0                                                          */
 } a2ats_params;
 
 /* Fills the paper's configuration: w = 64, b = 2048, n_sink = 4, topk = 0,
- * theta = 1e4, GROUP_MAX, KV on device. */
+ * theta = 1e4, GROUP_MAX, KV on device, LUT engine AUTO. */
 void a2ats_default_params(a2ats_params* p);
 
 const char* a2ats_status_string(int status);

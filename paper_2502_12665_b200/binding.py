@@ -25,6 +25,7 @@ A2ATS_GROUP_MAX = 0
 A2ATS_GROUP_SUM = 1
 A2ATS_KV_DEVICE = 0
 A2ATS_KV_HOST_MAPPED = 1
+A2ATS_LUT_AUTO, A2ATS_LUT_TENSOR, A2ATS_LUT_FMA = 0, 1, 2
 
 
 class A2ATSError(RuntimeError):
@@ -45,7 +46,7 @@ class a2ats_params(ctypes.Structure):
     _fields_ = [("window", ctypes.c_int32), ("bridge", ctypes.c_int32), ("n_sink", ctypes.c_int32),
                 ("topk", ctypes.c_int32), ("rope_theta", ctypes.c_double),
                 ("inv_freq", ctypes.POINTER(ctypes.c_double)), ("group_reduce", ctypes.c_int32),
-                ("kv_location", ctypes.c_int32)]
+                ("kv_location", ctypes.c_int32), ("lut_engine", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 _VP = ctypes.c_void_p
@@ -72,7 +73,7 @@ _SIGS = {
 _lib = None
 
 
-ABI_VERSION = 4  # include/a2ats.h A2ATS_ABI_VERSION
+ABI_VERSION = 5  # include/a2ats.h A2ATS_ABI_VERSION
 
 
 def load(path: str = LIB_PATH, build_if_missing: bool = True) -> ctypes.CDLL:
@@ -120,6 +121,7 @@ class Params:
     inv_freq: tuple | None = None
     group_reduce: int = A2ATS_GROUP_MAX
     kv_location: int = A2ATS_KV_DEVICE
+    lut_engine: int = A2ATS_LUT_AUTO
 
     def c(self) -> a2ats_params:
         p = a2ats_params()
@@ -129,7 +131,7 @@ class Params:
         if self.inv_freq is not None:
             self._freq_buf = (ctypes.c_double * len(self.inv_freq))(*self.inv_freq)
             p.inv_freq = ctypes.cast(self._freq_buf, ctypes.POINTER(ctypes.c_double))
-        p.group_reduce, p.kv_location = self.group_reduce, self.kv_location
+        p.group_reduce, p.kv_location, p.lut_engine = self.group_reduce, self.kv_location, self.lut_engine
         return p
 
 

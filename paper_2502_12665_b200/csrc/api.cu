@@ -67,6 +67,7 @@ int check_params(const a2ats_params* p) {
   if (!(p->rope_theta > 0.0) && !p->inv_freq) return A2ATS_EINVAL;
   if (p->group_reduce != A2ATS_GROUP_MAX && p->group_reduce != A2ATS_GROUP_SUM) return A2ATS_EINVAL;
   if (p->kv_location != A2ATS_KV_DEVICE && p->kv_location != A2ATS_KV_HOST_MAPPED) return A2ATS_EINVAL;
+  if (p->lut_engine < A2ATS_LUT_AUTO || p->lut_engine > A2ATS_LUT_FMA) return A2ATS_EINVAL;
   return A2ATS_OK;
 }
 
@@ -327,6 +328,7 @@ void a2ats_default_params(a2ats_params* p) {
   p->inv_freq = nullptr;
   p->group_reduce = A2ATS_GROUP_MAX;
   p->kv_location = A2ATS_KV_DEVICE;
+  p->lut_engine = A2ATS_LUT_AUTO;
 }
 
 const char* a2ats_status_string(int status) {
@@ -473,10 +475,15 @@ int decode_impl(const a2ats_shape* shape, const a2ats_params* params, int32_t n_
   // concurrent roles of one kernel; the new token is inside the window, so the selection never
   // reads its code, and its histogram entry is added by the select kernel after its counts
   LutArgs la = make_lut_args(shape, params, d, q, codebook, agg, lut_full, cs);
+  // LUT engine (a2): FP32 FMA for small B*G*L, tensor cores otherwise (reading of SURVEY 8d C5)
+  const long long bgl = (long long)shape->B * d.G * shape->L;
+  const bool lut_fma = params->lut_engine == A2ATS_LUT_FMA ||
+                       (params->lut_engine == A2ATS_LUT_AUTO && bgl <= A2ATS_LUT_FMA_MAX);
   // wide query tiles: q~ hi|lo computed once by qprep_kernel instead of in every LUT CTA
-  if (la.NV > 64) la.qt = reinterpret_cast<uint16_t*>(base + Lw.qt);
+  if (la.NV > 64 && !lut_fma) la.qt = reinterpret_cast<uint16_t*>(base + Lw.qt);
   PrepArgs p = prep_empty();
   prep_set_lut(p, la);
+  if (lut_fma) p.n_lut = 0;  // lut_fma_kernel computes agg (and the window table) before the prep kernel
   // long contexts: the window logits are computed by the select threshold kernel, before its
   // dependency wait (it waits for this kernel anyway); otherwise by the prep kernel's window role
   const int nchunk = d.c1 > d.c0 ? (d.c1 - ((d.c0 >> 3) << 3) + select_chunk_tokens() - 1) / select_chunk_tokens() : 0;
@@ -519,6 +526,10 @@ int decode_impl(const a2ats_shape* shape, const a2ats_params* params, int32_t n_
   stage_mark(0, st);
   if (la.qt) {
     rc = cuda_status(launch_qprep(la, st));
+    if (rc) return rc;
+  }
+  if (lut_fma) {
+    rc = cuda_status(launch_lut_fma(la, st));
     if (rc) return rc;
   }
   rc = cuda_status(launch_prep(p, tmA, tmC, st));

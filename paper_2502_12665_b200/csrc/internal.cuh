@@ -253,6 +253,8 @@ int prep_lut_cols(int NV);
 int prep_smem_bytes(const PrepArgs& p);  // dynamic smem of a prep launch (max over its roles)
 // q~ = q R_b split hi|lo into the LUT's canonical B-tile layout (la.qt), once per step
 cudaError_t launch_qprep(const LutArgs& la, cudaStream_t st);
+// a2 on the FP32 pipes (lut_engine FMA / AUTO for small B*G*L): agg, lut_full and the window table
+cudaError_t launch_lut_fma(const LutArgs& la, cudaStream_t st);
 size_t qprep_bytes(int Hkv, int nvt, int NV);
 cudaError_t launch_prep(const PrepArgs& p, const CUtensorMap& tm_codebook, const CUtensorMap& tm_chat,
                         cudaStream_t st);

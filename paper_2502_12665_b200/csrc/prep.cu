@@ -351,6 +351,99 @@ __global__ __launch_bounds__(256) void qprep_kernel(LutArgs a) {
   dst[(c + 24) * NV + n] = pack8(l2);
 }
 
+// a2 on the FP32 pipes: LUT[b, hq, l] = q~ . c_l (Eq. 21) with q~ = q R_b (Eq. 12) in fp32,
+// folded over the G query heads (Q10) into agg.  CTA = (128-codeword tile, KV head, tile of
+// 32 query vectors); thread = codeword row (its 256-B codeword streamed in 16-element
+// pieces); q~ rows in shared memory, read as broadcasts.  For contractions too small for the
+// tensor cores to pay off (B*G*L up to ~1e5).  CTAs of vector tile 0 / head 0
+// also write the window table cs[r][m] (fp64 angles), as the tensor LUT's CTAs do.
+template <int G, int FV>
+__global__ __launch_bounds__(128) void lut_fma_kernel(LutArgs a) {
+  __shared__ __align__(16) float sq[FV][kD];
+  __shared__ float2 sbcs[kHalf];
+  const int tid = threadIdx.x, h = blockIdx.y, y = blockIdx.z;
+  const int nvec = a.B * G, v0 = y * FV;
+  const int l = blockIdx.x * 128 + tid;
+  // the thread's codeword row (256 B), all loads in flight before the q~ build
+  uint4 u[16];
+  const uint16_t* cr = a.codebook + ((size_t)h * a.L + min(l, a.L - 1)) * kD;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) u[i] = ld_nc_u4(cr + 8 * i);
+  if (tid < kHalf) sbcs[tid] = a.bcs[tid];
+  __syncthreads();
+  {  // q~ rows of this tile (zero past B*G); all q loads in flight before use
+    constexpr int kJ = FV * kHalf / 128;
+    uint16_t x1[kJ], x2[kJ];
+#pragma unroll
+    for (int j = 0; j < kJ; ++j) {
+      const int it = tid + 128 * j, v = it >> 6, m = it & (kHalf - 1), vn = v0 + v;
+      x1[j] = x2[j] = 0;
+      if (vn < nvec) {
+        const uint16_t* qp = a.q + (size_t)((vn / G) * a.Hq + h * G + vn % G) * kD;
+        x1[j] = __ldg(qp + m);
+        x2[j] = __ldg(qp + m + kHalf);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kJ; ++j) {
+      const int it = tid + 128 * j, v = it >> 6, m = it & (kHalf - 1);
+      const float2 cs = sbcs[m];
+      const float f1 = bf_u16(x1[j]), f2 = bf_u16(x2[j]);
+      sq[v][m] = fmaf(f1, cs.x, -f2 * cs.y);
+      sq[v][m + kHalf] = fmaf(f2, cs.x, f1 * cs.y);
+    }
+  }
+  pdl_wait();  // the previous step's select reads agg, its attention the window table
+  pdl_trigger();
+  if (y == 0 && h == 0)
+    for (int k = blockIdx.x * 128 + tid; k < a.window * kHalf; k += gridDim.x * 128) {
+      double sn, cn;
+      sincos((double)(k >> 6) * a.rt.inv_freq[k & (kHalf - 1)], &sn, &cn);
+      a.cs[k] = make_float2((float)cn, (float)sn);
+    }
+  __syncthreads();
+  if (l >= a.L) return;
+  float acc[FV];
+#pragma unroll
+  for (int v = 0; v < FV; ++v) acc[v] = 0.f;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const float cf[8] = {bf_lo(u[i].x), bf_hi(u[i].x), bf_lo(u[i].y), bf_hi(u[i].y),
+                         bf_lo(u[i].z), bf_hi(u[i].z), bf_lo(u[i].w), bf_hi(u[i].w)};
+#pragma unroll
+    for (int v = 0; v < FV; ++v) {
+      const float4 qa = *reinterpret_cast<const float4*>(&sq[v][8 * i]);
+      const float4 qb = *reinterpret_cast<const float4*>(&sq[v][8 * i + 4]);
+      float t = acc[v];
+      t = fmaf(cf[0], qa.x, t);
+      t = fmaf(cf[1], qa.y, t);
+      t = fmaf(cf[2], qa.z, t);
+      t = fmaf(cf[3], qa.w, t);
+      t = fmaf(cf[4], qb.x, t);
+      t = fmaf(cf[5], qb.y, t);
+      t = fmaf(cf[6], qb.z, t);
+      t = fmaf(cf[7], qb.w, t);
+      acc[v] = t;
+    }
+  }
+  const bool sum = (a.group_reduce == A2ATS_GROUP_SUM);
+#pragma unroll
+  for (int v = 0; v < FV; ++v) {
+    const int vn = v0 + v;
+    if (vn < nvec && a.lut_full) a.lut_full[((size_t)(vn / G) * a.Hq + h * G + vn % G) * a.L + l] = acc[v];
+  }
+#pragma unroll
+  for (int v = 0; v < FV; v += G) {  // fold groups of G consecutive vectors (G | FV)
+    const int vn = v0 + v;
+    if (vn < nvec) {
+      float x = acc[v];
+#pragma unroll
+      for (int g = 1; g < G; ++g) x = sum ? x + acc[v + g] : fmaxf(x, acc[v + g]);
+      a.agg[((size_t)(vn / G) * a.Hkv + h) * a.L + l] = x;
+    }
+  }
+}
+
 template <int G>
 __global__ __launch_bounds__(128, 1) void prep_kernel(const __grid_constant__ CUtensorMap tmA,
                                                       const __grid_constant__ CUtensorMap tmC, PrepArgs p) {
@@ -410,6 +503,21 @@ int prep_smem_bytes(const PrepArgs& p) {
   if (p.n_enc) smem = max(smem, encode_tile_smem(p.enc_nv));
   if (p.n_win) smem = max(smem, kWinSmem);
   return smem + 1024;  // alignment slack for the SW128 slabs
+}
+
+template <int FV>
+cudaError_t launch_lut_fma_fv(const LutArgs& la, cudaStream_t st) {
+  const dim3 grid((la.L + 127) / 128, la.Hkv, (la.B * la.G + FV - 1) / FV);
+  switch (la.G) {
+    case 1: return launch_pdl(lut_fma_kernel<1, FV>, grid, dim3(128), 0, st, la);
+    case 2: return launch_pdl(lut_fma_kernel<2, FV>, grid, dim3(128), 0, st, la);
+    case 4: return launch_pdl(lut_fma_kernel<4, FV>, grid, dim3(128), 0, st, la);
+    default: return launch_pdl(lut_fma_kernel<8, FV>, grid, dim3(128), 0, st, la);
+  }
+}
+// vector tile of 8 for tiny batches (no wasted FMAs), 32 otherwise
+cudaError_t launch_lut_fma(const LutArgs& la, cudaStream_t st) {
+  return la.B * la.G <= 8 ? launch_lut_fma_fv<8>(la, st) : launch_lut_fma_fv<32>(la, st);
 }
 
 size_t qprep_bytes(int Hkv, int nvt, int NV) { return (size_t)Hkv * nvt * 32 * NV * 16; }

@@ -24,7 +24,8 @@ def hist_of(codes: torch.Tensor, L: int, n_ctx: int) -> torch.Tensor:
 
 
 def run_case(cfg: Config, seed: int, family="g2", code_dist="uniform", bridge=None, n_ctx=None, use_hist=True,
-             scores=True, gap_redraw=True, group_reduce=O.GROUP_MAX, pairs=None, device="cuda", n_max=None):
+             scores=True, gap_redraw=True, group_reduce=O.GROUP_MAX, pairs=None, device="cuda", n_max=None,
+             lut_engine=0):
     n_ctx = cfg.N if n_ctx is None else n_ctx
     bridge = cfg.bridge if bridge is None else bridge
     inp = make_inputs(cfg, seed, device="cpu", family=family, code_dist=code_dist, with_h=False, n_max=n_max)
@@ -32,7 +33,8 @@ def run_case(cfg: Config, seed: int, family="g2", code_dist="uniform", bridge=No
     if gap_redraw and family != "g1":
         redraw_for_gap(inp, cfg.with_(bridge=bridge), n_ctx, seed, pairs=pairs)
     dev = {k: (v.to(device) if isinstance(v, torch.Tensor) else v) for k, v in inp.items()}
-    params = A.Params(window=cfg.window, bridge=bridge, n_sink=cfg.n_sink, topk=cfg.K, group_reduce=group_reduce)
+    params = A.Params(window=cfg.window, bridge=bridge, n_sink=cfg.n_sink, topk=cfg.K, group_reduce=group_reduce,
+                      lut_engine=lut_engine)
     shape = A.make_shape(cfg.B, cfg.Hq, cfg.Hkv, cfg.d, cfg.L, inp["n_max"])
     ws = torch.zeros(A.a2ats_decode_workspace_bytes(shape, params), dtype=torch.uint8, device=device)
     out = torch.full((cfg.B, cfg.Hq, cfg.d), float("nan"), device=device)
@@ -74,17 +76,23 @@ def check_against_oracle(cfg, inp, gpu, n_ctx=None, bridge=None, pairs=None, exa
 
 
 # ------------------------------------------------------------------ C1 and small multi-tile shapes
-def test_c1_realistic():
+# LUT engines (a2): AUTO (tensor cores, reading Q26), forced tensor cores, forced FMA
+ENGINES = [0, 1, 2]
+
+
+@pytest.mark.parametrize("lut_engine", ENGINES)
+def test_c1_realistic(lut_engine):
     cfg = CONFIGS["C1"]
-    inp, gpu, _ = run_case(cfg, seed=11)
+    inp, gpu, _ = run_case(cfg, seed=11, lut_engine=lut_engine)
     w = check_against_oracle(cfg, inp, gpu)
     assert w["out"] < 1e-4
 
 
-def test_c1_integer_exact_ties():
+@pytest.mark.parametrize("lut_engine", ENGINES)
+def test_c1_integer_exact_ties(lut_engine):
     # G1 family with b = 0: LUT values exact in fp32 -> cross-code ties exact on both sides
     cfg = CONFIGS["C1"]
-    inp, gpu, _ = run_case(cfg, seed=12, family="g1", bridge=0)
+    inp, gpu, _ = run_case(cfg, seed=12, family="g1", bridge=0, lut_engine=lut_engine)
     check_against_oracle(cfg, inp, gpu, bridge=0)
 
 
@@ -97,9 +105,10 @@ def test_multi_tile_ragged(use_hist):
     check_against_oracle(SMALL, inp, gpu)
 
 
-def test_multi_tile_integer_ties_gqa():
+@pytest.mark.parametrize("lut_engine", [1, 2])
+def test_multi_tile_integer_ties_gqa(lut_engine):
     cfg = SMALL.with_(L=300, K=5000)
-    inp, gpu, _ = run_case(cfg, seed=22, family="g1", bridge=0, code_dist="zipf")
+    inp, gpu, _ = run_case(cfg, seed=22, family="g1", bridge=0, code_dist="zipf", lut_engine=lut_engine)
     check_against_oracle(cfg, inp, gpu, bridge=0)
 
 
@@ -138,15 +147,17 @@ def test_long_context_stream_integer_ties():
 
 
 @pytest.mark.parametrize("G", [1, 2, 4, 8])
-def test_gqa_group_sizes(G):
+@pytest.mark.parametrize("lut_engine", [1, 2])
+def test_gqa_group_sizes(G, lut_engine):
     cfg = Config("gqa", B=2, Hq=2 * G, Hkv=2, d=128, N=3000, L=512, K=180)
-    inp, gpu, _ = run_case(cfg, seed=30 + G)
+    inp, gpu, _ = run_case(cfg, seed=30 + G, lut_engine=lut_engine)
     check_against_oracle(cfg, inp, gpu)
 
 
-def test_group_sum():
+@pytest.mark.parametrize("lut_engine", [1, 2])
+def test_group_sum(lut_engine):
     cfg = Config("gsum", B=2, Hq=8, Hkv=2, d=128, N=5000, L=512, K=300)
-    inp, gpu, _ = run_case(cfg, seed=41, family="g1", bridge=0, group_reduce=O.GROUP_SUM)
+    inp, gpu, _ = run_case(cfg, seed=41, family="g1", bridge=0, group_reduce=O.GROUP_SUM, lut_engine=lut_engine)
     check_against_oracle(cfg, inp, gpu, bridge=0, group_reduce=O.GROUP_SUM)
 
 

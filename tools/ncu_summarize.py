@@ -18,7 +18,7 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-STAGE = [("attn", "attention"), ("select_kernel", "select"), ("prep_kernel", "prep"), ("lut_umma", "lut"), ("qprep", "lut_prep"),
+STAGE = [("attn", "attention"), ("select_kernel", "select"), ("select_thresh", "select"), ("select_scan", "select"), ("prep_kernel", "prep"), ("lut_umma", "lut"), ("qprep", "prep"),
          ("encode_cw", "encode"), ("encode_kernel", "encode"), ("keyh", "encode_keyh")]
 # prefill (encode_bulk_kernel, prepare_kernel) runs before the timed steps: not a path stage
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
