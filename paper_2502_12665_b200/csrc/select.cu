@@ -1041,16 +1041,18 @@ __device__ __forceinline__ uint4 lds_v4(uint32_t addr) {
   asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
   return v;
 }
-// classify8 with the lane's table replica at shared address tl (= table + 4 * lane)
+// classify8 with the lane's table replica at shared address tl = table | 4 * lane, the
+// table 32-KB aligned in the shared window and codes < 4096: word (code >> 4) of the replica
+// is at tl | (code >> 4) << 7, one LOP3 per code (no add)
 __device__ __forceinline__ uint32_t classify8s(uint32_t tl, uint4 v) {
   const uint32_t w[4] = {v.x, v.y, v.z, v.w};
   uint32_t cls = 0u;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const uint32_t x = w[j];
-    const uint32_t wl = lds_u32(tl + ((x << 3) & 0x7ff80u));
+    const uint32_t wl = lds_u32(((x << 3) & 0x7f80u) | tl);
     cls = __funnelshift_r(cls, __funnelshift_r(wl, wl, x << 1), 2);
-    const uint32_t wh = lds_u32(tl + ((x >> 13) & 0x7ff80u));
+    const uint32_t wh = lds_u32(((x >> 13) & 0x7f80u) | tl);
     cls = __funnelshift_r(cls, __funnelshift_r(wh, wh, x >> 15), 2);
   }
   return cls >> 16;
@@ -1184,8 +1186,9 @@ __global__ __launch_bounds__(kTT, 4) void select_thresh_kernel(SelArgs a) {
 // tokens): thread t takes stage t >> 9, row (t & 511) >> 1 (64 tokens), half t & 1 (32
 // consecutive tokens, pieces 4 (t & 1) .. + 3, read through the SWIZZLE_128B layout:
 // conflict-free); one warp scan + one CTA barrier per super-round give the output offsets,
-// then the two freed stages are refilled.  At the first super-round's barrier the next
-// unit's table is written into the other buffer (its loads were issued at unit start).
+// then the two freed stages are refilled.  At the end of the unit the next unit's table is
+// written into the other buffer (its loads were issued at unit start; the previous unit,
+// which read that buffer, finished before this one began).
 struct ScanCtx {
   const SelArgs& a;
   const PipeGeom& g;
@@ -1199,7 +1202,7 @@ template <bool FWD, class Issue, class Expand>
 __device__ __forceinline__ void scan_unit(const ScanCtx& c, int buf, int pair, int nr, const PipeUnit pu, int& j,
                                           Issue& issue, Expand& expand) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t tl = c.tbl0 + buf * (c.a.W * 128) + (uint32_t)lane * 4u;
+  const uint32_t tl = (c.tbl0 + buf * 32768u) | ((uint32_t)lane * 4u);
   const int half = tid >> 9;  // 0: lower stage of the super-round, 1: upper
   const int row = (tid & 511) >> 1, hp = tid & 1;
   int32_t* selp = c.a.sel + (size_t)pair * c.a.sel_stride;
@@ -1256,12 +1259,13 @@ __device__ __forceinline__ void scan_unit(const ScanCtx& c, int buf, int pair, i
     }
     const int par = (i >> 1) & 1;
     if (lane == (FWD ? 31 : 0)) c.sTot[par * 32 + warp] = incl;
+    if (tid == 0 && j < 2) A2ATS_TLX(g_selc_tl, 5);
     __syncthreads();  // every thread has read its stage (and the previous unit is done with the other table)
+    if (tid == 0 && j < 2) A2ATS_TLX(g_selc_tl, 6);
     if (tid == 0) {
       if (j + kPStage < c.nchunks) issue(j + kPStage);
       if (two && j + 1 + kPStage < c.nchunks) issue(j + 1 + kPStage);
     }
-    if (i == 0) expand();
     j += two ? 2 : 1;
     // lane w holds warp w's total: the super-round total and this warp's offset
     const uint32_t wv = c.sTot[par * 32 + lane];
@@ -1280,7 +1284,9 @@ __device__ __forceinline__ void scan_unit(const ScanCtx& c, int buf, int pair, i
     }
     run_gt += tot & 0xffffu;
     run_eq += tot >> 16;
+    if (tid == 0 && j <= 2) A2ATS_TLX(g_selc_tl, 7);
   }
+  expand();  // the next unit's table into the other buffer (its loads were issued at unit start)
 }
 
 __global__ __launch_bounds__(kPAll, 1) void select_scan_kernel(const __grid_constant__ CUtensorMap tmK, SelArgs a) {
@@ -1290,8 +1296,12 @@ __global__ __launch_bounds__(kPAll, 1) void select_scan_kernel(const __grid_cons
   __shared__ __align__(8) uint64_t full[kPStage];
   const int P = a.P, nblk = gridDim.x, W = a.W;
   const int tid = threadIdx.x;
-  uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smp) + 1023) & ~uintptr_t(1023));  // [kPStage][32 KB]
-  uint32_t* tbl0 = reinterpret_cast<uint32_t*>(ring + kPStage * kPRound * 2);  // [2][W * 32]
+  // tables at the first 32-KB boundary of the shared window ([2][32 KB], 32x-replicated class
+  // words: OR-addressing in classify8s), then the ring ([kPStage][32 KB], 1024-B aligned)
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smp);
+  const uint32_t tsh = (sbase + 32767u) & ~32767u;
+  uint32_t* tbl0 = reinterpret_cast<uint32_t*>(smp + (tsh - sbase));
+  uint8_t* ring = smp + (tsh - sbase) + 65536;
   const PipeGeom g = pipe_geom(a);
   const int R1 = g.R - g.R0;
   const int nunit = (2 * P - (int)blockIdx.x + nblk - 1) / nblk;        // units u = blockIdx.x + k * nblk
@@ -1332,17 +1342,19 @@ __global__ __launch_bounds__(kPAll, 1) void select_scan_kernel(const __grid_cons
     const int u = blockIdx.x + k * nblk;
     return u < P ? u : u - P;
   };
+  // loads of unit k's table word and (m, K_eff, E): issued one unit ahead, consumed (E - m)
+  // only when that unit starts, so the L2 latency is never waited for
   auto load_unit = [&](int k, uint32_t& x, PipeUnit& pu) {
     if (k >= nunit) return;
     const int pair = pair_of(k);
     x = tw < W ? __ldcg(a.tblg + (size_t)pair * W + tw) : 0u;
-    const uint32_t m = __ldcg(a.pinfo + pair * 4 + 1), cap = __ldcg(a.pinfo + pair * 4 + 2);
-    const uint32_t E = __ldcg(a.pinfo + pair * 4 + 3);
-    pu = PipeUnit{m, E - m, cap, 0u};
+    pu.m = __ldcg(a.pinfo + pair * 4 + 1);
+    pu.cap = __ldcg(a.pinfo + pair * 4 + 2);
+    pu.D = __ldcg(a.pinfo + pair * 4 + 3);  // E for now
   };
   auto store_table = [&](int buf, uint32_t x) {
     if (tw < W) {
-      uint4* dst = reinterpret_cast<uint4*>(tbl0 + buf * (W * 32) + tw * 32);
+      uint4* dst = reinterpret_cast<uint4*>(tbl0 + buf * 8192 + tw * 32);
       const uint4 v = make_uint4(x, x, x, x);
       dst[(tq + tw) & 7] = v;
       dst[(tq + 1 + tw) & 7] = v;
@@ -1352,7 +1364,9 @@ __global__ __launch_bounds__(kPAll, 1) void select_scan_kernel(const __grid_cons
   PipeUnit pu_cur{}, pu_nxt{};
   load_unit(0, x_cur, pu_cur);
   store_table(0, x_cur);
+  pu_cur.D -= pu_cur.m;
   __syncthreads();
+  if (tid == 0) A2ATS_TLX(g_selc_tl, 4);
   int j = 0;
   ScanCtx c{a, g, (uint32_t)__cvta_generic_to_shared(ring), (uint32_t)__cvta_generic_to_shared(tbl0), full,
             &sTot[0][0], nchunks};
@@ -1367,13 +1381,14 @@ __global__ __launch_bounds__(kPAll, 1) void select_scan_kernel(const __grid_cons
     else scan_unit<false>(c, k & 1, pair_of(k), R1, pu_cur, j, issue, expand);
     __syncthreads();  // the next unit's table is visible
     pu_cur = pu_nxt;
+    pu_cur.D -= pu_cur.m;
     if (tid == 0 && k == 0) A2ATS_TLX(g_selc_tl, 3);
   }
   A2ATS_TL(g_selc_tl, 1);
 }
 
 size_t thresh_smem_bytes(int L) { return (size_t)((L + 3) & ~3) * 8 + 2 * kTSurv * 4; }
-size_t scan_smem_bytes(int W) { return 1024 + (size_t)kPStage * kPRound * 2 + (size_t)2 * W * 32 * 4; }
+size_t scan_smem_bytes(int) { return 32768 + 65536 + (size_t)kPStage * kPRound * 2; }  // align slack + tables + ring
 
 size_t stream_smem_bytes(int L, int W) {
   const int tbl_words = (std::max(((L + 3) & ~3) + L, W * 32) + 3) / 4 * 4;

@@ -118,6 +118,8 @@ for it in range(args.iters):
     if len(m) and (m[:, 3] > m[:, 2]).all():  # scan kernel marks: 2 wait returned, 3 first unit done
         d = lambda x, y: np.percentile((m[:, x] - m[:, y]) / 1e3, [10, 50, 90]).round(2)
         print("  scan (p10/p50/p90 us): start->wait", d(2, 0), " unit0", d(3, 2), " rest", d(1, 3))
+        print("    unit0: table0", d(4, 2), " sr1 classify+scan", d(5, 4), " barrier", d(6, 5), " sr1 emit", d(7, 6),
+              " sr2 + unit end", d(3, 7))
     if args.select_only:
         continue
     if len(valid["selc"]):
