@@ -92,7 +92,7 @@ void derive(const a2ats_shape* s, const a2ats_params* p, int n_ctx, Derived* d) 
 }
 
 struct DecodeWs {
-  size_t cs, agg, lut, sel, part, actr, cand_keep, pinfo, nsel, wlog, eslot, ectr, tblg, desc, flag, qt, total;
+  size_t cs, agg, lut, sel, part, actr, cand_keep, pinfo, nsel, wlog, eslot, ectr, tblg, desc, qt, total;
 };
 
 DecodeWs decode_layout(const a2ats_shape* s, const a2ats_params* p) {
@@ -118,7 +118,6 @@ DecodeWs decode_layout(const a2ats_shape* s, const a2ats_params* p) {
   w.ectr = o; o = align_up(o + (size_t)s->Hkv * 2 * 4);
   w.tblg = o; o = align_up(o + (size_t)P * ((s->L + 15) / 16) * 4);                       // long-context select
   w.desc = o; o = align_up(o + (size_t)P * (s->n_max / select_chunk_tokens() + 2) * 8);
-  w.flag = o; o = align_up(o + (size_t)P * 4);                                              // pipe select
   {
     const int NV = lut_tile_nv(s->B * G), nvt = (s->B * G + NV - 1) / NV;
     w.qt = o; o = align_up(o + qprep_bytes(s->Hkv, nvt, NV));                                // q~ B tiles
@@ -491,7 +490,6 @@ int decode_impl(const a2ats_shape* shape, const a2ats_params* params, int32_t n_
   // hist given: the warp-specialized persistent select (forward / backward half per pair);
   // otherwise threshold + chunked scan (the counts need a pass over the codes)
   const bool pipe_select = long_select && hist != nullptr && select_pipe_ok(shape->L) && shape->n_max % 64 == 0;
-  const bool stream_select = false;
   const bool split_select = long_select && !pipe_select;
   prep_set_window(p, shape, k_cache, wlog, n_ctx, d.w0, d.n_w, 0);
   const int n_wl = p.n_wl;
@@ -553,7 +551,6 @@ int decode_impl(const a2ats_shape* shape, const a2ats_params* params, int32_t n_
     sa.B = shape->B;
     sa.wlog = nullptr;
     sa.P = d.P;
-    sa.flag = reinterpret_cast<unsigned int*>(base + Lw.flag);
     if (split_select && attend) {
       sa.wlog = wlog;
       sa.q = static_cast<const uint16_t*>(q);
@@ -586,7 +583,6 @@ int decode_impl(const a2ats_shape* shape, const a2ats_params* params, int32_t n_
       if (rc) return rc;
     }
     rc = cuda_status(pipe_select    ? launch_select_pipe(sa, tmK, std::min(sm_count(), 2 * d.P), st)
-                     : stream_select  ? launch_select_stream(sa, d.P, st)
                      : split_select ? launch_select_split(sa, d.P, st)
                                     : launch_select(sa, d.P, st));
     if (rc) return rc;

@@ -180,10 +180,7 @@ struct SelArgs {
   uint32_t* tblg;               // [P, W] compact 2-bit classes
   unsigned long long* desc;     // [P, desc_stride] published (#above, #tied) per chunk, 0 = not yet
   int nchunk, desc_stride;
-  // warp-specialized long-context select (launch_select_pipe): P pairs over a persistent grid,
-  // flag[pair] = 1 once the pair's class table is in tblg (reset to 0 by its reader)
-  int P;
-  unsigned int* flag;           // [P]
+  int P;                        // pairs (launch_select_pipe: the scan grid is persistent)
   // window logits computed by the threshold kernel before its dependency wait (long contexts;
   // otherwise the prep kernel's window role): wlog == nullptr disables
   float* wlog;                  // [P, 64, 8]
@@ -265,8 +262,6 @@ cudaError_t launch_shard_hist(const SelArgs& a, int P, cudaStream_t st);
 cudaError_t launch_shard_thresh(const SelArgs& a, int P, cudaStream_t st);
 cudaError_t launch_shard_scan(const SelArgs& a, int P, cudaStream_t st);
 cudaError_t launch_select_split(const SelArgs& a, int P, cudaStream_t st);
-// long contexts with a caller-maintained hist: one streaming CTA per pair (no look-back)
-cudaError_t launch_select_stream(const SelArgs& a, int P, cudaStream_t st);
 int select_chunk_tokens();
 // long-context select with hist (L <= 4096): threshold kernel (grid P) + persistent scan (nblk CTAs)
 cudaError_t launch_select_pipe(const SelArgs& a, const CUtensorMap& tmK, int nblk, cudaStream_t st);

@@ -57,16 +57,10 @@ struct ModeTraits {
   static constexpr int min_blocks = (MODE == kThresh || MODE == kScanC) ? 2 : 1;
 };
 
-// Thread groups: the whole CTA, or a named-barrier group of N threads starting at thread
-// BASE (warp-specialized kernels; BASE is a multiple of 32)
+// Thread group policy of the selection helpers (thread index and barrier): the whole CTA
 struct CtaGrp {
   static __device__ __forceinline__ int tid() { return threadIdx.x; }
   static __device__ __forceinline__ void sync() { __syncthreads(); }
-};
-template <int BASE, int ID, int N>
-struct NamedGrp {
-  static __device__ __forceinline__ int tid() { return (int)threadIdx.x - BASE; }
-  static __device__ __forceinline__ void sync() { asm volatile("bar.sync %0, %1;" ::"n"(ID), "n"(N) : "memory"); }
 };
 
 struct SelShared {
@@ -815,55 +809,7 @@ __device__ __forceinline__ void split_body(const SelArgs& a, SelShared& S, int* 
   }
 }
 
-// ---------------------------------------------------------------- long contexts with hist
-// select_stream_kernel: one 256-thread CTA per pair, four resident per SM, streaming the
-// pair's whole candidate range (no cross-CTA look-back).  Before the dependency wait:
-// counts from hist, the first round of codes into registers; after: v*, m, the 2-bit class
-// table (replicated 32x), then rounds of 8192 tokens, each thread 32 consecutive tokens
-// (two 32-B loads; the next round's are issued before the current one is classified).
-// Output offsets: one warp scan, the warp totals through shared memory (one barrier per
-// round), a running count per CTA.  The codes base must be 32-B aligned.
-constexpr int kST = 256;             // threads per CTA (stream kernel)
-constexpr int kSSurv = 1024;         // survivor list capacity (stream kernel)
-constexpr int kRound = kST * 32;     // tokens per round
-
-__device__ __forceinline__ void ld_nc_v8(const uint16_t* p, uint32_t* r) {
-  asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-               : "l"(p));
-}
-
-// tokens [t, t + 32) of the row (32-B aligned address): codes at or past c1 read as 0 (masked)
-__device__ __forceinline__ void stream_load(const uint16_t* cp, int t, int c1, uint32_t (&v)[16]) {
-  if (t < c1) {
-    ld_nc_v8(cp + t, v);
-  } else {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = 0u;
-  }
-  if (t + 16 < c1) {
-    ld_nc_v8(cp + t + 16, v + 8);
-  } else {
-#pragma unroll
-    for (int i = 8; i < 16; ++i) v[i] = 0u;
-  }
-}
-
-// 2-bit classes of 16 tokens (token e at bits 2e, 2e + 1): word (code >> 4) of the table,
-// replica lane, rotated right by 2 (code & 15); its low field shifted in from the top.
-__device__ __forceinline__ uint32_t classify16(const uint8_t* tb, uint32_t lane4, const uint32_t* w) {
-  uint32_t cls = 0u;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const uint32_t x = w[j];
-    const uint32_t wl = *reinterpret_cast<const uint32_t*>(tb + (((x << 3) & 0x7ff80u) | lane4));
-    cls = __funnelshift_r(cls, __funnelshift_r(wl, wl, x << 1), 2);
-    const uint32_t wh = *reinterpret_cast<const uint32_t*>(tb + (((x >> 13) & 0x7ff80u) | lane4));
-    cls = __funnelshift_r(cls, __funnelshift_r(wh, wh, x >> 15), 2);  // bit 15 of x is 0 (L <= 16384)
-  }
-  return cls;
-}
-
+// ---------------------------------------------------------------- emission helper
 // emit the tokens of a 16-token class word: above-v* fields at base++, tied fields (rare)
 // through the quota; returns nothing, advances gb / eb
 __device__ __forceinline__ void emit16(uint32_t q, int t0, uint32_t& gb, uint32_t& eb, uint32_t m, uint32_t cap,
@@ -896,93 +842,6 @@ __device__ __forceinline__ void emit16(uint32_t q, int t0, uint32_t& gb, uint32_
   }
 }
 
-__global__ __launch_bounds__(kST, 4) void select_stream_kernel(SelArgs a) {
-  A2ATS_TL(g_sel_tl, 0);
-  extern __shared__ __align__(16) uint32_t sm[];
-  __shared__ SelShared S;
-  __shared__ __align__(16) uint32_t sTot[2][8];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int pair = blockIdx.x;
-  int* cnt = reinterpret_cast<int*>(sm);
-  uint32_t* key = sm + ((a.L + 3) & ~3);
-  uint32_t* tbl = sm;
-  const int tbl_words = (max(((a.L + 3) & ~3) + a.L, a.W * 32) + 3) / 4 * 4;
-  uint32_t* skey = sm + tbl_words;
-  int* scnt = reinterpret_cast<int*>(skey + kSSurv);
-  const uint16_t* cp = a.codes + (size_t)pair * a.n_max;
-  const int c0 = a.c0, c1 = a.c1;
-  // rounds start 32-B aligned in memory: rows are 16-B aligned, so a row may start 8 tokens
-  // past a 32-B boundary (then first may be -8: the previous row's last codes, masked; pair 0
-  // starts at the 32-B aligned base)
-  const int mis = (int)((reinterpret_cast<uintptr_t>(cp) >> 1) & 15u);
-  const int first = ((c0 + mis) & ~15) - mis;
-  const int nround = c1 > c0 ? (c1 - first + kRound - 1) / kRound : 0;
-  float wacc[512 / kST];
-  if (a.wlog) {  // the window rows' logits (scratch aliases cnt / key, dead until load_cnt)
-    window_logits<kST>(a, pair, reinterpret_cast<uint8_t*>(sm), wacc);
-    __syncthreads();
-  }
-  uint32_t cur[16];
-  stream_load(cp, first + tid * 32, c1, cur);
-  load_cnt<kST>(a, pair, cnt, cp);
-  pdl_wait();  // agg comes from the prep kernel
-  pdl_trigger();
-  A2ATS_TL(g_sel_tl, 3);
-  if (a.wlog) store_window_logits<kST>(a, pair, wacc);
-  load_keys<kST>(a, S, pair, cnt, key);
-  A2ATS_TL(g_sel_tl, 4);
-  find_level<kST, kSSurv>(a, S, cnt, key, a.keff, skey, scnt);
-  A2ATS_TL(g_sel_tl, 5);
-  const uint32_t kstar = S.s_kstar, m = S.s_m, cap = (uint32_t)a.keff;
-  build_table<kST>(a, key, kstar, tbl);
-  A2ATS_TL(g_sel_tl, 2);
-  int32_t* selp = a.sel + (size_t)pair * a.sel_stride;
-  const uint8_t* tb = reinterpret_cast<const uint8_t*>(tbl);
-  const uint32_t lane4 = (uint32_t)lane * 4u;
-  uint32_t run_gt = 0, run_eq = 0;
-#pragma unroll 1
-  for (int r = 0; r < nround; ++r) {
-    const int t0 = first + r * kRound + tid * 32;
-    uint32_t nxt[16];
-    stream_load(cp, t0 + kRound, r + 1 < nround ? c1 : 0, nxt);
-    uint32_t ca = classify16(tb, lane4, cur), cb = classify16(tb, lane4, cur + 8);
-    if (r == 0 || r + 1 == nround) {  // tokens outside [c0, c1)
-      ca &= span_mask(c0 - t0, c1 - t0);
-      cb &= span_mask(c0 - t0 - 16, c1 - t0 - 16);
-    }
-    const uint32_t pk = (uint32_t)(__popc(ca & 0x55555555u) + __popc(cb & 0x55555555u)) |
-                        ((uint32_t)(__popc(ca & 0xaaaaaaaau) + __popc(cb & 0xaaaaaaaau)) << 16);
-    uint32_t incl = pk;  // 16-bit fields: a warp holds 1024 tokens per round
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
-      if (lane >= off) incl += y;
-    }
-    const int par = r & 1;
-    if (lane == 31) sTot[par][warp] = incl;
-    __syncthreads();
-    const uint4 s0 = *reinterpret_cast<const uint4*>(&sTot[par][0]);
-    const uint4 s1 = *reinterpret_cast<const uint4*>(&sTot[par][4]);
-    const uint32_t sv[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
-    uint32_t pre = 0, tot = 0;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) {
-      pre += (w < warp) ? sv[w] : 0u;
-      tot += sv[w];
-    }
-    const uint32_t ex = pre + incl - pk;
-    uint32_t gb = run_gt + (ex & 0xffffu), eb = run_eq + (ex >> 16);
-    if (ca) emit16(ca, t0, gb, eb, m, cap, selp);
-    if (cb) emit16(cb, t0 + 16, gb, eb, m, cap, selp);
-    run_gt += tot & 0xffffu;
-    run_eq += tot >> 16;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) cur[i] = nxt[i];
-  }
-  append_hist(a, pair, cp);
-  A2ATS_TL(g_sel_tl, 1);
-}
-
 // ---------------------------------------------------------------- long contexts with hist
 // Two kernels after the LUT (prep) kernel:
 //  select_thresh_kernel (grid P, 256 threads, four resident per SM: one wave at C4): per
@@ -1011,25 +870,6 @@ struct PipeUnit {
   uint32_t m, D, cap, pad;
 };
 
-__device__ __forceinline__ void bar_sync_n(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-__device__ __forceinline__ void bar_arrive_n(int id, int n) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* mbar) {
-  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
-  const uint32_t m = static_cast<uint32_t>(__cvta_generic_to_shared(mbar));
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-               ::"r"(d), "l"(src), "r"(bytes), "r"(m)
-               : "memory");
-}
-__device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
-  unsigned int v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_u32(unsigned int* p, unsigned int v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 
 __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
   uint32_t v;
@@ -1058,21 +898,6 @@ __device__ __forceinline__ uint32_t classify8s(uint32_t tl, uint4 v) {
   return cls >> 16;
 }
 
-// 2-bit classes of the 8 tokens of one 16-B piece (token e at bits 2e), from the table
-// replica of this lane
-__device__ __forceinline__ uint32_t classify8(const uint8_t* tb, uint32_t lane4, uint4 v) {
-  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-  uint32_t cls = 0u;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const uint32_t x = w[j];
-    const uint32_t wl = *reinterpret_cast<const uint32_t*>(tb + (((x << 3) & 0x7ff80u) | lane4));
-    cls = __funnelshift_r(cls, __funnelshift_r(wl, wl, x << 1), 2);
-    const uint32_t wh = *reinterpret_cast<const uint32_t*>(tb + (((x >> 13) & 0x7ff80u) | lane4));
-    cls = __funnelshift_r(cls, __funnelshift_r(wh, wh, x >> 15), 2);
-  }
-  return cls >> 16;
-}
 
 // backward emission of a 16-token class word: tokens in decreasing order; a token with
 // ga above-v* and ea tied tokens after it (in this unit) goes to top - 1 - (ga + max(ea - D, 0));
@@ -1390,10 +1215,6 @@ __global__ __launch_bounds__(kPAll, 1) void select_scan_kernel(const __grid_cons
 size_t thresh_smem_bytes(int L) { return (size_t)((L + 3) & ~3) * 8 + 2 * kTSurv * 4; }
 size_t scan_smem_bytes(int) { return 32768 + 65536 + (size_t)kPStage * kPRound * 2; }  // align slack + tables + ring
 
-size_t stream_smem_bytes(int L, int W) {
-  const int tbl_words = (std::max(((L + 3) & ~3) + L, W * 32) + 3) / 4 * 4;
-  return std::max((size_t)tbl_words * 4 + 2 * kSSurv * 4, (size_t)kWinScratch);
-}
 
 template <int MODE>
 __device__ __forceinline__ void select_body(const SelArgs& a) {
@@ -1592,16 +1413,6 @@ cudaError_t launch_select_pipe(const SelArgs& a, const CUtensorMap& tmK, int nbl
   return launch_pdl(select_scan_kernel, dim3(nblk), dim3(kPAll), sms, st, tmK, a);
 }
 
-cudaError_t launch_select_stream(const SelArgs& a, int P, cudaStream_t st) {
-  const int smem = (int)stream_smem_bytes(a.L, a.W);
-  static int smem_set = -1;
-  if (smem_set < smem) {
-    cudaError_t e = cudaFuncSetAttribute(select_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    smem_set = smem;
-  }
-  return launch_pdl(select_stream_kernel, dim3(P), dim3(kST), smem, st, a);
-}
 
 }  // namespace a2ats
 

@@ -350,6 +350,39 @@ def test_c2_full_size_sampled():
     check_against_oracle(cfg, small, gpu, pairs=sample)
 
 
+def test_c4_full_size_sampled():
+    """BASELINE configs[3] on one GPU (B = 64, N = 131072, L = 4096, K = 7865): the long-context
+    select (threshold kernel + persistent half-pair scan) and the attention in the launch
+    configuration bench.py --config C4 times; every pair checked for validity, sampled pairs
+    (both scan halves of different CTAs) against the oracle bit for bit / within 2e-3."""
+    cfg = CONFIGS["C4"]
+    seed = 0xA2A75 + 4
+    inp = make_inputs(cfg, seed, device="cuda", with_h=False)
+    inp["codes"] = inp["z"].to(torch.uint16)
+    del inp["z"]
+    sample = [(0, 0), (17, 3), (40, 7), (63, 5)]
+    host = dict(q=inp["q"].cpu(), codebook=inp["codebook"].cpu(), codes=inp["codes"].cpu())
+    redraw_for_gap(host, cfg, cfg.N, seed, pairs=sample)
+    inp["q"] = host["q"].cuda()
+    dec = A.Decoder(cfg.B, cfg.Hq, cfg.Hkv, cfg.L, inp["n_max"], inp["codebook"])
+    dec.codes = inp["codes"]
+    dec.hist = hist_of(inp["codes"], cfg.L, cfg.N)
+    dec.set_topk(cfg.K)
+    sel = torch.empty((cfg.B, cfg.Hkv, cfg.K), dtype=torch.int32, device="cuda")
+    out = dec.step(inp["q"], inp["k_cache"], inp["v_cache"], cfg.N, sel_out=sel)
+    sel2 = torch.empty_like(sel)
+    dec.select(inp["q"], cfg.N, sel2)
+    torch.cuda.synchronize()
+    assert torch.equal(sel, sel2)
+    s = sel.cpu().numpy()
+    assert np.all(np.diff(s, axis=2) > 0)
+    assert s.min() >= cfg.n_sink and s.max() < cfg.N - cfg.window
+    small = dict(q=host["q"], codebook=host["codebook"], codes=host["codes"],
+                 k_cache=_PairView(inp["k_cache"]), v_cache=_PairView(inp["v_cache"]))
+    gpu = dict(out=out.cpu().numpy(), sel=s, scores=None)
+    check_against_oracle(cfg, small, gpu, pairs=sample)
+
+
 class _PairView:
     """Indexes [b, h] of a device tensor lazily so only sampled pairs cross to the host."""
 
