@@ -32,9 +32,13 @@ inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 // (b, KV head) pairs to fill the GPU a pair is one CTA (no cross-CTA combine) up to
 // kAttnRowsMax rows; with few pairs the rows are split so the grid covers the SMs.
 constexpr int kAttnRowsMax = 2048;  // s_tok capacity of the attention smem layout
+#ifndef A2ATS_ATTN_SPLITS
+#define A2ATS_ATTN_SPLITS 0  // tuning builds only: force the splits per pair (0 = heuristic below)
+#endif
 int attn_rows(int P, long long mmax) {
   const int sms = sm_count();
-  const long long want = (4LL * P >= 3LL * sms) ? 1 : (sms + P - 1) / P;  // splits per pair
+  long long want = (4LL * P >= 3LL * sms) ? 1 : (sms + P - 1) / P;  // splits per pair
+  if (A2ATS_ATTN_SPLITS > 0) want = A2ATS_ATTN_SPLITS;
   long long R = (mmax + want - 1) / want;
   R = (R + 15) / 16 * 16;
   return (int)std::max<long long>(256, std::min<long long>(kAttnRowsMax, R));
@@ -278,9 +282,12 @@ void prep_set_encode(PrepArgs& p, const EncArgs& e, int tpc = 1) {
 }
 // Code tiles per CTA for the LUT / encode roles so that all prep CTAs are resident at once
 // (one wave: the roles then run concurrently), doubling the encode's first.
+#ifndef A2ATS_PREP_WAVES
+#define A2ATS_PREP_WAVES 1
+#endif
 void prep_balance(PrepArgs& p) {
   const int per_sm = std::max(1, (227 * 1024) / (prep_smem_bytes(p) + 1024));
-  const int cap = per_sm * sm_count();
+  const int cap = A2ATS_PREP_WAVES * per_sm * sm_count();
   const int npairs = p.lut.B * p.lut.Hkv;
   for (int guard = 0; guard < 24 && p.n_lut + p.n_enc + p.n_win > cap; ++guard) {
     // shrink the role with the most CTAs per unit of work first
