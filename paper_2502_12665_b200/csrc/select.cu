@@ -947,61 +947,190 @@ __device__ __forceinline__ PipeGeom pipe_geom(const SelArgs& a) {
   return g;
 }
 
+// Threshold of one pair with every thread holding 16 consecutive codewords' keys and counts
+// in registers (L <= 16 * kTT): the range, the 256-bin weighted value histogram, the
+// survivors of the K-th bin (one block scan), their ranking, and -- since a thread's 16
+// codewords are exactly one word of the compact 2-bit table -- the table and E, without
+// re-reading shared memory.  Same selection rule (and bins) as find_level.
 __global__ __launch_bounds__(kTT, 4) void select_thresh_kernel(SelArgs a) {
   A2ATS_TL(g_sel_tl, 0);
   extern __shared__ __align__(16) uint32_t sm[];
   __shared__ SelShared S;
-  const int tid = threadIdx.x, lane = tid & 31, pair = blockIdx.x;
-  const int W = a.W, L4 = (a.L + 3) & ~3;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, pair = blockIdx.x;
+  const int L4 = (a.L + 3) & ~3;
   int* cnt = reinterpret_cast<int*>(sm);
-  uint32_t* key = sm + L4;
-  uint32_t* skey = key + L4;
+  uint32_t* skey = sm + L4;
   int* scnt = reinterpret_cast<int*>(skey + kTSurv);
   const uint16_t* cp = a.codes + (size_t)pair * a.n_max;
   load_cnt<kTT>(a, pair, cnt, cp);  // step inputs
+  const int l0 = tid * 16;
+  int c[16];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    int4 v = make_int4(0, 0, 0, 0);
+    if (l0 + 4 * q + 4 <= a.L) v = *reinterpret_cast<const int4*>(cnt + l0 + 4 * q);
+    else
+      for (int e = 0; e < 4; ++e) (&v.x)[e] = (l0 + 4 * q + e < a.L) ? cnt[l0 + 4 * q + e] : 0;
+    c[4 * q] = v.x; c[4 * q + 1] = v.y; c[4 * q + 2] = v.z; c[4 * q + 3] = v.w;
+  }
   pdl_wait();                       // agg comes from the prep kernel
   pdl_trigger();
   A2ATS_TL(g_sel_tl, 3);
   append_hist(a, pair, cp);         // counts taken: the new token joins hist
-  load_keys<kTT>(a, S, pair, cnt, key);
-  if (tid == 0) A2ATS_TLX(g_sel_tl, 5);
-  find_level<kTT, kTSurv>(a, S, cnt, key, a.keff, skey, scnt);
-  A2ATS_TL(g_sel_tl, 4);
-  const uint32_t kstar = S.s_kstar, m = S.s_m;
-  if (tid == 0) S.s_eq = 0;
-  // classes of codewords l = 32 i + lane (conflict-free reads), packed by ballots: lanes
-  // 0..15 of the warp form word 2 i', lanes 16..31 word 2 i' + 1 (16 x 2 bits each)
-  int e_cnt = 0;
-  for (int l0 = (tid >> 5) * 32; l0 < a.L; l0 += kTT) {
-    const int l = l0 + lane;
-    uint32_t c = 0;
-    if (l < a.L) {
-      const uint32_t kk = key[l];
-      c = (kk < kstar) ? 1u : ((kk == kstar) ? 2u : 0u);
-      if (c == 2u) e_cnt += max(cnt[l], 0);
+  uint32_t k[16];
+  {
+    const float* aggp = a.agg + (size_t)pair * a.L + l0;
+    float f[16];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (l0 + 4 * q + 4 <= a.L) v = __ldcg(reinterpret_cast<const float4*>(aggp + 4 * q));
+      else
+        for (int e = 0; e < 4; ++e) (&v.x)[e] = (l0 + 4 * q + e < a.L) ? __ldcg(aggp + 4 * q + e) : 0.f;
+      f[4 * q] = v.x; f[4 * q + 1] = v.y; f[4 * q + 2] = v.z; f[4 * q + 3] = v.w;
     }
-    const uint32_t b0 = __ballot_sync(0xffffffffu, c & 1u), b1 = __ballot_sync(0xffffffffu, c >> 1);
-    if (lane < 2 && l0 + 16 * lane < a.L) {  // interleave 16 bits of b0 (even bits) and b1 (odd bits)
-      uint32_t x0 = (b0 >> (16 * lane)) & 0xffffu, x1 = (b1 >> (16 * lane)) & 0xffffu;
-      x0 = (x0 | (x0 << 8)) & 0x00ff00ffu;
-      x0 = (x0 | (x0 << 4)) & 0x0f0f0f0fu;
-      x0 = (x0 | (x0 << 2)) & 0x33333333u;
-      x0 = (x0 | (x0 << 1)) & 0x55555555u;
-      x1 = (x1 | (x1 << 8)) & 0x00ff00ffu;
-      x1 = (x1 | (x1 << 4)) & 0x0f0f0f0fu;
-      x1 = (x1 | (x1 << 2)) & 0x33333333u;
-      x1 = (x1 | (x1 << 1)) & 0x55555555u;
-      a.tblg[(size_t)pair * W + (l0 >> 4) + lane] = x0 | (x1 << 1);
+    uint32_t kmn = 0xffffffffu, kmx = 0u;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      k[e] = ~ordered_key(f[e]);
+      if (c[e] > 0) {
+        kmn = min(kmn, k[e]);
+        kmx = max(kmx, k[e]);
+      }
     }
+    kmn = __reduce_min_sync(0xffffffffu, kmn);
+    kmx = __reduce_max_sync(0xffffffffu, kmx);
+    if (tid == 0) {
+      S.s_kmin = 0xffffffffu;
+      S.s_kmax = 0u;
+      S.s_eq = 0;
+    }
+    for (int i = tid; i < 256; i += kTT) S.bins[i] = 0;
+    __syncthreads();
+    if (lane == 0) {
+      atomicMin(&S.s_kmin, kmn);
+      atomicMax(&S.s_kmax, kmx);
+    }
+    __syncthreads();
   }
+  if (tid == 0) A2ATS_TLX(g_sel_tl, 5);
+  const int keff = a.keff;
+  uint32_t kstar, m;
+  const uint32_t kmn = S.s_kmin, kmx = S.s_kmax;
+  if (kmn == kmx) {  // a single level holds every candidate
+    kstar = kmn;
+    m = (uint32_t)keff;
+  } else {
+    auto key_val = [](uint32_t kk) {
+      const uint32_t o = ~kk;
+      return __uint_as_float((o & 0x80000000u) ? (o & 0x7fffffffu) : ~o);
+    };
+    const float amax = key_val(kmn), amin = key_val(kmx);
+    const float scale = 255.99f / (amax - amin);
+    uint32_t binp[4] = {0u, 0u, 0u, 0u};  // 16 bins, one byte each
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const float d = amax - key_val(k[e]);
+      const uint32_t b = d > 0.f ? (uint32_t)min(255, (int)(d * scale)) : 0u;
+      binp[e >> 2] |= b << (8 * (e & 3));
+      if (c[e] > 0) atomicAdd(&S.bins[b], c[e]);
+    }
+    auto bin = [&](int e) { return (binp[e >> 2] >> (8 * (e & 3))) & 255u; };
+    __syncthreads();
+    if (warp == 0) pick_digit(S, keff);
+    __syncthreads();
+    if (tid == 0) A2ATS_TLX(g_sel_tl, 6);
+    const uint32_t bstar = (uint32_t)S.s_digit;
+    int kk = S.s_kk;
+    uint32_t kmask = 0u;
+#pragma unroll
+    for (int e = 0; e < 16; ++e)
+      if (c[e] > 0 && bin(e) == bstar) kmask |= 1u << e;
+    const int nk = __popc(kmask);
+    int incl = nk;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += y;
+    }
+    if (lane == 31) S.wsum[warp] = (uint32_t)incl;
+    __syncthreads();
+    int base = incl - nk, nsurv = 0;
+#pragma unroll
+    for (int w = 0; w < kTT / 32; ++w) {
+      const int v = (int)S.wsum[w];
+      base += (w < warp) ? v : 0;
+      nsurv += v;
+    }
+    if (nsurv <= kTSurv) {
+#pragma unroll
+      for (int e = 0; e < 16; ++e)
+        if ((kmask >> e) & 1u) {
+          skey[base] = k[e];
+          scnt[base] = c[e];
+          ++base;
+        }
+    }
+    __syncthreads();
+    if (tid == 0) A2ATS_TLX(g_sel_tl, 7);
+    if (nsurv <= kTT) {  // rank each survivor directly: #(< v*) < kk <= #(<= v*)
+      if (tid < nsurv) {
+        const uint32_t ki = skey[tid];
+        int less = 0, leq = 0;
+#pragma unroll 4
+        for (int jj = 0; jj < nsurv; ++jj) {
+          const uint32_t kj = skey[jj];
+          const int cj = scnt[jj];
+          less += (kj < ki) ? cj : 0;
+          leq += (kj <= ki) ? cj : 0;
+        }
+        if (less < kk && kk <= leq) {
+          S.s_kstar = ki;
+          S.s_m = (uint32_t)(kk - less);
+        }
+      }
+    } else {  // many survivors: byte passes (from the first differing bit) over the registers
+      uint32_t prefix = 0, mask = 0;
+      for (int pass = 3; pass >= 0; --pass) {
+        const int shift = 8 * pass;
+        for (int i = tid; i < 256; i += kTT) S.bins[i] = 0;
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          if (c[e] > 0 && bin(e) == bstar && (k[e] & mask) == prefix) atomicAdd(&S.bins[(k[e] >> shift) & 255u], c[e]);
+        __syncthreads();
+        if (warp == 0) pick_digit(S, kk);
+        __syncthreads();
+        prefix |= (uint32_t)S.s_digit << shift;
+        mask |= 0xffu << shift;
+        kk = S.s_kk;
+      }
+      if (tid == 0) {
+        S.s_kstar = prefix;
+        S.s_m = (uint32_t)kk;
+      }
+    }
+    __syncthreads();
+    kstar = S.s_kstar;
+    m = S.s_m;
+  }
+  A2ATS_TL(g_sel_tl, 4);
+  // this thread's 16 codewords = word tid of the compact class table; E = #candidates at v*
+  uint32_t x = 0;
+  int e_cnt = 0;
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    x |= ((k[e] < kstar) ? 1u : ((k[e] == kstar) ? 2u : 0u)) << (2 * e);
+    if (k[e] == kstar) e_cnt += max(c[e], 0);
+  }
+  if (tid < a.W) a.tblg[(size_t)pair * a.W + tid] = x;
   e_cnt = __reduce_add_sync(0xffffffffu, e_cnt);
-  __syncthreads();
   if (lane == 0 && e_cnt) atomicAdd(&S.s_eq, e_cnt);
   __syncthreads();
   if (tid == 0) {
     a.pinfo[pair * 4 + 0] = kstar;
     a.pinfo[pair * 4 + 1] = m;
-    a.pinfo[pair * 4 + 2] = (uint32_t)a.keff;
+    a.pinfo[pair * 4 + 2] = (uint32_t)keff;
     a.pinfo[pair * 4 + 3] = (uint32_t)S.s_eq;
   }
   A2ATS_TL(g_sel_tl, 1);
@@ -1212,7 +1341,7 @@ __global__ __launch_bounds__(kPAll, 1) void select_scan_kernel(const __grid_cons
   A2ATS_TL(g_selc_tl, 1);
 }
 
-size_t thresh_smem_bytes(int L) { return (size_t)((L + 3) & ~3) * 8 + 2 * kTSurv * 4; }
+size_t thresh_smem_bytes(int L) { return (size_t)((L + 3) & ~3) * 4 + 2 * kTSurv * 4; }  // cnt + survivors
 size_t scan_smem_bytes(int) { return 32768 + 65536 + (size_t)kPStage * kPRound * 2; }  // align slack + tables + ring
 
 
