@@ -947,51 +947,59 @@ __device__ __forceinline__ PipeGeom pipe_geom(const SelArgs& a) {
   return g;
 }
 
-// Threshold of one pair with every thread holding 16 consecutive codewords' keys and counts
-// in registers (L <= 16 * kTT): the range, the 256-bin weighted value histogram, the
-// survivors of the K-th bin (one block scan), their ranking, and -- since a thread's 16
-// codewords are exactly one word of the compact 2-bit table -- the table and E, without
-// re-reading shared memory.  Same selection rule (and bins) as find_level.
-__global__ __launch_bounds__(kTT, 4) void select_thresh_kernel(SelArgs a) {
-  A2ATS_TL(g_sel_tl, 0);
-  extern __shared__ __align__(16) uint32_t sm[];
-  __shared__ SelShared S;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, pair = blockIdx.x;
-  const int L4 = (a.L + 3) & ~3;
-  int* cnt = reinterpret_cast<int*>(sm);
-  uint32_t* skey = sm + L4;
-  int* scnt = reinterpret_cast<int*>(skey + kTSurv);
-  const uint16_t* cp = a.codes + (size_t)pair * a.n_max;
-  load_cnt<kTT>(a, pair, cnt, cp);  // step inputs
-  const int l0 = tid * 16;
-  int c[16];
+// Thresholds with register-resident codewords: thread t holds the keys and candidate counts
+// of codewords [PT t, PT t + PT) (L <= PT * NT): the range, the 256-bin weighted value
+// histogram, the survivors of the K-th bin (one block scan), their ranking (or byte passes
+// over the registers when there are more than NT), without re-reading shared memory.  Same
+// selection rule and bins as find_level.
+template <int PT>
+__device__ __forceinline__ void load_c_regs(const SelArgs& a, const int* cnt, int (&c)[PT]) {
+  const int l0 = threadIdx.x * PT;
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < PT / 4; ++q) {
     int4 v = make_int4(0, 0, 0, 0);
-    if (l0 + 4 * q + 4 <= a.L) v = *reinterpret_cast<const int4*>(cnt + l0 + 4 * q);
-    else
-      for (int e = 0; e < 4; ++e) (&v.x)[e] = (l0 + 4 * q + e < a.L) ? cnt[l0 + 4 * q + e] : 0;
-    c[4 * q] = v.x; c[4 * q + 1] = v.y; c[4 * q + 2] = v.z; c[4 * q + 3] = v.w;
+    if (l0 + 4 * q + 4 <= a.L) {
+      v = *reinterpret_cast<const int4*>(cnt + l0 + 4 * q);
+    } else {
+      v.x = (l0 + 4 * q + 0 < a.L) ? cnt[l0 + 4 * q + 0] : 0;
+      v.y = (l0 + 4 * q + 1 < a.L) ? cnt[l0 + 4 * q + 1] : 0;
+      v.z = (l0 + 4 * q + 2 < a.L) ? cnt[l0 + 4 * q + 2] : 0;
+      v.w = (l0 + 4 * q + 3 < a.L) ? cnt[l0 + 4 * q + 3] : 0;
+    }
+    c[4 * q] = v.x;
+    c[4 * q + 1] = v.y;
+    c[4 * q + 2] = v.z;
+    c[4 * q + 3] = v.w;
   }
-  pdl_wait();                       // agg comes from the prep kernel
-  pdl_trigger();
-  A2ATS_TL(g_sel_tl, 3);
-  append_hist(a, pair, cp);         // counts taken: the new token joins hist
-  uint32_t k[16];
+}
+
+template <int NT, int PT>
+__device__ __forceinline__ void level_regs(const SelArgs& a, SelShared& S, int pair, const int (&c)[PT],
+                                           uint32_t (&k)[PT], uint32_t* skey, int* scnt, int survcap,
+                                           uint32_t& kstar_out, uint32_t& m_out) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, l0 = tid * PT;
   {
     const float* aggp = a.agg + (size_t)pair * a.L + l0;
-    float f[16];
+    float f[PT];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < PT / 4; ++q) {
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (l0 + 4 * q + 4 <= a.L) v = __ldcg(reinterpret_cast<const float4*>(aggp + 4 * q));
-      else
-        for (int e = 0; e < 4; ++e) (&v.x)[e] = (l0 + 4 * q + e < a.L) ? __ldcg(aggp + 4 * q + e) : 0.f;
-      f[4 * q] = v.x; f[4 * q + 1] = v.y; f[4 * q + 2] = v.z; f[4 * q + 3] = v.w;
+      if (l0 + 4 * q + 4 <= a.L) {
+        v = __ldcg(reinterpret_cast<const float4*>(aggp + 4 * q));
+      } else {
+        v.x = (l0 + 4 * q + 0 < a.L) ? __ldcg(aggp + 4 * q + 0) : 0.f;
+        v.y = (l0 + 4 * q + 1 < a.L) ? __ldcg(aggp + 4 * q + 1) : 0.f;
+        v.z = (l0 + 4 * q + 2 < a.L) ? __ldcg(aggp + 4 * q + 2) : 0.f;
+        v.w = (l0 + 4 * q + 3 < a.L) ? __ldcg(aggp + 4 * q + 3) : 0.f;
+      }
+      f[4 * q] = v.x;
+      f[4 * q + 1] = v.y;
+      f[4 * q + 2] = v.z;
+      f[4 * q + 3] = v.w;
     }
     uint32_t kmn = 0xffffffffu, kmx = 0u;
 #pragma unroll
-    for (int e = 0; e < 16; ++e) {
+    for (int e = 0; e < PT; ++e) {
       k[e] = ~ordered_key(f[e]);
       if (c[e] > 0) {
         kmn = min(kmn, k[e]);
@@ -1003,9 +1011,8 @@ __global__ __launch_bounds__(kTT, 4) void select_thresh_kernel(SelArgs a) {
     if (tid == 0) {
       S.s_kmin = 0xffffffffu;
       S.s_kmax = 0u;
-      S.s_eq = 0;
     }
-    for (int i = tid; i < 256; i += kTT) S.bins[i] = 0;
+    for (int i = tid; i < 256; i += NT) S.bins[i] = 0;
     __syncthreads();
     if (lane == 0) {
       atomicMin(&S.s_kmin, kmn);
@@ -1013,116 +1020,146 @@ __global__ __launch_bounds__(kTT, 4) void select_thresh_kernel(SelArgs a) {
     }
     __syncthreads();
   }
-  if (tid == 0) A2ATS_TLX(g_sel_tl, 5);
+  if (NT == 256 && tid == 0) A2ATS_TLX(g_sel_tl, 5);
   const int keff = a.keff;
-  uint32_t kstar, m;
   const uint32_t kmn = S.s_kmin, kmx = S.s_kmax;
   if (kmn == kmx) {  // a single level holds every candidate
-    kstar = kmn;
-    m = (uint32_t)keff;
-  } else {
-    auto key_val = [](uint32_t kk) {
-      const uint32_t o = ~kk;
-      return __uint_as_float((o & 0x80000000u) ? (o & 0x7fffffffu) : ~o);
-    };
-    const float amax = key_val(kmn), amin = key_val(kmx);
-    const float scale = 255.99f / (amax - amin);
-    uint32_t binp[4] = {0u, 0u, 0u, 0u};  // 16 bins, one byte each
-#pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      const float d = amax - key_val(k[e]);
-      const uint32_t b = d > 0.f ? (uint32_t)min(255, (int)(d * scale)) : 0u;
-      binp[e >> 2] |= b << (8 * (e & 3));
-      if (c[e] > 0) atomicAdd(&S.bins[b], c[e]);
-    }
-    auto bin = [&](int e) { return (binp[e >> 2] >> (8 * (e & 3))) & 255u; };
-    __syncthreads();
-    if (warp == 0) pick_digit(S, keff);
-    __syncthreads();
-    if (tid == 0) A2ATS_TLX(g_sel_tl, 6);
-    const uint32_t bstar = (uint32_t)S.s_digit;
-    int kk = S.s_kk;
-    uint32_t kmask = 0u;
-#pragma unroll
-    for (int e = 0; e < 16; ++e)
-      if (c[e] > 0 && bin(e) == bstar) kmask |= 1u << e;
-    const int nk = __popc(kmask);
-    int incl = nk;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl, off);
-      if (lane >= off) incl += y;
-    }
-    if (lane == 31) S.wsum[warp] = (uint32_t)incl;
-    __syncthreads();
-    int base = incl - nk, nsurv = 0;
-#pragma unroll
-    for (int w = 0; w < kTT / 32; ++w) {
-      const int v = (int)S.wsum[w];
-      base += (w < warp) ? v : 0;
-      nsurv += v;
-    }
-    if (nsurv <= kTSurv) {
-#pragma unroll
-      for (int e = 0; e < 16; ++e)
-        if ((kmask >> e) & 1u) {
-          skey[base] = k[e];
-          scnt[base] = c[e];
-          ++base;
-        }
-    }
-    __syncthreads();
-    if (tid == 0) A2ATS_TLX(g_sel_tl, 7);
-    if (nsurv <= kTT) {  // rank each survivor directly: #(< v*) < kk <= #(<= v*)
-      if (tid < nsurv) {
-        const uint32_t ki = skey[tid];
-        int less = 0, leq = 0;
-#pragma unroll 4
-        for (int jj = 0; jj < nsurv; ++jj) {
-          const uint32_t kj = skey[jj];
-          const int cj = scnt[jj];
-          less += (kj < ki) ? cj : 0;
-          leq += (kj <= ki) ? cj : 0;
-        }
-        if (less < kk && kk <= leq) {
-          S.s_kstar = ki;
-          S.s_m = (uint32_t)(kk - less);
-        }
-      }
-    } else {  // many survivors: byte passes (from the first differing bit) over the registers
-      uint32_t prefix = 0, mask = 0;
-      for (int pass = 3; pass >= 0; --pass) {
-        const int shift = 8 * pass;
-        for (int i = tid; i < 256; i += kTT) S.bins[i] = 0;
-        __syncthreads();
-#pragma unroll
-        for (int e = 0; e < 16; ++e)
-          if (c[e] > 0 && bin(e) == bstar && (k[e] & mask) == prefix) atomicAdd(&S.bins[(k[e] >> shift) & 255u], c[e]);
-        __syncthreads();
-        if (warp == 0) pick_digit(S, kk);
-        __syncthreads();
-        prefix |= (uint32_t)S.s_digit << shift;
-        mask |= 0xffu << shift;
-        kk = S.s_kk;
-      }
-      if (tid == 0) {
-        S.s_kstar = prefix;
-        S.s_m = (uint32_t)kk;
-      }
-    }
-    __syncthreads();
-    kstar = S.s_kstar;
-    m = S.s_m;
+    kstar_out = kmn;
+    m_out = (uint32_t)keff;
+    return;
   }
-  A2ATS_TL(g_sel_tl, 4);
-  // this thread's 16 codewords = word tid of the compact class table; E = #candidates at v*
-  uint32_t x = 0;
-  int e_cnt = 0;
+  auto key_val = [](uint32_t kk) {
+    const uint32_t o = ~kk;
+    return __uint_as_float((o & 0x80000000u) ? (o & 0x7fffffffu) : ~o);
+  };
+  const float amax = key_val(kmn), amin = key_val(kmx);
+  const float scale = 255.99f / (amax - amin);
+  uint32_t binp[PT / 4];  // PT bins, one byte each
 #pragma unroll
-  for (int e = 0; e < 16; ++e) {
+  for (int q = 0; q < PT / 4; ++q) binp[q] = 0u;
+#pragma unroll
+  for (int e = 0; e < PT; ++e) {
+    const float d = amax - key_val(k[e]);
+    const uint32_t b = d > 0.f ? (uint32_t)min(255, (int)(d * scale)) : 0u;
+    binp[e >> 2] |= b << (8 * (e & 3));
+    if (c[e] > 0) atomicAdd(&S.bins[b], c[e]);
+  }
+  auto bin = [&](int e) { return (binp[e >> 2] >> (8 * (e & 3))) & 255u; };
+  __syncthreads();
+  if (warp == 0) pick_digit(S, keff);
+  __syncthreads();
+  if (NT == 256 && tid == 0) A2ATS_TLX(g_sel_tl, 6);
+  const uint32_t bstar = (uint32_t)S.s_digit;
+  int kk = S.s_kk;
+  uint32_t kmask = 0u;
+#pragma unroll
+  for (int e = 0; e < PT; ++e)
+    if (c[e] > 0 && bin(e) == bstar) kmask |= 1u << e;
+  const int nk = __popc(kmask);
+  int incl = nk;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += y;
+  }
+  if (lane == 31) S.wsum[warp] = (uint32_t)incl;
+  __syncthreads();
+  int base = incl - nk, nsurv = 0;
+#pragma unroll
+  for (int w = 0; w < NT / 32; ++w) {
+    const int v = (int)S.wsum[w];
+    base += (w < warp) ? v : 0;
+    nsurv += v;
+  }
+  if (nsurv <= NT && nsurv <= survcap) {
+#pragma unroll
+    for (int e = 0; e < PT; ++e)
+      if ((kmask >> e) & 1u) {
+        skey[base] = k[e];
+        scnt[base] = c[e];
+        ++base;
+      }
+  }
+  __syncthreads();
+  if (NT == 256 && tid == 0) A2ATS_TLX(g_sel_tl, 7);
+  if (nsurv <= NT && nsurv <= survcap) {  // rank each survivor directly: #(< v*) < kk <= #(<= v*)
+    if (tid < nsurv) {
+      const uint32_t ki = skey[tid];
+      int less = 0, leq = 0;
+#pragma unroll 4
+      for (int jj = 0; jj < nsurv; ++jj) {
+        const uint32_t kj = skey[jj];
+        const int cj = scnt[jj];
+        less += (kj < ki) ? cj : 0;
+        leq += (kj <= ki) ? cj : 0;
+      }
+      if (less < kk && kk <= leq) {
+        S.s_kstar = ki;
+        S.s_m = (uint32_t)(kk - less);
+      }
+    }
+  } else {  // many survivors: byte passes over the registers, restricted to bin b*
+    uint32_t prefix = 0, mask = 0;
+    for (int pass = 3; pass >= 0; --pass) {
+      const int shift = 8 * pass;
+      for (int i = tid; i < 256; i += NT) S.bins[i] = 0;
+      __syncthreads();
+#pragma unroll
+      for (int e = 0; e < PT; ++e)
+        if (c[e] > 0 && bin(e) == bstar && (k[e] & mask) == prefix) atomicAdd(&S.bins[(k[e] >> shift) & 255u], c[e]);
+      __syncthreads();
+      if (warp == 0) pick_digit(S, kk);
+      __syncthreads();
+      prefix |= (uint32_t)S.s_digit << shift;
+      mask |= 0xffu << shift;
+      kk = S.s_kk;
+    }
+    if (tid == 0) {
+      S.s_kstar = prefix;
+      S.s_m = (uint32_t)kk;
+    }
+  }
+  __syncthreads();
+  kstar_out = S.s_kstar;
+  m_out = S.s_m;
+}
+
+// 2-bit classes of the thread's PT codewords (codeword e at bits 2e) and their candidates at v*
+template <int PT>
+__device__ __forceinline__ uint32_t class_bits(const uint32_t (&k)[PT], const int (&c)[PT], uint32_t kstar, int& e_cnt) {
+  uint32_t x = 0;
+#pragma unroll
+  for (int e = 0; e < PT; ++e) {
     x |= ((k[e] < kstar) ? 1u : ((k[e] == kstar) ? 2u : 0u)) << (2 * e);
     if (k[e] == kstar) e_cnt += max(c[e], 0);
   }
+  return x;
+}
+
+__global__ __launch_bounds__(kTT, 4) void select_thresh_kernel(SelArgs a) {
+  A2ATS_TL(g_sel_tl, 0);
+  extern __shared__ __align__(16) uint32_t sm[];
+  __shared__ SelShared S;
+  const int tid = threadIdx.x, lane = tid & 31, pair = blockIdx.x;
+  const int L4 = (a.L + 3) & ~3;
+  int* cnt = reinterpret_cast<int*>(sm);
+  uint32_t* skey = sm + L4;
+  int* scnt = reinterpret_cast<int*>(skey + kTSurv);
+  const uint16_t* cp = a.codes + (size_t)pair * a.n_max;
+  load_cnt<kTT>(a, pair, cnt, cp);  // step inputs
+  int c[16];
+  load_c_regs<16>(a, cnt, c);
+  pdl_wait();                       // agg comes from the prep kernel
+  pdl_trigger();
+  A2ATS_TL(g_sel_tl, 3);
+  append_hist(a, pair, cp);         // counts taken: the new token joins hist
+  if (tid == 0) S.s_eq = 0;
+  uint32_t k[16], kstar, m;
+  level_regs<kTT, 16>(a, S, pair, c, k, skey, scnt, kTSurv, kstar, m);
+  A2ATS_TL(g_sel_tl, 4);
+  // this thread's 16 codewords = word tid of the compact class table; E = #candidates at v*
+  int e_cnt = 0;
+  const uint32_t x = class_bits<16>(k, c, kstar, e_cnt);
   if (tid < a.W) a.tblg[(size_t)pair * a.W + tid] = x;
   e_cnt = __reduce_add_sync(0xffffffffu, e_cnt);
   if (lane == 0 && e_cnt) atomicAdd(&S.s_eq, e_cnt);
@@ -1130,7 +1167,7 @@ __global__ __launch_bounds__(kTT, 4) void select_thresh_kernel(SelArgs a) {
   if (tid == 0) {
     a.pinfo[pair * 4 + 0] = kstar;
     a.pinfo[pair * 4 + 1] = m;
-    a.pinfo[pair * 4 + 2] = (uint32_t)keff;
+    a.pinfo[pair * 4 + 2] = (uint32_t)a.keff;
     a.pinfo[pair * 4 + 3] = (uint32_t)S.s_eq;
   }
   A2ATS_TL(g_sel_tl, 1);
@@ -1430,7 +1467,11 @@ __device__ __forceinline__ void select_body(const SelArgs& a) {
   // the first chunk of local candidate codes, and (fused) the candidate counts
   const int first = lo + (((c0 - lo) >> 3) << 3);
   if (c0 < c1) prefetch_chunk(a, cp_local, first, c1, sC);
+  // L <= 8 * kNT: every thread keeps 8 codewords' counts and keys in registers (level_regs)
+  const bool regs = (MODE == kFused) && a.L <= 8 * kNT;
+  int c8[8];
   if (MODE == kFused) load_cnt(a, pair, cnt, cp_local);
+  if (regs) load_c_regs<8>(a, cnt, c8);
   A2ATS_PHASE(g_sel_phase, 1);
   pdl_wait();  // agg comes from the LUT kernel
   pdl_trigger();
@@ -1442,12 +1483,30 @@ __device__ __forceinline__ void select_body(const SelArgs& a) {
       append_hist(a, pair, cp_local);
       return;
     }
-    load_keys(a, S, pair, cnt, key);
-    A2ATS_PHASE(g_sel_phase, 2);
-    find_level(a, S, cnt, key, a.keff, skey, scnt);
-    A2ATS_PHASE(g_sel_phase, 5);
-    kstar = S.s_kstar;
-    m = S.s_m;
+    if (regs) {
+      uint32_t k8[8];
+      level_regs<kNT, 8>(a, S, pair, c8, k8, skey, scnt, kSurvCap, kstar, m);
+      // class table: word w = codewords of threads 2w (low half) and 2w + 1, replicated 32x
+      int e_unused = 0;
+      const uint32_t x = class_bits<8>(k8, c8, kstar, e_unused);
+      const uint32_t o = __shfl_xor_sync(0xffffffffu, x, 1);
+      const uint32_t xw = (tid & 1) ? (o | (x << 16)) : (x | (o << 16));
+      const int w = tid >> 1;
+      if (w < a.W) {
+        uint4* dst = reinterpret_cast<uint4*>(tbl + w * 32);
+        const uint4 v = make_uint4(xw, xw, xw, xw);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dst[((tid & 1) * 4 + q + w) & 7] = v;
+      }
+      __syncthreads();
+    } else {
+      load_keys(a, S, pair, cnt, key);
+      A2ATS_PHASE(g_sel_phase, 2);
+      find_level(a, S, cnt, key, a.keff, skey, scnt);
+      A2ATS_PHASE(g_sel_phase, 5);
+      kstar = S.s_kstar;
+      m = S.s_m;
+    }
     cap = (uint32_t)a.keff;
   } else {
     // shard scan: key from agg, v*/m from shard_thresh, this rank's tie quota from the gather
@@ -1466,7 +1525,7 @@ __device__ __forceinline__ void select_body(const SelArgs& a) {
     if (tid == 0) a.nsel_out[pair] = (int)cap;
     __syncthreads();
   }
-  build_table(a, key, kstar, tbl);
+  if (!regs) build_table(a, key, kstar, tbl);
   A2ATS_PHASE(g_sel_phase, 6);
   if (MODE == kShardScan && cap == 0) {
     cp_async_wait<0>();
