@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define A2ATS_ABI_VERSION 5
+#define A2ATS_ABI_VERSION 6
 
 /* ---- status codes ---------------------------------------------------- */
 #define A2ATS_OK 0
@@ -200,6 +200,22 @@ int a2ats_select_topk(const a2ats_shape* shape, const a2ats_params* params, int3
                       const void* q, const uint16_t* codes, const void* codebook,
                       const int32_t* hist, int32_t* sel_out, void* ws, size_t ws_bytes,
                       void* stream);
+
+/* ---------------------------------------------------------------------
+ * a2ats_stage_rows -- the step's inputs into device memory with one kernel
+ * (no copy-engine operation): q_src [B, Hq, d] bf16 -> q_dst [B, Hq, d], and
+ * the new token's key / value rows k_src, v_src [B, Hkv, d] bf16 ->
+ * k_cache / v_cache [B, Hkv, n_max, d] at row n_ctx - 1.  Sources may be
+ * device memory or MAPPED PINNED HOST memory (cudaHostAlloc / torch
+ * pin_memory under UVA), read over PCIe by the kernel; any NULL source is
+ * skipped.  All pointers 16-B aligned; 1 <= n_ctx <= n_max, else EINVAL.
+ * Enqueued on `stream`, chained to the next library kernel (PDL).
+ * Not a step of the paper: the plumbing of an end-to-end decode step.  The
+ * output of a decode step may likewise be mapped pinned host memory (`out`
+ * is written once per (b, hq) row by the attention kernel).
+ * ------------------------------------------------------------------- */
+int a2ats_stage_rows(const a2ats_shape* shape, int32_t n_ctx, const void* q_src, const void* k_src,
+                     const void* v_src, void* q_dst, void* k_cache, void* v_cache, void* stream);
 
 /* ---------------------------------------------------------------------
  * a2ats_decode_step_append -- a0 for the new token, then a1..a6 (one

@@ -54,6 +54,7 @@ _SIGS = {
     "a2ats_default_params": (None, [ctypes.POINTER(a2ats_params)]),
     "a2ats_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "a2ats_abi_version": (ctypes.c_int, []),
+    "a2ats_stage_rows": (ctypes.c_int, [ctypes.POINTER(a2ats_shape), ctypes.c_int32, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
     "a2ats_last_cuda_error": (ctypes.c_char_p, []),
     "a2ats_qavq_prepare": (ctypes.c_int, [ctypes.POINTER(a2ats_shape), _VP, _VP, _VP, _VP, _VP]),
     "a2ats_build_codes_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(a2ats_shape)]),
@@ -73,7 +74,7 @@ _SIGS = {
 _lib = None
 
 
-ABI_VERSION = 5  # include/a2ats.h A2ATS_ABI_VERSION
+ABI_VERSION = 6  # include/a2ats.h A2ATS_ABI_VERSION
 
 
 def load(path: str = LIB_PATH, build_if_missing: bool = True) -> ctypes.CDLL:
@@ -146,8 +147,11 @@ def _ptr(t, name, dtype=None, optional=False, host_ok=False):
         raise TypeError(f"{name}: expected {dtype}, got {t.dtype}")
     if not t.is_contiguous():
         raise ValueError(f"{name} must be contiguous")
-    if not host_ok and not t.is_cuda:
-        raise ValueError(f"{name} must be a CUDA tensor")
+    if not t.is_cuda:
+        if not host_ok:
+            raise ValueError(f"{name} must be a CUDA tensor")
+        if host_ok == "pinned" and not t.is_pinned():
+            raise ValueError(f"{name}: host tensors must be pinned (mapped) memory")
     return t.data_ptr()
 
 
@@ -209,10 +213,23 @@ def a2ats_decode_step_append(shape: a2ats_shape, params, n_ctx: int, q, k_cache,
         _ptr(k_cache, "k_cache", torch.bfloat16), _ptr(v_cache, "v_cache", torch.bfloat16),
         _ptr(codes, "codes", torch.uint16), _ptr(codebook, "codebook", torch.bfloat16),
         _ptr(hist, "hist", torch.int32, optional=True), _ptr(chat, "chat", torch.bfloat16),
-        _ptr(nrm, "nrm", torch.float32), _ptr(out, "out", torch.float32),
+        _ptr(nrm, "nrm", torch.float32), _ptr(out, "out", torch.float32, host_ok="pinned"),
         _ptr(sel_out, "sel_out", torch.int32, optional=True), _ptr(scores_out, "scores_out", torch.float32, optional=True),
         _ptr(ws, "ws"), ws.numel() * ws.element_size(), _stream(stream))
     _check("a2ats_decode_step_append", rc)
+
+
+def a2ats_stage_rows(shape: a2ats_shape, n_ctx: int, q_src, k_src, v_src, q_dst, k_cache, v_cache, stream=None):
+    """One kernel copies q and the new token's K/V rows (device or pinned host sources) into
+    q_dst and row n_ctx - 1 of the caches."""
+    import torch
+    rc = load().a2ats_stage_rows(
+        ctypes.byref(shape), int(n_ctx), _ptr(q_src, "q_src", torch.bfloat16, optional=True, host_ok="pinned"),
+        _ptr(k_src, "k_src", torch.bfloat16, optional=True, host_ok="pinned"),
+        _ptr(v_src, "v_src", torch.bfloat16, optional=True, host_ok="pinned"),
+        _ptr(q_dst, "q_dst", torch.bfloat16, optional=True), _ptr(k_cache, "k_cache", torch.bfloat16, optional=True),
+        _ptr(v_cache, "v_cache", torch.bfloat16, optional=True), _stream(stream))
+    _check("a2ats_stage_rows", rc)
 
 
 def a2ats_select_topk(shape: a2ats_shape, params, n_ctx: int, q, codes, codebook, hist, sel_out, ws, stream=None):

@@ -668,6 +668,49 @@ int a2ats_select_topk(const a2ats_shape* shape, const a2ats_params* params, int3
                      false);
 }
 
+// ------------------------------------------------------------------ end-to-end staging
+namespace a2ats {
+// one 16-B piece per thread: q pieces first, then the key rows, then the value rows
+__global__ __launch_bounds__(256) void stage_rows_kernel(const uint4* q_src, const uint4* k_src, const uint4* v_src,
+                                                         uint4* q_dst, uint8_t* k_cache, uint8_t* v_cache, int nq,
+                                                         int nkv, int n_max, int row) {
+  pdl_wait();  // the previous step reads q and the caches
+  pdl_trigger();
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nq) {
+    if (q_src) q_dst[i] = q_src[i];
+    return;
+  }
+  i -= nq;
+  const bool val = i >= nkv;
+  if (val) i -= nkv;
+  if (i >= nkv) return;
+  const uint4* src = val ? v_src : k_src;
+  if (!src) return;
+  const int pair = i >> 4, c = i & 15;  // 16 pieces of 16 B per 256-B row
+  uint8_t* dst = (val ? v_cache : k_cache) + ((size_t)pair * n_max + row) * 256 + c * 16;
+  *reinterpret_cast<uint4*>(dst) = src[i];
+}
+}  // namespace a2ats
+
+extern "C" int a2ats_stage_rows(const a2ats_shape* shape, int32_t n_ctx, const void* q_src, const void* k_src,
+                                const void* v_src, void* q_dst, void* k_cache, void* v_cache, void* stream) {
+  int rc = check_shape(shape);
+  if (rc) return rc;
+  if (n_ctx <= 0 || n_ctx > shape->n_max) return A2ATS_EINVAL;
+  if ((q_src && (!q_dst || !aligned16(q_src) || !aligned16(q_dst))) ||
+      (k_src && (!k_cache || !aligned16(k_src) || !aligned16(k_cache))) ||
+      (v_src && (!v_cache || !aligned16(v_src) || !aligned16(v_cache))))
+    return A2ATS_EINVAL;
+  const int nq = shape->B * shape->Hq * (kD / 8), nkv = shape->B * shape->Hkv * (kD / 8);
+  const int n = nq + 2 * nkv;
+  return cuda_status(launch_pdl(a2ats::stage_rows_kernel, dim3((n + 255) / 256), dim3(256), 0,
+                                static_cast<cudaStream_t>(stream), static_cast<const uint4*>(q_src),
+                                static_cast<const uint4*>(k_src), static_cast<const uint4*>(v_src),
+                                static_cast<uint4*>(q_dst), static_cast<uint8_t*>(k_cache),
+                                static_cast<uint8_t*>(v_cache), nq, nkv, shape->n_max, n_ctx - 1));
+}
+
 // ------------------------------------------------------------------ sequence-sharded step
 namespace {
 int shard_common(const a2ats_shape* shape, const a2ats_params* params, int n_ctx, int shard_begin, int shard_len,

@@ -538,3 +538,35 @@ def test_select_many_pairs_long_context(family, code_dist, N, L):
                 assert np.all(np.diff(s) > 0) and np.all(np.isin(s, cand))
                 np.testing.assert_allclose(np.sort(agg[s]), np.sort(agg[ref]), rtol=0, atol=2e-3)
     assert checked >= B * Hkv * 8 // 10
+
+
+def test_stage_rows_and_host_output_equal_device_path():
+    """a2ats_stage_rows (q and the new K/V rows from pinned host memory, one kernel) + a
+    decode step whose output is mapped pinned host memory == the all-device path, bitwise."""
+    cfg = Config("stage", B=4, Hq=16, Hkv=4, d=128, N=5000, L=512, K=300)
+    inp = make_inputs(cfg, 77, device="cuda", with_h=True)
+    n = cfg.N
+    params = A.Params(topk=cfg.K)
+    outs = []
+    for staged in (False, True):
+        kc, vc = inp["k_cache"].clone(), inp["v_cache"].clone()
+        dec = A.Decoder(cfg.B, cfg.Hq, cfg.Hkv, cfg.L, inp["n_max"], inp["codebook"], inp["H"], params)
+        dec.encode(kc, 0, n - 1)
+        if staged:
+            q_host = inp["q"].cpu().pin_memory()
+            k_host = kc[:, :, n - 1].contiguous().cpu().pin_memory()
+            v_host = vc[:, :, n - 1].contiguous().cpu().pin_memory()
+            kc[:, :, n - 1] = 0
+            vc[:, :, n - 1] = 0
+            q_dev = torch.zeros_like(inp["q"])
+            A.a2ats_stage_rows(dec.shape, n, q_host, k_host, v_host, q_dev, kc, vc)
+            out = torch.full((cfg.B, cfg.Hq, 128), float("nan")).pin_memory()
+            dec.step_append(q_dev, kc, vc, n, out=out)
+            torch.cuda.synchronize()
+            assert torch.equal(kc[:, :, n - 1].cpu(), k_host) and torch.equal(q_dev.cpu(), q_host)
+            outs.append(out.clone())
+        else:
+            out = dec.step_append(inp["q"], kc, vc, n)
+            torch.cuda.synchronize()
+            outs.append(out.cpu())
+    assert torch.equal(outs[0], outs[1])
