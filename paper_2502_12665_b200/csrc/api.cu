@@ -500,8 +500,8 @@ int decode_impl(const a2ats_shape* shape, const a2ats_params* params, int32_t n_
   const bool split_select = long_select && !pipe_select;
   prep_set_window(p, shape, k_cache, wlog, n_ctx, d.w0, d.n_w, 0);
   const int n_wl = p.n_wl;
-  // split select: its threshold kernel computes the window logits before its wait
-  if (split_select || !attend) p.n_win = 0;
+  // long contexts: the threshold kernel computes the window logits before its wait
+  if (long_select || !attend) p.n_win = 0;
   CUtensorMap tmA, tmC;
   rc = cuda_status(make_tmap_sw128(&tmA, codebook, (uint64_t)shape->Hkv * shape->L, kD, 128));
   if (rc) return rc;
@@ -558,7 +558,7 @@ int decode_impl(const a2ats_shape* shape, const a2ats_params* params, int32_t n_
     sa.B = shape->B;
     sa.wlog = nullptr;
     sa.P = d.P;
-    if (split_select && attend) {
+    if (long_select && attend) {  // the threshold kernel computes the window logits before its wait
       sa.wlog = wlog;
       sa.q = static_cast<const uint16_t*>(q);
       sa.kc = static_cast<const uint16_t*>(k_cache);

@@ -112,8 +112,7 @@ __device__ __forceinline__ void encode_tiles(const CUtensorMap& tmC, const EncAr
   umma::fence_before();
   __syncthreads();
   umma::fence_after();
-  pdl_wait();  // slots / codes / hist are written below
-  pdl_trigger();
+  pdl_trigger();  // the dependent kernel may launch; this CTA waits only before its global writes
   const uint32_t tmem = tslot;
   const uint32_t idesc = umma::idesc_bf16(kCW, NV);
 #pragma unroll 1
@@ -161,6 +160,7 @@ __device__ __forceinline__ void encode_tiles(const CUtensorMap& tmC, const EncAr
     umma::fence_after();
   }
   if (warp == 0) umma::tmem_dealloc_n(tmem, ncols);
+  pdl_wait();  // slots / codes / hist are written below (the MMA work above only read step inputs)
   // tid <-> key column (nvec <= 256: two passes at most)
   for (int base = 0; base < a.nvec; base += 128) {
     const int v = base + tid;

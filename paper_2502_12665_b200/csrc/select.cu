@@ -845,7 +845,8 @@ __device__ __forceinline__ void emit16(uint32_t q, int t0, uint32_t& gb, uint32_
 // ---------------------------------------------------------------- long contexts with hist
 // Two kernels after the LUT (prep) kernel:
 //  select_thresh_kernel (grid P, 256 threads, four resident per SM: one wave at C4): per
-//    pair, counts (hist - sink/window codes) before the dependency wait, then keys, v*, m,
+//    pair, the window rows' logits (for the attention) and the counts (hist - sink/window
+//    codes) before the dependency wait, then keys, v*, m,
 //    E = #{candidates at level v*}, and the compact 2-bit class table -> tblg, (v*, m, K_eff,
 //    E) -> pinfo; appends the step's new token to hist.
 //  select_scan_kernel: a persistent grid (one 1024-thread CTA per SM) over 2P work units:
@@ -1146,12 +1147,18 @@ __global__ __launch_bounds__(kTT, 4) void select_thresh_kernel(SelArgs a) {
   uint32_t* skey = sm + L4;
   int* scnt = reinterpret_cast<int*>(skey + kTSurv);
   const uint16_t* cp = a.codes + (size_t)pair * a.n_max;
+  float wacc[512 / kTT];
+  if (a.wlog) {  // the pair's window-row logits (step inputs only; scratch aliases cnt / survivors)
+    window_logits<kTT>(a, pair, reinterpret_cast<uint8_t*>(sm), wacc);
+    __syncthreads();
+  }
   load_cnt<kTT>(a, pair, cnt, cp);  // step inputs
   int c[16];
   load_c_regs<16>(a, cnt, c);
   pdl_wait();                       // agg comes from the prep kernel
   pdl_trigger();
   A2ATS_TL(g_sel_tl, 3);
+  if (a.wlog) store_window_logits<kTT>(a, pair, wacc);  // the previous step's attention has read wlog
   append_hist(a, pair, cp);         // counts taken: the new token joins hist
   if (tid == 0) S.s_eq = 0;
   uint32_t k[16], kstar, m;
@@ -1584,7 +1591,8 @@ bool select_pipe_ok(int L) { return L <= 4096; }
 
 cudaError_t launch_select_pipe(const SelArgs& a, const CUtensorMap& tmK, int nblk, cudaStream_t st) {
   if (!select_pipe_ok(a.L)) return cudaErrorInvalidValue;
-  const int smt = (int)thresh_smem_bytes(a.L), sms = (int)scan_smem_bytes(a.W);
+  const int smt = (int)std::max(thresh_smem_bytes(a.L), a.wlog ? (size_t)kWinScratch : (size_t)0);
+  const int sms = (int)scan_smem_bytes(a.W);
   static int set_t = -1, set_s = -1;
   if (set_t < smt) {
     cudaError_t e = cudaFuncSetAttribute(select_thresh_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smt);
