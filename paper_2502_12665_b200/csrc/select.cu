@@ -1334,35 +1334,44 @@ __global__ __launch_bounds__(kPAll, 1) void select_scan_kernel(const __grid_cons
   pdl_wait();  // tblg / pinfo come from the threshold kernel (sel: read by the previous step's attention,
   pdl_trigger();  // complete before the prep kernel triggered)
   A2ATS_TL(g_selc_tl, 2);
-  // table of unit k: thread t < 4 W replicates word t >> 2 (two 16-B stores); loads issued early
+  // table of unit k: its compact words and (v*, m, K_eff, E) are staged into shared memory by
+  // cp.async one unit ahead (no registers held, no stall at use); thread t < 4 W then
+  // replicates word t >> 2 (two 16-B stores)
+  __shared__ __align__(16) uint32_t sStage[2][256 + 4];
   const int tw = tid >> 2, tq = (tid & 3) * 2;
   auto pair_of = [&](int k) {
     const int u = blockIdx.x + k * nblk;
     return u < P ? u : u - P;
   };
-  // loads of unit k's table word and (m, K_eff, E): issued one unit ahead, consumed (E - m)
-  // only when that unit starts, so the L2 latency is never waited for
-  auto load_unit = [&](int k, uint32_t& x, PipeUnit& pu) {
+  auto load_unit = [&](int k) {
     if (k >= nunit) return;
     const int pair = pair_of(k);
-    x = tw < W ? __ldcg(a.tblg + (size_t)pair * W + tw) : 0u;
-    pu.m = __ldcg(a.pinfo + pair * 4 + 1);
-    pu.cap = __ldcg(a.pinfo + pair * 4 + 2);
-    pu.D = __ldcg(a.pinfo + pair * 4 + 3);  // E for now
+    uint32_t* st = sStage[k & 1];
+    if (tid < W) {
+      const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(st + tid));
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(a.tblg + (size_t)pair * W + tid) : "memory");
+    }
+    if (tid == kPAll - 1) cp_async16(st + 256, a.pinfo + pair * 4);
+    cp_async_commit();
   };
-  auto store_table = [&](int buf, uint32_t x) {
+  auto unit_info = [&](int k) {  // after the staging of unit k is visible
+    const uint32_t* st = sStage[k & 1];
+    return PipeUnit{st[257], st[259] - st[257], st[258], 0u};  // m, D = E - m, cap = K_eff
+  };
+  auto store_table = [&](int k) {
     if (tw < W) {
-      uint4* dst = reinterpret_cast<uint4*>(tbl0 + buf * 8192 + tw * 32);
+      const uint32_t x = sStage[k & 1][tw];
+      uint4* dst = reinterpret_cast<uint4*>(tbl0 + (k & 1) * 8192 + tw * 32);
       const uint4 v = make_uint4(x, x, x, x);
       dst[(tq + tw) & 7] = v;
       dst[(tq + 1 + tw) & 7] = v;
     }
   };
-  uint32_t x_cur = 0, x_nxt = 0;
-  PipeUnit pu_cur{}, pu_nxt{};
-  load_unit(0, x_cur, pu_cur);
-  store_table(0, x_cur);
-  pu_cur.D -= pu_cur.m;
+  load_unit(0);
+  cp_async_wait<0>();
+  __syncthreads();
+  store_table(0);
+  PipeUnit pu_cur = unit_info(0);
   __syncthreads();
   if (tid == 0) A2ATS_TLX(g_selc_tl, 4);
   int j = 0;
@@ -1371,15 +1380,18 @@ __global__ __launch_bounds__(kPAll, 1) void select_scan_kernel(const __grid_cons
   for (int k = 0; k < nunit; ++k) {
     const int u = blockIdx.x + k * nblk;
     const bool fwd = u < P;
-    load_unit(k + 1, x_nxt, pu_nxt);
+    load_unit(k + 1);
     auto expand = [&]() {
-      if (k + 1 < nunit) store_table((k + 1) & 1, x_nxt);
+      if (k + 1 < nunit) {
+        cp_async_wait<0>();
+        __syncthreads();  // every thread's staged words
+        store_table(k + 1);
+      }
     };
     if (fwd) scan_unit<true>(c, k & 1, pair_of(k), g.R0, pu_cur, j, issue, expand);
     else scan_unit<false>(c, k & 1, pair_of(k), R1, pu_cur, j, issue, expand);
     __syncthreads();  // the next unit's table is visible
-    pu_cur = pu_nxt;
-    pu_cur.D -= pu_cur.m;
+    if (k + 1 < nunit) pu_cur = unit_info(k + 1);
     if (tid == 0 && k == 0) A2ATS_TLX(g_selc_tl, 3);
   }
   A2ATS_TL(g_selc_tl, 1);
