@@ -175,7 +175,12 @@ int a2ats_build_codes(const a2ats_shape* shape, const void* keys, int32_t t_begi
  *              [0, N) exactly (as maintained by a2ats_build_codes).  With it
  *              the code stream is read once; NULL => histogram computed
  *              in-step with an extra pass.  Results are bitwise identical.
- *   out      : [B, Hq, d] fp32 attention output
+ *              Long contexts (> 32768 candidates) with hist, L <= 4096 and
+ *              n_max % 64 == 0 take the threshold + persistent half-pair scan
+ *              (code rows loaded by TMA as 128-B rows); other shapes the
+ *              threshold + chunked scan.  Same results either way.
+ *   out      : [B, Hq, d] fp32 attention output (device or mapped pinned
+ *              host memory)
  *   sel_out  : optional [B, Hkv, K_eff] int32, the top-K token indices in
  *              ascending order, K_eff = min(topk, |Cand|)
  *   scores_out : optional [B, Hq, n_ctx] fp32 debug output of the
