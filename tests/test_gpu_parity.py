@@ -570,3 +570,21 @@ def test_stage_rows_and_host_output_equal_device_path():
             torch.cuda.synchronize()
             outs.append(out.cpu())
     assert torch.equal(outs[0], outs[1])
+
+
+def test_stage_rows_device_sources_and_errors():
+    """a2ats_stage_rows with device sources, partial (NULL) sources, and its argument checks."""
+    cfg = Config("stage2", B=2, Hq=4, Hkv=2, d=128, N=100, L=64, K=5)
+    shape = A.make_shape(cfg.B, cfg.Hq, cfg.Hkv, 128, cfg.L, 128)
+    kc = torch.zeros((2, 2, 128, 128), dtype=torch.bfloat16, device="cuda")
+    vc = torch.zeros_like(kc)
+    q_src = torch.randn((2, 4, 128), device="cuda").to(torch.bfloat16)
+    k_src = torch.randn((2, 2, 128), device="cuda").to(torch.bfloat16)
+    q_dst = torch.zeros_like(q_src)
+    A.a2ats_stage_rows(shape, 77, q_src, k_src, None, q_dst, kc, vc)
+    torch.cuda.synchronize()
+    assert torch.equal(q_dst, q_src) and torch.equal(kc[:, :, 76], k_src)
+    assert int(vc.abs().sum()) == 0 and int(kc[:, :, :76].abs().sum()) == 0
+    for bad_n in (0, 129):
+        with pytest.raises(A.A2ATSError):
+            A.a2ats_stage_rows(shape, bad_n, q_src, k_src, None, q_dst, kc, vc)
