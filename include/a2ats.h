@@ -70,10 +70,10 @@ extern "C" {
 /* lut_engine: which pipes compute the score table LUT = q~ C^T (a2, Eq. 21).  The
  * contraction is M = L, N = B*G, K = d per KV head: a dense GEMM for large B*G*L (tensor
  * cores, bf16 hi+lo split of q~), a few thousand FMAs per CTA otherwise. */
-#define A2ATS_LUT_AUTO 0    /* FMA when B*G*L <= A2ATS_LUT_FMA_MAX (0: never), tensor cores above */
+#define A2ATS_LUT_AUTO 0    /* FMA when B*G <= A2ATS_LUT_FMA_MAX_VECTORS, tensor cores above */
 #define A2ATS_LUT_TENSOR 1  /* tcgen05 (TMEM accumulators)                             */
 #define A2ATS_LUT_FMA 2     /* FP32 FMA, one thread per codeword                        */
-#define A2ATS_LUT_FMA_MAX 0  /* measured: no crossover (reading Q26) */
+#define A2ATS_LUT_FMA_MAX_VECTORS 8  /* measured crossover (reading Q26, profiles/lut_sweep_r1.json) */
 
 typedef struct a2ats_shape {
   int32_t B;      /* batch size (sequences)                                   */

@@ -482,9 +482,8 @@ int decode_impl(const a2ats_shape* shape, const a2ats_params* params, int32_t n_
   // reads its code, and its histogram entry is added by the select kernel after its counts
   LutArgs la = make_lut_args(shape, params, d, q, codebook, agg, lut_full, cs);
   // LUT engine (a2): FP32 FMA for small B*G*L, tensor cores otherwise (reading of SURVEY 8d C5)
-  const long long bgl = (long long)shape->B * d.G * shape->L;
   const bool lut_fma = params->lut_engine == A2ATS_LUT_FMA ||
-                       (params->lut_engine == A2ATS_LUT_AUTO && bgl <= A2ATS_LUT_FMA_MAX);
+                       (params->lut_engine == A2ATS_LUT_AUTO && shape->B * d.G <= A2ATS_LUT_FMA_MAX_VECTORS);
   // wide query tiles: q~ hi|lo computed once by qprep_kernel instead of in every LUT CTA
   if (la.NV > 64 && !lut_fma) la.qt = reinterpret_cast<uint16_t*>(base + Lw.qt);
   PrepArgs p = prep_empty();

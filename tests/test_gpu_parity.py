@@ -76,7 +76,7 @@ def check_against_oracle(cfg, inp, gpu, n_ctx=None, bridge=None, pairs=None, exa
 
 
 # ------------------------------------------------------------------ C1 and small multi-tile shapes
-# LUT engines (a2): AUTO (tensor cores, reading Q26), forced tensor cores, forced FMA
+# LUT engines (a2): AUTO (FMA for B*G <= 8, reading Q26), forced tensor cores, forced FMA
 ENGINES = [0, 1, 2]
 
 
