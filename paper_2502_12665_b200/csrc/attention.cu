@@ -531,8 +531,11 @@ cudaError_t launch_attention_nw(const AttnArgs& a, int P, cudaStream_t st) {
 
 // 4-warp CTAs (two per SM) when the grid has at least two (pair, split) items per SM
 // (measured at C4: 362 -> 350 us), 8-warp CTAs otherwise (C2: one CTA per pair is faster)
+#ifndef A2ATS_ATTN_NW4
+#define A2ATS_ATTN_NW4 0  // tuning builds only: 1 forces 4-warp CTAs
+#endif
 cudaError_t launch_attention(const AttnArgs& a, int P, int /*GT*/, cudaStream_t st) {
-  if ((long long)P * a.nsplit >= 2LL * sm_count()) return launch_attention_nw<4>(a, P, st);
+  if (A2ATS_ATTN_NW4 || (long long)P * a.nsplit >= 2LL * sm_count()) return launch_attention_nw<4>(a, P, st);
   return launch_attention_nw<8>(a, P, st);
 }
 
