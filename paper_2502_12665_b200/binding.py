@@ -130,6 +130,8 @@ class Params:
         p.window, p.bridge, p.n_sink, p.topk = self.window, self.bridge, self.n_sink, self.topk
         p.rope_theta = self.rope_theta
         if self.inv_freq is not None:
+            if len(self.inv_freq) != 64:  # the library reads d/2 = 64 doubles
+                raise ValueError(f"inv_freq must hold d/2 = 64 frequencies, got {len(self.inv_freq)}")
             self._freq_buf = (ctypes.c_double * len(self.inv_freq))(*self.inv_freq)
             p.inv_freq = ctypes.cast(self._freq_buf, ctypes.POINTER(ctypes.c_double))
         p.group_reduce, p.kv_location, p.lut_engine = self.group_reduce, self.kv_location, self.lut_engine
@@ -198,7 +200,7 @@ def a2ats_decode_step(shape: a2ats_shape, params, n_ctx: int, q, k_cache, v_cach
         ctypes.byref(shape), ctypes.byref(p), int(n_ctx), _ptr(q, "q", torch.bfloat16),
         _ptr(k_cache, "k_cache", torch.bfloat16, host_ok=kv_host), _ptr(v_cache, "v_cache", torch.bfloat16, host_ok=kv_host),
         _ptr(codes, "codes", torch.uint16), _ptr(codebook, "codebook", torch.bfloat16),
-        _ptr(hist, "hist", torch.int32, optional=True), _ptr(out, "out", torch.float32),
+        _ptr(hist, "hist", torch.int32, optional=True), _ptr(out, "out", torch.float32, host_ok="pinned"),
         _ptr(sel_out, "sel_out", torch.int32, optional=True), _ptr(scores_out, "scores_out", torch.float32, optional=True),
         _ptr(ws, "ws"), ws.numel() * ws.element_size(), _stream(stream))
     _check("a2ats_decode_step", rc)
@@ -245,7 +247,7 @@ def a2ats_select_topk(shape: a2ats_shape, params, n_ctx: int, q, codes, codebook
 
 
 def a2ats_set_stage_events(events):
-    """events: list of >= 6 torch.cuda.Event(enable_timing=True) (already recorded
+    """events: list of >= 5 torch.cuda.Event(enable_timing=True) (already recorded
     once so the handle exists), or None to disable."""
     lib = load()
     if events is None:

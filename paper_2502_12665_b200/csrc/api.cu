@@ -4,7 +4,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <utility>
 
 #include "internal.cuh"
 
@@ -20,6 +22,20 @@ int sm_count() {
     cached[dev] = n > 0 ? n : 148;
   }
   return cached[dev];
+}
+
+cudaError_t ensure_smem_attr(const void* kernel, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> done;  // (kernel, device) -> bytes opted in
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  int& have = done[{kernel, dev}];
+  if (have >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) have = bytes;
+  return e;
 }
 
 namespace {
@@ -108,20 +124,23 @@ DecodeWs decode_layout(const a2ats_shape* s, const a2ats_params* p) {
   const int GT = G >= 4 ? 4 : G;
   DecodeWs w;
   size_t o = 0;
+  // regions that must be zero on entry (each kernel leaves them zero on exit) come first, at
+  // offsets that depend on the shape only: params (topk, window) may change between calls on
+  // the same workspace without moving them onto bytes other regions left non-zero
+  w.actr = o; o = align_up(o + (size_t)P * (G / GT) * 4);                                    // attention split counters
+  w.eslot = o; o = align_up(o + (size_t)s->Hkv * std::max(s->B, 1) * 8);                    // append encode slots
+  w.ectr = o; o = align_up(o + (size_t)s->Hkv * 2 * 4);
+  w.desc = o; o = align_up(o + (size_t)P * (s->n_max / select_chunk_tokens() + 2) * 8);     // look-back descriptors
   w.cs = o; o = align_up(o + (size_t)p->window * kHalf * 8);
   w.agg = o; o = align_up(o + (size_t)P * s->L * 4);
   w.lut = o; o = align_up(o + (size_t)s->B * s->Hq * s->L * 4);
   w.sel = o; o = align_up(o + (size_t)P * std::max<long long>(kmax, 1) * 4);
   w.part = o; o = align_up(o + (size_t)P * (G / GT) * GT * nsplit_max * 130 * 4);
-  w.actr = o; o = align_up(o + (size_t)P * (G / GT) * 4);
   w.cand_keep = o; o = align_up(o + (size_t)P * s->L * 4);   // sharded step only
   w.pinfo = o; o = align_up(o + (size_t)P * 16);
   w.nsel = o; o = align_up(o + (size_t)P * 4);
   w.wlog = o; o = align_up(o + (size_t)P * kWinPre * 8 * 4);
-  w.eslot = o; o = align_up(o + (size_t)s->Hkv * std::max(s->B, 1) * 8);   // decode_step_append's encode
-  w.ectr = o; o = align_up(o + (size_t)s->Hkv * 2 * 4);
   w.tblg = o; o = align_up(o + (size_t)P * ((s->L + 15) / 16) * 4);                       // long-context select
-  w.desc = o; o = align_up(o + (size_t)P * (s->n_max / select_chunk_tokens() + 2) * 8);
   {
     const int NV = lut_tile_nv(s->B * G), nvt = (s->B * G + NV - 1) / NV;
     w.qt = o; o = align_up(o + qprep_bytes(s->Hkv, nvt, NV));                                // q~ B tiles
@@ -674,7 +693,8 @@ __global__ __launch_bounds__(256) void stage_rows_kernel(const uint4* q_src, con
                                                          uint4* q_dst, uint8_t* k_cache, uint8_t* v_cache, int nq,
                                                          int nkv, int n_max, int row) {
   pdl_wait();  // the previous step reads q and the caches
-  pdl_trigger();
+  // no early pdl_trigger(): the next kernel's pre-wait prologue reads q and the new K/V rows
+  // written here, so dependents launch only at this grid's completion (implicit trigger)
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < nq) {
     if (q_src) q_dst[i] = q_src[i];

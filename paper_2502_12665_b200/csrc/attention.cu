@@ -519,12 +519,8 @@ __global__ void combine_kernel(const float* __restrict__ parts, int R, int rows,
 template <int NW>
 cudaError_t launch_attention_nw(const AttnArgs& a, int P, cudaStream_t st) {
   const SmemLayout L = attn_smem<NW>(a.R);
-  static int smem_set = -1;
-  if (smem_set < L.total) {
-    cudaError_t e = cudaFuncSetAttribute(attn_mma_kernel<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);
-    if (e != cudaSuccess) return e;
-    smem_set = L.total;
-  }
+  cudaError_t e = ensure_smem(attn_mma_kernel<NW>, L.total);
+  if (e != cudaSuccess) return e;
   dim3 grid(a.nsplit, P, 1);
   return launch_pdl(attn_mma_kernel<NW>, grid, dim3(NW * 32), L.total, st, a);
 }

@@ -179,12 +179,8 @@ cudaError_t launch_prepare(const uint16_t* codebook, const float* H, float* nrm,
 // Prefill encoder (more than encode_cw_max() keys per head); fewer keys go through the
 // decode-time encode role of the step kernel (prep.cu).
 cudaError_t launch_encode_bulk(const EncArgs& a, const CUtensorMap& tm, cudaStream_t st) {
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(encode_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkSmem);
-    if (e != cudaSuccess) return e;
-    attr_done = true;
-  }
+  cudaError_t e = ensure_smem(encode_bulk_kernel, kBulkSmem);
+  if (e != cudaSuccess) return e;
   const int ntile = (a.L + kCW - 1) / kCW;
   dim3 grid((a.nvec + kTV - 1) / kTV, a.Hkv, (ntile + a.tiles_per_split - 1) / a.tiles_per_split);
   return launch_pdl(encode_bulk_kernel, grid, dim3(128), kBulkSmem, st, tm, a);

@@ -112,7 +112,6 @@ __device__ __forceinline__ void encode_tiles(const CUtensorMap& tmC, const EncAr
   umma::fence_before();
   __syncthreads();
   umma::fence_after();
-  pdl_trigger();  // the dependent kernel may launch; this CTA waits only before its global writes
   const uint32_t tmem = tslot;
   const uint32_t idesc = umma::idesc_bf16(kCW, NV);
 #pragma unroll 1
@@ -161,6 +160,7 @@ __device__ __forceinline__ void encode_tiles(const CUtensorMap& tmC, const EncAr
   }
   if (warp == 0) umma::tmem_dealloc_n(tmem, ncols);
   pdl_wait();  // slots / codes / hist are written below (the MMA work above only read step inputs)
+  pdl_trigger();  // after the wait, like every kernel of the path (internal.cuh invariant)
   // tid <-> key column (nvec <= 256: two passes at most)
   for (int base = 0; base < a.nvec; base += 128) {
     const int v = base + tid;

@@ -81,6 +81,14 @@ constexpr int kTlMax = 8192;
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// Opt a kernel into `bytes` of dynamic shared memory on the CURRENT device (cached per
+// (kernel, device) under a mutex; a second device in the same process gets its own opt-in).
+cudaError_t ensure_smem_attr(const void* kernel, int bytes);
+template <typename... KArgs>
+inline cudaError_t ensure_smem(void (*kern)(KArgs...), int bytes) {
+  return ensure_smem_attr(reinterpret_cast<const void*>(kern), bytes);
+}
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                               Args... args) {

@@ -485,12 +485,8 @@ __global__ void scores_kernel(const float* __restrict__ lut_full, const uint16_t
 template <int G>
 cudaError_t launch_prep_g(const PrepArgs& p, const CUtensorMap& tmA, const CUtensorMap& tmC, cudaStream_t st) {
   const int smem = prep_smem_bytes(p);
-  static int smem_set = -1;
-  if (smem_set < smem) {
-    cudaError_t e = cudaFuncSetAttribute(prep_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    smem_set = smem;
-  }
+  cudaError_t e = ensure_smem(prep_kernel<G>, smem);
+  if (e != cudaSuccess) return e;
   const int n = p.n_lut + p.n_enc + p.n_win;
   if (n == 0) return cudaSuccess;
   return launch_pdl(prep_kernel<G>, dim3(n), dim3(128), smem, st, tmA, tmC, p);

@@ -1575,12 +1575,8 @@ cudaError_t launch_mode(const SelArgs& a, int P, cudaStream_t st) {  // P: CTAs
   const int tbl_words = (max(((a.L + 3) & ~3) + a.L, a.W * 32) + 3) / 4 * 4;
   const int smem = tbl_words * 4 + (ModeTraits<MODE>::surv ? 2 * kSurvCap * 4 : 0) +
                    (ModeTraits<MODE>::codes ? kCH * 2 : 0) + ModeTraits<MODE>::extra;
-  static int smem_set = -1;
-  if (smem_set < smem) {
-    cudaError_t e = cudaFuncSetAttribute(select_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    smem_set = smem;
-  }
+  cudaError_t e = ensure_smem(select_kernel<MODE>, smem);
+  if (e != cudaSuccess) return e;
   return launch_pdl(select_kernel<MODE>, dim3(P), dim3(kNT), smem, st, a);
 }
 }  // namespace
@@ -1605,18 +1601,11 @@ cudaError_t launch_select_pipe(const SelArgs& a, const CUtensorMap& tmK, int nbl
   if (!select_pipe_ok(a.L)) return cudaErrorInvalidValue;
   const int smt = (int)std::max(thresh_smem_bytes(a.L), a.wlog ? (size_t)kWinScratch : (size_t)0);
   const int sms = (int)scan_smem_bytes(a.W);
-  static int set_t = -1, set_s = -1;
-  if (set_t < smt) {
-    cudaError_t e = cudaFuncSetAttribute(select_thresh_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smt);
-    if (e != cudaSuccess) return e;
-    set_t = smt;
-  }
-  if (set_s < sms) {
-    cudaError_t e = cudaFuncSetAttribute(select_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sms);
-    if (e != cudaSuccess) return e;
-    set_s = sms;
-  }
-  cudaError_t e = launch_pdl(select_thresh_kernel, dim3(a.P), dim3(kTT), smt, st, a);
+  cudaError_t e = ensure_smem(select_thresh_kernel, smt);
+  if (e != cudaSuccess) return e;
+  e = ensure_smem(select_scan_kernel, sms);
+  if (e != cudaSuccess) return e;
+  e = launch_pdl(select_thresh_kernel, dim3(a.P), dim3(kTT), smt, st, a);
   if (e != cudaSuccess) return e;
   return launch_pdl(select_scan_kernel, dim3(nblk), dim3(kPAll), sms, st, tmK, a);
 }

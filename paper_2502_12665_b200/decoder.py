@@ -33,6 +33,8 @@ class Decoder:
         need = _b.a2ats_decode_workspace_bytes(self.shape, self.params)
         if need > self.ws_dec.numel():
             self.ws_dec = torch.zeros(need, dtype=torch.uint8, device=self.device)
+        # (the zero-on-entry counters sit at shape-only offsets at the front of the workspace,
+        # so a smaller topk on the same workspace finds them where the kernels left them)
 
     def encode(self, keys, t_begin: int, t_end: int, update_hist: bool = True, codes=None):
         _b.a2ats_build_codes(self.shape, keys, t_begin, t_end, self.chat, self.nrm,
