@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define A2ATS_ABI_VERSION 6
+#define A2ATS_ABI_VERSION 7
 
 /* ---- status codes ---------------------------------------------------- */
 #define A2ATS_OK 0
@@ -246,43 +246,80 @@ int a2ats_decode_step_append(const a2ats_shape* shape, const a2ats_params* param
                              void* ws, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------
- * Sequence-sharded decode step (the paper is single-GPU,
- * P:732-733).  Rank r of R holds, for every (b, KV head), the contiguous
- * global token range [shard_begin, shard_begin + shard_len) of the context in
- * its own arrays of capacity shape->n_max (local row = global - shard_begin):
- * codes [B,Hkv,n_max] uint16, k_cache / v_cache [B,Hkv,n_max,d] bf16 and the
- * optional running histogram hist [B,Hkv,L] of the local tokens' codes.  q and
- * the codebook are replicated.  n_ctx is the GLOBAL context length.  One step:
+ * Sequence-sharded decode step (the paper itself
+ * is single-GPU).  R <= 8 ranks, one process per GPU.  Rank r holds,
+ * for every (b, KV head), the global tokens [bounds[r], bounds[r+1]) of the
+ * context in its own arrays of capacity shape->n_max (local row = global -
+ * bounds[r]; n_max % 64 == 0): codes [B,Hkv,n_max] uint16 and k_cache /
+ * v_cache [B,Hkv,n_max,d] bf16.  q, the codebook (and its prepared terms chat,
+ * nrm of a2ats_qavq_prepare) and the shard STATE are replicated.  bounds is a
+ * HOST array [R+1], bounds[0] = 0, non-decreasing, the same on every rank.
  *
- *   a2ats_shard_hist       LUT (a1+a2; bitwise identical on every rank) and the
- *                          rank's candidate histogram -> cand_hist [B,Hkv,L] i32
- *   [caller]               all-reduce(SUM) cand_hist over ranks (in place)
- *   a2ats_shard_threshold  the K-th level v* and tie quota m of the GLOBAL
- *                          top-K (identical on every rank) and this rank's
- *                          (#candidates above v*, #at v*) -> counts [B,Hkv,2] i32
- *   [caller]               all-gather counts -> counts_all [R,B,Hkv,2]
- *   a2ats_shard_attend     local top-K emission (ties to the lowest global index,
- *                          Q12: rank r keeps the first m - sum_{r'<r} eq_{r'}
- *                          tied tokens it holds) and exact attention over the
- *                          rank's rows of Sel -> partial [B,Hq,130] f32 =
- *                          (max logit m, sum l, unnormalised o[128]) in the
- *                          base-2 logit domain; optional sel_out [B,Hkv,K]
- *   [caller]               all-gather partials -> [R,B,Hq,130]
- *   a2ats_combine          log-sum-exp combine in rank order -> out [B,Hq,d]
- * The union of the ranks' selections equals the single-GPU top-K exactly.
- * All calls share one zero-initialised workspace (a2ats_shard_workspace_bytes).
+ * State (a2ats_shard_state_bytes, caller-owned device memory, built by
+ * a2ats_shard_state_build, then updated by every step identically on every
+ * rank): the code histogram of all tokens [0, n) and every rank's histogram of
+ * its tokens (int32 [B*Hkv, L] and [R, B*Hkv, L]), the codes of the first
+ * n_sink tokens and of the latest WR tokens (WR = the power of two >= window).
+ * From it every rank derives, with NO exchange, the K-th level v* and tie
+ * quota m of the GLOBAL top-K (the LUT is bitwise identical on every rank)
+ * and its own share of the ties (the first m tied tokens in global order,
+ * reading Q12: lower ranks first) -- the collective-free exact global top-K
+ * of SURVEY §8f.1.  The union of the ranks' selections equals the
+ * single-GPU top-K exactly.
+ *
+ * a2ats_decode_step_sharded(n_ctx): token n_ctx-1 (its K/V row already in its
+ * owner's cache: the rank with bounds[r] <= n_ctx-1 < bounds[r+1]) is encoded
+ * on its owner (a0); every rank computes the LUT, its local selection and the
+ * exact attention over its rows of Sel (a1..a5) into a partial (m, l, o) in the
+ * base-2 logit domain; ONE ncclAllGather exchanges the partials and the new
+ * token's code (msg = a2ats_shard_msg_bytes per rank, ~1 MB at C4); then the
+ * log-sum-exp combine in rank order (a6) -> out [B,Hq,d] fp32 on EVERY rank,
+ * and the state update.  All on the caller's stream, no host synchronisation:
+ * one call per step, capturable in a CUDA graph.  sel_out (optional, [B,Hkv,
+ * topk]): this rank's selected GLOBAL token indices, ascending.  ws: a2ats_
+ * shard_workspace_bytes, zero-initialised once, reusable.  comm: from
+ * a2ats_comm_init (NCCL, loaded with dlopen: the process's libnccl.so.2 or
+ * A2ATS_NCCL_LIB); NULL only when R == 1.  Errors: A2ATS_EINVAL (bounds,
+ * rank, pointers), A2ATS_EUNSUPPORTED (n_max % 64, L > 4096, B > 256, host
+ * K/V), A2ATS_ENCCL.
  * ------------------------------------------------------------------- */
-size_t a2ats_shard_workspace_bytes(const a2ats_shape* shape, const a2ats_params* params);
-int a2ats_shard_hist(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx, int32_t shard_begin,
-                     int32_t shard_len, const void* q, const uint16_t* codes, const void* codebook,
-                     const int32_t* hist, int32_t* cand_hist, void* ws, size_t ws_bytes, void* stream);
-int a2ats_shard_threshold(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx,
-                          const int32_t* cand_hist_global, int32_t* counts, void* ws, size_t ws_bytes,
-                          void* stream);
-int a2ats_shard_attend(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx, int32_t shard_begin,
-                       int32_t shard_len, int32_t rank, int32_t nranks, const int32_t* counts_all, const void* q,
-                       const void* k_cache, const void* v_cache, const uint16_t* codes, float* partial,
-                       int32_t* sel_out, void* ws, size_t ws_bytes, void* stream);
+#define A2ATS_COMM_ID_BYTES 128
+typedef struct a2ats_comm_id { char internal[A2ATS_COMM_ID_BYTES]; } a2ats_comm_id;  /* = ncclUniqueId */
+typedef struct a2ats_comm a2ats_comm;
+int a2ats_comm_unique_id(void* id);   /* rank 0; the caller broadcasts the 128 bytes (torch.distributed) */
+int a2ats_comm_init(const void* id, int32_t world, int32_t rank, a2ats_comm** out);
+int a2ats_comm_destroy(a2ats_comm* comm);
+size_t a2ats_shard_state_bytes(const a2ats_shape* shape, const a2ats_params* params, int32_t world);
+/* byte offsets in the state: [0] hist_g int32 [B*Hkv, L], [1] hist_r int32 [R, B*Hkv, L],
+ * [2] ring uint16 [B*Hkv, WR], [3] sink codes uint16 [B*Hkv, n_sink_cap]; [4] WR, [5] n_sink_cap */
+int a2ats_shard_state_layout(const a2ats_shape* shape, const a2ats_params* params, int32_t world, size_t* offsets);
+size_t a2ats_shard_msg_bytes(const a2ats_shape* shape);
+size_t a2ats_shard_workspace_bytes(const a2ats_shape* shape, const a2ats_params* params, int32_t world);
+/* state of tokens [0, n_tokens) from every rank's codes (NCCL all-reduces; once, at prefill).
+ * comm == NULL with world > 1: only this rank's contribution is written (zeros elsewhere);
+ * the replicated state is then the element-wise sum of the ranks' contributions (int32
+ * histograms, uint16 codes) -- single-process rank simulation (tests).  ws: workspace of
+ * a2ats_shard_workspace_bytes. */
+int a2ats_shard_state_build(const a2ats_shape* shape, const a2ats_params* params, int32_t world, int32_t rank,
+                            const int32_t* bounds, int32_t n_tokens, const uint16_t* codes, void* state,
+                            void* ws, size_t ws_bytes, a2ats_comm* comm, void* stream);
+int a2ats_decode_step_sharded(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx,
+                              int32_t world, int32_t rank, const int32_t* bounds, const void* q,
+                              const void* k_cache, const void* v_cache, uint16_t* codes, const void* codebook,
+                              const void* chat, const float* nrm, void* state, float* out, int32_t* sel_out,
+                              void* ws, size_t ws_bytes, a2ats_comm* comm, void* stream);
+/* The two halves of a2ats_decode_step_sharded around its all-gather (tests
+ * simulate ranks in one process): partial writes this rank's message
+ * (msg: a2ats_shard_msg_bytes, device); finish reads all ranks' messages
+ * [R][msg] and writes out + updates the state. */
+int a2ats_shard_step_partial(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx, int32_t world,
+                             int32_t rank, const int32_t* bounds, const void* q, const void* k_cache,
+                             const void* v_cache, uint16_t* codes, const void* codebook, const void* chat,
+                             const float* nrm, const void* state, void* msg, int32_t* sel_out, void* ws,
+                             size_t ws_bytes, void* stream);
+int a2ats_shard_step_finish(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx, int32_t world,
+                            const int32_t* bounds, const void* msgs, void* state, float* out, void* stream);
+/* log-sum-exp combine of R partials [R,B,Hq,130] (base-2 domain) in rank order */
 int a2ats_combine(const a2ats_shape* shape, int32_t nparts, const float* partials, float* out, void* stream);
 
 /* ---------------------------------------------------------------------

@@ -74,7 +74,7 @@ _SIGS = {
 _lib = None
 
 
-ABI_VERSION = 6  # include/a2ats.h A2ATS_ABI_VERSION
+ABI_VERSION = 7  # include/a2ats.h A2ATS_ABI_VERSION
 
 
 def load(path: str = LIB_PATH, build_if_missing: bool = True) -> ctypes.CDLL:
@@ -257,66 +257,128 @@ def a2ats_set_stage_events(events):
     _check("a2ats_set_stage_events", lib.a2ats_set_stage_events(arr, len(events)))
 
 
-# ------------------------------------------------------------------ sequence-sharded step (SURVEY §8e)
+# ------------------------------------------------------------------ sequence-sharded step (SURVEY §8b/8e/8f.1)
+_SZ = ctypes.c_size_t
+_SP, _PP = ctypes.POINTER(a2ats_shape), ctypes.POINTER(a2ats_params)
+_I32P = ctypes.POINTER(ctypes.c_int32)
 _SIGS.update({
-    "a2ats_shard_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(a2ats_shape), ctypes.POINTER(a2ats_params)]),
-    "a2ats_shard_hist": (ctypes.c_int, [ctypes.POINTER(a2ats_shape), ctypes.POINTER(a2ats_params), ctypes.c_int32,
-                                        ctypes.c_int32, ctypes.c_int32, _VP, _VP, _VP, _VP, _VP, _VP, ctypes.c_size_t,
-                                        _VP]),
-    "a2ats_shard_threshold": (ctypes.c_int, [ctypes.POINTER(a2ats_shape), ctypes.POINTER(a2ats_params),
-                                             ctypes.c_int32, _VP, _VP, _VP, ctypes.c_size_t, _VP]),
-    "a2ats_shard_attend": (ctypes.c_int, [ctypes.POINTER(a2ats_shape), ctypes.POINTER(a2ats_params), ctypes.c_int32,
-                                          ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _VP, _VP,
-                                          _VP, _VP, _VP, _VP, _VP, _VP, ctypes.c_size_t, _VP]),
-    "a2ats_combine": (ctypes.c_int, [ctypes.POINTER(a2ats_shape), ctypes.c_int32, _VP, _VP, _VP]),
+    "a2ats_comm_unique_id": (ctypes.c_int, [_VP]),
+    "a2ats_comm_init": (ctypes.c_int, [_VP, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(_VP)]),
+    "a2ats_comm_destroy": (ctypes.c_int, [_VP]),
+    "a2ats_shard_state_bytes": (_SZ, [_SP, _PP, ctypes.c_int32]),
+    "a2ats_shard_msg_bytes": (_SZ, [_SP]),
+    "a2ats_shard_state_layout": (ctypes.c_int, [_SP, _PP, ctypes.c_int32, ctypes.POINTER(_SZ)]),
+    "a2ats_shard_workspace_bytes": (_SZ, [_SP, _PP, ctypes.c_int32]),
+    "a2ats_shard_state_build": (ctypes.c_int, [_SP, _PP, ctypes.c_int32, ctypes.c_int32, _I32P, ctypes.c_int32, _VP,
+                                               _VP, _VP, _SZ, _VP, _VP]),
+    "a2ats_decode_step_sharded": (ctypes.c_int, [_SP, _PP, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _I32P,
+                                                 _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _SZ, _VP,
+                                                 _VP]),
+    "a2ats_shard_step_partial": (ctypes.c_int, [_SP, _PP, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _I32P,
+                                                _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _SZ, _VP]),
+    "a2ats_shard_step_finish": (ctypes.c_int, [_SP, _PP, ctypes.c_int32, ctypes.c_int32, _I32P, _VP, _VP, _VP, _VP]),
+    "a2ats_combine": (ctypes.c_int, [_SP, ctypes.c_int32, _VP, _VP, _VP]),
 })
 if _lib is not None:  # declared after load(): attach the new signatures
-    for _n in ("a2ats_shard_workspace_bytes", "a2ats_shard_hist", "a2ats_shard_threshold", "a2ats_shard_attend",
-               "a2ats_combine"):
+    for _n in ("a2ats_comm_unique_id", "a2ats_comm_init", "a2ats_comm_destroy", "a2ats_shard_state_bytes",
+               "a2ats_shard_msg_bytes", "a2ats_shard_state_layout", "a2ats_shard_workspace_bytes", "a2ats_shard_state_build",
+               "a2ats_decode_step_sharded", "a2ats_shard_step_partial", "a2ats_shard_step_finish", "a2ats_combine"):
         _f = getattr(_lib, _n)
         _f.restype, _f.argtypes = _SIGS[_n]
 
+A2ATS_COMM_ID_BYTES = 128
 
-def a2ats_shard_workspace_bytes(shape: a2ats_shape, params) -> int:
+
+def _bounds(bounds):
+    arr = (ctypes.c_int32 * len(bounds))(*[int(b) for b in bounds])
+    return arr
+
+
+def a2ats_comm_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(A2ATS_COMM_ID_BYTES)
+    _check("a2ats_comm_unique_id", load().a2ats_comm_unique_id(buf))
+    return buf.raw
+
+
+def a2ats_comm_init(uid: bytes, world: int, rank: int):
+    if len(uid) != A2ATS_COMM_ID_BYTES:
+        raise ValueError("uid must be 128 bytes")
+    out = _VP()
+    buf = ctypes.create_string_buffer(uid, A2ATS_COMM_ID_BYTES)
+    _check("a2ats_comm_init", load().a2ats_comm_init(buf, int(world), int(rank), ctypes.byref(out)))
+    return out
+
+
+def a2ats_comm_destroy(comm):
+    _check("a2ats_comm_destroy", load().a2ats_comm_destroy(comm))
+
+
+def a2ats_shard_state_bytes(shape, params, world: int) -> int:
     p = params.c() if isinstance(params, Params) else params
-    return int(load().a2ats_shard_workspace_bytes(ctypes.byref(shape), ctypes.byref(p)))
+    return int(load().a2ats_shard_state_bytes(ctypes.byref(shape), ctypes.byref(p), int(world)))
 
 
-def a2ats_shard_hist(shape, params, n_ctx, shard_begin, shard_len, q, codes, codebook, hist, cand_hist, ws,
-                     stream=None):
+def a2ats_shard_state_layout(shape, params, world: int) -> dict:
+    p = params.c() if isinstance(params, Params) else params
+    off = (_SZ * 6)()
+    _check("a2ats_shard_state_layout", load().a2ats_shard_state_layout(ctypes.byref(shape), ctypes.byref(p),
+                                                                       int(world), off))
+    return dict(hist_g=off[0], hist_r=off[1], ring=off[2], sinkc=off[3], WR=off[4], n_sink_cap=off[5])
+
+
+def a2ats_shard_msg_bytes(shape) -> int:
+    return int(load().a2ats_shard_msg_bytes(ctypes.byref(shape)))
+
+
+def a2ats_shard_workspace_bytes(shape, params, world: int) -> int:
+    p = params.c() if isinstance(params, Params) else params
+    return int(load().a2ats_shard_workspace_bytes(ctypes.byref(shape), ctypes.byref(p), int(world)))
+
+
+def a2ats_shard_state_build(shape, params, world, rank, bounds, n_tokens, codes, state, ws, comm=None, stream=None):
     import torch
     p = params.c() if isinstance(params, Params) else params
-    rc = load().a2ats_shard_hist(ctypes.byref(shape), ctypes.byref(p), int(n_ctx), int(shard_begin), int(shard_len),
-                                 _ptr(q, "q", torch.bfloat16), _ptr(codes, "codes", torch.uint16),
-                                 _ptr(codebook, "codebook", torch.bfloat16),
-                                 _ptr(hist, "hist", torch.int32, optional=True),
-                                 _ptr(cand_hist, "cand_hist", torch.int32), _ptr(ws, "ws"),
-                                 ws.numel() * ws.element_size(), _stream(stream))
-    _check("a2ats_shard_hist", rc)
+    rc = load().a2ats_shard_state_build(ctypes.byref(shape), ctypes.byref(p), int(world), int(rank), _bounds(bounds),
+                                        int(n_tokens), _ptr(codes, "codes", torch.uint16), _ptr(state, "state"),
+                                        _ptr(ws, "ws"), ws.numel() * ws.element_size(), comm, _stream(stream))
+    _check("a2ats_shard_state_build", rc)
 
 
-def a2ats_shard_threshold(shape, params, n_ctx, cand_hist_global, counts, ws, stream=None):
+def a2ats_decode_step_sharded(shape, params, n_ctx, world, rank, bounds, q, k_cache, v_cache, codes, codebook, chat,
+                              nrm, state, out, sel_out, ws, comm=None, stream=None):
     import torch
     p = params.c() if isinstance(params, Params) else params
-    rc = load().a2ats_shard_threshold(ctypes.byref(shape), ctypes.byref(p), int(n_ctx),
-                                      _ptr(cand_hist_global, "cand_hist_global", torch.int32),
-                                      _ptr(counts, "counts", torch.int32), _ptr(ws, "ws"),
-                                      ws.numel() * ws.element_size(), _stream(stream))
-    _check("a2ats_shard_threshold", rc)
+    rc = load().a2ats_decode_step_sharded(
+        ctypes.byref(shape), ctypes.byref(p), int(n_ctx), int(world), int(rank), _bounds(bounds),
+        _ptr(q, "q", torch.bfloat16), _ptr(k_cache, "k_cache", torch.bfloat16), _ptr(v_cache, "v_cache", torch.bfloat16),
+        _ptr(codes, "codes", torch.uint16), _ptr(codebook, "codebook", torch.bfloat16), _ptr(chat, "chat", torch.bfloat16),
+        _ptr(nrm, "nrm", torch.float32), _ptr(state, "state"), _ptr(out, "out", torch.float32),
+        _ptr(sel_out, "sel_out", torch.int32, optional=True), _ptr(ws, "ws"), ws.numel() * ws.element_size(), comm,
+        _stream(stream))
+    _check("a2ats_decode_step_sharded", rc)
 
 
-def a2ats_shard_attend(shape, params, n_ctx, shard_begin, shard_len, rank, nranks, counts_all, q, k_cache, v_cache,
-                       codes, partial, sel_out, ws, stream=None):
+def a2ats_shard_step_partial(shape, params, n_ctx, world, rank, bounds, q, k_cache, v_cache, codes, codebook, chat,
+                             nrm, state, msg, sel_out, ws, stream=None):
     import torch
     p = params.c() if isinstance(params, Params) else params
-    rc = load().a2ats_shard_attend(ctypes.byref(shape), ctypes.byref(p), int(n_ctx), int(shard_begin), int(shard_len),
-                                   int(rank), int(nranks), _ptr(counts_all, "counts_all", torch.int32),
-                                   _ptr(q, "q", torch.bfloat16), _ptr(k_cache, "k_cache", torch.bfloat16),
-                                   _ptr(v_cache, "v_cache", torch.bfloat16), _ptr(codes, "codes", torch.uint16),
-                                   _ptr(partial, "partial", torch.float32),
-                                   _ptr(sel_out, "sel_out", torch.int32, optional=True), _ptr(ws, "ws"),
-                                   ws.numel() * ws.element_size(), _stream(stream))
-    _check("a2ats_shard_attend", rc)
+    rc = load().a2ats_shard_step_partial(
+        ctypes.byref(shape), ctypes.byref(p), int(n_ctx), int(world), int(rank), _bounds(bounds),
+        _ptr(q, "q", torch.bfloat16), _ptr(k_cache, "k_cache", torch.bfloat16), _ptr(v_cache, "v_cache", torch.bfloat16),
+        _ptr(codes, "codes", torch.uint16), _ptr(codebook, "codebook", torch.bfloat16), _ptr(chat, "chat", torch.bfloat16),
+        _ptr(nrm, "nrm", torch.float32), _ptr(state, "state"), _ptr(msg, "msg"),
+        _ptr(sel_out, "sel_out", torch.int32, optional=True), _ptr(ws, "ws"), ws.numel() * ws.element_size(),
+        _stream(stream))
+    _check("a2ats_shard_step_partial", rc)
+
+
+def a2ats_shard_step_finish(shape, params, n_ctx, world, bounds, msgs, state, out, stream=None):
+    import torch
+    p = params.c() if isinstance(params, Params) else params
+    rc = load().a2ats_shard_step_finish(ctypes.byref(shape), ctypes.byref(p), int(n_ctx), int(world),
+                                        _bounds(bounds), _ptr(msgs, "msgs"), _ptr(state, "state"),
+                                        _ptr(out, "out", torch.float32), _stream(stream))
+    _check("a2ats_shard_step_finish", rc)
 
 
 def a2ats_combine(shape, nparts, partials, out, stream=None):

@@ -1,6 +1,8 @@
 // C-ABI of liba2ats.so (declared and documented in include/a2ats.h).
 // Host orchestration only: validation, workspace carving, kernel launches on
 // the caller's stream.  No allocation, no host synchronisation.
+#include <dlfcn.h>
+
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -112,7 +114,7 @@ void derive(const a2ats_shape* s, const a2ats_params* p, int n_ctx, Derived* d) 
 }
 
 struct DecodeWs {
-  size_t cs, agg, lut, sel, part, actr, cand_keep, pinfo, nsel, wlog, eslot, ectr, tblg, desc, qt, total;
+  size_t cs, agg, lut, sel, part, actr, pinfo, nsel, wlog, eslot, ectr, tblg, desc, qt, total;
 };
 
 DecodeWs decode_layout(const a2ats_shape* s, const a2ats_params* p) {
@@ -136,7 +138,6 @@ DecodeWs decode_layout(const a2ats_shape* s, const a2ats_params* p) {
   w.lut = o; o = align_up(o + (size_t)s->B * s->Hq * s->L * 4);
   w.sel = o; o = align_up(o + (size_t)P * std::max<long long>(kmax, 1) * 4);
   w.part = o; o = align_up(o + (size_t)P * (G / GT) * GT * nsplit_max * 130 * 4);
-  w.cand_keep = o; o = align_up(o + (size_t)P * s->L * 4);   // sharded step only
   w.pinfo = o; o = align_up(o + (size_t)P * 16);
   w.nsel = o; o = align_up(o + (size_t)P * 4);
   w.wlog = o; o = align_up(o + (size_t)P * kWinPre * 8 * 4);
@@ -730,123 +731,341 @@ extern "C" int a2ats_stage_rows(const a2ats_shape* shape, int32_t n_ctx, const v
                                 static_cast<uint8_t*>(v_cache), nq, nkv, shape->n_max, n_ctx - 1));
 }
 
+}  // extern "C"
+
 // ------------------------------------------------------------------ sequence-sharded step
+// SURVEY 8b / 8e / 8f.1 (the paper itself is single-GPU).  Rank r holds the global
+// tokens [bounds[r], bounds[r + 1]) of every (b, KV head) sequence in its own K / V / code
+// arrays (local index = global - bounds[r]); q, the codebook and the shard STATE are
+// replicated.  One step = a0 for the new token n-1 on its owner + the LUT (bitwise identical on
+// every rank) + the collective-free global top-K from the replicated histograms + the local
+// attention partial, then ONE all-gather (every rank's partial (m, l, o) and the new token's
+// code) and the finish: LSE combine in rank order + the state update (the new code joins the
+// replicated histograms, the code ring and, for the first tokens, the sink codes).
+namespace a2ats {
 namespace {
-int shard_common(const a2ats_shape* shape, const a2ats_params* params, int n_ctx, int shard_begin, int shard_len,
-                 void* ws, size_t ws_bytes) {
-  int rc = check_shape(shape);
-  if (rc) return rc;
-  rc = check_params(params);
-  if (rc) return rc;
-  if (n_ctx <= 0 || shard_begin < 0 || shard_len < 0 || shard_len > shape->n_max || shard_begin > n_ctx)
-    return A2ATS_EINVAL;
-  if (!ws || ws_bytes < decode_layout(shape, params).total) return A2ATS_EWORKSPACE;
+
+// NCCL through dlopen (the process's libnccl.so.2: the one torch.distributed loaded, or the
+// path in A2ATS_NCCL_LIB): no link-time dependency, a build without NCCL still loads.
+struct NcclApi {
+  bool ok = false;
+  int (*get_unique_id)(void*) = nullptr;
+  int (*comm_init_rank)(void**, int, a2ats_comm_id, int) = nullptr;
+  int (*comm_destroy)(void*) = nullptr;
+  int (*all_gather)(const void*, void*, size_t, int, void*, cudaStream_t) = nullptr;
+  int (*all_reduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+};
+const NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi x;
+    const char* path = std::getenv("A2ATS_NCCL_LIB");
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);  // already in the process (torch)
+    if (!h) h = dlopen(path ? path : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return x;
+    x.get_unique_id = reinterpret_cast<int (*)(void*)>(dlsym(h, "ncclGetUniqueId"));
+    x.comm_init_rank = reinterpret_cast<int (*)(void**, int, a2ats_comm_id, int)>(dlsym(h, "ncclCommInitRank"));
+    x.comm_destroy = reinterpret_cast<int (*)(void*)>(dlsym(h, "ncclCommDestroy"));
+    x.all_gather = reinterpret_cast<int (*)(const void*, void*, size_t, int, void*, cudaStream_t)>(
+        dlsym(h, "ncclAllGather"));
+    x.all_reduce = reinterpret_cast<int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t)>(
+        dlsym(h, "ncclAllReduce"));
+    x.ok = x.get_unique_id && x.comm_init_rank && x.comm_destroy && x.all_gather && x.all_reduce;
+    return x;
+  }();
+  return api;
+}
+constexpr int kNcclInt32 = 2, kNcclFloat32 = 7, kNcclSum = 0;  // ncclDataType_t / ncclRedOp_t values
+
+struct ShardState {  // offsets in the caller's state buffer (a2ats_shard_state_bytes)
+  size_t hist_g, hist_r, ring, sinkc, total;
+  int WR, n_sink_cap;
+};
+ShardState state_layout(const a2ats_shape* s, const a2ats_params* p, int world) {
+  ShardState st;
+  const size_t P = (size_t)s->B * s->Hkv;
+  st.WR = 1;
+  while (st.WR < p->window) st.WR <<= 1;
+  st.n_sink_cap = std::max(p->n_sink, 1);
+  size_t o = 0;
+  st.hist_g = o; o = align_up(o + P * s->L * 4);
+  st.hist_r = o; o = align_up(o + (size_t)world * P * s->L * 4);
+  st.ring = o; o = align_up(o + P * st.WR * 2);
+  st.sinkc = o; o = align_up(o + P * st.n_sink_cap * 2);
+  st.total = o;
+  return st;
+}
+size_t msg_floats(const a2ats_shape* s) {  // partial [B*Hq][130] + the new token's code per pair
+  return ((size_t)s->B * s->Hq * 130 + (size_t)s->B * s->Hkv + 3) / 4 * 4;
+}
+struct ShardWs {
+  size_t dec, msg, recv, nsel, total;
+};
+ShardWs shard_ws_layout(const a2ats_shape* s, const a2ats_params* p, int world) {
+  ShardWs w;
+  size_t o = 0;
+  w.dec = o; o = align_up(o + decode_layout(s, p).total);
+  w.msg = o; o = align_up(o + msg_floats(s) * 4);
+  w.recv = o; o = align_up(o + (size_t)world * msg_floats(s) * 4);
+  w.nsel = o; o = align_up(o + (size_t)s->B * s->Hkv * 4);
+  w.total = o;
+  return w;
+}
+
+int check_bounds(const int32_t* bounds, int world, int rank, const a2ats_shape* s) {
+  if (!bounds || world < 1 || world > kMaxRanks || rank < 0 || rank >= world) return A2ATS_EINVAL;
+  if (bounds[0] != 0) return A2ATS_EINVAL;
+  for (int r = 0; r < world; ++r)
+    if (bounds[r + 1] < bounds[r]) return A2ATS_EINVAL;
+  if (bounds[rank + 1] - bounds[rank] > s->n_max) return A2ATS_EINVAL;
   return A2ATS_OK;
 }
+int owner_of_host(const int32_t* bounds, int world, int t) {
+  for (int r = 0; r < world; ++r)
+    if (t >= bounds[r] && t < bounds[r + 1]) return r;
+  return -1;
+}
+
+// state of tokens [0, n): local histogram (hist_r[rank], hist_g) and the codes of the sinks and
+// the latest WR tokens held by this rank; other entries 0 (summed across ranks by the caller)
+__global__ void shard_state_local_kernel(const uint16_t* codes, int n_max, int L, int P, int lo, int hi, int n,
+                                         int rank, int WR, int n_sink_cap, int32_t* hist_g, int32_t* hist_r,
+                                         int32_t* ring32, int32_t* sink32) {
+  const int pair = blockIdx.y;
+  const uint16_t* cp = codes + (size_t)pair * n_max;
+  const int e = min(hi, n);
+  for (int t = lo + blockIdx.x * blockDim.x + threadIdx.x; t < e; t += gridDim.x * blockDim.x) {
+    const int code = cp[t - lo];
+    atomicAdd(&hist_g[(size_t)pair * L + code], 1);
+    atomicAdd(&hist_r[((size_t)rank * P + pair) * L + code], 1);
+    if (t >= n - WR) ring32[(size_t)pair * WR + (t % WR)] = code;
+    if (t < n_sink_cap) sink32[(size_t)pair * n_sink_cap + t] = code;
+  }
+}
+__global__ void shard_state_pack_kernel(const int32_t* ring32, const int32_t* sink32, uint16_t* ring,
+                                        uint16_t* sinkc, int nring, int nsink) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nring + nsink; i += gridDim.x * blockDim.x) {
+    if (i < nring) ring[i] = (uint16_t)ring32[i];
+    else sinkc[i - nring] = (uint16_t)sink32[i - nring];
+  }
+}
+// finish: the new token's code (from its owner's message) joins the replicated state
+__global__ void shard_state_update_kernel(const float* msgs, size_t msg_stride, size_t code_off, int owner, int P,
+                                          int L, int t_new, int WR, int n_sink_cap, int32_t* hist_g,
+                                          int32_t* hist_r, uint16_t* ring, uint16_t* sinkc) {
+  pdl_wait();
+  pdl_trigger();
+  const int pair = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pair >= P) return;
+  const uint32_t code = reinterpret_cast<const uint32_t*>(msgs + (size_t)owner * msg_stride + code_off)[pair];
+  if (code >= (uint32_t)L) return;  // (never: the encoder emits codes < L)
+  hist_g[(size_t)pair * L + code] += 1;
+  hist_r[((size_t)owner * P + pair) * L + code] += 1;
+  ring[(size_t)pair * WR + (t_new % WR)] = (uint16_t)code;
+  if (t_new < n_sink_cap) sinkc[(size_t)pair * n_sink_cap + t_new] = (uint16_t)code;
+}
+
 }  // namespace
+}  // namespace a2ats
 
-size_t a2ats_shard_workspace_bytes(const a2ats_shape* shape, const a2ats_params* params) {
-  return a2ats_decode_workspace_bytes(shape, params);
+extern "C" {
+
+int a2ats_comm_unique_id(void* id) {
+  if (!id) return A2ATS_EINVAL;
+  if (!nccl().ok) return A2ATS_ENCCL;
+  return nccl().get_unique_id(id) == 0 ? A2ATS_OK : A2ATS_ENCCL;
 }
 
-int a2ats_shard_hist(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx, int32_t shard_begin,
-                     int32_t shard_len, const void* q, const uint16_t* codes, const void* codebook,
-                     const int32_t* hist, int32_t* cand_hist, void* ws, size_t ws_bytes, void* stream) {
-  int rc = shard_common(shape, params, n_ctx, shard_begin, shard_len, ws, ws_bytes);
+struct a2ats_comm {
+  void* nccl_comm;
+  int world, rank;
+};
+
+int a2ats_comm_init(const void* id, int32_t world, int32_t rank, a2ats_comm** out) {
+  if (!id || !out || world < 1 || world > kMaxRanks || rank < 0 || rank >= world) return A2ATS_EINVAL;
+  if (!nccl().ok) return A2ATS_ENCCL;
+  a2ats_comm_id uid;
+  std::memcpy(&uid, id, sizeof(uid));
+  void* c = nullptr;
+  if (nccl().comm_init_rank(&c, world, uid, rank) != 0) return A2ATS_ENCCL;
+  *out = new a2ats_comm{c, world, rank};
+  return A2ATS_OK;
+}
+
+int a2ats_comm_destroy(a2ats_comm* comm) {
+  if (!comm) return A2ATS_EINVAL;
+  const int r = nccl().ok && nccl().comm_destroy(comm->nccl_comm) == 0 ? A2ATS_OK : A2ATS_ENCCL;
+  delete comm;
+  return r;
+}
+
+size_t a2ats_shard_state_bytes(const a2ats_shape* shape, const a2ats_params* params, int32_t world) {
+  if (check_shape(shape) || check_params(params) || world < 1 || world > kMaxRanks) return 0;
+  return state_layout(shape, params, world).total;
+}
+int a2ats_shard_state_layout(const a2ats_shape* shape, const a2ats_params* params, int32_t world, size_t* offsets) {
+  if (check_shape(shape) || check_params(params) || world < 1 || world > kMaxRanks || !offsets) return A2ATS_EINVAL;
+  const ShardState st = state_layout(shape, params, world);
+  offsets[0] = st.hist_g;
+  offsets[1] = st.hist_r;
+  offsets[2] = st.ring;
+  offsets[3] = st.sinkc;
+  offsets[4] = (size_t)st.WR;
+  offsets[5] = (size_t)st.n_sink_cap;
+  return A2ATS_OK;
+}
+size_t a2ats_shard_msg_bytes(const a2ats_shape* shape) {
+  if (check_shape(shape)) return 0;
+  return msg_floats(shape) * 4;
+}
+size_t a2ats_shard_workspace_bytes(const a2ats_shape* shape, const a2ats_params* params, int32_t world) {
+  if (check_shape(shape) || check_params(params) || world < 1 || world > kMaxRanks) return 0;
+  return shard_ws_layout(shape, params, world).total;
+}
+
+int a2ats_shard_state_build(const a2ats_shape* shape, const a2ats_params* params, int32_t world, int32_t rank,
+                            const int32_t* bounds, int32_t n_tokens, const uint16_t* codes, void* state, void* ws,
+                            size_t ws_bytes, a2ats_comm* comm, void* stream) {
+  int rc = check_shape(shape);
+  if (!rc) rc = check_params(params);
+  if (!rc) rc = check_bounds(bounds, world, rank, shape);
   if (rc) return rc;
-  if (!q || !codes || !codebook || !cand_hist || !aligned16(q) || !aligned16(codes) || !aligned16(codebook))
+  if (!codes || !state || n_tokens < 0 || n_tokens > bounds[world]) return A2ATS_EINVAL;
+  if (comm && (comm->world != world || comm->rank != rank)) return A2ATS_EINVAL;
+  const ShardWs W = shard_ws_layout(shape, params, world);
+  const ShardState S = state_layout(shape, params, world);
+  const int P = shape->B * shape->Hkv;
+  const size_t nring = (size_t)P * S.WR, nsink = (size_t)P * S.n_sink_cap;
+  if (!ws || ws_bytes < W.total || (size_t)world * msg_floats(shape) * 4 < (nring + nsink) * 4) return A2ATS_EWORKSPACE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint8_t* sb = static_cast<uint8_t*>(state);
+  // scratch: the message receive area (the step's zero-on-entry counters must stay untouched)
+  int32_t* ring32 = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(ws) + W.recv);
+  int32_t* sink32 = ring32 + nring;
+  rc = cuda_status(cudaMemsetAsync(state, 0, S.total, st));
+  if (!rc) rc = cuda_status(cudaMemsetAsync(ws, 0, (nring + nsink) * 4, st));
+  if (rc) return rc;
+  dim3 grid(std::max(1, std::min(64, (bounds[rank + 1] - bounds[rank] + 1023) / 1024)), P);
+  shard_state_local_kernel<<<grid, 256, 0, st>>>(codes, shape->n_max, shape->L, P, bounds[rank], bounds[rank + 1],
+                                                  n_tokens, rank, S.WR, S.n_sink_cap,
+                                                  reinterpret_cast<int32_t*>(sb + S.hist_g),
+                                                  reinterpret_cast<int32_t*>(sb + S.hist_r), ring32, sink32);
+  rc = cuda_status(cudaGetLastError());
+  if (rc) return rc;
+  if (world > 1 && comm) {  // every rank's entries are zero elsewhere: sums assemble the replicated state
+    const size_t nh = (size_t)(world + 1) * P * shape->L;  // hist_g and hist_r are adjacent int32 arrays
+    if (S.hist_r != S.hist_g + align_up((size_t)P * shape->L * 4)) return A2ATS_EINVAL;
+    int r1 = nccl().all_reduce(sb + S.hist_g, sb + S.hist_g, (size_t)P * shape->L, kNcclInt32, kNcclSum,
+                               comm->nccl_comm, st);
+    int r2 = nccl().all_reduce(sb + S.hist_r, sb + S.hist_r, (size_t)world * P * shape->L, kNcclInt32, kNcclSum,
+                               comm->nccl_comm, st);
+    int r3 = nccl().all_reduce(ring32, ring32, nring + nsink, kNcclInt32, kNcclSum, comm->nccl_comm, st);
+    (void)nh;
+    if (r1 || r2 || r3) return A2ATS_ENCCL;
+  }
+  shard_state_pack_kernel<<<64, 256, 0, st>>>(ring32, sink32, reinterpret_cast<uint16_t*>(sb + S.ring),
+                                             reinterpret_cast<uint16_t*>(sb + S.sinkc), (int)nring, (int)nsink);
+  return cuda_status(cudaGetLastError());
+}
+
+}  // extern "C"
+
+namespace a2ats {
+namespace {
+int shard_common(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx, int32_t world, int32_t rank,
+                 const int32_t* bounds) {
+  int rc = check_shape(shape);
+  if (!rc) rc = check_params(params);
+  if (!rc) rc = check_bounds(bounds, world, rank, shape);
+  if (rc) return rc;
+  if (n_ctx <= 0 || n_ctx > bounds[world]) return A2ATS_EINVAL;
+  if (owner_of_host(bounds, world, n_ctx - 1) < 0) return A2ATS_EINVAL;
+  if (params->kv_location != A2ATS_KV_DEVICE) return A2ATS_EUNSUPPORTED;
+  if (shape->n_max % 64 || !select_pipe_ok(shape->L) || shape->B > encode_cw_max()) return A2ATS_EUNSUPPORTED;
+  return A2ATS_OK;
+}
+
+// phase A: a0 (owner) + LUT + global threshold from the state + local scan + local attention
+// partial, into this rank's message [msg_floats]
+int shard_partial(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx, int32_t world, int32_t rank,
+                  const int32_t* bounds, const void* q, const void* k_cache, const void* v_cache, uint16_t* codes,
+                  const void* codebook, const void* chat, const float* nrm, const void* state, float* msg,
+                  int32_t* sel_out, void* ws, size_t ws_bytes, cudaStream_t st) {
+  int rc = shard_common(shape, params, n_ctx, world, rank, bounds);
+  if (rc) return rc;
+  if (!q || !k_cache || !v_cache || !codes || !codebook || !chat || !nrm || !state || !msg) return A2ATS_EINVAL;
+  if (!aligned16(q) || !aligned16(k_cache) || !aligned16(v_cache) || !aligned16(codes) || !aligned16(codebook) ||
+      !aligned16(chat) || !aligned16(msg))
     return A2ATS_EINVAL;
+  const ShardWs W = shard_ws_layout(shape, params, world);
+  if (!ws || ws_bytes < W.total) return A2ATS_EWORKSPACE;
   const DecodeWs Lw = decode_layout(shape, params);
+  const ShardState S = state_layout(shape, params, world);
   Derived d;
   derive(shape, params, n_ctx, &d);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  uint8_t* base = static_cast<uint8_t*>(ws);
-  const LutArgs la = make_lut_args(shape, params, d, q, codebook, reinterpret_cast<float*>(base + Lw.agg), nullptr,
-                                   reinterpret_cast<float2*>(base + Lw.cs));
-  PrepArgs p = prep_empty();
-  prep_set_lut(p, la);
-  CUtensorMap tm;
-  rc = cuda_status(make_tmap_sw128(&tm, codebook, (uint64_t)shape->Hkv * shape->L, kD, 128));
-  if (rc) return rc;
-  rc = cuda_status(launch_prep(p, tm, tm, st));  // the LUT, replicated on every rank, bitwise identical
-  if (rc) return rc;
-  SelArgs sa{};
-  sa.agg = la.agg;
-  sa.hist = const_cast<int32_t*>(hist);  // read only (no append in the sharded step)
-  sa.codes = codes;
-  sa.L = shape->L;
-  sa.W = d.W;
-  sa.n_max = shape->n_max;
-  sa.n_ctx = n_ctx;
-  sa.c0 = d.c0;
-  sa.c1 = d.c1;
-  sa.n_s = d.n_s;
-  sa.w0 = d.w0;
-  sa.keff = d.keff;
-  sa.shard_begin = shard_begin;
-  sa.shard_len = shard_len;
-  sa.cand_out = cand_hist;
-  sa.cand_keep = reinterpret_cast<int32_t*>(base + Lw.cand_keep);
-  return cuda_status(launch_shard_hist(sa, d.P, st));
-}
-
-int a2ats_shard_threshold(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx,
-                          const int32_t* cand_hist_global, int32_t* counts, void* ws, size_t ws_bytes, void* stream) {
-  int rc = shard_common(shape, params, n_ctx, 0, 0, ws, ws_bytes);
-  if (rc) return rc;
-  if (!cand_hist_global || !counts) return A2ATS_EINVAL;
-  const DecodeWs Lw = decode_layout(shape, params);
-  Derived d;
-  derive(shape, params, n_ctx, &d);
-  uint8_t* base = static_cast<uint8_t*>(ws);
-  SelArgs sa{};
-  sa.agg = reinterpret_cast<float*>(base + Lw.agg);
-  sa.L = shape->L;
-  sa.W = d.W;
-  sa.n_max = shape->n_max;
-  sa.n_ctx = n_ctx;
-  sa.keff = d.keff;
-  sa.cand_in = cand_hist_global;
-  sa.cand_keep = reinterpret_cast<int32_t*>(base + Lw.cand_keep);
-  sa.pinfo = reinterpret_cast<uint32_t*>(base + Lw.pinfo);
-  sa.counts_out = counts;
-  return cuda_status(launch_shard_thresh(sa, d.P, static_cast<cudaStream_t>(stream)));
-}
-
-int a2ats_shard_attend(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx, int32_t shard_begin,
-                       int32_t shard_len, int32_t rank, int32_t nranks, const int32_t* counts_all, const void* q,
-                       const void* k_cache, const void* v_cache, const uint16_t* codes, float* partial,
-                       int32_t* sel_out, void* ws, size_t ws_bytes, void* stream) {
-  int rc = shard_common(shape, params, n_ctx, shard_begin, shard_len, ws, ws_bytes);
-  if (rc) return rc;
-  if (nranks < 1 || rank < 0 || rank >= nranks) return A2ATS_EINVAL;
-  if (!counts_all || !q || !k_cache || !v_cache || !codes || !partial) return A2ATS_EINVAL;
-  if (!aligned16(q) || !aligned16(k_cache) || !aligned16(v_cache) || !aligned16(codes)) return A2ATS_EINVAL;
-  const DecodeWs Lw = decode_layout(shape, params);
-  Derived d;
-  derive(shape, params, n_ctx, &d);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  uint8_t* base = static_cast<uint8_t*>(ws);
+  uint8_t* base = static_cast<uint8_t*>(ws) + W.dec;
+  const uint8_t* sb = static_cast<const uint8_t*>(state);
+  const int lo = bounds[rank], hi = bounds[rank + 1];
+  const int owner = owner_of_host(bounds, world, n_ctx - 1);
   const int kcap = std::max(1, (int)std::min<long long>(params->topk, shape->n_max));
   int32_t* sel = sel_out ? sel_out : reinterpret_cast<int32_t*>(base + Lw.sel);
-  int32_t* nsel = reinterpret_cast<int32_t*>(base + Lw.nsel);
-  // rows of Sel held by this rank
-  const int se = std::min(shard_begin + shard_len, n_ctx);
-  const int s_lo = std::max(0, shard_begin), s_hi = std::min(d.n_s, se);
-  const int w_lo = std::max(d.w0, shard_begin), w_hi = std::min(n_ctx, se);
-  // logits of the rank's window rows (prep kernel, window role only)
+  int32_t* nsel = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(ws) + W.nsel);
   float* wlog = reinterpret_cast<float*>(base + Lw.wlog);
+  float* agg = reinterpret_cast<float*>(base + Lw.agg);
+
+  // 1. prep: LUT (every rank: bitwise identical), the new token's code (owner), the logits of
+  //    this rank's window rows
+  LutArgs la = make_lut_args(shape, params, d, q, codebook, agg, nullptr, reinterpret_cast<float2*>(base + Lw.cs));
+  const bool lut_fma = params->lut_engine == A2ATS_LUT_FMA ||
+                       (params->lut_engine == A2ATS_LUT_AUTO && shape->B * d.G <= A2ATS_LUT_FMA_MAX_VECTORS);
+  if (la.NV > 64 && !lut_fma) la.qt = reinterpret_cast<uint16_t*>(base + Lw.qt);
   PrepArgs p = prep_empty();
-  p.lut = make_lut_args(shape, params, d, q, nullptr, nullptr, nullptr, nullptr);  // q, shapes, rotations
-  prep_set_window(p, shape, k_cache, wlog, n_ctx, w_lo, std::max(0, w_hi - w_lo), shard_begin);
-  if (p.n_win) {
-    CUtensorMap tm;  // unused by the window role
-    std::memset(&tm, 0, sizeof(tm));
-    rc = cuda_status(launch_prep(p, tm, tm, st));
+  prep_set_lut(p, la);
+  if (lut_fma) p.n_lut = 0;
+  const int w_lo = std::max(d.w0, lo), w_hi = std::min(n_ctx, hi);
+  prep_set_window(p, shape, k_cache, wlog, n_ctx, w_lo, std::max(0, w_hi - w_lo), lo);
+  const int n_wl = p.n_wl;
+  CUtensorMap tmA, tmC;
+  rc = cuda_status(make_tmap_sw128(&tmA, codebook, (uint64_t)shape->Hkv * shape->L, kD, 128));
+  if (rc) return rc;
+  tmC = tmA;
+  if (rank == owner) {
+    EncArgs e;
+    e.keys = static_cast<const uint16_t*>(k_cache);
+    e.chat = static_cast<const uint16_t*>(chat);
+    e.nrm = nrm;
+    e.slot = reinterpret_cast<unsigned long long*>(base + Lw.eslot);
+    e.counter = reinterpret_cast<unsigned int*>(base + Lw.ectr);
+    e.codes = codes;
+    e.hist = nullptr;  // the state update (finish) adds the new code everywhere
+    e.B = shape->B;
+    e.Hkv = shape->Hkv;
+    e.L = shape->L;
+    e.n_max = shape->n_max;
+    e.t_begin = n_ctx - 1 - lo;
+    e.T = 1;
+    e.nvec = shape->B;
+    e.lsplit = e.tiles_per_split = 0;
+    prep_set_encode(p, e);
+    rc = cuda_status(make_tmap_sw128(&tmC, chat, (uint64_t)shape->Hkv * shape->L, 2 * kD, encode_codeword_tile()));
     if (rc) return rc;
   }
+  prep_balance(p);
+  stage_mark(0, st);
+  if (la.qt) {
+    rc = cuda_status(launch_qprep(la, st));
+    if (rc) return rc;
+  }
+  if (lut_fma) {
+    rc = cuda_status(launch_lut_fma(la, st));
+    if (rc) return rc;
+  }
+  rc = cuda_status(launch_prep(p, tmA, tmC, st));
+  if (rc) return rc;
+  stage_mark(1, st);
+
+  // 2. global threshold from the replicated state + this rank's tie share; local scan
   SelArgs sa{};
-  sa.agg = reinterpret_cast<float*>(base + Lw.agg);
+  sa.agg = agg;
   sa.codes = codes;
   sa.sel = sel;
   sa.sel_stride = kcap;
@@ -854,24 +1073,47 @@ int a2ats_shard_attend(const a2ats_shape* shape, const a2ats_params* params, int
   sa.W = d.W;
   sa.n_max = shape->n_max;
   sa.n_ctx = n_ctx;
-  sa.c0 = d.c0;
-  sa.c1 = d.c1;
   sa.n_s = d.n_s;
   sa.w0 = d.w0;
-  sa.keff = d.keff;
-  sa.shard_begin = shard_begin;
-  sa.shard_len = shard_len;
+  sa.keff = d.keff;  // global K_eff
+  sa.P = d.P;
+  sa.B = shape->B;
+  sa.shard_begin = lo;
+  sa.shard_len = hi - lo;
   sa.rank = rank;
+  sa.world = world;
+  sa.owner = owner;
+  for (int r = 0; r <= world; ++r) sa.bounds[r] = bounds[r];
+  sa.hist_g = reinterpret_cast<const int32_t*>(sb + S.hist_g);
+  sa.hist_r = reinterpret_cast<const int32_t*>(sb + S.hist_r);
+  sa.ring = reinterpret_cast<const uint16_t*>(sb + S.ring);
+  sa.sinkc = reinterpret_cast<const uint16_t*>(sb + S.sinkc);
+  sa.WR = S.WR;
+  sa.n_sink_cap = S.n_sink_cap;
+  sa.send_codes = reinterpret_cast<uint32_t*>(msg + (size_t)shape->B * shape->Hq * 130);
   sa.pinfo = reinterpret_cast<uint32_t*>(base + Lw.pinfo);
-  sa.counts_all = counts_all;
+  sa.tblg = reinterpret_cast<uint32_t*>(base + Lw.tblg);
   sa.nsel_out = nsel;
-  rc = cuda_status(launch_shard_scan(sa, d.P, st));
+  // the scan's range: this rank's part of the candidates [c0, c1), in local indices
+  const int lc0 = std::max(d.c0, lo), lc1 = std::min(d.c1, hi);
+  sa.c0 = lc1 > lc0 ? lc0 - lo : 0;
+  sa.c1 = lc1 > lc0 ? lc1 - lo : 0;
+  sa.sel_base = lo;
+  const int nblk = (lc1 > lc0 && d.keff > 0) ? std::min(sm_count(), 2 * d.P) : 0;
+  CUtensorMap tmK;
+  rc = cuda_status(make_tmap_codes(&tmK, codes, (uint64_t)d.P, (uint64_t)shape->n_max));
   if (rc) return rc;
+  rc = cuda_status(launch_select_shard(sa, tmK, nblk, st));
+  if (rc) return rc;
+  stage_mark(2, st);
+
+  // 3. attention over this rank's rows of Sel -> partial (m, l, o) into the message
+  const int s_lo = std::max(0, lo), s_hi = std::min(d.n_s, hi);
   AttnArgs aa;
   aa.q = static_cast<const uint16_t*>(q);
-  std::memcpy(aa.bcs, p.lut.bcs, sizeof(aa.bcs));
+  std::memcpy(aa.bcs, la.bcs, sizeof(aa.bcs));
   aa.wlog = wlog;
-  aa.n_wl = p.n_wl;
+  aa.n_wl = n_wl;
   aa.cs = reinterpret_cast<float2*>(base + Lw.cs);
   aa.kc = static_cast<const uint16_t*>(k_cache);
   aa.vc = static_cast<const uint16_t*>(v_cache);
@@ -880,7 +1122,7 @@ int a2ats_shard_attend(const a2ats_shape* shape, const a2ats_params* params, int
   aa.part = reinterpret_cast<float*>(base + Lw.part);
   aa.counter = reinterpret_cast<unsigned int*>(base + Lw.actr);
   aa.out = nullptr;
-  aa.part_out = partial;
+  aa.part_out = msg;
   aa.Hq = shape->Hq;
   aa.Hkv = shape->Hkv;
   aa.G = d.G;
@@ -893,19 +1135,91 @@ int a2ats_shard_attend(const a2ats_shape* shape, const a2ats_params* params, int
   aa.sink_lo = s_lo;
   aa.n_w = std::max(0, w_hi - w_lo);
   aa.win_lo = w_lo;
-  aa.shard_begin = shard_begin;
-  const int local_cand = std::max(0, std::min(d.c1, se) - std::max(d.c0, shard_begin));
+  aa.shard_begin = lo;
+  const int local_cand = std::max(0, lc1 - lc0);
   const int mmax = aa.n_s + std::min(d.keff, local_cand) + aa.n_w;
-  aa.nsplit = std::max(1, (mmax + d.R - 1) / d.R);  // <= the workspace's max splits
+  aa.nsplit = std::max(1, (mmax + d.R - 1) / d.R);
   aa.scale_log2 = kScaleLog2;
-  return cuda_status(launch_attention(aa, d.P, d.GT, st));
+  rc = cuda_status(launch_attention(aa, d.P, d.GT, st));
+  if (rc) return rc;
+  stage_mark(3, st);
+  return A2ATS_OK;
+}
+
+// phase B: LSE combine of the world's partials in rank order + the state update
+int shard_finish(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx, int32_t world,
+                 const int32_t* bounds, const float* msgs, void* state, float* out, cudaStream_t st) {
+  const ShardState S = state_layout(shape, params, world);
+  const int owner = owner_of_host(bounds, world, n_ctx - 1);
+  const size_t mf = msg_floats(shape);
+  const int P = shape->B * shape->Hkv;
+  int rc = cuda_status(launch_combine(msgs, world, shape->B * shape->Hq, mf, out, st));
+  if (rc) return rc;
+  uint8_t* sb = static_cast<uint8_t*>(state);
+  rc = cuda_status(launch_pdl(shard_state_update_kernel, dim3((P + 255) / 256), dim3(256), 0, st, msgs, mf,
+                              (size_t)shape->B * shape->Hq * 130, owner, P, shape->L, n_ctx - 1, S.WR,
+                              S.n_sink_cap, reinterpret_cast<int32_t*>(sb + S.hist_g),
+                              reinterpret_cast<int32_t*>(sb + S.hist_r), reinterpret_cast<uint16_t*>(sb + S.ring),
+                              reinterpret_cast<uint16_t*>(sb + S.sinkc)));
+  stage_mark(4, st);
+  return rc;
+}
+}  // namespace
+}  // namespace a2ats
+
+extern "C" {
+
+int a2ats_shard_step_partial(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx, int32_t world,
+                             int32_t rank, const int32_t* bounds, const void* q, const void* k_cache,
+                             const void* v_cache, uint16_t* codes, const void* codebook, const void* chat,
+                             const float* nrm, const void* state, void* msg, int32_t* sel_out, void* ws,
+                             size_t ws_bytes, void* stream) {
+  return shard_partial(shape, params, n_ctx, world, rank, bounds, q, k_cache, v_cache, codes, codebook, chat, nrm,
+                       state, static_cast<float*>(msg), sel_out, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
+int a2ats_shard_step_finish(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx, int32_t world,
+                            const int32_t* bounds, const void* msgs, void* state, float* out, void* stream) {
+  int rc = shard_common(shape, params, n_ctx, world, 0, bounds);
+  if (rc) return rc;
+  if (!msgs || !state || !out || !aligned16(msgs)) return A2ATS_EINVAL;
+  return shard_finish(shape, params, n_ctx, world, bounds, static_cast<const float*>(msgs), state, out,
+                      static_cast<cudaStream_t>(stream));
+}
+
+int a2ats_decode_step_sharded(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx, int32_t world,
+                              int32_t rank, const int32_t* bounds, const void* q, const void* k_cache,
+                              const void* v_cache, uint16_t* codes, const void* codebook, const void* chat,
+                              const float* nrm, void* state, float* out, int32_t* sel_out, void* ws,
+                              size_t ws_bytes, a2ats_comm* comm, void* stream) {
+  int rc = shard_common(shape, params, n_ctx, world, rank, bounds);
+  if (rc) return rc;
+  if (!out) return A2ATS_EINVAL;
+  if (world > 1 && (!comm || comm->world != world || comm->rank != rank)) return A2ATS_EINVAL;
+  if (world > 1 && !nccl().ok) return A2ATS_ENCCL;
+  const ShardWs W = shard_ws_layout(shape, params, world);
+  if (!ws || ws_bytes < W.total) return A2ATS_EWORKSPACE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  float* msg = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + W.msg);
+  float* recv = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + W.recv);
+  rc = shard_partial(shape, params, n_ctx, world, rank, bounds, q, k_cache, v_cache, codes, codebook, chat, nrm,
+                     state, msg, sel_out, ws, ws_bytes, st);
+  if (rc) return rc;
+  const size_t mf = msg_floats(shape);
+  if (world > 1) {  // the step's only collective: every rank's partial and the new token's code
+    if (nccl().all_gather(msg, recv, mf, kNcclFloat32, comm->nccl_comm, st) != 0) return A2ATS_ENCCL;
+  } else {
+    recv = msg;
+  }
+  return shard_finish(shape, params, n_ctx, world, bounds, recv, state, out, st);
 }
 
 int a2ats_combine(const a2ats_shape* shape, int32_t nparts, const float* partials, float* out, void* stream) {
   int rc = check_shape(shape);
   if (rc) return rc;
   if (nparts < 1 || !partials || !out) return A2ATS_EINVAL;
-  return cuda_status(launch_combine(partials, nparts, shape->B * shape->Hq, out, static_cast<cudaStream_t>(stream)));
+  const size_t rows = (size_t)shape->B * shape->Hq;
+  return cuda_status(launch_combine(partials, nparts, (int)rows, rows * 130, out, static_cast<cudaStream_t>(stream)));
 }
 
 }  // extern "C"

@@ -497,17 +497,19 @@ __global__ __launch_bounds__(NW * 32, NW <= 4 ? 2 : 1) void attn_mma_kernel(Attn
   A2ATS_TL(g_attn_tl, 1);
 }
 
-// Cross-rank log-sum-exp combine of partials [R][B*Hq][130] (base-2 logits), fixed rank order.
-__global__ void combine_kernel(const float* __restrict__ parts, int R, int rows, float* __restrict__ out) {
+// Cross-rank log-sum-exp combine of partials (base-2 logits), fixed rank order; rank r's
+// partials [rows][130] start at parts + r * stride.
+__global__ void combine_kernel(const float* __restrict__ parts, int R, int rows, size_t stride,
+                               float* __restrict__ out) {
   pdl_wait();
   pdl_trigger();
   const int row = blockIdx.x, e = threadIdx.x;
   if (row >= rows) return;
   float M = -INFINITY;
-  for (int r = 0; r < R; ++r) M = fmaxf(M, parts[((size_t)r * rows + row) * 130]);
+  for (int r = 0; r < R; ++r) M = fmaxf(M, parts[(size_t)r * stride + (size_t)row * 130]);
   float num = 0.f, den = 0.f;
   for (int r = 0; r < R; ++r) {
-    const float* p = parts + ((size_t)r * rows + row) * 130;
+    const float* p = parts + (size_t)r * stride + (size_t)row * 130;
     const float sw = (p[0] == -INFINITY) ? 0.f : exp2f(p[0] - M);
     num = fmaf(p[2 + e], sw, num);
     den = fmaf(p[1], sw, den);
@@ -535,8 +537,8 @@ cudaError_t launch_attention(const AttnArgs& a, int P, int /*GT*/, cudaStream_t 
   return launch_attention_nw<8>(a, P, st);
 }
 
-cudaError_t launch_combine(const float* parts, int R, int rows, float* out, cudaStream_t st) {
-  return launch_pdl(combine_kernel, dim3(rows), dim3(kD), 0, st, parts, R, rows, out);
+cudaError_t launch_combine(const float* parts, int R, int rows, size_t stride, float* out, cudaStream_t st) {
+  return launch_pdl(combine_kernel, dim3(rows), dim3(kD), 0, st, parts, R, rows, stride, out);
 }
 
 }  // namespace a2ats

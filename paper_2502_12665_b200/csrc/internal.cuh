@@ -13,6 +13,7 @@ namespace a2ats {
 
 constexpr int kD = 128;     // head dimension supported by this version
 constexpr int kHalf = 64;   // d / 2 rotation pairs (half-split pairing, Q2)
+constexpr int kMaxRanks = 8;  // sequence-sharded step: ranks of one node
 
 // Rotation frequencies theta^(-2m/d) (or the caller's override), fp64, passed by
 // value to the kernels that need angles (bridge b*f_m, window r*f_m).
@@ -177,18 +178,24 @@ struct SelArgs {
   int L, W, n_max, n_ctx, c0, c1, n_s, w0, keff, sel_stride, B;
   // sequence sharding (single GPU: shard_begin = 0, shard_len = n_max)
   int shard_begin, shard_len, rank;
-  int32_t* cand_out;            // [P, L] local candidate histogram, exchanged (all-reduce in place)
-  int32_t* cand_keep;           // [P, L] local candidate histogram, kept in the workspace
-  const int32_t* cand_in;       // [P, L] all-reduced candidate histogram
-  uint32_t* pinfo;              // [P, 4] key(v*), m, K_eff (global)
-  int32_t* counts_out;          // [P, 2] this rank's candidates above / at v*
-  const int32_t* counts_all;    // [R, P, 2] all-gathered counts
-  int32_t* nsel_out;            // [P] number of locally selected tokens
+  uint32_t* pinfo;              // [P, 4] key(v*), m, K_eff, E (this rank's share when sharded)
+  int32_t* nsel_out;            // [P] number of locally selected tokens (sharded step)
   // long contexts (launch_select_split): per-pair class table, chunk descriptors, completion
   uint32_t* tblg;               // [P, W] compact 2-bit classes
   unsigned long long* desc;     // [P, desc_stride] published (#above, #tied) per chunk, 0 = not yet
   int nchunk, desc_stride;
   int P;                        // pairs (launch_select_pipe: the scan grid is persistent)
+  // sequence-sharded step with replicated histograms (a2ats_decode_step_sharded):
+  // the global histogram and every rank's histogram of tokens [0, n_ctx - 1), the codes of the
+  // sinks and of the most recent WR tokens (ring, slot t % WR), the ranks' global bounds
+  const int32_t* hist_g;        // [P, L]
+  const int32_t* hist_r;        // [world, P, L]
+  const uint16_t* ring;         // [P, WR]
+  const uint16_t* sinkc;        // [P, n_sink_cap]
+  int WR, n_sink_cap, world, owner;
+  int bounds[kMaxRanks + 1];    // rank r holds global tokens [bounds[r], bounds[r + 1])
+  uint32_t* send_codes;         // [P] the new token's code (owner rank), into the all-gather message
+  int sel_base;                 // added to emitted token indices (local -> global)
   // window logits computed by the threshold kernel before its dependency wait (long contexts;
   // otherwise the prep kernel's window role): wlog == nullptr disables
   float* wlog;                  // [P, 64, 8]
@@ -266,16 +273,16 @@ cudaError_t launch_prep(const PrepArgs& p, const CUtensorMap& tm_codebook, const
 cudaError_t launch_scores(const float* lut_full, const uint16_t* codes, float* scores, int B, int Hq, int Hkv,
                           int G, int L, int n_max, int n_ctx, cudaStream_t st);
 cudaError_t launch_select(const SelArgs& a, int P, cudaStream_t st);
-cudaError_t launch_shard_hist(const SelArgs& a, int P, cudaStream_t st);
-cudaError_t launch_shard_thresh(const SelArgs& a, int P, cudaStream_t st);
-cudaError_t launch_shard_scan(const SelArgs& a, int P, cudaStream_t st);
 cudaError_t launch_select_split(const SelArgs& a, int P, cudaStream_t st);
 int select_chunk_tokens();
 // long-context select with hist (L <= 4096): threshold kernel (grid P) + persistent scan (nblk CTAs)
 cudaError_t launch_select_pipe(const SelArgs& a, const CUtensorMap& tmK, int nblk, cudaStream_t st);
+// sharded step: threshold from the replicated histograms (grid P) + the persistent scan over
+// the rank's local candidate range (tmK over the local codes)
+cudaError_t launch_select_shard(const SelArgs& a, const CUtensorMap& tmK, int nblk, cudaStream_t st);
 bool select_pipe_ok(int L);
 cudaError_t launch_attention(const AttnArgs& a, int P, int GT, cudaStream_t st);
-cudaError_t launch_combine(const float* parts, int R, int rows, float* out, cudaStream_t st);
+cudaError_t launch_combine(const float* parts, int R, int rows, size_t stride, float* out, cudaStream_t st);
 cudaError_t launch_prepare(const uint16_t* codebook, const float* H, float* nrm, uint16_t* chat, int Hkv, int L,
                            cudaStream_t st);
 cudaError_t launch_encode_bulk(const EncArgs& a, const CUtensorMap& tm_chat, cudaStream_t st);

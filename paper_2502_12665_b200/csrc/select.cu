@@ -20,10 +20,9 @@
 //     written in ascending order.  A token with agg == v* is kept iff fewer than
 //     m such tokens precede it: the lowest-index tie-break of reading Q12.
 //
-// The same phases serve the sequence-sharded step: shard_hist
-// (local candidate histogram), shard_thresh (v*, m from the all-reduced
-// histogram + this rank's above/at counts) and shard_scan (local emission with
-// the rank's tie quota, from the all-gathered counts).
+// The sequence-sharded step takes v*, m and this rank's tie
+// share from replicated histograms (select_shard_thresh_kernel) and then runs the
+// same persistent scan over the rank's local candidate range.
 #include "internal.cuh"
 #include "umma.cuh"
 
@@ -45,14 +44,14 @@ constexpr int kRankMax = kNT;        // survivors ranked directly (one thread ea
 // split it: kThresh (per pair: counts, v*, m, compact class table to global) then kScanC
 // (per (pair, chunk of 32768 tokens): classify, publish the chunk's counts, look back at
 // the pair's earlier chunks for the output offsets, emit).
-enum SelMode { kFused = 0, kShardHist = 1, kShardThresh = 2, kShardScan = 3, kThresh = 4, kScanC = 5 };
+enum SelMode { kFused = 0, kThresh = 4, kScanC = 5 };
 
 constexpr int kWinScratch = 32768 + 16384 + 8 * kD * 4;  // window logits scratch (threshold kernel)
 
 template <int MODE>
 struct ModeTraits {
-  static constexpr bool surv = (MODE == kFused || MODE == kShardThresh || MODE == kThresh);  // find_level
-  static constexpr bool codes = (MODE == kFused || MODE == kShardScan || MODE == kScanC);    // code chunk
+  static constexpr bool surv = (MODE == kFused || MODE == kThresh);   // find_level
+  static constexpr bool codes = (MODE == kFused || MODE == kScanC);   // code chunk
   static constexpr int extra = (MODE == kThresh) ? kWinScratch : 0;  // bytes after the survivors
   static constexpr int min_blocks = (MODE == kThresh || MODE == kScanC) ? 2 : 1;
 };
@@ -1180,6 +1179,117 @@ __global__ __launch_bounds__(kTT, 4) void select_thresh_kernel(SelArgs a) {
   A2ATS_TL(g_sel_tl, 1);
 }
 
+// ---------------------------------------------------------------- sharded step, replicated histograms
+// Collective-free exact global top-K: every rank holds the global code histogram
+// and every rank's histogram of tokens [0, n-1), plus the codes of the sinks and of the latest
+// WR tokens (the caller-visible shard state, updated identically on every rank from the step's
+// all-gather).  So every rank derives the same K-th level v* and tie quota m (the LUT is
+// bitwise identical on every rank), and its own share of the ties -- the first m tied tokens in
+// global order go to the lowest ranks first (reading Q12) -- without exchanging anything:
+//   cand_r[l] = hist_r[r][l] - #(rank r's sink / window tokens < n-1 with code l)
+//   E_before  = sum over ranks r' < rank of cand_r'[l] for the tied codes l (agg_l == v*)
+//   m_local   = clamp(m - E_before, 0, E_local),  K_eff_local = #above_local + m_local.
+// (v*, m_local, K_eff_local, E_local) and the class table feed the persistent scan over the
+// rank's local candidate range, exactly as on one GPU.  The owner of the new token n-1 also
+// copies its code (just encoded by the prep kernel) into the all-gather message.
+__device__ __forceinline__ int owner_of(const SelArgs& a, int t) {
+  int r = 0;
+  while (r + 1 < a.world && t >= a.bounds[r + 1]) ++r;
+  return r;
+}
+
+__global__ __launch_bounds__(kTT, 3) void select_shard_thresh_kernel(SelArgs a) {
+  extern __shared__ __align__(16) uint32_t sm[];
+  __shared__ SelShared S;
+  __shared__ int s_above, s_eq, s_before;
+  const int tid = threadIdx.x, lane = tid & 31, pair = blockIdx.x;
+  const int L4 = (a.L + 3) & ~3;
+  int* cnt = reinterpret_cast<int*>(sm);        // [L] global candidate counts
+  int* cnl = cnt + L4;                          // [L] this rank's candidate counts
+  uint32_t* keys = reinterpret_cast<uint32_t*>(cnl + L4);  // [L]
+  uint32_t* skey = keys + L4;
+  int* scnt = reinterpret_cast<int*>(skey + kTSurv);
+  const size_t PL = (size_t)gridDim.x * a.L;
+  // step inputs (replicated state): counts of tokens [0, n-1) minus sinks and window tokens
+  for (int l = tid; l < a.L; l += kTT) {
+    cnt[l] = a.hist_g[(size_t)pair * a.L + l];
+    cnl[l] = a.hist_r[(size_t)a.rank * PL + (size_t)pair * a.L + l];
+  }
+  if (tid == 0) s_above = s_eq = s_before = 0;
+  __syncthreads();
+  const int n = a.n_ctx, t_new = n - 1;
+  const int n_stat = a.n_s + (t_new - a.w0);  // sinks + window tokens other than the new one
+  for (int i = tid; i < n_stat; i += kTT) {
+    const int t = i < a.n_s ? i : a.w0 + (i - a.n_s);
+    const int code = i < a.n_s ? a.sinkc[(size_t)pair * a.n_sink_cap + t] : a.ring[(size_t)pair * a.WR + (t % a.WR)];
+    atomicSub(&cnt[code], 1);
+    if (owner_of(a, t) == a.rank) atomicSub(&cnl[code], 1);
+  }
+  __syncthreads();
+  int c[16];
+  load_c_regs<16>(a, cnt, c);
+  pdl_wait();  // agg from the prep kernel (and the new token's code from its encode role)
+  pdl_trigger();
+  if (a.send_codes && a.rank == a.owner && tid == 0)
+    a.send_codes[pair] = a.codes[(size_t)pair * a.n_max + (t_new - a.shard_begin)];
+  uint32_t k[16], kstar = 0u, m = 0u;
+  if (a.keff > 0) {
+    level_regs<kTT, 16>(a, S, pair, c, k, skey, scnt, kTSurv, kstar, m);
+  } else {
+    const float* aggp = a.agg + (size_t)pair * a.L;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) k[e] = tid * 16 + e < a.L ? ~ordered_key(__ldcg(aggp + tid * 16 + e)) : 0u;
+    kstar = 0u;  // no key is below 0: nothing above; ties (key 0) are not candidates
+  }
+  // this rank's counts above / at v*, the lower ranks' ties at v*, the compact class table
+  int above = 0, eq = 0, before = 0;
+  uint32_t x = 0u;
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    const int l = tid * 16 + e;
+    if (l >= a.L) break;
+    keys[l] = k[e];
+    if (a.keff == 0) continue;
+    if (k[e] < kstar) {
+      above += cnl[l];
+      x |= 1u << (2 * e);
+    } else if (k[e] == kstar) {
+      eq += cnl[l];
+      x |= 2u << (2 * e);
+      for (int r = 0; r < a.rank; ++r) before += a.hist_r[(size_t)r * PL + (size_t)pair * a.L + l];
+    }
+  }
+  if (tid < a.W) a.tblg[(size_t)pair * a.W + tid] = x;
+  above = __reduce_add_sync(0xffffffffu, above);
+  eq = __reduce_add_sync(0xffffffffu, eq);
+  before = __reduce_add_sync(0xffffffffu, before);
+  if (lane == 0) {
+    atomicAdd(&s_above, above);
+    atomicAdd(&s_eq, eq);
+    atomicAdd(&s_before, before);
+  }
+  __syncthreads();
+  // lower ranks' sink / window tokens at v* are in their histograms but are not candidates
+  if (a.keff > 0) {
+    for (int i = tid; i < n_stat; i += kTT) {
+      const int t = i < a.n_s ? i : a.w0 + (i - a.n_s);
+      const int code = i < a.n_s ? a.sinkc[(size_t)pair * a.n_sink_cap + t] : a.ring[(size_t)pair * a.WR + (t % a.WR)];
+      if (keys[code] == kstar && owner_of(a, t) < a.rank) atomicSub(&s_before, 1);
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const int e_loc = s_eq;
+    const int m_loc = a.keff > 0 ? min(max((int)m - s_before, 0), e_loc) : 0;
+    const int cap = a.keff > 0 ? s_above + m_loc : 0;
+    a.pinfo[pair * 4 + 0] = kstar;
+    a.pinfo[pair * 4 + 1] = (uint32_t)m_loc;
+    a.pinfo[pair * 4 + 2] = (uint32_t)cap;
+    a.pinfo[pair * 4 + 3] = (uint32_t)e_loc;
+    a.nsel_out[pair] = cap;
+  }
+}
+
 // Stream one unit (half of a pair's candidate stages).  Super-rounds of two stages (32768
 // tokens): thread t takes stage t >> 9, row (t & 511) >> 1 (64 tokens), half t & 1 (32
 // consecutive tokens, pieces 4 (t & 1) .. + 3, read through the SWIZZLE_128B layout:
@@ -1272,12 +1382,13 @@ __device__ __forceinline__ void scan_unit(const ScanCtx& c, int buf, int pair, i
     const uint32_t ex = pre + incl - pk;
     uint32_t gb = run_gt + (ex & 0xffffu), eb = run_eq + (ex >> 16);
     if (pk) {
+      const int te = t0 + c.a.sel_base;  // emitted index (sharded step: local -> global)
       if (FWD) {
-        if (cw[0]) emit16(cw[0], t0, gb, eb, pu.m, pu.cap, selp);
-        if (cw[1]) emit16(cw[1], t0 + 16, gb, eb, pu.m, pu.cap, selp);
+        if (cw[0]) emit16(cw[0], te, gb, eb, pu.m, pu.cap, selp);
+        if (cw[1]) emit16(cw[1], te + 16, gb, eb, pu.m, pu.cap, selp);
       } else {
-        if (cw[1]) emit16_rev(cw[1], t0 + 16, gb, eb, pu.D, pu.cap, selp);
-        if (cw[0]) emit16_rev(cw[0], t0, gb, eb, pu.D, pu.cap, selp);
+        if (cw[1]) emit16_rev(cw[1], te + 16, gb, eb, pu.D, pu.cap, selp);
+        if (cw[0]) emit16_rev(cw[0], te, gb, eb, pu.D, pu.cap, selp);
       }
     }
     run_gt += tot & 0xffffu;
@@ -1397,6 +1508,7 @@ __global__ __launch_bounds__(kPAll, 1) void select_scan_kernel(const __grid_cons
   A2ATS_TL(g_selc_tl, 1);
 }
 
+size_t shard_thresh_smem_bytes(int L) { return (size_t)((L + 3) & ~3) * 12 + 2 * kTSurv * 4; }
 size_t thresh_smem_bytes(int L) { return (size_t)((L + 3) & ~3) * 4 + 2 * kTSurv * 4; }  // cnt + survivors
 size_t scan_smem_bytes(int) { return 32768 + 65536 + (size_t)kPStage * kPRound * 2; }  // align slack + tables + ring
 
@@ -1424,65 +1536,7 @@ __device__ __forceinline__ void select_body(const SelArgs& a) {
   const int c0 = max(a.c0, lo), c1 = min(a.c1, hi);             // local part of the candidate range
   A2ATS_PHASE(g_sel_phase, 0);
 
-  if (MODE == kShardHist) {
-    load_cnt(a, pair, cnt, cp_local);
-    pdl_wait();
-    pdl_trigger();
-    for (int l = tid; l < a.L; l += kNT) {
-      a.cand_out[(size_t)pair * a.L + l] = cnt[l];
-      a.cand_keep[(size_t)pair * a.L + l] = cnt[l];
-    }
-    return;
-  }
-  if (MODE == kShardThresh) {
-    pdl_wait();
-    pdl_trigger();
-    // cnt <- all-reduced histogram; key from agg
-    for (int l = tid; l < a.L; l += kNT) cnt[l] = a.cand_in[(size_t)pair * a.L + l];
-    if (tid == 0) S.s_total = 0;
-    __syncthreads();
-    load_keys(a, S, pair, cnt, key);
-    int total = 0;
-    for (int l = tid; l < a.L; l += kNT) total += max(cnt[l], 0);
-    total = __reduce_add_sync(0xffffffffu, total);
-    if ((tid & 31) == 0) atomicAdd(&S.s_total, total);
-    __syncthreads();
-    const int keff = min(a.keff, S.s_total);
-    uint32_t kstar = 0, m = 0;
-    if (keff > 0) {
-      find_level(a, S, cnt, key, keff, skey, scnt);
-      kstar = S.s_kstar;
-      m = S.s_m;
-    }
-    // this rank's candidates above / at v*
-    int gt = 0, eq = 0;
-    if (keff > 0) {
-      for (int l = tid; l < a.L; l += kNT) {
-        const int c = a.cand_keep[(size_t)pair * a.L + l];
-        if (key[l] < kstar) gt += c;
-        else if (key[l] == kstar) eq += c;
-      }
-    }
-    gt = __reduce_add_sync(0xffffffffu, gt);
-    eq = __reduce_add_sync(0xffffffffu, eq);
-    if (tid == 0) S.s_gt = S.s_eq = 0;
-    __syncthreads();
-    if ((tid & 31) == 0) {
-      atomicAdd(&S.s_gt, gt);
-      atomicAdd(&S.s_eq, eq);
-    }
-    __syncthreads();
-    if (tid == 0) {
-      a.pinfo[pair * 4 + 0] = kstar;
-      a.pinfo[pair * 4 + 1] = m;
-      a.pinfo[pair * 4 + 2] = (uint32_t)keff;
-      a.counts_out[pair * 2 + 0] = S.s_gt;
-      a.counts_out[pair * 2 + 1] = S.s_eq;
-    }
-    return;
-  }
-
-  // kFused / kShardScan: step inputs first (overlapping the previous kernel's tail):
+  // kFused: step inputs first (overlapping the previous kernel's tail):
   // the first chunk of local candidate codes, and (fused) the candidate counts
   const int first = lo + (((c0 - lo) >> 3) << 3);
   if (c0 < c1) prefetch_chunk(a, cp_local, first, c1, sC);
@@ -1527,29 +1581,9 @@ __device__ __forceinline__ void select_body(const SelArgs& a) {
       m = S.s_m;
     }
     cap = (uint32_t)a.keff;
-  } else {
-    // shard scan: key from agg, v*/m from shard_thresh, this rank's tie quota from the gather
-    const float* aggp = a.agg + (size_t)pair * a.L;
-    for (int l = tid; l < a.L; l += kNT) key[l] = ~ordered_key(__ldcg(aggp + l));
-    kstar = a.pinfo[pair * 4 + 0];
-    const int mg = (int)a.pinfo[pair * 4 + 1];
-    const int keffg = (int)a.pinfo[pair * 4 + 2];
-    int eq_before = 0;
-    for (int r = 0; r < a.rank; ++r) eq_before += a.counts_all[((size_t)r * gridDim.x + pair) * 2 + 1];
-    const int gt_r = a.counts_all[((size_t)a.rank * gridDim.x + pair) * 2 + 0];
-    const int eq_r = a.counts_all[((size_t)a.rank * gridDim.x + pair) * 2 + 1];
-    m = keffg > 0 ? (uint32_t)min(max(mg - eq_before, 0), eq_r) : 0u;
-    cap = keffg > 0 ? (uint32_t)(gt_r + (int)m) : 0u;
-    if (keffg == 0) kstar = 0u;  // nothing above key 0 except impossible keys: emit nothing
-    if (tid == 0) a.nsel_out[pair] = (int)cap;
-    __syncthreads();
   }
   if (!regs) build_table(a, key, kstar, tbl);
   A2ATS_PHASE(g_sel_phase, 6);
-  if (MODE == kShardScan && cap == 0) {
-    cp_async_wait<0>();
-    return;
-  }
   scan_emit(a, S, tbl, cp_local, c0, c1, m, cap, selp, sC);
   A2ATS_PHASE(g_sel_phase, 7);
   if (MODE == kFused) append_hist(a, pair, cp_local);
@@ -1583,11 +1617,6 @@ cudaError_t launch_mode(const SelArgs& a, int P, cudaStream_t st) {  // P: CTAs
 
 cudaError_t launch_select(const SelArgs& a, int P, cudaStream_t st) { return launch_mode<kFused>(a, P, st); }
 
-cudaError_t launch_shard_hist(const SelArgs& a, int P, cudaStream_t st) { return launch_mode<kShardHist>(a, P, st); }
-cudaError_t launch_shard_thresh(const SelArgs& a, int P, cudaStream_t st) {
-  return launch_mode<kShardThresh>(a, P, st);
-}
-cudaError_t launch_shard_scan(const SelArgs& a, int P, cudaStream_t st) { return launch_mode<kShardScan>(a, P, st); }
 cudaError_t launch_select_split(const SelArgs& a, int P, cudaStream_t st) {
   cudaError_t e = launch_mode<kThresh>(a, P, st);
   if (e != cudaSuccess) return e;
@@ -1596,6 +1625,19 @@ cudaError_t launch_select_split(const SelArgs& a, int P, cudaStream_t st) {
 int select_chunk_tokens() { return kCH; }
 
 bool select_pipe_ok(int L) { return L <= 4096; }
+
+cudaError_t launch_select_shard(const SelArgs& a, const CUtensorMap& tmK, int nblk, cudaStream_t st) {
+  if (!select_pipe_ok(a.L)) return cudaErrorInvalidValue;
+  const int smt = (int)shard_thresh_smem_bytes(a.L);
+  const int sms = (int)scan_smem_bytes(a.W);
+  cudaError_t e = ensure_smem(select_shard_thresh_kernel, smt);
+  if (e != cudaSuccess) return e;
+  e = ensure_smem(select_scan_kernel, sms);
+  if (e != cudaSuccess) return e;
+  e = launch_pdl(select_shard_thresh_kernel, dim3(a.P), dim3(kTT), smt, st, a);
+  if (e != cudaSuccess || nblk <= 0) return e;
+  return launch_pdl(select_scan_kernel, dim3(nblk), dim3(kPAll), sms, st, tmK, a);
+}
 
 cudaError_t launch_select_pipe(const SelArgs& a, const CUtensorMap& tmK, int nblk, cudaStream_t st) {
   if (!select_pipe_ok(a.L)) return cudaErrorInvalidValue;

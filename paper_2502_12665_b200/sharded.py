@@ -1,31 +1,22 @@
-"""Sequence-sharded decode step across ranks (the paper itself is
-single-GPU).
+"""Sequence-sharded decode step across ranks (the paper
+itself is single-GPU).
 
-Rank r holds, for every (b, KV head), the contiguous global token range
-[shard_begin, shard_begin + shard_len) of the context in its own K/V/code
-arrays (local index = global index - shard_begin).  q and the codebook are
-replicated.  One decode step exchanges only small, query-dependent summaries:
-
-  1. kernels.hist       LUT (replicated, bitwise identical on every rank) and the
-                        rank's candidate histogram over codewords      [B,Hkv,L] i32
-  2. all_reduce(SUM)    -> global candidate histogram: every rank derives the same
-                        K-th level v* and tie quota m (exact global top-K,
-                        no candidate exchange)
-  3. kernels.threshold  v*, m and this rank's (#above v*, #at v*)     [B,Hkv,2] i32
-  4. all_gather         -> every rank knows how many tied tokens lower ranks hold
-                        (ties go to the lowest global token index, reading Q12)
-  5. kernels.attend     local selection + exact attention over the rank's rows of
-                        Sel -> partial (m, l, o)                        [B,Hq,130] f32
-  6. all_gather         -> kernels.combine: log-sum-exp combine in rank order
-
-Collectives go through torch.distributed (NCCL on GPUs, gloo in CPU tests);
-`kernels` is the C-ABI binding (or, in tests, any object with the same four
-methods).  Bytes exchanged per step: 4*B*Hkv*L (allreduce) + 8*B*Hkv*R +
-520*B*Hq*R, independent of the context length.
+Rank r holds, for every (b, KV head), the global tokens [bounds[r], bounds[r+1])
+in its own K/V/code arrays (local index = global index - bounds[r]); q, the
+codebook and the shard STATE are replicated.  The state -- the global code
+histogram, every rank's code histogram, the codes of the sinks and of the
+latest tokens -- lets every rank derive the exact global top-K threshold and its
+own share of the ties with no exchange (collective-free exact top-K, §8f.1).
+Each decode step is ONE call into liba2ats.so (a2ats_decode_step_sharded): a0 on
+the new token's owner, the LUT, the local selection and attention, one NCCL
+all-gather of the partials (m, l, o) and the new token's code, the log-sum-exp
+combine and the state update, all on the caller's stream (graph-capturable).
+This module holds no collectives: only the communicator bootstrap (the NCCL
+unique id travels through torch.distributed) and buffer ownership.
 """
 from __future__ import annotations
 
-from dataclasses import dataclass
+from . import binding as _b
 
 
 def shard_ranges(n_tokens: int, world: int):
@@ -39,80 +30,75 @@ def shard_ranges(n_tokens: int, world: int):
     return out
 
 
-def tie_offsets(counts_all):
-    """counts_all[r, ..., 1] = #tied candidates on rank r; returns, per rank, the
-    number of tied candidates held by lower ranks (exclusive prefix over ranks)."""
-    import torch
-    eq = counts_all[..., 1]
-    return torch.cumsum(eq, dim=0) - eq
+def step_bounds(ranges, n_ctx: int):
+    """Bounds [R+1] of a step: the prefill shards, new tokens appended to the last rank."""
+    bounds = [b for b, _ in ranges] + [max(ranges[-1][1], n_ctx)]
+    return bounds
 
 
-@dataclass
-class ShardStep:
-    """Collective orchestration of one sharded decode step."""
-    kernels: object
-    rank: int
-    world: int
-    group: object = None
+def comm_from_torch(world: int, rank: int, group=None):
+    """NCCL communicator of liba2ats.so; the 128-byte unique id is broadcast from rank 0
+    through torch.distributed (plumbing only)."""
+    import torch.distributed as dist
+    obj = [_b.a2ats_comm_unique_id() if rank == 0 else None]
+    if world > 1:
+        dist.broadcast_object_list(obj, src=0, group=group)
+    return _b.a2ats_comm_init(obj[0], world, rank)
 
-    def __call__(self, n_ctx: int, shard_begin: int, shard_len: int, q, k_local, v_local, codes_local, hist_local,
-                 out):
+
+class ShardedDecoder:
+    """One rank's buffers for the sharded step: prepared codebook terms, local codes, the
+    replicated shard state, the workspace and (world > 1) the communicator."""
+
+    def __init__(self, B, Hq, Hkv, L, n_max_local, codebook, H, params: _b.Params, world: int, rank: int,
+                 comm=None, device="cuda", stream=None):
         import torch
-        import torch.distributed as dist
-        K = self.kernels
-        cand = K.hist(n_ctx, shard_begin, shard_len, q, codes_local, hist_local)       # [B,Hkv,L] int32
-        if self.world > 1:
-            dist.all_reduce(cand, op=dist.ReduceOp.SUM, group=self.group)
-        counts = K.threshold(n_ctx, cand)                                               # [B,Hkv,2] int32
-        if self.world > 1:
-            gathered = [torch.empty_like(counts) for _ in range(self.world)]
-            dist.all_gather(gathered, counts, group=self.group)
-            counts_all = torch.stack(gathered)
-        else:
-            counts_all = counts.unsqueeze(0)
-        part = K.attend(n_ctx, shard_begin, shard_len, self.rank, self.world, counts_all, q, k_local, v_local,
-                        codes_local)                                                    # [B,Hq,130] f32
-        if self.world > 1:
-            parts = [torch.empty_like(part) for _ in range(self.world)]
-            dist.all_gather(parts, part, group=self.group)
-            parts_all = torch.stack(parts)
-        else:
-            parts_all = part.unsqueeze(0)
-        return K.combine(parts_all, out)
-
-
-class GpuShardKernels:
-    """The four per-rank steps of ShardStep on the C ABI (liba2ats.so)."""
-
-    def __init__(self, B, Hq, Hkv, L, n_max_local, codebook, params, device="cuda", stream=None):
-        import torch
-
-        from . import binding as _b
-        self._b = _b
+        self.world, self.rank, self.comm, self.stream = world, rank, comm, stream
+        self.device = torch.device(device)
         self.shape = _b.make_shape(B, Hq, Hkv, 128, L, n_max_local)
         self.params = params
-        self.codebook = codebook
-        self.stream = stream
-        self.ws = torch.zeros(_b.a2ats_shard_workspace_bytes(self.shape, params), dtype=torch.uint8, device=device)
-        self.cand = torch.empty((B, Hkv, L), dtype=torch.int32, device=device)
-        self.counts = torch.empty((B, Hkv, 2), dtype=torch.int32, device=device)
-        self.part = torch.empty((B, Hq, 130), dtype=torch.float32, device=device)
-        self.sel_out = None
+        self.codebook = codebook.contiguous()
+        self.nrm = torch.empty((Hkv, L), dtype=torch.float32, device=self.device)
+        self.chat = torch.empty((Hkv, L, 256), dtype=torch.bfloat16, device=self.device)
+        _b.a2ats_qavq_prepare(self.shape, self.codebook, None if H is None else H.contiguous().float(), self.nrm,
+                              self.chat, stream)
+        self.codes = torch.zeros((B, Hkv, n_max_local), dtype=torch.uint16, device=self.device)
+        self.state = torch.zeros(_b.a2ats_shard_state_bytes(self.shape, params, world), dtype=torch.uint8,
+                                 device=self.device)
+        self.ws = torch.zeros(_b.a2ats_shard_workspace_bytes(self.shape, params, world), dtype=torch.uint8,
+                              device=self.device)
+        self.ws_enc = torch.zeros(_b.a2ats_build_codes_workspace_bytes(self.shape), dtype=torch.uint8,
+                                  device=self.device)
 
-    def hist(self, n_ctx, sb, sl, q, codes_local, hist_local):
-        self._b.a2ats_shard_hist(self.shape, self.params, n_ctx, sb, sl, q, codes_local, self.codebook, hist_local,
-                                 self.cand, self.ws, self.stream)
-        return self.cand
+    def encode(self, k_local, t_begin: int, t_end: int):
+        """a0 for local tokens [t_begin, t_end) (prefill of this rank's shard)."""
+        _b.a2ats_build_codes(self.shape, k_local, t_begin, t_end, self.chat, self.nrm, self.codes, None, self.ws_enc,
+                             self.stream)
 
-    def threshold(self, n_ctx, cand_global):
-        self._b.a2ats_shard_threshold(self.shape, self.params, n_ctx, cand_global, self.counts, self.ws, self.stream)
-        return self.counts
+    def build_state(self, bounds, n_tokens: int):
+        """Replicated state of tokens [0, n_tokens) (NCCL all-reduces inside the library)."""
+        _b.a2ats_shard_state_build(self.shape, self.params, self.world, self.rank, bounds, n_tokens, self.codes,
+                                   self.state, self.ws, self.comm, self.stream)
 
-    def attend(self, n_ctx, sb, sl, rank, world, counts_all, q, k_local, v_local, codes_local):
-        self._b.a2ats_shard_attend(self.shape, self.params, n_ctx, sb, sl, rank, world, counts_all.contiguous(), q,
-                                   k_local, v_local, codes_local, self.part, self.sel_out, self.ws, self.stream)
-        return self.part
-
-    def combine(self, parts_all, out):
-        self._b.a2ats_combine(self.shape, parts_all.shape[0], parts_all.contiguous(), out, self.stream)
+    def step(self, n_ctx: int, bounds, q, k_local, v_local, out, sel_out=None):
+        """One decode step (token n_ctx - 1 already in its owner's K/V cache)."""
+        _b.a2ats_decode_step_sharded(self.shape, self.params, n_ctx, self.world, self.rank, bounds, q, k_local,
+                                     v_local, self.codes, self.codebook, self.chat, self.nrm, self.state, out,
+                                     sel_out, self.ws, self.comm, self.stream)
         return out
+
+    # the two halves around the all-gather (single-process rank simulation in tests)
+    def partial(self, n_ctx: int, bounds, q, k_local, v_local, msg, sel_out=None):
+        _b.a2ats_shard_step_partial(self.shape, self.params, n_ctx, self.world, self.rank, bounds, q, k_local,
+                                    v_local, self.codes, self.codebook, self.chat, self.nrm, self.state, msg, sel_out,
+                                    self.ws, self.stream)
+
+    def finish(self, n_ctx: int, bounds, msgs, out):
+        _b.a2ats_shard_step_finish(self.shape, self.params, n_ctx, self.world, bounds, msgs, self.state, out,
+                                   self.stream)
+        return out
+
+    def close(self):
+        if self.comm is not None:
+            _b.a2ats_comm_destroy(self.comm)
+            self.comm = None

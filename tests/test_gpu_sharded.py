@@ -1,105 +1,183 @@
-"""GPU parity of the sequence-sharded decode step on one device:
-R ranks are simulated in one process (each with its own local K/V/code arrays
-and workspace); the collectives are replaced by their definitions (sum of the
-candidate histograms, stacking of counts / partials).  The union of the
-per-rank selections must equal the oracle's top-K exactly and the combined
-output must meet the 2e-3 tolerance."""
+"""GPU parity of the sequence-sharded decode step on one device.
+
+R ranks are simulated in one process through the two halves of the C entry point
+a2ats_decode_step_sharded (a2ats_shard_step_partial / a2ats_shard_step_finish):
+every rank has its own local K/V/code arrays, workspace and replicated state; the
+step's single collective (all-gather of the messages) is replaced by its definition
+(stacking), and the prefill state build's all-reduce by the sum of the ranks'
+contributions.  Checked against the fp64 oracle: the union of the ranks' selections
+equals the oracle's top-K exactly (ties across ranks included), every rank's output is
+the same and within 2e-3 of the oracle, the new token's code (a0 on its owner) equals
+the oracle's, and the state after several steps equals the state built from scratch.
+"""
 import numpy as np
 import pytest
 import torch
 
 from helpers import OUT_RTOL, codes_np, f64, pair_oracle, redraw_for_gap, rel_l2
+from oracle import a2ats_oracle as O
 from synth import Config, make_inputs
 
 pytestmark = pytest.mark.gpu
 
 if torch.cuda.is_available():
     import paper_2502_12665_b200 as A
-    from paper_2502_12665_b200.sharded import GpuShardKernels, shard_ranges
+    from paper_2502_12665_b200 import binding as Bd
+    from paper_2502_12665_b200.sharded import ShardedDecoder, shard_ranges, step_bounds
 
 
-def run_sharded(cfg, inp, ranges, use_hist=True):
-    dev = "cuda"
+def state_views(dec):
+    lay = Bd.a2ats_shard_state_layout(dec.shape, dec.params, dec.world)
+    P = dec.shape.B * dec.shape.Hkv
+    L = dec.shape.L
+    st = dec.state
+    hg = st[lay["hist_g"]:lay["hist_g"] + P * L * 4].view(torch.int32)
+    hr = st[lay["hist_r"]:lay["hist_r"] + dec.world * P * L * 4].view(torch.int32)
+    ring = st[lay["ring"]:lay["ring"] + P * lay["WR"] * 2].view(torch.int16)
+    sk = st[lay["sinkc"]:lay["sinkc"] + P * lay["n_sink_cap"] * 2].view(torch.int16)
+    return [hg, hr, ring, sk]
+
+
+def make_ranks(cfg, inp, ranges, n_pre, extra):
     R = len(ranges)
-    n_loc = max(e - b for b, e in ranges)
-    n_loc = (n_loc + 7) // 8 * 8
+    n_loc = max(e - b for b, e in ranges) + extra
+    n_loc = (n_loc + 63) // 64 * 64
     params = A.Params(window=cfg.window, bridge=cfg.bridge, n_sink=cfg.n_sink, topk=cfg.K)
-    q = inp["q"].to(dev)
-    C = inp["codebook"].to(dev)
+    C = inp["codebook"].cuda()
     ranks = []
     for r, (b0, e0) in enumerate(ranges):
+        e_all = e0 + (extra if r == R - 1 else 0)
+
         def local(t):
             x = torch.zeros((cfg.B, cfg.Hkv, n_loc) + tuple(t.shape[3:]), dtype=t.dtype)
-            x[:, :, :e0 - b0] = t[:, :, b0:e0]
-            return x.to(dev)
-        codes = local(inp["codes"])
-        hist = None
-        if use_hist:
-            c = codes[:, :, :min(e0, cfg.N) - b0].to(torch.int64)
-            hist = torch.zeros((cfg.B, cfg.Hkv, cfg.L), dtype=torch.int32, device=dev)
-            hist.scatter_add_(2, c, torch.ones_like(c, dtype=torch.int32))
-        kern = GpuShardKernels(cfg.B, cfg.Hq, cfg.Hkv, cfg.L, n_loc, C, params)
-        kern.sel_out = torch.full((cfg.B, cfg.Hkv, max(cfg.K, 1)), -1, dtype=torch.int32, device=dev)
-        ranks.append(dict(b=b0, e=e0, codes=codes, hist=hist, k=local(inp["k_cache"]), v=local(inp["v_cache"]),
-                          kern=kern))
-    cands = [rk["kern"].hist(cfg.N, rk["b"], rk["e"] - rk["b"], q, rk["codes"], rk["hist"]).clone() for rk in ranks]
-    glob = torch.stack(cands).sum(0).to(torch.int32)                       # all_reduce(SUM)
-    counts = torch.stack([rk["kern"].threshold(cfg.N, glob).clone() for rk in ranks])   # all_gather
-    parts = []
+            x[:, :, :e_all - b0] = t[:, :, b0:e_all]
+            return x.cuda()
+        dec = ShardedDecoder(cfg.B, cfg.Hq, cfg.Hkv, cfg.L, n_loc, C, None, params, R, r)
+        lc = local(inp["codes"])
+        lc[:, :, max(0, n_pre - b0):] = 0           # tokens >= n_pre are encoded by the steps (a0)
+        dec.codes.copy_(lc)
+        ranks.append(dict(dec=dec, b=b0, k=local(inp["k_cache"]), v=local(inp["v_cache"])))
+    # prefill state: the all-reduce of the ranks' contributions, by definition
+    bounds0 = step_bounds(ranges, n_pre)
+    for rk in ranks:
+        rk["dec"].build_state(bounds0, n_pre)
+    torch.cuda.synchronize()
+    views = [state_views(rk["dec"]) for rk in ranks]
+    summed = [sum(v[i].to(torch.int64) for v in views) for i in range(4)]
+    for v in views:
+        for i in range(4):
+            v[i].copy_(summed[i].to(v[i].dtype))
+    return ranks
+
+
+def sharded_step(cfg, ranks, ranges, n_ctx, q):
+    R = len(ranks)
+    bounds = step_bounds(ranges, n_ctx)
+    msg_f = Bd.a2ats_shard_msg_bytes(ranks[0]["dec"].shape) // 4
+    msgs = torch.empty((R, msg_f), dtype=torch.float32, device="cuda")
     sels = []
     for r, rk in enumerate(ranks):
-        parts.append(rk["kern"].attend(cfg.N, rk["b"], rk["e"] - rk["b"], r, R, counts, q, rk["k"], rk["v"],
-                                       rk["codes"]).clone())
-        torch.cuda.synchronize()
-        ns = int(counts[r, :, :, 0].max())  # upper bound; the real per-pair count is read back below
-        sels.append(rk["kern"].sel_out.cpu().numpy())
-    out = torch.empty((cfg.B, cfg.Hq, 128), device=dev)
-    ranks[0]["kern"].combine(torch.stack(parts), out)                     # all_gather + LSE combine
+        sel = torch.full((cfg.B, cfg.Hkv, max(cfg.K, 1)), -1, dtype=torch.int32, device="cuda")
+        rk["dec"].partial(n_ctx, bounds, q, rk["k"], rk["v"], msgs[r], sel_out=sel)
+        sels.append(sel)
+    outs = []
+    for rk in ranks:
+        out = torch.empty((cfg.B, cfg.Hq, 128), device="cuda")
+        rk["dec"].finish(n_ctx, bounds, msgs, out)
+        outs.append(out)
     torch.cuda.synchronize()
-    return out.cpu().numpy(), sels, counts.cpu().numpy()
+    return [o.cpu().numpy() for o in outs], [s.cpu().numpy() for s in sels]
 
 
-def check(cfg, inp, ranges, use_hist=True):
-    out, sels, counts = run_sharded(cfg, inp, ranges, use_hist)
+def check_step(cfg, inp, outs, sels, n_ctx, ref_codes):
+    for o in outs[1:]:
+        np.testing.assert_array_equal(o, outs[0])     # every rank holds the same combined output
     G = cfg.Hq // cfg.Hkv
     C = f64(inp["codebook"])
-    codes = codes_np(inp["codes"])
     for b in range(cfg.B):
         for h in range(cfg.Hkv):
             r = pair_oracle(f64(inp["q"][b, h * G:(h + 1) * G]), f64(inp["k_cache"][b, h]),
-                            f64(inp["v_cache"][b, h]), codes[b, h], C[h], cfg.N, cfg)
-            got = []
-            # per-rank count = above + min(max(m - eq_before, 0), eq): recompute from the emitted -1-padded list
-            for s in sels:
-                row = s[b, h]
-                got.extend(int(x) for x in row if x >= 0)
-            np.testing.assert_array_equal(np.sort(got), r["sel"], err_msg=f"pair {(b, h)}")
+                            f64(inp["v_cache"][b, h]), ref_codes[b, h], C[h], n_ctx, cfg.with_(N=n_ctx))
+            got = sorted(int(x) for s in sels for x in s[b, h] if x >= 0)
+            np.testing.assert_array_equal(got, r["sel"], err_msg=f"pair {(b, h)} at n = {n_ctx}")
             for g in range(G):
-                e = rel_l2(out[b, h * G + g], r["out"][g])
+                e = rel_l2(outs[0][b, h * G + g], r["out"][g])
                 assert e <= OUT_RTOL, (b, h, g, e)
 
 
-SH = Config("shard", B=2, Hq=8, Hkv=2, d=128, N=20001, L=1000, K=1200)
+def run_case(cfg, inp, ranges, steps=1):
+    """Prefill [0, N - steps), then `steps` sharded decode steps ending at n = N."""
+    N = cfg.N
+    n_pre = N - steps
+    ranks = make_ranks(cfg, inp, ranges, n_pre, extra=steps + 8)
+    ref_codes = codes_np(inp["codes"]).copy()
+    keys = f64(inp["k_cache"])
+    for s in range(steps):
+        n = n_pre + s + 1
+        for b in range(cfg.B):                        # the oracle's code of the new token (a0, Eq. 14)
+            for h in range(cfg.Hkv):
+                ref_codes[b, h, n - 1] = O.qavq_encode(keys[b, h, n - 1:n], f64(inp["codebook"])[h])[0]
+        outs, sels = sharded_step(cfg, ranks, ranges, n, inp["q"].cuda())
+        own = ranks[-1]
+        got = own["dec"].codes[:, :, n - 1 - own["b"]].cpu().to(torch.int64).numpy()
+        np.testing.assert_array_equal(got, ref_codes[:, :, n - 1])   # a0 on the owner == the oracle
+        check_step(cfg, inp, outs, sels, n, ref_codes)
+    # the state after the steps == the state of the final codes (the ranks' codes are the oracle's)
+    views = [state_views(rk["dec"]) for rk in ranks]
+    for v in views[1:]:
+        for i in range(4):
+            assert torch.equal(v[i], views[0][i])
+    P = cfg.B * cfg.Hkv
+    hg = views[0][0].view(P, cfg.L).cpu().numpy()
+    want = np.stack([np.bincount(ref_codes[b, h, :N], minlength=cfg.L) for b in range(cfg.B) for h in range(cfg.Hkv)])
+    np.testing.assert_array_equal(hg, want)
+    hr = views[0][1].view(len(ranges), P, cfg.L).cpu().numpy()
+    bounds = step_bounds(ranges, N)
+    for r in range(len(ranges)):
+        want_r = np.stack([np.bincount(ref_codes[b, h, bounds[r]:bounds[r + 1]], minlength=cfg.L)
+                           for b in range(cfg.B) for h in range(cfg.Hkv)])
+        np.testing.assert_array_equal(hr[r], want_r)
 
 
-@pytest.mark.parametrize("R", [2, 3, 4])
+SH = Config("shard", B=2, Hq=8, Hkv=2, d=128, N=40001, L=1000, K=2400)
+
+
+def prepared(cfg, seed, **kw):
+    inp = make_inputs(cfg, seed, device="cpu", with_h=False, **kw)
+    inp["codes"] = inp["z"].to(torch.uint16)
+    return inp
+
+
+@pytest.mark.parametrize("R", [1, 2, 3, 4])
 def test_sharded_matches_oracle(R):
-    inp = make_inputs(SH, 201 + R, device="cpu", with_h=False)
-    inp["codes"] = inp["z"].to(torch.uint16)
+    inp = prepared(SH, 201 + R)
     redraw_for_gap(inp, SH, SH.N, 201 + R)
-    check(SH, inp, shard_ranges(SH.N, R))
+    run_case(SH, inp, shard_ranges(SH.N - 1, R))
 
 
-def test_sharded_integer_ties_across_ranks_no_hist():
+def test_sharded_three_steps_state_update():
+    inp = prepared(SH, 231)
+    for n in (SH.N - 2, SH.N - 1, SH.N):
+        redraw_for_gap(inp, SH.with_(N=n), n, 231 + n)
+    run_case(SH, inp, shard_ranges(SH.N - 3, 3), steps=3)
+
+
+def test_sharded_integer_ties_across_ranks():
     cfg = SH.with_(L=300, K=5000, bridge=0)
-    inp = make_inputs(cfg, 211, device="cpu", family="g1", code_dist="zipf", with_h=False)
-    inp["codes"] = inp["z"].to(torch.uint16)
-    check(cfg, inp, shard_ranges(cfg.N, 3), use_hist=False)
+    inp = prepared(cfg, 211, family="g1", code_dist="zipf")
+    run_case(cfg, inp, shard_ranges(cfg.N - 1, 3))
 
 
 def test_sharded_window_and_sinks_straddle_ranks():
-    inp = make_inputs(SH, 221, device="cpu", with_h=False)
-    inp["codes"] = inp["z"].to(torch.uint16)
+    inp = prepared(SH, 221)
     redraw_for_gap(inp, SH, SH.N, 221)
     N = SH.N
-    check(SH, inp, [(0, 2), (2, N - 30), (N - 30, N)])
+    run_case(SH, inp, [(0, 2), (2, N - 31), (N - 31, N - 1)])
+
+
+def test_sharded_rank_without_candidates():
+    """A middle rank holding only a few tokens (and one holding none)."""
+    inp = prepared(SH, 241)
+    redraw_for_gap(inp, SH, SH.N, 241)
+    N = SH.N
+    run_case(SH, inp, [(0, 20000), (20000, 20000), (20000, 20010), (20010, N - 1)])
