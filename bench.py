@@ -1,13 +1,18 @@
 #!/usr/bin/env python
 """Benchmark of the B200-native A^2ATS decode-time retrieval path.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl a2ats|reference] [--config C2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl a2ats|reference] [--config C4]
 
 One "step" = one decode step of the whole hot path over the batch: a0 (encode
-the new token's key and update the code histogram) + a1..a6
-(a2ats_decode_step: WRoPE query, LUT, code scan + exact top-K, sparse
-attention, LSE combine), through the C ABI of liba2ats.so.  The context grows
-by one token per step (a real decode loop) and ends at the config's N.
+the new token's key and update the code histogram) + a1..a6 (WRoPE query,
+LUT, code scan + exact top-K, sparse attention, LSE combine), through the C
+ABI of liba2ats.so.  The context grows by one token per step (a real decode
+loop) and ends at the config's N.  Default workload: BASELINE.json configs[3]
+(C4: Llama-3.1-8B shapes, 128K context, batch 64) -- the configuration the
+north star's 70 % target is stated on.  N = 1: a2ats_decode_step_append on
+one GPU; N > 1 (torchrun): the sequence-sharded step a2ats_decode_step_sharded
+(one C call per step on each rank, NCCL all-gather inside the library), total
+work fixed ("scaling": "strong").
 
 Metric (BASELINE.json): approx-scored tokens/s = sum over steps of B*Hkv*n_ctx
 (every cached token is scored once per KV head; the G query heads of a group
@@ -55,7 +60,7 @@ class ClockSampler:
         0x100: "display_clock_setting",
     }
 
-    def __init__(self, index: int, period_s: float = 0.005):
+    def __init__(self, index: int, period_s: float = 0.0005):
         self.samples, self.reasons, self.ok = [], set(), False
         self.period, self._stop = period_s, threading.Event()
         try:
@@ -121,6 +126,20 @@ def stage_model(cfg, n_ctx: int, k: int):
         "attention": dict(bytes=P * M * d * 2 * 2 + P * keff * 4 + B * Hq * d * (2 + 4 + 4),
                           flops=4 * B * Hq * M * d, bound="hbm", rows=P * M),
     }
+
+
+def measured_traffic(cfg, kernel: str):
+    """DRAM bytes (read + written) per launch of `kernel` from the ncu --set full capture of THIS
+    workload (profiles/ncu_traffic_<workload>.json, written by tools/ncu_summarize.py with the
+    workload's shape); None when no capture of the same workload and shape exists."""
+    path = os.path.join(ROOT, "profiles", f"ncu_traffic_{cfg.name}.json")
+    try:
+        t = json.load(open(path))
+    except Exception:
+        return None
+    if t.get("workload") != cfg.name or t.get("B") != cfg.B or t.get("N") != cfg.N or t.get("L") != cfg.L:
+        return None
+    return t.get("per_launch", {}).get(kernel)
 
 
 def scoring_line(cfg, r, pk):
@@ -429,42 +448,62 @@ def run_e2e(steps, dec, cfg, kc, vc, q, n_start, A, budget_k, use_graph, world, 
                          "writes the output into pinned host memory"}
 
 
-def oracle_sample(cfg, seconds_budget: float = 15.0, max_pairs: int = 64):
-    """Times the fp64 oracle (as it stands) on whole (b, kv-head) pairs of the
-    workload: same N, L, G, budget; per-pair work identical to the GPU arm."""
+_PAIR = {}
+
+
+def _oracle_init(name, seed):
+    """Worker initializer: one (b, kv-head) pair of the workload as fp64 arrays (untimed), one
+    BLAS thread per worker process."""
     import numpy as np
-    import torch
 
-    from oracle import a2ats_oracle as O
-    from synth import budget_k, make_inputs
-
+    from synth import CONFIGS, make_inputs
     try:
         from threadpoolctl import threadpool_limits
-        limiter = threadpool_limits(1)
+        threadpool_limits(1)
     except Exception:
-        limiter = None
+        pass
+    cfg = CONFIGS[name]
     G = cfg.Hq // cfg.Hkv
-    one = cfg.with_(B=1, Hq=G, Hkv=1)
-    inp = make_inputs(one, SEED + 99, device="cpu", with_h=False)
-    qg = inp["q"][0].double().numpy()
-    k = inp["k_cache"][0, 0].double().numpy()
-    v = inp["v_cache"][0, 0].double().numpy()
-    codes = inp["z"][0, 0].numpy().astype(np.int64)
-    C = inp["codebook"][0].double().numpy()
-    K = budget_k(cfg.N)
-    pairs, t_total = 0, 0.0
-    while pairs < max_pairs and (t_total < seconds_budget or pairs == 0):
-        t0 = time.perf_counter()
-        O.decode_step_pair(qg, k, v, codes, C, cfg.N, window=cfg.window, bridge=cfg.bridge, n_sink=cfg.n_sink, topk=K)
-        t_total += time.perf_counter() - t0
-        pairs += 1
-    if limiter is not None:
-        limiter.unregister() if hasattr(limiter, "unregister") else None
-    value = pairs * cfg.N / t_total
-    return dict(value=value, unit=UNIT, cores=1, kind="oracle",
-                sample=f"{pairs} (b, kv-head) pairs of {cfg.name} (N={cfg.N}, L={cfg.L}, G={G}, K={K}), "
-                       f"fp64 numpy oracle, 1 thread, {t_total:.1f} s; tokens/s = pairs*N/time",
-                cpu=platform.processor() or _cpu_model(), seconds=t_total)
+    inp = make_inputs(cfg.with_(B=1, Hq=G, Hkv=1), seed + os.getpid() % 97, device="cpu", with_h=False)
+    _PAIR.update(cfg=cfg, q=inp["q"][0].double().numpy(), k=inp["k_cache"][0, 0].double().numpy(),
+                 v=inp["v_cache"][0, 0].double().numpy(), codes=inp["z"][0, 0].numpy().astype(np.int64),
+                 C=inp["codebook"][0].double().numpy())
+
+
+def _oracle_pair(_job):
+    """One pair through the fp64 oracle (a1..a6 given the codes); returns (t_start, t_end) on
+    the system-wide monotonic clock."""
+    from oracle import a2ats_oracle as O
+    from synth import budget_k
+    c = _PAIR["cfg"]
+    t0 = time.perf_counter()
+    O.decode_step_pair(_PAIR["q"], _PAIR["k"], _PAIR["v"], _PAIR["codes"], _PAIR["C"], c.N, window=c.window,
+                       bridge=c.bridge, n_sink=c.n_sink, topk=budget_k(c.N))
+    return t0, time.perf_counter()
+
+
+def oracle_sample(cfg, seconds_budget: float = 20.0, threads: int | None = None):
+    """Times the fp64 oracle, as it stands, on whole (b, kv-head) pairs of the workload (same N,
+    L, G, budget as the GPU arm) on the box's host cores: T = `threads` worker processes (default
+    all cores), one BLAS thread each, pairs in parallel (inputs generated untimed per worker);
+    tokens/s = pairs * N / (last end - first start), and the single-thread rate (T = 1) from the
+    per-pair times.  Bounded: about `seconds_budget` of oracle time."""
+    import multiprocessing as mp
+    T = threads or os.cpu_count() or 1
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(T, initializer=_oracle_init, initargs=(cfg.name, SEED + 99)) as pool:
+        warm = pool.map(_oracle_pair, range(T), chunksize=1)             # every worker runs one pair first
+        t1 = max(b - a for a, b in warm)
+        rounds = max(1, int(seconds_budget / max(t1, 1e-3)))
+        spans = pool.map(_oracle_pair, range(T * rounds), chunksize=1)
+    wall = max(b for _, b in spans) - min(a for a, _ in spans)
+    value = len(spans) * cfg.N / wall
+    value1 = cfg.N / (sum(b - a for a, b in spans) / len(spans))
+    return dict(value=value, unit=UNIT, cores=T, kind="oracle",
+                sample=f"{len(spans)} (b, kv-head) pairs of {cfg.name} (N={cfg.N}, L={cfg.L}, G={cfg.Hq // cfg.Hkv}, "
+                       f"K={cfg.K}) through the fp64 numpy oracle (a1-a6 given the codes), {T} worker processes x 1 "
+                       f"BLAS thread, {wall:.1f} s of oracle wall time; tokens/s = pairs*N/wall",
+                value_1_thread=value1, cpu=_cpu_model(), seconds=wall)
 
 
 def _cpu_model():
@@ -478,26 +517,33 @@ def _cpu_model():
 
 
 def run_reference(args):
+    """The reference arm of this tier = the fp64 oracle as it stands, on the host cores: each
+    step is a bounded sample (one pair per worker process) of the same workload."""
+    import multiprocessing as mp
     from synth import CONFIGS
     cfg = CONFIGS[args.config]
-    per_step = []
+    T = os.cpu_count() or 1
     t_all = time.perf_counter()
-    for s in range(args.warmup + args.steps):
-        r = oracle_sample(cfg, seconds_budget=args.ref_seconds, max_pairs=1)
-        if s >= args.warmup:
-            per_step.append(r)
-    tot = sum(r["seconds"] for r in per_step)
-    tokens = len(per_step) * cfg.N
-    value = tokens / tot
+    ctx = mp.get_context("spawn")
+    walls = []
+    with ctx.Pool(T, initializer=_oracle_init, initargs=(cfg.name, SEED + 7)) as pool:
+        for s in range(args.warmup + args.steps):
+            spans = pool.map(_oracle_pair, range(T), chunksize=1)
+            if s >= args.warmup:
+                walls.append(max(b for _, b in spans) - min(a for a, _ in spans))
+    tot = sum(walls)
+    value = len(walls) * T * cfg.N / tot
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(per_step),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(walls),
+        "higher_is_better": True, "scaling": "strong" if args.gpus > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
         "config": {"workload": cfg.name, "note": cfg.note, "B": cfg.B, "Hq": cfg.Hq, "Hkv": cfg.Hkv, "d": cfg.d,
                    "N": cfg.N, "L": cfg.L, "K": cfg.K},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                         "sample": f"each step = 1 (b, kv-head) pair of {cfg.name} through the fp64 numpy oracle "
-                                   f"(a1-a6 given codes), 1 thread; tokens/s = N/time"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": T, "kind": "oracle", "cpu": _cpu_model(),
+                         "sample": f"each step = {T} (b, kv-head) pairs of {cfg.name} through the fp64 numpy oracle "
+                                   f"(a1-a6 given codes), one per worker process ({T} processes x 1 BLAS thread); "
+                                   f"tokens/s = pairs*N/wall"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "wall_s": time.perf_counter() - t_all,
     }
@@ -505,15 +551,17 @@ def run_reference(args):
 
 
 def run_sharded(args, rank: int, world: int):
-    """Sequence-sharded step: every rank holds a contiguous token range of every
-    (b, KV head) sequence; q and the codebook are replicated.  One step = the new token's
-    code on its owner rank + ShardStep (LUT + local candidate histogram, all-reduce, threshold,
-    all-gather of tie counts, local selection + attention, all-gather of partials, LSE
-    combine).  Total work is fixed as N grows: strong scaling."""
+    """Sequence-sharded step: rank r holds a contiguous token range of every
+    (b, KV head) sequence; q, the codebook and the shard state are replicated.  One step = ONE
+    call of a2ats_decode_step_sharded per rank: a0 for the new token on its owner (the last
+    rank), the LUT, the collective-free global top-K from the replicated histograms, the local
+    scan and attention, one NCCL all-gather (partials + the new code) inside the library, the
+    LSE combine and the state update.  Each step is one CUDA-graph replay.  Total work is the
+    fixed C4 job as N grows: strong scaling."""
     import torch
 
     import paper_2502_12665_b200 as A
-    from paper_2502_12665_b200.sharded import GpuShardKernels, ShardStep, shard_ranges
+    from paper_2502_12665_b200.sharded import ShardedDecoder, comm_from_torch, shard_ranges, step_bounds
     from synth import CONFIGS, budget_k, make_inputs
 
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -522,58 +570,210 @@ def run_sharded(args, rank: int, world: int):
     cfg = CONFIGS[args.config]
     if args.batch:
         cfg = cfg.with_(B=args.batch)
-    steps_total = args.warmup + args.steps
-    N0 = cfg.N - steps_total                       # context before the first step; the last has N
-    lo, hi = shard_ranges(N0, world)[rank]
-    own_new = rank == world - 1                    # new tokens join the last rank's shard
-    cap = (hi - lo) + (steps_total + 8 if own_new else 0)
-    cap = (cap + 7) // 8 * 8
+    e2e_steps = max(3, args.steps // 2)
+    steps_total = 1 + args.warmup + 2 * args.steps + e2e_steps   # eager + graphs + profiling pass + e2e
+    n0 = cfg.N - (1 + args.warmup + args.steps)                 # the last timed step has n = N
+    ranges = shard_ranges(n0, world)
+    lo, hi = ranges[rank]
+    last = rank == world - 1                                   # new tokens join the last rank
+    cap = (hi - lo) + (steps_total + 8 if last else 0)
+    cap = (cap + 63) // 64 * 64
     rep = make_inputs(cfg.with_(N=8), SEED, device=dev, with_h=True)          # replicated q, C, H
-    loc = make_inputs(cfg.with_(N=cap), SEED + 1 + rank, device=dev, with_h=False, n_max=cap)  # local K/V
-    params = A.Params(topk=budget_k(cfg.N))
-    kern = GpuShardKernels(cfg.B, cfg.Hq, cfg.Hkv, cfg.L, cap, rep["codebook"], params, device=dev)
-    dec = A.Decoder(cfg.B, cfg.Hq, cfg.Hkv, cfg.L, cap, rep["codebook"], rep["H"], params, device=dev)
-    kc, vc = loc["k_cache"], loc["v_cache"]
-    dec.encode(kc, 0, hi - lo)                     # local codes + local histogram (untimed)
-    step = ShardStep(kern, rank, world)
+    loc = make_inputs(cfg.with_(N=min(cap, cfg.N)), SEED + 1 + rank, device=dev, with_h=False, n_max=cap,
+                      codebook=rep["codebook"])
+    kc, vc, q = loc["k_cache"], loc["v_cache"], rep["q"]
+    del loc
+    params = A.Params(topk=budget_k(cfg.N + steps_total))
+    comm = comm_from_torch(world, rank)                        # NCCL (also at N = 1: the all-gather runs)
+    dec = ShardedDecoder(cfg.B, cfg.Hq, cfg.Hkv, cfg.L, cap, rep["codebook"], rep["H"], params, world, rank, comm,
+                         device=dev)
+    dec.encode(kc, 0, hi - lo)                                 # local prefill codes (a0, untimed)
+    dec.build_state(step_bounds(ranges, n0), n0)               # replicated state (NCCL all-reduces, untimed)
     out = torch.empty((cfg.B, cfg.Hq, cfg.d), dtype=torch.float32, device=dev)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
     torch.cuda.synchronize()
 
-    def one(s):
-        n = N0 + s + 1
-        sl = (hi - lo) + (s + 1 if own_new else 0)
-        if own_new:                                # a0 for the new token, on its owner
-            dec.encode(kc, sl - 1, sl)
+    def one(n, o=None):
         params.topk = budget_k(n)
-        step(n, lo, sl, rep["q"], kc, vc, dec.codes, dec.hist, out)
+        dec.step(n, step_bounds(ranges, n), q, kc, vc, out if o is None else o)
 
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    n = n0 + 1
+    one(n)                                                     # eager: one-time attributes, NCCL warm-up
+    torch.cuda.synchronize()
+    graphs, ns = [], []
+    use_graph = not args.no_graph
+    for s in range(args.warmup + args.steps):
+        n += 1
+        ns.append(n)
+        if use_graph:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                one(n)
+            graphs.append(g)
+    torch.cuda.synchronize()
+
+    def run(s):
+        if use_graph:
+            graphs[s].replay()
+        else:
+            one(ns[s])
+
     for s in range(args.warmup):
         flush.fill_(1.0)
-        one(s)
+        run(s)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    stream = torch.cuda.current_stream()
     tokens = 0
     with ClockSampler(local) as clk:
         for k in range(args.steps):
             s = args.warmup + k
-            flush.fill_(float(k))
-            evs[k][0].record()
-            one(s)
-            evs[k][1].record()
-            tokens += cfg.B * cfg.Hkv * (N0 + s + 1)   # whole-job tokens scored per step (all ranks)
+            if not args.no_flush:
+                flush.fill_(float(k))
+            evs[k][0].record(stream)
+            run(s)
+            evs[k][1].record(stream)
+            tokens += cfg.B * cfg.Hkv * ns[s]                  # whole-job tokens scored per step (all ranks)
         torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
     total_ms = sum(a.elapsed_time(b) for a, b in evs)
+    del graphs
+    # profiling pass (eager, stage events: PDL edges serialised): per-stage device times on this rank
+    names = ["prep", "select", "attention", "exchange+combine"]
+    stage_ms = {nm: [] for nm in names}
+    for k in range(args.steps):
+        n += 1
+        if not args.no_flush:
+            flush.fill_(float(k))
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        for e in ev:
+            e.record()
+        torch.cuda.synchronize()
+        A.a2ats_set_stage_events(ev)
+        one(n)
+        A.a2ats_set_stage_events(None)
+        torch.cuda.synchronize()
+        for i, nm in enumerate(names):
+            stage_ms[nm].append(ev[i].elapsed_time(ev[i + 1]))
+    e2e = run_e2e_sharded(e2e_steps, dec, cfg, kc, vc, q, n, ranges, rank, world, lo, A, budget_k, use_graph, dev)
     if world > 1:
         t = torch.tensor([total_ms], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
         torch.distributed.barrier()
+    dec.close()
     return dict(value=tokens / (total_ms / 1e3), ms_per_step=total_ms / args.steps, clocks=clk.summary(), cfg=cfg,
-                lo=lo, hi=hi)
+                lo=lo, hi=hi, stage_ms={k: statistics.mean(v) for k, v in stage_ms.items()}, e2e=e2e,
+                n_last=ns[args.warmup + args.steps - 1], graph=use_graph, ranges=ranges)
+
+
+def run_e2e_sharded(steps, dec, cfg, kc, vc, q, n_start, ranges, rank, world, lo, A, budget_k, use_graph, dev):
+    """The sharded step through the public API with HOST buffers: every step stages q (every
+    rank) and the new token's K/V rows (owner) from pinned host memory (a2ats_stage_rows, one
+    kernel reading the mapped buffers) and the combine writes the output into pinned host
+    memory; CUDA events around the whole loop, max over ranks."""
+    import torch
+
+    from paper_2502_12665_b200.sharded import step_bounds
+    last = rank == world - 1
+    q_host = q.detach().cpu().pin_memory()
+    k_host = [kc[:, :, n_start - lo + s].contiguous().cpu().pin_memory() for s in range(steps)] if last else None
+    v_host = [vc[:, :, n_start - lo + s].contiguous().cpu().pin_memory() for s in range(steps)] if last else None
+    out_host = torch.empty((cfg.B, cfg.Hq, cfg.d), dtype=torch.float32).pin_memory()
+    q_dev = torch.empty_like(q)
+
+    def one(s):
+        n = n_start + s + 1
+        A.a2ats_stage_rows(dec.shape, n - lo if last else 1, q_host, k_host[s] if last else None,
+                           v_host[s] if last else None, q_dev, kc, vc)
+        dec.params.topk = budget_k(n)
+        dec.step(n, step_bounds(ranges, n), q_dev, kc, vc, out_host)
+
+    graphs = []
+    if use_graph:
+        for s in range(steps):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                one(s)
+            graphs.append(g)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    tokens = 0
+    ev0.record()
+    for s in range(steps):
+        if use_graph:
+            graphs[s].replay()
+        else:
+            one(s)
+        tokens += cfg.B * cfg.Hkv * (n_start + s + 1)
+    ev1.record()
+    ev1.synchronize()
+    tot = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([tot], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        tot = float(t.item())
+    h2d = q_host.numel() * 2 + (k_host[0].numel() * 2 * 2 if last else 0)
+    d2h = out_host.numel() * 4
+    return {"value": tokens / (tot / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "ms_per_step": tot / steps, "steps": steps, "l2": "not flushed (back-to-back steps)",
+            "transfers": "a2ats_stage_rows reads pinned host q (every rank) and the new K/V rows (owner) over "
+                         "PCIe; the combine writes the output into pinned host memory (rank 0's bytes counted)"}
+
+
+def sharded_line(args, r, world):
+    from synth import budget_k
+    pk = peaks()
+    cfg = r["cfg"]
+    n = r["n_last"]
+    k = budget_k(n)
+    lo, hi = r["lo"], r["hi"]
+    P = cfg.B * cfg.Hkv
+    # rank 0's rows of Sel: its sinks and its share of the top-K (about K * its share of the candidates)
+    share = max(0, min(hi, n - cfg.window) - max(lo, cfg.n_sink)) / max(1, n - cfg.window - cfg.n_sink)
+    rows = P * (min(cfg.n_sink, hi) + k * share + (cfg.window if hi >= n - 1 else 0))
+    att_bytes = rows * cfg.d * 2 * 2 + P * k * share * 4
+    att_ms = r["stage_ms"]["attention"]
+    ach = att_bytes / (att_ms * 1e-3) / 1e9 if att_ms > 0 else None
+    roof = {"bound": "hbm", "achieved": ach, "peak": pk["hbm"], "unit": "GB/s",
+            "frac": (ach / pk["hbm"]) if ach else None, "traffic": measured_traffic(cfg, "attention"),
+            "kernel": "attention (rank 0, its rows of Sel)", "peak_source": pk["source"]}
+    launches = 7 + (1 if cfg.B * (cfg.Hq // cfg.Hkv) > 64 else 0)
+    return {
+        "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": cfg.name, "note": cfg.note, "B": cfg.B, "Hq": cfg.Hq, "Hkv": cfg.Hkv, "d": cfg.d,
+                   "N_final": n, "L": cfg.L, "K_final": k,
+                   "parallelism": f"sequence-sharded x{world} (a2ats_decode_step_sharded: replicated code "
+                                  f"histograms, one NCCL all-gather of partials + new code per step)",
+                   "shards_at_prefill": r["ranges"],
+                   "l2": "flushed between steps (256 MB write, outside the timed events)" if not args.no_flush
+                   else "not flushed",
+                   "launch": "one CUDA graph per step (replay)" if r["graph"] else "eager launches"},
+        "roofline": roof,
+        "kernels_rank0_ms": r["stage_ms"],
+        "cpu_baseline": None if world > 1 else _cpu_baseline_or_error(cfg, args),
+        "cpu_baseline_note": "measured at N = 1 only (the base contract); see the N = 1 line" if world > 1 else None,
+        "e2e": r["e2e"],
+        "gpu_launches": launches * args.steps,
+        "clocks": r["clocks"],
+    }
+
+
+def _cpu_baseline_or_error(cfg, args):
+    if args.no_cpu_baseline:
+        return None
+    try:
+        return oracle_sample(cfg)
+    except Exception as e:  # never let the baseline kill the line
+        return {"error": repr(e)}
 
 
 def main():
@@ -582,17 +782,15 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="a2ats", choices=["a2ats", "reference", "ours"])
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C4")
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=2.0)
     ap.add_argument("--sharded", action="store_true",
-                    help="sequence-sharded step over the ranks (SURVEY 8e; default config C4, strong scaling)")
+                    help="the sequence-sharded step also at N = 1 (always used at N > 1)")
     args = ap.parse_args()
-    if args.sharded and args.config == "C2":
-        args.config = "C4"
     args.warmup = max(args.warmup, 3)
 
     rank = int(os.environ.get("RANK", "0"))
@@ -606,19 +804,11 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
         dist.init_process_group("nccl")
-    if args.sharded:
+    from synth import CONFIGS
+    if (args.sharded or world > 1) and not getattr(CONFIGS[args.config], "kv_host", False):
         r = run_sharded(args, rank, world)
         if rank == 0:
-            print(json.dumps({
-                "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-                "config": {"workload": r["cfg"].name + "-sharded", "B": r["cfg"].B, "Hq": r["cfg"].Hq,
-                           "Hkv": r["cfg"].Hkv, "N_final": r["cfg"].N, "L": r["cfg"].L,
-                           "parallelism": f"sequence-sharded x{world} (NCCL all-reduce of code histograms, "
-                                          f"all-gather of tie counts and partials)",
-                           "l2": "flushed between steps (256 MB write, outside the timed events)"},
-                "clocks": r["clocks"]}))
+            print(json.dumps(sharded_line(args, r, world)))
         return
     from synth import CONFIGS
     if getattr(CONFIGS[args.config], "kv_host", False):
@@ -657,13 +847,7 @@ def main():
                        "frac_hbm": (gbs / pk["hbm"]) if gbs else None, "flops": m["flops"],
                        "TFLOPs": m["flops"] / (ms * 1e-3) / 1e12 if ms > 0 else None}
     dom = max(("attention", "select", "prep"), key=lambda k: r["stage_ms"][k])
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get(dom)
-        except Exception:
-            traffic = None
+    traffic = measured_traffic(cfg, dom)
     if model[dom]["bound"] == "alu":
         # FMA-bound LUT: peak = 148 SMs x 128 FP32 lanes x 2 flop x clock
         sm_mhz = r["clocks"]["sm_mhz"] or pk["sm_max"]
@@ -675,12 +859,7 @@ def main():
         ach = kernels[dom]["GBps"]
         roof = {"bound": "hbm", "achieved": ach, "peak": pk["hbm"], "unit": "GB/s", "frac": ach / pk["hbm"],
                 "traffic": traffic, "kernel": dom, "peak_source": pk["source"]}
-    cpu = None
-    if not args.no_cpu_baseline and world >= 1:
-        try:
-            cpu = oracle_sample(cfg, seconds_budget=15.0)
-        except Exception as e:  # never let the baseline kill the line
-            cpu = {"error": repr(e)}
+    cpu = _cpu_baseline_or_error(cfg, args)
     # prep (encode + LUT + window logits) + select + attention; qprep for wide query tiles
     # (B*G > 64); long contexts with hist: threshold + scan kernels
     n_last = r["n_last"]

@@ -352,7 +352,7 @@ def a2ats_decode_step_sharded(shape, params, n_ctx, world, rank, bounds, q, k_ca
         ctypes.byref(shape), ctypes.byref(p), int(n_ctx), int(world), int(rank), _bounds(bounds),
         _ptr(q, "q", torch.bfloat16), _ptr(k_cache, "k_cache", torch.bfloat16), _ptr(v_cache, "v_cache", torch.bfloat16),
         _ptr(codes, "codes", torch.uint16), _ptr(codebook, "codebook", torch.bfloat16), _ptr(chat, "chat", torch.bfloat16),
-        _ptr(nrm, "nrm", torch.float32), _ptr(state, "state"), _ptr(out, "out", torch.float32),
+        _ptr(nrm, "nrm", torch.float32), _ptr(state, "state"), _ptr(out, "out", torch.float32, host_ok="pinned"),
         _ptr(sel_out, "sel_out", torch.int32, optional=True), _ptr(ws, "ws"), ws.numel() * ws.element_size(), comm,
         _stream(stream))
     _check("a2ats_decode_step_sharded", rc)

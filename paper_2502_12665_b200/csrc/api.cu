@@ -989,7 +989,7 @@ int shard_common(const a2ats_shape* shape, const a2ats_params* params, int32_t n
 int shard_partial(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx, int32_t world, int32_t rank,
                   const int32_t* bounds, const void* q, const void* k_cache, const void* v_cache, uint16_t* codes,
                   const void* codebook, const void* chat, const float* nrm, const void* state, float* msg,
-                  int32_t* sel_out, void* ws, size_t ws_bytes, cudaStream_t st) {
+                  int32_t* sel_out, void* ws, size_t ws_bytes, cudaStream_t st, float* out_direct = nullptr) {
   int rc = shard_common(shape, params, n_ctx, world, rank, bounds);
   if (rc) return rc;
   if (!q || !k_cache || !v_cache || !codes || !codebook || !chat || !nrm || !state || !msg) return A2ATS_EINVAL;
@@ -1024,6 +1024,7 @@ int shard_partial(const a2ats_shape* shape, const a2ats_params* params, int32_t 
   const int w_lo = std::max(d.w0, lo), w_hi = std::min(n_ctx, hi);
   prep_set_window(p, shape, k_cache, wlog, n_ctx, w_lo, std::max(0, w_hi - w_lo), lo);
   const int n_wl = p.n_wl;
+  p.n_win = 0;  // the window-row logits are computed by the threshold kernel before its wait
   CUtensorMap tmA, tmC;
   rc = cuda_status(make_tmap_sw128(&tmA, codebook, (uint64_t)shape->Hkv * shape->L, kD, 128));
   if (rc) return rc;
@@ -1099,6 +1100,17 @@ int shard_partial(const a2ats_shape* shape, const a2ats_params* params, int32_t 
   sa.c0 = lc1 > lc0 ? lc0 - lo : 0;
   sa.c1 = lc1 > lc0 ? lc1 - lo : 0;
   sa.sel_base = lo;
+  if (n_wl > 0) {  // this rank's window rows: logits in the threshold kernel's prologue
+    sa.wlog = wlog;
+    sa.q = static_cast<const uint16_t*>(q);
+    sa.kc = static_cast<const uint16_t*>(k_cache);
+    sa.Hq = shape->Hq;
+    sa.G = d.G;
+    sa.n_wl = n_wl;
+    sa.win_lo = w_lo;
+    sa.scale_log2 = kScaleLog2;
+    sa.rt = la.rt;
+  }
   const int nblk = (lc1 > lc0 && d.keff > 0) ? std::min(sm_count(), 2 * d.P) : 0;
   CUtensorMap tmK;
   rc = cuda_status(make_tmap_codes(&tmK, codes, (uint64_t)d.P, (uint64_t)shape->n_max));
@@ -1121,8 +1133,8 @@ int shard_partial(const a2ats_shape* shape, const a2ats_params* params, int32_t 
   aa.nsel = nsel;
   aa.part = reinterpret_cast<float*>(base + Lw.part);
   aa.counter = reinterpret_cast<unsigned int*>(base + Lw.actr);
-  aa.out = nullptr;
-  aa.part_out = msg;
+  aa.out = out_direct;  // one rank: the normalised output directly (no combine)
+  aa.part_out = out_direct ? nullptr : msg;
   aa.Hq = shape->Hq;
   aa.Hkv = shape->Hkv;
   aa.G = d.G;
@@ -1148,12 +1160,14 @@ int shard_partial(const a2ats_shape* shape, const a2ats_params* params, int32_t 
 
 // phase B: LSE combine of the world's partials in rank order + the state update
 int shard_finish(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx, int32_t world,
-                 const int32_t* bounds, const float* msgs, void* state, float* out, cudaStream_t st) {
+                 const int32_t* bounds, const float* msgs, void* state, float* out, cudaStream_t st,
+                 bool combine = true) {
   const ShardState S = state_layout(shape, params, world);
   const int owner = owner_of_host(bounds, world, n_ctx - 1);
   const size_t mf = msg_floats(shape);
   const int P = shape->B * shape->Hkv;
-  int rc = cuda_status(launch_combine(msgs, world, shape->B * shape->Hq, mf, out, st));
+  int rc = A2ATS_OK;
+  if (combine) rc = cuda_status(launch_combine(msgs, world, shape->B * shape->Hq, mf, out, st));
   if (rc) return rc;
   uint8_t* sb = static_cast<uint8_t*>(state);
   rc = cuda_status(launch_pdl(shard_state_update_kernel, dim3((P + 255) / 256), dim3(256), 0, st, msgs, mf,
@@ -1195,15 +1209,16 @@ int a2ats_decode_step_sharded(const a2ats_shape* shape, const a2ats_params* para
   int rc = shard_common(shape, params, n_ctx, world, rank, bounds);
   if (rc) return rc;
   if (!out) return A2ATS_EINVAL;
-  if (world > 1 && (!comm || comm->world != world || comm->rank != rank)) return A2ATS_EINVAL;
-  if (world > 1 && !nccl().ok) return A2ATS_ENCCL;
+  if ((world > 1 && !comm) || (comm && (comm->world != world || comm->rank != rank))) return A2ATS_EINVAL;
+  if (comm && !nccl().ok) return A2ATS_ENCCL;
   const ShardWs W = shard_ws_layout(shape, params, world);
   if (!ws || ws_bytes < W.total) return A2ATS_EWORKSPACE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   float* msg = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + W.msg);
   float* recv = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + W.recv);
+  // one rank: the attention writes the normalised output itself; only the state update follows
   rc = shard_partial(shape, params, n_ctx, world, rank, bounds, q, k_cache, v_cache, codes, codebook, chat, nrm,
-                     state, msg, sel_out, ws, ws_bytes, st);
+                     state, msg, sel_out, ws, ws_bytes, st, world == 1 ? out : nullptr);
   if (rc) return rc;
   const size_t mf = msg_floats(shape);
   if (world > 1) {  // the step's only collective: every rank's partial and the new token's code
@@ -1211,7 +1226,7 @@ int a2ats_decode_step_sharded(const a2ats_shape* shape, const a2ats_params* para
   } else {
     recv = msg;
   }
-  return shard_finish(shape, params, n_ctx, world, bounds, recv, state, out, st);
+  return shard_finish(shape, params, n_ctx, world, bounds, recv, state, out, st, world > 1);
 }
 
 int a2ats_combine(const a2ats_shape* shape, int32_t nparts, const float* partials, float* out, void* stream) {

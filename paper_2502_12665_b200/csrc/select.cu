@@ -1198,18 +1198,23 @@ __device__ __forceinline__ int owner_of(const SelArgs& a, int t) {
   return r;
 }
 
-__global__ __launch_bounds__(kTT, 3) void select_shard_thresh_kernel(SelArgs a) {
+__global__ __launch_bounds__(kTT, 4) void select_shard_thresh_kernel(SelArgs a) {
   extern __shared__ __align__(16) uint32_t sm[];
   __shared__ SelShared S;
   __shared__ int s_above, s_eq, s_before;
   const int tid = threadIdx.x, lane = tid & 31, pair = blockIdx.x;
   const int L4 = (a.L + 3) & ~3;
-  int* cnt = reinterpret_cast<int*>(sm);        // [L] global candidate counts
+  int* cnt = reinterpret_cast<int*>(sm);        // [L] global candidate counts (registers after load_c_regs)
   int* cnl = cnt + L4;                          // [L] this rank's candidate counts
-  uint32_t* keys = reinterpret_cast<uint32_t*>(cnl + L4);  // [L]
-  uint32_t* skey = keys + L4;
+  uint32_t* keys = reinterpret_cast<uint32_t*>(cnt);  // [L] keys, once cnt is dead
+  uint32_t* skey = reinterpret_cast<uint32_t*>(cnl + L4);
   int* scnt = reinterpret_cast<int*>(skey + kTSurv);
   const size_t PL = (size_t)gridDim.x * a.L;
+  float wacc[512 / kTT];
+  if (a.wlog) {  // this rank's window-row logits (step inputs only; scratch aliases the counts)
+    window_logits<kTT>(a, pair, reinterpret_cast<uint8_t*>(sm), wacc);
+    __syncthreads();
+  }
   // step inputs (replicated state): counts of tokens [0, n-1) minus sinks and window tokens
   for (int l = tid; l < a.L; l += kTT) {
     cnt[l] = a.hist_g[(size_t)pair * a.L + l];
@@ -1228,8 +1233,10 @@ __global__ __launch_bounds__(kTT, 3) void select_shard_thresh_kernel(SelArgs a) 
   __syncthreads();
   int c[16];
   load_c_regs<16>(a, cnt, c);
+  __syncthreads();  // cnt is dead: its space holds the keys below
   pdl_wait();  // agg from the prep kernel (and the new token's code from its encode role)
   pdl_trigger();
+  if (a.wlog) store_window_logits<kTT>(a, pair, wacc);  // the previous step's attention has read wlog
   if (a.send_codes && a.rank == a.owner && tid == 0)
     a.send_codes[pair] = a.codes[(size_t)pair * a.n_max + (t_new - a.shard_begin)];
   uint32_t k[16], kstar = 0u, m = 0u;
@@ -1241,22 +1248,26 @@ __global__ __launch_bounds__(kTT, 3) void select_shard_thresh_kernel(SelArgs a) 
     for (int e = 0; e < 16; ++e) k[e] = tid * 16 + e < a.L ? ~ordered_key(__ldcg(aggp + tid * 16 + e)) : 0u;
     kstar = 0u;  // no key is below 0: nothing above; ties (key 0) are not candidates
   }
-  // this rank's counts above / at v*, the lower ranks' ties at v*, the compact class table
-  int above = 0, eq = 0, before = 0;
+  // the compact class table (this thread's 16 codewords = word tid) and the keys into smem
   uint32_t x = 0u;
 #pragma unroll
   for (int e = 0; e < 16; ++e) {
     const int l = tid * 16 + e;
-    if (l >= a.L) break;
-    keys[l] = k[e];
-    if (a.keff == 0) continue;
-    if (k[e] < kstar) {
-      above += cnl[l];
-      x |= 1u << (2 * e);
-    } else if (k[e] == kstar) {
-      eq += cnl[l];
-      x |= 2u << (2 * e);
-      for (int r = 0; r < a.rank; ++r) before += a.hist_r[(size_t)r * PL + (size_t)pair * a.L + l];
+    if (l < a.L) keys[l] = k[e];
+    if (a.keff > 0) x |= ((k[e] < kstar) ? 1u : ((k[e] == kstar) ? 2u : 0u)) << (2 * e);
+  }
+  __syncthreads();
+  // this rank's counts above / at v* and the lower ranks' ties at v*
+  int above = 0, eq = 0, before = 0;
+  if (a.keff > 0) {
+    for (int l = tid; l < a.L; l += kTT) {
+      const uint32_t kl = keys[l];
+      if (kl < kstar) {
+        above += cnl[l];
+      } else if (kl == kstar) {
+        eq += cnl[l];
+        for (int r = 0; r < a.rank; ++r) before += a.hist_r[(size_t)r * PL + (size_t)pair * a.L + l];
+      }
     }
   }
   if (tid < a.W) a.tblg[(size_t)pair * a.W + tid] = x;
@@ -1508,7 +1519,7 @@ __global__ __launch_bounds__(kPAll, 1) void select_scan_kernel(const __grid_cons
   A2ATS_TL(g_selc_tl, 1);
 }
 
-size_t shard_thresh_smem_bytes(int L) { return (size_t)((L + 3) & ~3) * 12 + 2 * kTSurv * 4; }
+size_t shard_thresh_smem_bytes(int L) { return (size_t)((L + 3) & ~3) * 8 + 2 * kTSurv * 4; }
 size_t thresh_smem_bytes(int L) { return (size_t)((L + 3) & ~3) * 4 + 2 * kTSurv * 4; }  // cnt + survivors
 size_t scan_smem_bytes(int) { return 32768 + 65536 + (size_t)kPStage * kPRound * 2; }  // align slack + tables + ring
 
@@ -1628,7 +1639,7 @@ bool select_pipe_ok(int L) { return L <= 4096; }
 
 cudaError_t launch_select_shard(const SelArgs& a, const CUtensorMap& tmK, int nblk, cudaStream_t st) {
   if (!select_pipe_ok(a.L)) return cudaErrorInvalidValue;
-  const int smt = (int)shard_thresh_smem_bytes(a.L);
+  const int smt = (int)std::max(shard_thresh_smem_bytes(a.L), a.wlog ? (size_t)kWinScratch : (size_t)0);
   const int sms = (int)scan_smem_bytes(a.W);
   cudaError_t e = ensure_smem(select_shard_thresh_kernel, smt);
   if (e != cudaSuccess) return e;

@@ -62,13 +62,16 @@ def make_codes(B: int, Hkv: int, n: int, L: int, dist: str, g: torch.Generator, 
 
 
 def make_inputs(cfg, seed: int, device="cpu", family: str = "g2", code_dist: str = "uniform",
-                n_max: int | None = None, with_h: bool = True, n_needles: int = 4) -> dict:
+                n_max: int | None = None, with_h: bool = True, n_needles: int = 4, codebook=None) -> dict:
     """All boundary inputs for one config.  Keys/values are drawn for n_max
-    tokens (>= cfg.N) so appended decode steps have rows to read."""
+    tokens (>= cfg.N) so appended decode steps have rows to read.  codebook: a given
+    (replicated) codebook the keys cluster around instead of a fresh draw (sharded runs)."""
     device = torch.device(device)
     g = _gen(seed, device)
     n_max = cfg.n_max() if n_max is None else n_max
     C = make_codebook(cfg.Hkv, cfg.L, cfg.d, family, g, device)
+    if codebook is not None:
+        C = codebook.to(device)
     q = make_query(cfg.B, cfg.Hq, cfg.d, family, g, device)
     z = make_codes(cfg.B, cfg.Hkv, n_max, cfg.L, code_dist, g, device)
     k = torch.empty((cfg.B, cfg.Hkv, n_max, cfg.d), dtype=BF16, device=device)

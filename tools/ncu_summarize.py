@@ -1,12 +1,15 @@
 """Summarise ncu captures into profiles/ (tracked).
 
-    python tools/ncu_summarize.py --rep gpurun_out/prof.ncu-rep --launches gpurun_out/launches.csv --tag r1
+    python tools/ncu_summarize.py --rep gpurun_out/prof.ncu-rep --launches gpurun_out/launches.csv --tag r2 \
+        --workload C4
 
 Writes profiles/ncu_<tag>_full.csv (one row per profiled kernel: duration,
 DRAM bytes, throughputs, tensor-pipe activity, registers, occupancy),
 profiles/ncu_<tag>_launches.csv (per-kernel mean device time and share of the
-step from the gpu__time_duration launch list) and profiles/ncu_traffic.json
-(DRAM bytes per launch by bench stage, read by bench.py's roofline.traffic).
+step from the gpu__time_duration launch list) and, with --workload,
+profiles/ncu_traffic_<workload>.json: DRAM bytes (read + written, each scaled by
+its own unit) per launch of each kernel and of each bench stage, keyed by the
+workload's shape -- bench.py's roofline.traffic reads it only for that workload.
 """
 import argparse
 import csv
@@ -18,7 +21,8 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-STAGE = [("attn", "attention"), ("select_kernel", "select"), ("select_thresh", "select"), ("select_scan", "select"), ("prep_kernel", "prep"), ("lut_umma", "lut"), ("qprep", "prep"),
+STAGE = [("attn", "attention"), ("select_kernel", "select"), ("select_thresh", "select"), ("select_shard", "select"),
+         ("select_scan", "select"), ("prep_kernel", "prep"), ("lut_fma", "prep"), ("qprep", "prep"),
          ("encode_cw", "encode"), ("encode_kernel", "encode"), ("keyh", "encode_keyh")]
 # prefill (encode_bulk_kernel, prepare_kernel) runs before the timed steps: not a path stage
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
@@ -43,7 +47,7 @@ def stage_of(name):
     return None
 
 
-def full(rep, tag):
+def full(rep, tag, workload=None):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units = rows[0], rows[1]
@@ -59,12 +63,13 @@ def full(rep, tag):
             except ValueError:
                 d[m] = v
         res.append(d)
-        st = stage_of(r[ki])
-        if st and "dram__bytes_read.sum" in d:
-            unit_r = units[idx["dram__bytes_read.sum"]]
-            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit_r, 1)
-            rw = (d["dram__bytes_read.sum"] + d.get("dram__bytes_write.sum", 0.0)) * scale
-            traffic.setdefault(st, []).append(rw)
+        if "dram__bytes_read.sum" in d:
+            def scaled(m):
+                if m not in idx or not isinstance(d.get(m), float):
+                    return 0.0
+                return d[m] * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(units[idx[m]], 1)
+            rw = scaled("dram__bytes_read.sum") + scaled("dram__bytes_write.sum")
+            traffic.setdefault(d["kernel"], []).append(rw)
     path = os.path.join(ROOT, "profiles", f"ncu_{tag}_full.csv")
     with open(path, "w", newline="") as f:
         w = csv.DictWriter(f, fieldnames=["kernel"] + [m for m in METRICS if m in idx])
@@ -74,10 +79,20 @@ def full(rep, tag):
     units_line = {m: units[i] for m, i in idx.items()}
     with open(path.replace(".csv", "_units.json"), "w") as f:
         json.dump(units_line, f, indent=1)
-    tj = {k: sum(v) / len(v) for k, v in traffic.items()}
-    with open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w") as f:
-        json.dump(dict(tj, _source=f"ncu --set full, {os.path.basename(rep)}, bytes read+written per launch"), f,
-                  indent=1)
+    per_kernel = {k: sum(v) / len(v) for k, v in traffic.items()}
+    if workload:
+        from synth import CONFIGS  # noqa: E402
+        cfg = CONFIGS[workload]
+        per_stage = {}
+        for k, v in per_kernel.items():
+            st = stage_of(k)
+            if st:
+                per_stage[st] = per_stage.get(st, 0.0) + v
+        out = dict(workload=cfg.name, B=cfg.B, N=cfg.N, L=cfg.L, per_launch=dict(per_kernel, **per_stage),
+                   _source=f"ncu --set full, {os.path.basename(rep)}: dram__bytes_read.sum + dram__bytes_write.sum "
+                           f"per launch (each in its own unit); stages sum their kernels' launches of one step")
+        with open(os.path.join(ROOT, "profiles", f"ncu_traffic_{cfg.name}.json"), "w") as f:
+            json.dump(out, f, indent=1)
     print(path)
 
 
@@ -104,9 +119,11 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--rep")
     ap.add_argument("--launches")
-    ap.add_argument("--tag", default="r1")
+    ap.add_argument("--tag", default="r2")
+    ap.add_argument("--workload", default=None, help="config name (C2, C4, ...) the capture ran")
     a = ap.parse_args()
+    sys.path.insert(0, ROOT)
     if a.rep:
-        full(a.rep, a.tag)
+        full(a.rep, a.tag, a.workload)
     if a.launches:
         launches(a.launches, a.tag)
