@@ -323,6 +323,34 @@ int a2ats_shard_step_finish(const a2ats_shape* shape, const a2ats_params* params
 int a2ats_combine(const a2ats_shape* shape, int32_t nparts, const float* partials, float* out, void* stream);
 
 /* ---------------------------------------------------------------------
+ * a2ats_qavq_train -- OFFLINE query-aware codebook construction for one KV
+ * head (§4.2):
+ *   H = (1/m) sum_i q_i^T q_i over the m post-PE queries (Eq. 10)
+ *       + eps * tr(H)/d * I (reading Q27; eps = 0: none), or H_in, or I
+ *       (queries == H_in == NULL: conventional VQ, Eq. 4);
+ *   H = L L^T (Cholesky), z = k L (Eq. 16);
+ *   k-means++ on z with the caller's uniform draws u[0..L-1] in
+ *       [0, 1): centre 0 = z[floor(u_0 n)], centre j = the first point whose
+ *       running sum of D^2 exceeds u_j * sum D^2 (reading Q28);
+ *   Lloyd on z: assignment argmin_j ||z - c^z_j||^2 (lowest j on ties),
+ *       centroid = mean of its points, an empty cluster keeps its centre
+ *       (reading Q29), until no assignment changes or max_iters (Eq. 18);
+ *   C = C^z L^{-1} (Eq. 19).
+ * keys [n_keys, d] bf16, queries [m_queries, d] bf16 (or NULL), H_in [d, d]
+ * fp64 (or NULL), u [L] fp64, C_out [L, d] fp64, H_out [d, d] fp64 (optional),
+ * labels_out [n_keys] int32 (optional), info_out int32[2] = {iterations run,
+ * Cholesky failure flag} (optional): all DEVICE pointers.  d <= 128,
+ * 1 <= L <= n_keys.  Computed in fp64 with fixed-order sums (deterministic);
+ * asynchronous on `stream`, no host synchronisation.  ws: a2ats_qavq_train_
+ * workspace_bytes.  Errors: A2ATS_EINVAL, A2ATS_EWORKSPACE, A2ATS_ECUDA.
+ * ------------------------------------------------------------------- */
+size_t a2ats_qavq_train_workspace_bytes(int32_t n_keys, int32_t d, int32_t L, int32_t m_queries);
+int a2ats_qavq_train(int32_t n_keys, int32_t d, int32_t L, const void* keys, int32_t m_queries, const void* queries,
+                     const double* H_in, double eps, const double* u, int32_t max_iters, double* C_out,
+                     double* H_out, int32_t* labels_out, int32_t* info_out, void* ws, size_t ws_bytes,
+                     void* stream);
+
+/* ---------------------------------------------------------------------
  * a2ats_set_stage_events -- optional instrumentation for benchmarks.
  *
  * events: host array of n cudaEvent_t handles (passed as void*), or NULL to

@@ -386,3 +386,42 @@ def a2ats_combine(shape, nparts, partials, out, stream=None):
     rc = load().a2ats_combine(ctypes.byref(shape), int(nparts), _ptr(partials, "partials", torch.float32),
                               _ptr(out, "out", torch.float32), _stream(stream))
     _check("a2ats_combine", rc)
+
+
+# ------------------------------------------------------------------ offline codebook construction
+_SIGS.update({
+    "a2ats_qavq_train_workspace_bytes": (_SZ, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]),
+    "a2ats_qavq_train": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _VP, ctypes.c_int32, _VP, _VP,
+                                        ctypes.c_double, _VP, ctypes.c_int32, _VP, _VP, _VP, _VP, _VP, _SZ, _VP]),
+})
+if _lib is not None:
+    for _n in ("a2ats_qavq_train_workspace_bytes", "a2ats_qavq_train"):
+        _f = getattr(_lib, _n)
+        _f.restype, _f.argtypes = _SIGS[_n]
+
+
+def a2ats_qavq_train_workspace_bytes(n_keys: int, d: int, L: int, m_queries: int = 0) -> int:
+    return int(load().a2ats_qavq_train_workspace_bytes(int(n_keys), int(d), int(L), int(m_queries)))
+
+
+def a2ats_qavq_train(keys, L: int, u, max_iters: int, queries=None, H_in=None, eps: float = 0.0, C_out=None,
+                     H_out=None, labels_out=None, info_out=None, ws=None, stream=None):
+    """Offline QAVQ codebook of one KV head (device tensors); returns C_out [L, d] fp64."""
+    import torch
+    n, d = keys.shape
+    m = 0 if queries is None else queries.shape[0]
+    dev = keys.device
+    if C_out is None:
+        C_out = torch.empty((L, d), dtype=torch.float64, device=dev)
+    if ws is None:
+        ws = torch.empty(a2ats_qavq_train_workspace_bytes(n, d, L, m), dtype=torch.uint8, device=dev)
+    rc = load().a2ats_qavq_train(int(n), int(d), int(L), _ptr(keys, "keys", torch.bfloat16), int(m),
+                                 _ptr(queries, "queries", torch.bfloat16, optional=True),
+                                 _ptr(H_in, "H_in", torch.float64, optional=True), float(eps),
+                                 _ptr(u, "u", torch.float64), int(max_iters), _ptr(C_out, "C_out", torch.float64),
+                                 _ptr(H_out, "H_out", torch.float64, optional=True),
+                                 _ptr(labels_out, "labels_out", torch.int32, optional=True),
+                                 _ptr(info_out, "info_out", torch.int32, optional=True), _ptr(ws, "ws"),
+                                 ws.numel() * ws.element_size(), _stream(stream))
+    _check("a2ats_qavq_train", rc)
+    return C_out

@@ -21,7 +21,7 @@ LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "liba2ats.so")
 OBJDIR = os.path.join(ROOT, "build", "obj")
 
-SOURCES = ["api.cu", "prep.cu", "select.cu", "attention.cu", "encode.cu"]
+SOURCES = ["api.cu", "prep.cu", "select.cu", "attention.cu", "encode.cu", "train.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
               "--expt-relaxed-constexpr", "-Xptxas", "-v"]

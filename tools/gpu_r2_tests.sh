@@ -1,4 +1,3 @@
-# Round-2: sharded-step GPU tests + full GPU suite
+# Round-2: codebook-construction GPU tests
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_sharded.py -x -q -m gpu > gpurun_out/pytest_sharded.log 2>&1
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_codebook.py -x -q -m gpu > gpurun_out/pytest_cb.log 2>&1
