@@ -246,6 +246,32 @@ int a2ats_decode_step_append(const a2ats_shape* shape, const a2ats_params* param
                              void* ws, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------
+ * Posting-list (inverted-index) selection.  A token's
+ * approximate score is its code's (Eq. 21), so the top-K set is
+ * the union of the token lists of the codes above v* plus the first m
+ * tokens (lowest index, reading Q12) of the tied codes' lists: the selection
+ * reads about K list entries per pair instead of every code.  The index is
+ * query-independent: a2ats_postings_build groups the tokens [0, n_tokens) of
+ * every pair by code (postings: a2ats_postings_bytes of device memory =
+ * int32 offsets [B*Hkv, L+1] then int32 tokens [B*Hkv, n_max], caller-owned);
+ * tokens [n_post, n_ctx) not yet in the index are classified from codes.
+ * a2ats_select_topk_postings / a2ats_decode_step_postings = a2ats_select_topk /
+ * a2ats_decode_step with that selection (hist required, L <= 4096, 0 <= n_post
+ * <= n_ctx; the results are identical: same sets, same order).
+ * ------------------------------------------------------------------- */
+size_t a2ats_postings_bytes(const a2ats_shape* shape);
+int a2ats_postings_build(const a2ats_shape* shape, const uint16_t* codes, int32_t n_tokens, void* postings,
+                         void* stream);
+int a2ats_select_topk_postings(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx, const void* q,
+                               const uint16_t* codes, const void* codebook, const int32_t* hist,
+                               const void* postings, int32_t n_post, int32_t* sel_out, void* ws, size_t ws_bytes,
+                               void* stream);
+int a2ats_decode_step_postings(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx, const void* q,
+                               const void* k_cache, const void* v_cache, const uint16_t* codes,
+                               const void* codebook, const int32_t* hist, const void* postings, int32_t n_post,
+                               float* out, int32_t* sel_out, void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------
  * Sequence-sharded decode step (the paper itself
  * is single-GPU).  R <= 8 ranks, one process per GPU.  Rank r holds,
  * for every (b, KV head), the global tokens [bounds[r], bounds[r+1]) of the

@@ -425,3 +425,56 @@ def a2ats_qavq_train(keys, L: int, u, max_iters: int, queries=None, H_in=None, e
                                  ws.numel() * ws.element_size(), _stream(stream))
     _check("a2ats_qavq_train", rc)
     return C_out
+
+
+# ------------------------------------------------------------------ posting-list selection
+_SIGS.update({
+    "a2ats_postings_bytes": (_SZ, [_SP]),
+    "a2ats_postings_build": (ctypes.c_int, [_SP, _VP, ctypes.c_int32, _VP, _VP]),
+    "a2ats_select_topk_postings": (ctypes.c_int, [_SP, _PP, ctypes.c_int32, _VP, _VP, _VP, _VP, _VP, ctypes.c_int32,
+                                                  _VP, _VP, _SZ, _VP]),
+    "a2ats_decode_step_postings": (ctypes.c_int, [_SP, _PP, ctypes.c_int32, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
+                                                  ctypes.c_int32, _VP, _VP, _VP, _SZ, _VP]),
+})
+if _lib is not None:
+    for _n in ("a2ats_postings_bytes", "a2ats_postings_build", "a2ats_select_topk_postings",
+               "a2ats_decode_step_postings"):
+        _f = getattr(_lib, _n)
+        _f.restype, _f.argtypes = _SIGS[_n]
+
+
+def a2ats_postings_bytes(shape) -> int:
+    return int(load().a2ats_postings_bytes(ctypes.byref(shape)))
+
+
+def a2ats_postings_build(shape, codes, n_tokens: int, postings, stream=None):
+    import torch
+    _check("a2ats_postings_build", load().a2ats_postings_build(
+        ctypes.byref(shape), _ptr(codes, "codes", torch.uint16), int(n_tokens), _ptr(postings, "postings"),
+        _stream(stream)))
+
+
+def a2ats_select_topk_postings(shape, params, n_ctx, q, codes, codebook, hist, postings, n_post, sel_out, ws,
+                               stream=None):
+    import torch
+    p = params.c() if isinstance(params, Params) else params
+    rc = load().a2ats_select_topk_postings(
+        ctypes.byref(shape), ctypes.byref(p), int(n_ctx), _ptr(q, "q", torch.bfloat16), _ptr(codes, "codes", torch.uint16),
+        _ptr(codebook, "codebook", torch.bfloat16), _ptr(hist, "hist", torch.int32), _ptr(postings, "postings"),
+        int(n_post), _ptr(sel_out, "sel_out", torch.int32), _ptr(ws, "ws"), ws.numel() * ws.element_size(),
+        _stream(stream))
+    _check("a2ats_select_topk_postings", rc)
+
+
+def a2ats_decode_step_postings(shape, params, n_ctx, q, k_cache, v_cache, codes, codebook, hist, postings, n_post,
+                               out, sel_out, ws, stream=None):
+    import torch
+    p = params.c() if isinstance(params, Params) else params
+    rc = load().a2ats_decode_step_postings(
+        ctypes.byref(shape), ctypes.byref(p), int(n_ctx), _ptr(q, "q", torch.bfloat16),
+        _ptr(k_cache, "k_cache", torch.bfloat16), _ptr(v_cache, "v_cache", torch.bfloat16),
+        _ptr(codes, "codes", torch.uint16), _ptr(codebook, "codebook", torch.bfloat16), _ptr(hist, "hist", torch.int32),
+        _ptr(postings, "postings"), int(n_post), _ptr(out, "out", torch.float32, host_ok="pinned"),
+        _ptr(sel_out, "sel_out", torch.int32, optional=True), _ptr(ws, "ws"), ws.numel() * ws.element_size(),
+        _stream(stream))
+    _check("a2ats_decode_step_postings", rc)

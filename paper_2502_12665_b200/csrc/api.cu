@@ -164,6 +164,18 @@ EncodeWs encode_layout(const a2ats_shape* s) {
   return w;
 }
 
+struct PostingsLayout {
+  size_t off, tok, total;
+};
+PostingsLayout postings_layout(const a2ats_shape* s) {
+  PostingsLayout w;
+  const size_t P = (size_t)s->B * s->Hkv;
+  w.off = 0;
+  w.tok = align_up(P * (s->L + 1) * 4);
+  w.total = align_up(w.tok + P * s->n_max * 4);
+  return w;
+}
+
 void fill_rope(const a2ats_params* p, RopeTab* rt) {
   for (int m = 0; m < kHalf; ++m)
     rt->inv_freq[m] = p->inv_freq ? p->inv_freq[m] : std::pow(p->rope_theta, -2.0 * m / (double)kD);
@@ -467,7 +479,8 @@ namespace {
 int decode_impl(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx, const void* q,
                 const void* k_cache, const void* v_cache, uint16_t* codes, const void* codebook, int32_t* hist,
                 const void* chat, const float* nrm, float* out, int32_t* sel_out, float* scores_out, void* ws,
-                size_t ws_bytes, void* stream, bool attend = true) {
+                size_t ws_bytes, void* stream, bool attend = true, const void* postings = nullptr,
+                int32_t n_post = 0) {
   int rc = check_shape(shape);
   if (rc) return rc;
   rc = check_params(params);
@@ -515,12 +528,15 @@ int decode_impl(const a2ats_shape* shape, const a2ats_params* params, int32_t n_
   const bool long_select = d.keff > 0 && nchunk >= 2;
   // hist given: the warp-specialized persistent select (forward / backward half per pair);
   // otherwise threshold + chunked scan (the counts need a pass over the codes)
-  const bool pipe_select = long_select && hist != nullptr && select_pipe_ok(shape->L) && shape->n_max % 64 == 0;
-  const bool split_select = long_select && !pipe_select;
+  // posting lists given: one CTA per pair reads only the hit codes' lists (f3)
+  const bool post_select = postings != nullptr && d.keff > 0;
+  const bool pipe_select = !post_select && long_select && hist != nullptr && select_pipe_ok(shape->L) &&
+                           shape->n_max % 64 == 0;
+  const bool split_select = !post_select && long_select && !pipe_select;
   prep_set_window(p, shape, k_cache, wlog, n_ctx, d.w0, d.n_w, 0);
   const int n_wl = p.n_wl;
-  // long contexts: the threshold kernel computes the window logits before its wait
-  if (long_select || !attend) p.n_win = 0;
+  // long contexts / postings: the threshold (postings) kernel computes the window logits before its wait
+  if (long_select || post_select || !attend) p.n_win = 0;
   CUtensorMap tmA, tmC;
   rc = cuda_status(make_tmap_sw128(&tmA, codebook, (uint64_t)shape->Hkv * shape->L, kD, 128));
   if (rc) return rc;
@@ -577,7 +593,7 @@ int decode_impl(const a2ats_shape* shape, const a2ats_params* params, int32_t n_
     sa.B = shape->B;
     sa.wlog = nullptr;
     sa.P = d.P;
-    if (long_select && attend) {  // the threshold kernel computes the window logits before its wait
+    if ((long_select || post_select) && attend) {  // the threshold kernel computes the window logits before its wait
       sa.wlog = wlog;
       sa.q = static_cast<const uint16_t*>(q);
       sa.kc = static_cast<const uint16_t*>(k_cache);
@@ -608,7 +624,14 @@ int decode_impl(const a2ats_shape* shape, const a2ats_params* params, int32_t n_
       rc = cuda_status(make_tmap_codes(&tmK, codes, (uint64_t)d.P, (uint64_t)shape->n_max));
       if (rc) return rc;
     }
-    rc = cuda_status(pipe_select    ? launch_select_pipe(sa, tmK, std::min(sm_count(), 2 * d.P), st)
+    if (post_select) {
+      const PostingsLayout pl = postings_layout(shape);
+      sa.post_off = reinterpret_cast<const int32_t*>(static_cast<const uint8_t*>(postings) + pl.off);
+      sa.post_tok = reinterpret_cast<const int32_t*>(static_cast<const uint8_t*>(postings) + pl.tok);
+      sa.n_post = n_post;
+    }
+    rc = cuda_status(post_select    ? launch_select_postings(sa, st)
+                     : pipe_select  ? launch_select_pipe(sa, tmK, std::min(sm_count(), 2 * d.P), st)
                      : split_select ? launch_select_split(sa, d.P, st)
                                     : launch_select(sa, d.P, st));
     if (rc) return rc;
@@ -685,6 +708,48 @@ int a2ats_select_topk(const a2ats_shape* shape, const a2ats_params* params, int3
   return decode_impl(shape, params, n_ctx, q, nullptr, nullptr, const_cast<uint16_t*>(codes), codebook,
                      const_cast<int32_t*>(hist), nullptr, nullptr, nullptr, sel_out, nullptr, ws, ws_bytes, stream,
                      false);
+}
+
+// ------------------------------------------------------------------ posting-list selection (f3)
+size_t a2ats_postings_bytes(const a2ats_shape* shape) {
+  if (check_shape(shape)) return 0;
+  return postings_layout(shape).total;
+}
+
+int a2ats_postings_build(const a2ats_shape* shape, const uint16_t* codes, int32_t n_tokens, void* postings,
+                         void* stream) {
+  int rc = check_shape(shape);
+  if (rc) return rc;
+  if (!codes || !postings || n_tokens < 0 || n_tokens > shape->n_max || !aligned16(postings)) return A2ATS_EINVAL;
+  const PostingsLayout pl = postings_layout(shape);
+  uint8_t* b = static_cast<uint8_t*>(postings);
+  return cuda_status(launch_postings_build(codes, shape->B * shape->Hkv, shape->n_max, shape->L, n_tokens,
+                                           reinterpret_cast<int32_t*>(b + pl.off),
+                                           reinterpret_cast<int32_t*>(b + pl.tok), static_cast<cudaStream_t>(stream)));
+}
+
+int a2ats_select_topk_postings(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx, const void* q,
+                               const uint16_t* codes, const void* codebook, const int32_t* hist,
+                               const void* postings, int32_t n_post, int32_t* sel_out, void* ws, size_t ws_bytes,
+                               void* stream) {
+  if (!postings || !hist || n_post < 0 || n_post > n_ctx) return A2ATS_EINVAL;
+  if (check_shape(shape)) return A2ATS_EINVAL;
+  if (!select_postings_ok(shape->L, n_ctx)) return A2ATS_EUNSUPPORTED;
+  return decode_impl(shape, params, n_ctx, q, nullptr, nullptr, const_cast<uint16_t*>(codes), codebook,
+                     const_cast<int32_t*>(hist), nullptr, nullptr, nullptr, sel_out, nullptr, ws, ws_bytes, stream,
+                     false, postings, n_post);
+}
+
+int a2ats_decode_step_postings(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx, const void* q,
+                               const void* k_cache, const void* v_cache, const uint16_t* codes,
+                               const void* codebook, const int32_t* hist, const void* postings, int32_t n_post,
+                               float* out, int32_t* sel_out, void* ws, size_t ws_bytes, void* stream) {
+  if (!postings || !hist || n_post < 0 || n_post > n_ctx) return A2ATS_EINVAL;
+  if (check_shape(shape)) return A2ATS_EINVAL;
+  if (!select_postings_ok(shape->L, n_ctx)) return A2ATS_EUNSUPPORTED;
+  return decode_impl(shape, params, n_ctx, q, k_cache, v_cache, const_cast<uint16_t*>(codes), codebook,
+                     const_cast<int32_t*>(hist), nullptr, nullptr, out, sel_out, nullptr, ws, ws_bytes, stream, true,
+                     postings, n_post);
 }
 
 // ------------------------------------------------------------------ end-to-end staging

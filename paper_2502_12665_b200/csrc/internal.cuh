@@ -196,6 +196,10 @@ struct SelArgs {
   int bounds[kMaxRanks + 1];    // rank r holds global tokens [bounds[r], bounds[r + 1])
   uint32_t* send_codes;         // [P] the new token's code (owner rank), into the all-gather message
   int sel_base;                 // added to emitted token indices (local -> global)
+  // posting-list selection (a2ats_*_postings): tokens [0, n_post) grouped by code
+  const int32_t* post_off;      // [P, L + 1] start of each code's list
+  const int32_t* post_tok;      // [P, n_max] token indices, grouped by code
+  int n_post;
   // window logits computed by the threshold kernel before its dependency wait (long contexts;
   // otherwise the prep kernel's window role): wlog == nullptr disables
   float* wlog;                  // [P, 64, 8]
@@ -280,6 +284,11 @@ cudaError_t launch_select_pipe(const SelArgs& a, const CUtensorMap& tmK, int nbl
 // sharded step: threshold from the replicated histograms (grid P) + the persistent scan over
 // the rank's local candidate range (tmK over the local codes)
 cudaError_t launch_select_shard(const SelArgs& a, const CUtensorMap& tmK, int nblk, cudaStream_t st);
+// posting-list selection: one CTA per pair (threshold + bitmaps from the lists + ordered emission)
+cudaError_t launch_select_postings(const SelArgs& a, cudaStream_t st);
+bool select_postings_ok(int L, int n_cand);
+cudaError_t launch_postings_build(const uint16_t* codes, int P, int n_max, int L, int n_tok, int32_t* post_off,
+                                  int32_t* post_tok, cudaStream_t st);
 bool select_pipe_ok(int L);
 cudaError_t launch_attention(const AttnArgs& a, int P, int GT, cudaStream_t st);
 cudaError_t launch_combine(const float* parts, int R, int rows, size_t stride, float* out, cudaStream_t st);

@@ -1519,6 +1519,318 @@ __global__ __launch_bounds__(kPAll, 1) void select_scan_kernel(const __grid_cons
   A2ATS_TL(g_selc_tl, 1);
 }
 
+// ---------------------------------------------------------------- posting-list selection (f3)
+// Inverted index: the tokens [0, n_post) of every pair grouped by code
+// (post_off / post_tok, query-independent, built at prefill by a2ats_postings_build).  Since a
+// token's approximate score is its code's (Eq. 21), the top-K set is the union of the lists of
+// the codes above v* plus the first m tokens (by index) of the tied codes' lists (Q12): the
+// step reads only those lists (about K entries per pair) instead of every code.  One CTA per
+// pair: counts (hist - sinks/window) and the window-row logits before the dependency wait;
+// v*, m from the registers (level_regs); the hit codes compacted with the prefix of their list
+// lengths; every list entry e (threads stride the flattened entries, the code found by binary
+// search in the prefix) sets its candidate bit in the above or the tied bitmap; tokens
+// [n_post, c1) not yet in the index are classified from their codes; then the bitmaps are
+// scanned in token order: ascending emission with the tie quota, as in the code scan.
+constexpr int kQT = 256;             // postings select threads (16 codewords / thread, L <= 4096)
+constexpr int kQWords = 16;          // bitmap words per thread per segment (4096-word segments)
+
+__global__ __launch_bounds__(kQT, 4) void select_postings_kernel(SelArgs a) {
+  extern __shared__ __align__(16) uint32_t sm[];
+  __shared__ SelShared S;
+  __shared__ int s_nh, s_tot;
+  __shared__ uint32_t s_cls[256];    // compact 2-bit classes (code >> 4), L <= 4096
+  __shared__ uint32_t s_part[2][kQT / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, pair = blockIdx.x;
+  const int L4 = (a.L + 3) & ~3;
+  int* cnt = reinterpret_cast<int*>(sm);                    // [L4]
+  uint32_t* skey = sm + L4;                                 // [kTSurv] survivors
+  int* scnt = reinterpret_cast<int*>(skey + kTSurv);        // [kTSurv]
+  const int ncand = max(0, a.c1 - a.c0), nwords = (ncand + 31) >> 5;
+  const int nw4 = (nwords + 3) & ~3;
+  uint32_t* bab = sm + L4 + 2 * kTSurv;                     // [nw4] above-v* bitmap of the candidates
+  uint32_t* bti = bab + nw4;                                // [nw4] tied bitmap
+  // hit codes (alias cnt + survivors, dead after the level): code, prefix of the list lengths,
+  // list start; capacity kHitCap (beyond it the list starts are read from global memory)
+  const int hcap = min(L4, (L4 * 4 + 2 * kTSurv * 4) / 14 / 4 * 4);
+  uint16_t* hcode = reinterpret_cast<uint16_t*>(sm);
+  int* hpre = reinterpret_cast<int*>(sm) + hcap / 2;
+  int* hstart = hpre + hcap;
+  const uint16_t* cp = a.codes + (size_t)pair * a.n_max;
+  float wacc[512 / kQT];
+  if (a.wlog) {  // the pair's window-row logits (step inputs; scratch aliases counts and bitmaps)
+    window_logits<kQT>(a, pair, reinterpret_cast<uint8_t*>(sm), wacc);
+    __syncthreads();
+  }
+  load_cnt<kQT>(a, pair, cnt, cp);  // hist - sinks / window codes (step inputs)
+  int c[16];
+  load_c_regs<16>(a, cnt, c);
+  for (int i = tid; i < 2 * nw4; i += kQT) bab[i] = 0u;
+  pdl_wait();  // agg comes from the prep kernel
+  pdl_trigger();
+  if (a.wlog) store_window_logits<kQT>(a, pair, wacc);
+  append_hist(a, pair, cp);
+  uint32_t k[16], kstar, m;
+  level_regs<kQT, 16>(a, S, pair, c, k, skey, scnt, kTSurv, kstar, m);  // (ends synced: cnt dead)
+  // classes of this thread's 16 codewords; hit codes (class != 0, candidates present) compacted
+  int e_unused = 0;
+  const uint32_t x = class_bits<16>(k, c, kstar, e_unused);
+  if (tid < 256) s_cls[tid] = x;
+  uint32_t hmask = 0u;
+#pragma unroll
+  for (int e = 0; e < 16; ++e)
+    if (c[e] > 0 && k[e] <= kstar) hmask |= 1u << e;
+  const int post0 = pair * (a.L + 1);
+  int len[16];
+  int mylen = 0;
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    len[e] = 0;
+    if ((hmask >> e) & 1u) {
+      const int l = tid * 16 + e;
+      len[e] = __ldg(a.post_off + post0 + l + 1) - __ldg(a.post_off + post0 + l);
+      mylen += len[e];
+    }
+  }
+  // block scans of (#hit codes, #entries)
+  const int nh = __popc(hmask);
+  int inh = nh, inl = mylen;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int y1 = __shfl_up_sync(0xffffffffu, inh, off), y2 = __shfl_up_sync(0xffffffffu, inl, off);
+    if (lane >= off) {
+      inh += y1;
+      inl += y2;
+    }
+  }
+  if (lane == 31) {
+    s_part[0][warp] = (uint32_t)inh;
+    s_part[1][warp] = (uint32_t)inl;
+  }
+  __syncthreads();
+  int bh = inh - nh, bl = inl - mylen;
+  for (int w = 0; w < warp; ++w) {
+    bh += (int)s_part[0][w];
+    bl += (int)s_part[1][w];
+  }
+  if (tid == kQT - 1) {
+    s_nh = bh + nh;
+    s_tot = bl + mylen;
+  }
+  __syncthreads();
+  const int nhit = s_nh, total = s_tot;
+  const bool in_smem = nhit <= hcap;
+  if (in_smem) {
+#pragma unroll
+    for (int e = 0; e < 16; ++e)
+      if ((hmask >> e) & 1u) {
+        const int l = tid * 16 + e;
+        hcode[bh] = (uint16_t)l;
+        hpre[bh] = bl;
+        hstart[bh] = __ldg(a.post_off + post0 + l);
+        ++bh;
+        bl += len[e];
+      }
+  }
+  __syncthreads();
+  // flattened list entries -> candidate bits (entries outside [c0, c1) are sinks / window):
+  // warps take blocks of 32 consecutive entries (lane j: entry E + j); the block's first hit code
+  // comes from one binary search over the prefix (same address in every lane: broadcast), each
+  // lane then walks the few codes the block spans; 4 blocks per pass keep 4 list loads in flight
+  const int32_t* ptok = a.post_tok + (size_t)pair * a.n_max;
+  const int nblocks = (total + 31) >> 5;
+  // first hit code of every 32-entry block (the code whose list holds entry 32 b): bstart[b],
+  // scattered by the hit codes themselves, after the per-hit arrays when it fits (else a binary
+  // search over the prefix per block)
+  int* bstart = hstart + hcap;
+  const bool use_bstart = in_smem && hcap * 10 + nblocks * 4 <= L4 * 4 + 2 * kTSurv * 4;
+  if (use_bstart) {
+    for (int h = tid; h < nhit; h += kQT) {
+      const int e0 = hpre[h], e1 = (h + 1 < nhit) ? hpre[h + 1] : total;
+      for (int b = (e0 + 31) >> 5; (b << 5) < e1; ++b) bstart[b] = h;
+    }
+    if (tid == 0 && nhit > 0 && hpre[0] == 0 && nblocks > 0) bstart[0] = 0;
+    __syncthreads();
+  }
+  if (in_smem) {
+    constexpr int kU = 4;
+    for (int b0 = warp; b0 < nblocks; b0 += (kQT / 32) * kU) {
+      int tk[kU];
+      int lc[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int blk = b0 + u * (kQT / 32), E = blk * 32, e = E + lane;
+        tk[u] = -1;
+        lc[u] = 0;
+        if (blk < nblocks) {
+          int lo = 0;
+          if (use_bstart) {
+            lo = bstart[blk];
+          } else {
+            int hi = nhit - 1;
+            while (lo < hi) {
+              const int mid = (lo + hi + 1) >> 1;
+              if (hpre[mid] <= E) lo = mid;
+              else hi = mid - 1;
+            }
+          }
+          while (lo + 1 < nhit && hpre[lo + 1] <= e) ++lo;
+          if (e < total) {
+            lc[u] = hcode[lo];
+            tk[u] = __ldg(ptok + hstart[lo] + (e - hpre[lo]));
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int t = tk[u];
+        if (t >= a.c0 && t < a.c1) {
+          const int l = lc[u];
+          const uint32_t cl = (s_cls[l >> 4] >> (2 * (l & 15))) & 3u;
+          atomicOr((cl == 1u ? bab : bti) + ((t - a.c0) >> 5), 1u << ((t - a.c0) & 31));
+        }
+      }
+    }
+  } else {  // very many hit codes (ties across much of the codebook): thread per hit codeword
+#pragma unroll 1
+    for (int e = 0; e < 16; ++e) {
+      if (!((hmask >> e) & 1u)) continue;
+      const int l = tid * 16 + e;
+      const uint32_t cl = (s_cls[l >> 4] >> (2 * (l & 15))) & 3u;
+      const int b0 = __ldg(a.post_off + post0 + l), b1 = __ldg(a.post_off + post0 + l + 1);
+      for (int i = b0; i < b1; ++i) {
+        const int t = __ldg(ptok + i);
+        if (t >= a.c0 && t < a.c1) atomicOr((cl == 1u ? bab : bti) + ((t - a.c0) >> 5), 1u << ((t - a.c0) & 31));
+      }
+    }
+  }
+  // tokens not yet in the index: classified from their codes
+  for (int t = max(a.n_post, a.c0) + tid; t < a.c1; t += kQT) {
+    const int l = cp[t];
+    const uint32_t cl = (s_cls[l >> 4] >> (2 * (l & 15))) & 3u;
+    if (cl) atomicOr((cl == 1u ? bab : bti) + ((t - a.c0) >> 5), 1u << ((t - a.c0) & 31));
+  }
+  __syncthreads();
+  // ordered emission over segments of kQT * kQWords words (32 tokens each)
+  int32_t* selp = a.sel + (size_t)pair * a.sel_stride;
+  const uint32_t cap = (uint32_t)a.keff;
+  uint32_t run_gt = 0u, run_eq = 0u;
+  for (int seg = 0; seg < nwords; seg += kQT * kQWords) {
+    const int w0 = seg + tid * kQWords;
+    uint32_t ng = 0u, ne = 0u;
+#pragma unroll
+    for (int i = 0; i < kQWords; ++i) {  // rotated order: the warp's lanes hit distinct banks
+      const int w = w0 + ((i + tid) & (kQWords - 1));
+      if (w < nwords) {
+        ng += __popc(bab[w]);
+        ne += __popc(bti[w]);
+      }
+    }
+    uint32_t ig = ng, ie = ne;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t y1 = __shfl_up_sync(0xffffffffu, ig, off), y2 = __shfl_up_sync(0xffffffffu, ie, off);
+      if (lane >= off) {
+        ig += y1;
+        ie += y2;
+      }
+    }
+    __syncthreads();  // the previous segment's s_part reads are done
+    if (lane == 31) {
+      s_part[0][warp] = ig;
+      s_part[1][warp] = ie;
+    }
+    __syncthreads();
+    uint32_t gb = run_gt + ig - ng, eb = run_eq + ie - ne, tg = 0u, te = 0u;
+    for (int w = 0; w < kQT / 32; ++w) {
+      const uint32_t pg = s_part[0][w], pe = s_part[1][w];
+      if (w < warp) {
+        gb += pg;
+        eb += pe;
+      }
+      tg += pg;
+      te += pe;
+    }
+#pragma unroll 1
+    for (int i = 0; i < kQWords; ++i) {
+      const int w = w0 + i;
+      if (w >= nwords) break;
+      uint32_t ga = bab[w], gt = bti[w];
+      const int tb = a.c0 + w * 32;
+      if ((ga | gt) == 0u) continue;
+      if (gt == 0u) {  // above v* only: positions gb + min(eb, m) .. + n - 1, ascending
+        const uint32_t pos = gb + min(eb, m);
+        uint32_t n = 0u;
+        while (ga) {
+          const int bit = __ffs(ga) - 1;
+          ga &= ga - 1u;
+          if (pos + n < cap) selp[pos + n] = tb + bit;
+          ++n;
+        }
+        gb += n;
+        continue;
+      }
+      uint32_t all = ga | gt;
+      while (all) {  // in token order: above -> gb + min(eb, m); tied -> kept iff eb < m
+        const int bit = __ffs(all) - 1;
+        all &= all - 1u;
+        if ((ga >> bit) & 1u) {
+          const uint32_t pos = gb + min(eb, m);
+          if (pos < cap) selp[pos] = tb + bit;
+          ++gb;
+        } else {
+          if (eb < m && gb + eb < cap) selp[gb + eb] = tb + bit;
+          ++eb;
+        }
+      }
+    }
+    run_gt += tg;
+    run_eq += te;
+  }
+}
+
+// Inverted index of tokens [0, n_tok) per pair: counts per code, exclusive prefix -> post_off,
+// tokens scattered into their code's list (order inside a list is irrelevant to the selection,
+// which goes through bitmaps).
+constexpr int kBT = 1024;
+__global__ __launch_bounds__(kBT) void postings_build_kernel(const uint16_t* __restrict__ codes, int n_max, int L,
+                                                             int n_tok, int32_t* __restrict__ post_off,
+                                                             int32_t* __restrict__ post_tok) {
+  extern __shared__ __align__(16) int pbuf[];  // cnt [L], cursor [L]
+  __shared__ int s_w[kBT / 32];
+  const int pair = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int* cnt = pbuf;
+  int* cur = pbuf + L;
+  const uint16_t* cp = codes + (size_t)pair * n_max;
+  for (int l = tid; l < L; l += kBT) cnt[l] = 0;
+  __syncthreads();
+  for (int t = tid; t < n_tok; t += kBT) atomicAdd(&cnt[cp[t]], 1);
+  __syncthreads();
+  // exclusive prefix over L codes: thread owns a contiguous run of ceil(L / kBT)
+  const int per = (L + kBT - 1) / kBT, l0 = tid * per;
+  int s = 0;
+  for (int i = 0; i < per && l0 + i < L; ++i) s += cnt[l0 + i];
+  int incl = s;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += y;
+  }
+  if (lane == 31) s_w[warp] = incl;
+  __syncthreads();
+  int base = incl - s;
+  for (int w = 0; w < warp; ++w) base += s_w[w];
+  int32_t* offp = post_off + (size_t)pair * (L + 1);
+  for (int i = 0; i < per && l0 + i < L; ++i) {
+    offp[l0 + i] = base;
+    cur[l0 + i] = base;
+    base += cnt[l0 + i];
+  }
+  if (tid == kBT - 1) offp[L] = base;
+  __syncthreads();
+  int32_t* tp = post_tok + (size_t)pair * n_max;
+  for (int t = tid; t < n_tok; t += kBT) tp[atomicAdd(&cur[cp[t]], 1)] = t;
+}
+
 size_t shard_thresh_smem_bytes(int L) { return (size_t)((L + 3) & ~3) * 8 + 2 * kTSurv * 4; }
 size_t thresh_smem_bytes(int L) { return (size_t)((L + 3) & ~3) * 4 + 2 * kTSurv * 4; }  // cnt + survivors
 size_t scan_smem_bytes(int) { return 32768 + 65536 + (size_t)kPStage * kPRound * 2; }  // align slack + tables + ring
@@ -1636,6 +1948,28 @@ cudaError_t launch_select_split(const SelArgs& a, int P, cudaStream_t st) {
 int select_chunk_tokens() { return kCH; }
 
 bool select_pipe_ok(int L) { return L <= 4096; }
+
+size_t postings_smem_bytes(int L, int n_cand) {
+  const size_t words = (size_t)(((n_cand + 31) / 32 + 3) & ~3);
+  const size_t base = (size_t)((L + 3) & ~3) * 4 + 2 * kTSurv * 4 + 2 * words * 4;
+  return std::max(base, (size_t)kWinScratch);
+}
+bool select_postings_ok(int L, int n_cand) { return L <= 4096 && postings_smem_bytes(L, n_cand) <= 200 * 1024; }
+
+cudaError_t launch_select_postings(const SelArgs& a, cudaStream_t st) {
+  const int smem = (int)postings_smem_bytes(a.L, std::max(0, a.c1 - a.c0));
+  cudaError_t e = ensure_smem(select_postings_kernel, smem);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(select_postings_kernel, dim3(a.P), dim3(kQT), smem, st, a);
+}
+
+cudaError_t launch_postings_build(const uint16_t* codes, int P, int n_max, int L, int n_tok, int32_t* post_off,
+                                  int32_t* post_tok, cudaStream_t st) {
+  const int smem = 2 * L * 4;
+  cudaError_t e = ensure_smem(postings_build_kernel, smem);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(postings_build_kernel, dim3(P), dim3(kBT), smem, st, codes, n_max, L, n_tok, post_off, post_tok);
+}
 
 cudaError_t launch_select_shard(const SelArgs& a, const CUtensorMap& tmK, int nblk, cudaStream_t st) {
   if (!select_pipe_ok(a.L)) return cudaErrorInvalidValue;

@@ -57,6 +57,25 @@ class Decoder:
                              self.hist if use_hist else None, sel_out, self.ws_dec, self.stream)
         return sel_out
 
+    def build_postings(self, n_tokens: int):
+        """Inverted index of tokens [0, n_tokens) (f3 posting-list selection)."""
+        if getattr(self, "postings", None) is None:
+            self.postings = torch.zeros(_b.a2ats_postings_bytes(self.shape), dtype=torch.uint8, device=self.device)
+        _b.a2ats_postings_build(self.shape, self.codes, n_tokens, self.postings, self.stream)
+        self.n_post = int(n_tokens)
+
+    def select_postings(self, q, n_ctx: int, sel_out):
+        _b.a2ats_select_topk_postings(self.shape, self.params, n_ctx, q, self.codes, self.codebook, self.hist,
+                                      self.postings, self.n_post, sel_out, self.ws_dec, self.stream)
+        return sel_out
+
+    def step_postings(self, q, k_cache, v_cache, n_ctx: int, out=None, sel_out=None):
+        if out is None:
+            out = torch.empty((self.shape.B, self.shape.Hq, 128), dtype=torch.float32, device=self.device)
+        _b.a2ats_decode_step_postings(self.shape, self.params, n_ctx, q, k_cache, v_cache, self.codes, self.codebook,
+                                      self.hist, self.postings, self.n_post, out, sel_out, self.ws_dec, self.stream)
+        return out
+
     def step_append(self, q, k_cache, v_cache, n_ctx: int, out=None, sel_out=None, scores_out=None,
                     use_hist=True):
         """a0 for token n_ctx - 1 (its key already in k_cache) fused with the step."""

@@ -23,6 +23,7 @@ ap.add_argument("--batch", type=int, default=0)
 ap.add_argument("--L", type=int, default=0)
 ap.add_argument("--N", type=int, default=0)
 ap.add_argument("--select-only", action="store_true", help="a2ats_select_topk (a1..a4) only")
+ap.add_argument("--postings", action="store_true", help="posting-list selection engine (f3)")
 args = ap.parse_args()
 cfg = CONFIGS[args.config]
 if args.batch:
@@ -49,10 +50,15 @@ hist0 = hist.clone()
 c0 = codes[:, :, :cfg.N - 1].to(torch.int64)
 hist0.zero_().scatter_add_(2, c0, torch.ones_like(c0, dtype=torch.int32))
 sel_buf = torch.empty((cfg.B, cfg.Hkv, max(cfg.K, 1)), dtype=torch.int32, device="cuda")
+if args.postings:
+    dec.build_postings(cfg.N - 1)
 for it in range(args.iters if args.select_only else 0):
     flush.fill_(it)
     e0.record()
-    dec.select(inp["q"], cfg.N, sel_buf)
+    if args.postings:
+        dec.select_postings(inp["q"], cfg.N, sel_buf)
+    else:
+        dec.select(inp["q"], cfg.N, sel_buf)
     e1.record()
     torch.cuda.synchronize()
     print("it", it, "select_topk %.1f us" % (e0.elapsed_time(e1) * 1e3))
