@@ -862,7 +862,10 @@ __device__ __forceinline__ void emit16(uint32_t q, int t0, uint32_t& gb, uint32_
 //    code), double-buffered: the next unit's table is written during the current one.
 constexpr int kPAll = 1024;          // scan kernel threads
 constexpr int kPRound = 256 * 64;    // tokens per stage: one TMA box of 256 128-B rows (32 KB)
-constexpr int kPStage = 4;
+#ifndef A2ATS_SCAN_STAGES
+#define A2ATS_SCAN_STAGES 5
+#endif
+constexpr int kPStage = A2ATS_SCAN_STAGES;  // ring stages (32 KB each): 5 fit beside one class table
 constexpr int kTT = 256;             // threshold kernel threads
 constexpr int kTSurv = 1024;         // its survivor list capacity
 
@@ -1417,11 +1420,13 @@ __global__ __launch_bounds__(kPAll, 1) void select_scan_kernel(const __grid_cons
   const int P = a.P, nblk = gridDim.x, W = a.W;
   const int tid = threadIdx.x;
   // tables at the first 32-KB boundary of the shared window ([2][32 KB], 32x-replicated class
-  // words: OR-addressing in classify8s), then the ring ([kPStage][32 KB], 1024-B aligned)
+  // words: OR-addressing in classify8s), then the ring ([kPStage][32 KB], 1024-B aligned).  One
+  // table buffer: the next unit's table is written by expand() after the unit's last super-round
+  // barrier, which every warp passes only once it has classified its last tokens of the unit
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smp);
   const uint32_t tsh = (sbase + 32767u) & ~32767u;
   uint32_t* tbl0 = reinterpret_cast<uint32_t*>(smp + (tsh - sbase));
-  uint8_t* ring = smp + (tsh - sbase) + 65536;
+  uint8_t* ring = smp + (tsh - sbase) + 32768;
   const PipeGeom g = pipe_geom(a);
   const int R1 = g.R - g.R0;
   const int nunit = (2 * P - (int)blockIdx.x + nblk - 1) / nblk;        // units u = blockIdx.x + k * nblk
@@ -1483,7 +1488,7 @@ __global__ __launch_bounds__(kPAll, 1) void select_scan_kernel(const __grid_cons
   auto store_table = [&](int k) {
     if (tw < W) {
       const uint32_t x = sStage[k & 1][tw];
-      uint4* dst = reinterpret_cast<uint4*>(tbl0 + (k & 1) * 8192 + tw * 32);
+      uint4* dst = reinterpret_cast<uint4*>(tbl0 + tw * 32);
       const uint4 v = make_uint4(x, x, x, x);
       dst[(tq + tw) & 7] = v;
       dst[(tq + 1 + tw) & 7] = v;
@@ -1510,8 +1515,8 @@ __global__ __launch_bounds__(kPAll, 1) void select_scan_kernel(const __grid_cons
         store_table(k + 1);
       }
     };
-    if (fwd) scan_unit<true>(c, k & 1, pair_of(k), g.R0, pu_cur, j, issue, expand);
-    else scan_unit<false>(c, k & 1, pair_of(k), R1, pu_cur, j, issue, expand);
+    if (fwd) scan_unit<true>(c, 0, pair_of(k), g.R0, pu_cur, j, issue, expand);
+    else scan_unit<false>(c, 0, pair_of(k), R1, pu_cur, j, issue, expand);
     __syncthreads();  // the next unit's table is visible
     if (k + 1 < nunit) pu_cur = unit_info(k + 1);
     if (tid == 0 && k == 0) A2ATS_TLX(g_selc_tl, 3);
@@ -1833,7 +1838,7 @@ __global__ __launch_bounds__(kBT) void postings_build_kernel(const uint16_t* __r
 
 size_t shard_thresh_smem_bytes(int L) { return (size_t)((L + 3) & ~3) * 8 + 2 * kTSurv * 4; }
 size_t thresh_smem_bytes(int L) { return (size_t)((L + 3) & ~3) * 4 + 2 * kTSurv * 4; }  // cnt + survivors
-size_t scan_smem_bytes(int) { return 32768 + 65536 + (size_t)kPStage * kPRound * 2; }  // align slack + tables + ring
+size_t scan_smem_bytes(int) { return 32768 + 32768 + (size_t)kPStage * kPRound * 2; }  // align slack + table + ring
 
 
 template <int MODE>

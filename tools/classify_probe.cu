@@ -77,6 +77,9 @@ __device__ __forceinline__ uint32_t cls_v3(uint32_t tl, uint4 v) {
   return cls;
 }
 
+// V4: V0 with 16 table replicas (lanes l and l + 16 share one: 2-way bank conflicts)
+__device__ __forceinline__ uint32_t cls_v4(uint32_t tl16, uint4 v) { return cls_v0(tl16, v); }
+
 template <int V>
 __global__ __launch_bounds__(1024, 1) void probe(int iters, uint32_t* out) {
   extern __shared__ __align__(128) uint8_t smp[];
@@ -96,7 +99,7 @@ __global__ __launch_bounds__(1024, 1) void probe(int iters, uint32_t* out) {
     codes[i] = v;
   }
   __syncthreads();
-  const uint32_t tl = tsh | (lane * 4u);
+  const uint32_t tl = V == 4 ? (tsh | ((lane & 15) * 4u)) : (tsh | (lane * 4u));
   const uint32_t cb = (uint32_t)__cvta_generic_to_shared(codes);
   uint32_t acc = 0;
   for (int it = 0; it < iters; ++it) {
@@ -109,6 +112,7 @@ __global__ __launch_bounds__(1024, 1) void probe(int iters, uint32_t* out) {
     if (V == 1) { c0 = cls_v1(tl, v[0]) | cls_v1(tl, v[1]) << 16; c1 = cls_v1(tl, v[2]) | cls_v1(tl, v[3]) << 16; }
     if (V == 2) { c0 = cls_v2(tl, v[0]) | cls_v2(tl, v[1]) << 8 | cls_v2(tl, v[2]) << 16 | cls_v2(tl, v[3]) << 24; c1 = 0; }
     if (V == 3) { c0 = cls_v3(tl, v[0]) | cls_v3(tl, v[1]) << 16; c1 = cls_v3(tl, v[2]) | cls_v3(tl, v[3]) << 16; }
+    if (V == 4) { c0 = cls_v4(tl, v[0]) | cls_v4(tl, v[1]) << 16; c1 = cls_v4(tl, v[2]) | cls_v4(tl, v[3]) << 16; }
     acc += __popc(c0 & 0x55555555u) + (__popc(c1 & 0xaaaaaaaau) << 16);
   }
   if (acc == 0x12345678u) out[0] = acc;
@@ -142,5 +146,6 @@ int main() {
   run<1>("v1 fma-shifts  ");
   run<2>("v2 1-bit       ");
   run<3>("v3 final-pos   ");
+  run<4>("v4 16 replicas ");
   return 0;
 }

@@ -1,8 +1,7 @@
-# Round-2: postings engine tests + timing
+# Round-2: scan ring depth (5 stages, single table) -- tests + C4 timing vs 4 stages
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_postings.py -x -q -m gpu > gpurun_out/pytest_post.log 2>&1
-for cfg in C4 C2; do for e in "" "--postings"; do
-  echo "== $cfg $e" >> gpurun_out/sel_eng.log
-  timeout 300 python tools/kbench.py --config $cfg --select-only --iters 8 $e 2>&1 | tail -2 >> gpurun_out/sel_eng.log
-done; done
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:"select_postings" -s 2 -c 1 -o gpurun_out/full_post_c4 -f python tools/kbench.py --config C4 --select-only --iters 4 --postings > gpurun_out/ncu_post.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_parity_r2.py tests/test_gpu_sharded.py -x -q -m gpu -k "long or stream or c4 or C4 or select or shard" > gpurun_out/pytest_scan.log 2>&1
+for v in liba2ats liba2ats_s4 liba2ats liba2ats_s4; do
+  echo "== $v" >> gpurun_out/sel_ring.log
+  A2ATS_LIB=paper_2502_12665_b200/lib/$v.so timeout 300 python tools/kbench.py --config C4 --select-only --iters 8 2>&1 | tail -3 >> gpurun_out/sel_ring.log
+done
