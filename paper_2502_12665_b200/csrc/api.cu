@@ -40,6 +40,16 @@ cudaError_t ensure_smem_attr(const void* kernel, int bytes) {
   return e;
 }
 
+// Tuning switches (tools/ variant builds): contexts of at least this many 32K-token code chunks
+// take the threshold + persistent scan select; query tiles wider than this many vectors take
+// the qprep kernel (q~ once per step instead of in every LUT CTA).
+#ifndef A2ATS_PIPE_MIN_CHUNKS
+#define A2ATS_PIPE_MIN_CHUNKS 2
+#endif
+#ifndef A2ATS_QPREP_MIN_NV
+#define A2ATS_QPREP_MIN_NV 64
+#endif
+
 namespace {
 
 constexpr size_t kAlign = 256;
@@ -518,14 +528,14 @@ int decode_impl(const a2ats_shape* shape, const a2ats_params* params, int32_t n_
   const bool lut_fma = params->lut_engine == A2ATS_LUT_FMA ||
                        (params->lut_engine == A2ATS_LUT_AUTO && shape->B * d.G <= A2ATS_LUT_FMA_MAX_VECTORS);
   // wide query tiles: q~ hi|lo computed once by qprep_kernel instead of in every LUT CTA
-  if (la.NV > 64 && !lut_fma) la.qt = reinterpret_cast<uint16_t*>(base + Lw.qt);
+  if (la.NV > A2ATS_QPREP_MIN_NV && !lut_fma) la.qt = reinterpret_cast<uint16_t*>(base + Lw.qt);
   PrepArgs p = prep_empty();
   prep_set_lut(p, la);
   if (lut_fma) p.n_lut = 0;  // lut_fma_kernel computes agg (and the window table) before the prep kernel
   // long contexts: the window logits are computed by the select threshold kernel, before its
   // dependency wait (it waits for this kernel anyway); otherwise by the prep kernel's window role
   const int nchunk = d.c1 > d.c0 ? (d.c1 - ((d.c0 >> 3) << 3) + select_chunk_tokens() - 1) / select_chunk_tokens() : 0;
-  const bool long_select = d.keff > 0 && nchunk >= 2;
+  const bool long_select = d.keff > 0 && nchunk >= A2ATS_PIPE_MIN_CHUNKS;
   // hist given: the warp-specialized persistent select (forward / backward half per pair);
   // otherwise threshold + chunked scan (the counts need a pass over the codes)
   // posting lists given: one CTA per pair reads only the hit codes' lists (f3)
@@ -1082,7 +1092,7 @@ int shard_partial(const a2ats_shape* shape, const a2ats_params* params, int32_t 
   LutArgs la = make_lut_args(shape, params, d, q, codebook, agg, nullptr, reinterpret_cast<float2*>(base + Lw.cs));
   const bool lut_fma = params->lut_engine == A2ATS_LUT_FMA ||
                        (params->lut_engine == A2ATS_LUT_AUTO && shape->B * d.G <= A2ATS_LUT_FMA_MAX_VECTORS);
-  if (la.NV > 64 && !lut_fma) la.qt = reinterpret_cast<uint16_t*>(base + Lw.qt);
+  if (la.NV > A2ATS_QPREP_MIN_NV && !lut_fma) la.qt = reinterpret_cast<uint16_t*>(base + Lw.qt);
   PrepArgs p = prep_empty();
   prep_set_lut(p, la);
   if (lut_fma) p.n_lut = 0;
