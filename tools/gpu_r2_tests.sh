@@ -1,6 +1,9 @@
-# Round-2: C2 step variants (pipe select at one chunk; qprep for NV = 64)
+# Round-2: codebook trainer timing, compute-sanitizer on small steps, full GPU suite + smoke
 mkdir -p gpurun_out
-for v in liba2ats liba2ats_pipe1 liba2ats_q32 liba2ats_both; do
-  echo "== $v" >> gpurun_out/c2_var.log
-  A2ATS_LIB=paper_2502_12665_b200/lib/$v.so timeout 600 python bench.py --config C2 --steps 20 --warmup 5 --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(d['ms_per_step'], d['scoring']['ms'], d['e2e']['ms_per_step'])" >> gpurun_out/c2_var.log
+timeout 600 python tools/train_bench.py > gpurun_out/train_r2.json 2> gpurun_out/train_r2.err
+for tool in memcheck racecheck synccheck; do
+  timeout 900 compute-sanitizer --tool $tool --print-limit 20 python tools/sanitize_small.py > gpurun_out/sanitize_$tool.log 2>&1
+  echo "rc=$?" >> gpurun_out/sanitize_$tool.log
 done
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
