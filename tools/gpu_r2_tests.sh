@@ -1,9 +1,4 @@
-# Round-2: codebook trainer timing, compute-sanitizer on small steps, full GPU suite + smoke
+# Round-2: two-CTAs-per-SM scan -- tests + C4 timing
 mkdir -p gpurun_out
-timeout 600 python tools/train_bench.py > gpurun_out/train_r2.json 2> gpurun_out/train_r2.err
-for tool in memcheck racecheck synccheck; do
-  timeout 900 compute-sanitizer --tool $tool --print-limit 20 python tools/sanitize_small.py > gpurun_out/sanitize_$tool.log 2>&1
-  echo "rc=$?" >> gpurun_out/sanitize_$tool.log
-done
-timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_parity_r2.py tests/test_gpu_sharded.py tests/test_gpu_postings.py -x -q -m gpu -k "long or stream or c4 or C4 or select or shard or postings" > gpurun_out/pytest_scan.log 2>&1
+timeout 300 python tools/kbench.py --config C4 --select-only --iters 8 > gpurun_out/sel_c4.log 2>&1
