@@ -124,7 +124,7 @@ void derive(const a2ats_shape* s, const a2ats_params* p, int n_ctx, Derived* d) 
 }
 
 struct DecodeWs {
-  size_t cs, agg, lut, sel, part, actr, pinfo, nsel, wlog, eslot, ectr, tblg, desc, qt, total;
+  size_t cs, agg, lut, sel, part, actr, pinfo, nsel, wlog, eslot, ectr, tblg, desc, tick, qt, total;
 };
 
 DecodeWs decode_layout(const a2ats_shape* s, const a2ats_params* p) {
@@ -143,6 +143,7 @@ DecodeWs decode_layout(const a2ats_shape* s, const a2ats_params* p) {
   w.eslot = o; o = align_up(o + (size_t)s->Hkv * std::max(s->B, 1) * 8);                    // append encode slots
   w.ectr = o; o = align_up(o + (size_t)s->Hkv * 2 * 4);
   w.desc = o; o = align_up(o + (size_t)P * (s->n_max / select_chunk_tokens() + 2) * 8);     // look-back descriptors
+  w.tick = o; o = align_up(o + 8);                                                           // chunk tickets
   w.cs = o; o = align_up(o + (size_t)p->window * kHalf * 8);
   w.agg = o; o = align_up(o + (size_t)P * s->L * 4);
   w.lut = o; o = align_up(o + (size_t)s->B * s->Hq * s->L * 4);
@@ -598,6 +599,7 @@ int decode_impl(const a2ats_shape* shape, const a2ats_params* params, int32_t n_
     sa.pinfo = reinterpret_cast<uint32_t*>(base + Lw.pinfo);
     sa.tblg = reinterpret_cast<uint32_t*>(base + Lw.tblg);
     sa.desc = reinterpret_cast<unsigned long long*>(base + Lw.desc);
+    sa.tickets = reinterpret_cast<unsigned int*>(base + Lw.tick);
     sa.desc_stride = shape->n_max / select_chunk_tokens() + 2;
     sa.nchunk = nchunk;
     sa.B = shape->B;

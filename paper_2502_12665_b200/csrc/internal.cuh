@@ -183,6 +183,7 @@ struct SelArgs {
   // long contexts (launch_select_split): per-pair class table, chunk descriptors, completion
   uint32_t* tblg;               // [P, W] compact 2-bit classes
   unsigned long long* desc;     // [P, desc_stride] published (#above, #tied) per chunk, 0 = not yet
+  unsigned int* tickets;        // [2] chunk tickets handed out / CTAs finished (zero on entry and exit)
   int nchunk, desc_stride;
   int P;                        // pairs (launch_select_pipe: the scan grid is persistent)
   // sequence-sharded step with replicated histograms (a2ats_decode_step_sharded):

@@ -652,9 +652,11 @@ __device__ __forceinline__ void store_window_logits(const SelArgs& a, int pair, 
 // Long contexts (several code chunks per pair), single GPU.
 //   kThresh (grid P): counts, v*, m -> pinfo; compact 2-bit class table -> tblg.
 //   kScanC (grid P x nchunk): one 32768-token chunk; classify, publish the chunk's
-//   (#above, #tied) with a release store, sum the pair's earlier chunks' counts (they have
-//   lower block indices, so they are resident or done: the wait terminates), emit.  The
-//   threshold kernel re-arms the descriptors of the next call.
+//   (#above, #tied) with a release store, sum the pair's earlier chunks' counts, emit.  A CTA
+//   takes its chunk from a ticket counter when it starts, so every chunk it waits for was
+//   handed to a CTA that started earlier (resident or done): the wait terminates whatever the
+//   block scheduling order.  The last CTA to finish re-zeroes the counters; the threshold
+//   kernel re-arms the descriptors of the next call.
 template <int MODE>
 __device__ __forceinline__ void split_body(const SelArgs& a, SelShared& S, int* cnt, uint32_t* key, uint32_t* tbl,
                                            uint32_t* skey, int* scnt, uint4* sC) {
@@ -696,7 +698,16 @@ __device__ __forceinline__ void split_body(const SelArgs& a, SelShared& S, int* 
     return;
   }
   // kScanC
-  const int pair = blockIdx.x / a.nchunk, ch = blockIdx.x - pair * a.nchunk;
+  __shared__ int s_item;
+  if (tid == 0) s_item = (int)atomicAdd(a.tickets, 1u);  // chunk item in start order
+  __syncthreads();
+  auto finish = [&]() {  // the last CTA out leaves the counters zero for the next call
+    if (tid == 0 && atomicAdd(a.tickets + 1, 1u) == gridDim.x - 1) {
+      a.tickets[0] = 0u;
+      a.tickets[1] = 0u;
+    }
+  };
+  const int pair = s_item / a.nchunk, ch = s_item - pair * a.nchunk;
   const uint16_t* cp_local = a.codes + (size_t)pair * a.n_max;
   const int c0 = a.c0, c1 = a.c1;
   const int cb = ((c0 >> 3) << 3) + ch * kCH;
@@ -707,6 +718,7 @@ __device__ __forceinline__ void split_body(const SelArgs& a, SelShared& S, int* 
   const uint32_t cap = __ldcg(a.pinfo + pair * 4 + 2);
   if (cap == 0 || cb >= c1) {
     cp_async_wait<0>();
+    finish();
     return;
   }
   for (int it = tid; it < a.W * 2; it += kNT) {  // class table, replicated 32x (2 threads per word)
@@ -806,6 +818,7 @@ __device__ __forceinline__ void split_body(const SelArgs& a, SelShared& S, int* 
       }
     }
   }
+  finish();
 }
 
 // ---------------------------------------------------------------- emission helper

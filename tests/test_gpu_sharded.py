@@ -181,3 +181,40 @@ def test_sharded_rank_without_candidates():
     redraw_for_gap(inp, SH, SH.N, 241)
     N = SH.N
     run_case(SH, inp, [(0, 20000), (20000, 20000), (20000, 20010), (20010, N - 1)])
+
+
+def test_full_entry_point_with_nccl_comm():
+    """a2ats_comm_unique_id / a2ats_comm_init (NCCL loaded by the library) and the one-call
+    a2ats_decode_step_sharded at one rank (state built by a2ats_shard_state_build with the
+    communicator), two steps: selection and output equal to the oracle's; a2ats_comm_destroy."""
+    from paper_2502_12665_b200.sharded import comm_from_torch
+    cfg = SH.with_(N=20001, K=1200)
+    inp = prepared(cfg, 251)
+    for n in (cfg.N - 1, cfg.N):
+        redraw_for_gap(inp, cfg.with_(N=n), n, 251 + n)
+    n_pre = cfg.N - 2
+    n_loc = (cfg.N + 8 + 63) // 64 * 64
+    params = A.Params(window=cfg.window, bridge=cfg.bridge, n_sink=cfg.n_sink, topk=cfg.K)
+    comm = comm_from_torch(1, 0)
+    dec = ShardedDecoder(cfg.B, cfg.Hq, cfg.Hkv, cfg.L, n_loc, inp["codebook"].cuda(), None, params, 1, 0, comm)
+    kc = torch.zeros((cfg.B, cfg.Hkv, n_loc, 128), dtype=torch.bfloat16)
+    vc = torch.zeros_like(kc)
+    kc[:, :, :cfg.N] = inp["k_cache"][:, :, :cfg.N]
+    vc[:, :, :cfg.N] = inp["v_cache"][:, :, :cfg.N]
+    kc, vc = kc.cuda(), vc.cuda()
+    lc = torch.zeros((cfg.B, cfg.Hkv, n_loc), dtype=torch.uint16)
+    lc[:, :, :n_pre] = inp["codes"][:, :, :n_pre]
+    dec.codes.copy_(lc.cuda())
+    dec.build_state([0, n_pre], n_pre)
+    ref_codes = codes_np(inp["codes"]).copy()
+    keys = f64(inp["k_cache"])
+    for n in (cfg.N - 1, cfg.N):
+        for b in range(cfg.B):
+            for h in range(cfg.Hkv):
+                ref_codes[b, h, n - 1] = O.qavq_encode(keys[b, h, n - 1:n], f64(inp["codebook"])[h])[0]
+        out = torch.empty((cfg.B, cfg.Hq, 128), device="cuda")
+        sel = torch.full((cfg.B, cfg.Hkv, cfg.K), -1, dtype=torch.int32, device="cuda")
+        dec.step(n, [0, n], inp["q"].cuda(), kc, vc, out, sel_out=sel)
+        torch.cuda.synchronize()
+        check_step(cfg.with_(N=n), inp, [out.cpu().numpy()], [sel.cpu().numpy()], n, ref_codes)
+    dec.close()
