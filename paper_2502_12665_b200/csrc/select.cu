@@ -1551,8 +1551,10 @@ __global__ __launch_bounds__(kPAll, 1) void select_scan_kernel(const __grid_cons
 // scanned in token order: ascending emission with the tie quota, as in the code scan.
 constexpr int kQT = 256;             // postings select threads (16 codewords / thread, L <= 4096)
 constexpr int kQWords = 16;          // bitmap words per thread per segment (4096-word segments)
+constexpr int kQSurv = 512;          // survivors ranked directly (more: byte passes) -- keeps 4 CTAs / SM
 
 __global__ __launch_bounds__(kQT, 4) void select_postings_kernel(SelArgs a) {
+  A2ATS_TL(g_sel_tl, 0);
   extern __shared__ __align__(16) uint32_t sm[];
   __shared__ SelShared S;
   __shared__ int s_nh, s_tot;
@@ -1561,15 +1563,15 @@ __global__ __launch_bounds__(kQT, 4) void select_postings_kernel(SelArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, pair = blockIdx.x;
   const int L4 = (a.L + 3) & ~3;
   int* cnt = reinterpret_cast<int*>(sm);                    // [L4]
-  uint32_t* skey = sm + L4;                                 // [kTSurv] survivors
-  int* scnt = reinterpret_cast<int*>(skey + kTSurv);        // [kTSurv]
+  uint32_t* skey = sm + L4;                                 // [kQSurv] survivors
+  int* scnt = reinterpret_cast<int*>(skey + kQSurv);        // [kQSurv]
   const int ncand = max(0, a.c1 - a.c0), nwords = (ncand + 31) >> 5;
   const int nw4 = (nwords + 3) & ~3;
-  uint32_t* bab = sm + L4 + 2 * kTSurv;                     // [nw4] above-v* bitmap of the candidates
+  uint32_t* bab = sm + L4 + 2 * kQSurv;                     // [nw4] above-v* bitmap of the candidates
   uint32_t* bti = bab + nw4;                                // [nw4] tied bitmap
   // hit codes (alias cnt + survivors, dead after the level): code, prefix of the list lengths,
   // list start; capacity kHitCap (beyond it the list starts are read from global memory)
-  const int hcap = min(L4, (L4 * 4 + 2 * kTSurv * 4) / 14 / 4 * 4);
+  const int hcap = min(L4, (L4 * 4 + 2 * kQSurv * 4) / 14 / 4 * 4);
   uint16_t* hcode = reinterpret_cast<uint16_t*>(sm);
   int* hpre = reinterpret_cast<int*>(sm) + hcap / 2;
   int* hstart = hpre + hcap;
@@ -1585,10 +1587,12 @@ __global__ __launch_bounds__(kQT, 4) void select_postings_kernel(SelArgs a) {
   for (int i = tid; i < 2 * nw4; i += kQT) bab[i] = 0u;
   pdl_wait();  // agg comes from the prep kernel
   pdl_trigger();
+  A2ATS_TL(g_sel_tl, 2);
   if (a.wlog) store_window_logits<kQT>(a, pair, wacc);
   append_hist(a, pair, cp);
   uint32_t k[16], kstar, m;
-  level_regs<kQT, 16>(a, S, pair, c, k, skey, scnt, kTSurv, kstar, m);  // (ends synced: cnt dead)
+  level_regs<kQT, 16>(a, S, pair, c, k, skey, scnt, kQSurv, kstar, m);  // (ends synced: cnt dead)
+  A2ATS_TL(g_sel_tl, 3);
   // classes of this thread's 16 codewords; hit codes (class != 0, candidates present) compacted
   int e_unused = 0;
   const uint32_t x = class_bits<16>(k, c, kstar, e_unused);
@@ -1598,17 +1602,14 @@ __global__ __launch_bounds__(kQT, 4) void select_postings_kernel(SelArgs a) {
   for (int e = 0; e < 16; ++e)
     if (c[e] > 0 && k[e] <= kstar) hmask |= 1u << e;
   const int post0 = pair * (a.L + 1);
-  int len[16];
+  // the list bounds of this thread's 16 consecutive codewords: 17 independent loads in flight
+  int o[17];
+#pragma unroll
+  for (int e = 0; e < 17; ++e) o[e] = (tid * 16 + e <= a.L) ? __ldg(a.post_off + post0 + tid * 16 + e) : 0;
   int mylen = 0;
 #pragma unroll
-  for (int e = 0; e < 16; ++e) {
-    len[e] = 0;
-    if ((hmask >> e) & 1u) {
-      const int l = tid * 16 + e;
-      len[e] = __ldg(a.post_off + post0 + l + 1) - __ldg(a.post_off + post0 + l);
-      mylen += len[e];
-    }
-  }
+  for (int e = 0; e < 16; ++e)
+    if ((hmask >> e) & 1u) mylen += o[e + 1] - o[e];
   // block scans of (#hit codes, #entries)
   const int nh = __popc(hmask);
   int inh = nh, inl = mylen;
@@ -1635,18 +1636,18 @@ __global__ __launch_bounds__(kQT, 4) void select_postings_kernel(SelArgs a) {
     s_tot = bl + mylen;
   }
   __syncthreads();
+  A2ATS_TL(g_sel_tl, 6);
   const int nhit = s_nh, total = s_tot;
   const bool in_smem = nhit <= hcap;
   if (in_smem) {
 #pragma unroll
     for (int e = 0; e < 16; ++e)
       if ((hmask >> e) & 1u) {
-        const int l = tid * 16 + e;
-        hcode[bh] = (uint16_t)l;
+        hcode[bh] = (uint16_t)(tid * 16 + e);
         hpre[bh] = bl;
-        hstart[bh] = __ldg(a.post_off + post0 + l);
+        hstart[bh] = o[e];
         ++bh;
-        bl += len[e];
+        bl += o[e + 1] - o[e];
       }
   }
   __syncthreads();
@@ -1660,7 +1661,7 @@ __global__ __launch_bounds__(kQT, 4) void select_postings_kernel(SelArgs a) {
   // scattered by the hit codes themselves, after the per-hit arrays when it fits (else a binary
   // search over the prefix per block)
   int* bstart = hstart + hcap;
-  const bool use_bstart = in_smem && hcap * 10 + nblocks * 4 <= L4 * 4 + 2 * kTSurv * 4;
+  const bool use_bstart = in_smem && hcap * 10 + nblocks * 4 <= L4 * 4 + 2 * kQSurv * 4;
   if (use_bstart) {
     for (int h = tid; h < nhit; h += kQT) {
       const int e0 = hpre[h], e1 = (h + 1 < nhit) ? hpre[h + 1] : total;
@@ -1669,8 +1670,9 @@ __global__ __launch_bounds__(kQT, 4) void select_postings_kernel(SelArgs a) {
     if (tid == 0 && nhit > 0 && hpre[0] == 0 && nblocks > 0) bstart[0] = 0;
     __syncthreads();
   }
+  A2ATS_TL(g_sel_tl, 7);
   if (in_smem) {
-    constexpr int kU = 4;
+    constexpr int kU = 8;
     for (int b0 = warp; b0 < nblocks; b0 += (kQT / 32) * kU) {
       int tk[kU];
       int lc[kU];
@@ -1704,7 +1706,11 @@ __global__ __launch_bounds__(kQT, 4) void select_postings_kernel(SelArgs a) {
         if (t >= a.c0 && t < a.c1) {
           const int l = lc[u];
           const uint32_t cl = (s_cls[l >> 4] >> (2 * (l & 15))) & 3u;
+#ifdef A2ATS_POST_PLAIN_OR  // tuning builds only (racy: measures the cost of the atomics)
+          (cl == 1u ? bab : bti)[(t - a.c0) >> 5] |= 1u << ((t - a.c0) & 31);
+#else
           atomicOr((cl == 1u ? bab : bti) + ((t - a.c0) >> 5), 1u << ((t - a.c0) & 31));
+#endif
         }
       }
     }
@@ -1721,6 +1727,7 @@ __global__ __launch_bounds__(kQT, 4) void select_postings_kernel(SelArgs a) {
       }
     }
   }
+  A2ATS_TL(g_sel_tl, 4);
   // tokens not yet in the index: classified from their codes
   for (int t = max(a.n_post, a.c0) + tid; t < a.c1; t += kQT) {
     const int l = cp[t];
@@ -1728,6 +1735,7 @@ __global__ __launch_bounds__(kQT, 4) void select_postings_kernel(SelArgs a) {
     if (cl) atomicOr((cl == 1u ? bab : bti) + ((t - a.c0) >> 5), 1u << ((t - a.c0) & 31));
   }
   __syncthreads();
+  A2ATS_TL(g_sel_tl, 5);
   // ordered emission over segments of kQT * kQWords words (32 tokens each)
   int32_t* selp = a.sel + (size_t)pair * a.sel_stride;
   const uint32_t cap = (uint32_t)a.keff;
@@ -1804,6 +1812,7 @@ __global__ __launch_bounds__(kQT, 4) void select_postings_kernel(SelArgs a) {
     run_gt += tg;
     run_eq += te;
   }
+  A2ATS_TL(g_sel_tl, 1);
 }
 
 // Inverted index of tokens [0, n_tok) per pair: counts per code, exclusive prefix -> post_off,
@@ -1969,7 +1978,7 @@ bool select_pipe_ok(int L) { return L <= 4096; }
 
 size_t postings_smem_bytes(int L, int n_cand) {
   const size_t words = (size_t)(((n_cand + 31) / 32 + 3) & ~3);
-  const size_t base = (size_t)((L + 3) & ~3) * 4 + 2 * kTSurv * 4 + 2 * words * 4;
+  const size_t base = (size_t)((L + 3) & ~3) * 4 + 2 * kQSurv * 4 + 2 * words * 4;
   return std::max(base, (size_t)kWinScratch);
 }
 bool select_postings_ok(int L, int n_cand) { return L <= 4096 && postings_smem_bytes(L, n_cand) <= 200 * 1024; }
