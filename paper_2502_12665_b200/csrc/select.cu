@@ -1544,22 +1544,57 @@ __global__ __launch_bounds__(kPAll, 1) void select_scan_kernel(const __grid_cons
 // the codes above v* plus the first m tokens (by index) of the tied codes' lists (Q12): the
 // step reads only those lists (about K entries per pair) instead of every code.  One CTA per
 // pair: counts (hist - sinks/window) and the window-row logits before the dependency wait;
-// v*, m from the registers (level_regs); the hit codes compacted with the prefix of their list
-// lengths; every list entry e (threads stride the flattened entries, the code found by binary
-// search in the prefix) sets its candidate bit in the above or the tied bitmap; tokens
-// [n_post, c1) not yet in the index are classified from their codes; then the bitmaps are
-// scanned in token order: ascending emission with the tie quota, as in the code scan.
+// v*, m from the registers (level_regs); the hit codes compacted into a table (list start,
+// length, tied flag); a warp per hit code sets its list's candidate bits in the above or the
+// tied bitmap; tokens [n_post, c1) not yet in the index are classified from their codes; then
+// the bitmaps are scanned in token order (lanes on consecutive words, warp prefix of the
+// counts): ascending emission with the tie quota, as in the code scan.
 constexpr int kQT = 256;             // postings select threads (16 codewords / thread, L <= 4096)
 constexpr int kQWords = 16;          // bitmap words per thread per segment (4096-word segments)
 constexpr int kQSurv = 512;          // survivors ranked directly (more: byte passes) -- keeps 4 CTAs / SM
+constexpr int kQSinkMax = 64;        // list path: indexed sink tokens at most
+constexpr int kQTiedMax = 8;         // list path: codes at v* at most (their lists are merged by rank)
+
+// Block-wide exclusive scan of NV ints per thread (kQT threads): returns the exclusive prefix of
+// each value and the block totals (in tot).  Ends synced; part[NV][kQT / 32] is scratch.
+template <int NV>
+__device__ __forceinline__ void q_scan(const int (&v)[NV], int (&ex)[NV], int (&tot)[NV], int (*part)[kQT / 32]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int inc[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) inc[i] = v[i];
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1)
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int y = __shfl_up_sync(0xffffffffu, inc[i], off);
+      if (lane >= off) inc[i] += y;
+    }
+  __syncthreads();  // part reusable
+  if (lane == 31)
+#pragma unroll
+    for (int i = 0; i < NV; ++i) part[i][warp] = inc[i];
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    ex[i] = inc[i] - v[i];
+    tot[i] = 0;
+    for (int w = 0; w < kQT / 32; ++w) {
+      const int p = part[i][w];
+      if (w < warp) ex[i] += p;
+      tot[i] += p;
+    }
+  }
+}
 
 __global__ __launch_bounds__(kQT, 4) void select_postings_kernel(SelArgs a) {
   A2ATS_TL(g_sel_tl, 0);
   extern __shared__ __align__(16) uint32_t sm[];
   __shared__ SelShared S;
-  __shared__ int s_nh, s_tot;
   __shared__ uint32_t s_cls[256];    // compact 2-bit classes (code >> 4), L <= 4096
-  __shared__ uint32_t s_part[2][kQT / 32];
+  __shared__ int s_part[4][kQT / 32];
+  __shared__ uint16_t s_sk[kQSinkMax];          // codes of the indexed sink tokens (fast path)
+  __shared__ int s_ts[kQTiedMax], s_tn[kQTiedMax];  // tied codes' lists (fast path)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, pair = blockIdx.x;
   const int L4 = (a.L + 3) & ~3;
   int* cnt = reinterpret_cast<int*>(sm);                    // [L4]
@@ -1567,15 +1602,17 @@ __global__ __launch_bounds__(kQT, 4) void select_postings_kernel(SelArgs a) {
   int* scnt = reinterpret_cast<int*>(skey + kQSurv);        // [kQSurv]
   const int ncand = max(0, a.c1 - a.c0), nwords = (ncand + 31) >> 5;
   const int nw4 = (nwords + 3) & ~3;
-  uint32_t* bab = sm + L4 + 2 * kQSurv;                     // [nw4] above-v* bitmap of the candidates
+  uint32_t* bab = sm + L4 + 2 * kQSurv;                     // [nw4] above-v* bitmap (bitmap path)
   uint32_t* bti = bab + nw4;                                // [nw4] tied bitmap
-  // hit codes (alias cnt + survivors, dead after the level): code, prefix of the list lengths,
-  // list start; capacity kHitCap (beyond it the list starts are read from global memory)
-  const int hcap = min(L4, (L4 * 4 + 2 * kQSurv * 4) / 14 / 4 * 4);
-  uint16_t* hcode = reinterpret_cast<uint16_t*>(sm);
-  int* hpre = reinterpret_cast<int*>(sm) + hcap / 2;
-  int* hstart = hpre + hcap;
+  const int R = L4 + 2 * kQSurv;                            // words dead after the level (cnt + survivors)
   const uint16_t* cp = a.codes + (size_t)pair * a.n_max;
+  const int32_t* ptok = a.post_tok + (size_t)pair * a.n_max;
+  int32_t* selp = a.sel + (size_t)pair * a.sel_stride;
+  const uint32_t cap = (uint32_t)a.keff;
+  // list path: the index holds no window token and few sinks (the sinks of a list are its first
+  // entries: lists are ascending)
+  const int nsk = min(a.c0, a.n_post);
+  const bool list_ok = a.n_post <= a.c1 && nsk <= kQSinkMax;
   float wacc[512 / kQT];
   if (a.wlog) {  // the pair's window-row logits (step inputs; scratch aliases counts and bitmaps)
     window_logits<kQT>(a, pair, reinterpret_cast<uint8_t*>(sm), wacc);
@@ -1584,7 +1621,10 @@ __global__ __launch_bounds__(kQT, 4) void select_postings_kernel(SelArgs a) {
   load_cnt<kQT>(a, pair, cnt, cp);  // hist - sinks / window codes (step inputs)
   int c[16];
   load_c_regs<16>(a, cnt, c);
-  for (int i = tid; i < 2 * nw4; i += kQT) bab[i] = 0u;
+  if (list_ok && tid < nsk) s_sk[tid] = cp[tid];
+  const int post0 = pair * (a.L + 1);
+  if (tid * 32 <= a.L)  // the pair's list bounds (step inputs) into L2 while the LUT finishes
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(a.post_off + post0 + tid * 32));
   pdl_wait();  // agg comes from the prep kernel
   pdl_trigger();
   A2ATS_TL(g_sel_tl, 2);
@@ -1593,124 +1633,252 @@ __global__ __launch_bounds__(kQT, 4) void select_postings_kernel(SelArgs a) {
   uint32_t k[16], kstar, m;
   level_regs<kQT, 16>(a, S, pair, c, k, skey, scnt, kQSurv, kstar, m);  // (ends synced: cnt dead)
   A2ATS_TL(g_sel_tl, 3);
-  // classes of this thread's 16 codewords; hit codes (class != 0, candidates present) compacted
+  // classes of this thread's 16 codewords; hit codes (above or at v*, candidates present)
   int e_unused = 0;
   const uint32_t x = class_bits<16>(k, c, kstar, e_unused);
-  if (tid < 256) s_cls[tid] = x;
-  uint32_t hmask = 0u;
+  s_cls[tid] = x;
+  uint32_t hmask = 0u, tmask = 0u;
 #pragma unroll
   for (int e = 0; e < 16; ++e)
-    if (c[e] > 0 && k[e] <= kstar) hmask |= 1u << e;
-  const int post0 = pair * (a.L + 1);
-  // the list bounds of this thread's 16 consecutive codewords: 17 independent loads in flight
+    if (c[e] > 0 && k[e] <= kstar) {
+      hmask |= 1u << e;
+      if (k[e] == kstar) tmask |= 1u << e;
+    }
+  // the list bounds of this thread's 16 consecutive codewords: the row read coalesced into
+  // shared memory (element i at i + i / 16: thread t's 17 reads are conflict-free)
   int o[17];
+  {
+    int* orow = reinterpret_cast<int*>(sm);  // (cnt is dead) L + 1 + (L + 1) / 16 <= R words
+    for (int i = tid; i <= a.L; i += kQT) orow[i + (i >> 4)] = __ldg(a.post_off + post0 + i);
+    __syncthreads();
 #pragma unroll
-  for (int e = 0; e < 17; ++e) o[e] = (tid * 16 + e <= a.L) ? __ldg(a.post_off + post0 + tid * 16 + e) : 0;
-  int mylen = 0;
-#pragma unroll
-  for (int e = 0; e < 16; ++e)
-    if ((hmask >> e) & 1u) mylen += o[e + 1] - o[e];
-  // block scans of (#hit codes, #entries)
-  const int nh = __popc(hmask);
-  int inh = nh, inl = mylen;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const int y1 = __shfl_up_sync(0xffffffffu, inh, off), y2 = __shfl_up_sync(0xffffffffu, inl, off);
-    if (lane >= off) {
-      inh += y1;
-      inl += y2;
+    for (int e = 0; e < 17; ++e) o[e] = (tid * 16 + e <= a.L) ? orow[tid * 17 + e + (e >> 4)] : 0;
+  }
+  // sink entries at the head of each hit list (list path; lists are ascending): the codes of this
+  // thread holding a sink are counted in 4-bit fields (more than 15 sinks on one code: the
+  // bitmap path)
+  unsigned long long skp = 0ull;
+  bool skov = false;
+  for (int i = 0; i < nsk; ++i) {
+    const int code = s_sk[i];
+    if ((code >> 4) == tid) {
+      const int sh = 4 * (code & 15);
+      skov |= ((skp >> sh) & 15ull) == 15ull;
+      skp += 1ull << sh;
     }
   }
-  if (lane == 31) {
-    s_part[0][warp] = (uint32_t)inh;
-    s_part[1][warp] = (uint32_t)inl;
-  }
-  __syncthreads();
-  int bh = inh - nh, bl = inl - mylen;
-  for (int w = 0; w < warp; ++w) {
-    bh += (int)s_part[0][w];
-    bl += (int)s_part[1][w];
-  }
-  if (tid == kQT - 1) {
-    s_nh = bh + nh;
-    s_tot = bl + mylen;
-  }
-  __syncthreads();
+  const bool list_go = list_ok && !__syncthreads_or(skov);
+  auto skip_of = [&](int e) { return (int)((skp >> (4 * e)) & 15ull); };
+  // block scans: [0] above codes, [1] above entries, [2] tied codes, [3] tied entries; o[e]
+  // becomes the start of code e's candidate entries (past its sinks)
+  int v[4] = {0, 0, 0, 0}, ex[4], tot[4];
+#pragma unroll
+  for (int e = 0; e < 16; ++e)
+    if ((hmask >> e) & 1u) {
+      if (list_go) o[e] += skip_of(e);
+      const int n = o[e + 1] - o[e];
+      const int g = ((tmask >> e) & 1u) ? 2 : 0;
+      v[g] += 1;
+      v[g + 1] += n;
+    }
+  q_scan<4>(v, ex, tot, s_part);
   A2ATS_TL(g_sel_tl, 6);
-  const int nhit = s_nh, total = s_tot;
+  const int nA = tot[0], A_idx = tot[1], nT = tot[2], E_idx = tot[3];
+  const int hcap3 = R / 3;
+  if (list_go && nA <= hcap3 && nT <= kQTiedMax) {
+    // ---- list path: the selection in index order (no ordered emission):
+    //   [0, A_idx)        the above-v* codes' lists (code order; each ascending)
+    //   [A_idx, A)        the above-v* tail tokens [n_post, c1) (ascending)
+    //   [A, A + m)        the first m tied tokens in token order (tied lists merged, then the tail)
+    int* hs = reinterpret_cast<int*>(sm);  // above code h: list start (past its sinks)
+    int* hn = hs + hcap3;                  //               entries
+    int* hp = hn + hcap3;                  //               output position
+    {
+      int ih = ex[0], ip = ex[1], it = ex[2];
+#pragma unroll
+      for (int e = 0; e < 16; ++e)
+        if ((hmask >> e) & 1u) {
+          // (o[e + 1] was advanced past code e + 1's sinks if that code is a hit)
+          const int n = o[e + 1] - o[e] - (e < 15 && ((hmask >> (e + 1)) & 1u) ? skip_of(e + 1) : 0);
+          if ((tmask >> e) & 1u) {
+            s_ts[it] = o[e];
+            s_tn[it] = n;
+            ++it;
+          } else {
+            hs[ih] = o[e];
+            hn[ih] = n;
+            hp[ih] = ip;
+            ++ih;
+            ip += n;
+          }
+        }
+    }
+    __syncthreads();
+    A2ATS_TL(g_sel_tl, 7);
+    // above lists -> output.  Staged: every entry fetched by cp.async into shared memory at its
+    // output position (the bitmaps' space: 2 nw4 words), one wait, then coalesced stores.
+    // Otherwise a warp per code (entries lane, lane + 32 together), kU codes in flight.
+    if (A_idx <= 2 * nw4) {
+      int* stg = reinterpret_cast<int*>(bab);
+      const int sub = lane & 7;  // groups of 8 lanes, a code each (lists average N / L entries)
+      for (int h = (warp << 2) + (lane >> 3); h < nA; h += (kQT / 32) * 4) {
+        const int n = hn[h];
+        const int32_t* src = ptok + hs[h] + sub;
+        uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(stg + hp[h] + sub));
+        for (int j = sub; j < n; j += 8, src += 8, d += 32)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
+      }
+      cp_async_commit();
+      cp_async_wait<0>();
+      __syncthreads();
+      const int lim = min(A_idx, (int)cap);
+      for (int i = tid; i < lim; i += kQT) selp[i] = stg[i];
+    } else {
+      constexpr int kU = 8, kW = kQT / 32;
+      for (int h0 = warp; h0 < nA; h0 += kW * kU) {
+        int tk[kU][2];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int h = h0 + u * kW;
+          tk[u][0] = tk[u][1] = 0;
+          if (h < nA) {
+            const int st = hs[h], n = hn[h];
+            if (lane < n) tk[u][0] = __ldg(ptok + st + lane);
+            if (lane + 32 < n) tk[u][1] = __ldg(ptok + st + lane + 32);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int h = h0 + u * kW;
+          if (h < nA) {
+            const int st = hs[h], n = hn[h], p = hp[h];
+            if (lane < n && (uint32_t)(p + lane) < cap) selp[p + lane] = tk[u][0];
+            if (lane + 32 < n && (uint32_t)(p + lane + 32) < cap) selp[p + lane + 32] = tk[u][1];
+            for (int j = 64 + lane; j < n; j += 32)
+              if ((uint32_t)(p + j) < cap) selp[p + j] = __ldg(ptok + st + j);
+          }
+        }
+      }
+    }
+    A2ATS_TL(g_sel_tl, 4);
+    // tail [max(n_post, c0), c1): classified from codes; counts first (A needs the above count)
+    const int tb0 = max(a.n_post, a.c0);
+    int tA = 0, tT = 0;
+    for (int t = tb0 + tid; t < a.c1; t += kQT) {
+      const int l = cp[t];
+      const uint32_t cl = (s_cls[l >> 4] >> (2 * (l & 15))) & 3u;
+      tA += cl == 1u;
+      tT += cl == 2u;
+    }
+    tA = __reduce_add_sync(0xffffffffu, tA);
+    tT = __reduce_add_sync(0xffffffffu, tT);
+    __syncthreads();
+    if (lane == 0) {
+      s_part[0][warp] = tA;
+      s_part[1][warp] = tT;
+    }
+    __syncthreads();
+    int A = A_idx;
+    for (int w = 0; w < kQT / 32; ++w) A += s_part[0][w];
+    if (tb0 < a.c1) {  // ordered compaction of the tail, kQT tokens per round
+      int runA = A_idx, runT = 0;
+      for (int base = tb0; base < a.c1; base += kQT) {
+        const int t = base + tid;
+        uint32_t cl = 0u;
+        if (t < a.c1) {
+          const int l = cp[t];
+          cl = (s_cls[l >> 4] >> (2 * (l & 15))) & 3u;
+        }
+        const int vv[2] = {cl == 1u, cl == 2u};
+        int e2[2], t2[2];
+        q_scan<2>(vv, e2, t2, s_part);
+        if (cl == 1u && (uint32_t)(runA + e2[0]) < cap) selp[runA + e2[0]] = t;
+        if (cl == 2u) {
+          const int r = E_idx + runT + e2[1];  // tie index
+          if (r < (int)m && (uint32_t)(A + r) < cap) selp[A + r] = t;
+        }
+        runA += t2[0];
+        runT += t2[1];
+      }
+    }
+    // the indexed ties: tie index of an entry = its rank in the merge of the tied lists
+    if (nT == 1) {
+      const int st = s_ts[0], n = min(s_tn[0], (int)m);
+      for (int j = tid; j < n; j += kQT)
+        if ((uint32_t)(A + j) < cap) selp[A + j] = __ldg(ptok + st + j);
+    } else {
+      for (int g = 0; g < nT; ++g) {
+        const int st = s_ts[g], n = s_tn[g];
+        for (int j = tid; j < n; j += kQT) {
+          const int t = __ldg(ptok + st + j);
+          int r = j;
+          for (int g2 = 0; g2 < nT; ++g2) {
+            if (g2 == g) continue;
+            int lo = 0, hi = s_tn[g2];  // #entries of list g2 below t
+            const int32_t* q2 = ptok + s_ts[g2];
+            while (lo < hi) {
+              const int mid = (lo + hi) >> 1;
+              if (__ldg(q2 + mid) < t) lo = mid + 1;
+              else hi = mid;
+            }
+            r += lo;
+          }
+          if (r < (int)m && (uint32_t)(A + r) < cap) selp[A + r] = t;
+        }
+      }
+    }
+    A2ATS_TL(g_sel_tl, 5);
+    A2ATS_TL(g_sel_tl, 1);
+    return;
+  }
+  // ---- bitmap path (sinks / window tokens in the index, or very many hit / tied codes):
+  // candidate bits in an above and a tied bitmap, then an ordered emission over the bitmaps
+  const int nhit = nA + nT, hcap = R / 2;
+  int* hs = reinterpret_cast<int*>(sm);  // hit code h: list start
+  int* hl = hs + hcap;                   //             length | bit 31 if tied at v*
+  for (int i = tid; i < 2 * nw4; i += kQT) bab[i] = 0u;
+  int bh = ex[0] + ex[2];
   const bool in_smem = nhit <= hcap;
   if (in_smem) {
 #pragma unroll
     for (int e = 0; e < 16; ++e)
       if ((hmask >> e) & 1u) {
-        hcode[bh] = (uint16_t)(tid * 16 + e);
-        hpre[bh] = bl;
-        hstart[bh] = o[e];
+        hs[bh] = o[e];
+        hl[bh] = (o[e + 1] - o[e]) | ((((x >> (2 * e)) & 3u) == 2u) ? (int)0x80000000 : 0);
         ++bh;
-        bl += o[e + 1] - o[e];
       }
   }
   __syncthreads();
-  // flattened list entries -> candidate bits (entries outside [c0, c1) are sinks / window):
-  // warps take blocks of 32 consecutive entries (lane j: entry E + j); the block's first hit code
-  // comes from one binary search over the prefix (same address in every lane: broadcast), each
-  // lane then walks the few codes the block spans; 4 blocks per pass keep 4 list loads in flight
-  const int32_t* ptok = a.post_tok + (size_t)pair * a.n_max;
-  const int nblocks = (total + 31) >> 5;
-  // first hit code of every 32-entry block (the code whose list holds entry 32 b): bstart[b],
-  // scattered by the hit codes themselves, after the per-hit arrays when it fits (else a binary
-  // search over the prefix per block)
-  int* bstart = hstart + hcap;
-  const bool use_bstart = in_smem && hcap * 10 + nblocks * 4 <= L4 * 4 + 2 * kQSurv * 4;
-  if (use_bstart) {
-    for (int h = tid; h < nhit; h += kQT) {
-      const int e0 = hpre[h], e1 = (h + 1 < nhit) ? hpre[h + 1] : total;
-      for (int b = (e0 + 31) >> 5; (b << 5) < e1; ++b) bstart[b] = h;
-    }
-    if (tid == 0 && nhit > 0 && hpre[0] == 0 && nblocks > 0) bstart[0] = 0;
-    __syncthreads();
-  }
   A2ATS_TL(g_sel_tl, 7);
+  // list entries -> candidate bits (entries outside [c0, c1) are sinks / window): a warp per hit
+  // code, lanes over its list (entries lane, lane + 32 loaded together); kU codes per warp in
+  // flight; longer lists loop
+  auto set_bit = [&](int t, bool tied) {
+    if (t >= a.c0 && t < a.c1) atomicOr((tied ? bti : bab) + ((t - a.c0) >> 5), 1u << ((t - a.c0) & 31));
+  };
   if (in_smem) {
-    constexpr int kU = 8;
-    for (int b0 = warp; b0 < nblocks; b0 += (kQT / 32) * kU) {
-      int tk[kU];
-      int lc[kU];
+    constexpr int kU = 8, kW = kQT / 32;
+    for (int h0 = warp; h0 < nhit; h0 += kW * kU) {
+      int tk[kU][2];
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
-        const int blk = b0 + u * (kQT / 32), E = blk * 32, e = E + lane;
-        tk[u] = -1;
-        lc[u] = 0;
-        if (blk < nblocks) {
-          int lo = 0;
-          if (use_bstart) {
-            lo = bstart[blk];
-          } else {
-            int hi = nhit - 1;
-            while (lo < hi) {
-              const int mid = (lo + hi + 1) >> 1;
-              if (hpre[mid] <= E) lo = mid;
-              else hi = mid - 1;
-            }
-          }
-          while (lo + 1 < nhit && hpre[lo + 1] <= e) ++lo;
-          if (e < total) {
-            lc[u] = hcode[lo];
-            tk[u] = __ldg(ptok + hstart[lo] + (e - hpre[lo]));
-          }
+        const int h = h0 + u * kW;
+        tk[u][0] = tk[u][1] = -1;
+        if (h < nhit) {
+          const int st = hs[h], len = hl[h] & 0x7fffffff;
+          if (lane < len) tk[u][0] = __ldg(ptok + st + lane);
+          if (lane + 32 < len) tk[u][1] = __ldg(ptok + st + lane + 32);
         }
       }
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
-        const int t = tk[u];
-        if (t >= a.c0 && t < a.c1) {
-          const int l = lc[u];
-          const uint32_t cl = (s_cls[l >> 4] >> (2 * (l & 15))) & 3u;
-#ifdef A2ATS_POST_PLAIN_OR  // tuning builds only (racy: measures the cost of the atomics)
-          (cl == 1u ? bab : bti)[(t - a.c0) >> 5] |= 1u << ((t - a.c0) & 31);
-#else
-          atomicOr((cl == 1u ? bab : bti) + ((t - a.c0) >> 5), 1u << ((t - a.c0) & 31));
-#endif
+        const int h = h0 + u * kW;
+        if (h < nhit) {
+          const int st = hs[h], len = hl[h] & 0x7fffffff;
+          const bool tied = hl[h] < 0;
+          set_bit(tk[u][0], tied);
+          set_bit(tk[u][1], tied);
+          for (int j = 64 + lane; j < len; j += 32) set_bit(__ldg(ptok + st + j), tied);
         }
       }
     }
@@ -1718,13 +1886,9 @@ __global__ __launch_bounds__(kQT, 4) void select_postings_kernel(SelArgs a) {
 #pragma unroll 1
     for (int e = 0; e < 16; ++e) {
       if (!((hmask >> e) & 1u)) continue;
-      const int l = tid * 16 + e;
-      const uint32_t cl = (s_cls[l >> 4] >> (2 * (l & 15))) & 3u;
-      const int b0 = __ldg(a.post_off + post0 + l), b1 = __ldg(a.post_off + post0 + l + 1);
-      for (int i = b0; i < b1; ++i) {
-        const int t = __ldg(ptok + i);
-        if (t >= a.c0 && t < a.c1) atomicOr((cl == 1u ? bab : bti) + ((t - a.c0) >> 5), 1u << ((t - a.c0) & 31));
-      }
+      const bool tied = ((x >> (2 * e)) & 3u) == 2u;
+      const int l = tid * 16 + e, i1 = __ldg(a.post_off + post0 + l + 1);
+      for (int i = __ldg(a.post_off + post0 + l); i < i1; ++i) set_bit(__ldg(ptok + i), tied);
     }
   }
   A2ATS_TL(g_sel_tl, 4);
@@ -1732,41 +1896,35 @@ __global__ __launch_bounds__(kQT, 4) void select_postings_kernel(SelArgs a) {
   for (int t = max(a.n_post, a.c0) + tid; t < a.c1; t += kQT) {
     const int l = cp[t];
     const uint32_t cl = (s_cls[l >> 4] >> (2 * (l & 15))) & 3u;
-    if (cl) atomicOr((cl == 1u ? bab : bti) + ((t - a.c0) >> 5), 1u << ((t - a.c0) & 31));
+    if (cl) set_bit(t, cl == 2u);
   }
   __syncthreads();
   A2ATS_TL(g_sel_tl, 5);
-  // ordered emission over segments of kQT * kQWords words (32 tokens each)
-  int32_t* selp = a.sel + (size_t)pair * a.sel_stride;
-  const uint32_t cap = (uint32_t)a.keff;
+  // ordered emission.  Segments of kQT * kQWords words; warp w takes words [512 w, 512 w + 512)
+  // of the segment, lane l word 32 i + l at step i (consecutive lanes: consecutive words and
+  // nearby output positions).  Selected bits of a word: the above-v* bits and the tied bits of
+  // tie index < m; they go, in token order, to #above-before + min(#tied-before, m) onwards.
   uint32_t run_gt = 0u, run_eq = 0u;
   for (int seg = 0; seg < nwords; seg += kQT * kQWords) {
-    const int w0 = seg + tid * kQWords;
+    const int wb = seg + warp * (32 * kQWords);
     uint32_t ng = 0u, ne = 0u;
 #pragma unroll
-    for (int i = 0; i < kQWords; ++i) {  // rotated order: the warp's lanes hit distinct banks
-      const int w = w0 + ((i + tid) & (kQWords - 1));
+    for (int i = 0; i < kQWords; ++i) {
+      const int w = wb + 32 * i + lane;
       if (w < nwords) {
         ng += __popc(bab[w]);
         ne += __popc(bti[w]);
       }
     }
-    uint32_t ig = ng, ie = ne;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const uint32_t y1 = __shfl_up_sync(0xffffffffu, ig, off), y2 = __shfl_up_sync(0xffffffffu, ie, off);
-      if (lane >= off) {
-        ig += y1;
-        ie += y2;
-      }
-    }
+    ng = __reduce_add_sync(0xffffffffu, ng);
+    ne = __reduce_add_sync(0xffffffffu, ne);
     __syncthreads();  // the previous segment's s_part reads are done
-    if (lane == 31) {
-      s_part[0][warp] = ig;
-      s_part[1][warp] = ie;
+    if (lane == 0) {
+      s_part[0][warp] = ng;
+      s_part[1][warp] = ne;
     }
     __syncthreads();
-    uint32_t gb = run_gt + ig - ng, eb = run_eq + ie - ne, tg = 0u, te = 0u;
+    uint32_t gb = run_gt, eb = run_eq, tg = 0u, te = 0u;
     for (int w = 0; w < kQT / 32; ++w) {
       const uint32_t pg = s_part[0][w], pe = s_part[1][w];
       if (w < warp) {
@@ -1778,36 +1936,36 @@ __global__ __launch_bounds__(kQT, 4) void select_postings_kernel(SelArgs a) {
     }
 #pragma unroll 1
     for (int i = 0; i < kQWords; ++i) {
-      const int w = w0 + i;
-      if (w >= nwords) break;
-      uint32_t ga = bab[w], gt = bti[w];
-      const int tb = a.c0 + w * 32;
-      if ((ga | gt) == 0u) continue;
-      if (gt == 0u) {  // above v* only: positions gb + min(eb, m) .. + n - 1, ascending
-        const uint32_t pos = gb + min(eb, m);
-        uint32_t n = 0u;
-        while (ga) {
-          const int bit = __ffs(ga) - 1;
-          ga &= ga - 1u;
-          if (pos + n < cap) selp[pos + n] = tb + bit;
-          ++n;
-        }
-        gb += n;
-        continue;
+      const int w = wb + 32 * i + lane;
+      if (wb + 32 * i >= nwords) break;  // (warp-uniform)
+      uint32_t A = 0u, T = 0u;
+      if (w < nwords) {
+        A = bab[w];
+        T = bti[w];
       }
-      uint32_t all = ga | gt;
-      while (all) {  // in token order: above -> gb + min(eb, m); tied -> kept iff eb < m
-        const int bit = __ffs(all) - 1;
-        all &= all - 1u;
-        if ((ga >> bit) & 1u) {
-          const uint32_t pos = gb + min(eb, m);
-          if (pos < cap) selp[pos] = tb + bit;
-          ++gb;
-        } else {
-          if (eb < m && gb + eb < cap) selp[gb + eb] = tb + bit;
-          ++eb;
-        }
+      const uint32_t pa = __popc(A), pt = __popc(T);
+      uint32_t incl = pa | (pt << 16);  // <= 32 * 32 per field
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += y;
       }
+      const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+      const uint32_t ab = gb + (incl & 0xffffu) - pa, tb_ = eb + (incl >> 16) - pt;
+      if (T) {  // keep the tied bits of tie index < m (all, none, or a prefix at the boundary)
+        const uint32_t keep = m > tb_ ? m - tb_ : 0u;
+        for (uint32_t d = pt > keep ? pt - keep : 0u; d > 0u; --d) T &= ~(0x80000000u >> __clz(T));
+      }
+      uint32_t S = A | T, pos = ab + min(tb_, m);
+      const int tok0 = a.c0 + w * 32;
+      while (S) {
+        const int bit = __ffs(S) - 1;
+        S &= S - 1u;
+        if (pos < cap) selp[pos] = tok0 + bit;
+        ++pos;
+      }
+      gb += tot & 0xffffu;
+      eb += tot >> 16;
     }
     run_gt += tg;
     run_eq += te;
@@ -1815,27 +1973,31 @@ __global__ __launch_bounds__(kQT, 4) void select_postings_kernel(SelArgs a) {
   A2ATS_TL(g_sel_tl, 1);
 }
 
-// Inverted index of tokens [0, n_tok) per pair: counts per code, exclusive prefix -> post_off,
-// tokens scattered into their code's list (order inside a list is irrelevant to the selection,
-// which goes through bitmaps).
-constexpr int kBT = 1024;
-__global__ __launch_bounds__(kBT) void postings_build_kernel(const uint16_t* __restrict__ codes, int n_max, int L,
-                                                             int n_tok, int32_t* __restrict__ post_off,
-                                                             int32_t* __restrict__ post_tok) {
-  extern __shared__ __align__(16) int pbuf[];  // cnt [L], cursor [L]
-  __shared__ int s_w[kBT / 32];
+
+// Inverted index of tokens [0, n_tok) per pair, every list ascending (deterministic): warp w
+// owns the contiguous tokens [w n / kBW, (w + 1) n / kBW); per-(warp, code) counts -> cursors
+// (code-major exclusive prefix: post_off, then the warps in order) -> each warp places its
+// tokens in order, 32 per step, ranks among equal codes of a step from match_any.
+constexpr int kBW = 8;
+__global__ __launch_bounds__(kBW * 32) void postings_build_kernel(const uint16_t* __restrict__ codes, int n_max, int L,
+                                                                  int n_tok, int32_t* __restrict__ post_off,
+                                                                  int32_t* __restrict__ post_tok) {
+  extern __shared__ __align__(16) int pcnt[];  // [kBW][L]: counts, then cursors
+  __shared__ int s_w[kBW];
+  constexpr int NT = kBW * 32;
   const int pair = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  int* cnt = pbuf;
-  int* cur = pbuf + L;
   const uint16_t* cp = codes + (size_t)pair * n_max;
-  for (int l = tid; l < L; l += kBT) cnt[l] = 0;
+  for (int i = tid; i < kBW * L; i += NT) pcnt[i] = 0;
   __syncthreads();
-  for (int t = tid; t < n_tok; t += kBT) atomicAdd(&cnt[cp[t]], 1);
+  const int per = (n_tok + kBW - 1) / kBW, t0 = min(n_tok, warp * per), t1 = min(n_tok, t0 + per);
+  int* my = pcnt + warp * L;
+  for (int t = t0 + lane; t < t1; t += 32) atomicAdd(&my[cp[t]], 1);
   __syncthreads();
-  // exclusive prefix over L codes: thread owns a contiguous run of ceil(L / kBT)
-  const int per = (L + kBT - 1) / kBT, l0 = tid * per;
+  // thread owns codes [l0, l0 + pc): its total, block scan, then the cursors
+  const int pc = (L + NT - 1) / NT, l0 = tid * pc;
   int s = 0;
-  for (int i = 0; i < per && l0 + i < L; ++i) s += cnt[l0 + i];
+  for (int i = 0; i < pc && l0 + i < L; ++i)
+    for (int w = 0; w < kBW; ++w) s += pcnt[w * L + l0 + i];
   int incl = s;
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
@@ -1844,18 +2006,37 @@ __global__ __launch_bounds__(kBT) void postings_build_kernel(const uint16_t* __r
   }
   if (lane == 31) s_w[warp] = incl;
   __syncthreads();
-  int base = incl - s;
-  for (int w = 0; w < warp; ++w) base += s_w[w];
-  int32_t* offp = post_off + (size_t)pair * (L + 1);
-  for (int i = 0; i < per && l0 + i < L; ++i) {
-    offp[l0 + i] = base;
-    cur[l0 + i] = base;
-    base += cnt[l0 + i];
+  int base = incl - s, total = 0;
+  for (int w = 0; w < kBW; ++w) {
+    if (w < warp) base += s_w[w];
+    total += s_w[w];
   }
-  if (tid == kBT - 1) offp[L] = base;
+  int32_t* offp = post_off + (size_t)pair * (L + 1);
+  for (int i = 0; i < pc && l0 + i < L; ++i) {
+    offp[l0 + i] = base;
+    for (int w = 0; w < kBW; ++w) {
+      const int cnt = pcnt[w * L + l0 + i];
+      pcnt[w * L + l0 + i] = base;
+      base += cnt;
+    }
+  }
+  if (tid == 0) offp[L] = total;
   __syncthreads();
   int32_t* tp = post_tok + (size_t)pair * n_max;
-  for (int t = tid; t < n_tok; t += kBT) tp[atomicAdd(&cur[cp[t]], 1)] = t;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int tb = t0; tb < t1; tb += 32) {
+    const int t = tb + lane;
+    const int code = t < t1 ? (int)cp[t] : -1 - lane;  // (inactive lanes: unique keys)
+    const unsigned peers = __match_any_sync(0xffffffffu, code);
+    int b = 0;
+    if (t < t1) {
+      b = my[code];
+      tp[b + __popc(peers & lt)] = t;
+    }
+    __syncwarp();
+    if (t < t1 && (peers & lt) == 0u) my[code] = b + __popc(peers);
+    __syncwarp();
+  }
 }
 
 size_t shard_thresh_smem_bytes(int L) { return (size_t)((L + 3) & ~3) * 8 + 2 * kTSurv * 4; }
@@ -1992,10 +2173,11 @@ cudaError_t launch_select_postings(const SelArgs& a, cudaStream_t st) {
 
 cudaError_t launch_postings_build(const uint16_t* codes, int P, int n_max, int L, int n_tok, int32_t* post_off,
                                   int32_t* post_tok, cudaStream_t st) {
-  const int smem = 2 * L * 4;
+  const int smem = kBW * L * 4;
   cudaError_t e = ensure_smem(postings_build_kernel, smem);
   if (e != cudaSuccess) return e;
-  return launch_pdl(postings_build_kernel, dim3(P), dim3(kBT), smem, st, codes, n_max, L, n_tok, post_off, post_tok);
+  return launch_pdl(postings_build_kernel, dim3(P), dim3(kBW * 32), smem, st, codes, n_max, L, n_tok, post_off,
+                    post_tok);
 }
 
 cudaError_t launch_select_shard(const SelArgs& a, const CUtensorMap& tmK, int nblk, cudaStream_t st) {

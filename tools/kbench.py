@@ -24,6 +24,7 @@ ap.add_argument("--L", type=int, default=0)
 ap.add_argument("--N", type=int, default=0)
 ap.add_argument("--select-only", action="store_true", help="a2ats_select_topk (a1..a4) only")
 ap.add_argument("--postings", action="store_true", help="posting-list selection engine (f3)")
+ap.add_argument("--post-lag", type=int, default=256, help="tokens behind the window start the index was built at")
 args = ap.parse_args()
 cfg = CONFIGS[args.config]
 if args.batch:
@@ -51,7 +52,7 @@ c0 = codes[:, :, :cfg.N - 1].to(torch.int64)
 hist0.zero_().scatter_add_(2, c0, torch.ones_like(c0, dtype=torch.int32))
 sel_buf = torch.empty((cfg.B, cfg.Hkv, max(cfg.K, 1)), dtype=torch.int32, device="cuda")
 if args.postings:
-    dec.build_postings(cfg.N - 1)
+    dec.build_postings(cfg.N - cfg.window - args.post_lag)
 for it in range(args.iters if args.select_only else 0):
     flush.fill_(it)
     e0.record()
