@@ -252,12 +252,20 @@ int a2ats_decode_step_append(const a2ats_shape* shape, const a2ats_params* param
  * tokens (lowest index, reading Q12) of the tied codes' lists: the selection
  * reads about K list entries per pair instead of every code.  The index is
  * query-independent: a2ats_postings_build groups the tokens [0, n_tokens) of
- * every pair by code (postings: a2ats_postings_bytes of device memory =
- * int32 offsets [B*Hkv, L+1] then int32 tokens [B*Hkv, n_max], caller-owned);
- * tokens [n_post, n_ctx) not yet in the index are classified from codes.
+ * every pair by code, each list ascending (deterministic; postings:
+ * a2ats_postings_bytes of device memory = int32 offsets [B*Hkv, L+1], then,
+ * 256-byte aligned, int32 tokens [B*Hkv, n_max], caller-owned); tokens
+ * [n_post, n_ctx) not yet in the index are classified from their codes.
  * a2ats_select_topk_postings / a2ats_decode_step_postings = a2ats_select_topk /
  * a2ats_decode_step with that selection (hist required, L <= 4096, 0 <= n_post
- * <= n_ctx; the results are identical: same sets, same order).
+ * <= n_ctx): the SAME SET per pair as the code scan.  Order of sel_out:
+ *   n_post <= n_ctx - window (the index holds no window token; at most 64
+ *   indexed sinks): index order -- the above-v* codes' lists (code order,
+ *   each ascending), the above-v* unindexed tokens, then the m selected ties
+ *   ascending; deterministic for a given index;
+ *   otherwise: ascending, as a2ats_select_topk.
+ * The attention output equals a2ats_decode_step's up to the summation order
+ * of the rows (fp32 rounding).
  * ------------------------------------------------------------------- */
 size_t a2ats_postings_bytes(const a2ats_shape* shape);
 int a2ats_postings_build(const a2ats_shape* shape, const uint16_t* codes, int32_t n_tokens, void* postings,
