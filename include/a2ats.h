@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define A2ATS_ABI_VERSION 7
+#define A2ATS_ABI_VERSION 8
 
 /* ---- status codes ---------------------------------------------------- */
 #define A2ATS_OK 0
@@ -278,6 +278,17 @@ int a2ats_decode_step_postings(const a2ats_shape* shape, const a2ats_params* par
                                const void* k_cache, const void* v_cache, const uint16_t* codes,
                                const void* codebook, const int32_t* hist, const void* postings, int32_t n_post,
                                float* out, int32_t* sel_out, void* ws, size_t ws_bytes, void* stream);
+/* One decode step of the paper with the posting-list selection: a0 for token
+ * n_ctx-1 (as a2ats_decode_step_append: its code into codes, +1 into hist)
+ * fused with a1..a6 over the index.  0 <= n_post <= n_ctx-1 (the new token is
+ * never in the index); tokens [n_post, n_ctx) are classified from their codes,
+ * so the caller rebuilds the index (a2ats_postings_build) as often as it likes
+ * -- the result does not depend on n_post.  EINVAL / EUNSUPPORTED as above. */
+int a2ats_decode_step_append_postings(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx,
+                                      const void* q, const void* k_cache, const void* v_cache, uint16_t* codes,
+                                      const void* codebook, int32_t* hist, const void* chat, const float* nrm,
+                                      const void* postings, int32_t n_post, float* out, int32_t* sel_out, void* ws,
+                                      size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------
  * Sequence-sharded decode step (the paper itself

@@ -74,7 +74,7 @@ _SIGS = {
 _lib = None
 
 
-ABI_VERSION = 7  # include/a2ats.h A2ATS_ABI_VERSION
+ABI_VERSION = 8  # include/a2ats.h A2ATS_ABI_VERSION
 
 
 def load(path: str = LIB_PATH, build_if_missing: bool = True) -> ctypes.CDLL:
@@ -435,10 +435,12 @@ _SIGS.update({
                                                   _VP, _VP, _SZ, _VP]),
     "a2ats_decode_step_postings": (ctypes.c_int, [_SP, _PP, ctypes.c_int32, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
                                                   ctypes.c_int32, _VP, _VP, _VP, _SZ, _VP]),
+    "a2ats_decode_step_append_postings": (ctypes.c_int, [_SP, _PP, ctypes.c_int32, _VP, _VP, _VP, _VP, _VP, _VP,
+                                                         _VP, _VP, _VP, ctypes.c_int32, _VP, _VP, _VP, _SZ, _VP]),
 })
 if _lib is not None:
     for _n in ("a2ats_postings_bytes", "a2ats_postings_build", "a2ats_select_topk_postings",
-               "a2ats_decode_step_postings"):
+               "a2ats_decode_step_postings", "a2ats_decode_step_append_postings"):
         _f = getattr(_lib, _n)
         _f.restype, _f.argtypes = _SIGS[_n]
 
@@ -478,3 +480,18 @@ def a2ats_decode_step_postings(shape, params, n_ctx, q, k_cache, v_cache, codes,
         _ptr(sel_out, "sel_out", torch.int32, optional=True), _ptr(ws, "ws"), ws.numel() * ws.element_size(),
         _stream(stream))
     _check("a2ats_decode_step_postings", rc)
+
+
+def a2ats_decode_step_append_postings(shape, params, n_ctx, q, k_cache, v_cache, codes, codebook, hist, chat, nrm,
+                                      postings, n_post, out, sel_out, ws, stream=None):
+    import torch
+    p = params.c() if isinstance(params, Params) else params
+    rc = load().a2ats_decode_step_append_postings(
+        ctypes.byref(shape), ctypes.byref(p), int(n_ctx), _ptr(q, "q", torch.bfloat16),
+        _ptr(k_cache, "k_cache", torch.bfloat16), _ptr(v_cache, "v_cache", torch.bfloat16),
+        _ptr(codes, "codes", torch.uint16), _ptr(codebook, "codebook", torch.bfloat16), _ptr(hist, "hist", torch.int32),
+        _ptr(chat, "chat", torch.bfloat16), _ptr(nrm, "nrm", torch.float32), _ptr(postings, "postings"),
+        int(n_post), _ptr(out, "out", torch.float32, host_ok="pinned"),
+        _ptr(sel_out, "sel_out", torch.int32, optional=True), _ptr(ws, "ws"), ws.numel() * ws.element_size(),
+        _stream(stream))
+    _check("a2ats_decode_step_append_postings", rc)

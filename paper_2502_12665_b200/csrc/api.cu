@@ -124,7 +124,7 @@ void derive(const a2ats_shape* s, const a2ats_params* p, int n_ctx, Derived* d) 
 }
 
 struct DecodeWs {
-  size_t cs, agg, lut, sel, part, actr, pinfo, nsel, wlog, eslot, ectr, tblg, desc, tick, qt, total;
+  size_t cs, agg, lut, sel, part, actr, pinfo, nsel, wlog, eslot, ectr, tblg, desc, tick, qt, pbits, total;
 };
 
 DecodeWs decode_layout(const a2ats_shape* s, const a2ats_params* p) {
@@ -157,6 +157,7 @@ DecodeWs decode_layout(const a2ats_shape* s, const a2ats_params* p) {
     const int NV = lut_tile_nv(s->B * G), nvt = (s->B * G + NV - 1) / NV;
     w.qt = o; o = align_up(o + qprep_bytes(s->Hkv, nvt, NV));                                // q~ B tiles
   }
+  w.pbits = o; o = align_up(o + (size_t)P * postings_bits_stride(s->n_max) * 4);             // postings bitmap path
   w.total = o;
   return w;
 }
@@ -641,6 +642,8 @@ int decode_impl(const a2ats_shape* shape, const a2ats_params* params, int32_t n_
       sa.post_off = reinterpret_cast<const int32_t*>(static_cast<const uint8_t*>(postings) + pl.off);
       sa.post_tok = reinterpret_cast<const int32_t*>(static_cast<const uint8_t*>(postings) + pl.tok);
       sa.n_post = n_post;
+      sa.pbits = reinterpret_cast<uint32_t*>(base + Lw.pbits);
+      sa.pbits_stride = postings_bits_stride(shape->n_max);
     }
     rc = cuda_status(post_select    ? launch_select_postings(sa, st)
                      : pipe_select  ? launch_select_pipe(sa, tmK, std::min(sm_count(), 2 * d.P), st)
@@ -762,6 +765,18 @@ int a2ats_decode_step_postings(const a2ats_shape* shape, const a2ats_params* par
   return decode_impl(shape, params, n_ctx, q, k_cache, v_cache, const_cast<uint16_t*>(codes), codebook,
                      const_cast<int32_t*>(hist), nullptr, nullptr, out, sel_out, nullptr, ws, ws_bytes, stream, true,
                      postings, n_post);
+}
+
+int a2ats_decode_step_append_postings(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx,
+                                      const void* q, const void* k_cache, const void* v_cache, uint16_t* codes,
+                                      const void* codebook, int32_t* hist, const void* chat, const float* nrm,
+                                      const void* postings, int32_t n_post, float* out, int32_t* sel_out, void* ws,
+                                      size_t ws_bytes, void* stream) {
+  if (!chat || !postings || !hist || n_post < 0 || n_post > n_ctx - 1) return A2ATS_EINVAL;
+  if (check_shape(shape)) return A2ATS_EINVAL;
+  if (!select_postings_ok(shape->L, n_ctx)) return A2ATS_EUNSUPPORTED;
+  return decode_impl(shape, params, n_ctx, q, k_cache, v_cache, codes, codebook, hist, chat, nrm, out, sel_out,
+                     nullptr, ws, ws_bytes, stream, true, postings, n_post);
 }
 
 // ------------------------------------------------------------------ end-to-end staging

@@ -201,6 +201,8 @@ struct SelArgs {
   const int32_t* post_off;      // [P, L + 1] start of each code's list
   const int32_t* post_tok;      // [P, n_max] token indices, grouped by code
   int n_post;
+  uint32_t* pbits;              // [P, pbits_stride] above / tied candidate bitmaps (bitmap path)
+  int pbits_stride;
   // window logits computed by the threshold kernel before its dependency wait (long contexts;
   // otherwise the prep kernel's window role): wlog == nullptr disables
   float* wlog;                  // [P, 64, 8]
@@ -288,6 +290,7 @@ cudaError_t launch_select_shard(const SelArgs& a, const CUtensorMap& tmK, int nb
 // posting-list selection: one CTA per pair (threshold + bitmaps from the lists + ordered emission)
 cudaError_t launch_select_postings(const SelArgs& a, cudaStream_t st);
 bool select_postings_ok(int L, int n_cand);
+inline int postings_bits_stride(int n_max) { return 2 * (((n_max + 31) / 32 + 3) & ~3); }
 cudaError_t launch_postings_build(const uint16_t* codes, int P, int n_max, int L, int n_tok, int32_t* post_off,
                                   int32_t* post_tok, cudaStream_t st);
 bool select_pipe_ok(int L);

@@ -30,6 +30,7 @@ namespace a2ats {
 
 namespace {
 A2ATS_TL_DECL(g_sel_tl)
+A2ATS_TL_DECL(g_selp_tl)  // postings kernel phase marks (tuning builds)
 A2ATS_TL_DECL(g_selc_tl)
 A2ATS_PHASE_DECL(g_sel_phase)
 
@@ -1549,6 +1550,9 @@ __global__ __launch_bounds__(kPAll, 1) void select_scan_kernel(const __grid_cons
 // tied bitmap; tokens [n_post, c1) not yet in the index are classified from their codes; then
 // the bitmaps are scanned in token order (lanes on consecutive words, warp prefix of the
 // counts): ascending emission with the tie quota, as in the code scan.
+#ifndef A2ATS_QT_MINB
+#define A2ATS_QT_MINB 4  // postings select CTAs per SM (tuning define)
+#endif
 constexpr int kQT = 256;             // postings select threads (16 codewords / thread, L <= 4096)
 constexpr int kQWords = 16;          // bitmap words per thread per segment (4096-word segments)
 constexpr int kQSurv = 512;          // survivors ranked directly (more: byte passes) -- keeps 4 CTAs / SM
@@ -1587,24 +1591,24 @@ __device__ __forceinline__ void q_scan(const int (&v)[NV], int (&ex)[NV], int (&
   }
 }
 
-__global__ __launch_bounds__(kQT, 4) void select_postings_kernel(SelArgs a) {
+__global__ __launch_bounds__(kQT, A2ATS_QT_MINB) void select_postings_kernel(SelArgs a) {
   A2ATS_TL(g_sel_tl, 0);
   extern __shared__ __align__(16) uint32_t sm[];
   __shared__ SelShared S;
   __shared__ uint32_t s_cls[256];    // compact 2-bit classes (code >> 4), L <= 4096
   __shared__ int s_part[4][kQT / 32];
-  __shared__ uint16_t s_sk[kQSinkMax];          // codes of the indexed sink tokens (fast path)
-  __shared__ int s_ts[kQTiedMax], s_tn[kQTiedMax];  // tied codes' lists (fast path)
+  __shared__ uint16_t s_sk[kQSinkMax];          // codes of the indexed sink tokens (list path)
+  __shared__ int s_ts[kQTiedMax], s_tn[kQTiedMax];  // tied codes' lists (list path)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, pair = blockIdx.x;
   const int L4 = (a.L + 3) & ~3;
-  int* cnt = reinterpret_cast<int*>(sm);                    // [L4]
-  uint32_t* skey = sm + L4;                                 // [kQSurv] survivors
-  int* scnt = reinterpret_cast<int*>(skey + kQSurv);        // [kQSurv]
-  const int ncand = max(0, a.c1 - a.c0), nwords = (ncand + 31) >> 5;
-  const int nw4 = (nwords + 3) & ~3;
-  uint32_t* bab = sm + L4 + 2 * kQSurv;                     // [nw4] above-v* bitmap (bitmap path)
-  uint32_t* bti = bab + nw4;                                // [nw4] tied bitmap
+  // shared memory (small, so that four CTAs per SM leave most of the unified L1 to the loads):
+  //   cnt [L4] | survivors skey, scnt [kQSurv each] | list bounds [L + 1 + (L + 1) / 16]
+  int* cnt = reinterpret_cast<int*>(sm);
+  uint32_t* skey = sm + L4;
+  int* scnt = reinterpret_cast<int*>(skey + kQSurv);
+  int* orow = scnt + kQSurv;                                // bound i at i + i / 16 (conflict-free rows)
   const int R = L4 + 2 * kQSurv;                            // words dead after the level (cnt + survivors)
+  const int ncand = max(0, a.c1 - a.c0), nwords = (ncand + 31) >> 5;
   const uint16_t* cp = a.codes + (size_t)pair * a.n_max;
   const int32_t* ptok = a.post_tok + (size_t)pair * a.n_max;
   int32_t* selp = a.sel + (size_t)pair * a.sel_stride;
@@ -1614,17 +1618,53 @@ __global__ __launch_bounds__(kQT, 4) void select_postings_kernel(SelArgs a) {
   const int nsk = min(a.c0, a.n_post);
   const bool list_ok = a.n_post <= a.c1 && nsk <= kQSinkMax;
   float wacc[512 / kQT];
-  if (a.wlog) {  // the pair's window-row logits (step inputs; scratch aliases counts and bitmaps)
+  if (a.wlog) {  // the pair's window-row logits (step inputs; scratch aliases the regions above)
     window_logits<kQT>(a, pair, reinterpret_cast<uint8_t*>(sm), wacc);
     __syncthreads();
   }
-  load_cnt<kQT>(a, pair, cnt, cp);  // hist - sinks / window codes (step inputs)
+  // step inputs, every global load in flight at once (coalesced): the pair's hist row, its list
+  // bounds, the codes of its sinks / window tokens (not candidates: subtracted from hist) and the
+  // indexed sinks' codes
+  const int post0 = pair * (a.L + 1);
+  {
+    constexpr int kH = (4096 + kQT - 1) / kQT, kO = (4096 + kQT) / kQT;  // L <= 4096
+    const int32_t* histp = a.hist + (size_t)pair * a.L;
+    int hv[kH], ob[kO];
+#pragma unroll
+    for (int j = 0; j < kH; ++j) {
+      const int l = j * kQT + tid;
+      hv[j] = l < a.L ? __ldg(histp + l) : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < kO; ++j) {
+      const int i = j * kQT + tid;
+      ob[j] = i <= a.L ? __ldg(a.post_off + post0 + i) : 0;
+    }
+    const int nrem = a.n_s + (a.n_ctx - a.append - a.w0);  // (append: hist lacks token n_ctx - 1)
+    int rc = -1;
+    if (tid < nrem) rc = cp[tid < a.n_s ? tid : a.w0 + (tid - a.n_s)];
+    int skc = 0;
+    if (list_ok && tid < nsk) skc = cp[tid];
+#pragma unroll
+    for (int j = 0; j < kH; ++j) {
+      const int l = j * kQT + tid;
+      if (l < a.L) cnt[l] = hv[j];
+    }
+#pragma unroll
+    for (int j = 0; j < kO; ++j) {
+      const int i = j * kQT + tid;
+      if (i <= a.L) orow[i + (i >> 4)] = ob[j];
+    }
+    if (list_ok && tid < nsk) s_sk[tid] = (uint16_t)skc;
+    A2ATS_TL(g_selp_tl, 0);
+    __syncthreads();
+    if (rc >= 0) atomicSub(&cnt[rc], 1);
+    for (int i = tid + kQT; i < nrem; i += kQT) atomicSub(&cnt[cp[i < a.n_s ? i : a.w0 + (i - a.n_s)]], 1);
+    __syncthreads();
+  }
   int c[16];
   load_c_regs<16>(a, cnt, c);
-  if (list_ok && tid < nsk) s_sk[tid] = cp[tid];
-  const int post0 = pair * (a.L + 1);
-  if (tid * 32 <= a.L)  // the pair's list bounds (step inputs) into L2 while the LUT finishes
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(a.post_off + post0 + tid * 32));
+  A2ATS_TL(g_selp_tl, 1);
   pdl_wait();  // agg comes from the prep kernel
   pdl_trigger();
   A2ATS_TL(g_sel_tl, 2);
@@ -1644,82 +1684,79 @@ __global__ __launch_bounds__(kQT, 4) void select_postings_kernel(SelArgs a) {
       hmask |= 1u << e;
       if (k[e] == kstar) tmask |= 1u << e;
     }
-  // the list bounds of this thread's 16 consecutive codewords: the row read coalesced into
-  // shared memory (element i at i + i / 16: thread t's 17 reads are conflict-free)
-  int o[17];
-  {
-    int* orow = reinterpret_cast<int*>(sm);  // (cnt is dead) L + 1 + (L + 1) / 16 <= R words
-    for (int i = tid; i <= a.L; i += kQT) orow[i + (i >> 4)] = __ldg(a.post_off + post0 + i);
-    __syncthreads();
-#pragma unroll
-    for (int e = 0; e < 17; ++e) o[e] = (tid * 16 + e <= a.L) ? orow[tid * 17 + e + (e >> 4)] : 0;
-  }
-  // sink entries at the head of each hit list (list path; lists are ascending): the codes of this
-  // thread holding a sink are counted in 4-bit fields (more than 15 sinks on one code: the
-  // bitmap path)
-  unsigned long long skp = 0ull;
-  bool skov = false;
-  for (int i = 0; i < nsk; ++i) {
-    const int code = s_sk[i];
-    if ((code >> 4) == tid) {
-      const int sh = 4 * (code & 15);
-      skov |= ((skp >> sh) & 15ull) == 15ull;
-      skp += 1ull << sh;
-    }
-  }
-  const bool list_go = list_ok && !__syncthreads_or(skov);
-  auto skip_of = [&](int e) { return (int)((skp >> (4 * e)) & 15ull); };
-  // block scans: [0] above codes, [1] above entries, [2] tied codes, [3] tied entries; o[e]
-  // becomes the start of code e's candidate entries (past its sinks)
+  // bound e of this thread's 16 consecutive codewords (e <= 16; staged before the wait)
+  auto bnd = [&](int e) { return orow[tid * 17 + e + (e >> 4)]; };
+  A2ATS_TL(g_selp_tl, 2);
+  const bool list_go = list_ok;
+  // list path: sink entries at the head of a hit list (lists are ascending) are skipped
+  auto skip_of = [&](int e) {
+    const int code = tid * 16 + e;
+    int sk = 0;
+    for (int i = 0; i < nsk; ++i) sk += s_sk[i] == code;
+    return sk;
+  };
+  A2ATS_TL(g_selp_tl, 3);
+  // block scans: [0] above codes, [1] above entries, [2] tied codes, [3] tied entries (list
+  // path: entries past the sinks).  Hit codes visited bit by bit (no unrolled per-code copies:
+  // the kernel stays small in the instruction cache)
   int v[4] = {0, 0, 0, 0}, ex[4], tot[4];
-#pragma unroll
-  for (int e = 0; e < 16; ++e)
-    if ((hmask >> e) & 1u) {
-      if (list_go) o[e] += skip_of(e);
-      const int n = o[e + 1] - o[e];
-      const int g = ((tmask >> e) & 1u) ? 2 : 0;
-      v[g] += 1;
-      v[g + 1] += n;
+  {
+    int nAc = 0, nAe = 0, nTc = 0, nTe = 0;
+    for (uint32_t mm = hmask; mm; mm &= mm - 1u) {
+      const int e = __ffs(mm) - 1;
+      const int n = bnd(e + 1) - bnd(e) - (list_go ? skip_of(e) : 0);
+      if ((tmask >> e) & 1u) {
+        ++nTc;
+        nTe += n;
+      } else {
+        ++nAc;
+        nAe += n;
+      }
     }
+    v[0] = nAc;
+    v[1] = nAe;
+    v[2] = nTc;
+    v[3] = nTe;
+  }
   q_scan<4>(v, ex, tot, s_part);
-  A2ATS_TL(g_sel_tl, 6);
+  A2ATS_TL(g_selp_tl, 4);
   const int nA = tot[0], A_idx = tot[1], nT = tot[2], E_idx = tot[3];
-  const int hcap3 = R / 3;
-  if (list_go && nA <= hcap3 && nT <= kQTiedMax) {
+  const int RT = R + ((a.L + 1 + (a.L + 1) / 16 + 3) & ~3);  // + the bounds rows (dead once the tables are built)
+  const int nA4 = (nA + 3) & ~3;
+  if (list_go && 3 * nA4 <= R && nT <= kQTiedMax) {
     // ---- list path: the selection in index order (no ordered emission):
     //   [0, A_idx)        the above-v* codes' lists (code order; each ascending)
     //   [A_idx, A)        the above-v* tail tokens [n_post, c1) (ascending)
     //   [A, A + m)        the first m tied tokens in token order (tied lists merged, then the tail)
     int* hs = reinterpret_cast<int*>(sm);  // above code h: list start (past its sinks)
-    int* hn = hs + hcap3;                  //               entries
-    int* hp = hn + hcap3;                  //               output position
+    int* hn = hs + nA4;                    //               entries
+    int* hp = hn + nA4;                    //               output position
+    int* stg = hp + nA4;                   // staging of the above entries at their output positions
+    const int stg_cap = RT - 3 * nA4;
     {
       int ih = ex[0], ip = ex[1], it = ex[2];
-#pragma unroll
-      for (int e = 0; e < 16; ++e)
-        if ((hmask >> e) & 1u) {
-          // (o[e + 1] was advanced past code e + 1's sinks if that code is a hit)
-          const int n = o[e + 1] - o[e] - (e < 15 && ((hmask >> (e + 1)) & 1u) ? skip_of(e + 1) : 0);
-          if ((tmask >> e) & 1u) {
-            s_ts[it] = o[e];
-            s_tn[it] = n;
-            ++it;
-          } else {
-            hs[ih] = o[e];
-            hn[ih] = n;
-            hp[ih] = ip;
-            ++ih;
-            ip += n;
-          }
+      for (uint32_t mm = hmask; mm; mm &= mm - 1u) {
+        const int e = __ffs(mm) - 1;
+        const int st = bnd(e) + skip_of(e), n = bnd(e + 1) - st;
+        if ((tmask >> e) & 1u) {
+          s_ts[it] = st;
+          s_tn[it] = n;
+          ++it;
+        } else {
+          hs[ih] = st;
+          hn[ih] = n;
+          hp[ih] = ip;
+          ++ih;
+          ip += n;
         }
+      }
     }
     __syncthreads();
-    A2ATS_TL(g_sel_tl, 7);
+    A2ATS_TL(g_selp_tl, 5);
     // above lists -> output.  Staged: every entry fetched by cp.async into shared memory at its
-    // output position (the bitmaps' space: 2 nw4 words), one wait, then coalesced stores.
-    // Otherwise a warp per code (entries lane, lane + 32 together), kU codes in flight.
-    if (A_idx <= 2 * nw4) {
-      int* stg = reinterpret_cast<int*>(bab);
+    // output position (one round trip for the whole selection), then coalesced stores.
+    // Otherwise a warp per code (entries lane, lane + 32 loaded together), kU codes in flight.
+    if (A_idx <= stg_cap) {
       const int sub = lane & 7;  // groups of 8 lanes, a code each (lists average N / L entries)
       for (int h = (warp << 2) + (lane >> 3); h < nA; h += (kQT / 32) * 4) {
         const int n = hn[h];
@@ -1760,7 +1797,7 @@ __global__ __launch_bounds__(kQT, 4) void select_postings_kernel(SelArgs a) {
         }
       }
     }
-    A2ATS_TL(g_sel_tl, 4);
+    A2ATS_TL(g_selp_tl, 6);
     // tail [max(n_post, c0), c1): classified from codes; counts first (A needs the above count)
     const int tb0 = max(a.n_post, a.c0);
     int tA = 0, tT = 0;
@@ -1827,7 +1864,7 @@ __global__ __launch_bounds__(kQT, 4) void select_postings_kernel(SelArgs a) {
         }
       }
     }
-    A2ATS_TL(g_sel_tl, 5);
+    A2ATS_TL(g_selp_tl, 7);
     A2ATS_TL(g_sel_tl, 1);
     return;
   }
@@ -1836,20 +1873,23 @@ __global__ __launch_bounds__(kQT, 4) void select_postings_kernel(SelArgs a) {
   const int nhit = nA + nT, hcap = R / 2;
   int* hs = reinterpret_cast<int*>(sm);  // hit code h: list start
   int* hl = hs + hcap;                   //             length | bit 31 if tied at v*
+  // above-v* and tied bitmaps of the candidates: the pair's workspace slice (global memory)
+  const int nw4 = (nwords + 3) & ~3;
+  uint32_t* bab = a.pbits + (size_t)pair * a.pbits_stride;
+  uint32_t* bti = bab + nw4;
   for (int i = tid; i < 2 * nw4; i += kQT) bab[i] = 0u;
   int bh = ex[0] + ex[2];
   const bool in_smem = nhit <= hcap;
   if (in_smem) {
-#pragma unroll
-    for (int e = 0; e < 16; ++e)
-      if ((hmask >> e) & 1u) {
-        hs[bh] = o[e];
-        hl[bh] = (o[e + 1] - o[e]) | ((((x >> (2 * e)) & 3u) == 2u) ? (int)0x80000000 : 0);
-        ++bh;
-      }
+    for (uint32_t mm = hmask; mm; mm &= mm - 1u) {
+      const int e = __ffs(mm) - 1;
+      hs[bh] = bnd(e);
+      hl[bh] = (bnd(e + 1) - bnd(e)) | ((((x >> (2 * e)) & 3u) == 2u) ? (int)0x80000000 : 0);
+      ++bh;
+    }
   }
   __syncthreads();
-  A2ATS_TL(g_sel_tl, 7);
+  A2ATS_TL(g_selp_tl, 5);
   // list entries -> candidate bits (entries outside [c0, c1) are sinks / window): a warp per hit
   // code, lanes over its list (entries lane, lane + 32 loaded together); kU codes per warp in
   // flight; longer lists loop
@@ -1891,7 +1931,7 @@ __global__ __launch_bounds__(kQT, 4) void select_postings_kernel(SelArgs a) {
       for (int i = __ldg(a.post_off + post0 + l); i < i1; ++i) set_bit(__ldg(ptok + i), tied);
     }
   }
-  A2ATS_TL(g_sel_tl, 4);
+  A2ATS_TL(g_selp_tl, 6);
   // tokens not yet in the index: classified from their codes
   for (int t = max(a.n_post, a.c0) + tid; t < a.c1; t += kQT) {
     const int l = cp[t];
@@ -1899,7 +1939,7 @@ __global__ __launch_bounds__(kQT, 4) void select_postings_kernel(SelArgs a) {
     if (cl) set_bit(t, cl == 2u);
   }
   __syncthreads();
-  A2ATS_TL(g_sel_tl, 5);
+  A2ATS_TL(g_selp_tl, 7);
   // ordered emission.  Segments of kQT * kQWords words; warp w takes words [512 w, 512 w + 512)
   // of the segment, lane l word 32 i + l at step i (consecutive lanes: consecutive words and
   // nearby output positions).  Selected bits of a word: the above-v* bits and the tied bits of
@@ -2157,15 +2197,14 @@ int select_chunk_tokens() { return kCH; }
 
 bool select_pipe_ok(int L) { return L <= 4096; }
 
-size_t postings_smem_bytes(int L, int n_cand) {
-  const size_t words = (size_t)(((n_cand + 31) / 32 + 3) & ~3);
-  const size_t base = (size_t)((L + 3) & ~3) * 4 + 2 * kQSurv * 4 + 2 * words * 4;
-  return std::max(base, (size_t)kWinScratch);
+size_t postings_smem_bytes(int L, bool window) {
+  const size_t base = (size_t)((L + 3) & ~3) * 4 + 2 * kQSurv * 4 + (size_t)((L + 1 + (L + 1) / 16 + 3) & ~3) * 4;
+  return window ? std::max(base, (size_t)kWinScratch) : base;
 }
-bool select_postings_ok(int L, int n_cand) { return L <= 4096 && postings_smem_bytes(L, n_cand) <= 200 * 1024; }
+bool select_postings_ok(int L, int) { return L <= 4096; }
 
 cudaError_t launch_select_postings(const SelArgs& a, cudaStream_t st) {
-  const int smem = (int)postings_smem_bytes(a.L, std::max(0, a.c1 - a.c0));
+  const int smem = (int)postings_smem_bytes(a.L, a.wlog != nullptr);
   cudaError_t e = ensure_smem(select_postings_kernel, smem);
   if (e != cudaSuccess) return e;
   return launch_pdl(select_postings_kernel, dim3(a.P), dim3(kQT), smem, st, a);
@@ -2212,3 +2251,4 @@ cudaError_t launch_select_pipe(const SelArgs& a, const CUtensorMap& tmK, int nbl
 A2ATS_PHASE_EXPORT(a2ats_debug_select_phases, a2ats::g_sel_phase)
 A2ATS_TL_EXPORT(a2ats_debug_select_timeline, a2ats::g_sel_tl)
 A2ATS_TL_EXPORT(a2ats_debug_selc_timeline, a2ats::g_selc_tl)
+A2ATS_TL_EXPORT(a2ats_debug_selp_timeline, a2ats::g_selp_tl)

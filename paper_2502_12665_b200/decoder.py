@@ -76,6 +76,15 @@ class Decoder:
                                       self.hist, self.postings, self.n_post, out, sel_out, self.ws_dec, self.stream)
         return out
 
+    def step_append_postings(self, q, k_cache, v_cache, n_ctx: int, out=None, sel_out=None):
+        """a0 for token n_ctx - 1 fused with the step, selection over the posting lists (f3)."""
+        if out is None:
+            out = torch.empty((self.shape.B, self.shape.Hq, 128), dtype=torch.float32, device=self.device)
+        _b.a2ats_decode_step_append_postings(self.shape, self.params, n_ctx, q, k_cache, v_cache, self.codes,
+                                             self.codebook, self.hist, self.chat, self.nrm, self.postings,
+                                             self.n_post, out, sel_out, self.ws_dec, self.stream)
+        return out
+
     def step_append(self, q, k_cache, v_cache, n_ctx: int, out=None, sel_out=None, scores_out=None,
                     use_hist=True):
         """a0 for token n_ctx - 1 (its key already in k_cache) fused with the step."""

@@ -134,3 +134,38 @@ def test_postings_list_path_deterministic():
         torch.cuda.synchronize()
         outs.append((s.clone(), o.clone()))
     assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+
+
+def test_append_postings_steps_equal_append_scan():
+    """a2ats_decode_step_append_postings over several decode steps (the index built once, the
+    unindexed tail growing by one token per step, one rebuild half-way) == a2ats_decode_step_append
+    (scan engine): the same new codes, the same running histogram, the same top-K sets, the
+    same output up to the row summation order."""
+    cfg = Config("posta", B=2, Hq=8, Hkv=2, d=128, N=20000, L=512, K=1200)
+    steps = 6
+    inp = make_inputs(cfg, 65, device="cuda", with_h=True, n_max=cfg.n_max(extra=steps + 8))
+    q, kc, vc = inp["q"], inp["k_cache"], inp["v_cache"]
+    params = A.Params(window=cfg.window, bridge=cfg.bridge, n_sink=cfg.n_sink, topk=cfg.K)
+    d1 = A.Decoder(cfg.B, cfg.Hq, cfg.Hkv, cfg.L, inp["n_max"], inp["codebook"], inp["H"], params)
+    d2 = A.Decoder(cfg.B, cfg.Hq, cfg.Hkv, cfg.L, inp["n_max"], inp["codebook"], inp["H"],
+                   A.Params(window=cfg.window, bridge=cfg.bridge, n_sink=cfg.n_sink, topk=cfg.K))
+    n0 = cfg.N - steps
+    d1.encode(kc, 0, n0)
+    d2.encode(kc, 0, n0)
+    d2.build_postings(n0 - cfg.window - 300)
+    for s in range(steps):
+        n = n0 + s + 1
+        if s == steps // 2:
+            d2.build_postings(n - 1 - cfg.window)  # the whole candidate range indexed
+        s1 = torch.full((cfg.B, cfg.Hkv, cfg.K), -1, dtype=torch.int32, device="cuda")
+        s2 = torch.full_like(s1, -1)
+        o1 = d1.step_append(q, kc, vc, n, sel_out=s1)
+        o2 = d2.step_append_postings(q, kc, vc, n, sel_out=s2)
+        torch.cuda.synchronize()
+        assert torch.equal(d1.codes[:, :, :n], d2.codes[:, :, :n])
+        assert torch.equal(d1.hist, d2.hist)
+        np.testing.assert_array_equal(np.sort(s2.cpu().numpy(), axis=2), s1.cpu().numpy())
+        rel = (o1 - o2).norm(dim=2) / o1.norm(dim=2)
+        assert float(rel.max()) <= 1e-5, float(rel.max())
+    # the running histogram is the histogram of the final codes
+    assert torch.equal(d2.hist, hist_of(d2.codes, cfg.L, n0 + steps))

@@ -52,7 +52,13 @@ c0 = codes[:, :, :cfg.N - 1].to(torch.int64)
 hist0.zero_().scatter_add_(2, c0, torch.ones_like(c0, dtype=torch.int32))
 sel_buf = torch.empty((cfg.B, cfg.Hkv, max(cfg.K, 1)), dtype=torch.int32, device="cuda")
 if args.postings:
-    dec.build_postings(cfg.N - cfg.window - args.post_lag)
+    for it in range(3):
+        flush.fill_(it)
+        e0.record()
+        dec.build_postings(cfg.N - cfg.window - args.post_lag)
+        e1.record()
+        torch.cuda.synchronize()
+        print("postings_build %.1f us" % (e0.elapsed_time(e1) * 1e3))
 for it in range(args.iters if args.select_only else 0):
     flush.fill_(it)
     e0.record()

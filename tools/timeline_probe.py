@@ -24,6 +24,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C2")
 ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--select-only", action="store_true", help="a2ats_select_topk (a1..a4) instead of the step")
+ap.add_argument("--postings", action="store_true", help="select-only through the posting-list engine (f3)")
 args = ap.parse_args()
 cfg = CONFIGS[args.config]
 inp = make_inputs(cfg, 5, device="cuda", with_h=True)
@@ -41,6 +42,8 @@ out = torch.empty((cfg.B, cfg.Hq, 128), device="cuda")
 lib = A.load()
 KMAX = 8192
 kernels = ["prep", "select", "selc"] if args.select_only else ["prep", "select", "selc", "attn"]
+if args.postings:
+    kernels = ["prep", "select", "selp"]
 sel_buf = torch.empty((cfg.B, cfg.Hkv, cfg.K), dtype=torch.int32, device="cuda")
 fns = {}
 for k in kernels:
@@ -48,11 +51,16 @@ for k in kernels:
     f.argtypes = [ctypes.POINTER(ctypes.c_ulonglong)]
     fns[k] = f
 flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+if args.postings:
+    args.select_only = True
+    dec.build_postings(cfg.N - cfg.window - 256)
 ncta = {}
 for it in range(args.iters):
     flush.fill_(it)
     dec.hist.copy_(hist if args.select_only else hist0)  # step: covers [0, N-1), the step appends N-1
-    if args.select_only:
+    if args.postings:
+        dec.select_postings(inp["q"], cfg.N, sel_buf)
+    elif args.select_only:
         dec.select(inp["q"], cfg.N, sel_buf)
     else:
         dec.step_append(inp["q"], inp["k_cache"], inp["v_cache"], cfg.N, out=out)
@@ -110,11 +118,23 @@ for it in range(args.iters):
               f" [keys {d(4, 3):.2f} level {d(5, 4):.2f} table {d(2, 5):.2f}]"
               f"  stream {d(1, 2):.2f}  (wait returns {(m[:, 3].min() - t0) / 1e3:.2f}..{(m[:, 3].max() - t0) / 1e3:.2f})")
     m = tl["select"][valid["select"]]
-    if len(m) and (m[:, 4] > m[:, 3]).all():  # threshold kernel marks: 3 wait returned, 4 level found
+    if args.postings and len(m):  # postings kernel marks: 2 wait, 3 level, 6 bounds+scan, 7 table, 4 copy, 5 tail+ties
+        d = lambda x, y: np.percentile((m[:, x] - m[:, y]) / 1e3, [10, 50, 90]).round(2)
+        print("  postings (p10/p50/p90 us): start->wait", d(2, 0), " level", d(3, 2), " bounds+scan", d(6, 3),
+              " table", d(7, 6), " copy", d(4, 7), " tail+ties", d(5, 4), " end", d(1, 5))
+        print("    wait returns", np.percentile((m[:, 2] - t0) / 1e3, [0, 50, 100]).round(2))
+        p2 = tl["selp"][valid["select"]]
+        mm = np.concatenate([m, p2], axis=1)  # columns 8.. = selp marks
+        d = lambda x, y: np.percentile((mm[:, x] - mm[:, y]) / 1e3, [10, 50, 90]).round(2)
+        print("    prologue: loads", d(8, 0), " corrections", d(9, 8), " wait", d(2, 9))
+        print("    level: range", d(5, 2), " bins+pick", d(6, 5), " survivors", d(7, 6), " rank", d(3, 7))
+        print("    after: classes", d(10, 3), " sink-skip", d(11, 10), " q_scan", d(12, 11), " table", d(13, 12),
+              " copy", d(14, 13), " tail+ties", d(15, 14), " end", d(1, 15))
+    elif len(m) and (m[:, 4] > m[:, 3]).all():  # threshold kernel marks: 3 wait returned, 4 level found
         d = lambda x, y: np.percentile((m[:, x] - m[:, y]) / 1e3, [10, 50, 90]).round(2)
         print("  thresh (p10/p50/p90 us): start->wait", d(3, 0), " keys+level", d(4, 3), " table+E", d(1, 4))
         print("    keys", d(5, 3), " bins+pick", d(6, 5), " survivors", d(7, 6), " rank", d(4, 7))
-    m = tl["selc"][valid["selc"]] if len(valid["selc"]) else []
+    m = tl["selc"][valid["selc"]] if "selc" in valid and len(valid["selc"]) else []
     if len(m) and (m[:, 3] > m[:, 2]).all():  # scan kernel marks: 2 wait returned, 3 first unit done
         d = lambda x, y: np.percentile((m[:, x] - m[:, y]) / 1e3, [10, 50, 90]).round(2)
         print("  scan (p10/p50/p90 us): start->wait", d(2, 0), " unit0", d(3, 2), " rest", d(1, 3))
