@@ -143,18 +143,35 @@ def measured_traffic(cfg, kernel: str):
 
 
 def scoring_line(cfg, r, pk):
-    """Score + top-K: a2ats_select_topk (a1..a4) timed as one graph replay."""
+    """Score + top-K: a2ats_select_topk (a1..a4; posting-list engine:
+    a2ats_select_topk_postings + the amortized index rebuild) timed as one graph replay."""
     from synth import budget_k
     n = r["score_n"]
     P = cfg.B * cfg.Hkv
     k = budget_k(n)
-    ms = r["score_ms"]
+    post = r.get("post")
+    ms_kernels = r["score_ms"]
+    ms = ms_kernels + (post["amortized_ms"] if post else 0.0)
+    # the code-stream design's algorithmic bytes (every code once, the codebook once, Sel out):
+    # the north star's 70 % target is stated on them
     score_bytes = P * n * 2 + cfg.Hkv * cfg.L * cfg.d * 2 + P * k * 4
-    return {"tokens_per_s": P * n / (ms * 1e-3) if ms > 0 else None, "ms": ms, "score_topk_bytes": score_bytes,
+    line = {"tokens_per_s": P * n / (ms * 1e-3) if ms > 0 else None, "ms": ms, "score_topk_bytes": score_bytes,
             "hbm_frac": (score_bytes / (ms * 1e-3) / 1e9 / pk["hbm"]) if ms > 0 else None,
-            "n_ctx": n, "topk": k,
-            "note": "a2ats_select_topk (LUT + approximate scores + exact top-K, no attention), CUDA-graph "
-                    "replay, L2 flushed before each replay; bytes = codes + codebook + Sel"}
+            "n_ctx": n, "topk": k, "engine": "postings" if post else "scan",
+            "note": "LUT + approximate scores + exact top-K, no attention; CUDA-graph replay, L2 flushed before "
+                    "each replay; hbm_frac = the code-stream bytes (codes + codebook + Sel) / time / HBM peak"}
+    if post:
+        # bytes the posting-list select actually needs: codebook + q~ tiles, agg out and in, hist,
+        # list bounds, the selected list entries in and Sel out (DESIGN.md §6)
+        pbytes = (cfg.Hkv * cfg.L * cfg.d * 2 + P * cfg.L * 4 * 2 + P * cfg.L * 4 + P * (cfg.L + 1) * 4
+                  + P * k * 4 * 2)
+        line.update({"ms_kernels": ms_kernels, "rebuild_ms": post["rebuild_ms"], "rebuild_every": post["every"],
+                     "postings_alg_bytes": pbytes,
+                     "postings_hbm_frac": pbytes / (ms_kernels * 1e-3) / 1e9 / pk["hbm"] if ms_kernels > 0 else None,
+                     "note_postings": "a2ats_select_topk_postings over an index rebuilt every rebuild_every steps "
+                                      "(rebuild_ms / rebuild_every added to ms); the selection reads only the "
+                                      "lists of the codes at or above the K-th level"})
+    return line
 
 
 # ---------------------------------------------------------------------------- our arm
@@ -182,12 +199,19 @@ def run_ours(args, rank: int, world: int):
     out = torch.empty((cfg.B, cfg.Hq, cfg.d), dtype=torch.float32, device=dev)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)   # 256 MB > 126 MB L2
     torch.cuda.synchronize()
+    engine = args.engine
+    if engine == "auto":  # posting lists where the code scan needs its long-context kernels (C4)
+        engine = "postings" if cfg.N - cfg.window > 2 * 32768 and cfg.L <= 4096 else "scan"
+    post = postings_setup(args, cfg, dec, n0, flush) if engine == "postings" else None
 
     def one_step(n, evs=None):
         if evs is not None:
             A.a2ats_set_stage_events(evs[1:])
         dec.params.topk = budget_k(n)
-        dec.step_append(q, kc, vc, n, out=out)      # a0 for token n-1 (+ hist) fused with a1..a6
+        if post is not None:                        # a0 for token n-1 (+ hist) fused with a1..a6,
+            dec.step_append_postings(q, kc, vc, n, out=out)   # selection over the posting lists
+        else:
+            dec.step_append(q, kc, vc, n, out=out)  # a0 for token n-1 (+ hist) fused with a1..a6
         if evs is not None:
             A.a2ats_set_stage_events(None)
 
@@ -272,6 +296,8 @@ def run_ours(args, rank: int, world: int):
         tk = torch.tensor([float(tokens)], device=dev)
         torch.distributed.all_reduce(tk)
         tokens = tk.item()
+    if post is not None:  # the index rebuild, every post["every"] steps, amortized into each step
+        total_ms += args.steps * post["amortized_ms"]
     value = tokens / (total_ms / 1e3)
     n_last = ns[-1]
     del graphs
@@ -280,13 +306,20 @@ def run_ours(args, rank: int, world: int):
     # one CUDA graph replayed, L2 flushed before each replay outside the events
     sel = torch.empty((cfg.B, cfg.Hkv, max(budget_k(n_last), 1)), dtype=torch.int32, device=dev)
     dec.params.topk = budget_k(n_last)
-    dec.select(q, n_last, sel)
+
+    def select():
+        if post is not None:
+            dec.select_postings(q, n_last, sel)
+        else:
+            dec.select(q, n_last, sel)
+
+    select()
     torch.cuda.synchronize()
     g_sel = None
     if use_graph:
         g_sel = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g_sel):
-            dec.select(q, n_last, sel)
+            select()
     sc_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     for k in range(args.steps):
         if not args.no_flush:
@@ -295,14 +328,14 @@ def run_ours(args, rank: int, world: int):
         if g_sel is not None:
             g_sel.replay()
         else:
-            dec.select(q, n_last, sel)
+            select()
         sc_ev[k][1].record(stream)
     torch.cuda.synchronize()
     score_ms = statistics.mean(a.elapsed_time(b) for a, b in sc_ev)
     del g_sel
 
-    e2e = run_e2e(e2e_steps, dec, cfg, kc, vc, q, n_last, A, budget_k, use_graph, world, dev)
-    return dict(value=value, ms_per_step=total_ms / args.steps, score_ms=score_ms, score_n=n_last,
+    e2e = run_e2e(e2e_steps, dec, cfg, kc, vc, q, n_last, A, budget_k, use_graph, world, dev, post)
+    return dict(value=value, ms_per_step=total_ms / args.steps, score_ms=score_ms, score_n=n_last, post=post,
                 stage_ms={k: statistics.mean(v) for k, v in stage_ms.items()},
                 prof_step_ms=statistics.mean(prof_step),
                 clocks=clk.summary(), e2e=e2e, n_last=ns[args.warmup + args.steps - 1], cfg=cfg, graph=use_graph)
@@ -393,7 +426,28 @@ def run_offload(args, rank: int, world: int):
                 gather_gbs=gather / (statistics.median(step_ms) * 1e-3) / 1e9)
 
 
-def run_e2e(steps, dec, cfg, kc, vc, q, n_start, A, budget_k, use_graph, world, dev):
+def postings_setup(args, cfg, dec, n0, flush):
+    """Posting-list engine (f3): the index of tokens [0, n_post) is rebuilt every `every` decode
+    steps (a2ats_postings_build); tokens after n_post are classified from their codes by the
+    select kernel.  The timed steps run at mid-period (tail = every / 2 tokens past the index) and
+    the measured rebuild time / every is added to each step (and to the score + top-K time)."""
+    import torch
+    every = args.post_every
+    n_post = max(0, n0 + 1 - cfg.window - every // 2)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ms = []
+    for i in range(4):
+        flush.fill_(float(i))
+        ev[0].record()
+        dec.build_postings(n_post)
+        ev[1].record()
+        torch.cuda.synchronize()
+        ms.append(ev[0].elapsed_time(ev[1]))
+    rebuild_ms = statistics.median(ms[1:])
+    return {"every": every, "n_post": n_post, "rebuild_ms": rebuild_ms, "amortized_ms": rebuild_ms / every}
+
+
+def run_e2e(steps, dec, cfg, kc, vc, q, n_start, A, budget_k, use_graph, world, dev, post=None):
     """Same step through the public API with HOST buffers: every step moves its
     inputs (q, the new token's k and v rows) from pinned host memory into the
     device (a2ats_stage_rows: one kernel reading the mapped host buffers over
@@ -411,7 +465,10 @@ def run_e2e(steps, dec, cfg, kc, vc, q, n_start, A, budget_k, use_graph, world, 
         n = n_start + s + 1
         A.a2ats_stage_rows(dec.shape, n, q_host, k_host[s], v_host[s], q_dev, kc, vc)
         dec.params.topk = budget_k(n)
-        dec.step_append(q_dev, kc, vc, n, out=out_host)
+        if post is not None:
+            dec.step_append_postings(q_dev, kc, vc, n, out=out_host)
+        else:
+            dec.step_append(q_dev, kc, vc, n, out=out_host)
 
     graphs = []
     if use_graph:
@@ -433,6 +490,8 @@ def run_e2e(steps, dec, cfg, kc, vc, q, n_start, A, budget_k, use_graph, world, 
     ev1.record()
     ev1.synchronize()
     tot = ev0.elapsed_time(ev1)
+    if post is not None:
+        tot += steps * post["amortized_ms"]
     if world > 1:
         t = torch.tensor([tot], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -788,6 +847,10 @@ def main():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=2.0)
+    ap.add_argument("--engine", default="auto", choices=["auto", "postings", "scan"],
+                    help="selection engine of the 1-GPU step: posting lists (f3), the code scan, or auto "
+                         "(posting lists for contexts beyond two 32K-token code chunks)")
+    ap.add_argument("--post-every", type=int, default=512, help="posting-index rebuild period (steps)")
     ap.add_argument("--sharded", action="store_true",
                     help="the sequence-sharded step also at N = 1 (always used at N > 1)")
     args = ap.parse_args()
@@ -865,7 +928,8 @@ def main():
     n_last = r["n_last"]
     c0, c1 = min(cfg.n_sink, max(0, n_last - cfg.window)), max(0, n_last - cfg.window)
     long_select = c1 > c0 and (c1 - (c0 // 8) * 8 + 32767) // 32768 >= 2
-    launches_per_step = 3 + (1 if cfg.B * (cfg.Hq // cfg.Hkv) > 64 else 0) + (1 if long_select else 0)
+    post = r.get("post")
+    launches_per_step = 3 + (1 if cfg.B * (cfg.Hq // cfg.Hkv) > 64 else 0) + (1 if long_select and not post else 0)
     line = {
         "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak",
@@ -875,7 +939,11 @@ def main():
                    "bridge": cfg.bridge, "n_sink": cfg.n_sink,
                    "parallelism": f"replicas x{world} (batch/head parallel, no collective)" if world > 1 else "1 GPU",
                    "l2": "flushed between steps (256 MB write, outside the timed events)" if not args.no_flush else "not flushed",
-                   "step": "a2ats_decode_step_append: a0 for the new token (+hist) fused with a1..a6",
+                   "step": ("a2ats_decode_step_append_postings: a0 for the new token (+hist) fused with a1..a6, "
+                            "selection over posting lists rebuilt every %d steps (rebuild %.3f ms, amortized "
+                            "into ms_per_step)" % (post["every"], post["rebuild_ms"]) if post else
+                            "a2ats_decode_step_append: a0 for the new token (+hist) fused with a1..a6"),
+                   "engine": "postings" if post else "scan",
                    "launch": "one CUDA graph per step (replay)" if r["graph"] else "eager launches",
                    "sparsity": (budget_k(r["n_last"]) + 68) / r["n_last"], "aux_mem": 2 / (cfg.d * 2)},
         "roofline": roof,

@@ -46,6 +46,9 @@ cudaError_t ensure_smem_attr(const void* kernel, int bytes) {
 #ifndef A2ATS_PIPE_MIN_CHUNKS
 #define A2ATS_PIPE_MIN_CHUNKS 2
 #endif
+#ifndef A2ATS_LUT_TPC_QT
+#define A2ATS_LUT_TPC_QT 4
+#endif
 #ifndef A2ATS_QPREP_MIN_NV
 #define A2ATS_QPREP_MIN_NV 64
 #endif
@@ -532,7 +535,9 @@ int decode_impl(const a2ats_shape* shape, const a2ats_params* params, int32_t n_
   // wide query tiles: q~ hi|lo computed once by qprep_kernel instead of in every LUT CTA
   if (la.NV > A2ATS_QPREP_MIN_NV && !lut_fma) la.qt = reinterpret_cast<uint16_t*>(base + Lw.qt);
   PrepArgs p = prep_empty();
-  prep_set_lut(p, la);
+  // precomputed q~ tiles: A2ATS_LUT_TPC_QT code tiles per LUT CTA (C4: 128 CTAs, at most one per
+  // SM, so the next kernel's CTAs are resident -- their step-input prologue overlapping the LUT)
+  prep_set_lut(p, la, la.qt ? A2ATS_LUT_TPC_QT : 1);
   if (lut_fma) p.n_lut = 0;  // lut_fma_kernel computes agg (and the window table) before the prep kernel
   // long contexts: the window logits are computed by the select threshold kernel, before its
   // dependency wait (it waits for this kernel anyway); otherwise by the prep kernel's window role

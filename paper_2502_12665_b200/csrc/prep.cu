@@ -66,7 +66,7 @@ __device__ __forceinline__ void lut_tile(const CUtensorMap& tmA, const PrepArgs&
     umma::tma_load_2d(sA, &tmA, 0, h * a.L + xt0 * kTC, &tbar);
     umma::tma_load_2d(sA + kTC * 128, &tmA, 64, h * a.L + xt0 * kTC, &tbar);
   }
-  if (tid < kHalf) sbcs[tid] = a.bcs[tid];
+  if (!a.qt && tid < kHalf) sbcs[tid] = a.bcs[tid];  // (precomputed q~ tiles need no rotation here)
   __syncthreads();
   if (!a.qt) {
     // query tile: vector n = b * G + g <-> q row b * Hq + h * G + g; item = (vector, 8-pair chunk).
@@ -167,45 +167,60 @@ __device__ __forceinline__ void lut_tile(const CUtensorMap& tmA, const PrepArgs&
     }
     A2ATS_PHASE(g_lut_phase, 3);
 
-    // epilogue: thread <-> codeword row code0 + 32*warp + lane
+    // epilogue: thread <-> codeword row code0 + 32*warp + lane; the G-fold of each group of G
+    // columns (one batch element) is stored at agg[b][h][code]: one pointer, one stride
     const int code = code0 + warp * 32 + lane;
-    // 32-column blocks: two TMEM loads in flight per wait
-    auto fold = [&](const uint32_t (&r)[16], int col0) {
-      if (code < a.L) {
-        if (a.lut_full) {
+    const bool live = code < a.L;
+    const size_t bstride = (size_t)a.Hkv * a.L;
+    float* aggp = a.agg + ((size_t)(vec0 / G) * a.Hkv + h) * a.L + code;
+    auto fold = [&](const uint32_t* r, int col0) {
+      if (a.lut_full && live) {
 #pragma unroll 1
-          for (int ii = 0; ii < 16 && vec0 + col0 + ii < nvec; ++ii) {
-            const int vn = vec0 + col0 + ii, b = vn / G, g = vn - b * G;
-            float xi = 0.f;
+        for (int ii = 0; ii < 16 && vec0 + col0 + ii < nvec; ++ii) {
+          const int vn = vec0 + col0 + ii, b = vn / G, g = vn - b * G;
+          float xi = 0.f;
 #pragma unroll
-            for (int j = 0; j < 16; ++j) xi = (j == ii) ? __uint_as_float(r[j]) : xi;
-            a.lut_full[((size_t)b * a.Hq + h * G + g) * a.L + code] = xi;
-          }
-        }
-#pragma unroll
-        for (int bb = 0; bb < 16 / G; ++bb) {  // G divides 16, vec0 + col0 is a multiple of G
-          const int n0 = vec0 + col0 + bb * G;
-          if (n0 < nvec) {
-            float v = __uint_as_float(r[bb * G]);
-#pragma unroll
-            for (int g = 1; g < G; ++g) {
-              const float xg = __uint_as_float(r[bb * G + g]);
-              v = sum ? v + xg : fmaxf(v, xg);
-            }
-            a.agg[((size_t)(n0 / G) * a.Hkv + h) * a.L + code] = v;
-          }
+          for (int j = 0; j < 16; ++j) xi = (j == ii) ? __uint_as_float(r[j]) : xi;
+          a.lut_full[((size_t)b * a.Hq + h * G + g) * a.L + code] = xi;
         }
       }
+      float* pb = aggp + (size_t)(col0 / G) * bstride;
+#pragma unroll
+      for (int bb = 0; bb < 16 / G; ++bb) {  // G divides 16, vec0 + col0 is a multiple of G
+        float v = __uint_as_float(r[bb * G]);
+#pragma unroll
+        for (int g = 1; g < G; ++g) {
+          const float xg = __uint_as_float(r[bb * G + g]);
+          v = sum ? v + xg : fmaxf(v, xg);
+        }
+#ifdef A2ATS_DIAG_LUT_NOSTORE
+        if (v == 123.f) pb[bb * bstride] = v;  // (diagnostic build: stores elided)
+#else
+        if (live && col0 + bb * G < nv_here) pb[bb * bstride] = v;
+#endif
+      }
     };
-#pragma unroll 1
-    for (int col0 = 0; col0 < nv_here; col0 += 32) {
-      uint32_t r0[16], r1[16];
-      const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16) + col0;
-      umma::tmem_ld16(ta, r0);
-      if (col0 + 16 < nv_here) umma::tmem_ld16(ta + 16, r1);
+    // 32-column blocks, software-pipelined: the next block's TMEM load is in flight while this
+    // block is folded and stored (columns past nv_here: allocated, never stored)
+    {
+      const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16);
+      uint32_t ra[32], rb[32];
+      umma::tmem_ld32(ta, ra);
       umma::tmem_wait_ld();
-      fold(r0, col0);
-      if (col0 + 16 < nv_here) fold(r1, col0 + 16);
+#pragma unroll 1
+      for (int col0 = 0; col0 < nv_here; col0 += 64) {
+        const bool nb = col0 + 32 < nv_here;
+        if (nb) umma::tmem_ld32(ta + col0 + 32, rb);
+        fold(ra, col0);
+        fold(ra + 16, col0 + 16);
+        if (nb) {
+          umma::tmem_wait_ld();
+          if (col0 + 64 < nv_here) umma::tmem_ld32(ta + col0 + 64, ra);
+          fold(rb, col0 + 32);
+          fold(rb + 16, col0 + 48);
+          if (col0 + 64 < nv_here) umma::tmem_wait_ld();
+        }
+      }
     }
     umma::fence_before();
     __syncthreads();  // TMEM read out before the next tile's MMAs
