@@ -253,7 +253,8 @@ int a2ats_decode_step_append(const a2ats_shape* shape, const a2ats_params* param
  * reads about K list entries per pair instead of every code.  The index is
  * query-independent: a2ats_postings_build groups the tokens [0, n_tokens) of
  * every pair by code, each list ascending (deterministic; postings:
- * a2ats_postings_bytes of device memory = int32 offsets [B*Hkv, L+1], then,
+ * a2ats_postings_bytes of device memory = int32 offsets [B*Hkv, LP] with
+ * LP = (L + 4) & ~3 (row = the L+1 list starts, padded to 16 B), then,
  * 256-byte aligned, int32 tokens [B*Hkv, n_max], caller-owned); tokens
  * [n_post, n_ctx) not yet in the index are classified from their codes.
  * a2ats_select_topk_postings / a2ats_decode_step_postings = a2ats_select_topk /

@@ -47,7 +47,7 @@ cudaError_t ensure_smem_attr(const void* kernel, int bytes) {
 #define A2ATS_PIPE_MIN_CHUNKS 2
 #endif
 #ifndef A2ATS_LUT_TPC_QT
-#define A2ATS_LUT_TPC_QT 4
+#define A2ATS_LUT_TPC_QT 2
 #endif
 #ifndef A2ATS_QPREP_MIN_NV
 #define A2ATS_QPREP_MIN_NV 64
@@ -186,7 +186,7 @@ PostingsLayout postings_layout(const a2ats_shape* s) {
   PostingsLayout w;
   const size_t P = (size_t)s->B * s->Hkv;
   w.off = 0;
-  w.tok = align_up(P * (s->L + 1) * 4);
+  w.tok = align_up(P * postings_off_stride(s->L) * 4);
   w.total = align_up(w.tok + P * s->n_max * 4);
   return w;
 }

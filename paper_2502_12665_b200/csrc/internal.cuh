@@ -290,6 +290,8 @@ cudaError_t launch_select_shard(const SelArgs& a, const CUtensorMap& tmK, int nb
 // posting-list selection: one CTA per pair (threshold + bitmaps from the lists + ordered emission)
 cudaError_t launch_select_postings(const SelArgs& a, cudaStream_t st);
 bool select_postings_ok(int L, int n_cand);
+// list-bounds row of a pair in the posting index: L + 1 int32, padded to 16 B
+inline __host__ __device__ int postings_off_stride(int L) { return (L + 1 + 3) & ~3; }
 inline int postings_bits_stride(int n_max) { return 2 * (((n_max + 31) / 32 + 3) & ~3); }
 cudaError_t launch_postings_build(const uint16_t* codes, int P, int n_max, int L, int n_tok, int32_t* post_off,
                                   int32_t* post_tok, cudaStream_t st);

@@ -1602,11 +1602,11 @@ __global__ __launch_bounds__(kQT, A2ATS_QT_MINB) void select_postings_kernel(Sel
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, pair = blockIdx.x;
   const int L4 = (a.L + 3) & ~3;
   // shared memory (small, so that four CTAs per SM leave most of the unified L1 to the loads):
-  //   cnt [L4] | survivors skey, scnt [kQSurv each] | list bounds [L + 1 + (L + 1) / 16]
+  //   cnt [L4] | survivors skey, scnt [kQSurv each] | list bounds [LP]
   int* cnt = reinterpret_cast<int*>(sm);
   uint32_t* skey = sm + L4;
   int* scnt = reinterpret_cast<int*>(skey + kQSurv);
-  int* orow = scnt + kQSurv;                                // bound i at i + i / 16 (conflict-free rows)
+  int* orow = scnt + kQSurv;                                // the pair's list bounds (16-B aligned)
   const int R = L4 + 2 * kQSurv;                            // words dead after the level (cnt + survivors)
   const int ncand = max(0, a.c1 - a.c0), nwords = (ncand + 31) >> 5;
   const uint16_t* cp = a.codes + (size_t)pair * a.n_max;
@@ -1622,42 +1622,43 @@ __global__ __launch_bounds__(kQT, A2ATS_QT_MINB) void select_postings_kernel(Sel
     window_logits<kQT>(a, pair, reinterpret_cast<uint8_t*>(sm), wacc);
     __syncthreads();
   }
-  // step inputs, every global load in flight at once (coalesced): the pair's hist row, its list
-  // bounds, the codes of its sinks / window tokens (not candidates: subtracted from hist) and the
-  // indexed sinks' codes
-  const int post0 = pair * (a.L + 1);
+  // step inputs, every load in flight at once: the pair's hist row and list-bounds row (one bulk
+  // copy each into shared memory when 16-B aligned, else coalesced loads), the codes of its sinks
+  // / window tokens (not candidates: subtracted from hist), the indexed sinks' codes and the first
+  // 2 kQT unindexed tail tokens' codes (registers)
+  const int LP = postings_off_stride(a.L);
+  const int post0 = pair * LP;
+  uint32_t tcode, skmask = 0u;
   {
-    constexpr int kH = (4096 + kQT - 1) / kQT, kO = (4096 + kQT) / kQT;  // L <= 4096
+    __shared__ __align__(8) uint64_t s_pbar;
     const int32_t* histp = a.hist + (size_t)pair * a.L;
-    int hv[kH], ob[kO];
-#pragma unroll
-    for (int j = 0; j < kH; ++j) {
-      const int l = j * kQT + tid;
-      hv[j] = l < a.L ? __ldg(histp + l) : 0;
-    }
-#pragma unroll
-    for (int j = 0; j < kO; ++j) {
-      const int i = j * kQT + tid;
-      ob[j] = i <= a.L ? __ldg(a.post_off + post0 + i) : 0;
+    const bool bulk = (a.L & 3) == 0 && (reinterpret_cast<uintptr_t>(a.hist) & 15) == 0;
+    if (bulk) {
+      if (tid == 0) {
+        umma::fence_proxy_async();  // (the window-logit scratch was written through the generic proxy)
+        umma::mbar_init(&s_pbar, 1);
+        umma::mbar_fence_init();
+        umma::mbar_expect_tx(&s_pbar, (uint32_t)(a.L + LP) * 4u);
+        umma::bulk_load(cnt, histp, (uint32_t)a.L * 4u, &s_pbar);
+        umma::bulk_load(orow, a.post_off + post0, (uint32_t)LP * 4u, &s_pbar);
+      }
+    } else {
+      for (int l = tid; l < a.L; l += kQT) cnt[l] = __ldg(histp + l);
+      for (int i = tid; i <= a.L; i += kQT) orow[i] = __ldg(a.post_off + post0 + i);
     }
     const int nrem = a.n_s + (a.n_ctx - a.append - a.w0);  // (append: hist lacks token n_ctx - 1)
     int rc = -1;
     if (tid < nrem) rc = cp[tid < a.n_s ? tid : a.w0 + (tid - a.n_s)];
-    int skc = 0;
-    if (list_ok && tid < nsk) skc = cp[tid];
-#pragma unroll
-    for (int j = 0; j < kH; ++j) {
-      const int l = j * kQT + tid;
-      if (l < a.L) cnt[l] = hv[j];
-    }
-#pragma unroll
-    for (int j = 0; j < kO; ++j) {
-      const int i = j * kQT + tid;
-      if (i <= a.L) orow[i + (i >> 4)] = ob[j];
-    }
-    if (list_ok && tid < nsk) s_sk[tid] = (uint16_t)skc;
+    if (list_ok && tid < nsk) s_sk[tid] = cp[tid];
+    const int tb = max(a.n_post, a.c0) + tid;
+    tcode = (tb < a.c1 ? (uint32_t)cp[tb] : 0u) | (tb + kQT < a.c1 ? (uint32_t)cp[tb + kQT] << 16 : 0u);
     A2ATS_TL(g_selp_tl, 0);
-    __syncthreads();
+    __syncthreads();  // (barrier init, s_sk)
+    for (int i = 0; i < nsk; ++i) {  // this thread's codewords holding an indexed sink
+      const int code = s_sk[i];
+      if ((code >> 4) == tid) skmask |= 1u << (code & 15);
+    }
+    if (bulk) umma::mbar_wait(&s_pbar, 0);
     if (rc >= 0) atomicSub(&cnt[rc], 1);
     for (int i = tid + kQT; i < nrem; i += kQT) atomicSub(&cnt[cp[i < a.n_s ? i : a.w0 + (i - a.n_s)]], 1);
     __syncthreads();
@@ -1685,11 +1686,12 @@ __global__ __launch_bounds__(kQT, A2ATS_QT_MINB) void select_postings_kernel(Sel
       if (k[e] == kstar) tmask |= 1u << e;
     }
   // bound e of this thread's 16 consecutive codewords (e <= 16; staged before the wait)
-  auto bnd = [&](int e) { return orow[tid * 17 + e + (e >> 4)]; };
+  auto bnd = [&](int e) { return orow[tid * 16 + e]; };
   A2ATS_TL(g_selp_tl, 2);
   const bool list_go = list_ok;
   // list path: sink entries at the head of a hit list (lists are ascending) are skipped
   auto skip_of = [&](int e) {
+    if (!((skmask >> e) & 1u)) return 0;
     const int code = tid * 16 + e;
     int sk = 0;
     for (int i = 0; i < nsk; ++i) sk += s_sk[i] == code;
@@ -1721,7 +1723,7 @@ __global__ __launch_bounds__(kQT, A2ATS_QT_MINB) void select_postings_kernel(Sel
   q_scan<4>(v, ex, tot, s_part);
   A2ATS_TL(g_selp_tl, 4);
   const int nA = tot[0], A_idx = tot[1], nT = tot[2], E_idx = tot[3];
-  const int RT = R + ((a.L + 1 + (a.L + 1) / 16 + 3) & ~3);  // + the bounds rows (dead once the tables are built)
+  const int RT = R + postings_off_stride(a.L);  // + the bounds row (dead once the tables are built)
   const int nA4 = (nA + 3) & ~3;
   if (list_go && 3 * nA4 <= R && nT <= kQTiedMax) {
     // ---- list path: the selection in index order (no ordered emission):
@@ -1756,6 +1758,10 @@ __global__ __launch_bounds__(kQT, A2ATS_QT_MINB) void select_postings_kernel(Sel
     // above lists -> output.  Staged: every entry fetched by cp.async into shared memory at its
     // output position (one round trip for the whole selection), then coalesced stores.
     // Otherwise a warp per code (entries lane, lane + 32 loaded together), kU codes in flight.
+    // one tied code: its first min(n, m) entries staged too (after the above entries), stored
+    // once the tail's above count is known
+    const int n_tie1 = nT == 1 ? min(s_tn[0], (int)m) : 0;
+    const bool tie_staged = nT == 1 && A_idx + n_tie1 <= stg_cap;
     if (A_idx <= stg_cap) {
       const int sub = lane & 7;  // groups of 8 lanes, a code each (lists average N / L entries)
       for (int h = (warp << 2) + (lane >> 3); h < nA; h += (kQT / 32) * 4) {
@@ -1765,6 +1771,11 @@ __global__ __launch_bounds__(kQT, A2ATS_QT_MINB) void select_postings_kernel(Sel
         for (int j = sub; j < n; j += 8, src += 8, d += 32)
           asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
       }
+      if (tie_staged)
+        for (int j = tid; j < n_tie1; j += kQT) {
+          const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(stg + A_idx + j));
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(ptok + s_ts[0] + j) : "memory");
+        }
       cp_async_commit();
       cp_async_wait<0>();
       __syncthreads();
@@ -1800,9 +1811,12 @@ __global__ __launch_bounds__(kQT, A2ATS_QT_MINB) void select_postings_kernel(Sel
     A2ATS_TL(g_selp_tl, 6);
     // tail [max(n_post, c0), c1): classified from codes; counts first (A needs the above count)
     const int tb0 = max(a.n_post, a.c0);
+    auto tail_code = [&](int t, int r) {  // code of tail token t = tb0 + r * kQT + tid
+      return r < 2 ? (int)((tcode >> (16 * r)) & 0xffffu) : (int)cp[t];
+    };
     int tA = 0, tT = 0;
-    for (int t = tb0 + tid; t < a.c1; t += kQT) {
-      const int l = cp[t];
+    for (int t = tb0 + tid, r = 0; t < a.c1; t += kQT, ++r) {
+      const int l = tail_code(t, r);
       const uint32_t cl = (s_cls[l >> 4] >> (2 * (l & 15))) & 3u;
       tA += cl == 1u;
       tT += cl == 2u;
@@ -1819,11 +1833,11 @@ __global__ __launch_bounds__(kQT, A2ATS_QT_MINB) void select_postings_kernel(Sel
     for (int w = 0; w < kQT / 32; ++w) A += s_part[0][w];
     if (tb0 < a.c1) {  // ordered compaction of the tail, kQT tokens per round
       int runA = A_idx, runT = 0;
-      for (int base = tb0; base < a.c1; base += kQT) {
+      for (int base = tb0, r = 0; base < a.c1; base += kQT, ++r) {
         const int t = base + tid;
         uint32_t cl = 0u;
         if (t < a.c1) {
-          const int l = cp[t];
+          const int l = tail_code(t, r);
           cl = (s_cls[l >> 4] >> (2 * (l & 15))) & 3u;
         }
         const int vv[2] = {cl == 1u, cl == 2u};
@@ -1839,9 +1853,12 @@ __global__ __launch_bounds__(kQT, A2ATS_QT_MINB) void select_postings_kernel(Sel
       }
     }
     // the indexed ties: tie index of an entry = its rank in the merge of the tied lists
-    if (nT == 1) {
-      const int st = s_ts[0], n = min(s_tn[0], (int)m);
-      for (int j = tid; j < n; j += kQT)
+    if (tie_staged) {
+      for (int j = tid; j < n_tie1; j += kQT)
+        if ((uint32_t)(A + j) < cap) selp[A + j] = stg[A_idx + j];
+    } else if (nT == 1) {
+      const int st = s_ts[0];
+      for (int j = tid; j < n_tie1; j += kQT)
         if ((uint32_t)(A + j) < cap) selp[A + j] = __ldg(ptok + st + j);
     } else {
       for (int g = 0; g < nT; ++g) {
@@ -2051,7 +2068,7 @@ __global__ __launch_bounds__(kBW * 32) void postings_build_kernel(const uint16_t
     if (w < warp) base += s_w[w];
     total += s_w[w];
   }
-  int32_t* offp = post_off + (size_t)pair * (L + 1);
+  int32_t* offp = post_off + (size_t)pair * postings_off_stride(L);
   for (int i = 0; i < pc && l0 + i < L; ++i) {
     offp[l0 + i] = base;
     for (int w = 0; w < kBW; ++w) {
@@ -2198,7 +2215,7 @@ int select_chunk_tokens() { return kCH; }
 bool select_pipe_ok(int L) { return L <= 4096; }
 
 size_t postings_smem_bytes(int L, bool window) {
-  const size_t base = (size_t)((L + 3) & ~3) * 4 + 2 * kQSurv * 4 + (size_t)((L + 1 + (L + 1) / 16 + 3) & ~3) * 4;
+  const size_t base = (size_t)((L + 3) & ~3) * 4 + 2 * kQSurv * 4 + (size_t)postings_off_stride(L) * 4;
   return window ? std::max(base, (size_t)kWinScratch) : base;
 }
 bool select_postings_ok(int L, int) { return L <= 4096; }

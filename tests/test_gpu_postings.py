@@ -107,8 +107,9 @@ def test_postings_index_is_stable_sort_by_code():
     A.binding.a2ats_postings_build(shape, codes, n, post)
     torch.cuda.synchronize()
     P = B * Hkv
-    t0 = (P * (L + 1) * 4 + 255) // 256 * 256   # a2ats.h: offsets, then tokens (256-B aligned)
-    off = post[:P * (L + 1) * 4].view(torch.int32).view(P, L + 1).cpu().numpy()
+    LP = (L + 4) // 4 * 4                       # a2ats.h: offset rows of L + 1 padded to 16 B
+    t0 = (P * LP * 4 + 255) // 256 * 256        # offsets, then tokens (256-B aligned)
+    off = post[:P * LP * 4].view(torch.int32).view(P, LP)[:, :L + 1].cpu().numpy()
     tok = post[t0:t0 + P * n_max * 4].view(torch.int32).view(P, n_max).cpu().numpy()
     c = codes.view(P, n_max)[:, :n].cpu().numpy().astype(np.int64)
     for p in range(P):
