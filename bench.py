@@ -850,7 +850,7 @@ def main():
     ap.add_argument("--engine", default="auto", choices=["auto", "postings", "scan"],
                     help="selection engine of the 1-GPU step: posting lists (f3), the code scan, or auto "
                          "(posting lists for contexts beyond two 32K-token code chunks)")
-    ap.add_argument("--post-every", type=int, default=512, help="posting-index rebuild period (steps)")
+    ap.add_argument("--post-every", type=int, default=1024, help="posting-index rebuild period (steps)")
     ap.add_argument("--sharded", action="store_true",
                     help="the sequence-sharded step also at N = 1 (always used at N > 1)")
     args = ap.parse_args()

@@ -36,6 +36,10 @@ cudaError_t ensure_smem_attr(const void* kernel, int bytes) {
   int& have = done[{kernel, dev}];
   if (have >= bytes) return cudaSuccess;
   e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  // the SM's shared / L1 split is fixed while CTAs are resident: at the maximum shared carveout
+  // a kernel's CTAs can join an SM that runs the previous kernel's (programmatic dependent launch)
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   if (e == cudaSuccess) have = bytes;
   return e;
 }
@@ -46,8 +50,8 @@ cudaError_t ensure_smem_attr(const void* kernel, int bytes) {
 #ifndef A2ATS_PIPE_MIN_CHUNKS
 #define A2ATS_PIPE_MIN_CHUNKS 2
 #endif
-#ifndef A2ATS_LUT_TPC_QT
-#define A2ATS_LUT_TPC_QT 2
+#ifndef A2ATS_LUT_PERSIST
+#define A2ATS_LUT_PERSIST 1  // persistent warp-specialized LUT for precomputed q~ tiles (tuning define)
 #endif
 #ifndef A2ATS_QPREP_MIN_NV
 #define A2ATS_QPREP_MIN_NV 64
@@ -535,10 +539,11 @@ int decode_impl(const a2ats_shape* shape, const a2ats_params* params, int32_t n_
   // wide query tiles: q~ hi|lo computed once by qprep_kernel instead of in every LUT CTA
   if (la.NV > A2ATS_QPREP_MIN_NV && !lut_fma) la.qt = reinterpret_cast<uint16_t*>(base + Lw.qt);
   PrepArgs p = prep_empty();
-  // precomputed q~ tiles: A2ATS_LUT_TPC_QT code tiles per LUT CTA (C4: 128 CTAs, at most one per
-  // SM, so the next kernel's CTAs are resident -- their step-input prologue overlapping the LUT)
-  prep_set_lut(p, la, la.qt ? A2ATS_LUT_TPC_QT : 1);
-  if (lut_fma) p.n_lut = 0;  // lut_fma_kernel computes agg (and the window table) before the prep kernel
+  prep_set_lut(p, la);
+  // lut_fma_kernel (FMA engine) or lut_persist_kernel (precomputed q~ tiles) computes agg before
+  // the prep kernel, which then runs only its encode / window roles
+  const bool lut_persist = la.qt != nullptr && A2ATS_LUT_PERSIST;
+  if (lut_fma || lut_persist) p.n_lut = 0;
   // long contexts: the window logits are computed by the select threshold kernel, before its
   // dependency wait (it waits for this kernel anyway); otherwise by the prep kernel's window role
   const int nchunk = d.c1 > d.c0 ? (d.c1 - ((d.c0 >> 3) << 3) + select_chunk_tokens() - 1) / select_chunk_tokens() : 0;
@@ -587,6 +592,10 @@ int decode_impl(const a2ats_shape* shape, const a2ats_params* params, int32_t n_
   }
   if (lut_fma) {
     rc = cuda_status(launch_lut_fma(la, st));
+    if (rc) return rc;
+  }
+  if (lut_persist) {
+    rc = cuda_status(launch_lut_persist(la, tmA, st));
     if (rc) return rc;
   }
   rc = cuda_status(launch_prep(p, tmA, tmC, st));

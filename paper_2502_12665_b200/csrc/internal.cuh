@@ -275,6 +275,8 @@ cudaError_t launch_qprep(const LutArgs& la, cudaStream_t st);
 // a2 on the FP32 pipes (lut_engine FMA / AUTO for small B*G*L): agg, lut_full and the window table
 cudaError_t launch_lut_fma(const LutArgs& la, cudaStream_t st);
 size_t qprep_bytes(int Hkv, int nvt, int NV);
+// a2 with precomputed q~ tiles (la.qt): persistent warp-specialized tcgen05 LUT, one CTA per SM
+cudaError_t launch_lut_persist(const LutArgs& la, const CUtensorMap& tm_codebook, cudaStream_t st);
 cudaError_t launch_prep(const PrepArgs& p, const CUtensorMap& tm_codebook, const CUtensorMap& tm_chat,
                         cudaStream_t st);
 cudaError_t launch_scores(const float* lut_full, const uint16_t* codes, float* scores, int B, int Hq, int Hkv,

@@ -231,6 +231,171 @@ __device__ __forceinline__ void lut_tile(const CUtensorMap& tmA, const PrepArgs&
   if (warp == 0) umma::tmem_dealloc_n(tmem, p.lut_cols);
 }
 
+// Persistent warp-specialized LUT (a2; wide query tiles with precomputed q~, la.qt): one CTA
+// per SM walks a contiguous range of units (head h, vector tile y, 128-codeword tile x), x
+// fastest, so consecutive units share the q~ B tile.  Warp 0 produces (codeword tile by TMA,
+// B tile by bulk copy when (h, y) changes), warp 1 issues the 16 tcgen05.mma of a unit into one
+// of two TMEM accumulators, warps 2..9 drain the other accumulator (8 warps: TMEM lane quarter
+// w % 4, column half (w - 2) / 4), fold the G heads and store agg -- so the next unit's codeword
+// load and MMAs run under the current unit's epilogue, whose TMEM reads bound the kernel.
+constexpr int kLpWarps = 10;  // producer, MMA, 8 epilogue warps
+__host__ __device__ constexpr int lut_persist_smem(int NV) { return kTC * kD * 2 + NV * 2 * kD * 2 + 1024; }
+
+template <int G>
+__global__ __launch_bounds__(kLpWarps * 32, 1) void lut_persist_kernel(const __grid_constant__ CUtensorMap tmA,
+                                                                       const LutArgs a, int n_units, int ntx) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sA = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sB = sA + kTC * kD * 2;  // [32 chunks][NV vectors][16 B]
+  __shared__ __align__(8) uint64_t a_full, a_empty, b_full, b_empty, t_full[2], t_empty[2];
+  __shared__ uint32_t tslot;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int NV = a.NV, ncols = (int)umma::tmem_cols_for(NV);
+  const int u0 = (int)((long long)blockIdx.x * n_units / gridDim.x);
+  const int u1 = (int)((long long)(blockIdx.x + 1) * n_units / gridDim.x);
+  auto hy_of = [&](int u) { return u / ntx; };  // (h, y) block index = h * nvt + y
+  if (tid == 0) {
+    umma::mbar_init(&a_full, 1);
+    umma::mbar_init(&a_empty, 1);
+    umma::mbar_init(&b_full, 1);
+    umma::mbar_init(&b_empty, 1);
+    for (int j = 0; j < 2; ++j) {
+      umma::mbar_init(&t_full[j], 1);
+      umma::mbar_init(&t_empty[j], 8);
+    }
+    umma::mbar_fence_init();
+    if (u0 < u1) {  // the first codeword tile (a step input) before the dependency wait
+      const int h = hy_of(u0) / a.nvt, x = u0 % ntx;
+      umma::mbar_expect_tx(&a_full, kTC * kD * 2);
+      umma::tma_load_2d(sA, &tmA, 0, h * a.L + x * kTC, &a_full);
+      umma::tma_load_2d(sA + kTC * 128, &tmA, 64, h * a.L + x * kTC, &a_full);
+    }
+  }
+  A2ATS_TL(g_prep_tl, 0);
+  if (warp == 1) umma::tmem_alloc_n(&tslot, 2 * ncols);
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  const uint32_t tmem = tslot;
+  // q~ tiles come from qprep_kernel; the previous step's select reads agg.  Dependents may launch
+  // now: their pre-wait prologues read only step inputs
+  pdl_wait();
+  pdl_trigger();
+  A2ATS_TL(g_prep_tl, 2);
+  if (warp == 0) {
+    if (lane == 0) {  // producer
+      int nb = 0, cur = -1;
+      for (int u = u0, it = 0; u < u1; ++u, ++it) {
+        const int hy = hy_of(u), h = hy / a.nvt, x = u % ntx;
+        if (it > 0) {  // (unit 0's tile was issued before the wait)
+          umma::mbar_wait(&a_empty, (it - 1) & 1);  // the previous unit's MMAs are done with sA
+          umma::mbar_expect_tx(&a_full, kTC * kD * 2);
+          umma::tma_load_2d(sA, &tmA, 0, h * a.L + x * kTC, &a_full);
+          umma::tma_load_2d(sA + kTC * 128, &tmA, 64, h * a.L + x * kTC, &a_full);
+        }
+        if (hy != cur) {
+          if (nb > 0) umma::mbar_wait(&b_empty, (nb - 1) & 1);
+          umma::mbar_expect_tx(&b_full, (uint32_t)NV * 32 * 16);
+          umma::bulk_load(sB, a.qt + (size_t)hy * 32 * NV * 8, (uint32_t)NV * 32 * 16, &b_full);
+          cur = hy;
+          ++nb;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      const uint32_t idesc = umma::idesc_bf16(kTC, NV);
+      const uint32_t aBase = smem_u32(sA), bBase = smem_u32(sB);
+      int nb = 0, cur = -1;
+      for (int u = u0, it = 0; u < u1; ++u, ++it) {
+        const int j = it & 1, hy = hy_of(u);
+        if (it >= 2) umma::mbar_wait(&t_empty[j], ((it - 2) >> 1) & 1);  // accumulator j drained
+        umma::mbar_wait(&a_full, it & 1);
+        if (it == 0) A2ATS_TLX(g_prep_tl, 6);
+        if (hy != cur) {
+          umma::mbar_wait(&b_full, nb & 1);
+          cur = hy;
+          ++nb;
+        }
+        if (it == 0) A2ATS_TLX(g_prep_tl, 7);
+        umma::fence_after();
+        const uint32_t td = tmem + (uint32_t)(j * ncols);
+#pragma unroll
+        for (int s = 0; s < 16; ++s) {  // K = 256: 8 steps against q~_hi, 8 against q~_lo, same A
+          const int kk = s & 7;
+          const uint64_t ad = umma::sdesc_sw128(aBase + (kk >> 2) * (kTC * 128) + (kk & 3) * 32);
+          const uint64_t bd = umma::sdesc(bBase + (2 * s) * (NV * 16), NV * 16, 128);
+          umma::mma_bf16(td, ad, bd, idesc, s > 0 ? 1u : 0u);
+        }
+        umma::commit(&a_empty);                                 // sA reusable once these MMAs complete
+        if (u + 1 == u1 || hy_of(u + 1) != hy) umma::commit(&b_empty);  // last unit on this B tile
+        umma::commit(&t_full[j]);
+      }
+    }
+  } else {  // epilogue: TMEM lane quarter q, columns [half * NV / 2, (half + 1) * NV / 2)
+    const int q = warp & 3, half = (warp - 2) >> 2, nvec = a.B * G;
+    const bool sum = (a.group_reduce == A2ATS_GROUP_SUM);
+    const size_t bstride = (size_t)a.Hkv * a.L;
+    for (int u = u0, it = 0; u < u1; ++u, ++it) {
+      const int j = it & 1, hy = hy_of(u), h = hy / a.nvt, y = hy % a.nvt, x = u % ntx;
+      const int vec0 = y * NV, nv_here = min(NV, nvec - vec0);
+      const int code = x * kTC + q * 32 + lane;
+      const bool live = code < a.L;
+      float* aggp = a.agg + ((size_t)(vec0 / G) * a.Hkv + h) * a.L + code;
+      umma::mbar_wait(&t_full[j], (it >> 1) & 1);
+      umma::fence_after();
+      if (tid == 64 && it == 0) A2ATS_TLX(g_prep_tl, 3);
+      if (tid == 64 && u + 1 == u1) A2ATS_TLX(g_prep_tl, 5);
+      const uint32_t ta = tmem + (uint32_t)(j * ncols) + ((uint32_t)(q * 32) << 16);
+      auto fold = [&](const uint32_t* r, int col0) {  // 16 columns = 16 / G batch elements
+        if (a.lut_full && live) {
+#pragma unroll 1
+          for (int ii = 0; ii < 16 && col0 + ii < nv_here; ++ii) {
+            const int vn = vec0 + col0 + ii, b = vn / G, g = vn - b * G;
+            float xi = 0.f;
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) xi = (jj == ii) ? __uint_as_float(r[jj]) : xi;
+            a.lut_full[((size_t)b * a.Hq + h * G + g) * a.L + code] = xi;
+          }
+        }
+        float* pb = aggp + (size_t)(col0 / G) * bstride;
+#pragma unroll
+        for (int bb = 0; bb < 16 / G; ++bb) {
+          float v = __uint_as_float(r[bb * G]);
+#pragma unroll
+          for (int g = 1; g < G; ++g) {
+            const float xg = __uint_as_float(r[bb * G + g]);
+            v = sum ? v + xg : fmaxf(v, xg);
+          }
+          if (live && col0 + bb * G < nv_here) pb[bb * bstride] = v;
+        }
+      };
+      const int c_lo = half * (NV >> 1), c_hi = min(c_lo + (NV >> 1), nv_here);
+      for (int col0 = c_lo; col0 < c_hi; col0 += 64) {  // two 32-column loads in flight per wait
+        uint32_t r[64];
+        umma::tmem_ld32(ta + col0, *reinterpret_cast<uint32_t(*)[32]>(r));
+        if (col0 + 32 < c_hi) umma::tmem_ld32(ta + col0 + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
+        umma::tmem_wait_ld();
+        fold(r, col0);
+        fold(r + 16, col0 + 16);
+        if (col0 + 32 < c_hi) {
+          fold(r + 32, col0 + 32);
+          fold(r + 48, col0 + 48);
+        }
+      }
+      umma::fence_before();
+      __syncwarp();
+      if (lane == 0) umma::mbar_arrive(&t_empty[j]);
+      if (tid == 64 && it == 0) A2ATS_TLX(g_prep_tl, 4);
+    }
+  }
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  if (warp == 1) umma::tmem_dealloc_n(tmem, 2 * ncols);
+  A2ATS_TL(g_prep_tl, 1);
+}
+
 // Window role: pairs [pair0, pair0 + np) (the window rows, hence the rotation table, are
 // the same for every pair).  Scratch (16-B chunks XOR-swizzled by row): cs [64][64] float2,
 // K rows [64][128] bf16, q (base-2 scaled) [8][128] fp32.
@@ -530,6 +695,24 @@ cudaError_t launch_lut_fma_fv(const LutArgs& la, cudaStream_t st) {
 // the speed of two 16-vector tiles)
 cudaError_t launch_lut_fma(const LutArgs& la, cudaStream_t st) {
   return la.B * la.G <= 8 ? launch_lut_fma_fv<8>(la, st) : launch_lut_fma_fv<16>(la, st);
+}
+
+template <int G>
+cudaError_t launch_lut_persist_g(const LutArgs& la, const CUtensorMap& tmA, cudaStream_t st) {
+  const int smem = lut_persist_smem(la.NV);
+  cudaError_t e = ensure_smem(lut_persist_kernel<G>, smem);
+  if (e != cudaSuccess) return e;
+  const int ntx = (la.L + kTC - 1) / kTC, n_units = la.Hkv * la.nvt * ntx;
+  const int grid = std::min(sm_count(), n_units);
+  return launch_pdl(lut_persist_kernel<G>, dim3(grid), dim3(kLpWarps * 32), smem, st, tmA, la, n_units, ntx);
+}
+cudaError_t launch_lut_persist(const LutArgs& la, const CUtensorMap& tmA, cudaStream_t st) {
+  switch (la.G) {
+    case 1: return launch_lut_persist_g<1>(la, tmA, st);
+    case 2: return launch_lut_persist_g<2>(la, tmA, st);
+    case 4: return launch_lut_persist_g<4>(la, tmA, st);
+    default: return launch_lut_persist_g<8>(la, tmA, st);
+  }
 }
 
 size_t qprep_bytes(int Hkv, int nvt, int NV) { return (size_t)Hkv * nvt * 32 * NV * 16; }

@@ -1625,10 +1625,10 @@ __global__ __launch_bounds__(kQT, A2ATS_QT_MINB) void select_postings_kernel(Sel
   // step inputs, every load in flight at once: the pair's hist row and list-bounds row (one bulk
   // copy each into shared memory when 16-B aligned, else coalesced loads), the codes of its sinks
   // / window tokens (not candidates: subtracted from hist), the indexed sinks' codes and the first
-  // 2 kQT unindexed tail tokens' codes (registers)
+  // 4 kQT unindexed tail tokens' codes (registers)
   const int LP = postings_off_stride(a.L);
   const int post0 = pair * LP;
-  uint32_t tcode, skmask = 0u;
+  uint32_t tcode[2], skmask = 0u;  // the first 4 kQT tail tokens' codes (16 bits each)
   {
     __shared__ __align__(8) uint64_t s_pbar;
     const int32_t* histp = a.hist + (size_t)pair * a.L;
@@ -1651,7 +1651,10 @@ __global__ __launch_bounds__(kQT, A2ATS_QT_MINB) void select_postings_kernel(Sel
     if (tid < nrem) rc = cp[tid < a.n_s ? tid : a.w0 + (tid - a.n_s)];
     if (list_ok && tid < nsk) s_sk[tid] = cp[tid];
     const int tb = max(a.n_post, a.c0) + tid;
-    tcode = (tb < a.c1 ? (uint32_t)cp[tb] : 0u) | (tb + kQT < a.c1 ? (uint32_t)cp[tb + kQT] << 16 : 0u);
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+      tcode[r] = (tb + 2 * r * kQT < a.c1 ? (uint32_t)cp[tb + 2 * r * kQT] : 0u) |
+                 (tb + (2 * r + 1) * kQT < a.c1 ? (uint32_t)cp[tb + (2 * r + 1) * kQT] << 16 : 0u);
     A2ATS_TL(g_selp_tl, 0);
     __syncthreads();  // (barrier init, s_sk)
     for (int i = 0; i < nsk; ++i) {  // this thread's codewords holding an indexed sink
@@ -1733,8 +1736,10 @@ __global__ __launch_bounds__(kQT, A2ATS_QT_MINB) void select_postings_kernel(Sel
     int* hs = reinterpret_cast<int*>(sm);  // above code h: list start (past its sinks)
     int* hn = hs + nA4;                    //               entries
     int* hp = hn + nA4;                    //               output position
-    int* stg = hp + nA4;                   // staging of the above entries at their output positions
-    const int stg_cap = RT - 3 * nA4;
+    // staging of the above entries at their output positions, 16-B phase of selp (bulk store)
+    const int sph = (int)((reinterpret_cast<uintptr_t>(selp) >> 2) & 3);
+    int* stg = hp + nA4 + sph;
+    const int stg_cap = RT - 3 * nA4 - 4;
     {
       int ih = ex[0], ip = ex[1], it = ex[2];
       for (uint32_t mm = hmask; mm; mm &= mm - 1u) {
@@ -1768,7 +1773,16 @@ __global__ __launch_bounds__(kQT, A2ATS_QT_MINB) void select_postings_kernel(Sel
         const int n = hn[h];
         const int32_t* src = ptok + hs[h] + sub;
         uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(stg + hp[h] + sub));
-        for (int j = sub; j < n; j += 8, src += 8, d += 32)
+        int j = sub;
+        for (; j + 24 < n; j += 32, src += 32, d += 128)
+          asm volatile(
+              "cp.async.ca.shared.global [%0], [%1], 4;\n\t"
+              "cp.async.ca.shared.global [%2], [%3], 4;\n\t"
+              "cp.async.ca.shared.global [%4], [%5], 4;\n\t"
+              "cp.async.ca.shared.global [%6], [%7], 4;" ::"r"(d), "l"(src), "r"(d + 32), "l"(src + 8), "r"(d + 64),
+              "l"(src + 16), "r"(d + 96), "l"(src + 24)
+              : "memory");
+        for (; j < n; j += 8, src += 8, d += 32)
           asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
       }
       if (tie_staged)
@@ -1779,8 +1793,18 @@ __global__ __launch_bounds__(kQT, A2ATS_QT_MINB) void select_postings_kernel(Sel
       cp_async_commit();
       cp_async_wait<0>();
       __syncthreads();
+      // out: the 16-B aligned middle by one bulk store (TMA engine), head / tail by threads
       const int lim = min(A_idx, (int)cap);
-      for (int i = tid; i < lim; i += kQT) selp[i] = stg[i];
+      const int i0 = min(lim, (4 - sph) & 3), i1 = i0 + ((lim - i0) & ~3);
+      if (tid < i0) selp[tid] = stg[tid];
+      if (tid < lim - i1) selp[i1 + tid] = stg[i1 + tid];
+      if (tid == 0 && i1 > i0) {
+        umma::fence_proxy_async();
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(selp + i0),
+                     "r"(static_cast<uint32_t>(__cvta_generic_to_shared(stg + i0))), "r"((uint32_t)(i1 - i0) * 4u)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
     } else {
       constexpr int kU = 8, kW = kQT / 32;
       for (int h0 = warp; h0 < nA; h0 += kW * kU) {
@@ -1812,7 +1836,7 @@ __global__ __launch_bounds__(kQT, A2ATS_QT_MINB) void select_postings_kernel(Sel
     // tail [max(n_post, c0), c1): classified from codes; counts first (A needs the above count)
     const int tb0 = max(a.n_post, a.c0);
     auto tail_code = [&](int t, int r) {  // code of tail token t = tb0 + r * kQT + tid
-      return r < 2 ? (int)((tcode >> (16 * r)) & 0xffffu) : (int)cp[t];
+      return r < 4 ? (int)(((r < 2 ? tcode[0] : tcode[1]) >> (16 * (r & 1))) & 0xffffu) : (int)cp[t];
     };
     int tA = 0, tT = 0;
     for (int t = tb0 + tid, r = 0; t < a.c1; t += kQT, ++r) {
@@ -1881,6 +1905,7 @@ __global__ __launch_bounds__(kQT, A2ATS_QT_MINB) void select_postings_kernel(Sel
         }
       }
     }
+    if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // (the bulk store complete)
     A2ATS_TL(g_selp_tl, 7);
     A2ATS_TL(g_sel_tl, 1);
     return;

@@ -80,6 +80,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t phase) {
       : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* mbar) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(mbar));
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* mbar, uint32_t bytes) {
   const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(mbar));
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");

@@ -1,3 +1,3 @@
-# ncu full capture of the C4 select-only path with postings (qprep, LUT prep kernel, postings select)
+# ncu full capture of the C4 select-only path with postings (LUT prep kernel, postings select, index build)
 mkdir -p gpurun_out
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:"qprep|prep_kernel|select_postings" -s 9 -c 3 -o gpurun_out/full_post -f python tools/kbench.py --config C4 --select-only --postings --iters 5 > gpurun_out/ncu_fp.log 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"prep_kernel|select_postings|postings_build" -s 3 -c 4 -o gpurun_out/full_post2 -f python tools/kbench.py --config C4 --select-only --postings --iters 4 > gpurun_out/ncu_fp.log 2>&1

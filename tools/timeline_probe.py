@@ -91,6 +91,11 @@ for it in range(args.iters):
         q = np.percentile(du, [0, 50, 90, 100])
         print(f"{k:7s} ctas {len(a):5d} start {st.min():7.2f}..{st.max():7.2f} end {en.min():7.2f}..{en.max():7.2f}"
               f"  dur min/med/p90/max {q[0]:6.2f} {q[1]:6.2f} {q[2]:6.2f} {q[3]:6.2f}")
+    if args.postings:  # persistent LUT marks: 2 wait, 3 first unit's accumulator, 4 first epilogue, 5 last accumulator, 6 last epilogue
+        r = tl["prep"][valid["prep"]]
+        d = lambda x, y: np.percentile((r[:, x] - r[:, y]) / 1e3, [10, 50, 90]).round(2)
+        print("  lut_persist (p10/p50/p90): setup+wait", d(2, 0), " first A", d(6, 2), " first B", d(7, 2),
+              " first mma", d(3, 7), " first epi", d(4, 3), " to last mma", d(5, 4), " last epi+end", d(1, 5))
     # prep roles (slot 7: 1 LUT, 2 encode, 3 window)
     pa, pidx = tl["prep"], valid["prep"]
     for name, role in (("lut", 1), ("encode", 2), ("window", 3)):
