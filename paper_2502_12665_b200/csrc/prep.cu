@@ -496,8 +496,22 @@ __device__ __forceinline__ void window_tile(const PrepArgs& p, int pair0, int np
 // Thread <-> (tile, 8-pair chunk c, vector n), n fastest (coalesced 16-B stores).  Also writes
 // the window table cs (fp64 angles) that the LUT CTAs write when there is no qprep.
 __global__ __launch_bounds__(256) void qprep_kernel(LutArgs a) {
+#ifdef A2ATS_PHASES
+  if (threadIdx.x == 0) {  // timeline rows 4096.. (tuning builds)
+    unsigned long long t_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+    g_prep_tl[4096 + blockIdx.x][0] = t_;
+  }
+#endif
   pdl_wait();  // the previous step's LUT reads qt
   pdl_trigger();
+#ifdef A2ATS_PHASES
+  if (threadIdx.x == 0) {
+    unsigned long long t_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+    g_prep_tl[4096 + blockIdx.x][2] = t_;
+  }
+#endif
   const int NV = a.NV, nvec = a.B * a.G;
   const int it = blockIdx.x * blockDim.x + threadIdx.x;
   for (int k = it; k < a.window * kHalf; k += gridDim.x * blockDim.x) {  // window table cs[r][m]
@@ -529,6 +543,13 @@ __global__ __launch_bounds__(256) void qprep_kernel(LutArgs a) {
   dst[(c + 8) * NV + n] = pack8(h2);
   dst[(c + 16) * NV + n] = pack8(l1);
   dst[(c + 24) * NV + n] = pack8(l2);
+#ifdef A2ATS_PHASES
+  if (threadIdx.x == 0) {
+    unsigned long long t_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+    g_prep_tl[4096 + blockIdx.x][1] = t_;
+  }
+#endif
 }
 
 // a2 on the FP32 pipes: LUT[b, hq, l] = q~ . c_l (Eq. 21) with q~ = q R_b (Eq. 12) in fp32,

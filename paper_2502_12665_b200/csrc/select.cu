@@ -2073,7 +2073,17 @@ __global__ __launch_bounds__(kBW * 32) void postings_build_kernel(const uint16_t
   __syncthreads();
   const int per = (n_tok + kBW - 1) / kBW, t0 = min(n_tok, warp * per), t1 = min(n_tok, t0 + per);
   int* my = pcnt + warp * L;
-  for (int t = t0 + lane; t < t1; t += 32) atomicAdd(&my[cp[t]], 1);
+  for (int tb = t0; tb < t1; tb += 32 * 8) {  // 8 code loads in flight per lane
+    int cc[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int t = tb + 32 * k + lane;
+      cc[k] = t < t1 ? (int)cp[t] : -1;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (cc[k] >= 0) atomicAdd(&my[cc[k]], 1);
+  }
   __syncthreads();
   // thread owns codes [l0, l0 + pc): its total, block scan, then the cursors
   const int pc = (L + NT - 1) / NT, l0 = tid * pc;
@@ -2106,18 +2116,26 @@ __global__ __launch_bounds__(kBW * 32) void postings_build_kernel(const uint16_t
   __syncthreads();
   int32_t* tp = post_tok + (size_t)pair * n_max;
   const unsigned lt = (1u << lane) - 1u;
-  for (int tb = t0; tb < t1; tb += 32) {
-    const int t = tb + lane;
-    const int code = t < t1 ? (int)cp[t] : -1 - lane;  // (inactive lanes: unique keys)
-    const unsigned peers = __match_any_sync(0xffffffffu, code);
-    int b = 0;
-    if (t < t1) {
-      b = my[code];
-      tp[b + __popc(peers & lt)] = t;
+  for (int tb0 = t0; tb0 < t1; tb0 += 32 * 8) {  // 8 code loads in flight per lane, then 8 steps of 32
+    int cc[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int t = tb0 + 32 * k + lane;
+      cc[k] = t < t1 ? (int)cp[t] : -1 - lane;  // (inactive lanes: unique keys)
     }
-    __syncwarp();
-    if (t < t1 && (peers & lt) == 0u) my[code] = b + __popc(peers);
-    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int t = tb0 + 32 * k + lane, code = cc[k];
+      const unsigned peers = __match_any_sync(0xffffffffu, code);
+      int b = 0;
+      if (t < t1) {
+        b = my[code];
+        tp[b + __popc(peers & lt)] = t;
+      }
+      __syncwarp();
+      if (t < t1 && (peers & lt) == 0u) my[code] = b + __popc(peers);
+      __syncwarp();
+    }
   }
 }
 

@@ -25,6 +25,7 @@ ap.add_argument("--config", default="C2")
 ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--select-only", action="store_true", help="a2ats_select_topk (a1..a4) instead of the step")
 ap.add_argument("--postings", action="store_true", help="select-only through the posting-list engine (f3)")
+ap.add_argument("--graph", action="store_true", help="the postings select replayed from a CUDA graph")
 args = ap.parse_args()
 cfg = CONFIGS[args.config]
 inp = make_inputs(cfg, 5, device="cuda", with_h=True)
@@ -55,10 +56,20 @@ if args.postings:
     args.select_only = True
     dec.build_postings(cfg.N - cfg.window - 256)
 ncta = {}
+g_post = None
+if args.postings and args.graph:
+    dec.select_postings(inp["q"], cfg.N, sel_buf)
+    torch.cuda.synchronize()
+    g_post = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g_post):
+        dec.select_postings(inp["q"], cfg.N, sel_buf)
+    torch.cuda.synchronize()
 for it in range(args.iters):
     flush.fill_(it)
     dec.hist.copy_(hist if args.select_only else hist0)  # step: covers [0, N-1), the step appends N-1
-    if args.postings:
+    if g_post is not None:
+        g_post.replay()
+    elif args.postings:
         dec.select_postings(inp["q"], cfg.N, sel_buf)
     elif args.select_only:
         dec.select(inp["q"], cfg.N, sel_buf)
@@ -79,6 +90,8 @@ for it in range(args.iters):
         a = tl[k]
         last = a[:, 0].max()
         m = (a[:, 0] > last - 2_000_000) & (a[:, 1] >= a[:, 0]) & (a[:, 0] > 0)  # this step's CTAs
+        if k == "prep":
+            m[4096:] = False  # (qprep rows)
         valid[k] = np.nonzero(m)[0]
     t0 = min(tl[k][valid[k], 0].min() for k in kernels if len(valid[k]))
     print(f"--- iter {it} (us from first CTA start)")
@@ -91,6 +104,12 @@ for it in range(args.iters):
         q = np.percentile(du, [0, 50, 90, 100])
         print(f"{k:7s} ctas {len(a):5d} start {st.min():7.2f}..{st.max():7.2f} end {en.min():7.2f}..{en.max():7.2f}"
               f"  dur min/med/p90/max {q[0]:6.2f} {q[1]:6.2f} {q[2]:6.2f} {q[3]:6.2f}")
+    qp = tl["prep"][4096:4096 + 256]
+    qp = qp[(qp[:, 0] > 0) & (qp[:, 1] >= qp[:, 0]) & (qp[:, 0] > tl["prep"][:, 0].max() - 2_000_000)]
+    if len(qp):
+        print(f"  qprep ctas {len(qp)} start {(qp[:, 0].min() - t0) / 1e3:.2f}..{(qp[:, 0].max() - t0) / 1e3:.2f}"
+              f" wait-ret {(qp[:, 2].min() - t0) / 1e3:.2f}..{(qp[:, 2].max() - t0) / 1e3:.2f}"
+              f" end {(qp[:, 1].min() - t0) / 1e3:.2f}..{(qp[:, 1].max() - t0) / 1e3:.2f}")
     if args.postings:  # persistent LUT marks: 2 wait, 3 first unit's accumulator, 4 first epilogue, 5 last accumulator, 6 last epilogue
         r = tl["prep"][valid["prep"]]
         d = lambda x, y: np.percentile((r[:, x] - r[:, y]) / 1e3, [10, 50, 90]).round(2)
