@@ -59,9 +59,16 @@ extern "C" {
 #define A2ATS_ENCCL (-5)        /* an NCCL call failed (sharded entry points) */
 
 /* group_reduce: how the G query heads of one KV head are folded into one
- * ranking score per token (paper silent; reading Q10). */
+ * ranking score per token (paper silent; reading Q10).  PER_HEAD: no fold --
+ * every query head selects its own top-K from its own LUT row and attends over
+ * its own Sel (the paper's per-head retrieval): the
+ * step runs G GQA-free sub-steps (G' = 1) over the same codes / hist / K / V,
+ * sel_out is then [B, Hq, topk] (row b, hq), scores_out is not supported
+ * (EUNSUPPORTED), and a workspace sized for one mode must be zeroed before it
+ * is used with the other. */
 #define A2ATS_GROUP_MAX 0
 #define A2ATS_GROUP_SUM 1
+#define A2ATS_GROUP_PER_HEAD 2
 
 /* kv_location (reading: the paper's CPU-resident KV cache of P:392-394). */
 #define A2ATS_KV_DEVICE 0       /* K/V cache in HBM */
@@ -92,7 +99,7 @@ typedef struct a2ats_params {
   double rope_theta;     /* RoPE base; 1e4 by default (reading Q1)                    */
   const double* inv_freq;/* optional HOST array [d/2] of rotation frequencies that
                             overrides rope_theta (e.g. Llama-3.1 scaled frequencies)   */
-  int32_t group_reduce;  /* A2ATS_GROUP_MAX (default) | A2ATS_GROUP_SUM               */
+  int32_t group_reduce;  /* A2ATS_GROUP_MAX (default) | _SUM | _PER_HEAD               */
   int32_t kv_location;   /* A2ATS_KV_DEVICE (default) | A2ATS_KV_HOST_MAPPED          */
   int32_t lut_engine;    /* A2ATS_LUT_AUTO (default) | A2ATS_LUT_TENSOR | A2ATS_LUT_FMA */
   int32_t reserved;      /* 0                                                          */

@@ -23,6 +23,7 @@ A2ATS_ECUDA = -4
 A2ATS_ENCCL = -5
 A2ATS_GROUP_MAX = 0
 A2ATS_GROUP_SUM = 1
+A2ATS_GROUP_PER_HEAD = 2
 A2ATS_KV_DEVICE = 0
 A2ATS_KV_HOST_MAPPED = 1
 A2ATS_LUT_AUTO, A2ATS_LUT_TENSOR, A2ATS_LUT_FMA = 0, 1, 2

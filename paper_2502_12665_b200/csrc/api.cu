@@ -104,7 +104,9 @@ int check_params(const a2ats_params* p) {
   if (!p) return A2ATS_EINVAL;
   if (p->window < 1 || p->bridge < 0 || p->n_sink < 0 || p->topk < 0) return A2ATS_EINVAL;
   if (!(p->rope_theta > 0.0) && !p->inv_freq) return A2ATS_EINVAL;
-  if (p->group_reduce != A2ATS_GROUP_MAX && p->group_reduce != A2ATS_GROUP_SUM) return A2ATS_EINVAL;
+  if (p->group_reduce != A2ATS_GROUP_MAX && p->group_reduce != A2ATS_GROUP_SUM &&
+      p->group_reduce != A2ATS_GROUP_PER_HEAD)
+    return A2ATS_EINVAL;
   if (p->kv_location != A2ATS_KV_DEVICE && p->kv_location != A2ATS_KV_HOST_MAPPED) return A2ATS_EINVAL;
   if (p->lut_engine < A2ATS_LUT_AUTO || p->lut_engine > A2ATS_LUT_FMA) return A2ATS_EINVAL;
   return A2ATS_OK;
@@ -165,6 +167,33 @@ DecodeWs decode_layout(const a2ats_shape* s, const a2ats_params* p) {
     w.qt = o; o = align_up(o + qprep_bytes(s->Hkv, nvt, NV));                                // q~ B tiles
   }
   w.pbits = o; o = align_up(o + (size_t)P * postings_bits_stride(s->n_max) * 4);             // postings bitmap path
+  w.total = o;
+  return w;
+}
+
+// Per-query-head selection (A2ATS_GROUP_PER_HEAD, G > 1): G sub-steps on the shape with Hq' = Hkv
+// (G' = 1); the workspace holds the sub-step's own layout first, then q of one head position g
+// [B, Hkv, d] bf16, the sub-step's output [B, Hkv, d] fp32 and selection [B, Hkv, K] int32.
+bool per_head(const a2ats_shape* s, const a2ats_params* p) {
+  return p->group_reduce == A2ATS_GROUP_PER_HEAD && s->Hq != s->Hkv;
+}
+struct PerHeadWs {
+  a2ats_shape sub;
+  a2ats_params subp;
+  size_t inner, qg, outg, selg, total;
+};
+PerHeadWs per_head_layout(const a2ats_shape* s, const a2ats_params* p) {
+  PerHeadWs w;
+  w.sub = *s;
+  w.sub.Hq = s->Hkv;
+  w.subp = *p;
+  w.subp.group_reduce = A2ATS_GROUP_MAX;  // (one query head per group: the fold is the identity)
+  const size_t P = (size_t)s->B * s->Hkv;
+  size_t o = 0;
+  w.inner = o; o = align_up(o + decode_layout(&w.sub, &w.subp).total);
+  w.qg = o; o = align_up(o + P * kD * 2);
+  w.outg = o; o = align_up(o + P * kD * 4);
+  w.selg = o; o = align_up(o + P * (size_t)std::max<long long>(std::min<long long>(p->topk, s->n_max), 1) * 4);
   w.total = o;
   return w;
 }
@@ -488,18 +517,104 @@ int a2ats_build_codes(const a2ats_shape* shape, const void* keys, int32_t t_begi
 
 size_t a2ats_decode_workspace_bytes(const a2ats_shape* shape, const a2ats_params* params) {
   if (check_shape(shape) || check_params(params)) return 0;
-  return decode_layout(shape, params).total;
+  return per_head(shape, params) ? per_head_layout(shape, params).total : decode_layout(shape, params).total;
 }
 
 }  // extern "C"
 
+namespace a2ats {
 namespace {
-// One decode step (a1..a6); with chat != nullptr also a0 for token n_ctx - 1 (append).
+// Per-query-head selection plumbing (no arithmetic): q of head position g -> [B, Hkv, d]; the
+// sub-step's output rows and selection rows back to (b, h * G + g).  One 16-B piece per thread.
+__global__ __launch_bounds__(256) void head_gather_q_kernel(const uint4* q, uint4* qg, int P, int Hkv, int G, int g) {
+  pdl_wait();  // the previous sub-step reads qg
+  pdl_trigger();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P * 16) return;
+  const int r = i >> 4, b = r / Hkv, h = r - b * Hkv;
+  qg[i] = q[((size_t)b * Hkv * G + (size_t)h * G + g) * 16 + (i & 15)];
+}
+__global__ __launch_bounds__(256) void head_scatter_kernel(const uint4* outg, uint4* out, const int32_t* selg,
+                                                           int32_t* sel, int P, int Hkv, int G, int g, int keff) {
+  pdl_wait();  // the sub-step's attention / select wrote outg, selg
+  pdl_trigger();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (out && i < P * 32) {
+    const int r = i >> 5, b = r / Hkv, h = r - b * Hkv;
+    out[((size_t)b * Hkv * G + (size_t)h * G + g) * 32 + (i & 31)] = outg[i];
+  }
+  if (sel) {
+    for (long long j = i; j < (long long)P * keff; j += (long long)gridDim.x * blockDim.x) {
+      const int r = (int)(j / keff), b = r / Hkv, h = r - b * Hkv;
+      sel[((size_t)b * Hkv * G + (size_t)h * G + g) * keff + (j - (long long)r * keff)] = selg[j];
+    }
+  }
+}
+}  // namespace
+}  // namespace a2ats
+
+namespace {
+int decode_impl_one(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx, const void* q,
+                    const void* k_cache, const void* v_cache, uint16_t* codes, const void* codebook, int32_t* hist,
+                    const void* chat, const float* nrm, float* out, int32_t* sel_out, float* scores_out, void* ws,
+                    size_t ws_bytes, void* stream, bool attend, const void* postings, int32_t n_post);
+
+// One decode step (a1..a6); with chat != nullptr also a0 for token n_ctx - 1 (append).  Per-query-
+// head selection (A2ATS_GROUP_PER_HEAD, G > 1): G sub-steps with G' = 1, the append (a0 + hist) in
+// the first only.
 int decode_impl(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx, const void* q,
                 const void* k_cache, const void* v_cache, uint16_t* codes, const void* codebook, int32_t* hist,
                 const void* chat, const float* nrm, float* out, int32_t* sel_out, float* scores_out, void* ws,
                 size_t ws_bytes, void* stream, bool attend = true, const void* postings = nullptr,
                 int32_t n_post = 0) {
+  int rc = check_shape(shape);
+  if (rc) return rc;
+  rc = check_params(params);
+  if (rc) return rc;
+  if (!per_head(shape, params)) {
+    a2ats_params p1 = *params;
+    if (p1.group_reduce == A2ATS_GROUP_PER_HEAD) p1.group_reduce = A2ATS_GROUP_MAX;  // (G = 1)
+    return decode_impl_one(shape, &p1, n_ctx, q, k_cache, v_cache, codes, codebook, hist, chat, nrm, out, sel_out,
+                           scores_out, ws, ws_bytes, stream, attend, postings, n_post);
+  }
+  if (scores_out) return A2ATS_EUNSUPPORTED;
+  if (!q || !aligned16(q) || n_ctx <= 0 || n_ctx > shape->n_max) return A2ATS_EINVAL;
+  if (attend ? !out : !sel_out) return A2ATS_EINVAL;
+  const PerHeadWs L = per_head_layout(shape, params);
+  if (!ws || ws_bytes < L.total) return A2ATS_EWORKSPACE;
+  Derived d;
+  derive(&L.sub, &L.subp, n_ctx, &d);
+  const int G = shape->Hq / shape->Hkv, P = shape->B * shape->Hkv;
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  uint4* qg = reinterpret_cast<uint4*>(base + L.qg);
+  float* outg = reinterpret_cast<float*>(base + L.outg);
+  int32_t* selg = reinterpret_cast<int32_t*>(base + L.selg);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  for (int g = 0; g < G; ++g) {
+    rc = cuda_status(launch_pdl(head_gather_q_kernel, dim3((P * 16 + 255) / 256), dim3(256), 0, st,
+                                static_cast<const uint4*>(q), qg, P, shape->Hkv, G, g));
+    if (rc) return rc;
+    rc = decode_impl_one(&L.sub, &L.subp, n_ctx, qg, k_cache, v_cache, codes, codebook, hist,
+                         g == 0 ? chat : nullptr, g == 0 ? nrm : nullptr, attend ? outg : nullptr,
+                         (sel_out || !attend) ? selg : nullptr, nullptr, base + L.inner, L.qg - L.inner, stream,
+                         attend, postings, n_post);
+    if (rc) return rc;
+    const int keff = sel_out ? d.keff : 0;
+    const long long work = std::max<long long>((long long)P * 32, (long long)P * keff);
+    const int grid = (int)std::min<long long>((work + 255) / 256, 4096);
+    rc = cuda_status(launch_pdl(head_scatter_kernel, dim3(std::max(grid, 1)), dim3(256), 0, st,
+                                reinterpret_cast<const uint4*>(outg), attend ? reinterpret_cast<uint4*>(out) : nullptr,
+                                selg, sel_out, P, shape->Hkv, G, g, keff));
+    if (rc) return rc;
+  }
+  return A2ATS_OK;
+}
+
+// One decode step (a1..a6) of one selection mode (max / sum fold, or G = 1).
+int decode_impl_one(const a2ats_shape* shape, const a2ats_params* params, int32_t n_ctx, const void* q,
+                    const void* k_cache, const void* v_cache, uint16_t* codes, const void* codebook, int32_t* hist,
+                const void* chat, const float* nrm, float* out, int32_t* sel_out, float* scores_out, void* ws,
+                size_t ws_bytes, void* stream, bool attend, const void* postings, int32_t n_post) {
   int rc = check_shape(shape);
   if (rc) return rc;
   rc = check_params(params);

@@ -1,2 +1,2 @@
 mkdir -p gpurun_out
-timeout 300 python tools/timeline_probe.py --config C4 --postings --graph --iters 3 > gpurun_out/tl_post.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_per_head.py -x -q -m gpu > gpurun_out/pytest_ph.log 2>&1
