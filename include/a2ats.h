@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define A2ATS_ABI_VERSION 8
+#define A2ATS_ABI_VERSION 9
 
 /* ---- status codes ---------------------------------------------------- */
 #define A2ATS_OK 0
@@ -89,6 +89,13 @@ typedef struct a2ats_shape {
   int32_t d;      /* head dimension; 128 in this version                      */
   int32_t L;      /* codebook size (P:431 uses 4096); 1 <= L <= 16384         */
   int32_t n_max;  /* capacity (tokens) of the K/V cache and code arrays; % 8 == 0 */
+  int32_t code_bytes; /* width of a code: 2 (uint16; 0 means 2) or 1 (uint8, L <= 256:
+                         half the index memory, aux-mem 1/256).  With 1
+                         every `uint16_t* codes` argument points to uint8 codes
+                         [B, Hkv, n_max]; supported by a2ats_build_codes, the posting-
+                         list entry points (a2ats_postings_build, a2ats_*_postings) and
+                         a2ats_qavq_prepare; the code-scan entry points, scores_out and
+                         the sharded step return A2ATS_EUNSUPPORTED */
 } a2ats_shape;
 
 typedef struct a2ats_params {

@@ -40,7 +40,8 @@ class A2ATSError(RuntimeError):
 
 class a2ats_shape(ctypes.Structure):
     _fields_ = [("B", ctypes.c_int32), ("Hq", ctypes.c_int32), ("Hkv", ctypes.c_int32),
-                ("d", ctypes.c_int32), ("L", ctypes.c_int32), ("n_max", ctypes.c_int32)]
+                ("d", ctypes.c_int32), ("L", ctypes.c_int32), ("n_max", ctypes.c_int32),
+                ("code_bytes", ctypes.c_int32)]
 
 
 class a2ats_params(ctypes.Structure):
@@ -75,7 +76,7 @@ _SIGS = {
 _lib = None
 
 
-ABI_VERSION = 8  # include/a2ats.h A2ATS_ABI_VERSION
+ABI_VERSION = 9  # include/a2ats.h A2ATS_ABI_VERSION
 
 
 def load(path: str = LIB_PATH, build_if_missing: bool = True) -> ctypes.CDLL:
@@ -109,8 +110,8 @@ def _check(fn: str, rc: int):
 
 
 # ------------------------------------------------------------------ shapes / params
-def make_shape(B, Hq, Hkv, d, L, n_max) -> a2ats_shape:
-    return a2ats_shape(B, Hq, Hkv, d, L, n_max)
+def make_shape(B, Hq, Hkv, d, L, n_max, code_bytes=2) -> a2ats_shape:
+    return a2ats_shape(B, Hq, Hkv, d, L, n_max, code_bytes)
 
 
 @dataclass
@@ -158,6 +159,11 @@ def _ptr(t, name, dtype=None, optional=False, host_ok=False):
     return t.data_ptr()
 
 
+def _code_dtype(shape):
+    import torch
+    return torch.uint8 if getattr(shape, "code_bytes", 2) == 1 else torch.uint16
+
+
 def _stream(stream):
     if stream is None:
         import torch
@@ -182,7 +188,7 @@ def a2ats_build_codes(shape: a2ats_shape, keys, t_begin: int, t_end: int, chat, 
                       stream=None):
     import torch
     rc = load().a2ats_build_codes(ctypes.byref(shape), _ptr(keys, "keys", torch.bfloat16), int(t_begin), int(t_end),
-                                  _ptr(chat, "chat", torch.bfloat16), _ptr(nrm, "nrm", torch.float32), _ptr(codes, "codes", torch.uint16),
+                                  _ptr(chat, "chat", torch.bfloat16), _ptr(nrm, "nrm", torch.float32), _ptr(codes, "codes", _code_dtype(shape)),
                                   _ptr(hist, "hist", torch.int32, optional=True), _ptr(ws, "ws"),
                                   ws.numel() * ws.element_size(), _stream(stream))
     _check("a2ats_build_codes", rc)
@@ -200,7 +206,7 @@ def a2ats_decode_step(shape: a2ats_shape, params, n_ctx: int, q, k_cache, v_cach
     rc = load().a2ats_decode_step(
         ctypes.byref(shape), ctypes.byref(p), int(n_ctx), _ptr(q, "q", torch.bfloat16),
         _ptr(k_cache, "k_cache", torch.bfloat16, host_ok=kv_host), _ptr(v_cache, "v_cache", torch.bfloat16, host_ok=kv_host),
-        _ptr(codes, "codes", torch.uint16), _ptr(codebook, "codebook", torch.bfloat16),
+        _ptr(codes, "codes", _code_dtype(shape)), _ptr(codebook, "codebook", torch.bfloat16),
         _ptr(hist, "hist", torch.int32, optional=True), _ptr(out, "out", torch.float32, host_ok="pinned"),
         _ptr(sel_out, "sel_out", torch.int32, optional=True), _ptr(scores_out, "scores_out", torch.float32, optional=True),
         _ptr(ws, "ws"), ws.numel() * ws.element_size(), _stream(stream))
@@ -214,7 +220,7 @@ def a2ats_decode_step_append(shape: a2ats_shape, params, n_ctx: int, q, k_cache,
     rc = load().a2ats_decode_step_append(
         ctypes.byref(shape), ctypes.byref(p), int(n_ctx), _ptr(q, "q", torch.bfloat16),
         _ptr(k_cache, "k_cache", torch.bfloat16), _ptr(v_cache, "v_cache", torch.bfloat16),
-        _ptr(codes, "codes", torch.uint16), _ptr(codebook, "codebook", torch.bfloat16),
+        _ptr(codes, "codes", _code_dtype(shape)), _ptr(codebook, "codebook", torch.bfloat16),
         _ptr(hist, "hist", torch.int32, optional=True), _ptr(chat, "chat", torch.bfloat16),
         _ptr(nrm, "nrm", torch.float32), _ptr(out, "out", torch.float32, host_ok="pinned"),
         _ptr(sel_out, "sel_out", torch.int32, optional=True), _ptr(scores_out, "scores_out", torch.float32, optional=True),
@@ -241,7 +247,7 @@ def a2ats_select_topk(shape: a2ats_shape, params, n_ctx: int, q, codes, codebook
     p = params.c() if isinstance(params, Params) else params
     rc = load().a2ats_select_topk(
         ctypes.byref(shape), ctypes.byref(p), int(n_ctx), _ptr(q, "q", torch.bfloat16),
-        _ptr(codes, "codes", torch.uint16), _ptr(codebook, "codebook", torch.bfloat16),
+        _ptr(codes, "codes", _code_dtype(shape)), _ptr(codebook, "codebook", torch.bfloat16),
         _ptr(hist, "hist", torch.int32, optional=True), _ptr(sel_out, "sel_out", torch.int32),
         _ptr(ws, "ws"), ws.numel() * ws.element_size(), _stream(stream))
     _check("a2ats_select_topk", rc)
@@ -340,7 +346,7 @@ def a2ats_shard_state_build(shape, params, world, rank, bounds, n_tokens, codes,
     import torch
     p = params.c() if isinstance(params, Params) else params
     rc = load().a2ats_shard_state_build(ctypes.byref(shape), ctypes.byref(p), int(world), int(rank), _bounds(bounds),
-                                        int(n_tokens), _ptr(codes, "codes", torch.uint16), _ptr(state, "state"),
+                                        int(n_tokens), _ptr(codes, "codes", _code_dtype(shape)), _ptr(state, "state"),
                                         _ptr(ws, "ws"), ws.numel() * ws.element_size(), comm, _stream(stream))
     _check("a2ats_shard_state_build", rc)
 
@@ -352,7 +358,7 @@ def a2ats_decode_step_sharded(shape, params, n_ctx, world, rank, bounds, q, k_ca
     rc = load().a2ats_decode_step_sharded(
         ctypes.byref(shape), ctypes.byref(p), int(n_ctx), int(world), int(rank), _bounds(bounds),
         _ptr(q, "q", torch.bfloat16), _ptr(k_cache, "k_cache", torch.bfloat16), _ptr(v_cache, "v_cache", torch.bfloat16),
-        _ptr(codes, "codes", torch.uint16), _ptr(codebook, "codebook", torch.bfloat16), _ptr(chat, "chat", torch.bfloat16),
+        _ptr(codes, "codes", _code_dtype(shape)), _ptr(codebook, "codebook", torch.bfloat16), _ptr(chat, "chat", torch.bfloat16),
         _ptr(nrm, "nrm", torch.float32), _ptr(state, "state"), _ptr(out, "out", torch.float32, host_ok="pinned"),
         _ptr(sel_out, "sel_out", torch.int32, optional=True), _ptr(ws, "ws"), ws.numel() * ws.element_size(), comm,
         _stream(stream))
@@ -366,7 +372,7 @@ def a2ats_shard_step_partial(shape, params, n_ctx, world, rank, bounds, q, k_cac
     rc = load().a2ats_shard_step_partial(
         ctypes.byref(shape), ctypes.byref(p), int(n_ctx), int(world), int(rank), _bounds(bounds),
         _ptr(q, "q", torch.bfloat16), _ptr(k_cache, "k_cache", torch.bfloat16), _ptr(v_cache, "v_cache", torch.bfloat16),
-        _ptr(codes, "codes", torch.uint16), _ptr(codebook, "codebook", torch.bfloat16), _ptr(chat, "chat", torch.bfloat16),
+        _ptr(codes, "codes", _code_dtype(shape)), _ptr(codebook, "codebook", torch.bfloat16), _ptr(chat, "chat", torch.bfloat16),
         _ptr(nrm, "nrm", torch.float32), _ptr(state, "state"), _ptr(msg, "msg"),
         _ptr(sel_out, "sel_out", torch.int32, optional=True), _ptr(ws, "ws"), ws.numel() * ws.element_size(),
         _stream(stream))
@@ -453,7 +459,7 @@ def a2ats_postings_bytes(shape) -> int:
 def a2ats_postings_build(shape, codes, n_tokens: int, postings, stream=None):
     import torch
     _check("a2ats_postings_build", load().a2ats_postings_build(
-        ctypes.byref(shape), _ptr(codes, "codes", torch.uint16), int(n_tokens), _ptr(postings, "postings"),
+        ctypes.byref(shape), _ptr(codes, "codes", _code_dtype(shape)), int(n_tokens), _ptr(postings, "postings"),
         _stream(stream)))
 
 
@@ -462,7 +468,7 @@ def a2ats_select_topk_postings(shape, params, n_ctx, q, codes, codebook, hist, p
     import torch
     p = params.c() if isinstance(params, Params) else params
     rc = load().a2ats_select_topk_postings(
-        ctypes.byref(shape), ctypes.byref(p), int(n_ctx), _ptr(q, "q", torch.bfloat16), _ptr(codes, "codes", torch.uint16),
+        ctypes.byref(shape), ctypes.byref(p), int(n_ctx), _ptr(q, "q", torch.bfloat16), _ptr(codes, "codes", _code_dtype(shape)),
         _ptr(codebook, "codebook", torch.bfloat16), _ptr(hist, "hist", torch.int32), _ptr(postings, "postings"),
         int(n_post), _ptr(sel_out, "sel_out", torch.int32), _ptr(ws, "ws"), ws.numel() * ws.element_size(),
         _stream(stream))
@@ -476,7 +482,7 @@ def a2ats_decode_step_postings(shape, params, n_ctx, q, k_cache, v_cache, codes,
     rc = load().a2ats_decode_step_postings(
         ctypes.byref(shape), ctypes.byref(p), int(n_ctx), _ptr(q, "q", torch.bfloat16),
         _ptr(k_cache, "k_cache", torch.bfloat16), _ptr(v_cache, "v_cache", torch.bfloat16),
-        _ptr(codes, "codes", torch.uint16), _ptr(codebook, "codebook", torch.bfloat16), _ptr(hist, "hist", torch.int32),
+        _ptr(codes, "codes", _code_dtype(shape)), _ptr(codebook, "codebook", torch.bfloat16), _ptr(hist, "hist", torch.int32),
         _ptr(postings, "postings"), int(n_post), _ptr(out, "out", torch.float32, host_ok="pinned"),
         _ptr(sel_out, "sel_out", torch.int32, optional=True), _ptr(ws, "ws"), ws.numel() * ws.element_size(),
         _stream(stream))
@@ -490,7 +496,7 @@ def a2ats_decode_step_append_postings(shape, params, n_ctx, q, k_cache, v_cache,
     rc = load().a2ats_decode_step_append_postings(
         ctypes.byref(shape), ctypes.byref(p), int(n_ctx), _ptr(q, "q", torch.bfloat16),
         _ptr(k_cache, "k_cache", torch.bfloat16), _ptr(v_cache, "v_cache", torch.bfloat16),
-        _ptr(codes, "codes", torch.uint16), _ptr(codebook, "codebook", torch.bfloat16), _ptr(hist, "hist", torch.int32),
+        _ptr(codes, "codes", _code_dtype(shape)), _ptr(codebook, "codebook", torch.bfloat16), _ptr(hist, "hist", torch.int32),
         _ptr(chat, "chat", torch.bfloat16), _ptr(nrm, "nrm", torch.float32), _ptr(postings, "postings"),
         int(n_post), _ptr(out, "out", torch.float32, host_ok="pinned"),
         _ptr(sel_out, "sel_out", torch.int32, optional=True), _ptr(ws, "ws"), ws.numel() * ws.element_size(),

@@ -93,6 +93,8 @@ int check_shape(const a2ats_shape* s) {
   if (s->d % 2) return A2ATS_EINVAL;
   if (s->Hq % s->Hkv) return A2ATS_EINVAL;
   if (s->n_max % 8) return A2ATS_EINVAL;
+  if (s->code_bytes < 0 || s->code_bytes > 2) return A2ATS_EINVAL;
+  if (s->code_bytes == 1 && s->L > 256) return A2ATS_EUNSUPPORTED;
   if (s->d != kD) return A2ATS_EUNSUPPORTED;
   const int G = s->Hq / s->Hkv;
   if (G != 1 && G != 2 && G != 4 && G != 8) return A2ATS_EUNSUPPORTED;
@@ -481,7 +483,8 @@ int a2ats_build_codes(const a2ats_shape* shape, const void* keys, int32_t t_begi
   a.nrm = nrm;
   a.slot = reinterpret_cast<unsigned long long*>(base + L.slot);
   a.counter = reinterpret_cast<unsigned int*>(base + L.ctr);
-  a.codes = codes;
+  a.codes = shape->code_bytes == 1 ? nullptr : codes;
+  a.codes8 = shape->code_bytes == 1 ? reinterpret_cast<uint8_t*>(codes) : nullptr;
   a.hist = hist;
   a.B = shape->B;
   a.Hkv = shape->Hkv;
@@ -666,7 +669,9 @@ int decode_impl_one(const a2ats_shape* shape, const a2ats_params* params, int32_
   // hist given: the warp-specialized persistent select (forward / backward half per pair);
   // otherwise threshold + chunked scan (the counts need a pass over the codes)
   // posting lists given: one CTA per pair reads only the hit codes' lists (f3)
-  const bool post_select = postings != nullptr && d.keff > 0;
+  // (uint8 codes: the posting-list kernel is the only reader, also for the append's histogram)
+  const bool post_select = postings != nullptr && (d.keff > 0 || shape->code_bytes == 1);
+  if (shape->code_bytes == 1 && (postings == nullptr || scores_out)) return A2ATS_EUNSUPPORTED;
   const bool pipe_select = !post_select && long_select && hist != nullptr && select_pipe_ok(shape->L) &&
                            shape->n_max % 64 == 0;
   const bool split_select = !post_select && long_select && !pipe_select;
@@ -685,7 +690,8 @@ int decode_impl_one(const a2ats_shape* shape, const a2ats_params* params, int32_
     e.nrm = nrm;
     e.slot = reinterpret_cast<unsigned long long*>(base + Lw.eslot);
     e.counter = reinterpret_cast<unsigned int*>(base + Lw.ectr);
-    e.codes = codes;
+    e.codes = shape->code_bytes == 1 ? nullptr : codes;
+    e.codes8 = shape->code_bytes == 1 ? reinterpret_cast<uint8_t*>(codes) : nullptr;
     e.hist = nullptr;  // the select kernel adds it
     e.B = shape->B;
     e.Hkv = shape->Hkv;
@@ -725,6 +731,7 @@ int decode_impl_one(const a2ats_shape* shape, const a2ats_params* params, int32_
     sa.append = append ? 1 : 0;
     sa.append_hist = append ? 1 : 0;
     sa.codes = codes;
+    sa.codes8 = shape->code_bytes == 1 ? reinterpret_cast<const uint8_t*>(codes) : nullptr;
     sa.sel = sel;
     sa.pinfo = reinterpret_cast<uint32_t*>(base + Lw.pinfo);
     sa.tblg = reinterpret_cast<uint32_t*>(base + Lw.tblg);
@@ -867,7 +874,8 @@ int a2ats_postings_build(const a2ats_shape* shape, const uint16_t* codes, int32_
   if (!codes || !postings || n_tokens < 0 || n_tokens > shape->n_max || !aligned16(postings)) return A2ATS_EINVAL;
   const PostingsLayout pl = postings_layout(shape);
   uint8_t* b = static_cast<uint8_t*>(postings);
-  return cuda_status(launch_postings_build(codes, shape->B * shape->Hkv, shape->n_max, shape->L, n_tokens,
+  return cuda_status(launch_postings_build(codes, shape->code_bytes == 1, shape->B * shape->Hkv, shape->n_max,
+                                           shape->L, n_tokens,
                                            reinterpret_cast<int32_t*>(b + pl.off),
                                            reinterpret_cast<int32_t*>(b + pl.tok), static_cast<cudaStream_t>(stream)));
 }
@@ -1150,6 +1158,7 @@ int a2ats_shard_state_build(const a2ats_shape* shape, const a2ats_params* params
   if (!rc) rc = check_params(params);
   if (!rc) rc = check_bounds(bounds, world, rank, shape);
   if (rc) return rc;
+  if (shape->code_bytes == 1) return A2ATS_EUNSUPPORTED;
   if (!codes || !state || n_tokens < 0 || n_tokens > bounds[world]) return A2ATS_EINVAL;
   if (comm && (comm->world != world || comm->rank != rank)) return A2ATS_EINVAL;
   const ShardWs W = shard_ws_layout(shape, params, world);
@@ -1200,7 +1209,7 @@ int shard_common(const a2ats_shape* shape, const a2ats_params* params, int32_t n
   if (rc) return rc;
   if (n_ctx <= 0 || n_ctx > bounds[world]) return A2ATS_EINVAL;
   if (owner_of_host(bounds, world, n_ctx - 1) < 0) return A2ATS_EINVAL;
-  if (params->kv_location != A2ATS_KV_DEVICE) return A2ATS_EUNSUPPORTED;
+  if (params->kv_location != A2ATS_KV_DEVICE || shape->code_bytes == 1) return A2ATS_EUNSUPPORTED;
   if (shape->n_max % 64 || !select_pipe_ok(shape->L) || shape->B > encode_cw_max()) return A2ATS_EUNSUPPORTED;
   return A2ATS_OK;
 }

@@ -22,7 +22,8 @@ __device__ __forceinline__ void finalize_code(const EncArgs& a, int h, int v, un
   const int code = (int)(packed & 0xffffffffull);
   const int b = v / a.T, t = a.t_begin + (v - b * a.T);
   const size_t pair = (size_t)b * a.Hkv + h;
-  a.codes[pair * a.n_max + t] = (uint16_t)code;
+  if (a.codes8) a.codes8[pair * a.n_max + t] = (uint8_t)code;
+  else a.codes[pair * a.n_max + t] = (uint16_t)code;
   if (a.hist) atomicAdd(a.hist + pair * a.L + code, 1);
 }
 

@@ -174,6 +174,7 @@ struct SelArgs {
   int append;                   // 1: token n_ctx-1 is encoded in this step: not in hist yet, code unread
   int append_hist;              // 1: select adds it to hist after taking the counts
   const uint16_t* codes;        // [P, n_max] local code array (local index = global - shard_begin)
+  const uint8_t* codes8;        // uint8 code array (code_bytes 1: posting-list select only) instead of codes
   int32_t* sel;                 // [P, sel_stride] selected global token indices, ascending
   int L, W, n_max, n_ctx, c0, c1, n_s, w0, keff, sel_stride, B;
   // sequence sharding (single GPU: shard_begin = 0, shard_len = n_max)
@@ -242,6 +243,7 @@ struct EncArgs {
   unsigned long long* slot;  // ws [Hkv, vcap]         ~pack(dist, code), 0 = empty
   unsigned int* counter;     // ws [Hkv, vcap / 64]
   uint16_t* codes;           // [B, Hkv, n_max]
+  uint8_t* codes8;           // [B, Hkv, n_max] uint8 codes (code_bytes 1) instead of codes
   int32_t* hist;             // [B, Hkv, L] or nullptr
   int B, Hkv, L, n_max, t_begin, T, nvec, lsplit, tiles_per_split;
 };
@@ -295,7 +297,7 @@ bool select_postings_ok(int L, int n_cand);
 // list-bounds row of a pair in the posting index: L + 1 int32, padded to 16 B
 inline __host__ __device__ int postings_off_stride(int L) { return (L + 1 + 3) & ~3; }
 inline int postings_bits_stride(int n_max) { return 2 * (((n_max + 31) / 32 + 3) & ~3); }
-cudaError_t launch_postings_build(const uint16_t* codes, int P, int n_max, int L, int n_tok, int32_t* post_off,
+cudaError_t launch_postings_build(const uint16_t* codes, bool codes8, int P, int n_max, int L, int n_tok, int32_t* post_off,
                                   int32_t* post_tok, cudaStream_t st);
 bool select_pipe_ok(int L);
 cudaError_t launch_attention(const AttnArgs& a, int P, int GT, cudaStream_t st);

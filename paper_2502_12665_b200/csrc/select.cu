@@ -549,7 +549,8 @@ __device__ uint32_t scan_emit(const SelArgs& a, SelShared& S, const uint32_t* tb
 
 // append: the step's new token n_ctx - 1 (encoded by the prep kernel) joins the histogram,
 // after this pair's counts were taken (end of the kernel, off the critical path)
-__device__ __forceinline__ void append_hist(const SelArgs& a, int pair, const uint16_t* cp_local) {
+template <typename CT>
+__device__ __forceinline__ void append_hist(const SelArgs& a, int pair, const CT* cp_local) {
   const int lo = a.shard_begin, t = a.n_ctx - 1;
   if (a.append_hist && a.hist && threadIdx.x == 0 && t >= lo && t < lo + a.shard_len)
     a.hist[(size_t)pair * a.L + cp_local[t - lo]] += 1;
@@ -1591,6 +1592,7 @@ __device__ __forceinline__ void q_scan(const int (&v)[NV], int (&ex)[NV], int (&
   }
 }
 
+template <typename CT>  // code type: uint16_t, or uint8_t (code_bytes 1)
 __global__ __launch_bounds__(kQT, A2ATS_QT_MINB) void select_postings_kernel(SelArgs a) {
   A2ATS_TL(g_sel_tl, 0);
   extern __shared__ __align__(16) uint32_t sm[];
@@ -1609,7 +1611,9 @@ __global__ __launch_bounds__(kQT, A2ATS_QT_MINB) void select_postings_kernel(Sel
   int* orow = scnt + kQSurv;                                // the pair's list bounds (16-B aligned)
   const int R = L4 + 2 * kQSurv;                            // words dead after the level (cnt + survivors)
   const int ncand = max(0, a.c1 - a.c0), nwords = (ncand + 31) >> 5;
-  const uint16_t* cp = a.codes + (size_t)pair * a.n_max;
+  const CT* cp = reinterpret_cast<const CT*>(sizeof(CT) == 1 ? static_cast<const void*>(a.codes8)
+                                                              : static_cast<const void*>(a.codes)) +
+                 (size_t)pair * a.n_max;
   const int32_t* ptok = a.post_tok + (size_t)pair * a.n_max;
   int32_t* selp = a.sel + (size_t)pair * a.sel_stride;
   const uint32_t cap = (uint32_t)a.keff;
@@ -1674,6 +1678,7 @@ __global__ __launch_bounds__(kQT, A2ATS_QT_MINB) void select_postings_kernel(Sel
   A2ATS_TL(g_sel_tl, 2);
   if (a.wlog) store_window_logits<kQT>(a, pair, wacc);
   append_hist(a, pair, cp);
+  if (a.keff <= 0) return;  // (uint8 codes: launched for the append's histogram alone)
   uint32_t k[16], kstar, m;
   level_regs<kQT, 16>(a, S, pair, c, k, skey, scnt, kQSurv, kstar, m);  // (ends synced: cnt dead)
   A2ATS_TL(g_sel_tl, 3);
@@ -2061,14 +2066,15 @@ __global__ __launch_bounds__(kQT, A2ATS_QT_MINB) void select_postings_kernel(Sel
 // (code-major exclusive prefix: post_off, then the warps in order) -> each warp places its
 // tokens in order, 32 per step, ranks among equal codes of a step from match_any.
 constexpr int kBW = 8;
-__global__ __launch_bounds__(kBW * 32) void postings_build_kernel(const uint16_t* __restrict__ codes, int n_max, int L,
+template <typename CT>
+__global__ __launch_bounds__(kBW * 32) void postings_build_kernel(const CT* __restrict__ codes, int n_max, int L,
                                                                   int n_tok, int32_t* __restrict__ post_off,
                                                                   int32_t* __restrict__ post_tok) {
   extern __shared__ __align__(16) int pcnt[];  // [kBW][L]: counts, then cursors
   __shared__ int s_w[kBW];
   constexpr int NT = kBW * 32;
   const int pair = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint16_t* cp = codes + (size_t)pair * n_max;
+  const CT* cp = codes + (size_t)pair * n_max;
   for (int i = tid; i < kBW * L; i += NT) pcnt[i] = 0;
   __syncthreads();
   const int per = (n_tok + kBW - 1) / kBW, t0 = min(n_tok, warp * per), t1 = min(n_tok, t0 + per);
@@ -2263,20 +2269,31 @@ size_t postings_smem_bytes(int L, bool window) {
 }
 bool select_postings_ok(int L, int) { return L <= 4096; }
 
-cudaError_t launch_select_postings(const SelArgs& a, cudaStream_t st) {
+template <typename CT>
+cudaError_t launch_select_postings_t(const SelArgs& a, cudaStream_t st) {
   const int smem = (int)postings_smem_bytes(a.L, a.wlog != nullptr);
-  cudaError_t e = ensure_smem(select_postings_kernel, smem);
+  cudaError_t e = ensure_smem(select_postings_kernel<CT>, smem);
   if (e != cudaSuccess) return e;
-  return launch_pdl(select_postings_kernel, dim3(a.P), dim3(kQT), smem, st, a);
+  return launch_pdl(select_postings_kernel<CT>, dim3(a.P), dim3(kQT), smem, st, a);
+}
+cudaError_t launch_select_postings(const SelArgs& a, cudaStream_t st) {
+  return a.codes8 ? launch_select_postings_t<uint8_t>(a, st) : launch_select_postings_t<uint16_t>(a, st);
 }
 
-cudaError_t launch_postings_build(const uint16_t* codes, int P, int n_max, int L, int n_tok, int32_t* post_off,
-                                  int32_t* post_tok, cudaStream_t st) {
+template <typename CT>
+cudaError_t launch_postings_build_t(const CT* codes, int P, int n_max, int L, int n_tok, int32_t* post_off,
+                                    int32_t* post_tok, cudaStream_t st) {
   const int smem = kBW * L * 4;
-  cudaError_t e = ensure_smem(postings_build_kernel, smem);
+  cudaError_t e = ensure_smem(postings_build_kernel<CT>, smem);
   if (e != cudaSuccess) return e;
-  return launch_pdl(postings_build_kernel, dim3(P), dim3(kBW * 32), smem, st, codes, n_max, L, n_tok, post_off,
+  return launch_pdl(postings_build_kernel<CT>, dim3(P), dim3(kBW * 32), smem, st, codes, n_max, L, n_tok, post_off,
                     post_tok);
+}
+cudaError_t launch_postings_build(const uint16_t* codes, bool codes8, int P, int n_max, int L, int n_tok,
+                                  int32_t* post_off, int32_t* post_tok, cudaStream_t st) {
+  return codes8 ? launch_postings_build_t(reinterpret_cast<const uint8_t*>(codes), P, n_max, L, n_tok, post_off,
+                                          post_tok, st)
+                : launch_postings_build_t(codes, P, n_max, L, n_tok, post_off, post_tok, st);
 }
 
 cudaError_t launch_select_shard(const SelArgs& a, const CUtensorMap& tmK, int nblk, cudaStream_t st) {

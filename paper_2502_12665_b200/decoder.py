@@ -11,9 +11,9 @@ from . import binding as _b
 
 class Decoder:
     def __init__(self, B, Hq, Hkv, L, n_max, codebook, H=None, params: _b.Params | None = None, device="cuda",
-                 stream=None):
+                 stream=None, code_bytes=2):
         self.device = torch.device(device)
-        self.shape = _b.make_shape(B, Hq, Hkv, 128, L, n_max)
+        self.shape = _b.make_shape(B, Hq, Hkv, 128, L, n_max, code_bytes)
         self.params = params or _b.Params()
         self.stream = stream
         self.codebook = codebook.contiguous()
@@ -25,7 +25,8 @@ class Decoder:
                                   device=self.device)
         self.ws_dec = torch.zeros(_b.a2ats_decode_workspace_bytes(self.shape, self.params), dtype=torch.uint8,
                                   device=self.device)
-        self.codes = torch.zeros((B, Hkv, n_max), dtype=torch.uint16, device=self.device)
+        self.codes = torch.zeros((B, Hkv, n_max), dtype=torch.uint8 if code_bytes == 1 else torch.uint16,
+                                 device=self.device)
         self.hist = torch.zeros((B, Hkv, L), dtype=torch.int32, device=self.device)
 
     def set_topk(self, k: int):
