@@ -74,7 +74,10 @@ for it in range(0 if args.select_only else args.iters):
     dec.hist.copy_(hist0)  # covers [0, N-1): the step appends token N-1
     e0.record()
     A.a2ats_set_stage_events(evs)
-    dec.step_append(inp["q"], inp["k_cache"], inp["v_cache"], cfg.N, out=out, use_hist=not args.no_hist)
+    if args.postings:
+        dec.step_append_postings(inp["q"], inp["k_cache"], inp["v_cache"], cfg.N, out=out)
+    else:
+        dec.step_append(inp["q"], inp["k_cache"], inp["v_cache"], cfg.N, out=out, use_hist=not args.no_hist)
     A.a2ats_set_stage_events(None)
     e1.record()
     torch.cuda.synchronize()

@@ -22,7 +22,8 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 STAGE = [("attn", "attention"), ("select_kernel", "select"), ("select_thresh", "select"), ("select_shard", "select"),
-         ("select_scan", "select"), ("prep_kernel", "prep"), ("lut_fma", "prep"), ("qprep", "prep"),
+         ("select_scan", "select"), ("select_postings", "select"), ("prep_kernel", "prep"), ("lut_fma", "prep"),
+         ("lut_persist", "prep"), ("qprep", "prep"), ("postings_build", "index"),
          ("encode_cw", "encode"), ("encode_kernel", "encode"), ("keyh", "encode_keyh")]
 # prefill (encode_bulk_kernel, prepare_kernel) runs before the timed steps: not a path stage
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
@@ -105,13 +106,15 @@ def launches(path_csv, tag):
     for r in rows[hi + 1:]:
         n = short(r[ki])
         agg.setdefault(n, []).append(float(r[vi].replace(",", "")))
-    tot = sum(sum(v) for k, v in agg.items() if stage_of(k))
+    # the posting-index rebuild (stage "index") runs once per rebuild period, not per step: no share
+    in_step = lambda k: stage_of(k) and stage_of(k) != "index"
+    tot = sum(sum(v) for k, v in agg.items() if in_step(k))
     out = os.path.join(ROOT, "profiles", f"ncu_{tag}_launches.csv")
     with open(out, "w", newline="") as f:
         w = csv.writer(f)
         w.writerow(["kernel", "launches", "mean_ns", "share_of_path_time"])
         for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
-            w.writerow([k, len(v), sum(v) / len(v), (sum(v) / tot) if stage_of(k) and tot else ""])
+            w.writerow([k, len(v), sum(v) / len(v), (sum(v) / tot) if in_step(k) and tot else ""])
     print(out)
 
 
