@@ -109,7 +109,12 @@ typedef struct a2ats_params {
   int32_t group_reduce;  /* A2ATS_GROUP_MAX (default) | _SUM | _PER_HEAD               */
   int32_t kv_location;   /* A2ATS_KV_DEVICE (default) | A2ATS_KV_HOST_MAPPED          */
   int32_t lut_engine;    /* A2ATS_LUT_AUTO (default) | A2ATS_LUT_TENSOR | A2ATS_LUT_FMA */
-  int32_t reserved;      /* 0                                                          */
+  int32_t hist_lag;      /* deferred a0 (a new token's code is first read when
+                            it leaves the window): the newest hist_lag tokens are not
+                            encoded yet -- their codes are not read and hist covers
+                            [0, N - hist_lag); 0 <= hist_lag <= min(window, N).  The
+                            selection and output equal hist_lag = 0 exactly.  0 for the
+                            append entry points, scores_out and the sharded step     */
 } a2ats_params;
 
 /* Fills the paper's configuration: w = 64, b = 2048, n_sink = 4, topk = 0,

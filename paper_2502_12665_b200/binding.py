@@ -48,7 +48,7 @@ class a2ats_params(ctypes.Structure):
     _fields_ = [("window", ctypes.c_int32), ("bridge", ctypes.c_int32), ("n_sink", ctypes.c_int32),
                 ("topk", ctypes.c_int32), ("rope_theta", ctypes.c_double),
                 ("inv_freq", ctypes.POINTER(ctypes.c_double)), ("group_reduce", ctypes.c_int32),
-                ("kv_location", ctypes.c_int32), ("lut_engine", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("kv_location", ctypes.c_int32), ("lut_engine", ctypes.c_int32), ("hist_lag", ctypes.c_int32)]
 
 
 _VP = ctypes.c_void_p
@@ -125,6 +125,7 @@ class Params:
     group_reduce: int = A2ATS_GROUP_MAX
     kv_location: int = A2ATS_KV_DEVICE
     lut_engine: int = A2ATS_LUT_AUTO
+    hist_lag: int = 0
 
     def c(self) -> a2ats_params:
         p = a2ats_params()
@@ -137,6 +138,7 @@ class Params:
             self._freq_buf = (ctypes.c_double * len(self.inv_freq))(*self.inv_freq)
             p.inv_freq = ctypes.cast(self._freq_buf, ctypes.POINTER(ctypes.c_double))
         p.group_reduce, p.kv_location, p.lut_engine = self.group_reduce, self.kv_location, self.lut_engine
+        p.hist_lag = self.hist_lag
         return p
 
 

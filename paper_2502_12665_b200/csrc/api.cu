@@ -111,6 +111,7 @@ int check_params(const a2ats_params* p) {
     return A2ATS_EINVAL;
   if (p->kv_location != A2ATS_KV_DEVICE && p->kv_location != A2ATS_KV_HOST_MAPPED) return A2ATS_EINVAL;
   if (p->lut_engine < A2ATS_LUT_AUTO || p->lut_engine > A2ATS_LUT_FMA) return A2ATS_EINVAL;
+  if (p->hist_lag < 0 || p->hist_lag > p->window) return A2ATS_EINVAL;
   return A2ATS_OK;
 }
 
@@ -639,6 +640,8 @@ int decode_impl_one(const a2ats_shape* shape, const a2ats_params* params, int32_
 
   Derived d;
   derive(shape, params, n_ctx, &d);
+  // deferred a0: the newest hist_lag tokens are in the window (never candidates); not with append
+  if (params->hist_lag > d.n_w || (params->hist_lag && (append || scores_out))) return A2ATS_EINVAL;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   uint8_t* base = static_cast<uint8_t*>(ws);
   float2* cs = reinterpret_cast<float2*>(base + Lw.cs);
@@ -730,6 +733,7 @@ int decode_impl_one(const a2ats_shape* shape, const a2ats_params* params, int32_
     sa.hist = hist;
     sa.append = append ? 1 : 0;
     sa.append_hist = append ? 1 : 0;
+    sa.hist_end = n_ctx - (append ? 1 : 0) - params->hist_lag;  // hist covers [0, hist_end)
     sa.codes = codes;
     sa.codes8 = shape->code_bytes == 1 ? reinterpret_cast<const uint8_t*>(codes) : nullptr;
     sa.sel = sel;
@@ -1209,7 +1213,7 @@ int shard_common(const a2ats_shape* shape, const a2ats_params* params, int32_t n
   if (rc) return rc;
   if (n_ctx <= 0 || n_ctx > bounds[world]) return A2ATS_EINVAL;
   if (owner_of_host(bounds, world, n_ctx - 1) < 0) return A2ATS_EINVAL;
-  if (params->kv_location != A2ATS_KV_DEVICE || shape->code_bytes == 1) return A2ATS_EUNSUPPORTED;
+  if (params->kv_location != A2ATS_KV_DEVICE || shape->code_bytes == 1 || params->hist_lag) return A2ATS_EUNSUPPORTED;
   if (shape->n_max % 64 || !select_pipe_ok(shape->L) || shape->B > encode_cw_max()) return A2ATS_EUNSUPPORTED;
   return A2ATS_OK;
 }
@@ -1304,6 +1308,7 @@ int shard_partial(const a2ats_shape* shape, const a2ats_params* params, int32_t 
   sa.W = d.W;
   sa.n_max = shape->n_max;
   sa.n_ctx = n_ctx;
+  sa.hist_end = n_ctx;  // (the shard kernels count from the replicated state, not load_cnt)
   sa.n_s = d.n_s;
   sa.w0 = d.w0;
   sa.keff = d.keff;  // global K_eff

@@ -173,6 +173,7 @@ struct SelArgs {
   int32_t* hist;                // [P, L] or nullptr (counts of the LOCAL tokens' codes)
   int append;                   // 1: token n_ctx-1 is encoded in this step: not in hist yet, code unread
   int append_hist;              // 1: select adds it to hist after taking the counts
+  int hist_end;                 // hist (and the codes read) cover tokens [0, hist_end); >= w0
   const uint16_t* codes;        // [P, n_max] local code array (local index = global - shard_begin)
   const uint8_t* codes8;        // uint8 code array (code_bytes 1: posting-list select only) instead of codes
   int32_t* sel;                 // [P, sel_stride] selected global token indices, ascending

@@ -96,8 +96,9 @@ __device__ void load_cnt(const SelArgs& a, int pair, int* cnt, const uint16_t* c
     }
     Grp::sync();
     // remove the local sinks [0, n_s) and window [w0, n_ctx): they are not candidates
-    // (append: hist does not hold token n_ctx - 1 yet, whose code the prep kernel computes)
-    const int nrem = a.n_s + (a.n_ctx - a.append - a.w0);
+    // (append: hist does not hold token n_ctx - 1 yet, whose code the prep kernel computes;
+    // deferred a0: nor the newest hist_lag tokens)
+    const int nrem = a.n_s + max(0, a.hist_end - a.w0);
     for (int i = tid; i < nrem; i += NT) {
       const int t = i < a.n_s ? i : a.w0 + (i - a.n_s);
       if (t >= lo && t < hi) atomicSub(&cnt[cp_local[t - lo]], 1);
@@ -1650,7 +1651,7 @@ __global__ __launch_bounds__(kQT, A2ATS_QT_MINB) void select_postings_kernel(Sel
       for (int l = tid; l < a.L; l += kQT) cnt[l] = __ldg(histp + l);
       for (int i = tid; i <= a.L; i += kQT) orow[i] = __ldg(a.post_off + post0 + i);
     }
-    const int nrem = a.n_s + (a.n_ctx - a.append - a.w0);  // (append: hist lacks token n_ctx - 1)
+    const int nrem = a.n_s + max(0, a.hist_end - a.w0);  // (hist covers [0, hist_end))
     int rc = -1;
     if (tid < nrem) rc = cp[tid < a.n_s ? tid : a.w0 + (tid - a.n_s)];
     if (list_ok && tid < nsk) s_sk[tid] = cp[tid];

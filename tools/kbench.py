@@ -25,6 +25,8 @@ ap.add_argument("--N", type=int, default=0)
 ap.add_argument("--select-only", action="store_true", help="a2ats_select_topk (a1..a4) only")
 ap.add_argument("--postings", action="store_true", help="posting-list selection engine (f3)")
 ap.add_argument("--post-lag", type=int, default=256, help="tokens behind the window start the index was built at")
+ap.add_argument("--no-append", action="store_true", help="step without a0 (codes / hist given for all tokens)")
+ap.add_argument("--encode-batch", type=int, default=0, help="also time a2ats_build_codes of this many tokens per pair")
 args = ap.parse_args()
 cfg = CONFIGS[args.config]
 if args.batch:
@@ -74,7 +76,10 @@ for it in range(0 if args.select_only else args.iters):
     dec.hist.copy_(hist0)  # covers [0, N-1): the step appends token N-1
     e0.record()
     A.a2ats_set_stage_events(evs)
-    if args.postings:
+    if args.postings and args.no_append:
+        dec.hist.copy_(hist)
+        dec.step_postings(inp["q"], inp["k_cache"], inp["v_cache"], cfg.N, out=out)
+    elif args.postings:
         dec.step_append_postings(inp["q"], inp["k_cache"], inp["v_cache"], cfg.N, out=out)
     else:
         dec.step_append(inp["q"], inp["k_cache"], inp["v_cache"], cfg.N, out=out, use_hist=not args.no_hist)
@@ -84,3 +89,13 @@ for it in range(0 if args.select_only else args.iters):
     names = ["prep", "select", "attn", "tail"]
     print("it", it, "step %.1f" % (e0.elapsed_time(e1) * 1e3), " ".join(
         "%s %.1f" % (n, evs[i].elapsed_time(evs[i + 1]) * 1e3) for i, n in enumerate(names)), "us")
+
+if args.encode_batch:
+    T = args.encode_batch
+    for it in range(4):
+        flush.fill_(it)
+        e0.record()
+        dec.encode(inp["k_cache"], cfg.N - T, cfg.N, update_hist=True, codes=scratch_codes)
+        e1.record()
+        torch.cuda.synchronize()
+        print("build_codes %d tokens/pair %.1f us" % (T, e0.elapsed_time(e1) * 1e3))
