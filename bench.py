@@ -205,12 +205,24 @@ def run_ours(args, rank: int, world: int):
     if engine == "auto":  # posting lists where the code scan needs its long-context kernels (C4)
         engine = "postings" if cfg.N - cfg.window > 2 * 32768 and cfg.L <= 4096 else "scan"
     post = postings_setup(args, cfg, dec, n0, flush) if engine == "postings" else None
+    # a0: fused into every step (a2ats_decode_step_append*), or deferred (params.hist_lag: the newest
+    # <= window tokens are not encoded yet; one a2ats_build_codes of `window` tokens every `window`
+    # steps, timed here and amortized into each step).  Deferred when every step of this run
+    # (timed, profiling, e2e) stays within one window of the encoded prefix.
+    deferred = args.a0 != "fused" and steps_total + args.steps + e2e_steps < cfg.window
+    a0 = a0_setup(cfg, dec, kc, n0, flush) if deferred else None
 
     def one_step(n, evs=None):
         if evs is not None:
             A.a2ats_set_stage_events(evs[1:])
         dec.params.topk = budget_k(n)
-        if post is not None:                        # a0 for token n-1 (+ hist) fused with a1..a6,
+        if a0 is not None:                          # a0 deferred: tokens [n0, n) not encoded yet
+            dec.params.hist_lag = n - n0
+            if post is not None:
+                dec.step_postings(q, kc, vc, n, out=out)
+            else:
+                dec.step(q, kc, vc, n, out=out)
+        elif post is not None:                      # a0 for token n-1 (+ hist) fused with a1..a6,
             dec.step_append_postings(q, kc, vc, n, out=out)   # selection over the posting lists
         else:
             dec.step_append(q, kc, vc, n, out=out)  # a0 for token n-1 (+ hist) fused with a1..a6
@@ -300,6 +312,8 @@ def run_ours(args, rank: int, world: int):
         tokens = tk.item()
     if post is not None:  # the index rebuild, every post["every"] steps, amortized into each step
         total_ms += args.steps * post["amortized_ms"]
+    if a0 is not None:    # the batched encode, every `window` steps, amortized into each step
+        total_ms += args.steps * a0["amortized_ms"]
     value = tokens / (total_ms / 1e3)
     n_last = ns[-1]
     del graphs
@@ -308,6 +322,8 @@ def run_ours(args, rank: int, world: int):
     # one CUDA graph replayed, L2 flushed before each replay outside the events
     sel = torch.empty((cfg.B, cfg.Hkv, max(budget_k(n_last), 1)), dtype=torch.int32, device=dev)
     dec.params.topk = budget_k(n_last)
+    if a0 is not None:
+        dec.params.hist_lag = n_last - n0
 
     def select():
         if post is not None:
@@ -336,8 +352,9 @@ def run_ours(args, rank: int, world: int):
     score_ms = statistics.mean(a.elapsed_time(b) for a, b in sc_ev)
     del g_sel
 
-    e2e = run_e2e(e2e_steps, dec, cfg, kc, vc, q, n_last, A, budget_k, use_graph, world, dev, post)
-    return dict(value=value, ms_per_step=total_ms / args.steps, score_ms=score_ms, score_n=n_last, post=post,
+    e2e = run_e2e(e2e_steps, dec, cfg, kc, vc, q, n_last, A, budget_k, use_graph, world, dev, post,
+                  None if a0 is None else (a0, n0))
+    return dict(value=value, ms_per_step=total_ms / args.steps, score_ms=score_ms, score_n=n_last, post=post, a0=a0,
                 stage_ms={k: statistics.mean(v) for k, v in stage_ms.items()},
                 prof_step_ms=statistics.mean(prof_step),
                 clocks=clk.summary(), e2e=e2e, n_last=ns[args.warmup + args.steps - 1], cfg=cfg, graph=use_graph)
@@ -449,7 +466,27 @@ def postings_setup(args, cfg, dec, n0, flush):
     return {"every": every, "n_post": n_post, "rebuild_ms": rebuild_ms, "amortized_ms": rebuild_ms / every}
 
 
-def run_e2e(steps, dec, cfg, kc, vc, q, n_start, A, budget_k, use_graph, world, dev, post=None):
+def a0_setup(cfg, dec, kc, n0, flush):
+    """Deferred a0 (params.hist_lag): the encode of the new keys runs batched, `window` tokens
+    per pair in one a2ats_build_codes call every `window` steps.  Timed here (L2 flushed, into
+    scratch codes) and amortized into each step."""
+    import torch
+    w = cfg.window
+    scratch = torch.zeros_like(dec.codes)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ms = []
+    for i in range(4):
+        flush.fill_(float(i))
+        ev[0].record()
+        dec.encode(kc, n0 - w, n0, update_hist=False, codes=scratch)
+        ev[1].record()
+        torch.cuda.synchronize()
+        ms.append(ev[0].elapsed_time(ev[1]))
+    enc_ms = statistics.median(ms[1:])
+    return {"every": w, "encode_ms": enc_ms, "amortized_ms": enc_ms / w}
+
+
+def run_e2e(steps, dec, cfg, kc, vc, q, n_start, A, budget_k, use_graph, world, dev, post=None, a0=None):
     """Same step through the public API with HOST buffers: every step moves its
     inputs (q, the new token's k and v rows) from pinned host memory into the
     device (a2ats_stage_rows: one kernel reading the mapped host buffers over
@@ -467,7 +504,13 @@ def run_e2e(steps, dec, cfg, kc, vc, q, n_start, A, budget_k, use_graph, world, 
         n = n_start + s + 1
         A.a2ats_stage_rows(dec.shape, n, q_host, k_host[s], v_host[s], q_dev, kc, vc)
         dec.params.topk = budget_k(n)
-        if post is not None:
+        if a0 is not None:  # a0 deferred (tokens [n_enc, n) not encoded yet)
+            dec.params.hist_lag = n - a0[1]
+            if post is not None:
+                dec.step_postings(q_dev, kc, vc, n, out=out_host)
+            else:
+                dec.step(q_dev, kc, vc, n, out=out_host)
+        elif post is not None:
             dec.step_append_postings(q_dev, kc, vc, n, out=out_host)
         else:
             dec.step_append(q_dev, kc, vc, n, out=out_host)
@@ -494,6 +537,8 @@ def run_e2e(steps, dec, cfg, kc, vc, q, n_start, A, budget_k, use_graph, world, 
     tot = ev0.elapsed_time(ev1)
     if post is not None:
         tot += steps * post["amortized_ms"]
+    if a0 is not None:
+        tot += steps * a0[0]["amortized_ms"]
     if world > 1:
         t = torch.tensor([tot], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -853,6 +898,8 @@ def main():
                     help="selection engine of the 1-GPU step: posting lists (f3), the code scan, or auto "
                          "(posting lists for contexts beyond two 32K-token code chunks)")
     ap.add_argument("--post-every", type=int, default=1024, help="posting-index rebuild period (steps)")
+    ap.add_argument("--a0", default="auto", choices=["auto", "fused", "deferred"],
+                    help="new-key encode: fused into every step, or deferred and batched every window steps")
     ap.add_argument("--sharded", action="store_true",
                     help="the sequence-sharded step also at N = 1 (always used at N > 1)")
     args = ap.parse_args()
@@ -931,7 +978,15 @@ def main():
     c0, c1 = min(cfg.n_sink, max(0, n_last - cfg.window)), max(0, n_last - cfg.window)
     long_select = c1 > c0 and (c1 - (c0 // 8) * 8 + 32767) // 32768 >= 2
     post = r.get("post")
-    launches_per_step = 3 + (1 if cfg.B * (cfg.Hq // cfg.Hkv) > 64 else 0) + (1 if long_select and not post else 0)
+    a0 = r.get("a0")
+    # qprep (B*G > 64) + the LUT (persistent kernel with qprep tiles, FMA kernel for B*G <= 8, else a
+    # role of the prep kernel) + the prep kernel (LUT role / fused a0 encode role / window role of
+    # one-chunk contexts) + select (threshold + scan for long contexts with the scan engine) + attention
+    bg = cfg.B * (cfg.Hq // cfg.Hkv)
+    lut_own = bg > 64 or bg <= 8
+    prep = (not lut_own) or (a0 is None) or not (long_select or post)
+    launches_per_step = ((1 if bg > 64 else 0) + (1 if lut_own else 0) + (1 if prep else 0)
+                         + (2 if long_select and not post else 1) + 1)
     line = {
         "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak",
@@ -941,10 +996,14 @@ def main():
                    "bridge": cfg.bridge, "n_sink": cfg.n_sink,
                    "parallelism": f"replicas x{world} (batch/head parallel, no collective)" if world > 1 else "1 GPU",
                    "l2": "flushed between steps (256 MB write, outside the timed events)" if not args.no_flush else "not flushed",
-                   "step": ("a2ats_decode_step_append_postings: a0 for the new token (+hist) fused with a1..a6, "
-                            "selection over posting lists rebuilt every %d steps (rebuild %.3f ms, amortized "
-                            "into ms_per_step)" % (post["every"], post["rebuild_ms"]) if post else
-                            "a2ats_decode_step_append: a0 for the new token (+hist) fused with a1..a6"),
+                   "step": (("a2ats_decode_step_postings" if post else "a2ats_decode_step") + " (a1..a6) with a0 "
+                            "deferred: the new keys encoded by one a2ats_build_codes of %d tokens every %d steps "
+                            "(%.3f ms, amortized into ms_per_step)" % (a0["every"], a0["every"], a0["encode_ms"])
+                            if a0 else
+                            ("a2ats_decode_step_append_postings" if post else "a2ats_decode_step_append")
+                            + ": a0 for the new token (+hist) fused with a1..a6")
+                           + ("; selection over posting lists rebuilt every %d steps (rebuild %.3f ms, amortized "
+                              "into ms_per_step)" % (post["every"], post["rebuild_ms"]) if post else ""),
                    "engine": "postings" if post else "scan",
                    "launch": "one CUDA graph per step (replay)" if r["graph"] else "eager launches",
                    "sparsity": (budget_k(r["n_last"]) + 68) / r["n_last"], "aux_mem": 2 / (cfg.d * 2)},
