@@ -239,24 +239,36 @@ __device__ __forceinline__ void lut_tile(const CUtensorMap& tmA, const PrepArgs&
 // w % 4, column half (w - 2) / 4), fold the G heads and store agg -- so the next unit's codeword
 // load and MMAs run under the current unit's epilogue, whose TMEM reads bound the kernel.
 constexpr int kLpWarps = 10;  // producer, MMA, 8 epilogue warps
-__host__ __device__ constexpr int lut_persist_smem(int NV) { return kTC * kD * 2 + NV * 2 * kD * 2 + 1024; }
+constexpr int kLpStages = 2;  // codeword-tile ring: the next unit's tile loads while this unit's MMAs run
+__host__ __device__ constexpr int lut_persist_smem(int NV) {
+  return kLpStages * kTC * kD * 2 + NV * 2 * kD * 2 + 1024;
+}
 
 template <int G>
 __global__ __launch_bounds__(kLpWarps * 32, 1) void lut_persist_kernel(const __grid_constant__ CUtensorMap tmA,
                                                                        const LutArgs a, int n_units, int ntx) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sA = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sB = sA + kTC * kD * 2;  // [32 chunks][NV vectors][16 B]
-  __shared__ __align__(8) uint64_t a_full, a_empty, b_full, b_empty, t_full[2], t_empty[2];
+  uint8_t* sB = sA + kLpStages * kTC * kD * 2;  // [32 chunks][NV vectors][16 B]
+  __shared__ __align__(8) uint64_t a_full[kLpStages], a_empty[kLpStages], b_full, b_empty, t_full[2], t_empty[2];
   __shared__ uint32_t tslot;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int NV = a.NV, ncols = (int)umma::tmem_cols_for(NV);
   const int u0 = (int)((long long)blockIdx.x * n_units / gridDim.x);
   const int u1 = (int)((long long)(blockIdx.x + 1) * n_units / gridDim.x);
   auto hy_of = [&](int u) { return u / ntx; };  // (h, y) block index = h * nvt + y
+  auto issue_a = [&](int u, int st) {           // codeword tile of unit u into ring stage st
+    const int h = hy_of(u) / a.nvt, x = u % ntx;
+    uint8_t* d = sA + st * (kTC * kD * 2);
+    umma::mbar_expect_tx(&a_full[st], kTC * kD * 2);
+    umma::tma_load_2d(d, &tmA, 0, h * a.L + x * kTC, &a_full[st]);
+    umma::tma_load_2d(d + kTC * 128, &tmA, 64, h * a.L + x * kTC, &a_full[st]);
+  };
   if (tid == 0) {
-    umma::mbar_init(&a_full, 1);
-    umma::mbar_init(&a_empty, 1);
+    for (int st = 0; st < kLpStages; ++st) {
+      umma::mbar_init(&a_full[st], 1);
+      umma::mbar_init(&a_empty[st], 1);
+    }
     umma::mbar_init(&b_full, 1);
     umma::mbar_init(&b_empty, 1);
     for (int j = 0; j < 2; ++j) {
@@ -264,12 +276,8 @@ __global__ __launch_bounds__(kLpWarps * 32, 1) void lut_persist_kernel(const __g
       umma::mbar_init(&t_empty[j], 8);
     }
     umma::mbar_fence_init();
-    if (u0 < u1) {  // the first codeword tile (a step input) before the dependency wait
-      const int h = hy_of(u0) / a.nvt, x = u0 % ntx;
-      umma::mbar_expect_tx(&a_full, kTC * kD * 2);
-      umma::tma_load_2d(sA, &tmA, 0, h * a.L + x * kTC, &a_full);
-      umma::tma_load_2d(sA + kTC * 128, &tmA, 64, h * a.L + x * kTC, &a_full);
-    }
+    // the first codeword tiles (step inputs) before the dependency wait
+    for (int st = 0; st < kLpStages && u0 + st < u1; ++st) issue_a(u0 + st, st);
   }
   A2ATS_TL(g_prep_tl, 0);
   if (warp == 1) umma::tmem_alloc_n(&tslot, 2 * ncols);
@@ -286,12 +294,10 @@ __global__ __launch_bounds__(kLpWarps * 32, 1) void lut_persist_kernel(const __g
     if (lane == 0) {  // producer
       int nb = 0, cur = -1;
       for (int u = u0, it = 0; u < u1; ++u, ++it) {
-        const int hy = hy_of(u), h = hy / a.nvt, x = u % ntx;
-        if (it > 0) {  // (unit 0's tile was issued before the wait)
-          umma::mbar_wait(&a_empty, (it - 1) & 1);  // the previous unit's MMAs are done with sA
-          umma::mbar_expect_tx(&a_full, kTC * kD * 2);
-          umma::tma_load_2d(sA, &tmA, 0, h * a.L + x * kTC, &a_full);
-          umma::tma_load_2d(sA + kTC * 128, &tmA, 64, h * a.L + x * kTC, &a_full);
+        const int hy = hy_of(u), st = it % kLpStages;
+        if (it >= kLpStages) {  // (the first kLpStages tiles were issued before the wait)
+          umma::mbar_wait(&a_empty[st], ((it - kLpStages) / kLpStages) & 1);  // unit it - S's MMAs done
+          issue_a(u, st);
         }
         if (hy != cur) {
           if (nb > 0) umma::mbar_wait(&b_empty, (nb - 1) & 1);
@@ -305,12 +311,13 @@ __global__ __launch_bounds__(kLpWarps * 32, 1) void lut_persist_kernel(const __g
   } else if (warp == 1) {
     if (lane == 0) {  // MMA issuer
       const uint32_t idesc = umma::idesc_bf16(kTC, NV);
-      const uint32_t aBase = smem_u32(sA), bBase = smem_u32(sB);
+      const uint32_t bBase = smem_u32(sB);
       int nb = 0, cur = -1;
       for (int u = u0, it = 0; u < u1; ++u, ++it) {
-        const int j = it & 1, hy = hy_of(u);
+        const int j = it & 1, hy = hy_of(u), st = it % kLpStages;
+        const uint32_t aBase = smem_u32(sA + st * (kTC * kD * 2));
         if (it >= 2) umma::mbar_wait(&t_empty[j], ((it - 2) >> 1) & 1);  // accumulator j drained
-        umma::mbar_wait(&a_full, it & 1);
+        umma::mbar_wait(&a_full[st], (it / kLpStages) & 1);
         if (it == 0) A2ATS_TLX(g_prep_tl, 6);
         if (hy != cur) {
           umma::mbar_wait(&b_full, nb & 1);
@@ -327,7 +334,7 @@ __global__ __launch_bounds__(kLpWarps * 32, 1) void lut_persist_kernel(const __g
           const uint64_t bd = umma::sdesc(bBase + (2 * s) * (NV * 16), NV * 16, 128);
           umma::mma_bf16(td, ad, bd, idesc, s > 0 ? 1u : 0u);
         }
-        umma::commit(&a_empty);                                 // sA reusable once these MMAs complete
+        umma::commit(&a_empty[st]);                             // stage st reusable once these MMAs complete
         if (u + 1 == u1 || hy_of(u + 1) != hy) umma::commit(&b_empty);  // last unit on this B tile
         umma::commit(&t_full[j]);
       }
@@ -742,7 +749,10 @@ cudaError_t launch_qprep(const LutArgs& la, cudaStream_t st) {
   return launch_pdl(qprep_kernel, dim3((n + 255) / 256), dim3(256), 0, st, la);
 }
 
-int lut_tile_nv(int nvec) { return nvec >= 128 ? 128 : ((nvec + 15) / 16) * 16; }  // MMA N: multiple of 16, <= 128 (B tile <= 64 KB)
+#ifndef A2ATS_LUT_NV_MAX
+#define A2ATS_LUT_NV_MAX 128  // tuning define: widest query tile (MMA N) of the LUT
+#endif
+int lut_tile_nv(int nvec) { return nvec >= A2ATS_LUT_NV_MAX ? A2ATS_LUT_NV_MAX : ((nvec + 15) / 16) * 16; }  // MMA N: multiple of 16, <= 128 (B tile <= 64 KB)
 int prep_lut_cols(int NV) { return (int)umma::tmem_cols_for(NV); }
 
 cudaError_t launch_prep(const PrepArgs& p, const CUtensorMap& tmA, const CUtensorMap& tmC, cudaStream_t st) {

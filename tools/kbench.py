@@ -81,6 +81,9 @@ for it in range(0 if args.select_only else args.iters):
         dec.step_postings(inp["q"], inp["k_cache"], inp["v_cache"], cfg.N, out=out)
     elif args.postings:
         dec.step_append_postings(inp["q"], inp["k_cache"], inp["v_cache"], cfg.N, out=out)
+    elif args.no_append:
+        dec.hist.copy_(hist)
+        dec.step(inp["q"], inp["k_cache"], inp["v_cache"], cfg.N, out=out, use_hist=not args.no_hist)
     else:
         dec.step_append(inp["q"], inp["k_cache"], inp["v_cache"], cfg.N, out=out, use_hist=not args.no_hist)
     A.a2ats_set_stage_events(None)
