@@ -532,7 +532,9 @@ namespace {
 // sub-step's output rows and selection rows back to (b, h * G + g).  One 16-B piece per thread.
 __global__ __launch_bounds__(256) void head_gather_q_kernel(const uint4* q, uint4* qg, int P, int Hkv, int G, int g) {
   pdl_wait();  // the previous sub-step reads qg
-  pdl_trigger();
+  // no early pdl_trigger(): the sub-step's kernels read q (= qg) in their pre-wait prologues, so
+  // they launch only at this grid's completion (implicit trigger), as after a2ats_stage_rows
+
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P * 16) return;
   const int r = i >> 4, b = r / Hkv, h = r - b * Hkv;

@@ -1599,7 +1599,7 @@ __global__ __launch_bounds__(kQT, A2ATS_QT_MINB) void select_postings_kernel(Sel
   extern __shared__ __align__(16) uint32_t sm[];
   __shared__ SelShared S;
   __shared__ uint32_t s_cls[256];    // compact 2-bit classes (code >> 4), L <= 4096
-  __shared__ int s_part[4][kQT / 32];
+  __shared__ int s_part[6][kQT / 32];  // (block scans of up to 6 values)
   __shared__ uint16_t s_sk[kQSinkMax];          // codes of the indexed sink tokens (list path)
   __shared__ int s_ts[kQTiedMax], s_tn[kQTiedMax];  // tied codes' lists (list path)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, pair = blockIdx.x;
@@ -1633,7 +1633,7 @@ __global__ __launch_bounds__(kQT, A2ATS_QT_MINB) void select_postings_kernel(Sel
   // 4 kQT unindexed tail tokens' codes (registers)
   const int LP = postings_off_stride(a.L);
   const int post0 = pair * LP;
-  uint32_t tcode[2], skmask = 0u;  // the first 4 kQT tail tokens' codes (16 bits each)
+  uint32_t tcode[2], skmask = 0u;  // codes of tail tokens tb0 + 4 tid .. + 3 (16 bits each)
   {
     __shared__ __align__(8) uint64_t s_pbar;
     const int32_t* histp = a.hist + (size_t)pair * a.L;
@@ -1655,11 +1655,11 @@ __global__ __launch_bounds__(kQT, A2ATS_QT_MINB) void select_postings_kernel(Sel
     int rc = -1;
     if (tid < nrem) rc = cp[tid < a.n_s ? tid : a.w0 + (tid - a.n_s)];
     if (list_ok && tid < nsk) s_sk[tid] = cp[tid];
-    const int tb = max(a.n_post, a.c0) + tid;
+    const int tb = max(a.n_post, a.c0) + 4 * tid;  // tail tokens tb .. tb + 3 (4 consecutive per thread)
 #pragma unroll
     for (int r = 0; r < 2; ++r)
-      tcode[r] = (tb + 2 * r * kQT < a.c1 ? (uint32_t)cp[tb + 2 * r * kQT] : 0u) |
-                 (tb + (2 * r + 1) * kQT < a.c1 ? (uint32_t)cp[tb + (2 * r + 1) * kQT] << 16 : 0u);
+      tcode[r] = (tb + 2 * r < a.c1 ? (uint32_t)cp[tb + 2 * r] : 0u) |
+                 (tb + 2 * r + 1 < a.c1 ? (uint32_t)cp[tb + 2 * r + 1] << 16 : 0u);
     A2ATS_TL(g_selp_tl, 0);
     __syncthreads();  // (barrier init, s_sk)
     for (int i = 0; i < nsk; ++i) {  // this thread's codewords holding an indexed sink
@@ -1710,7 +1710,26 @@ __global__ __launch_bounds__(kQT, A2ATS_QT_MINB) void select_postings_kernel(Sel
   // block scans: [0] above codes, [1] above entries, [2] tied codes, [3] tied entries (list
   // path: entries past the sinks).  Hit codes visited bit by bit (no unrolled per-code copies:
   // the kernel stays small in the instruction cache)
-  int v[4] = {0, 0, 0, 0}, ex[4], tot[4];
+  // short unindexed tails (<= 4 kQT tokens, 4 consecutive per thread from registers) are classified
+  // here and ride on the same block scan: [4] tail above v*, [5] tail tied
+  const int tb0 = max(a.n_post, a.c0);
+  const bool short_tail = a.c1 - tb0 <= 4 * kQT;
+  uint32_t tcl = 0u;  // 2-bit classes of this thread's 4 tail tokens
+  int v[6] = {0, 0, 0, 0, 0, 0}, ex[6], tot[6];
+  if (list_go && short_tail) {
+    __syncthreads();  // (s_cls complete)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int t = tb0 + 4 * tid + j;
+      if (t < a.c1) {
+        const int l = (int)((tcode[j >> 1] >> (16 * (j & 1))) & 0xffffu);
+        const uint32_t cl = (s_cls[l >> 4] >> (2 * (l & 15))) & 3u;
+        tcl |= cl << (2 * j);
+        v[4] += cl == 1u;
+        v[5] += cl == 2u;
+      }
+    }
+  }
   {
     int nAc = 0, nAe = 0, nTc = 0, nTe = 0;
     for (uint32_t mm = hmask; mm; mm &= mm - 1u) {
@@ -1729,7 +1748,7 @@ __global__ __launch_bounds__(kQT, A2ATS_QT_MINB) void select_postings_kernel(Sel
     v[2] = nTc;
     v[3] = nTe;
   }
-  q_scan<4>(v, ex, tot, s_part);
+  q_scan<6>(v, ex, tot, s_part);
   A2ATS_TL(g_selp_tl, 4);
   const int nA = tot[0], A_idx = tot[1], nT = tot[2], E_idx = tot[3];
   const int RT = R + postings_off_stride(a.L);  // + the bounds row (dead once the tables are built)
@@ -1772,6 +1791,87 @@ __global__ __launch_bounds__(kQT, A2ATS_QT_MINB) void select_postings_kernel(Sel
     // one tied code: its first min(n, m) entries staged too (after the above entries), stored
     // once the tail's above count is known
     const int n_tie1 = nT == 1 ? min(s_tn[0], (int)m) : 0;
+    // short tail: A (above count incl. the tail) is known, so the whole selection -- above lists,
+    // tail tokens, the m ties -- is staged at its final positions and leaves by one bulk store
+    const int A_s = A_idx + tot[4];
+    const bool all_staged = short_tail && A_s + (int)m <= stg_cap;
+    if (all_staged) {
+      const int sub = lane & 7;
+      for (int h = (warp << 2) + (lane >> 3); h < nA; h += (kQT / 32) * 4) {
+        const int n = hn[h];
+        const int32_t* src = ptok + hs[h] + sub;
+        uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(stg + hp[h] + sub));
+        int j = sub;
+        for (; j + 24 < n; j += 32, src += 32, d += 128)
+          asm volatile(
+              "cp.async.ca.shared.global [%0], [%1], 4;\n\t"
+              "cp.async.ca.shared.global [%2], [%3], 4;\n\t"
+              "cp.async.ca.shared.global [%4], [%5], 4;\n\t"
+              "cp.async.ca.shared.global [%6], [%7], 4;" ::"r"(d), "l"(src), "r"(d + 32), "l"(src + 8), "r"(d + 64),
+              "l"(src + 16), "r"(d + 96), "l"(src + 24)
+              : "memory");
+        for (; j < n; j += 8, src += 8, d += 32)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
+      }
+      if (nT == 1)  // the tied list's first min(n, m) entries: tie indices 0 ..
+        for (int j = tid; j < n_tie1; j += kQT) {
+          const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(stg + A_s + j));
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(ptok + s_ts[0] + j) : "memory");
+        }
+      // this thread's tail tokens: above ones after the lists, tied ones after the indexed ties
+      {
+        int pa = A_idx + ex[4], rt = E_idx + ex[5];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t cl = (tcl >> (2 * j)) & 3u;
+          const int t = tb0 + 4 * tid + j;
+          if (cl == 1u) stg[pa++] = t;
+          if (cl == 2u) {
+            if (rt < (int)m) stg[A_s + rt] = t;
+            ++rt;
+          }
+        }
+      }
+      if (nT > 1)  // several tied codes: tie index of an entry = its rank in the merge of the lists
+        for (int g = 0; g < nT; ++g) {
+          const int st = s_ts[g], n = s_tn[g];
+          for (int j = tid; j < n; j += kQT) {
+            const int t = __ldg(ptok + st + j);
+            int r = j;
+            for (int g2 = 0; g2 < nT; ++g2) {
+              if (g2 == g) continue;
+              int lo = 0, hi = s_tn[g2];
+              const int32_t* q2 = ptok + s_ts[g2];
+              while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (__ldg(q2 + mid) < t) lo = mid + 1;
+                else hi = mid;
+              }
+              r += lo;
+            }
+            if (r < (int)m) stg[A_s + r] = t;
+          }
+        }
+      cp_async_commit();
+      cp_async_wait<0>();
+      __syncthreads();
+      const int lim = min(A_s + (int)m, (int)cap);
+      const int i0 = min(lim, (4 - sph) & 3), i1 = i0 + ((lim - i0) & ~3);
+      if (tid < i0) selp[tid] = stg[tid];
+      if (tid < lim - i1) selp[i1 + tid] = stg[i1 + tid];
+      if (tid == 0 && i1 > i0) {
+        umma::fence_proxy_async();
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(selp + i0),
+                     "r"(static_cast<uint32_t>(__cvta_generic_to_shared(stg + i0))), "r"((uint32_t)(i1 - i0) * 4u)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      }
+      A2ATS_TL(g_selp_tl, 6);
+      A2ATS_TL(g_selp_tl, 7);
+      A2ATS_TL(g_sel_tl, 1);
+      return;
+    }
     const bool tie_staged = nT == 1 && A_idx + n_tie1 <= stg_cap;
     if (A_idx <= stg_cap) {
       const int sub = lane & 7;  // groups of 8 lanes, a code each (lists average N / L entries)
@@ -1840,10 +1940,7 @@ __global__ __launch_bounds__(kQT, A2ATS_QT_MINB) void select_postings_kernel(Sel
     }
     A2ATS_TL(g_selp_tl, 6);
     // tail [max(n_post, c0), c1): classified from codes; counts first (A needs the above count)
-    const int tb0 = max(a.n_post, a.c0);
-    auto tail_code = [&](int t, int r) {  // code of tail token t = tb0 + r * kQT + tid
-      return r < 4 ? (int)(((r < 2 ? tcode[0] : tcode[1]) >> (16 * (r & 1))) & 0xffffu) : (int)cp[t];
-    };
+    auto tail_code = [&](int t, int) { return (int)cp[t]; };
     int tA = 0, tT = 0;
     for (int t = tb0 + tid, r = 0; t < a.c1; t += kQT, ++r) {
       const int l = tail_code(t, r);

@@ -120,3 +120,19 @@ def test_per_head_append_step():
     cpu = {k: (v.cpu() if isinstance(v, torch.Tensor) else v) for k, v in inp.items()}
     cpu["codes"] = inp["z"].cpu()
     check(cfg, cpu, sel.cpu().numpy(), out.cpu().numpy(), heads=[(0, 1), (1, 6), (1, 7)])
+
+
+def test_per_head_repeated_steps_stable():
+    """Stress for the sub-step plumbing: the gathered q of head position g is written by the kernel
+    right before the sub-step, whose kernels read q before their dependency wait -- a gather that
+    let its dependents launch early raced with them (seen as one head's stale selection)."""
+    cfg = Config("phs", B=2, Hq=8, Hkv=2, d=128, N=12000, L=300, K=800, bridge=0)
+    ref = None
+    for rep in range(6):
+        inp, sel, out = run(cfg, 97, postings=0.5, code_dist="zipf")
+        if ref is None:
+            ref = (sel, out)
+            check(cfg, inp, sel, out, sorted_sets=True, heads=[(0, 2), (1, 2), (1, 7)])
+        else:
+            np.testing.assert_array_equal(sel, ref[0])
+            assert np.array_equal(out.view(np.uint32), ref[1].view(np.uint32))
