@@ -801,6 +801,7 @@ int decode_impl_one(const a2ats_shape* shape, const a2ats_params* params, int32_
   aa.q = static_cast<const uint16_t*>(q);
   std::memcpy(aa.bcs, la.bcs, sizeof(aa.bcs));
   aa.wlog = wlog;
+  aa.wlog_late = (long_select || post_select) ? 1 : 0;  // (the select kernel wrote wlog)
   aa.n_wl = n_wl;
   aa.cs = cs;
   aa.kc = static_cast<const uint16_t*>(k_cache);
@@ -1362,6 +1363,7 @@ int shard_partial(const a2ats_shape* shape, const a2ats_params* params, int32_t 
   aa.q = static_cast<const uint16_t*>(q);
   std::memcpy(aa.bcs, la.bcs, sizeof(aa.bcs));
   aa.wlog = wlog;
+  aa.wlog_late = 1;  // (the shard threshold kernel writes wlog)
   aa.n_wl = n_wl;
   aa.cs = reinterpret_cast<float2*>(base + Lw.cs);
   aa.kc = static_cast<const uint16_t*>(k_cache);

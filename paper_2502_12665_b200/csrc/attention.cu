@@ -149,8 +149,9 @@ __device__ __forceinline__ void attn_body(const AttnArgs& a) {
     return npre;
   };
   // wlog comes from the prep kernel, two launches back when a select kernel runs in between
-  // (complete when this grid starts); with keff == 0 no select is launched: read after the wait
-  const bool wlog_early = !a.nsel && a.keff > 0;
+  // (complete when this grid starts); with keff == 0 no select is launched, and long-context /
+  // posting-list selects write wlog themselves: read after the wait
+  const bool wlog_early = !a.nsel && a.keff > 0 && !a.wlog_late;
   int nwpre = 0;
   if (wlog_early) nwpre = load_wlog(a.keff);
   pdl_wait();  // sel / counts come from select

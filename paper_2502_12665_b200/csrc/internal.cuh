@@ -78,7 +78,12 @@ constexpr int kTlMax = 8192;
 // kernel N+1 may start while kernel N runs, does its input-independent prologue
 // (TMEM alloc, constant / input loads), then pdl_wait()s for N's completion.
 // Each kernel calls pdl_trigger() only AFTER its own pdl_wait(), so at most two
-// kernels overlap and a pre-wait prologue never races a kernel two back.
+// kernels overlap and a pre-wait prologue never races a kernel two back.  A pre-wait
+// prologue reads only data written before the step or at least two launches back; a
+// kernel whose output its successor reads before the wait (a2ats_stage_rows, the
+// per-query-head q gather) does not trigger early, and the attention reads the window
+// logits after its wait when its predecessor (a long-context / posting-list select)
+// wrote them.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
@@ -234,6 +239,7 @@ struct AttnArgs {
   float scale_log2;       // log2(e) / sqrt(d)
   float2 bcs[kHalf];      // (cos, sin)(b f_m), from fp64 angles on the host
   const float* wlog;      // [P, 64, 8] logits of the first n_wl window rows (prep kernel)
+  int wlog_late;          // 1: the select kernel (this grid's predecessor) writes wlog: read after the wait
   int n_wl;
 };
 
