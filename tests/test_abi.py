@@ -103,3 +103,25 @@ def test_workspace_size_grows_with_budget(lib):
     big = b.a2ats_decode_workspace_bytes(s, b.Params(topk=2000))
     assert big > small > 0
     assert b.a2ats_build_codes_workspace_bytes(s) > 0
+
+
+def test_round2_abi_fields_without_gpu(lib):
+    """ABI 9 fields validated on the host: code width (uint8 only for L <= 256), hist_lag (deferred
+    a0, at most the window), per-query-head mode (its own workspace layout), padded posting rows."""
+    from paper_2502_12665_b200 import binding as b
+    p = b.Params(topk=100)
+    assert b.a2ats_decode_workspace_bytes(b.make_shape(2, 8, 2, 128, 256, 4096, code_bytes=1), p) > 0
+    assert b.a2ats_decode_workspace_bytes(b.make_shape(2, 8, 2, 128, 300, 4096, code_bytes=1), p) == 0
+    assert b.a2ats_decode_workspace_bytes(b.make_shape(2, 8, 2, 128, 256, 4096, code_bytes=3), p) == 0
+    s = b.make_shape(2, 8, 2, 128, 1000, 4096)
+    assert b.a2ats_decode_workspace_bytes(s, b.Params(topk=100, hist_lag=64)) > 0
+    assert b.a2ats_decode_workspace_bytes(s, b.Params(topk=100, hist_lag=65)) == 0
+    assert b.a2ats_decode_workspace_bytes(s, b.Params(topk=100, hist_lag=-1)) == 0
+    gqa = b.a2ats_decode_workspace_bytes(s, b.Params(topk=100))
+    per_head = b.a2ats_decode_workspace_bytes(s, b.Params(topk=100, group_reduce=b.A2ATS_GROUP_PER_HEAD))
+    assert per_head > 0 and gqa > 0 and per_head != gqa  # (the sub-step's own layout + q / out / sel buffers)
+    assert b.a2ats_decode_workspace_bytes(s, b.Params(topk=100, group_reduce=3)) == 0
+    # posting index: offsets [P, (L + 4) & ~3] int32, then (256-B aligned) tokens [P, n_max] int32
+    P, LP = 4, (1000 + 4) // 4 * 4
+    tok = (P * LP * 4 + 255) // 256 * 256
+    assert b.a2ats_postings_bytes(s) == (tok + P * 4096 * 4 + 255) // 256 * 256
