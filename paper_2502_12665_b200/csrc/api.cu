@@ -309,6 +309,7 @@ inline void stage_mark(int i, cudaStream_t st) {
 LutArgs make_lut_args(const a2ats_shape* shape, const a2ats_params* params, const Derived& d, const void* q,
                       const void* codebook, float* agg, float* lut_full, float2* cs) {
   LutArgs la;
+  la.cs_in_lut = 0;
   la.q = static_cast<const uint16_t*>(q);
   la.qt = nullptr;
   la.codebook = static_cast<const uint16_t*>(codebook);
@@ -666,6 +667,7 @@ int decode_impl_one(const a2ats_shape* shape, const a2ats_params* params, int32_
   // lut_fma_kernel (FMA engine) or lut_persist_kernel (precomputed q~ tiles) computes agg before
   // the prep kernel, which then runs only its encode / window roles
   const bool lut_persist = la.qt != nullptr && A2ATS_LUT_PERSIST;
+  la.cs_in_lut = lut_persist ? 1 : 0;
   if (lut_fma || lut_persist) p.n_lut = 0;
   // long contexts: the window logits are computed by the select threshold kernel, before its
   // dependency wait (it waits for this kernel anyway); otherwise by the prep kernel's window role

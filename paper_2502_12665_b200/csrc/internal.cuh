@@ -168,6 +168,7 @@ struct LutArgs {
   float2* cs;                // [window, 64]   (cos, sin)(r f_m)
   int B, Hq, Hkv, G, L, window, bridge, group_reduce;
   int NV, nvt;               // query rows per MMA tile (multiple of 16, <= 256), tiles per head
+  int cs_in_lut;             // 1: the persistent LUT writes the window table cs (not qprep)
   RopeTab rt;
   float2 bcs[kHalf];         // (cos, sin)(b f_m), from fp64 angles on the host
 };

@@ -343,6 +343,12 @@ __global__ __launch_bounds__(kLpWarps * 32, 1) void lut_persist_kernel(const __g
     const int q = warp & 3, half = (warp - 2) >> 2, nvec = a.B * G;
     const bool sum = (a.group_reduce == A2ATS_GROUP_SUM);
     const size_t bstride = (size_t)a.Hkv * a.L;
+    if (a.cs_in_lut)  // window table cs[r][m] (fp64 angles) while the first MMA runs
+      for (int k = blockIdx.x * 256 + tid - 64; k < a.window * kHalf; k += gridDim.x * 256) {
+        double sn, cn;
+        sincos((double)(k >> 6) * a.rt.inv_freq[k & (kHalf - 1)], &sn, &cn);
+        a.cs[k] = make_float2((float)cn, (float)sn);
+      }
     for (int u = u0, it = 0; u < u1; ++u, ++it) {
       const int j = it & 1, hy = hy_of(u), h = hy / a.nvt, y = hy % a.nvt, x = u % ntx;
       const int vec0 = y * NV, nv_here = min(NV, nvec - vec0);
@@ -521,11 +527,12 @@ __global__ __launch_bounds__(256) void qprep_kernel(LutArgs a) {
 #endif
   const int NV = a.NV, nvec = a.B * a.G;
   const int it = blockIdx.x * blockDim.x + threadIdx.x;
-  for (int k = it; k < a.window * kHalf; k += gridDim.x * blockDim.x) {  // window table cs[r][m]
-    double sn, cn;
-    sincos((double)(k >> 6) * a.rt.inv_freq[k & (kHalf - 1)], &sn, &cn);
-    a.cs[k] = make_float2((float)cn, (float)sn);
-  }
+  if (!a.cs_in_lut)  // (else the persistent LUT's idle epilogue warps write it, off this kernel's path)
+    for (int k = it; k < a.window * kHalf; k += gridDim.x * blockDim.x) {  // window table cs[r][m]
+      double sn, cn;
+      sincos((double)(k >> 6) * a.rt.inv_freq[k & (kHalf - 1)], &sn, &cn);
+      a.cs[k] = make_float2((float)cn, (float)sn);
+    }
   if (it >= a.Hkv * a.nvt * 8 * NV) return;
   const int n = it % NV, c = (it / NV) & 7, ty = it / (NV * 8), y = ty % a.nvt, h = ty / a.nvt;
   const int vn = y * NV + n;
