@@ -992,7 +992,8 @@ __device__ __forceinline__ void load_c_regs(const SelArgs& a, const int* cnt, in
   }
 }
 
-template <int NT, int PT>
+// PRE: the caller set S.s_kmin = ~0, S.s_kmax = 0 and zeroed S.bins before a barrier (saves one)
+template <int NT, int PT, bool PRE = false>
 __device__ __forceinline__ void level_regs(const SelArgs& a, SelShared& S, int pair, const int (&c)[PT],
                                            uint32_t (&k)[PT], uint32_t* skey, int* scnt, int survcap,
                                            uint32_t& kstar_out, uint32_t& m_out) {
@@ -1027,12 +1028,14 @@ __device__ __forceinline__ void level_regs(const SelArgs& a, SelShared& S, int p
     }
     kmn = __reduce_min_sync(0xffffffffu, kmn);
     kmx = __reduce_max_sync(0xffffffffu, kmx);
-    if (tid == 0) {
-      S.s_kmin = 0xffffffffu;
-      S.s_kmax = 0u;
+    if (!PRE) {
+      if (tid == 0) {
+        S.s_kmin = 0xffffffffu;
+        S.s_kmax = 0u;
+      }
+      for (int i = tid; i < 256; i += NT) S.bins[i] = 0;
+      __syncthreads();
     }
-    for (int i = tid; i < 256; i += NT) S.bins[i] = 0;
-    __syncthreads();
     if (lane == 0) {
       atomicMin(&S.s_kmin, kmn);
       atomicMax(&S.s_kmax, kmx);
@@ -1047,6 +1050,8 @@ __device__ __forceinline__ void level_regs(const SelArgs& a, SelShared& S, int p
     m_out = (uint32_t)keff;
     return;
   }
+  // 256 bins over the candidates' VALUE range (the key range spans the sign boundary of the
+  // floats: binning keys by shifts puts most candidates into a few bins -- measured 8x the rank)
   auto key_val = [](uint32_t kk) {
     const uint32_t o = ~kk;
     return __uint_as_float((o & 0x80000000u) ? (o & 0x7fffffffu) : ~o);
@@ -1655,6 +1660,11 @@ __global__ __launch_bounds__(kQT, A2ATS_QT_MINB) void select_postings_kernel(Sel
     int rc = -1;
     if (tid < nrem) rc = cp[tid < a.n_s ? tid : a.w0 + (tid - a.n_s)];
     if (list_ok && tid < nsk) s_sk[tid] = cp[tid];
+    if (tid == 0) {  // level_regs<.., PRE>: range and bins initialised here (before a barrier)
+      S.s_kmin = 0xffffffffu;
+      S.s_kmax = 0u;
+    }
+    S.bins[tid] = 0;  // (kQT == 256 bins)
     const int tb = max(a.n_post, a.c0) + 4 * tid;  // tail tokens tb .. tb + 3 (4 consecutive per thread)
 #pragma unroll
     for (int r = 0; r < 2; ++r)
@@ -1681,7 +1691,7 @@ __global__ __launch_bounds__(kQT, A2ATS_QT_MINB) void select_postings_kernel(Sel
   append_hist(a, pair, cp);
   if (a.keff <= 0) return;  // (uint8 codes: launched for the append's histogram alone)
   uint32_t k[16], kstar, m;
-  level_regs<kQT, 16>(a, S, pair, c, k, skey, scnt, kQSurv, kstar, m);  // (ends synced: cnt dead)
+  level_regs<kQT, 16, true>(a, S, pair, c, k, skey, scnt, kQSurv, kstar, m);  // (ends synced: cnt dead)
   A2ATS_TL(g_sel_tl, 3);
   // classes of this thread's 16 codewords; hit codes (above or at v*, candidates present)
   int e_unused = 0;
