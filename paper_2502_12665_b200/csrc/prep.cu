@@ -245,7 +245,9 @@ __host__ __device__ constexpr int lut_persist_smem(int NV) {
 }
 
 template <int G>
-__global__ __launch_bounds__(kLpWarps * 32, 1) void lut_persist_kernel(const __grid_constant__ CUtensorMap tmA,
+// (<= 96 registers: with the LUT CTA's 320 threads, two posting-select CTAs (256 x 64) still fit on
+// its SM, so they run their step-input prologue during the LUT)
+__global__ __launch_bounds__(kLpWarps * 32, 2) void lut_persist_kernel(const __grid_constant__ CUtensorMap tmA,
                                                                        const LutArgs a, int n_units, int ntx) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sA = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -384,17 +386,12 @@ __global__ __launch_bounds__(kLpWarps * 32, 1) void lut_persist_kernel(const __g
         }
       };
       const int c_lo = half * (NV >> 1), c_hi = min(c_lo + (NV >> 1), nv_here);
-      for (int col0 = c_lo; col0 < c_hi; col0 += 64) {  // two 32-column loads in flight per wait
-        uint32_t r[64];
-        umma::tmem_ld32(ta + col0, *reinterpret_cast<uint32_t(*)[32]>(r));
-        if (col0 + 32 < c_hi) umma::tmem_ld32(ta + col0 + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
+      for (int col0 = c_lo; col0 < c_hi; col0 += 32) {
+        uint32_t r[32];
+        umma::tmem_ld32(ta + col0, r);
         umma::tmem_wait_ld();
         fold(r, col0);
         fold(r + 16, col0 + 16);
-        if (col0 + 32 < c_hi) {
-          fold(r + 32, col0 + 32);
-          fold(r + 48, col0 + 48);
-        }
       }
       umma::fence_before();
       __syncwarp();
