@@ -113,6 +113,19 @@ def test_scores_at_wide_lut_tiles(B, note):
     assert worst <= SCORE_RTOL
 
 
+@pytest.mark.parametrize("B,Hq,Hkv,L", [(10, 64, 8, 1000),   # G = 8, B*G = 80: one ragged tile, 125-row codeword tail
+                                       (40, 16, 8, 512),    # G = 2, B*G = 80
+                                       (20, 32, 8, 384),    # G = 4, B*G = 80, L not a multiple of 256
+                                       (72, 8, 8, 256)])    # G = 1, B*G = 72
+def test_scores_persistent_lut_group_sizes(B, Hq, Hkv, L):
+    """The persistent LUT kernel (query tiles wider than 64 vectors, q~ tiles from qprep) for every
+    group size and ragged vector / codeword tiles: scores at 1e-4, sets and outputs vs the oracle."""
+    cfg = Config("plut", B=B, Hq=Hq, Hkv=Hkv, d=128, N=700, L=L, K=60)
+    pairs = [(b, h) for b in range(B) for h in range(Hkv)][::max(1, B * Hkv // 12)]
+    worst = run_and_check(cfg, 950 + B + Hq, pairs=pairs)
+    assert worst <= SCORE_RTOL
+
+
 # ------------------------------------------------------------------ window / sinks / frequencies
 @pytest.mark.parametrize("window,n_sink", [(96, 4), (128, 0), (100, 7), (65, 1)])
 def test_window_beyond_precomputed_rows(window, n_sink):
