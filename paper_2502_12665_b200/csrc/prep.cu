@@ -193,11 +193,7 @@ __device__ __forceinline__ void lut_tile(const CUtensorMap& tmA, const PrepArgs&
           const float xg = __uint_as_float(r[bb * G + g]);
           v = sum ? v + xg : fmaxf(v, xg);
         }
-#ifdef A2ATS_DIAG_LUT_NOSTORE
-        if (v == 123.f) pb[bb * bstride] = v;  // (diagnostic build: stores elided)
-#else
         if (live && col0 + bb * G < nv_here) pb[bb * bstride] = v;
-#endif
       }
     };
     // 32-column blocks, software-pipelined: the next block's TMEM load is in flight while this
