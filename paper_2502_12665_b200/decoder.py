@@ -95,3 +95,38 @@ class Decoder:
                                     self.hist if use_hist else None, self.chat, self.nrm, out, sel_out, scores_out,
                                     self.ws_dec, self.stream)
         return out
+
+    # ------------------------------------------------------------------ serving loop
+    def start(self, keys, n_ctx: int, engine: str = "auto", rebuild_every: int = 1024):
+        """Prefill: encode tokens [0, n_ctx) (a0, running histogram) and pick the selection engine
+        for the decode loop: posting lists (f3) where the code scan would need its long-context
+        kernels, the code scan otherwise ("auto"), or as given.  Then call decode() per step."""
+        self.encode(keys, 0, n_ctx)
+        self._n_enc = int(n_ctx)
+        if engine == "auto":
+            engine = "postings" if n_ctx - self.params.window > 2 * 32768 and self.shape.L <= 4096 else "scan"
+        self._engine = engine
+        self._every = int(rebuild_every)
+        if engine == "postings":
+            self.build_postings(max(0, n_ctx - self.params.window))
+
+    def decode(self, q, k_cache, v_cache, n_ctx: int, out=None, sel_out=None):
+        """One decode step for a context of n_ctx tokens (token n_ctx - 1's K/V row already in the
+        caches) with the library's maintenance policy: a0 batched -- the newest tokens are encoded
+        in one a2ats_build_codes call when the oldest unencoded one would leave the window
+        (params.hist_lag covers the rest; reading Q34) -- and, with posting lists, the index rebuilt
+        every `rebuild_every` steps (reading Q33).  Results equal a2ats_decode_step_append's (the
+        same top-K sets; with posting lists the rows are summed in index order)."""
+        w = self.params.window
+        if n_ctx - self._n_enc > w:          # the oldest unencoded token would become a candidate
+            self.encode(k_cache, self._n_enc, n_ctx - 1)
+            self._n_enc = n_ctx - 1
+        self.params.hist_lag = n_ctx - self._n_enc
+        try:
+            if self._engine == "postings":
+                if n_ctx - w - self.n_post > self._every:
+                    self.build_postings(n_ctx - w)
+                return self.step_postings(q, k_cache, v_cache, n_ctx, out=out, sel_out=sel_out)
+            return self.step(q, k_cache, v_cache, n_ctx, out=out, sel_out=sel_out)
+        finally:
+            self.params.hist_lag = 0

@@ -108,3 +108,34 @@ def test_batched_encode_policy_equals_fused_append():
     torch.cuda.synchronize()
     assert torch.equal(fused.codes[:, :, :n0 + steps], lagged.codes[:, :, :n0 + steps])
     assert torch.equal(fused.hist, lagged.hist)
+
+
+@pytest.mark.parametrize("engine", ["scan", "postings"])
+def test_decoder_serving_loop_equals_fused_append(engine):
+    """Decoder.start / decode (batched a0 every window, posting index rebuilt every few steps) over
+    a run of decode steps == the fused append step of every step: the same codes, histogram and
+    top-K sets; outputs equal up to the summation order of the rows (index order)."""
+    cfg = Config("loop", B=2, Hq=8, Hkv=2, d=128, N=9000, L=512, K=540)
+    steps = 150
+    inp = make_inputs(cfg, 320, device="cuda", with_h=True, n_max=cfg.n_max(extra=steps + 8))
+    q, kc, vc = inp["q"], inp["k_cache"], inp["v_cache"]
+    n0 = cfg.N - steps
+    mk = lambda: A.Decoder(cfg.B, cfg.Hq, cfg.Hkv, cfg.L, inp["n_max"], inp["codebook"], inp["H"],
+                           A.Params(window=cfg.window, bridge=cfg.bridge, n_sink=cfg.n_sink, topk=cfg.K))
+    ref, dut = mk(), mk()
+    ref.encode(kc, 0, n0)
+    dut.start(kc, n0, engine=engine, rebuild_every=40)
+    for s in range(steps):
+        n = n0 + s + 1
+        s1 = torch.full((cfg.B, cfg.Hkv, cfg.K), -1, dtype=torch.int32, device="cuda")
+        s2 = torch.full_like(s1, -1)
+        o1 = ref.step_append(q, kc, vc, n, sel_out=s1)
+        o2 = dut.decode(q, kc, vc, n, sel_out=s2)
+        torch.cuda.synchronize()
+        assert torch.equal(s1, torch.sort(s2, dim=2).values), s
+        rel = ((o1 - o2).norm(dim=2) / o1.norm(dim=2)).max().item()
+        assert rel <= 1e-5, (s, rel)
+    dut.encode(kc, dut._n_enc, n0 + steps)
+    torch.cuda.synchronize()
+    assert torch.equal(ref.codes[:, :, :n0 + steps], dut.codes[:, :, :n0 + steps])
+    assert torch.equal(ref.hist, dut.hist)
