@@ -136,3 +136,26 @@ def test_per_head_repeated_steps_stable():
         else:
             np.testing.assert_array_equal(sel, ref[0])
             assert np.array_equal(out.view(np.uint32), ref[1].view(np.uint32))
+
+
+def test_per_head_with_uint8_codes_and_deferred_a0():
+    """The variants compose: per-query-head selection over uint8 codes with the posting-list engine
+    and a0 deferred (the newest 20 tokens not encoded) == the per-head oracle."""
+    cfg = Config("phc", B=2, Hq=8, Hkv=2, d=128, N=6000, L=256, K=400, bridge=0)
+    lag = 20
+    inp = make_inputs(cfg, 99, device="cpu", family="g1", with_h=False)
+    inp["codes"] = inp["z"].to(torch.uint16)
+    dev = {k: (v.cuda() if isinstance(v, torch.Tensor) else v) for k, v in inp.items()}
+    params = A.Params(window=cfg.window, bridge=0, n_sink=cfg.n_sink, topk=cfg.K, group_reduce=PH, hist_lag=lag)
+    dec = A.Decoder(cfg.B, cfg.Hq, cfg.Hkv, cfg.L, inp["n_max"], dev["codebook"], None, params, code_bytes=1)
+    codes8 = dev["codes"].to(torch.int32).to(torch.uint8)
+    codes8[:, :, cfg.N - lag:cfg.N] = 255 - codes8[:, :, cfg.N - lag:cfg.N]  # not encoded yet: garbage
+    dec.codes = codes8
+    c = dev["codes"][:, :, :cfg.N - lag].to(torch.int64)
+    dec.hist = torch.zeros((cfg.B, cfg.Hkv, cfg.L), dtype=torch.int32, device="cuda")
+    dec.hist.scatter_add_(2, c, torch.ones_like(c, dtype=torch.int32))
+    dec.build_postings(cfg.N - cfg.window - 300)
+    sel = torch.full((cfg.B, cfg.Hq, cfg.K), -1, dtype=torch.int32, device="cuda")
+    out = dec.step_postings(dev["q"], dev["k_cache"], dev["v_cache"], cfg.N, sel_out=sel)
+    torch.cuda.synchronize()
+    check(cfg, inp, sel.cpu().numpy(), out.cpu().numpy(), sorted_sets=True, heads=[(0, 0), (0, 5), (1, 3), (1, 6)])
