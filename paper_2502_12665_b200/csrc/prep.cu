@@ -509,7 +509,32 @@ __global__ __launch_bounds__(256) void qprep_kernel(LutArgs a) {
     g_prep_tl[4096 + blockIdx.x][0] = t_;
   }
 #endif
-  pdl_wait();  // the previous step's LUT reads qt
+  // step inputs first (q, the bridge rotation), the q~ tile written after the dependency wait
+  __shared__ float2 sbcs[kHalf];  // bridge (cos, sin) in smem: per-lane indices would serialize param loads
+  if (threadIdx.x < kHalf) sbcs[threadIdx.x] = a.bcs[threadIdx.x];
+  const int NV = a.NV, nvec = a.B * a.G;
+  const int it = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool work = it < a.Hkv * a.nvt * 8 * NV;
+  const int n = it % NV, c = (it / NV) & 7, ty = it / (NV * 8), y = ty % a.nvt, h = ty / a.nvt;
+  const int vn = y * NV + n;
+  uint4 u1 = make_uint4(0, 0, 0, 0), u2 = u1;
+  if (work && vn < nvec) {
+    const uint16_t* qp = a.q + (size_t)((vn / a.G) * a.Hq + h * a.G + vn % a.G) * kD + c * 8;
+    u1 = ld_nc_u4(qp);
+    u2 = ld_nc_u4(qp + kHalf);
+  }
+  __syncthreads();
+  const uint32_t w1[4] = {u1.x, u1.y, u1.z, u1.w}, w2[4] = {u2.x, u2.y, u2.z, u2.w};
+  uint16_t h1[8], l1[8], h2[8], l2[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {  // half-split pair (m, m+64); zero rows stay zero
+    const float x1 = (e & 1) ? bf_hi(w1[e >> 1]) : bf_lo(w1[e >> 1]);
+    const float x2 = (e & 1) ? bf_hi(w2[e >> 1]) : bf_lo(w2[e >> 1]);
+    const float2 cs = sbcs[c * 8 + e];
+    umma::split_bf16(fmaf(x1, cs.x, -x2 * cs.y), h1[e], l1[e]);
+    umma::split_bf16(fmaf(x2, cs.x, x1 * cs.y), h2[e], l2[e]);
+  }
+  pdl_wait();  // the previous step's LUT reads qt (and its attention the window table)
   pdl_trigger();
 #ifdef A2ATS_PHASES
   if (threadIdx.x == 0) {
@@ -518,38 +543,19 @@ __global__ __launch_bounds__(256) void qprep_kernel(LutArgs a) {
     g_prep_tl[4096 + blockIdx.x][2] = t_;
   }
 #endif
-  const int NV = a.NV, nvec = a.B * a.G;
-  const int it = blockIdx.x * blockDim.x + threadIdx.x;
   if (!a.cs_in_lut)  // (else the persistent LUT's idle epilogue warps write it, off this kernel's path)
     for (int k = it; k < a.window * kHalf; k += gridDim.x * blockDim.x) {  // window table cs[r][m]
       double sn, cn;
       sincos((double)(k >> 6) * a.rt.inv_freq[k & (kHalf - 1)], &sn, &cn);
       a.cs[k] = make_float2((float)cn, (float)sn);
     }
-  if (it >= a.Hkv * a.nvt * 8 * NV) return;
-  const int n = it % NV, c = (it / NV) & 7, ty = it / (NV * 8), y = ty % a.nvt, h = ty / a.nvt;
-  const int vn = y * NV + n;
-  uint4 u1 = make_uint4(0, 0, 0, 0), u2 = u1;
-  if (vn < nvec) {
-    const uint16_t* qp = a.q + (size_t)((vn / a.G) * a.Hq + h * a.G + vn % a.G) * kD + c * 8;
-    u1 = ld_nc_u4(qp);
-    u2 = ld_nc_u4(qp + kHalf);
+  if (work) {
+    uint4* dst = reinterpret_cast<uint4*>(a.qt + (size_t)ty * 32 * NV * 8);
+    dst[c * NV + n] = pack8(h1);
+    dst[(c + 8) * NV + n] = pack8(h2);
+    dst[(c + 16) * NV + n] = pack8(l1);
+    dst[(c + 24) * NV + n] = pack8(l2);
   }
-  const uint32_t w1[4] = {u1.x, u1.y, u1.z, u1.w}, w2[4] = {u2.x, u2.y, u2.z, u2.w};
-  uint16_t h1[8], l1[8], h2[8], l2[8];
-#pragma unroll
-  for (int e = 0; e < 8; ++e) {  // half-split pair (m, m+64); zero rows stay zero
-    const float x1 = (e & 1) ? bf_hi(w1[e >> 1]) : bf_lo(w1[e >> 1]);
-    const float x2 = (e & 1) ? bf_hi(w2[e >> 1]) : bf_lo(w2[e >> 1]);
-    const float2 cs = a.bcs[c * 8 + e];
-    umma::split_bf16(fmaf(x1, cs.x, -x2 * cs.y), h1[e], l1[e]);
-    umma::split_bf16(fmaf(x2, cs.x, x1 * cs.y), h2[e], l2[e]);
-  }
-  uint4* dst = reinterpret_cast<uint4*>(a.qt + (size_t)ty * 32 * NV * 8);
-  dst[c * NV + n] = pack8(h1);
-  dst[(c + 8) * NV + n] = pack8(h2);
-  dst[(c + 16) * NV + n] = pack8(l1);
-  dst[(c + 24) * NV + n] = pack8(l2);
 #ifdef A2ATS_PHASES
   if (threadIdx.x == 0) {
     unsigned long long t_;
