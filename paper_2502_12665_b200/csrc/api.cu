@@ -50,6 +50,9 @@ cudaError_t ensure_smem_attr(const void* kernel, int bytes) {
 #ifndef A2ATS_PIPE_MIN_CHUNKS
 #define A2ATS_PIPE_MIN_CHUNKS 2
 #endif
+#ifndef A2ATS_POST_WLOG
+#define A2ATS_POST_WLOG 1  // tuning define: the posting select precomputes the first 64 window logits
+#endif
 #ifndef A2ATS_LUT_PERSIST
 #define A2ATS_LUT_PERSIST 1  // persistent warp-specialized LUT for precomputed q~ tiles (tuning define)
 #endif
@@ -683,7 +686,9 @@ int decode_impl_one(const a2ats_shape* shape, const a2ats_params* params, int32_
                            shape->n_max % 64 == 0;
   const bool split_select = !post_select && long_select && !pipe_select;
   prep_set_window(p, shape, k_cache, wlog, n_ctx, d.w0, d.n_w, 0);
-  const int n_wl = p.n_wl;
+  // posting-list select (A2ATS_POST_WLOG 0): no window logits precomputed -- the attention rotates
+  // every window row itself (its cs-table branch), the select keeps its small shared memory
+  const int n_wl = (post_select && !A2ATS_POST_WLOG) ? 0 : p.n_wl;
   // long contexts / postings: the threshold (postings) kernel computes the window logits before its wait
   if (long_select || post_select || !attend) p.n_win = 0;
   CUtensorMap tmA, tmC;
@@ -750,7 +755,7 @@ int decode_impl_one(const a2ats_shape* shape, const a2ats_params* params, int32_
     sa.B = shape->B;
     sa.wlog = nullptr;
     sa.P = d.P;
-    if ((long_select || post_select) && attend) {  // the threshold kernel computes the window logits before its wait
+    if ((long_select || post_select) && attend && n_wl > 0) {  // the threshold kernel computes the window logits before its wait
       sa.wlog = wlog;
       sa.q = static_cast<const uint16_t*>(q);
       sa.kc = static_cast<const uint16_t*>(k_cache);
