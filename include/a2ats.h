@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define A2ATS_ABI_VERSION 9
+#define A2ATS_ABI_VERSION 10
 
 /* ---- status codes ---------------------------------------------------- */
 #define A2ATS_OK 0
@@ -73,6 +73,10 @@ extern "C" {
 /* kv_location (reading: the paper's CPU-resident KV cache of P:392-394). */
 #define A2ATS_KV_DEVICE 0       /* K/V cache in HBM */
 #define A2ATS_KV_HOST_MAPPED 1  /* K/V cache in mapped pinned host memory, read over PCIe */
+
+/* rope_mode (the ablation configurations of P:419-427). */
+#define A2ATS_ROPE_WINDOWED 0   /* WRoPE, the method (Eqs. 11-12) */
+#define A2ATS_ROPE_STANDARD 1   /* standard RoPE on post-PE keys (the "Baseline" / "QAVQ" ablations) */
 
 /* lut_engine: which pipes compute the score table LUT = q~ C^T (a2, Eq. 21).  The
  * contraction is M = L, N = B*G, K = d per KV head: a dense GEMM for large B*G*L (tensor
@@ -115,6 +119,13 @@ typedef struct a2ats_params {
                             [0, N - hist_lag); 0 <= hist_lag <= min(window, N).  The
                             selection and output equal hist_lag = 0 exactly.  0 for the
                             append entry points, scores_out and the sharded step     */
+  int32_t rope_mode;     /* A2ATS_ROPE_WINDOWED (default): WRoPE (Eq. 11-12) on pre-PE
+                            keys | A2ATS_ROPE_STANDARD: the ablation "Baseline" / "QAVQ"
+                            configurations: the cache holds POST-PE keys
+                            k_j R_j (codes quantize them), q~ = q R_i with i = N - 1
+                            (params.bridge ignored) and every selected row -- sinks,
+                            top-K, window -- gets the standard logit q~ . k~_j; the
+                            sharded step refuses it (EUNSUPPORTED)                      */
 } a2ats_params;
 
 /* Fills the paper's configuration: w = 64, b = 2048, n_sink = 4, topk = 0,

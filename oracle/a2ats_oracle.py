@@ -295,6 +295,31 @@ def decode_step_pair(q_g, keys, values, codes, C, n_ctx: int, *, window: int = 6
     return dict(out=out, sel=sel, agg=agg, scores=scores, q_rot=q_rot, sel_rows=rows)
 
 
+def decode_step_pair_standard(q_g, keys_post, values, codes, C, n_ctx: int, *, window: int = 64,
+                              n_sink: int = 4, topk: int = 0, freqs=None, group_reduce: int = GROUP_MAX):
+    """One pair of the ablation configurations with standard RoPE ("Baseline" / "QAVQ"):
+    the cache holds POST-PE keys k~_j = k_j R_j (RoPE, Eq. 1 P:54-62) and the codes quantize them;
+    the query is rotated to the current position i = N-1, q~ = q R_i; approximate scores
+    u^_j = q~ . c_{s_j} (Eq. 21 with the standard query), the same candidate sets and top-K rule as
+    decode_step_pair (readings Q8, Q12), and every selected row -- sinks, top-K, window -- gets the
+    standard logit u_j = q~ . k~_j (Eq. 2 with RoPE: no window rotation)."""
+    q_g = np.asarray(q_g, dtype=F64)
+    d = q_g.shape[1]
+    if freqs is None:
+        freqs = inv_freq(d)
+    q_rot = rope_rotate(q_g, n_ctx - 1, freqs)                       # q R_i
+    codes_n = np.asarray(codes, dtype=np.int64)[:n_ctx]
+    scores = approx_scores(q_rot, codes_n, C)
+    agg = group_aggregate(scores, group_reduce)
+    S, Cand, W = token_sets(n_ctx, window, n_sink)
+    sel = select_topk(agg, Cand, topk)
+    rows = np.concatenate([S, sel, W]).astype(np.int64)
+    kp = np.asarray(keys_post, dtype=F64)[rows]
+    vr = np.asarray(values, dtype=F64)[rows]
+    out = np.stack([softmax_attention(kp @ q_rot[g], vr) for g in range(q_g.shape[0])])
+    return dict(out=out, sel=sel, agg=agg, scores=scores, q_rot=q_rot, sel_rows=rows)
+
+
 def decode_step(q, k_cache, v_cache, codes, codebook, n_ctx: int, *, window=64, bridge=2048,
                 n_sink=4, topk=0, freqs=None, group_reduce=GROUP_MAX, pairs=None):
     """Batched decode step.  q [B, Hq, d]; caches [B, Hkv, >=N, d]; codes

@@ -24,6 +24,8 @@ A2ATS_ENCCL = -5
 A2ATS_GROUP_MAX = 0
 A2ATS_GROUP_SUM = 1
 A2ATS_GROUP_PER_HEAD = 2
+A2ATS_ROPE_WINDOWED = 0
+A2ATS_ROPE_STANDARD = 1
 A2ATS_KV_DEVICE = 0
 A2ATS_KV_HOST_MAPPED = 1
 A2ATS_LUT_AUTO, A2ATS_LUT_TENSOR, A2ATS_LUT_FMA = 0, 1, 2
@@ -48,7 +50,8 @@ class a2ats_params(ctypes.Structure):
     _fields_ = [("window", ctypes.c_int32), ("bridge", ctypes.c_int32), ("n_sink", ctypes.c_int32),
                 ("topk", ctypes.c_int32), ("rope_theta", ctypes.c_double),
                 ("inv_freq", ctypes.POINTER(ctypes.c_double)), ("group_reduce", ctypes.c_int32),
-                ("kv_location", ctypes.c_int32), ("lut_engine", ctypes.c_int32), ("hist_lag", ctypes.c_int32)]
+                ("kv_location", ctypes.c_int32), ("lut_engine", ctypes.c_int32), ("hist_lag", ctypes.c_int32),
+                ("rope_mode", ctypes.c_int32)]
 
 
 _VP = ctypes.c_void_p
@@ -76,7 +79,7 @@ _SIGS = {
 _lib = None
 
 
-ABI_VERSION = 9  # include/a2ats.h A2ATS_ABI_VERSION
+ABI_VERSION = 10  # include/a2ats.h A2ATS_ABI_VERSION
 
 
 def load(path: str = LIB_PATH, build_if_missing: bool = True) -> ctypes.CDLL:
@@ -126,6 +129,7 @@ class Params:
     kv_location: int = A2ATS_KV_DEVICE
     lut_engine: int = A2ATS_LUT_AUTO
     hist_lag: int = 0
+    rope_mode: int = 0  # A2ATS_ROPE_WINDOWED | A2ATS_ROPE_STANDARD
 
     def c(self) -> a2ats_params:
         p = a2ats_params()
@@ -139,6 +143,7 @@ class Params:
             p.inv_freq = ctypes.cast(self._freq_buf, ctypes.POINTER(ctypes.c_double))
         p.group_reduce, p.kv_location, p.lut_engine = self.group_reduce, self.kv_location, self.lut_engine
         p.hist_lag = self.hist_lag
+        p.rope_mode = self.rope_mode
         return p
 
 

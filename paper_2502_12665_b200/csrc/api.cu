@@ -115,6 +115,7 @@ int check_params(const a2ats_params* p) {
   if (p->kv_location != A2ATS_KV_DEVICE && p->kv_location != A2ATS_KV_HOST_MAPPED) return A2ATS_EINVAL;
   if (p->lut_engine < A2ATS_LUT_AUTO || p->lut_engine > A2ATS_LUT_FMA) return A2ATS_EINVAL;
   if (p->hist_lag < 0 || p->hist_lag > p->window) return A2ATS_EINVAL;
+  if (p->rope_mode != A2ATS_ROPE_WINDOWED && p->rope_mode != A2ATS_ROPE_STANDARD) return A2ATS_EINVAL;
   return A2ATS_OK;
 }
 
@@ -629,6 +630,15 @@ int decode_impl_one(const a2ats_shape* shape, const a2ats_params* params, int32_
   if (rc) return rc;
   rc = check_params(params);
   if (rc) return rc;
+  // standard RoPE (ablation baseline): q~ = q R_{N-1}, the bridge of every row; no per-row rotation
+  const bool rope_std = params->rope_mode == A2ATS_ROPE_STANDARD;
+  a2ats_params pstd;
+  if (rope_std) {
+    if (n_ctx <= 0) return A2ATS_EINVAL;
+    pstd = *params;
+    pstd.bridge = n_ctx - 1;
+    params = &pstd;
+  }
   if (attend) {
     if (!k_cache || !v_cache || !out || !aligned16(k_cache) || !aligned16(v_cache) || !aligned16(out))
       return A2ATS_EINVAL;
@@ -688,7 +698,8 @@ int decode_impl_one(const a2ats_shape* shape, const a2ats_params* params, int32_
   prep_set_window(p, shape, k_cache, wlog, n_ctx, d.w0, d.n_w, 0);
   // posting-list select (A2ATS_POST_WLOG 0): no window logits precomputed -- the attention rotates
   // every window row itself (its cs-table branch), the select keeps its small shared memory
-  const int n_wl = (post_select && !A2ATS_POST_WLOG) ? 0 : p.n_wl;
+  const int n_wl = ((post_select && !A2ATS_POST_WLOG) || rope_std) ? 0 : p.n_wl;
+  if (rope_std) p.n_win = 0;  // (no window-row logits: every row takes the bridge logit)
   // long contexts / postings: the threshold (postings) kernel computes the window logits before its wait
   if (long_select || post_select || !attend) p.n_win = 0;
   CUtensorMap tmA, tmC;
@@ -809,6 +820,7 @@ int decode_impl_one(const a2ats_shape* shape, const a2ats_params* params, int32_
   std::memcpy(aa.bcs, la.bcs, sizeof(aa.bcs));
   aa.wlog = wlog;
   aa.wlog_late = (long_select || post_select) ? 1 : 0;  // (the select kernel wrote wlog)
+  aa.win_as_bridge = rope_std ? 1 : 0;
   aa.n_wl = n_wl;
   aa.cs = cs;
   aa.kc = static_cast<const uint16_t*>(k_cache);
@@ -1223,7 +1235,9 @@ int shard_common(const a2ats_shape* shape, const a2ats_params* params, int32_t n
   if (rc) return rc;
   if (n_ctx <= 0 || n_ctx > bounds[world]) return A2ATS_EINVAL;
   if (owner_of_host(bounds, world, n_ctx - 1) < 0) return A2ATS_EINVAL;
-  if (params->kv_location != A2ATS_KV_DEVICE || shape->code_bytes == 1 || params->hist_lag) return A2ATS_EUNSUPPORTED;
+  if (params->kv_location != A2ATS_KV_DEVICE || shape->code_bytes == 1 || params->hist_lag ||
+      params->rope_mode != A2ATS_ROPE_WINDOWED)
+    return A2ATS_EUNSUPPORTED;
   if (shape->n_max % 64 || !select_pipe_ok(shape->L) || shape->B > encode_cw_max()) return A2ATS_EUNSUPPORTED;
   return A2ATS_OK;
 }
@@ -1371,6 +1385,7 @@ int shard_partial(const a2ats_shape* shape, const a2ats_params* params, int32_t 
   std::memcpy(aa.bcs, la.bcs, sizeof(aa.bcs));
   aa.wlog = wlog;
   aa.wlog_late = 1;  // (the shard threshold kernel writes wlog)
+  aa.win_as_bridge = 0;
   aa.n_wl = n_wl;
   aa.cs = reinterpret_cast<float2*>(base + Lw.cs);
   aa.kc = static_cast<const uint16_t*>(k_cache);

@@ -174,7 +174,8 @@ __device__ __forceinline__ void attn_body(const AttnArgs& a) {
   if (split >= nsplit) return;
   const int p0 = split * a.R, p1 = min(p0 + a.R, M);
   const int pw = a.n_s + keff;               // first window position in the Sel list
-  const int nA = max(0, min(p1, pw) - p0);   // bridge rows of this split
+  const int pwc = a.win_as_bridge ? M : pw;  // first row with a per-row (window) rotation
+  const int nA = max(0, min(p1, pwc) - p0);  // bridge rows of this split
   const int nB = (p1 - p0) - nA;             // window rows of this split
   const int gA = (nA + 15) >> 4, gB = (nB + 15) >> 4, ngroups = gA + gB;
 

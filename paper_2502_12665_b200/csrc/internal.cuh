@@ -241,6 +241,7 @@ struct AttnArgs {
   float2 bcs[kHalf];      // (cos, sin)(b f_m), from fp64 angles on the host
   const float* wlog;      // [P, 64, 8] logits of the first n_wl window rows (prep kernel)
   int wlog_late;          // 1: the select kernel (this grid's predecessor) writes wlog: read after the wait
+  int win_as_bridge;      // 1 (standard RoPE): window rows take the bridge logit q~ . k_j like the others
   int n_wl;
 };
 

@@ -46,7 +46,7 @@ def test_sm100a_code_present(lib):
 
 def test_status_strings_and_version(lib):
     from paper_2502_12665_b200 import binding as b
-    assert lib.a2ats_abi_version() == b.ABI_VERSION == 9
+    assert lib.a2ats_abi_version() == b.ABI_VERSION == 10
     for s in (b.A2ATS_OK, b.A2ATS_EINVAL, b.A2ATS_EUNSUPPORTED, b.A2ATS_EWORKSPACE, b.A2ATS_ECUDA, b.A2ATS_ENCCL):
         assert b.status_string(s).startswith("A2ATS")
 
